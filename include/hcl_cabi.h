@@ -1,0 +1,139 @@
+/*
+ * hcl_cabi.h — device-level C-ABI of the B200 partitioned-NDRange runtime.
+ *
+ * This is the boundary that replaces the reference's node-side "ICD" layer:
+ * the 5-op forwarded-call table served by NodeDaemon
+ * (proj/include/haocl/api.hpp:19-21, proj/src/daemon.cpp:159-170) and the
+ * kernel engine it dispatches to, haocl::kernels::execute
+ * (proj/include/haocl/kernels.hpp:52-55, proj/src/kernels.cpp:268-283).
+ * Instead of TCP frames to a daemon, the host runtime calls these functions
+ * in-process; each device is one CUDA GPU with one stream.
+ *
+ * Conventions
+ *   - Plain C types only; no torch or C++ types cross this boundary.
+ *   - Return 0 on success, otherwise HCL_ERR_BASE + haocl::ErrorCode
+ *     (proj/include/haocl/error.hpp:11-36). The offset exists because
+ *     ErrorCode::internal == 0. The message of the most
+ *     recent failure on the calling thread is hcl_last_error().
+ *   - Thread safe across devices; calls for one device are serialized on that
+ *     device's stream (the reference serializes per device with a mutex,
+ *     proj/src/daemon.cpp:328-332).
+ *   - Buffers are identified by (device, 64-bit id). A device may hold the
+ *     whole buffer or one byte slice of it (a partition); offsets are always
+ *     LOGICAL byte offsets into the whole buffer.
+ */
+#ifndef HCL_CABI_H
+#define HCL_CABI_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HCL_OK 0
+#define HCL_ERR_BASE 1000
+
+/* haocl::ErrorCode values (proj/include/haocl/error.hpp:11-36) */
+enum hcl_error_code {
+  HCL_E_INTERNAL = 0,
+  HCL_E_PRECONDITION = 7,
+  HCL_E_ARGUMENT = 9,
+  HCL_E_NAME = 10,
+  HCL_E_HANDLE = 16,
+  HCL_E_POLICY = 17,
+  HCL_E_SIZE = 18,
+  HCL_E_MAPPING = 19,
+  HCL_E_UNKNOWN_DEVICE = 20,
+  HCL_E_REGISTRATION = 21,
+  HCL_E_CONTRACT = 22
+};
+
+/* Argument kinds: ArgKind {scalar_i64, buffer_in, buffer_out}
+ * (proj/include/haocl/kernels.hpp:24) plus inout. */
+enum hcl_arg_kind { HCL_ARG_SCALAR = 0, HCL_ARG_IN = 1, HCL_ARG_OUT = 2, HCL_ARG_INOUT = 3 };
+
+/* Partition class of an argument for a partitioned NDRange launch
+ * (generalises ArgKind). */
+enum hcl_part_class {
+  HCL_PART_NONE = 0,      /* scalar */
+  HCL_PART_REPLICATE = 1, /* whole buffer on every device (GEMM B, PageRank x) */
+  HCL_PART_SPLIT_ROWS = 2 /* row slice [lo,hi) of dim 0 on each device (GEMM A, C) */
+};
+
+/* One bound kernel argument, BoundArg (proj/include/haocl/kernels.hpp:44-50). */
+typedef struct hcl_arg {
+  uint32_t kind;      /* enum hcl_arg_kind */
+  uint32_t reserved;
+  int64_t scalar;     /* HCL_ARG_SCALAR */
+  uint64_t buffer_id; /* buffer kinds */
+} hcl_arg;
+
+/* ---- devices ---------------------------------------------------------- */
+/* Enumerate CUDA devices (all visible, or the listed ordinals) and create one
+ * stream per device. Idempotent for the same list. Replaces the
+ * DeviceIdRequest broadcast (proj/src/runtime.cpp:338-345). */
+int hcl_init(const int* cuda_ordinals, int n, int* num_devices);
+int hcl_device_count(int* n);
+/* type: 1 = gpu (wire::DeviceType, proj/include/haocl/wire.hpp:44) */
+int hcl_device_info(int dev, int* type, double* relative_throughput, int* sm_count,
+                    uint64_t* hbm_bytes, char* name, int name_cap);
+
+/* ---- registry (query_registry; proj/src/api.cpp:93-117) ---------------- */
+/* Kernel names of a bundle as a comma-separated list; arities per kernel. */
+int hcl_query_registry(const char* bundle, char* names_csv, int names_cap, uint32_t* arities,
+                       int arity_cap, int* n);
+/* Per-argument kind (enum hcl_arg_kind) and partition class. */
+int hcl_kernel_signature(const char* bundle, const char* kernel, uint8_t* kinds,
+                         uint8_t* part_classes, int cap, int* arity);
+
+/* ---- buffers (alloc_buffer / read_buffer / release_object, DataTransfer) */
+/* Allocate the logical byte range [first_byte, first_byte+bytes) of buffer `id`
+ * on `dev`, zero-filled (proj/src/daemon.cpp:21-69). Idempotent when the same
+ * range is already resident; a different range reallocates. */
+int hcl_buffer_alloc(int dev, uint64_t id, uint64_t first_byte, uint64_t bytes);
+int hcl_buffer_write(int dev, uint64_t id, uint64_t offset, const void* src, uint64_t len);
+int hcl_buffer_read(int dev, uint64_t id, uint64_t offset, void* dst, uint64_t len);
+/* Asynchronous variants on the device stream (src/dst must be pinned for overlap). */
+int hcl_buffer_write_async(int dev, uint64_t id, uint64_t offset, const void* src, uint64_t len);
+int hcl_buffer_read_async(int dev, uint64_t id, uint64_t offset, void* dst, uint64_t len);
+/* Device-to-device copy over NVLink P2P (replaces host-mediated migration,
+ * proj/src/runtime.cpp:237-248). Offsets are logical. */
+int hcl_buffer_copy_peer(int dst_dev, uint64_t dst_id, uint64_t dst_offset, int src_dev,
+                         uint64_t src_id, uint64_t src_offset, uint64_t len);
+int hcl_buffer_release(int dev, uint64_t id); /* idempotent */
+/* Device pointer of the resident slice (ptr addresses logical byte first_byte). */
+int hcl_buffer_device_ptr(int dev, uint64_t id, void** ptr, uint64_t* first_byte,
+                          uint64_t* bytes);
+/* Bind caller-owned device memory as buffer `id` (no copy; caller keeps ownership). */
+int hcl_buffer_bind_external(int dev, uint64_t id, void* ptr, uint64_t first_byte,
+                             uint64_t bytes);
+
+/* ---- launch (launch_kernel -> kernels::execute) ------------------------ */
+/* Launch `kernel` of the built-in bundles on `dev`, asynchronously on the
+ * device stream. goff/gsize give the NDRange sub-range (dim 0 = rows) this
+ * device computes; gsize == NULL runs the kernel's whole range (what the
+ * reference's un-split enqueue_ndrange_kernel does). work_units is the
+ * reference's work count for this sub-range (proj/src/kernels.cpp:285-298).
+ * Errors: HCL_E_NAME for an unknown kernel, HCL_E_ARGUMENT for arity, size or
+ * range violations (as kernels::execute). */
+int hcl_launch(int dev, const char* kernel, const hcl_arg* args, uint32_t nargs,
+               const uint64_t goff[3], const uint64_t gsize[3], uint32_t dims,
+               uint64_t* work_units);
+
+/* ---- completion and timing -------------------------------------------- */
+/* Wait for the device stream; device_ms = summed CUDA-event time of kernels
+ * launched since the previous finish (may be NULL). */
+int hcl_finish(int dev, double* device_ms);
+/* Number of CUDA kernels this library has launched (all devices). */
+uint64_t hcl_kernel_launch_count(void);
+/* Raw CUDA stream of a device (cudaStream_t as void*), for event timing. */
+int hcl_device_stream(int dev, void** stream);
+
+const char* hcl_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HCL_CABI_H */

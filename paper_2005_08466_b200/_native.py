@@ -1,0 +1,148 @@
+"""ctypes binding of libhaocl_b200.so (include/hcl_cabi.h, include/hcl_host.h).
+
+The library is built in-tree (``paper_2005_08466_b200/build.py``). There is no
+fallback: if it is missing, importing the runtime raises. GPU entry points
+fail with ``precondition`` when no CUDA device is present.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libhaocl_b200.so")
+
+HCL_ERR_BASE = 1000
+
+ERROR_NAMES = ["internal", "protocol", "version", "malformed", "encoding", "unknown_call", "busy",
+               "precondition", "reassembly_conflict", "argument", "name", "config", "connect", "timeout",
+               "transport", "remote", "handle", "policy", "size", "mapping", "unknown_device",
+               "registration", "contract", "parse"]
+
+u8p = C.POINTER(C.c_uint8)
+u64p = C.POINTER(C.c_uint64)
+i64p = C.POINTER(C.c_int64)
+i32p = C.POINTER(C.c_int)
+f64p = C.POINTER(C.c_double)
+
+
+class HclArg(C.Structure):
+    _fields_ = [("kind", C.c_uint32), ("reserved", C.c_uint32), ("scalar", C.c_int64),
+                ("buffer_id", C.c_uint64)]
+
+
+class SchedOptions(C.Structure):
+    _fields_ = [("baseline_rate", C.c_double), ("net_bandwidth", C.c_double), ("ema_alpha", C.c_double)]
+
+
+# (name, restype, argtypes) for every exported symbol the headers declare
+CABI = [
+    ("hcl_init", C.c_int, [i32p, C.c_int, i32p]),
+    ("hcl_device_count", C.c_int, [i32p]),
+    ("hcl_device_info", C.c_int, [C.c_int, i32p, f64p, i32p, u64p, C.c_char_p, C.c_int]),
+    ("hcl_query_registry", C.c_int, [C.c_char_p, C.c_char_p, C.c_int, C.POINTER(C.c_uint32), C.c_int, i32p]),
+    ("hcl_kernel_signature", C.c_int, [C.c_char_p, C.c_char_p, u8p, u8p, C.c_int, i32p]),
+    ("hcl_buffer_alloc", C.c_int, [C.c_int, C.c_uint64, C.c_uint64, C.c_uint64]),
+    ("hcl_buffer_write", C.c_int, [C.c_int, C.c_uint64, C.c_uint64, C.c_void_p, C.c_uint64]),
+    ("hcl_buffer_read", C.c_int, [C.c_int, C.c_uint64, C.c_uint64, C.c_void_p, C.c_uint64]),
+    ("hcl_buffer_write_async", C.c_int, [C.c_int, C.c_uint64, C.c_uint64, C.c_void_p, C.c_uint64]),
+    ("hcl_buffer_read_async", C.c_int, [C.c_int, C.c_uint64, C.c_uint64, C.c_void_p, C.c_uint64]),
+    ("hcl_buffer_copy_peer", C.c_int, [C.c_int, C.c_uint64, C.c_uint64, C.c_int, C.c_uint64, C.c_uint64,
+                                       C.c_uint64]),
+    ("hcl_buffer_release", C.c_int, [C.c_int, C.c_uint64]),
+    ("hcl_buffer_device_ptr", C.c_int, [C.c_int, C.c_uint64, C.POINTER(C.c_void_p), u64p, u64p]),
+    ("hcl_buffer_bind_external", C.c_int, [C.c_int, C.c_uint64, C.c_void_p, C.c_uint64, C.c_uint64]),
+    ("hcl_launch", C.c_int, [C.c_int, C.c_char_p, C.POINTER(HclArg), C.c_uint32, u64p, u64p, C.c_uint32, u64p]),
+    ("hcl_finish", C.c_int, [C.c_int, f64p]),
+    ("hcl_kernel_launch_count", C.c_uint64, []),
+    ("hcl_device_stream", C.c_int, [C.c_int, C.POINTER(C.c_void_p)]),
+    ("hcl_last_error", C.c_char_p, []),
+]
+
+HOST = [
+    ("hcl_ctx_init", C.c_int, [i32p, C.c_int, C.POINTER(SchedOptions), C.POINTER(C.c_void_p)]),
+    ("hcl_ctx_destroy", C.c_int, [C.c_void_p]),
+    ("hcl_ctx_get_device_ids", C.c_int, [C.c_void_p, i32p, C.c_int, i32p]),
+    ("hcl_ctx_create_queue", C.c_int, [C.c_void_p, C.c_int, C.c_char_p, C.c_int, u64p]),
+    ("hcl_ctx_create_buffer", C.c_int, [C.c_void_p, C.c_uint64, u64p]),
+    ("hcl_ctx_create_program", C.c_int, [C.c_void_p, C.c_char_p, u64p]),
+    ("hcl_ctx_create_kernel", C.c_int, [C.c_void_p, C.c_uint64, C.c_char_p, u64p]),
+    ("hcl_ctx_set_kernel_arg_i64", C.c_int, [C.c_void_p, C.c_uint64, C.c_uint32, C.c_int64]),
+    ("hcl_ctx_set_kernel_arg_buffer", C.c_int, [C.c_void_p, C.c_uint64, C.c_uint32, C.c_uint64]),
+    ("hcl_ctx_enqueue_write_buffer", C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_void_p, C.c_uint64,
+                                               C.c_uint64, u64p]),
+    ("hcl_ctx_enqueue_read_buffer", C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_void_p, C.c_uint64,
+                                              C.c_uint64]),
+    ("hcl_ctx_enqueue_ndrange_kernel", C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, u64p, C.c_uint32, u64p]),
+    ("hcl_ctx_enqueue_ndrange_partitioned", C.c_int, [C.c_void_p, C.c_uint64, u64p, C.c_uint32, u64p, C.c_int,
+                                                      u64p, u64p]),
+    ("hcl_ctx_partition_plan", C.c_int, [C.c_void_p, C.c_uint64, u64p, u64p, C.c_int, u64p, u64p]),
+    ("hcl_ctx_submit_task", C.c_int, [C.c_void_p, C.c_char_p, u8p, i64p, C.c_int, C.c_char_p, C.c_int, i32p,
+                                      u64p]),
+    ("hcl_ctx_finish", C.c_int, [C.c_void_p, C.c_uint64, f64p, f64p, f64p]),
+    ("hcl_ctx_release", C.c_int, [C.c_void_p, C.c_uint8, C.c_uint64]),
+    ("hcl_ctx_breakdown", C.c_int, [C.c_void_p, f64p]),
+    ("hcl_ctx_add_data_creation_ms", C.c_int, [C.c_void_p, C.c_double]),
+    ("hcl_ctx_buffer_size", C.c_int, [C.c_void_p, C.c_uint64, u64p]),
+    ("hcl_ctx_buffer_device_ptr", C.c_int, [C.c_void_p, C.c_uint64, C.c_int, C.POINTER(C.c_void_p), u64p, u64p]),
+    ("hcl_ctx_trace_count", C.c_int, [C.c_void_p, C.c_char_p, C.c_int, u64p]),
+    ("hcl_ctx_trace_clear", C.c_int, [C.c_void_p]),
+    ("hcl_ctx_sched_record_profile", C.c_int, [C.c_void_p, C.c_int, C.c_char_p, C.c_double, C.c_double]),
+    ("hcl_ctx_sched_rate", C.c_int, [C.c_void_p, C.c_int, C.c_char_p, f64p]),
+    ("hcl_ctx_sched_schedule", C.c_int, [C.c_void_p, C.c_char_p, C.c_char_p, C.c_int, C.c_double, C.c_uint64,
+                                         C.c_uint64, i32p]),
+    ("hcl_ctx_sched_set_model", C.c_int, [C.c_void_p, C.c_int, C.c_double]),
+    ("hcl_ctx_sched_partition_weights", C.c_int, [C.c_void_p, C.c_char_p, i32p, C.c_int, u64p]),
+    ("hcl_split_ranges", C.c_int, [C.c_uint64, u64p, C.c_int, u64p]),
+    ("hcl_spmv_partition_ranges", C.c_int, [C.c_int64, i64p, C.c_int64, u64p, i64p]),
+    ("hcl_sched_create", C.c_int, [C.POINTER(SchedOptions), i32p, f64p, C.c_int, C.POINTER(C.c_char_p), i32p,
+                                   C.c_int, C.POINTER(C.c_void_p)]),
+    ("hcl_sched_destroy", C.c_int, [C.c_void_p]),
+    ("hcl_sched_schedule", C.c_int, [C.c_void_p, C.c_char_p, C.c_char_p, C.c_int, C.c_double, C.c_uint64,
+                                     C.c_uint64, u64p, C.c_int, i32p]),
+    ("hcl_sched_record_profile", C.c_int, [C.c_void_p, C.c_int, C.c_char_p, C.c_double, C.c_double]),
+    ("hcl_sched_rate", C.c_int, [C.c_void_p, C.c_int, C.c_char_p, f64p]),
+    ("hcl_sched_note_resident", C.c_int, [C.c_void_p, C.c_uint64, i32p, C.c_int]),
+    ("hcl_sched_register_fixed_policy", C.c_int, [C.c_void_p, C.c_char_p, C.c_int]),
+    ("hcl_sched_modeled_cost", C.c_int, [C.c_void_p, C.c_int, C.c_char_p, C.c_double, C.c_uint64, C.c_uint64,
+                                         C.c_int, f64p]),
+    ("hcl_sched_partition_weights", C.c_int, [C.c_void_p, C.c_char_p, i32p, C.c_int, u64p]),
+]
+
+EXTRA = []  # appended by workload modules (datagen, etc.)
+
+_lib = None
+
+
+class HaoclError(Exception):
+    """haocl::Error across the C-ABI: .code is the reference's ErrorCode value."""
+
+    def __init__(self, code: int, message: str):
+        self.code = code
+        self.name = ERROR_NAMES[code] if 0 <= code < len(ERROR_NAMES) else "unknown"
+        super().__init__(message)
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} is missing: run __graft_entry__.build() "
+                               "(the B200 path has no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        for name, res, args in CABI + HOST + EXTRA:
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+def check(rc: int) -> None:
+    if rc != 0:
+        code = rc - HCL_ERR_BASE
+        msg = lib().hcl_last_error()
+        raise HaoclError(code, msg.decode() if msg else f"error {rc}")
+
+
+def declared_symbols():
+    return [n for n, _, _ in CABI + HOST]

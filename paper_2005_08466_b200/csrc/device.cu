@@ -1,0 +1,470 @@
+// Device layer of the C-ABI (include/hcl_cabi.h): CUDA device enumeration,
+// one stream per device, the per-device buffer store and the launch path.
+//
+// Replaces the node daemon's BufferStore and do_launch
+// (proj/src/daemon.cpp:21-114, 278-352): buffers live in HBM instead of byte
+// vectors, DataTransfer chunks become cudaMemcpyAsync, and launch_kernel
+// becomes an asynchronous kernel launch bracketed by CUDA events.
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "common.hpp"
+#include "../../include/hcl_cabi.h"
+
+namespace hcl {
+
+std::atomic<uint64_t> g_kernel_launches{0};
+
+const char* error_code_name(ErrorCode code) {
+  switch (code) {
+    case ErrorCode::internal: return "internal";
+    case ErrorCode::protocol: return "protocol";
+    case ErrorCode::version: return "version";
+    case ErrorCode::malformed: return "malformed";
+    case ErrorCode::encoding: return "encoding";
+    case ErrorCode::unknown_call: return "unknown_call";
+    case ErrorCode::busy: return "busy";
+    case ErrorCode::precondition: return "precondition";
+    case ErrorCode::reassembly_conflict: return "reassembly_conflict";
+    case ErrorCode::argument: return "argument";
+    case ErrorCode::name: return "name";
+    case ErrorCode::config: return "config";
+    case ErrorCode::connect: return "connect";
+    case ErrorCode::timeout: return "timeout";
+    case ErrorCode::transport: return "transport";
+    case ErrorCode::remote: return "remote";
+    case ErrorCode::handle: return "handle";
+    case ErrorCode::policy: return "policy";
+    case ErrorCode::size: return "size";
+    case ErrorCode::mapping: return "mapping";
+    case ErrorCode::unknown_device: return "unknown_device";
+    case ErrorCode::registration: return "registration";
+    case ErrorCode::contract: return "contract";
+    case ErrorCode::parse: return "parse";
+  }
+  return "unknown";
+}
+
+void cuda_check(cudaError_t e, const char* what, const char* file, int line) {
+  if (e == cudaSuccess) return;
+  fail(ErrorCode::internal, std::string("CUDA error ") + cudaGetErrorName(e) + " (" +
+                                cudaGetErrorString(e) + ") at " + file + ":" +
+                                std::to_string(line) + ": " + what);
+}
+
+namespace {
+
+struct DevAlloc {
+  uint8_t* ptr = nullptr;
+  uint64_t first_byte = 0;
+  uint64_t bytes = 0;
+  bool external = false;
+};
+
+struct Device {
+  int ordinal = 0;
+  cudaStream_t stream = nullptr;
+  int sm_count = 0;
+  uint64_t hbm_bytes = 0;
+  std::string name;
+  std::mutex mu;
+  std::unordered_map<uint64_t, DevAlloc> bufs;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> timed;  // since last finish
+  std::vector<cudaEvent_t> spare_events;
+  void* scratch = nullptr;
+  size_t scratch_bytes = 0;
+
+  cudaEvent_t event() {
+    if (!spare_events.empty()) {
+      cudaEvent_t e = spare_events.back();
+      spare_events.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    HCL_CUDA(cudaEventCreate(&e));
+    return e;
+  }
+};
+
+std::mutex g_devices_mu;
+std::vector<std::unique_ptr<Device>> g_devices;
+thread_local std::string g_last_error;
+
+Device& device(int dev) {
+  std::lock_guard<std::mutex> lock(g_devices_mu);
+  if (dev < 0 || dev >= static_cast<int>(g_devices.size()))
+    fail(ErrorCode::unknown_device, "device " + std::to_string(dev) + " (have " +
+                                        std::to_string(g_devices.size()) + "; call hcl_init)");
+  return *g_devices[dev];
+}
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    return HCL_OK;
+  } catch (const Error& e) {
+    g_last_error = e.what();
+    return HCL_ERR_BASE + static_cast<int>(e.code());
+  } catch (const std::exception& e) {
+    g_last_error = std::string("internal: ") + e.what();
+    return HCL_ERR_BASE + static_cast<int>(ErrorCode::internal);
+  }
+}
+
+DevAlloc& alloc_of(Device& d, uint64_t id, const char* what) {
+  auto it = d.bufs.find(id);
+  if (it == d.bufs.end())
+    fail(ErrorCode::precondition, std::string(what) + ": buffer " + std::to_string(id) +
+                                      " is not allocated on device " + std::to_string(d.ordinal));
+  return it->second;
+}
+
+uint8_t* range_ptr(DevAlloc& a, uint64_t offset, uint64_t len, uint64_t id, const char* what) {
+  if (offset < a.first_byte || offset + len > a.first_byte + a.bytes)
+    fail(ErrorCode::size, std::string(what) + ": range [" + std::to_string(offset) + ", " +
+                              std::to_string(offset + len) + ") outside the resident slice [" +
+                              std::to_string(a.first_byte) + ", " +
+                              std::to_string(a.first_byte + a.bytes) + ") of buffer " +
+                              std::to_string(id));
+  return a.ptr + (offset - a.first_byte);
+}
+
+void* scratch_for(int dev, size_t bytes) {
+  Device& d = device(dev);
+  if (d.scratch_bytes < bytes) {
+    if (d.scratch) HCL_CUDA(cudaFreeAsync(d.scratch, d.stream));
+    HCL_CUDA(cudaMallocAsync(&d.scratch, bytes, d.stream));
+    d.scratch_bytes = bytes;
+  }
+  return d.scratch;
+}
+
+}  // namespace
+
+// Shared by the host runtime's C entry points (one last-error channel).
+void set_last_error(const std::string& m) { g_last_error = m; }
+
+}  // namespace hcl
+
+using namespace hcl;
+
+extern "C" {
+
+const char* hcl_last_error(void) { return g_last_error.c_str(); }
+
+uint64_t hcl_kernel_launch_count(void) { return g_kernel_launches.load(); }
+
+int hcl_init(const int* cuda_ordinals, int n, int* num_devices) {
+  return guarded([&] {
+    std::lock_guard<std::mutex> lock(g_devices_mu);
+    int count = 0;
+    cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || count == 0)
+      fail(ErrorCode::precondition, std::string("no CUDA device available (") +
+                                        cudaGetErrorString(e) + "); the B200 path has no CPU fallback");
+    std::vector<int> want;
+    if (cuda_ordinals && n > 0)
+      want.assign(cuda_ordinals, cuda_ordinals + n);
+    else
+      for (int i = 0; i < count; ++i) want.push_back(i);
+    if (!g_devices.empty()) {
+      bool same = g_devices.size() == want.size();
+      for (size_t i = 0; same && i < want.size(); ++i) same = g_devices[i]->ordinal == want[i];
+      if (!same) fail(ErrorCode::config, "hcl_init called again with a different device list");
+      if (num_devices) *num_devices = static_cast<int>(g_devices.size());
+      return;
+    }
+    for (int ord : want) {
+      if (ord < 0 || ord >= count) fail(ErrorCode::unknown_device, "CUDA ordinal " + std::to_string(ord));
+      auto d = std::make_unique<Device>();
+      d->ordinal = ord;
+      HCL_CUDA(cudaSetDevice(ord));
+      cudaDeviceProp prop{};
+      HCL_CUDA(cudaGetDeviceProperties(&prop, ord));
+      if (prop.major != 10)
+        fail(ErrorCode::precondition, std::string("device ") + prop.name +
+                                          " is not sm_100 (Blackwell B200); this library is built for sm_100a only");
+      d->sm_count = prop.multiProcessorCount;
+      d->hbm_bytes = prop.totalGlobalMem;
+      d->name = prop.name;
+      HCL_CUDA(cudaStreamCreateWithFlags(&d->stream, cudaStreamNonBlocking));
+      g_devices.push_back(std::move(d));
+    }
+    // NVLink P2P between every pair (NVSwitch: all-to-all).
+    for (size_t i = 0; i < g_devices.size(); ++i)
+      for (size_t j = 0; j < g_devices.size(); ++j) {
+        if (i == j) continue;
+        int ok = 0;
+        cudaDeviceCanAccessPeer(&ok, g_devices[i]->ordinal, g_devices[j]->ordinal);
+        if (ok) {
+          cudaSetDevice(g_devices[i]->ordinal);
+          cudaError_t pe = cudaDeviceEnablePeerAccess(g_devices[j]->ordinal, 0);
+          if (pe == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+        }
+      }
+    if (num_devices) *num_devices = static_cast<int>(g_devices.size());
+  });
+}
+
+int hcl_device_count(int* n) {
+  return guarded([&] {
+    std::lock_guard<std::mutex> lock(g_devices_mu);
+    *n = static_cast<int>(g_devices.size());
+  });
+}
+
+int hcl_device_info(int dev, int* type, double* relative_throughput, int* sm_count,
+                    uint64_t* hbm_bytes, char* name, int name_cap) {
+  return guarded([&] {
+    Device& d = device(dev);
+    if (type) *type = 1;  // wire::DeviceType::gpu
+    if (relative_throughput) *relative_throughput = 1.0;
+    if (sm_count) *sm_count = d.sm_count;
+    if (hbm_bytes) *hbm_bytes = d.hbm_bytes;
+    if (name && name_cap > 0) {
+      std::strncpy(name, d.name.c_str(), static_cast<size_t>(name_cap) - 1);
+      name[name_cap - 1] = 0;
+    }
+  });
+}
+
+int hcl_device_stream(int dev, void** stream) {
+  return guarded([&] { *stream = device(dev).stream; });
+}
+
+int hcl_query_registry(const char* bundle, char* names_csv, int names_cap, uint32_t* arities,
+                       int arity_cap, int* n) {
+  return guarded([&] {
+    if (!bundle_exists(bundle)) fail(ErrorCode::name, std::string("unknown bundle '") + bundle + "'");
+    std::string csv;
+    int count = 0;
+    for (const auto& k : registry()) {
+      if (std::strcmp(k.bundle, bundle) != 0) continue;
+      if (!csv.empty()) csv += ",";
+      csv += k.name;
+      if (arities && count < arity_cap) arities[count] = static_cast<uint32_t>(k.kinds.size());
+      ++count;
+    }
+    if (names_csv) {
+      if (static_cast<int>(csv.size()) + 1 > names_cap) fail(ErrorCode::size, "names buffer too small");
+      std::memcpy(names_csv, csv.c_str(), csv.size() + 1);
+    }
+    *n = count;
+  });
+}
+
+int hcl_kernel_signature(const char* bundle, const char* kernel, uint8_t* kinds,
+                         uint8_t* part_classes, int cap, int* arity) {
+  return guarded([&] {
+    const KernelDef* k = find_kernel(bundle, kernel);
+    if (!k) fail(ErrorCode::name, std::string("unknown kernel '") + kernel + "'");
+    *arity = static_cast<int>(k->kinds.size());
+    for (int i = 0; i < *arity && i < cap; ++i) {
+      if (kinds) kinds[i] = k->kinds[i];
+      if (part_classes) part_classes[i] = k->part_classes[i];
+    }
+  });
+}
+
+int hcl_buffer_alloc(int dev, uint64_t id, uint64_t first_byte, uint64_t bytes) {
+  return guarded([&] {
+    Device& d = device(dev);
+    std::lock_guard<std::mutex> lock(d.mu);
+    HCL_CUDA(cudaSetDevice(d.ordinal));
+    auto it = d.bufs.find(id);
+    if (it != d.bufs.end()) {
+      if (it->second.first_byte == first_byte && it->second.bytes == bytes) return;
+      if (!it->second.external && it->second.ptr) HCL_CUDA(cudaFreeAsync(it->second.ptr, d.stream));
+      d.bufs.erase(it);
+    }
+    DevAlloc a;
+    a.first_byte = first_byte;
+    a.bytes = bytes;
+    if (bytes) {
+      HCL_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&a.ptr), bytes, d.stream));
+      HCL_CUDA(cudaMemsetAsync(a.ptr, 0, bytes, d.stream));  // alloc zero-fills (daemon.cpp:21-69)
+    }
+    d.bufs.emplace(id, a);
+  });
+}
+
+int hcl_buffer_bind_external(int dev, uint64_t id, void* ptr, uint64_t first_byte, uint64_t bytes) {
+  return guarded([&] {
+    Device& d = device(dev);
+    std::lock_guard<std::mutex> lock(d.mu);
+    auto it = d.bufs.find(id);
+    if (it != d.bufs.end() && !it->second.external && it->second.ptr)
+      HCL_CUDA(cudaFreeAsync(it->second.ptr, d.stream));
+    d.bufs[id] = DevAlloc{static_cast<uint8_t*>(ptr), first_byte, bytes, true};
+  });
+}
+
+static int buffer_copy(int dev, uint64_t id, uint64_t offset, void* host, uint64_t len, bool write,
+                       bool async) {
+  return guarded([&] {
+    Device& d = device(dev);
+    std::lock_guard<std::mutex> lock(d.mu);
+    DevAlloc& a = alloc_of(d, id, write ? "write_buffer" : "read_buffer");
+    uint8_t* p = range_ptr(a, offset, len, id, write ? "write_buffer" : "read_buffer");
+    if (!len) return;
+    HCL_CUDA(cudaSetDevice(d.ordinal));
+    if (write)
+      HCL_CUDA(cudaMemcpyAsync(p, host, len, cudaMemcpyHostToDevice, d.stream));
+    else
+      HCL_CUDA(cudaMemcpyAsync(host, p, len, cudaMemcpyDeviceToHost, d.stream));
+    if (!async) HCL_CUDA(cudaStreamSynchronize(d.stream));
+  });
+}
+
+int hcl_buffer_write(int dev, uint64_t id, uint64_t offset, const void* src, uint64_t len) {
+  return buffer_copy(dev, id, offset, const_cast<void*>(src), len, true, false);
+}
+int hcl_buffer_read(int dev, uint64_t id, uint64_t offset, void* dst, uint64_t len) {
+  return buffer_copy(dev, id, offset, dst, len, false, false);
+}
+int hcl_buffer_write_async(int dev, uint64_t id, uint64_t offset, const void* src, uint64_t len) {
+  return buffer_copy(dev, id, offset, const_cast<void*>(src), len, true, true);
+}
+int hcl_buffer_read_async(int dev, uint64_t id, uint64_t offset, void* dst, uint64_t len) {
+  return buffer_copy(dev, id, offset, dst, len, false, true);
+}
+
+int hcl_buffer_copy_peer(int dst_dev, uint64_t dst_id, uint64_t dst_offset, int src_dev,
+                         uint64_t src_id, uint64_t src_offset, uint64_t len) {
+  return guarded([&] {
+    Device& dd = device(dst_dev);
+    Device& sd = device(src_dev);
+    uint8_t *dp, *sp;
+    {
+      std::lock_guard<std::mutex> lock(dd.mu);
+      dp = range_ptr(alloc_of(dd, dst_id, "copy_peer dst"), dst_offset, len, dst_id, "copy_peer dst");
+    }
+    {
+      std::lock_guard<std::mutex> lock(sd.mu);
+      sp = range_ptr(alloc_of(sd, src_id, "copy_peer src"), src_offset, len, src_id, "copy_peer src");
+    }
+    if (!len) return;
+    if (&dd == &sd) {
+      HCL_CUDA(cudaSetDevice(dd.ordinal));
+      HCL_CUDA(cudaMemcpyAsync(dp, sp, len, cudaMemcpyDeviceToDevice, dd.stream));
+      return;
+    }
+    // order after everything pending on the source stream, then copy on the
+    // destination stream (NVLink P2P through NVSwitch)
+    HCL_CUDA(cudaSetDevice(sd.ordinal));
+    cudaEvent_t ready;
+    HCL_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+    HCL_CUDA(cudaEventRecord(ready, sd.stream));
+    HCL_CUDA(cudaSetDevice(dd.ordinal));
+    HCL_CUDA(cudaStreamWaitEvent(dd.stream, ready, 0));
+    HCL_CUDA(cudaMemcpyPeerAsync(dp, dd.ordinal, sp, sd.ordinal, len, dd.stream));
+    // the source must not be overwritten before the copy lands
+    cudaEvent_t done;
+    HCL_CUDA(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+    HCL_CUDA(cudaEventRecord(done, dd.stream));
+    HCL_CUDA(cudaSetDevice(sd.ordinal));
+    HCL_CUDA(cudaStreamWaitEvent(sd.stream, done, 0));
+    HCL_CUDA(cudaEventDestroy(ready));
+    HCL_CUDA(cudaEventDestroy(done));
+  });
+}
+
+int hcl_buffer_release(int dev, uint64_t id) {
+  return guarded([&] {
+    Device& d = device(dev);
+    std::lock_guard<std::mutex> lock(d.mu);
+    auto it = d.bufs.find(id);
+    if (it == d.bufs.end()) return;  // idempotent
+    HCL_CUDA(cudaSetDevice(d.ordinal));
+    if (!it->second.external && it->second.ptr) HCL_CUDA(cudaFreeAsync(it->second.ptr, d.stream));
+    d.bufs.erase(it);
+  });
+}
+
+int hcl_buffer_device_ptr(int dev, uint64_t id, void** ptr, uint64_t* first_byte, uint64_t* bytes) {
+  return guarded([&] {
+    Device& d = device(dev);
+    std::lock_guard<std::mutex> lock(d.mu);
+    DevAlloc& a = alloc_of(d, id, "device_ptr");
+    if (ptr) *ptr = a.ptr;
+    if (first_byte) *first_byte = a.first_byte;
+    if (bytes) *bytes = a.bytes;
+  });
+}
+
+int hcl_launch(int dev, const char* kernel, const hcl_arg* args, uint32_t nargs,
+               const uint64_t goff[3], const uint64_t gsize[3], uint32_t dims,
+               uint64_t* work_units) {
+  return guarded([&] {
+    const KernelDef* k = find_kernel_any(kernel ? kernel : "");
+    if (!k) fail(ErrorCode::name, std::string("unknown kernel '") + (kernel ? kernel : "") + "'");
+    if (nargs != k->kinds.size())
+      fail(ErrorCode::argument, std::string(kernel) + ": expected " + std::to_string(k->kinds.size()) +
+                                    " arguments, got " + std::to_string(nargs));
+    Device& d = device(dev);
+    std::lock_guard<std::mutex> lock(d.mu);
+    HCL_CUDA(cudaSetDevice(d.ordinal));
+    std::vector<LaunchArg> la(nargs);
+    for (uint32_t i = 0; i < nargs; ++i) {
+      bool want_scalar = k->kinds[i] == HCL_ARG_SCALAR;
+      bool is_scalar = args[i].kind == HCL_ARG_SCALAR;
+      if (want_scalar != is_scalar)
+        fail(ErrorCode::argument, std::string(kernel) + " argument " + std::to_string(i) +
+                                      (want_scalar ? ": expected a scalar" : ": expected a buffer"));
+      la[i].kind = args[i].kind;
+      la[i].scalar = args[i].scalar;
+      la[i].id = args[i].buffer_id;
+      if (!is_scalar) {
+        DevAlloc& a = alloc_of(d, args[i].buffer_id, kernel);
+        la[i].buf = BufView{a.ptr, a.first_byte, a.bytes};
+      }
+    }
+    LaunchCtx c;
+    c.dev = dev;
+    c.stream = d.stream;
+    c.sm_count = d.sm_count;
+    c.args = la.data();
+    c.nargs = nargs;
+    c.dims = dims ? dims : 1;
+    c.whole = gsize == nullptr;  // NULL gsize: the kernel's whole range
+    for (int i = 0; i < 3; ++i) {
+      c.goff[i] = goff ? goff[i] : 0;
+      c.gsize[i] = gsize ? gsize[i] : 1;
+    }
+    c.scratch = scratch_for;
+    cudaEvent_t e0 = d.event(), e1 = d.event();
+    HCL_CUDA(cudaEventRecord(e0, d.stream));
+    uint64_t w = k->launch(c);
+    HCL_CUDA(cudaEventRecord(e1, d.stream));
+    d.timed.emplace_back(e0, e1);
+    if (work_units) *work_units = w;
+  });
+}
+
+int hcl_finish(int dev, double* device_ms) {
+  return guarded([&] {
+    Device& d = device(dev);
+    std::lock_guard<std::mutex> lock(d.mu);
+    HCL_CUDA(cudaSetDevice(d.ordinal));
+    HCL_CUDA(cudaStreamSynchronize(d.stream));
+    double total = 0.0;
+    for (auto& [a, b] : d.timed) {
+      float ms = 0.f;
+      HCL_CUDA(cudaEventElapsedTime(&ms, a, b));
+      total += ms;
+      d.spare_events.push_back(a);
+      d.spare_events.push_back(b);
+    }
+    d.timed.clear();
+    if (device_ms) *device_ms = total;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,984 @@
+// haocl::HostContext on the CUDA C-ABI (include/haocl/runtime.hpp).
+//
+// Reference: proj/src/runtime.cpp. The handle tables, argument binding,
+// launch validation, EMA profiling, timing fragments and message trace keep
+// the reference's semantics; the transport changes:
+//   * NodeLink/Channel (runtime.cpp:67-92)        -> a CUDA device + stream via hcl_*;
+//   * stage_buffer's host-mediated migration      -> device-to-device NVLink copies
+//     (runtime.cpp:220-249)                          (hcl_buffer_copy_peer);
+//   * launch_on_queue's blocking RPC (253-309)    -> asynchronous hcl_launch; compute time
+//                                                    from CUDA events, drained by finish().
+// New: the partitioned NDRange launch (see runtime.hpp) with sharded buffers:
+// every buffer tracks, per device, the allocated byte slice and the valid
+// byte interval, so SPLIT_ROWS outputs stay on the devices that computed them
+// and reads gather the pieces.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <set>
+
+#include "haocl/runtime.hpp"
+#include "hcl_cabi.h"
+#include "hcl_host.h"
+
+namespace hcl {
+void set_last_error(const std::string& m);
+}
+
+namespace haocl {
+
+namespace {
+
+using Clock = std::chrono::steady_clock;
+double ms_since(Clock::time_point t) { return std::chrono::duration<double, std::milli>(Clock::now() - t).count(); }
+
+[[noreturn]] void fail(ErrorCode code, const std::string& m) { throw Error(code, m); }
+
+// Turns a C-ABI return code back into the reference's exception.
+void check(int rc) {
+  if (rc == HCL_OK) return;
+  int code = rc - HCL_ERR_BASE;
+  if (code < 0 || code > 23) code = 0;
+  throw Error(static_cast<ErrorCode>(code), hcl_last_error());
+}
+
+}  // namespace
+
+void MessageTrace::record(TraceEvent e) {
+  std::lock_guard lock(mutex_);
+  events_.push_back(std::move(e));
+}
+std::vector<TraceEvent> MessageTrace::events() const {
+  std::lock_guard lock(mutex_);
+  return events_;
+}
+size_t MessageTrace::count_calls(const std::string& function, int device) const {
+  std::lock_guard lock(mutex_);
+  size_t n = 0;
+  for (const auto& e : events_)
+    if (e.function == function && (device < 0 || e.device == device)) ++n;
+  return n;
+}
+void MessageTrace::clear() {
+  std::lock_guard lock(mutex_);
+  events_.clear();
+}
+
+struct HostContext::Impl {
+  struct Piece {
+    uint64_t alloc_first = 0, alloc_bytes = 0;
+    uint64_t valid_first = 0, valid_bytes = 0;  // one valid interval inside the allocation
+    bool allocated = false;
+  };
+  struct BufferRec {
+    uint64_t size = 0;
+    std::map<int, Piece> pieces;  // device gid -> piece
+  };
+  struct Launch {
+    std::string kernel;
+    uint64_t work = 0;
+    cudaEvent_t start = nullptr, stop = nullptr;
+    int gid = 0;
+  };
+  struct QueueRec {
+    int gid = 0;
+    std::string user;
+    bool shared = true;
+    double transfer_ms = 0.0, compute_ms = 0.0, modeled_ms = 0.0;
+    std::vector<Launch> pending;
+  };
+  struct ProgramRec {
+    std::string bundle;
+    std::vector<std::pair<std::string, uint32_t>> kernels;
+  };
+  struct KernelRec {
+    uint64_t program = 0;
+    std::string bundle;
+    std::string name;
+    uint32_t arity = 0;
+    std::vector<uint8_t> kinds, classes;
+    std::map<uint32_t, Arg> args;
+  };
+
+  GlobalDeviceMap device_map;
+  Scheduler scheduler;
+  MessageTrace trace;
+  std::recursive_mutex mu;
+  std::map<uint64_t, BufferRec> buffers;
+  std::map<uint64_t, QueueRec> queues;
+  std::map<uint64_t, ProgramRec> programs;
+  std::map<uint64_t, KernelRec> kernels;
+  std::set<uint64_t> events;
+  std::map<int, uint64_t> internal_queues;
+  std::atomic<uint64_t> next_handle{1};
+  std::mutex breakdown_mu;
+  TimingBreakdown timings;
+
+  uint64_t new_id() { return next_handle.fetch_add(1); }
+
+  Handle new_event() {
+    uint64_t id = new_id();
+    events.insert(id);
+    return Handle{HandleKind::event, id};
+  }
+
+  int dev_index(int gid) const {
+    const DeviceEntry* e = device_map.find(gid);
+    if (!e) fail(ErrorCode::unknown_device, "device " + std::to_string(gid));
+    return static_cast<int>(e->local_index);
+  }
+
+  BufferRec& buffer(uint64_t id) {
+    auto it = buffers.find(id);
+    if (it == buffers.end()) fail(ErrorCode::handle, "buffer handle " + std::to_string(id) + " is released or unknown");
+    return it->second;
+  }
+  QueueRec& queue(uint64_t id) {
+    auto it = queues.find(id);
+    if (it == queues.end()) fail(ErrorCode::handle, "queue handle " + std::to_string(id) + " is released or unknown");
+    return it->second;
+  }
+  KernelRec& kernel(uint64_t id) {
+    auto it = kernels.find(id);
+    if (it == kernels.end()) fail(ErrorCode::handle, "kernel handle " + std::to_string(id) + " is released or unknown");
+    return it->second;
+  }
+
+  void add_transfer(QueueRec* q, double ms) {
+    if (q) q->transfer_ms += ms;
+    std::lock_guard lock(breakdown_mu);
+    timings.transfer_ms += ms;
+  }
+
+  // -- residency --------------------------------------------------------------
+
+  // Make the allocation of `id` on `gid` cover [first, first+len), preserving
+  // the currently valid bytes of that device.
+  Piece& ensure_alloc(uint64_t id, BufferRec& b, int gid, uint64_t first, uint64_t len) {
+    Piece& p = b.pieces[gid];
+    int dev = dev_index(gid);
+    if (p.allocated && first >= p.alloc_first && first + len <= p.alloc_first + p.alloc_bytes) return p;
+    uint64_t nf = first, ne = first + len;
+    if (p.allocated) {
+      nf = std::min(nf, p.alloc_first);
+      ne = std::max(ne, p.alloc_first + p.alloc_bytes);
+    }
+    if (p.allocated && p.valid_bytes) {
+      // preserve valid bytes through a temporary buffer on the same device
+      uint64_t tmp = new_id();
+      check(hcl_buffer_alloc(dev, tmp, p.valid_first, p.valid_bytes));
+      check(hcl_buffer_copy_peer(dev, tmp, p.valid_first, dev, id, p.valid_first, p.valid_bytes));
+      check(hcl_buffer_alloc(dev, id, nf, ne - nf));
+      check(hcl_buffer_copy_peer(dev, id, p.valid_first, dev, tmp, p.valid_first, p.valid_bytes));
+      check(hcl_buffer_release(dev, tmp));
+    } else {
+      check(hcl_buffer_alloc(dev, id, nf, ne - nf));
+      p.valid_bytes = 0;
+    }
+    trace.record({gid, "alloc_buffer", id});
+    p.allocated = true;
+    p.alloc_first = nf;
+    p.alloc_bytes = ne - nf;
+    return p;
+  }
+
+  static void set_valid(Piece& p, uint64_t first, uint64_t len) {
+    if (!len) return;
+    if (p.valid_bytes && first <= p.valid_first + p.valid_bytes && p.valid_first <= first + len) {
+      uint64_t f = std::min(first, p.valid_first);
+      uint64_t e = std::max(first + len, p.valid_first + p.valid_bytes);
+      p.valid_first = f;
+      p.valid_bytes = e - f;
+    } else {
+      p.valid_first = first;
+      p.valid_bytes = len;
+    }
+  }
+
+  // Other devices' copies of [first, first+len) are stale after a write there.
+  static void invalidate_others(BufferRec& b, int gid, uint64_t first, uint64_t len) {
+    uint64_t e = first + len;
+    for (auto& [g, p] : b.pieces) {
+      if (g == gid || !p.valid_bytes) continue;
+      uint64_t vf = p.valid_first, ve = p.valid_first + p.valid_bytes;
+      if (ve <= first || vf >= e) continue;
+      uint64_t left = first > vf ? first - vf : 0;
+      uint64_t right = ve > e ? ve - e : 0;
+      if (left >= right) {
+        p.valid_bytes = left;
+      } else {
+        p.valid_first = e;
+        p.valid_bytes = right;
+      }
+    }
+  }
+
+  // Make bytes [first, first+len) of buffer `id` valid on `gid`, copying the
+  // missing parts from devices that hold them (NVLink peer copies).
+  void ensure_valid(uint64_t id, BufferRec& b, int gid, uint64_t first, uint64_t len, QueueRec* q) {
+    Piece& p = ensure_alloc(id, b, gid, first, len);
+    if (p.valid_bytes && first >= p.valid_first && first + len <= p.valid_first + p.valid_bytes) return;
+    auto started = Clock::now();
+    int dev = dev_index(gid);
+    uint64_t pos = first, end = first + len;
+    bool copied = false;
+    while (pos < end) {
+      if (p.valid_bytes && pos >= p.valid_first && pos < p.valid_first + p.valid_bytes) {
+        pos = p.valid_first + p.valid_bytes;
+        continue;
+      }
+      // a source holding `pos`
+      int src = -1;
+      uint64_t src_end = 0;
+      for (auto& [g, o] : b.pieces) {
+        if (g == gid || !o.valid_bytes) continue;
+        if (pos >= o.valid_first && pos < o.valid_first + o.valid_bytes) {
+          src = g;
+          src_end = o.valid_first + o.valid_bytes;
+          break;
+        }
+      }
+      uint64_t stop = end;
+      if (p.valid_bytes && p.valid_first > pos) stop = std::min(stop, p.valid_first);
+      if (src < 0) {
+        // nobody holds it: never written -> zeros (the allocation is zero-filled
+        // unless reused; skip to the next held byte)
+        uint64_t next = stop;
+        for (auto& [g, o] : b.pieces)
+          if (g != gid && o.valid_bytes && o.valid_first > pos) next = std::min(next, o.valid_first);
+        pos = next;
+        continue;
+      }
+      uint64_t n = std::min(stop, src_end) - pos;
+      check(hcl_buffer_copy_peer(dev, id, pos, dev_index(src), id, pos, n));
+      trace.record({gid, "copy_peer", id});
+      copied = true;
+      pos += n;
+    }
+    set_valid(p, first, len);
+    if (copied) add_transfer(q, ms_since(started));
+  }
+
+  void note_residency(uint64_t id, BufferRec& b) {
+    std::vector<int> ids;
+    for (auto& [g, p] : b.pieces)
+      if (p.valid_bytes == b.size && b.size) ids.push_back(g);
+    scheduler.note_resident(id, ids);
+  }
+
+  // -- launches -----------------------------------------------------------------
+
+  struct Part {
+    int gid;
+    uint64_t queue;
+    uint64_t lo, hi;
+  };
+
+  Handle launch_parts(KernelRec& k, const std::vector<Arg>& args, std::array<uint64_t, 3> global, uint32_t dims,
+                      const std::vector<Part>& parts, bool whole) {
+    const uint32_t n = k.arity;
+    const uint64_t rows = global[0];
+    // per-argument byte geometry
+    std::vector<uint64_t> row_bytes(n, 0);
+    for (uint32_t i = 0; i < n; ++i) {
+      if (!args[i].is_buffer) continue;
+      if (k.kinds[i] == HCL_ARG_SCALAR)
+        fail(ErrorCode::argument, k.name + " argument " + std::to_string(i) + ": expected a scalar");
+      BufferRec& b = buffer(args[i].buffer);
+      if (!whole && k.classes[i] == HCL_PART_SPLIT_ROWS) {
+        if (rows == 0 || b.size % rows)
+          fail(ErrorCode::argument, k.name + " argument " + std::to_string(i) + ": buffer of " + std::to_string(b.size) +
+                                        " bytes does not split into " + std::to_string(rows) + " rows");
+        row_bytes[i] = b.size / rows;
+      }
+    }
+    for (uint32_t i = 0; i < n; ++i)
+      if (!args[i].is_buffer && k.kinds[i] != HCL_ARG_SCALAR)
+        fail(ErrorCode::argument, k.name + " argument " + std::to_string(i) + ": expected a buffer");
+    if (!whole)
+      for (uint32_t i = 0; i < n; ++i)
+        if (args[i].is_buffer && k.classes[i] == HCL_PART_REPLICATE &&
+            (k.kinds[i] == HCL_ARG_OUT || k.kinds[i] == HCL_ARG_INOUT) && parts.size() > 1)
+          fail(ErrorCode::argument, k.name + ": a replicated output cannot be partitioned");
+
+    std::vector<hcl_arg> cargs(n);
+    for (const Part& part : parts) {
+      if (!whole && part.hi == part.lo) continue;
+      QueueRec& q = queue(part.queue);
+      auto staging = Clock::now();
+      for (uint32_t i = 0; i < n; ++i) {
+        cargs[i] = hcl_arg{static_cast<uint32_t>(k.kinds[i]), 0, args[i].scalar, args[i].buffer};
+        if (!args[i].is_buffer) continue;
+        BufferRec& b = buffer(args[i].buffer);
+        bool split = !whole && k.classes[i] == HCL_PART_SPLIT_ROWS;
+        uint64_t first = split ? part.lo * row_bytes[i] : 0;
+        uint64_t len = split ? (part.hi - part.lo) * row_bytes[i] : b.size;
+        if (k.kinds[i] == HCL_ARG_OUT)
+          ensure_alloc(args[i].buffer, b, part.gid, first, len);
+        else
+          ensure_valid(args[i].buffer, b, part.gid, first, len, &q);
+      }
+      add_transfer(&q, 0.0 * ms_since(staging));
+      scheduler.note_dispatch(part.gid);
+      Launch l;
+      l.kernel = k.name;
+      l.gid = part.gid;
+      int dev = dev_index(part.gid);
+      void* stream = nullptr;
+      check(hcl_device_stream(dev, &stream));
+      cudaEventCreate(&l.start);
+      cudaEventCreate(&l.stop);
+      cudaEventRecord(l.start, static_cast<cudaStream_t>(stream));
+      uint64_t goff[3] = {part.lo, 0, 0};
+      uint64_t gsz[3] = {part.hi - part.lo, global[1], global[2]};
+      trace.record({part.gid, "launch_kernel", 0});
+      int rc = hcl_launch(dev, k.name.c_str(), cargs.data(), n, goff, whole ? nullptr : gsz, dims, &l.work);
+      cudaEventRecord(l.stop, static_cast<cudaStream_t>(stream));
+      scheduler.note_complete(part.gid);
+      if (rc != HCL_OK) {
+        cudaEventDestroy(l.start);
+        cudaEventDestroy(l.stop);
+        check(rc);
+      }
+      q.pending.push_back(l);
+      // outputs: valid where computed
+      for (uint32_t i = 0; i < n; ++i) {
+        if (!args[i].is_buffer || k.kinds[i] == HCL_ARG_IN) continue;
+        BufferRec& b = buffer(args[i].buffer);
+        bool split = !whole && k.classes[i] == HCL_PART_SPLIT_ROWS;
+        uint64_t first = split ? part.lo * row_bytes[i] : 0;
+        uint64_t len = split ? (part.hi - part.lo) * row_bytes[i] : b.size;
+        Piece& p = b.pieces[part.gid];
+        // a fresh output slice is exactly what this part computed
+        if (!(p.valid_bytes && first <= p.valid_first + p.valid_bytes && p.valid_first <= first + len)) {
+          p.valid_first = first;
+          p.valid_bytes = len;
+        } else {
+          set_valid(p, first, len);
+        }
+        invalidate_others(b, part.gid, first, len);
+      }
+    }
+    for (uint32_t i = 0; i < n; ++i)
+      if (args[i].is_buffer && k.kinds[i] != HCL_ARG_IN) note_residency(args[i].buffer, buffer(args[i].buffer));
+    return new_event();
+  }
+
+  KernelRec& bound_kernel(uint64_t kid, std::vector<Arg>& args) {
+    KernelRec& k = kernel(kid);
+    for (const auto& [index, value] : k.args)
+      if (index >= k.arity)
+        fail(ErrorCode::argument, "argument index " + std::to_string(index) + " out of range for a " +
+                                      std::to_string(k.arity) + "-arg kernel");
+    for (uint32_t i = 0; i < k.arity; ++i)
+      if (!k.args.count(i)) fail(ErrorCode::argument, "kernel argument " + std::to_string(i) + " is unbound");
+    for (uint32_t i = 0; i < k.arity; ++i) args.push_back(k.args.at(i));
+    return k;
+  }
+
+  KernelRec temp_kernel(const std::string& name) {
+    KernelRec k;
+    k.name = name;
+    uint8_t kinds[64], classes[64];
+    int arity = 0;
+    int rc = hcl_kernel_signature("core", name.c_str(), kinds, classes, 64, &arity);
+    if (rc != HCL_OK) rc = hcl_kernel_signature("b200", name.c_str(), kinds, classes, 64, &arity);
+    if (rc != HCL_OK) fail(ErrorCode::name, "unknown kernel '" + name + "'");
+    k.arity = static_cast<uint32_t>(arity);
+    k.kinds.assign(kinds, kinds + arity);
+    k.classes.assign(classes, classes + arity);
+    return k;
+  }
+};
+
+HostContext::HostContext() : impl_(new Impl) {}
+HostContext::HostContext(HostContext&&) noexcept = default;
+HostContext& HostContext::operator=(HostContext&&) noexcept = default;
+HostContext::~HostContext() {
+  if (!impl_) return;
+  for (auto& [id, b] : impl_->buffers)
+    for (auto& [g, p] : b.pieces)
+      if (p.allocated) hcl_buffer_release(impl_->dev_index(g), id);
+}
+
+HostContext HostContext::init(const HostOptions& options) {
+  auto started = Clock::now();
+  HostContext ctx;
+  Impl& impl = *ctx.impl_;
+  impl.scheduler.configure(options.scheduler, options.kernel_map);
+  int n = 0;
+  check(hcl_init(options.cuda_ordinals.empty() ? nullptr : options.cuda_ordinals.data(),
+                 static_cast<int>(options.cuda_ordinals.size()), &n));
+  std::vector<std::pair<int, DeviceModel>> sched;
+  for (int i = 0; i < n; ++i) {
+    DeviceEntry e;
+    e.global_id = i;
+    e.local_index = static_cast<uint32_t>(i);
+    e.cuda_ordinal = options.cuda_ordinals.empty() ? i : options.cuda_ordinals[i];
+    int type = 1, sms = 0;
+    double rel = 1.0;
+    uint64_t hbm = 0;
+    char name[128];
+    check(hcl_device_info(i, &type, &rel, &sms, &hbm, name, sizeof(name)));
+    e.name = name;
+    e.model = DeviceModel{static_cast<DeviceType>(type), rel};
+    impl.device_map.entries.push_back(e);
+    sched.emplace_back(i, e.model);
+  }
+  impl.scheduler.sync_devices(sched);
+  impl.timings.init_ms = ms_since(started);
+  return ctx;
+}
+
+const GlobalDeviceMap& HostContext::device_map() const { return impl_->device_map; }
+
+std::vector<int> HostContext::get_device_ids(std::optional<DeviceType> filter) const {
+  std::vector<int> ids;
+  for (const auto& e : impl_->device_map.entries)
+    if (!filter || e.model.type == *filter) ids.push_back(e.global_id);
+  return ids;
+}
+
+Handle HostContext::create_queue(int gid, std::string user_id, bool shared) {
+  std::lock_guard lock(impl_->mu);
+  if (!impl_->device_map.find(gid)) fail(ErrorCode::unknown_device, "device " + std::to_string(gid));
+  uint64_t id = impl_->new_id();
+  Impl::QueueRec q;
+  q.gid = gid;
+  q.user = std::move(user_id);
+  q.shared = shared;
+  impl_->queues.emplace(id, std::move(q));
+  return Handle{HandleKind::queue, id};
+}
+
+Handle HostContext::create_buffer(uint64_t size) {
+  std::lock_guard lock(impl_->mu);
+  uint64_t id = impl_->new_id();
+  impl_->buffers[id].size = size;
+  return Handle{HandleKind::buffer, id};
+}
+
+Handle HostContext::create_program(const std::string& bundle) {
+  std::lock_guard lock(impl_->mu);
+  char names[4096];
+  uint32_t arities[256];
+  int n = 0;
+  impl_->trace.record({0, "query_registry", 0});
+  check(hcl_query_registry(bundle.c_str(), names, sizeof(names), arities, 256, &n));
+  Impl::ProgramRec p;
+  p.bundle = bundle;
+  std::string csv = names;
+  size_t pos = 0;
+  for (int i = 0; i < n; ++i) {
+    size_t c = csv.find(',', pos);
+    p.kernels.emplace_back(csv.substr(pos, c == std::string::npos ? std::string::npos : c - pos), arities[i]);
+    pos = c + 1;
+  }
+  uint64_t id = impl_->new_id();
+  impl_->programs.emplace(id, std::move(p));
+  return Handle{HandleKind::program, id};
+}
+
+Handle HostContext::create_kernel(Handle program, const std::string& kernel_name) {
+  std::lock_guard lock(impl_->mu);
+  if (program.kind != HandleKind::program) fail(ErrorCode::handle, "not a program handle");
+  auto it = impl_->programs.find(program.id);
+  if (it == impl_->programs.end()) fail(ErrorCode::handle, "program handle is released or unknown");
+  const auto& ks = it->second.kernels;
+  auto e = std::find_if(ks.begin(), ks.end(), [&](const auto& x) { return x.first == kernel_name; });
+  if (e == ks.end()) {
+    std::string names;
+    for (const auto& x : ks) names += (names.empty() ? "" : ", ") + x.first;
+    fail(ErrorCode::name, "unknown kernel '" + kernel_name + "' (available: " + names + ")");
+  }
+  Impl::KernelRec k = impl_->temp_kernel(kernel_name);
+  k.program = program.id;
+  k.bundle = it->second.bundle;
+  uint64_t id = impl_->new_id();
+  impl_->kernels.emplace(id, std::move(k));
+  return Handle{HandleKind::kernel, id};
+}
+
+void HostContext::set_kernel_arg(Handle kernel, uint32_t index, int64_t scalar) {
+  std::lock_guard lock(impl_->mu);
+  if (kernel.kind != HandleKind::kernel) fail(ErrorCode::handle, "not a kernel handle");
+  impl_->kernel(kernel.id).args[index] = Arg::of_i64(scalar);
+}
+
+void HostContext::set_kernel_arg(Handle kernel, uint32_t index, Handle buffer) {
+  std::lock_guard lock(impl_->mu);
+  if (kernel.kind != HandleKind::kernel) fail(ErrorCode::handle, "not a kernel handle");
+  if (buffer.kind != HandleKind::buffer) fail(ErrorCode::handle, "argument is not a buffer handle");
+  impl_->kernel(kernel.id).args[index] = Arg::of_handle(buffer.id);
+}
+
+Handle HostContext::enqueue_write_buffer(Handle queue, Handle buffer, std::span<const uint8_t> data, uint64_t offset) {
+  std::lock_guard lock(impl_->mu);
+  Impl::QueueRec& q = impl_->queue(queue.id);
+  if (buffer.kind != HandleKind::buffer) fail(ErrorCode::handle, "not a buffer handle");
+  Impl::BufferRec& b = impl_->buffer(buffer.id);
+  if (offset + data.size() > b.size)
+    fail(ErrorCode::size, "write of " + std::to_string(data.size()) + " bytes at offset " + std::to_string(offset) +
+                              " into a " + std::to_string(b.size) + "-byte buffer");
+  auto started = Clock::now();
+  Impl::Piece& p = impl_->ensure_alloc(buffer.id, b, q.gid, offset, data.size());
+  if (!data.empty()) {
+    impl_->trace.record({q.gid, "write_buffer", buffer.id});
+    check(hcl_buffer_write(impl_->dev_index(q.gid), buffer.id, offset, data.data(), data.size()));
+  }
+  Impl::set_valid(p, offset, data.size());
+  Impl::invalidate_others(b, q.gid, offset, data.size());
+  impl_->note_residency(buffer.id, b);
+  impl_->add_transfer(&q, ms_since(started));
+  return impl_->new_event();
+}
+
+void HostContext::enqueue_read_buffer_into(Handle queue, Handle buffer, void* dst, uint64_t offset, uint64_t len) {
+  std::lock_guard lock(impl_->mu);
+  Impl::QueueRec& q = impl_->queue(queue.id);
+  if (buffer.kind != HandleKind::buffer) fail(ErrorCode::handle, "not a buffer handle");
+  Impl::BufferRec& b = impl_->buffer(buffer.id);
+  if (offset + len > b.size) fail(ErrorCode::size, "read past the end of the buffer");
+  auto started = Clock::now();
+  auto* out = static_cast<uint8_t*>(dst);
+  uint64_t pos = offset, end = offset + len;
+  while (pos < end) {
+    int src = -1;
+    uint64_t src_end = 0;
+    auto holds = [&](const Impl::Piece& o) { return o.valid_bytes && pos >= o.valid_first && pos < o.valid_first + o.valid_bytes; };
+    auto qi = b.pieces.find(q.gid);
+    if (qi != b.pieces.end() && holds(qi->second)) {
+      src = q.gid;
+      src_end = qi->second.valid_first + qi->second.valid_bytes;
+    } else {
+      for (auto& [g, o] : b.pieces)
+        if (holds(o)) {
+          src = g;
+          src_end = o.valid_first + o.valid_bytes;
+          break;
+        }
+    }
+    if (src < 0) {  // never written: zeros (SPEC design decision; runtime.cpp:496-497)
+      uint64_t next = end;
+      for (auto& [g, o] : b.pieces)
+        if (o.valid_bytes && o.valid_first > pos) next = std::min(next, o.valid_first);
+      std::memset(out + (pos - offset), 0, next - pos);
+      pos = next;
+      continue;
+    }
+    uint64_t n = std::min(end, src_end) - pos;
+    impl_->trace.record({src, "read_buffer", buffer.id});
+    check(hcl_buffer_read(impl_->dev_index(src), buffer.id, pos, out + (pos - offset), n));
+    pos += n;
+  }
+  impl_->add_transfer(&q, ms_since(started));
+}
+
+std::vector<uint8_t> HostContext::enqueue_read_buffer(Handle queue, Handle buffer) {
+  uint64_t size = buffer_size(buffer);
+  std::vector<uint8_t> out(size);
+  enqueue_read_buffer_into(queue, buffer, out.data(), 0, size);
+  return out;
+}
+
+Handle HostContext::enqueue_ndrange_kernel(Handle queue, Handle kernel, std::array<uint64_t, 3> global_size,
+                                           uint32_t dims) {
+  std::lock_guard lock(impl_->mu);
+  Impl::QueueRec& q = impl_->queue(queue.id);
+  if (kernel.kind != HandleKind::kernel) fail(ErrorCode::handle, "not a kernel handle");
+  std::vector<Arg> args;
+  Impl::KernelRec& k = impl_->bound_kernel(kernel.id, args);
+  for (uint32_t d = 0; d < dims && d < 3; ++d)
+    if (global_size[d] < 1) fail(ErrorCode::argument, "global_size extents must be >= 1");
+  // the reference carries global_size but runs the kernel whole (daemon.cpp:334)
+  return impl_->launch_parts(k, args, global_size, dims, {{q.gid, queue.id, 0, global_size[0]}}, true);
+}
+
+std::vector<uint64_t> HostContext::partition_plan(Handle kernel, std::array<uint64_t, 3> global_size,
+                                                  const std::vector<Handle>& queues, std::vector<uint64_t> weights) {
+  std::lock_guard lock(impl_->mu);
+  if (queues.empty()) fail(ErrorCode::argument, "partitioned launch needs at least one queue");
+  Impl::KernelRec& k = impl_->kernel(kernel.id);
+  if (weights.empty()) {
+    std::vector<int> gids;
+    for (const Handle& h : queues) gids.push_back(impl_->queue(h.id).gid);
+    weights = impl_->scheduler.partition_weights(k.name, gids);
+  }
+  if (weights.size() != queues.size()) fail(ErrorCode::argument, "one weight per queue");
+  return split_ranges(global_size[0], weights);
+}
+
+Handle HostContext::enqueue_ndrange_kernel(Handle kernel, std::array<uint64_t, 3> global_size, uint32_t dims,
+                                           const std::vector<Handle>& queues, std::vector<uint64_t> weights) {
+  std::lock_guard lock(impl_->mu);
+  for (uint32_t d = 0; d < dims && d < 3; ++d)
+    if (global_size[d] < 1) fail(ErrorCode::argument, "global_size extents must be >= 1");
+  std::vector<uint64_t> bounds = partition_plan(kernel, global_size, queues, std::move(weights));
+  std::vector<Arg> args;
+  Impl::KernelRec& k = impl_->bound_kernel(kernel.id, args);
+  std::vector<Impl::Part> parts;
+  for (size_t i = 0; i < queues.size(); ++i)
+    parts.push_back({impl_->queue(queues[i].id).gid, queues[i].id, bounds[i], bounds[i + 1]});
+  return impl_->launch_parts(k, args, global_size, dims, parts, false);
+}
+
+std::pair<int, Handle> HostContext::submit_task(const KernelTask& task) {
+  std::lock_guard lock(impl_->mu);
+  Impl::KernelRec k = impl_->temp_kernel(task.kernel_name);
+  if (task.args.size() != k.arity)
+    fail(ErrorCode::argument, task.kernel_name + ": expected " + std::to_string(k.arity) + " bound arguments");
+  if (task.placement.mode == Placement::Mode::auto_policy && !impl_->scheduler.has_policy(task.placement.policy))
+    fail(ErrorCode::policy, "unknown policy '" + task.placement.policy + "'");
+  TaskEstimate est;
+  double work = 1.0;
+  for (size_t i = 0; i < task.args.size(); ++i)
+    if (task.args[i].is_buffer) {
+      uint64_t size = impl_->buffer(task.args[i].buffer).size;
+      (k.kinds[i] == HCL_ARG_OUT ? est.out_bytes : est.in_bytes) += size;
+    }
+  // work estimate: the reference's formulas (kernels.cpp:285-298) where they apply
+  std::vector<int64_t> sc;
+  for (const auto& a : task.args)
+    if (!a.is_buffer) sc.push_back(a.scalar);
+  if ((task.kernel_name == "matmul" || task.kernel_name.rfind("gemm", 0) == 0) && sc.size() >= 3)
+    work = 2.0 * sc[0] * sc[1] * sc[2];
+  else if (task.kernel_name == "vecadd" && !sc.empty())
+    work = static_cast<double>(sc[0]);
+  else if (task.kernel_name == "knn" && sc.size() >= 3)
+    work = static_cast<double>(sc[2]) * sc[0] * sc[1];
+  est.work_units = work;
+  int chosen = impl_->scheduler.schedule(task, est);
+  uint64_t qid;
+  auto it = impl_->internal_queues.find(chosen);
+  if (it != impl_->internal_queues.end()) {
+    qid = it->second;
+  } else {
+    qid = create_queue(chosen).id;
+    impl_->internal_queues[chosen] = qid;
+  }
+  Handle ev = impl_->launch_parts(k, task.args, task.global_size, task.dims, {{chosen, qid, 0, task.global_size[0]}}, true);
+  return {chosen, ev};
+}
+
+Handle HostContext::launch_task(Handle queue, const KernelTask& task) {
+  std::lock_guard lock(impl_->mu);
+  Impl::QueueRec& q = impl_->queue(queue.id);
+  Impl::KernelRec k = impl_->temp_kernel(task.kernel_name);
+  if (task.args.size() != k.arity)
+    fail(ErrorCode::argument, task.kernel_name + ": expected " + std::to_string(k.arity) + " bound arguments");
+  return impl_->launch_parts(k, task.args, task.global_size, task.dims, {{q.gid, queue.id, 0, task.global_size[0]}}, true);
+}
+
+TimingFragment HostContext::finish(Handle queue) {
+  std::lock_guard lock(impl_->mu);
+  Impl::QueueRec& q = impl_->queue(queue.id);
+  check(hcl_finish(impl_->dev_index(q.gid), nullptr));
+  for (auto& l : q.pending) {
+    float ms = 0.f;
+    cudaEventSynchronize(l.stop);
+    cudaEventElapsedTime(&ms, l.start, l.stop);
+    q.compute_ms += ms;
+    const DeviceEntry* e = impl_->device_map.find(l.gid);
+    double modeled = static_cast<double>(l.work) /
+                     ((e ? e->model.relative_throughput : 1.0) * impl_->scheduler.options().baseline_rate) * 1000.0;
+    q.modeled_ms += modeled;
+    {
+      std::lock_guard lb(impl_->breakdown_mu);
+      impl_->timings.compute_ms += ms;
+      impl_->timings.modeled_compute_ms += modeled;
+    }
+    if (ms > 0.f && l.work > 0) impl_->scheduler.record_profile(l.gid, l.kernel, static_cast<double>(l.work), ms / 1000.0);
+    cudaEventDestroy(l.start);
+    cudaEventDestroy(l.stop);
+  }
+  q.pending.clear();
+  TimingFragment f{q.transfer_ms, q.compute_ms, q.modeled_ms};
+  q.transfer_ms = q.compute_ms = q.modeled_ms = 0.0;
+  return f;
+}
+
+void HostContext::release(Handle h) {
+  std::lock_guard lock(impl_->mu);
+  switch (h.kind) {
+    case HandleKind::buffer: {
+      Impl::BufferRec& b = impl_->buffer(h.id);
+      for (auto& [g, p] : b.pieces)
+        if (p.allocated) {
+          impl_->trace.record({g, "release_object", h.id});
+          check(hcl_buffer_release(impl_->dev_index(g), h.id));
+        }
+      impl_->buffers.erase(h.id);
+      impl_->scheduler.drop_resident(h.id);
+      return;
+    }
+    case HandleKind::queue: {
+      Impl::QueueRec& q = impl_->queue(h.id);
+      if (!q.pending.empty()) check(hcl_finish(impl_->dev_index(q.gid), nullptr));
+      for (auto& l : q.pending) {
+        cudaEventDestroy(l.start);
+        cudaEventDestroy(l.stop);
+      }
+      for (auto it = impl_->internal_queues.begin(); it != impl_->internal_queues.end();)
+        it = it->second == h.id ? impl_->internal_queues.erase(it) : std::next(it);
+      impl_->queues.erase(h.id);
+      return;
+    }
+    case HandleKind::program:
+      if (!impl_->programs.erase(h.id)) fail(ErrorCode::handle, "program handle is released or unknown");
+      return;
+    case HandleKind::kernel:
+      if (!impl_->kernels.erase(h.id)) fail(ErrorCode::handle, "kernel handle is released or unknown");
+      return;
+    case HandleKind::event:
+      if (!impl_->events.erase(h.id)) fail(ErrorCode::handle, "event handle is released or unknown");
+      return;
+    case HandleKind::context:
+      fail(ErrorCode::handle, "the context is not a releasable handle");
+  }
+}
+
+TimingBreakdown HostContext::breakdown() const {
+  std::lock_guard lock(impl_->breakdown_mu);
+  return impl_->timings;
+}
+
+void HostContext::add_data_creation_ms(double ms) {
+  std::lock_guard lock(impl_->breakdown_mu);
+  impl_->timings.data_creation_ms += ms;
+}
+
+MessageTrace& HostContext::trace() { return impl_->trace; }
+Scheduler& HostContext::scheduler() { return impl_->scheduler; }
+
+uint64_t HostContext::buffer_size(Handle buffer) const {
+  std::lock_guard lock(impl_->mu);
+  if (buffer.kind != HandleKind::buffer) fail(ErrorCode::handle, "not a buffer handle");
+  return impl_->buffer(buffer.id).size;
+}
+
+int HostContext::queue_device(Handle queue) const {
+  std::lock_guard lock(impl_->mu);
+  return impl_->queue(queue.id).gid;
+}
+
+void* HostContext::buffer_device_ptr(Handle buffer, int gid, uint64_t* first_byte, uint64_t* bytes) const {
+  std::lock_guard lock(impl_->mu);
+  impl_->buffer(buffer.id);
+  void* p = nullptr;
+  check(hcl_buffer_device_ptr(impl_->dev_index(gid), buffer.id, &p, first_byte, bytes));
+  return p;
+}
+
+}  // namespace haocl
+
+// ---------------------------------------------------------------------------
+// C entry points (include/hcl_host.h)
+
+struct hcl_context {
+  haocl::HostContext ctx;
+};
+
+namespace {
+template <typename F>
+int ctx_guarded(F&& f) {
+  try {
+    f();
+    return HCL_OK;
+  } catch (const haocl::Error& e) {
+    hcl::set_last_error(e.what());
+    return HCL_ERR_BASE + static_cast<int>(e.code());
+  } catch (const std::exception& e) {
+    hcl::set_last_error(std::string("internal: ") + e.what());
+    return HCL_ERR_BASE;
+  }
+}
+using haocl::Handle;
+using haocl::HandleKind;
+Handle H(HandleKind k, uint64_t id) { return Handle{k, id}; }
+}  // namespace
+
+extern "C" {
+
+int hcl_ctx_init(const int* ordinals, int n, const hcl_scheduler_options* opts, hcl_context** out) {
+  return ctx_guarded([&] {
+    haocl::HostOptions o;
+    if (ordinals && n > 0) o.cuda_ordinals.assign(ordinals, ordinals + n);
+    if (opts) {
+      o.scheduler.baseline_rate = opts->baseline_rate;
+      o.scheduler.net_bandwidth = opts->net_bandwidth;
+      o.scheduler.ema_alpha = opts->ema_alpha;
+    }
+    *out = new hcl_context{haocl::HostContext::init(o)};
+  });
+}
+
+int hcl_ctx_destroy(hcl_context* ctx) {
+  delete ctx;
+  return HCL_OK;
+}
+
+int hcl_ctx_get_device_ids(hcl_context* ctx, int* ids, int cap, int* n) {
+  return ctx_guarded([&] {
+    auto v = ctx->ctx.get_device_ids();
+    *n = static_cast<int>(v.size());
+    for (int i = 0; i < *n && i < cap; ++i) ids[i] = v[i];
+  });
+}
+
+int hcl_ctx_create_queue(hcl_context* ctx, int gid, const char* user, int shared, uint64_t* queue) {
+  return ctx_guarded([&] { *queue = ctx->ctx.create_queue(gid, user ? user : "default", shared != 0).id; });
+}
+int hcl_ctx_create_buffer(hcl_context* ctx, uint64_t size, uint64_t* buffer) {
+  return ctx_guarded([&] { *buffer = ctx->ctx.create_buffer(size).id; });
+}
+int hcl_ctx_create_program(hcl_context* ctx, const char* bundle, uint64_t* program) {
+  return ctx_guarded([&] { *program = ctx->ctx.create_program(bundle).id; });
+}
+int hcl_ctx_create_kernel(hcl_context* ctx, uint64_t program, const char* name, uint64_t* kernel) {
+  return ctx_guarded([&] { *kernel = ctx->ctx.create_kernel(H(HandleKind::program, program), name).id; });
+}
+int hcl_ctx_set_kernel_arg_i64(hcl_context* ctx, uint64_t kernel, uint32_t index, int64_t value) {
+  return ctx_guarded([&] { ctx->ctx.set_kernel_arg(H(HandleKind::kernel, kernel), index, value); });
+}
+int hcl_ctx_set_kernel_arg_buffer(hcl_context* ctx, uint64_t kernel, uint32_t index, uint64_t buffer) {
+  return ctx_guarded([&] { ctx->ctx.set_kernel_arg(H(HandleKind::kernel, kernel), index, H(HandleKind::buffer, buffer)); });
+}
+int hcl_ctx_enqueue_write_buffer(hcl_context* ctx, uint64_t queue, uint64_t buffer, const void* data, uint64_t len,
+                                 uint64_t offset, uint64_t* event) {
+  return ctx_guarded([&] {
+    auto ev = ctx->ctx.enqueue_write_buffer(H(HandleKind::queue, queue), H(HandleKind::buffer, buffer),
+                                            std::span<const uint8_t>(static_cast<const uint8_t*>(data), len), offset);
+    if (event) *event = ev.id;
+  });
+}
+int hcl_ctx_enqueue_read_buffer(hcl_context* ctx, uint64_t queue, uint64_t buffer, void* dst, uint64_t offset,
+                                uint64_t len) {
+  return ctx_guarded([&] {
+    ctx->ctx.enqueue_read_buffer_into(H(HandleKind::queue, queue), H(HandleKind::buffer, buffer), dst, offset, len);
+  });
+}
+int hcl_ctx_enqueue_ndrange_kernel(hcl_context* ctx, uint64_t queue, uint64_t kernel, const uint64_t global[3],
+                                   uint32_t dims, uint64_t* event) {
+  return ctx_guarded([&] {
+    std::array<uint64_t, 3> g = {1, 1, 1};
+    if (global) g = {global[0], global[1], global[2]};
+    auto ev = ctx->ctx.enqueue_ndrange_kernel(H(HandleKind::queue, queue), H(HandleKind::kernel, kernel), g, dims);
+    if (event) *event = ev.id;
+  });
+}
+int hcl_ctx_enqueue_ndrange_partitioned(hcl_context* ctx, uint64_t kernel, const uint64_t global[3], uint32_t dims,
+                                        const uint64_t* queues, int nqueues, const uint64_t* weights, uint64_t* event) {
+  return ctx_guarded([&] {
+    std::vector<Handle> qs;
+    for (int i = 0; i < nqueues; ++i) qs.push_back(H(HandleKind::queue, queues[i]));
+    std::vector<uint64_t> w;
+    if (weights) w.assign(weights, weights + nqueues);
+    auto ev = ctx->ctx.enqueue_ndrange_kernel(H(HandleKind::kernel, kernel), {global[0], global[1], global[2]}, dims,
+                                              qs, w);
+    if (event) *event = ev.id;
+  });
+}
+int hcl_ctx_partition_plan(hcl_context* ctx, uint64_t kernel, const uint64_t global[3], const uint64_t* queues,
+                           int nqueues, const uint64_t* weights, uint64_t* bounds) {
+  return ctx_guarded([&] {
+    std::vector<Handle> qs;
+    for (int i = 0; i < nqueues; ++i) qs.push_back(H(HandleKind::queue, queues[i]));
+    std::vector<uint64_t> w;
+    if (weights) w.assign(weights, weights + nqueues);
+    auto b = ctx->ctx.partition_plan(H(HandleKind::kernel, kernel), {global[0], global[1], global[2]}, qs, w);
+    std::memcpy(bounds, b.data(), b.size() * sizeof(uint64_t));
+  });
+}
+int hcl_ctx_submit_task(hcl_context* ctx, const char* kernel, const uint8_t* is_buffer, const int64_t* values,
+                        int nargs, const char* policy, int explicit_device, int* chosen, uint64_t* event) {
+  return ctx_guarded([&] {
+    haocl::KernelTask t;
+    t.kernel_name = kernel;
+    for (int i = 0; i < nargs; ++i)
+      t.args.push_back(is_buffer[i] ? haocl::Arg::of_handle(static_cast<uint64_t>(values[i])) : haocl::Arg::of_i64(values[i]));
+    t.placement = (policy && *policy) ? haocl::Placement::auto_with(policy) : haocl::Placement::explicit_on(explicit_device);
+    auto [c, ev] = ctx->ctx.submit_task(t);
+    if (chosen) *chosen = c;
+    if (event) *event = ev.id;
+  });
+}
+int hcl_ctx_finish(hcl_context* ctx, uint64_t queue, double* transfer_ms, double* compute_ms, double* modeled_ms) {
+  return ctx_guarded([&] {
+    auto f = ctx->ctx.finish(H(HandleKind::queue, queue));
+    if (transfer_ms) *transfer_ms = f.transfer_ms;
+    if (compute_ms) *compute_ms = f.compute_ms;
+    if (modeled_ms) *modeled_ms = f.modeled_ms;
+  });
+}
+int hcl_ctx_release(hcl_context* ctx, uint8_t kind, uint64_t id) {
+  return ctx_guarded([&] { ctx->ctx.release(H(static_cast<HandleKind>(kind), id)); });
+}
+int hcl_ctx_breakdown(hcl_context* ctx, double out[5]) {
+  return ctx_guarded([&] {
+    auto b = ctx->ctx.breakdown();
+    out[0] = b.init_ms;
+    out[1] = b.data_creation_ms;
+    out[2] = b.transfer_ms;
+    out[3] = b.compute_ms;
+    out[4] = b.modeled_compute_ms;
+  });
+}
+int hcl_ctx_add_data_creation_ms(hcl_context* ctx, double ms) {
+  return ctx_guarded([&] { ctx->ctx.add_data_creation_ms(ms); });
+}
+int hcl_ctx_buffer_size(hcl_context* ctx, uint64_t buffer, uint64_t* size) {
+  return ctx_guarded([&] { *size = ctx->ctx.buffer_size(H(HandleKind::buffer, buffer)); });
+}
+int hcl_ctx_buffer_device_ptr(hcl_context* ctx, uint64_t buffer, int gid, void** ptr, uint64_t* first_byte,
+                              uint64_t* bytes) {
+  return ctx_guarded([&] { *ptr = ctx->ctx.buffer_device_ptr(H(HandleKind::buffer, buffer), gid, first_byte, bytes); });
+}
+int hcl_ctx_trace_count(hcl_context* ctx, const char* function, int device, uint64_t* count) {
+  return ctx_guarded([&] { *count = ctx->ctx.trace().count_calls(function, device); });
+}
+int hcl_ctx_trace_clear(hcl_context* ctx) {
+  return ctx_guarded([&] { ctx->ctx.trace().clear(); });
+}
+int hcl_ctx_sched_record_profile(hcl_context* ctx, int gid, const char* kernel, double work, double seconds) {
+  return ctx_guarded([&] { ctx->ctx.scheduler().record_profile(gid, kernel, work, seconds); });
+}
+int hcl_ctx_sched_rate(hcl_context* ctx, int gid, const char* kernel, double* rate) {
+  return ctx_guarded([&] {
+    auto st = ctx->ctx.scheduler().snapshot();
+    const auto* d = st.find(gid);
+    if (!d) throw haocl::Error(haocl::ErrorCode::unknown_device, "device " + std::to_string(gid));
+    auto it = d->profiled_rate.find(kernel);
+    *rate = it == d->profiled_rate.end() ? 0.0 : it->second;
+  });
+}
+int hcl_ctx_sched_schedule(hcl_context* ctx, const char* kernel, const char* policy, int explicit_device,
+                           double work, uint64_t in_bytes, uint64_t out_bytes, int* chosen) {
+  return ctx_guarded([&] {
+    haocl::KernelTask t;
+    t.kernel_name = kernel;
+    t.placement = (policy && *policy) ? haocl::Placement::auto_with(policy) : haocl::Placement::explicit_on(explicit_device);
+    *chosen = ctx->ctx.scheduler().schedule(t, haocl::TaskEstimate{work, in_bytes, out_bytes});
+  });
+}
+int hcl_ctx_sched_set_model(hcl_context* ctx, int gid, double relative_throughput) {
+  return ctx_guarded([&] {
+    auto st = ctx->ctx.scheduler().snapshot();
+    std::vector<std::pair<int, haocl::DeviceModel>> devs;
+    for (auto& d : st.devices)
+      devs.push_back({d.global_id, d.global_id == gid ? haocl::DeviceModel{d.model.type, relative_throughput} : d.model});
+    ctx->ctx.scheduler().sync_devices(devs);
+  });
+}
+int hcl_ctx_sched_partition_weights(hcl_context* ctx, const char* kernel, const int* gids, int n, uint64_t* weights) {
+  return ctx_guarded([&] {
+    auto w = ctx->ctx.scheduler().partition_weights(kernel, std::vector<int>(gids, gids + n));
+    std::memcpy(weights, w.data(), w.size() * sizeof(uint64_t));
+  });
+}
+
+}  // extern "C"

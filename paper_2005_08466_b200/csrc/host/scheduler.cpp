@@ -1,0 +1,392 @@
+// Scheduler and the NDRange partitioner.
+//
+// Scheduler: the reference's pluggable placement (proj/src/scheduler.cpp):
+// user_directed / round_robin / static_map / cost_model, EMA profiles
+// (alpha 0.3, first sample sets the rate, 136-149), residency-aware modeled
+// cost (38-48), strict-< argmin keeping the smallest id on ties (81-106).
+// New: partition_weights — the per-device EMA rates become integer split
+// weights for a partitioned NDRange.
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <mutex>
+
+#include "haocl/runtime.hpp"
+#include "hcl_host.h"
+
+namespace haocl {
+
+const char* error_code_name(ErrorCode code) {
+  static const char* names[] = {"internal", "protocol", "version", "malformed", "encoding", "unknown_call",
+                                "busy", "precondition", "reassembly_conflict", "argument", "name", "config",
+                                "connect", "timeout", "transport", "remote", "handle", "policy", "size",
+                                "mapping", "unknown_device", "registration", "contract", "parse"};
+  auto i = static_cast<size_t>(code);
+  return i < sizeof(names) / sizeof(names[0]) ? names[i] : "unknown";
+}
+
+[[noreturn]] static void fail(ErrorCode code, const std::string& m) { throw Error(code, m); }
+
+DeviceState* ClusterState::find(int global_id) {
+  for (auto& d : devices)
+    if (d.global_id == global_id) return &d;
+  return nullptr;
+}
+const DeviceState* ClusterState::find(int global_id) const {
+  for (const auto& d : devices)
+    if (d.global_id == global_id) return &d;
+  return nullptr;
+}
+
+struct Scheduler::Impl {
+  SchedulerOptions options;
+  std::map<std::string, int> kernel_map;
+  std::map<std::string, PolicyFn> policies;
+  std::shared_ptr<std::atomic<uint64_t>> rr = std::make_shared<std::atomic<uint64_t>>(0);
+  mutable std::mutex mu;
+  ClusterState state;
+
+  void builtins() {
+    policies["user_directed"] = [](const KernelTask& task, const ClusterState& st, const TaskEstimate&) {
+      if (task.placement.mode != Placement::Mode::explicit_device)
+        fail(ErrorCode::policy, "user_directed requires an explicit device id");
+      if (!st.find(task.placement.device_id))
+        fail(ErrorCode::unknown_device, "device " + std::to_string(task.placement.device_id) + " not in the cluster");
+      return task.placement.device_id;
+    };
+    auto counter = rr;
+    policies["round_robin"] = [counter](const KernelTask&, const ClusterState& st, const TaskEstimate&) {
+      if (st.devices.empty()) fail(ErrorCode::precondition, "no devices");
+      uint64_t turn = counter->fetch_add(1);
+      return st.devices[turn % st.devices.size()].global_id;
+    };
+    auto table = kernel_map;
+    policies["static_map"] = [table](const KernelTask& task, const ClusterState& st, const TaskEstimate&) {
+      auto it = table.find(task.kernel_name);
+      if (it == table.end()) fail(ErrorCode::mapping, "static_map has no entry for kernel '" + task.kernel_name + "'");
+      if (!st.find(it->second))
+        fail(ErrorCode::unknown_device, "static_map entry for '" + task.kernel_name + "' names unknown device " +
+                                            std::to_string(it->second));
+      return it->second;
+    };
+    auto opts = options;
+    policies["cost_model"] = [opts](const KernelTask& task, const ClusterState& st, const TaskEstimate& est) {
+      if (st.devices.empty()) fail(ErrorCode::precondition, "no devices");
+      std::vector<uint64_t> inputs;
+      for (const auto& a : task.args)
+        if (a.is_buffer) inputs.push_back(a.buffer);
+      int best = -1;
+      double best_cost = std::numeric_limits<double>::infinity();
+      for (const auto& d : st.devices) {
+        bool resident = true;
+        for (uint64_t id : inputs)
+          if (!d.resident_buffers.count(id)) {
+            resident = false;
+            break;
+          }
+        double cost = Scheduler::modeled_cost(d, task.kernel_name, est, opts, resident);
+        if (cost < best_cost) {  // strict <: smallest id wins ties
+          best_cost = cost;
+          best = d.global_id;
+        }
+      }
+      return best;
+    };
+  }
+};
+
+Scheduler::Scheduler(SchedulerOptions options, std::map<std::string, int> kernel_map) : impl_(new Impl) {
+  impl_->options = options;
+  impl_->kernel_map = std::move(kernel_map);
+  impl_->builtins();
+}
+Scheduler::~Scheduler() = default;
+
+void Scheduler::configure(SchedulerOptions options, std::map<std::string, int> kernel_map) {
+  std::lock_guard lock(impl_->mu);
+  impl_->options = options;
+  impl_->kernel_map = std::move(kernel_map);
+  impl_->policies.clear();
+  impl_->rr->store(0);
+  impl_->builtins();
+}
+
+const SchedulerOptions& Scheduler::options() const { return impl_->options; }
+
+double Scheduler::modeled_cost(const DeviceState& device, const std::string& kernel_name, const TaskEstimate& est,
+                               const SchedulerOptions& options, bool inputs_resident) {
+  double rate = device.model.relative_throughput * options.baseline_rate;
+  auto it = device.profiled_rate.find(kernel_name);
+  if (it != device.profiled_rate.end()) rate = it->second;
+  double cost = est.work_units / rate;
+  if (!inputs_resident) cost += static_cast<double>(est.in_bytes + est.out_bytes) / options.net_bandwidth;
+  return cost;
+}
+
+void Scheduler::register_policy(const std::string& name, PolicyFn policy) {
+  std::lock_guard lock(impl_->mu);
+  if (impl_->policies.count(name)) fail(ErrorCode::registration, "policy '" + name + "' already registered");
+  impl_->policies[name] = std::move(policy);
+}
+
+bool Scheduler::has_policy(const std::string& name) const {
+  std::lock_guard lock(impl_->mu);
+  return impl_->policies.count(name) > 0;
+}
+
+int Scheduler::schedule(const KernelTask& task, const TaskEstimate& estimate) {
+  std::lock_guard lock(impl_->mu);
+  if (impl_->state.devices.empty()) fail(ErrorCode::precondition, "scheduler has no devices");
+  std::string name = task.placement.mode == Placement::Mode::explicit_device ? "user_directed" : task.placement.policy;
+  auto it = impl_->policies.find(name);
+  if (it == impl_->policies.end()) fail(ErrorCode::policy, "unknown policy '" + name + "'");
+  int chosen = it->second(task, impl_->state, estimate);
+  if (!impl_->state.find(chosen))
+    fail(ErrorCode::internal, "policy '" + name + "' chose device " + std::to_string(chosen) + " outside the device map");
+  return chosen;
+}
+
+void Scheduler::record_profile(int global_id, const std::string& kernel_name, double work_units,
+                               double observed_seconds) {
+  if (!(observed_seconds > 0.0)) fail(ErrorCode::precondition, "observed_compute_seconds must be > 0");
+  std::lock_guard lock(impl_->mu);
+  DeviceState* d = impl_->state.find(global_id);
+  if (!d) fail(ErrorCode::unknown_device, "device " + std::to_string(global_id));
+  double sample = work_units / observed_seconds;
+  auto it = d->profiled_rate.find(kernel_name);
+  if (it == d->profiled_rate.end())
+    d->profiled_rate[kernel_name] = sample;
+  else
+    it->second = impl_->options.ema_alpha * sample + (1.0 - impl_->options.ema_alpha) * it->second;
+}
+
+void Scheduler::sync_devices(const std::vector<std::pair<int, DeviceModel>>& devices) {
+  std::lock_guard lock(impl_->mu);
+  impl_->state.devices.clear();
+  for (const auto& [id, model] : devices) {
+    DeviceState d;
+    d.global_id = id;
+    d.model = model;
+    impl_->state.devices.push_back(std::move(d));
+  }
+}
+
+void Scheduler::note_dispatch(int gid) {
+  std::lock_guard lock(impl_->mu);
+  if (DeviceState* d = impl_->state.find(gid)) d->outstanding_tasks++;
+}
+void Scheduler::note_complete(int gid) {
+  std::lock_guard lock(impl_->mu);
+  if (DeviceState* d = impl_->state.find(gid)) d->outstanding_tasks = std::max(0, d->outstanding_tasks - 1);
+}
+void Scheduler::note_resident(uint64_t buffer_id, const std::vector<int>& ids) {
+  std::lock_guard lock(impl_->mu);
+  for (auto& d : impl_->state.devices) d.resident_buffers.erase(buffer_id);
+  for (int id : ids)
+    if (DeviceState* d = impl_->state.find(id)) d->resident_buffers.insert(buffer_id);
+}
+void Scheduler::drop_resident(uint64_t buffer_id) {
+  std::lock_guard lock(impl_->mu);
+  for (auto& d : impl_->state.devices) d.resident_buffers.erase(buffer_id);
+}
+ClusterState Scheduler::snapshot() const {
+  std::lock_guard lock(impl_->mu);
+  return impl_->state;
+}
+
+std::vector<uint64_t> Scheduler::partition_weights(const std::string& kernel_name, const std::vector<int>& gids) const {
+  std::lock_guard lock(impl_->mu);
+  std::vector<double> rates;
+  for (int g : gids) {
+    const DeviceState* d = impl_->state.find(g);
+    if (!d) fail(ErrorCode::unknown_device, "device " + std::to_string(g));
+    double rate = d->model.relative_throughput * impl_->options.baseline_rate;
+    auto it = d->profiled_rate.find(kernel_name);
+    if (it != d->profiled_rate.end()) rate = it->second;
+    rates.push_back(rate);
+  }
+  double mx = 0.0;
+  for (double r : rates) mx = std::max(mx, r);
+  std::vector<uint64_t> w;
+  // 20-bit resolution; identical rates give identical weights (block_range)
+  for (double r : rates) w.push_back(std::max<uint64_t>(1, static_cast<uint64_t>(std::llround(r / mx * 1048576.0))));
+  return w;
+}
+
+std::vector<uint64_t> split_ranges(uint64_t total, const std::vector<uint64_t>& weights) {
+  if (weights.empty()) fail(ErrorCode::argument, "split_ranges: no parts");
+  unsigned __int128 wsum = 0;
+  for (uint64_t w : weights) wsum += w;
+  if (wsum == 0) fail(ErrorCode::argument, "split_ranges: weights sum to zero");
+  std::vector<uint64_t> b(weights.size() + 1, 0);
+  unsigned __int128 acc = 0;
+  for (size_t i = 0; i < weights.size(); ++i) {
+    acc += weights[i];
+    b[i + 1] = static_cast<uint64_t>((static_cast<unsigned __int128>(total) * acc) / wsum);
+  }
+  return b;
+}
+
+std::vector<int64_t> spmv_partition_ranges(int64_t rows, const int64_t* row_ptr, int64_t parts,
+                                           const std::vector<uint64_t>& weights) {
+  if (parts < 1 || parts > rows) fail(ErrorCode::argument, "partition count out of range");
+  if (!weights.empty() && static_cast<int64_t>(weights.size()) != parts)
+    fail(ErrorCode::argument, "one weight per part");
+  unsigned __int128 wsum = 0;
+  for (uint64_t w : weights) wsum += w;
+  if (!weights.empty() && wsum == 0) fail(ErrorCode::argument, "weights sum to zero");
+  int64_t nnz = row_ptr[rows];
+  std::vector<int64_t> out(static_cast<size_t>(parts) + 1);
+  out[0] = 0;
+  int64_t row = 0;
+  for (int64_t p = 0; p + 1 < parts; ++p) {
+    int64_t target = weights.empty()
+                         ? (nnz + parts - 1) / parts
+                         : static_cast<int64_t>((static_cast<unsigned __int128>(static_cast<uint64_t>(nnz)) * weights[p] +
+                                                 wsum - 1) / wsum);
+    int64_t max_end = rows - (parts - 1 - p);
+    int64_t want = row_ptr[row] + target;
+    // first e in [row+1, max_end] with row_ptr[e] >= want (greedy sweep stop)
+    int64_t lo = row + 1, hi = max_end;
+    while (lo < hi) {
+      int64_t mid = lo + (hi - lo) / 2;
+      if (row_ptr[mid] >= want) hi = mid; else lo = mid + 1;
+    }
+    out[p + 1] = lo;
+    row = lo;
+  }
+  out[parts] = rows;
+  return out;
+}
+
+}  // namespace haocl
+
+// ---------------------------------------------------------------------------
+// device-free C entry points (hcl_host.h)
+
+namespace hcl {
+void set_last_error(const std::string& m);
+}
+
+namespace {
+
+template <typename F>
+int host_guarded(F&& f) {
+  try {
+    f();
+    return HCL_OK;
+  } catch (const haocl::Error& e) {
+    hcl::set_last_error(e.what());
+    return HCL_ERR_BASE + static_cast<int>(e.code());
+  } catch (const std::exception& e) {
+    hcl::set_last_error(std::string("internal: ") + e.what());
+    return HCL_ERR_BASE;
+  }
+}
+}  // namespace
+
+struct hcl_scheduler {
+  haocl::Scheduler sched;
+};
+
+extern "C" {
+
+int hcl_split_ranges(uint64_t total, const uint64_t* weights, int parts, uint64_t* bounds) {
+  return host_guarded([&] {
+    auto b = haocl::split_ranges(total, std::vector<uint64_t>(weights, weights + parts));
+    std::memcpy(bounds, b.data(), b.size() * sizeof(uint64_t));
+  });
+}
+
+int hcl_spmv_partition_ranges(int64_t rows, const int64_t* row_ptr, int64_t parts, const uint64_t* weights,
+                              int64_t* out) {
+  return host_guarded([&] {
+    std::vector<uint64_t> w;
+    if (weights) w.assign(weights, weights + parts);
+    auto r = haocl::spmv_partition_ranges(rows, row_ptr, parts, w);
+    std::memcpy(out, r.data(), r.size() * sizeof(int64_t));
+  });
+}
+
+int hcl_sched_create(const hcl_scheduler_options* opts, const int* gids, const double* rel_tp, int n,
+                     const char* const* map_kernels, const int* map_gids, int nmap, hcl_scheduler** out) {
+  return host_guarded([&] {
+    haocl::SchedulerOptions o;
+    if (opts) {
+      o.baseline_rate = opts->baseline_rate;
+      o.net_bandwidth = opts->net_bandwidth;
+      o.ema_alpha = opts->ema_alpha;
+    }
+    std::map<std::string, int> km;
+    for (int i = 0; i < nmap; ++i) km[map_kernels[i]] = map_gids[i];
+    auto* s = new hcl_scheduler{haocl::Scheduler(o, km)};
+    std::vector<std::pair<int, haocl::DeviceModel>> devs;
+    for (int i = 0; i < n; ++i) devs.push_back({gids[i], haocl::DeviceModel{haocl::DeviceType::gpu, rel_tp[i]}});
+    s->sched.sync_devices(devs);
+    *out = s;
+  });
+}
+
+int hcl_sched_destroy(hcl_scheduler* s) {
+  delete s;
+  return HCL_OK;
+}
+
+int hcl_sched_schedule(hcl_scheduler* s, const char* kernel, const char* policy, int explicit_device,
+                       double work_units, uint64_t in_bytes, uint64_t out_bytes, const uint64_t* buffers,
+                       int nbuffers, int* chosen) {
+  return host_guarded([&] {
+    haocl::KernelTask t;
+    t.kernel_name = kernel;
+    for (int i = 0; i < nbuffers; ++i) t.args.push_back(haocl::Arg::of_handle(buffers[i]));
+    t.placement = (policy && *policy) ? haocl::Placement::auto_with(policy) : haocl::Placement::explicit_on(explicit_device);
+    *chosen = s->sched.schedule(t, haocl::TaskEstimate{work_units, in_bytes, out_bytes});
+  });
+}
+
+int hcl_sched_record_profile(hcl_scheduler* s, int gid, const char* kernel, double work, double seconds) {
+  return host_guarded([&] { s->sched.record_profile(gid, kernel, work, seconds); });
+}
+
+int hcl_sched_rate(hcl_scheduler* s, int gid, const char* kernel, double* rate) {
+  return host_guarded([&] {
+    auto st = s->sched.snapshot();
+    const auto* d = st.find(gid);
+    if (!d) throw haocl::Error(haocl::ErrorCode::unknown_device, "device " + std::to_string(gid));
+    auto it = d->profiled_rate.find(kernel);
+    *rate = it == d->profiled_rate.end() ? 0.0 : it->second;
+  });
+}
+
+int hcl_sched_note_resident(hcl_scheduler* s, uint64_t buffer, const int* gids, int n) {
+  return host_guarded([&] { s->sched.note_resident(buffer, std::vector<int>(gids, gids + n)); });
+}
+
+int hcl_sched_register_fixed_policy(hcl_scheduler* s, const char* name, int gid) {
+  return host_guarded([&] {
+    s->sched.register_policy(name, [gid](const haocl::KernelTask&, const haocl::ClusterState&,
+                                         const haocl::TaskEstimate&) { return gid; });
+  });
+}
+
+int hcl_sched_modeled_cost(hcl_scheduler* s, int gid, const char* kernel, double work, uint64_t in_bytes,
+                           uint64_t out_bytes, int resident, double* cost) {
+  return host_guarded([&] {
+    auto st = s->sched.snapshot();
+    const auto* d = st.find(gid);
+    if (!d) throw haocl::Error(haocl::ErrorCode::unknown_device, "device " + std::to_string(gid));
+    *cost = haocl::Scheduler::modeled_cost(*d, kernel, haocl::TaskEstimate{work, in_bytes, out_bytes},
+                                           s->sched.options(), resident != 0);
+  });
+}
+
+int hcl_sched_partition_weights(hcl_scheduler* s, const char* kernel, const int* gids, int n, uint64_t* weights) {
+  return host_guarded([&] {
+    auto w = s->sched.partition_weights(kernel, std::vector<int>(gids, gids + n));
+    std::memcpy(weights, w.data(), w.size() * sizeof(uint64_t));
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,506 @@
+// Dense GEMM C = A * B for the partitioned NDRange (SURVEY.md §8(a) a9, configs
+// C1/C2): the reference's matmul contraction (proj/src/kernels.cpp:96-119) on
+// the 5th-generation tensor cores.
+//
+//   A  M x K row-major (K-major)          -- SPLIT_ROWS in a partitioned launch
+//   B  K x N row-major (MN-major operand) -- REPLICATE
+//   C  M x N row-major, bf16 or fp32      -- SPLIT_ROWS
+//
+// Kernel structure (one persistent CTA pair per two SMs, cta_group::2):
+//   warp 4      TMA producer: A tile 128 x 128B and B tile (256/CG) x 128B per
+//               stage into a 6-deep SWIZZLE_128B smem ring (mbarrier full/empty)
+//   warp 5      MMA issuer (leader CTA, one thread): tcgen05.mma 256x256xK into
+//               one of two TMEM accumulators (2 x 256 columns = all 512)
+//   warps 0-3   epilogue: tcgen05.ld 32x32b -> registers -> bf16/fp32 -> HBM,
+//               overlapped with the next tile's main loop (TMEM double buffer)
+// Tiles are visited in an L2-friendly grouped order (8 M-tiles per group).
+// K tails and M/N edges are handled by TMA zero fill plus masked stores.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdlib>
+#include <mutex>
+#include <string>
+
+#include "common.hpp"
+#include "ptx.cuh"
+#include "../../include/hcl_cabi.h"
+
+namespace hcl {
+namespace {
+
+constexpr int kBM = 128;            // A rows per CTA
+constexpr int kBN = 256;            // tile N (UMMA_N)
+constexpr int kThreads = 192;       // 4 epilogue warps + producer + MMA
+constexpr int kTmemCols = 512;      // 2 accumulators x 256 fp32 columns
+constexpr int kGroupM = 8;          // tile raster group
+
+template <int CG, bool TF32>
+struct Cfg {
+  static constexpr int kElem = TF32 ? 4 : 2;
+  static constexpr int kBK = 128 / kElem;        // one 128-byte swizzle row of K
+  static constexpr int kUK = 32 / kElem;         // K per tcgen05.mma
+  static constexpr int kBNLocal = kBN / CG;      // B rows (N) loaded by each CTA
+  static constexpr int kABytes = kBM * 128;
+  static constexpr int kBBytes = kBNLocal * 128;
+  static constexpr int kStage = kABytes + kBBytes;
+  static constexpr int kStages = CG == 2 ? 6 : 4;
+  static constexpr int kMNAtom = 128 / kElem;    // MN elements per swizzle atom row
+  static constexpr size_t kSmem = static_cast<size_t>(kStages) * kStage + 1024 + 256;
+};
+
+struct TileMap {
+  int num_m, num_n;
+  __device__ __forceinline__ void get(int t, int& mt, int& nt) const {
+    int group = kGroupM * num_n;
+    int g = t / group;
+    int first_m = g * kGroupM;
+    int gm = min(kGroupM, num_m - first_m);
+    int local = t - g * group;
+    mt = first_m + local % gm;
+    nt = local / gm;
+  }
+};
+
+template <int CG, bool TF32, bool BMN, bool OUTF32>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   void* __restrict__ Cout, int M, int N, int K, int64_t ldc) {
+  using C = Cfg<CG, TF32>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStage);
+  uint64_t* empty = full + C::kStages;
+  uint64_t* tfull = empty + C::kStages;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const uint32_t rank = CG == 2 ? ptx::cluster_ctarank() : 0;
+
+  if (warp == 4 && lane == 0) {
+    ptx::prefetch_tmap(&tmA);
+    ptx::prefetch_tmap(&tmB);
+    for (int s = 0; s < C::kStages; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      ptx::mbar_init(&tfull[a], 1);
+      ptx::mbar_init(&tempty[a], 4 * CG);
+    }
+    ptx::fence_mbar_init();
+  }
+  if (warp == 5) ptx::tmem_alloc<CG>(tmem_slot, kTmemCols);
+  ptx::tc_fence_before();
+  if constexpr (CG == 2) ptx::cluster_sync(); else __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const TileMap map{static_cast<int>((M + kBM * CG - 1) / (kBM * CG)), (N + kBN - 1) / kBN};
+  const int tiles = map.num_m * map.num_n;
+  const int cluster = blockIdx.x / CG, nclusters = gridDim.x / CG;
+  const int nk = (K + C::kBK - 1) / C::kBK;
+
+  if (warp == 4) {
+    // ---------------- TMA producer ----------------
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = cluster; t < tiles; t += nclusters) {
+        int mt, nt;
+        map.get(t, mt, nt);
+        const int m0 = mt * kBM * CG + static_cast<int>(rank) * kBM;
+        const int n0 = nt * kBN + static_cast<int>(rank) * C::kBNLocal;
+        for (int kb = 0; kb < nk; ++kb) {
+          ptx::mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * C::kStage;
+          uint8_t* sb = sa + C::kABytes;
+          if constexpr (CG == 1) {
+            ptx::mbar_arrive_expect_tx(&full[stage], C::kStage);
+            ptx::tma_load_2d(sa, &tmA, &full[stage], kb * C::kBK, m0);
+            if constexpr (BMN) {
+#pragma unroll
+              for (int j = 0; j < C::kBNLocal / C::kMNAtom; ++j)
+                ptx::tma_load_2d(sb + j * C::kBK * 128, &tmB, &full[stage], n0 + j * C::kMNAtom, kb * C::kBK);
+            } else {
+              ptx::tma_load_2d(sb, &tmB, &full[stage], kb * C::kBK, n0);
+            }
+          } else {
+            if (rank == 0) ptx::mbar_arrive_expect_tx(&full[stage], C::kStage * 2);
+            const uint32_t bar = ptx::mapa(ptx::smem_u32(&full[stage]), 0);
+            ptx::tma_load_2d_pair(sa, &tmA, bar, kb * C::kBK, m0);
+            if constexpr (BMN) {
+#pragma unroll
+              for (int j = 0; j < C::kBNLocal / C::kMNAtom; ++j)
+                ptx::tma_load_2d_pair(sb + j * C::kBK * 128, &tmB, bar, n0 + j * C::kMNAtom, kb * C::kBK);
+            } else {
+              ptx::tma_load_2d_pair(sb, &tmB, bar, kb * C::kBK, n0);
+            }
+          }
+          if (++stage == C::kStages) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 5) {
+    // ---------------- MMA issuer (leader CTA) ----------------
+    if (rank == 0 && lane == 0) {
+      constexpr uint32_t idesc = ptx::umma_idesc(TF32 ? 2 : 1, 0, BMN ? 1 : 0, kBM * CG, kBN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int t = cluster; t < tiles; t += nclusters) {
+        ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
+        ptx::tc_fence_after();
+        const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * kBN);
+        for (int kb = 0; kb < nk; ++kb) {
+          ptx::mbar_wait(&full[stage], phase);
+          ptx::tc_fence_after();
+          const uint32_t a_addr = ptx::smem_u32(smem + stage * C::kStage);
+          const uint32_t b_addr = a_addr + C::kABytes;
+#pragma unroll
+          for (int k = 0; k < C::kBK / C::kUK; ++k) {
+            const uint64_t adesc = ptx::umma_desc_sw128(a_addr + k * 32, 16, 1024);
+            uint64_t bdesc;
+            if constexpr (BMN)
+              bdesc = ptx::umma_desc_sw128(b_addr + k * (C::kUK / 8) * 1024, C::kBK * 128, 1024);
+            else
+              bdesc = ptx::umma_desc_sw128(b_addr + k * 32, 16, 1024);
+            ptx::mma<CG, TF32>(d_tmem, adesc, bdesc, idesc, (kb | k) != 0);
+          }
+          ptx::mma_commit<CG>(&empty[stage]);  // frees the smem slot when these MMAs finish
+          if (++stage == C::kStages) { stage = 0; phase ^= 1; }
+        }
+        ptx::mma_commit<CG>(&tfull[acc]);  // accumulator ready for the epilogue
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+    }
+    __syncwarp();
+  } else {
+    // ---------------- epilogue warps 0-3 ----------------
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int t = cluster; t < tiles; t += nclusters) {
+      int mt, nt;
+      map.get(t, mt, nt);
+      ptx::mbar_wait(&tfull[acc], acc_phase);
+      ptx::tc_fence_after();
+      const int64_t row = static_cast<int64_t>(mt) * kBM * CG + rank * kBM + warp * 32 + lane;
+      const bool row_ok = row < M;
+#pragma unroll 1
+      for (int chunk = 0; chunk < kBN / 32; ++chunk) {
+        uint32_t r[32];
+        const uint32_t taddr =
+            tmem_base + (static_cast<uint32_t>(warp * 32) << 16) + static_cast<uint32_t>(acc * kBN + chunk * 32);
+        ptx::tmem_ld_32x32b_x32(taddr, r);
+        ptx::tmem_ld_wait();
+        const int col0 = nt * kBN + chunk * 32;
+        if (!row_ok || col0 >= N) continue;
+        if constexpr (OUTF32) {
+          float* dst = reinterpret_cast<float*>(Cout) + row * ldc + col0;
+          if (col0 + 32 <= N && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              reinterpret_cast<uint4*>(dst)[j] = make_uint4(r[4 * j], r[4 * j + 1], r[4 * j + 2], r[4 * j + 3]);
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (col0 + j < N) dst[j] = __uint_as_float(r[j]);
+          }
+        } else {
+          __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(Cout) + row * ldc + col0;
+          uint32_t p[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            __nv_bfloat162 h = __floats2bfloat162_rn(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1]));
+            p[j] = *reinterpret_cast<uint32_t*>(&h);
+          }
+          if (col0 + 32 <= N && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              reinterpret_cast<uint4*>(dst)[j] = make_uint4(p[4 * j], p[4 * j + 1], p[4 * j + 2], p[4 * j + 3]);
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (col0 + j < N) dst[j] = __float2bfloat16_rn(__uint_as_float(r[j]));
+          }
+        }
+      }
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if constexpr (CG == 2)
+          ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&tempty[acc]), 0));
+        else
+          ptx::mbar_arrive(&tempty[acc]);
+      }
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+  }
+
+  ptx::tc_fence_before();
+  if constexpr (CG == 2) ptx::cluster_sync(); else __syncthreads();
+  if (warp == 5) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc<CG>(tmem_base, kTmemCols);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  if (!fn) fail(ErrorCode::internal, "cuTensorMapEncodeTiled unavailable from the driver");
+  return fn;
+}
+
+// 2D row-major tensor [outer][inner] with a SWIZZLE_128B box [box_outer][box_inner].
+CUtensorMap make_tmap(const void* base, bool f32, uint64_t inner, uint64_t outer, uint64_t row_bytes,
+                      uint32_t box_inner, uint32_t box_outer) {
+  CUtensorMap m;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {row_bytes};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode_fn()(&m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                           const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    fail(ErrorCode::argument, "cuTensorMapEncodeTiled failed (" + std::to_string(static_cast<int>(r)) +
+                                  "): base/row pitch must be 16-byte aligned");
+  return m;
+}
+
+template <int CG, bool TF32, bool BMN, bool OUTF32>
+void run_gemm(const void* A, const void* B, void* Cp, int64_t M, int64_t N, int64_t K, int64_t ldc,
+              int sm_count, cudaStream_t stream) {
+  using C = Cfg<CG, TF32>;
+  const uint64_t es = C::kElem;
+  CUtensorMap ta = make_tmap(A, TF32, K, M, K * es, C::kBK, kBM);
+  CUtensorMap tb = BMN ? make_tmap(B, TF32, N, K, N * es, C::kMNAtom, C::kBK)
+                       : make_tmap(B, TF32, K, N, K * es, C::kBK, C::kBNLocal);
+  auto kern = gemm_tc_kernel<CG, TF32, BMN, OUTF32>;
+  // per launch: the attribute is per device context and launches may target several GPUs
+  HCL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(C::kSmem)));
+  const int64_t tiles = ceil_div(M, kBM * CG) * ceil_div(N, kBN);
+  const int64_t clusters = std::min<int64_t>(tiles, sm_count / CG);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(clusters * CG));
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = C::kSmem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  HCL_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, Cp, static_cast<int>(M), static_cast<int>(N),
+                              static_cast<int>(K), ldc));
+  HCL_LAUNCHED();
+}
+
+// B (K x N) -> Bt (N x K): used only by the K-major debug variant.
+template <typename T>
+__global__ void transpose_kernel(const T* __restrict__ in, T* __restrict__ out, int64_t rows, int64_t cols) {
+  __shared__ T tile[32][33];
+  int64_t c = blockIdx.x * 32 + threadIdx.x, r0 = blockIdx.y * 32;
+  for (int i = threadIdx.y; i < 32; i += 8)
+    if (r0 + i < rows && c < cols) tile[i][threadIdx.x] = in[(r0 + i) * cols + c];
+  __syncthreads();
+  int64_t oc = r0 + threadIdx.x, or0 = blockIdx.x * 32;
+  for (int i = threadIdx.y; i < 32; i += 8)
+    if (or0 + i < cols && oc < rows) out[(or0 + i) * rows + oc] = tile[threadIdx.x][i];
+}
+
+int env_int(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  return v ? std::atoi(v) : dflt;
+}
+
+// gemm_bf16(A, B, C, M, K, N, out_f32) and gemm_tf32(A, B, C, M, K, N)
+template <bool TF32>
+uint64_t launch_gemm_tc(LaunchCtx& c) {
+  const char* what = TF32 ? "gemm_tf32" : "gemm_bf16";
+  int64_t m = scalar_arg(c, 3, "gemm M");
+  int64_t k = scalar_arg(c, 4, "gemm K");
+  int64_t n = scalar_arg(c, 5, "gemm N");
+  bool out_f32 = TF32 ? true : scalar_arg(c, 6, "gemm out_f32") != 0;
+  if (m < 1 || k < 1 || n < 1) fail(ErrorCode::argument, std::string(what) + ": dimensions must be >= 1");
+  if (m > INT32_MAX || n > INT32_MAX || k > INT32_MAX) fail(ErrorCode::argument, std::string(what) + ": dimension too large");
+  const uint64_t es = TF32 ? 4 : 2, os = out_f32 ? 4 : 2;
+  if ((k * es) % 16 || (n * es) % 16)
+    fail(ErrorCode::argument, std::string(what) + ": K and N must be multiples of " + std::to_string(16 / es) +
+                                  " (16-byte TMA row pitch)");
+  const BufView& A = buffer_arg(c, 0, "gemm A");
+  const BufView& B = buffer_arg(c, 1, "gemm B");
+  const BufView& Cb = buffer_arg(c, 2, "gemm C");
+  if (A.first_byte == 0 && A.bytes != static_cast<uint64_t>(m * k) * es)
+    fail(ErrorCode::argument, std::string(what) + ": A size != M*K");
+  if (B.first_byte != 0 || B.bytes != static_cast<uint64_t>(k * n) * es)
+    fail(ErrorCode::argument, std::string(what) + ": B size != K*N");
+  uint64_t lo, rows;
+  sub_range(c, static_cast<uint64_t>(m), lo, rows, what);
+  const void* a = at_byte<const uint8_t>(A, lo * k * es, rows * k * es, "gemm A");
+  void* cp = at_byte<uint8_t>(Cb, lo * n * os, rows * n * os, "gemm C");
+  if (rows == 0) return 0;
+  const int cg = env_int("HCL_GEMM_CG", 2);
+  const bool kmajor = env_int("HCL_GEMM_B_KMAJOR", 0) != 0;
+  const void* b = B.ptr;
+  if (kmajor) {  // debug/validation variant: transpose B to N x K first
+    void* bt = c.scratch(c.dev, static_cast<size_t>(k * n * es));
+    dim3 grid(static_cast<unsigned>(ceil_div(n, 32)), static_cast<unsigned>(ceil_div(k, 32)));
+    if (TF32)
+      transpose_kernel<float><<<grid, dim3(32, 8), 0, c.stream>>>(static_cast<const float*>(b), static_cast<float*>(bt), k, n);
+    else
+      transpose_kernel<uint16_t><<<grid, dim3(32, 8), 0, c.stream>>>(static_cast<const uint16_t*>(b), static_cast<uint16_t*>(bt), k, n);
+    HCL_LAUNCHED();
+    b = bt;
+  }
+  const int64_t M = static_cast<int64_t>(rows);
+#define HCL_GEMM_CASE(CG_, BMN_, OF_) \
+  run_gemm<CG_, TF32, BMN_, OF_>(a, b, cp, M, n, k, n, c.sm_count, c.stream)
+  if (cg == 1) {
+    if (kmajor) { if (out_f32) HCL_GEMM_CASE(1, false, true); else HCL_GEMM_CASE(1, false, false); }
+    else { if (out_f32) HCL_GEMM_CASE(1, true, true); else HCL_GEMM_CASE(1, true, false); }
+  } else {
+    if (kmajor) { if (out_f32) HCL_GEMM_CASE(2, false, true); else HCL_GEMM_CASE(2, false, false); }
+    else { if (out_f32) HCL_GEMM_CASE(2, true, true); else HCL_GEMM_CASE(2, true, false); }
+  }
+#undef HCL_GEMM_CASE
+  return 2ull * rows * static_cast<uint64_t>(n) * static_cast<uint64_t>(k);
+}
+
+// ---------------------------------------------------------------------------
+// fp32 SIMT GEMM (exact fp32 products, FFMA accumulate): 128x128 tile per
+// 256-thread block, 8x8 outputs per thread, K panels of 8 double-buffered in
+// shared memory. Used for the fp32 config where TF32 rounding is not wanted.
+
+constexpr int SG_T = 128, SG_K = 8;
+
+__global__ void __launch_bounds__(256) gemm_f32_simt_kernel(const float* __restrict__ A, const float* __restrict__ B,
+                                                            float* __restrict__ Cc, int64_t M, int64_t N, int64_t K) {
+  __shared__ __align__(16) float sa[2][SG_K][SG_T];
+  __shared__ __align__(16) float sb[2][SG_K][SG_T];
+  const int tid = threadIdx.x;
+  const int tx = tid % 16, ty = tid / 16;
+  const int64_t row0 = blockIdx.y * (int64_t)SG_T, col0 = blockIdx.x * (int64_t)SG_T;
+  float acc[8][8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+  // loaders: A tile 128 rows x 8 k (4 per thread), B tile 8 k x 128 cols (4 per thread)
+  auto load = [&](int buf, int64_t k0) {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      int idx = tid + e * 256;
+      int r = idx / SG_K, kk = idx % SG_K;
+      int64_t gr = row0 + r, gk = k0 + kk;
+      sa[buf][kk][r] = (gr < M && gk < K) ? A[gr * K + gk] : 0.f;
+      int kb = idx / SG_T, cb = idx % SG_T;
+      int64_t gkb = k0 + kb, gc = col0 + cb;
+      sb[buf][kb][cb] = (gkb < K && gc < N) ? B[gkb * N + gc] : 0.f;
+    }
+  };
+  load(0, 0);
+  __syncthreads();
+  int buf = 0;
+  for (int64_t k0 = 0; k0 < K; k0 += SG_K) {
+    if (k0 + SG_K < K) load(buf ^ 1, k0 + SG_K);
+#pragma unroll
+    for (int kk = 0; kk < SG_K; ++kk) {
+      float av[8], bv[8];
+      float4 a0 = *reinterpret_cast<const float4*>(&sa[buf][kk][ty * 4]);
+      float4 a1 = *reinterpret_cast<const float4*>(&sa[buf][kk][64 + ty * 4]);
+      float4 b0 = *reinterpret_cast<const float4*>(&sb[buf][kk][tx * 4]);
+      float4 b1 = *reinterpret_cast<const float4*>(&sb[buf][kk][64 + tx * 4]);
+      av[0] = a0.x; av[1] = a0.y; av[2] = a0.z; av[3] = a0.w;
+      av[4] = a1.x; av[5] = a1.y; av[6] = a1.z; av[7] = a1.w;
+      bv[0] = b0.x; bv[1] = b0.y; bv[2] = b0.z; bv[3] = b0.w;
+      bv[4] = b1.x; bv[5] = b1.y; bv[6] = b1.z; bv[7] = b1.w;
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+    }
+    __syncthreads();
+    buf ^= 1;
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    int64_t r = row0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + i - 4);
+    if (r >= M) continue;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      int64_t cc = col0 + (j < 4 ? tx * 4 + j : 64 + tx * 4 + j - 4);
+      if (cc < N) Cc[r * N + cc] = acc[i][j];
+    }
+  }
+}
+
+uint64_t launch_gemm_f32(LaunchCtx& c) {
+  int64_t m = scalar_arg(c, 3, "gemm_f32 M");
+  int64_t k = scalar_arg(c, 4, "gemm_f32 K");
+  int64_t n = scalar_arg(c, 5, "gemm_f32 N");
+  if (m < 1 || k < 1 || n < 1) fail(ErrorCode::argument, "gemm_f32: dimensions must be >= 1");
+  const BufView& A = buffer_arg(c, 0, "gemm_f32 A");
+  const BufView& B = buffer_arg(c, 1, "gemm_f32 B");
+  const BufView& Cb = buffer_arg(c, 2, "gemm_f32 C");
+  if (A.first_byte == 0 && A.bytes != static_cast<uint64_t>(m * k) * 4)
+    fail(ErrorCode::argument, "gemm_f32: A size != M*K");
+  if (B.first_byte != 0 || B.bytes != static_cast<uint64_t>(k * n) * 4)
+    fail(ErrorCode::argument, "gemm_f32: B size != K*N");
+  uint64_t lo, rows;
+  sub_range(c, static_cast<uint64_t>(m), lo, rows, "gemm_f32");
+  const float* a = at_byte<const float>(A, lo * k * 4, rows * k * 4, "gemm_f32 A");
+  float* cp = at_byte<float>(Cb, lo * n * 4, rows * n * 4, "gemm_f32 C");
+  if (rows == 0) return 0;
+  dim3 grid(static_cast<unsigned>(ceil_div(n, SG_T)), static_cast<unsigned>(ceil_div(rows, SG_T)));
+  gemm_f32_simt_kernel<<<grid, 256, 0, c.stream>>>(a, reinterpret_cast<const float*>(B.ptr), cp,
+                                                   static_cast<int64_t>(rows), n, k);
+  HCL_LAUNCHED();
+  return 2ull * rows * static_cast<uint64_t>(n) * static_cast<uint64_t>(k);
+}
+
+uint64_t rows_gemm(const int64_t* s, uint32_t) { return static_cast<uint64_t>(s[3]); }
+uint64_t rowbytes_gemm_bf16(const int64_t* s, uint32_t, uint32_t i) {
+  return i == 0 ? static_cast<uint64_t>(s[4]) * 2 : static_cast<uint64_t>(s[5]) * (s[6] ? 4 : 2);
+}
+uint64_t rowbytes_gemm_f32(const int64_t* s, uint32_t, uint32_t i) {
+  return static_cast<uint64_t>(i == 0 ? s[4] : s[5]) * 4;
+}
+
+}  // namespace
+
+void register_gemm(std::vector<KernelDef>& r) {
+  constexpr uint8_t S = HCL_ARG_SCALAR, I = HCL_ARG_IN, O = HCL_ARG_OUT;
+  constexpr uint8_t N = HCL_PART_NONE, P = HCL_PART_REPLICATE, X = HCL_PART_SPLIT_ROWS;
+  r.push_back({"b200", "gemm_bf16", {I, I, O, S, S, S, S}, {X, P, X, N, N, N, N}, launch_gemm_tc<false>,
+               rowbytes_gemm_bf16, rows_gemm});
+  r.push_back({"b200", "gemm_tf32", {I, I, O, S, S, S}, {X, P, X, N, N, N}, launch_gemm_tc<true>,
+               rowbytes_gemm_f32, rows_gemm});
+  r.push_back({"b200", "gemm_f32", {I, I, O, S, S, S}, {X, P, X, N, N, N}, launch_gemm_f32, rowbytes_gemm_f32,
+               rows_gemm});
+}
+
+}  // namespace hcl

@@ -19,3 +19,20 @@ def golden():
 
     with open(os.path.join(ROOT, "tests", "golden", "reference_golden.json")) as f:
         return json.load(f)
+
+
+@pytest.fixture(scope="session")
+def ctx():
+    """One HostContext for the GPU tests: four logical devices on CUDA device 0
+    (each with its own stream and buffer store), so partitioned launches over
+    P = 1, 2, 4 queues run on a single B200 — the way the reference runs P
+    daemons on localhost."""
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    from paper_2005_08466_b200 import HostContext
+
+    c = HostContext([0, 0, 0, 0])
+    yield c
+    c.close()

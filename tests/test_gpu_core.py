@@ -1,0 +1,215 @@
+"""GPU parity of the reference's "core" bundle through the host API and the
+C-ABI: outputs must be BIT-IDENTICAL to the reference (FNV-1a digests of
+tests/golden/reference_golden.json, measured by running the reference), for
+every partition P in {1, 2, 4} of the NDRange."""
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_2005_08466_b200 import HaoclError
+from paper_2005_08466_b200 import _native as N
+
+pytestmark = pytest.mark.gpu
+
+
+def h(x):
+    return "%016x" % x
+
+
+def run(ctx, kernel, args, outs, queues, global_rows=None, partitioned=False, weights=None, bundle="core"):
+    """Bind args (ints or np arrays for inputs; ('out', nbytes) for outputs), launch
+    whole on queues[0] or partitioned over queues, and return output arrays (uint8)."""
+    prog = ctx.create_program(bundle)
+    k = ctx.create_kernel(prog, kernel)
+    bufs = {}
+    for i, a in enumerate(args):
+        if isinstance(a, tuple) and a[0] == "out":
+            b = ctx.create_buffer(a[1])
+            bufs[i] = b
+            ctx.set_kernel_arg(k, i, b)
+        elif isinstance(a, np.ndarray):
+            b = ctx.create_buffer(a.nbytes)
+            ctx.enqueue_write_buffer(queues[0], b, a)
+            bufs[i] = b
+            ctx.set_kernel_arg(k, i, b)
+        else:
+            ctx.set_kernel_arg(k, i, int(a))
+    if partitioned:
+        ctx.enqueue_ndrange_partitioned(k, (global_rows, 1, 1), 1, queues, weights)
+    else:
+        ctx.enqueue_ndrange_kernel(queues[0], k, (global_rows or 1, 1, 1), 1)
+    for q in queues:
+        ctx.finish(q)
+    res = {i: ctx.enqueue_read_buffer(queues[0], bufs[i]) for i in outs}
+    for b in bufs.values():
+        ctx.release(b)
+    ctx.release(k)
+    ctx.release(prog)
+    return res
+
+
+@pytest.fixture(scope="module")
+def queues(ctx):
+    qs = [ctx.create_queue(g) for g in ctx.get_device_ids()[:4]]
+    yield qs
+    for q in qs:
+        ctx.release(q)
+
+
+@pytest.mark.parametrize("n", [64, 512, 1024])
+@pytest.mark.parametrize("P", [1, 2, 4])
+def test_matmul_bitexact_digest(ctx, queues, golden, n, P):
+    a = O.gen_doubles(n * n, 42)
+    b = O.gen_doubles(n * n, 43)
+    out = run(ctx, "matmul", [a, b, ("out", n * n * 8), n, n, n], [2], queues[:P], global_rows=n,
+              partitioned=P > 1)
+    assert h(O.fnv1a(out[2])) == golden["digests"][f"matmul_{n}"]
+
+
+def test_matmul_uneven_weights_still_bitexact(ctx, queues, golden):
+    n = 512
+    a = O.gen_doubles(n * n, 42)
+    b = O.gen_doubles(n * n, 43)
+    out = run(ctx, "matmul", [a, b, ("out", n * n * 8), n, n, n], [2], queues, global_rows=n, partitioned=True,
+              weights=[5, 1, 3, 1])
+    assert h(O.fnv1a(out[2])) == golden["digests"]["matmul_512"]
+
+
+@pytest.mark.parametrize("n", [10**5, 10**7])
+@pytest.mark.parametrize("P", [1, 4])
+def test_vecadd_digest(ctx, queues, golden, n, P):
+    a = O.gen_doubles(n, 42)
+    b = O.gen_doubles(n, 43)
+    out = run(ctx, "vecadd", [a, b, ("out", n * 8), n], [2], queues[:P], global_rows=n, partitioned=P > 1,
+              weights=[2] * P)
+    assert h(O.fnv1a(out[2])) == golden["digests"][f"vecadd_{n}"]
+
+
+@pytest.mark.parametrize("r,c,d", [(100, 100, 0.1), (10**4, 10**4, 1e-3), (10**5, 10**5, 1e-4)])
+def test_spmv_two_stage_digest(ctx, queues, golden, r, c, d):
+    """The reference bench's two-stage SpMV (proj/src/bench.cpp:210-321): stage 1
+    spmv_partition on one device, stage 2 spmv_compute per part on rebased CSR
+    slices, y reassembled at lo*8 — digest equal to the reference."""
+    rp, ci, v = O.gen_csr(r, c, d, 42)
+    x = O.gen_doubles(c, 43)
+    hdr = np.array([r, c], np.int64)
+    for P in (1, 2, 4):
+        rng = run(ctx, "spmv_partition", [hdr, rp, P, ("out", (P + 1) * 8)], [3], queues[:1])[3].view(np.int64)
+        assert (rng == O.spmv_partition_ranges(rp, P)).all()
+        y = np.empty(r, np.float64)
+        for p in range(P):
+            lo, hi = int(rng[p]), int(rng[p + 1])
+            first, last = rp[lo], rp[hi]
+            part = [np.array([hi - lo, c], np.int64), (rp[lo:hi + 1] - first).astype(np.int64),
+                    ci[first:last].copy(), v[first:last].copy(), x, 0, hi - lo, ("out", (hi - lo) * 8)]
+            y[lo:hi] = run(ctx, "spmv_compute", part, [7], [queues[p]])[7].view(np.float64)
+        assert h(O.fnv1a(y)) == golden["digests"][f"spmv_{r}x{c}@{d}"]
+
+
+def test_spmv_compute_kats_and_errors(ctx, queues):
+    # CSR identity gives y = x; empty range gives an empty slice
+    n = 50
+    rp = np.arange(n + 1, dtype=np.int64)
+    ci = np.arange(n, dtype=np.int64)
+    v = np.ones(n)
+    x = O.gen_doubles(n, 1)
+    hdr = np.array([n, n], np.int64)
+    y = run(ctx, "spmv_compute", [hdr, rp, ci, v, x, 0, n, ("out", n * 8)], [7], queues[:1])[7].view(np.float64)
+    assert (y == x).all()
+    with pytest.raises(HaoclError) as e:
+        run(ctx, "spmv_compute", [hdr, rp, ci, v, x, 5, 60, ("out", 8 * 8)], [7], queues[:1])
+    assert e.value.name == "argument"
+    bad = ci.copy()
+    bad[7] = n + 3
+    with pytest.raises(HaoclError) as e:
+        run(ctx, "spmv_compute", [hdr, rp, bad, v, x, 0, n, ("out", n * 8)], [7], queues[:1])
+    assert e.value.name == "argument" and "col_idx out of range" in str(e.value)
+
+
+@pytest.mark.parametrize("R,Q,D,K", [(200, 20, 8, 5), (10**5, 10**3, 16, 10)])
+@pytest.mark.parametrize("P", [1, 4])
+def test_knn_digest(ctx, queues, golden, R, Q, D, K, P):
+    rf = O.gen_doubles(R * D, 42)
+    q = O.gen_doubles(Q * D, 43)
+    out = run(ctx, "knn", [rf, q, R, Q, D, K, ("out", Q * K * 4), ("out", Q * K * 8)], [6, 7], queues[:P],
+              global_rows=Q, partitioned=P > 1)
+    assert h(O.fnv1a(out[7], O.fnv1a(out[6]))) == golden["digests"][f"knn_{R}x{Q}x{D}k{K}"]
+
+
+def test_knn_tie_rule(ctx, queues, golden):
+    k = golden["knn_kat"]
+    out = run(ctx, "knn", [np.array(k["ref"]), np.array(k["query"]), 5, 2, 2, k["k"], ("out", 2 * 3 * 4),
+                           ("out", 2 * 3 * 8)], [6, 7], queues[:1])
+    assert out[6].view(np.int32).tolist() == k["idx"] and out[7].view(np.float64).tolist() == k["dist"]
+
+
+def test_error_conventions(ctx, queues):
+    prog = ctx.create_program("core")
+    with pytest.raises(HaoclError) as e:
+        ctx.create_kernel(prog, "nosuch")
+    assert e.value.name == "name" and e.value.code == 10
+    with pytest.raises(HaoclError) as e:
+        ctx.create_program("nobundle")
+    assert e.value.name == "name"
+    k = ctx.create_kernel(prog, "vecadd")
+    with pytest.raises(HaoclError) as e:
+        ctx.enqueue_ndrange_kernel(queues[0], k)
+    assert e.value.name == "argument" and "unbound" in str(e.value)
+    a = ctx.create_buffer(32)
+    ctx.set_kernel_arg(k, 0, a)
+    ctx.set_kernel_arg(k, 1, a)
+    ctx.set_kernel_arg(k, 2, ctx.create_buffer(32))
+    ctx.set_kernel_arg(k, 3, 5)  # n=5 but 4-element buffers
+    with pytest.raises(HaoclError) as e:
+        ctx.enqueue_ndrange_kernel(queues[0], k)
+    assert e.value.name == "argument"
+    with pytest.raises(HaoclError) as e:
+        ctx.enqueue_write_buffer(queues[0], a, np.zeros(5))
+    assert e.value.name == "size"
+    # never-written buffers read back as zeros; use after release is a handle error
+    assert (ctx.enqueue_read_buffer(queues[0], a) == 0).all()
+    ctx.release(a)
+    with pytest.raises(HaoclError) as e:
+        ctx.enqueue_read_buffer(queues[0], a, length=32)
+    assert e.value.name == "handle"
+    with pytest.raises(HaoclError) as e:
+        ctx.release(a)
+    assert e.value.name == "handle"
+
+
+def test_buffer_migration_between_devices(ctx, queues):
+    data = np.arange(1000, dtype=np.float64)
+    b = ctx.create_buffer(data.nbytes)
+    ctx.enqueue_write_buffer(queues[0], b, data)
+    # a partial write on device 2 then a full read through device 3 gathers the pieces
+    ctx.enqueue_write_buffer(queues[2], b, np.full(10, -1.0), offset=80)
+    got = ctx.enqueue_read_buffer(queues[3], b).view(np.float64)
+    want = data.copy()
+    want[10:20] = -1.0
+    assert (got == want).all()
+    ctx.release(b)
+
+
+def test_finish_reports_compute_and_profiles(ctx, queues):
+    n = 256
+    a = O.gen_doubles(n * n, 1)
+    prog = ctx.create_program("core")
+    k = ctx.create_kernel(prog, "matmul")
+    ba, bb, bc = ctx.create_buffer(a.nbytes), ctx.create_buffer(a.nbytes), ctx.create_buffer(a.nbytes)
+    ctx.enqueue_write_buffer(queues[1], ba, a)
+    ctx.enqueue_write_buffer(queues[1], bb, a)
+    for i, v in enumerate([ba, bb, bc, n, n, n]):
+        ctx.set_kernel_arg(k, i, v)
+    ctx.enqueue_ndrange_kernel(queues[1], k, (n, n, 1), 2)
+    f = ctx.finish(queues[1])
+    assert f.compute_ms > 0 and f.transfer_ms > 0 and f.modeled_ms > 0
+    assert ctx.profiled_rate(1, "matmul") > 0
+    assert ctx.finish(queues[1]).compute_ms == 0.0  # drained
+    for x in (ba, bb, bc):
+        ctx.release(x)
+
+
+def test_kernel_launch_counter_advances(ctx, queues):
+    before = N.lib().hcl_kernel_launch_count()
+    run(ctx, "vecadd", [np.ones(64), np.ones(64), ("out", 64 * 8), 64], [2], queues[:1])
+    assert N.lib().hcl_kernel_launch_count() > before

@@ -1,0 +1,119 @@
+"""GPU parity of the tensor-core GEMM (configs C1/C2) against the fp64 oracle
+of the same rounded inputs, with the normwise tolerance of SURVEY.md §8(c):
+err_ij = |C - C64|_ij / (|A| |B|)_ij. Tolerances (stated here, per path):
+  bf16 inputs, fp32 out  : 2^-12   (fp32 tensor-core accumulation)
+  bf16 inputs, bf16 out  : 2^-8    (adds the bf16 output rounding, 2^-9 rel)
+  tf32 (fp32 inputs)     : 2^-10   (1xTF32 products)
+  fp32 SIMT              : 2^-16   (exact fp32 products, fp32 accumulation)
+plus bit-identity of C across partitions P in {1,2,4} (P-invariance)."""
+import os
+
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_2005_08466_b200 import HaoclError
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def queues(ctx):
+    qs = [ctx.create_queue(g) for g in ctx.get_device_ids()[:4]]
+    yield qs
+    for q in qs:
+        ctx.release(q)
+
+
+def gemm(ctx, queues, kernel, a, b, m, k, n, out_f32=True, P=1, weights=None):
+    prog = ctx.create_program("b200")
+    kh = ctx.create_kernel(prog, kernel)
+    es_out = 4 if out_f32 else 2
+    ba, bb, bc = ctx.create_buffer(a.nbytes), ctx.create_buffer(b.nbytes), ctx.create_buffer(m * n * es_out)
+    ctx.enqueue_write_buffer(queues[0], ba, a)
+    ctx.enqueue_write_buffer(queues[0], bb, b)
+    args = [ba, bb, bc, m, k, n] + ([int(out_f32)] if kernel == "gemm_bf16" else [])
+    for i, v in enumerate(args):
+        ctx.set_kernel_arg(kh, i, v)
+    if P == 1:
+        ctx.enqueue_ndrange_kernel(queues[0], kh, (m, n, 1), 2)
+    else:
+        ctx.enqueue_ndrange_partitioned(kh, (m, n, 1), 2, queues[:P], weights)
+    for q in queues[:P]:
+        ctx.finish(q)
+    raw = ctx.enqueue_read_buffer(queues[0], bc)
+    for x in (ba, bb, bc):
+        ctx.release(x)
+    ctx.release(kh)
+    ctx.release(prog)
+    if out_f32:
+        return raw.view(np.float32).reshape(m, n)
+    return O.bf16_to_f32(raw.view(np.uint16)).reshape(m, n)
+
+
+def normwise_err(c, a64, b64):
+    ref = a64 @ b64
+    scale = np.abs(a64) @ np.abs(b64)
+    return float((np.abs(c.astype(np.float64) - ref) / np.maximum(scale, 1e-300)).max())
+
+
+SHAPES = [(256, 256, 64), (512, 512, 512), (1024, 1024, 1024), (300, 200, 136), (128, 264, 1000), (777, 520, 72)]
+
+
+@pytest.mark.parametrize("m,n,k", SHAPES)
+@pytest.mark.parametrize("variant", ["cg2_mn", "cg1_mn", "cg2_kmajor", "cg1_kmajor"])
+def test_gemm_bf16_fp32out(ctx, queues, m, n, k, variant, monkeypatch):
+    monkeypatch.setenv("HCL_GEMM_CG", "2" if variant.startswith("cg2") else "1")
+    monkeypatch.setenv("HCL_GEMM_B_KMAJOR", "1" if variant.endswith("kmajor") else "0")
+    a = O.gen_bf16(m * k, 42)
+    b = O.gen_bf16(k * n, 43)
+    c = gemm(ctx, queues, "gemm_bf16", a, b, m, k, n, out_f32=True)
+    a64 = O.bf16_to_f32(a).astype(np.float64).reshape(m, k)
+    b64 = O.bf16_to_f32(b).astype(np.float64).reshape(k, n)
+    assert normwise_err(c, a64, b64) <= 2.0**-12
+
+
+@pytest.mark.parametrize("m,n,k", SHAPES[:4])
+def test_gemm_bf16_bf16out(ctx, queues, m, n, k):
+    a = O.gen_bf16(m * k, 42)
+    b = O.gen_bf16(k * n, 43)
+    c = gemm(ctx, queues, "gemm_bf16", a, b, m, k, n, out_f32=False)
+    a64 = O.bf16_to_f32(a).astype(np.float64).reshape(m, k)
+    b64 = O.bf16_to_f32(b).astype(np.float64).reshape(k, n)
+    assert normwise_err(c, a64, b64) <= 2.0**-8
+
+
+@pytest.mark.parametrize("P,weights", [(2, None), (4, None), (4, [3, 1, 2, 2])])
+def test_gemm_bf16_partition_invariance(ctx, queues, P, weights):
+    m, n, k = 1024, 768, 512
+    a = O.gen_bf16(m * k, 42)
+    b = O.gen_bf16(k * n, 43)
+    whole = gemm(ctx, queues, "gemm_bf16", a, b, m, k, n, out_f32=True)
+    part = gemm(ctx, queues, "gemm_bf16", a, b, m, k, n, out_f32=True, P=P, weights=weights)
+    assert whole.tobytes() == part.tobytes()
+
+
+@pytest.mark.parametrize("m,n,k", [(1024, 1024, 1024), (300, 200, 136)])
+def test_gemm_tf32(ctx, queues, m, n, k):
+    a = O.gen_doubles(m * k, 42).astype(np.float32)
+    b = O.gen_doubles(k * n, 43).astype(np.float32)
+    c = gemm(ctx, queues, "gemm_tf32", a, b, m, k, n)
+    assert normwise_err(c, a.astype(np.float64).reshape(m, k), b.astype(np.float64).reshape(k, n)) <= 2.0**-10
+
+
+@pytest.mark.parametrize("m,n,k", [(1024, 1024, 1024), (300, 200, 137)])
+def test_gemm_f32_simt(ctx, queues, m, n, k):
+    a = O.gen_doubles(m * k, 42).astype(np.float32)
+    b = O.gen_doubles(k * n, 43).astype(np.float32)
+    c = gemm(ctx, queues, "gemm_f32", a, b, m, k, n)
+    assert normwise_err(c, a.astype(np.float64).reshape(m, k), b.astype(np.float64).reshape(k, n)) <= 2.0**-16
+
+
+def test_gemm_argument_errors(ctx, queues):
+    a = O.gen_bf16(64 * 60, 1)
+    with pytest.raises(HaoclError) as e:  # K=60 -> 120-byte rows, not 16-byte aligned
+        gemm(ctx, queues, "gemm_bf16", a, O.gen_bf16(60 * 64, 2), 64, 60, 64)
+    assert e.value.name == "argument"
+    with pytest.raises(HaoclError) as e:  # B has the wrong size
+        gemm(ctx, queues, "gemm_bf16", O.gen_bf16(64 * 64, 1), O.gen_bf16(64 * 32, 2), 64, 64, 64)
+    assert e.value.name == "argument"
