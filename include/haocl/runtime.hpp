@@ -252,6 +252,12 @@ class HostContext {
   // Partitioned NDRange over several queues (one device each).
   Handle enqueue_ndrange_kernel(Handle kernel, std::array<uint64_t, 3> global_size, uint32_t dims,
                                 const std::vector<Handle>& queues, std::vector<uint64_t> weights = {});
+  // One sub-range [row_offset, row_offset+rows) of dim 0 of the global range on
+  // one queue (clEnqueueNDRangeKernel's global_work_offset): the unit a rank
+  // runs when the partitioned NDRange spans processes (one process per GPU).
+  // SPLIT_ROWS buffers need only that slice resident on the queue's device.
+  Handle enqueue_ndrange_range(Handle queue, Handle kernel, std::array<uint64_t, 3> global_size, uint32_t dims,
+                               uint64_t row_offset, uint64_t rows);
   // The split a partitioned launch of `kernel` would use (parts+1 row boundaries).
   std::vector<uint64_t> partition_plan(Handle kernel, std::array<uint64_t, 3> global_size,
                                        const std::vector<Handle>& queues, std::vector<uint64_t> weights = {});

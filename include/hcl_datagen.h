@@ -1,0 +1,35 @@
+/*
+ * hcl_datagen.h — synthetic input generators of the product (host side,
+ * multithreaded). Replace haocl::gen_doubles / SplitMix64
+ * (proj/include/haocl/datagen.hpp:13-62, proj/src/datagen.cpp:11-16) and add
+ * the restated generators of the B200 configs. Every generator is counter
+ * based: element i of a stream depends only on (seed, i), so `first` selects
+ * any sub-range (one rank's row block) bit-identically. threads <= 0: all cores.
+ */
+#ifndef HCL_DATAGEN_H
+#define HCL_DATAGEN_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+uint64_t hcl_gen_splitmix_at(uint64_t seed, uint64_t index);
+/* U[-1,1) doubles: element i = gen_doubles(seed)[first + i] (datagen.cpp:11-16) */
+void hcl_gen_doubles(double* out, uint64_t first, uint64_t count, uint64_t seed, int threads);
+/* the same values rounded to fp32 (RN) */
+void hcl_gen_f32(float* out, uint64_t first, uint64_t count, uint64_t seed, int threads);
+/* the same values rounded double -> fp32 -> bf16 (RN-even), bf16 bit patterns */
+void hcl_gen_bf16(uint16_t* out, uint64_t first, uint64_t count, uint64_t seed, int threads);
+/* R-MAT (.57,.19,.19,.05) edges [first_edge, first_edge+count) of a 2^scale graph */
+void hcl_gen_rmat_edges(int scale, uint64_t first_edge, uint64_t count, uint64_t seed, uint32_t* src, uint32_t* dst,
+                        int threads);
+/* k-means points [first, first+count) x d, multiples of 2^-12 in [-8, 8) */
+void hcl_gen_kmeans_points(uint64_t seed, uint64_t first, uint64_t count, int64_t d, int64_t blobs, float* out,
+                           int threads);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -54,6 +54,10 @@ int hcl_ctx_enqueue_ndrange_kernel(hcl_context* ctx, uint64_t queue, uint64_t ke
 int hcl_ctx_enqueue_ndrange_partitioned(hcl_context* ctx, uint64_t kernel, const uint64_t global[3], uint32_t dims,
                                         const uint64_t* queues, int nqueues, const uint64_t* weights,
                                         uint64_t* event);
+/* One sub-range [row_offset, row_offset+rows) of dim 0 on one queue (the part a
+ * rank runs when the partitioned NDRange spans processes; OpenCL's global_work_offset). */
+int hcl_ctx_enqueue_ndrange_range(hcl_context* ctx, uint64_t queue, uint64_t kernel, const uint64_t global[3],
+                                  uint32_t dims, uint64_t row_offset, uint64_t rows, uint64_t* event);
 /* The row boundaries (nqueues+1) the partitioned launch would use. */
 int hcl_ctx_partition_plan(hcl_context* ctx, uint64_t kernel, const uint64_t global[3], const uint64_t* queues,
                            int nqueues, const uint64_t* weights, uint64_t* bounds);

@@ -75,6 +75,8 @@ HOST = [
     ("hcl_ctx_enqueue_ndrange_kernel", C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, u64p, C.c_uint32, u64p]),
     ("hcl_ctx_enqueue_ndrange_partitioned", C.c_int, [C.c_void_p, C.c_uint64, u64p, C.c_uint32, u64p, C.c_int,
                                                       u64p, u64p]),
+    ("hcl_ctx_enqueue_ndrange_range", C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, u64p, C.c_uint32,
+                                                C.c_uint64, C.c_uint64, u64p]),
     ("hcl_ctx_partition_plan", C.c_int, [C.c_void_p, C.c_uint64, u64p, u64p, C.c_int, u64p, u64p]),
     ("hcl_ctx_submit_task", C.c_int, [C.c_void_p, C.c_char_p, u8p, i64p, C.c_int, C.c_char_p, C.c_int, i32p,
                                       u64p]),
@@ -108,7 +110,17 @@ HOST = [
     ("hcl_sched_partition_weights", C.c_int, [C.c_void_p, C.c_char_p, i32p, C.c_int, u64p]),
 ]
 
-EXTRA = []  # appended by workload modules (datagen, etc.)
+DATAGEN = [
+    ("hcl_gen_splitmix_at", C.c_uint64, [C.c_uint64, C.c_uint64]),
+    ("hcl_gen_doubles", None, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint64, C.c_int]),
+    ("hcl_gen_f32", None, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint64, C.c_int]),
+    ("hcl_gen_bf16", None, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint64, C.c_int]),
+    ("hcl_gen_rmat_edges", None, [C.c_int, C.c_uint64, C.c_uint64, C.c_uint64, C.c_void_p, C.c_void_p, C.c_int]),
+    ("hcl_gen_kmeans_points", None, [C.c_uint64, C.c_uint64, C.c_uint64, C.c_int64, C.c_int64, C.c_void_p,
+                                     C.c_int]),
+]
+
+EXTRA = []  # appended by workload modules
 
 _lib = None
 
@@ -129,7 +141,7 @@ def lib():
             raise RuntimeError(f"{LIB_PATH} is missing: run __graft_entry__.build() "
                                "(the B200 path has no CPU fallback)")
         L = C.CDLL(LIB_PATH)
-        for name, res, args in CABI + HOST + EXTRA:
+        for name, res, args in CABI + HOST + DATAGEN + EXTRA:
             fn = getattr(L, name)
             fn.restype = res
             fn.argtypes = args
@@ -145,4 +157,4 @@ def check(rc: int) -> None:
 
 
 def declared_symbols():
-    return [n for n, _, _ in CABI + HOST]
+    return [n for n, _, _ in CABI + HOST + DATAGEN]

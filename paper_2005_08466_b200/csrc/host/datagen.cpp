@@ -1,0 +1,117 @@
+// Product-side synthetic data generation: the
+// reference's SplitMix64 streams (proj/include/haocl/datagen.hpp:13-31,
+// proj/src/datagen.cpp:11-16) plus the restated generators of the B200
+// configs. SplitMix64 is counter based — output i of the stream seeded with s
+// is mix(s + (i+1)*gamma) — so any sub-range (one rank's row block) is
+// generated independently and in parallel, bit-identical to the serial stream.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <thread>
+#include <vector>
+
+#include "hcl_datagen.h"
+
+namespace {
+
+constexpr uint64_t kGamma = 0x9e3779b97f4a7c15ULL;
+
+inline uint64_t mix(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+inline uint64_t at(uint64_t seed, uint64_t i) { return mix(seed + (i + 1) * kGamma); }
+inline double unit_sym(uint64_t r) { return static_cast<double>(r >> 11) * 0x1.0p-53 * 2.0 - 1.0; }
+
+inline uint16_t bf16_rne(float f) {
+  uint32_t u;
+  std::memcpy(&u, &f, 4);
+  if ((u & 0x7f800000u) == 0x7f800000u) return static_cast<uint16_t>((u >> 16) | ((u & 0xffff) ? 0x40 : 0));
+  u += 0x7fffu + ((u >> 16) & 1u);
+  return static_cast<uint16_t>(u >> 16);
+}
+
+template <typename F>
+void parallel_for(uint64_t n, int threads, F&& f) {
+  if (threads <= 0) threads = static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
+  if (n < (1u << 16) || threads == 1) {
+    f(0, n);
+    return;
+  }
+  std::vector<std::thread> ts;
+  uint64_t chunk = (n + threads - 1) / threads;
+  for (int t = 0; t < threads; ++t) {
+    uint64_t lo = t * chunk, hi = std::min(n, lo + chunk);
+    if (lo >= hi) break;
+    ts.emplace_back([&, lo, hi] { f(lo, hi); });
+  }
+  for (auto& t : ts) t.join();
+}
+
+// R-MAT quadrant thresholds (a, b, c) = (.57, .19, .19) as 32-bit integers.
+constexpr uint32_t kT1 = 2448131358u, kT2 = 3264175144u, kT3 = 4080218930u;
+
+}  // namespace
+
+extern "C" {
+
+uint64_t hcl_gen_splitmix_at(uint64_t seed, uint64_t index) { return at(seed, index); }
+
+void hcl_gen_doubles(double* out, uint64_t first, uint64_t count, uint64_t seed, int threads) {
+  parallel_for(count, threads, [&](uint64_t lo, uint64_t hi) {
+    for (uint64_t i = lo; i < hi; ++i) out[i] = unit_sym(at(seed, first + i));
+  });
+}
+
+void hcl_gen_f32(float* out, uint64_t first, uint64_t count, uint64_t seed, int threads) {
+  parallel_for(count, threads, [&](uint64_t lo, uint64_t hi) {
+    for (uint64_t i = lo; i < hi; ++i) out[i] = static_cast<float>(unit_sym(at(seed, first + i)));
+  });
+}
+
+void hcl_gen_bf16(uint16_t* out, uint64_t first, uint64_t count, uint64_t seed, int threads) {
+  parallel_for(count, threads, [&](uint64_t lo, uint64_t hi) {
+    for (uint64_t i = lo; i < hi; ++i) out[i] = bf16_rne(static_cast<float>(unit_sym(at(seed, first + i))));
+  });
+}
+
+void hcl_gen_rmat_edges(int scale, uint64_t first_edge, uint64_t count, uint64_t seed, uint32_t* src,
+                        uint32_t* dst, int threads) {
+  parallel_for(count, threads, [&](uint64_t lo, uint64_t hi) {
+    for (uint64_t i = lo; i < hi; ++i) {
+      uint64_t e = first_edge + i;
+      uint32_t s = 0, d = 0;
+      for (int l = 0; l < scale; ++l) {
+        uint32_t u = static_cast<uint32_t>(at(seed, e * static_cast<uint64_t>(scale) + l) >> 32);
+        uint32_t bs = u >= kT2;
+        uint32_t bd = (u >= kT1 && u < kT2) || u >= kT3;
+        s = (s << 1) | bs;
+        d = (d << 1) | bd;
+      }
+      src[i] = s;
+      dst[i] = d;
+    }
+  });
+}
+
+void hcl_gen_kmeans_points(uint64_t seed, uint64_t first, uint64_t count, int64_t d, int64_t blobs, float* out,
+                           int threads) {
+  parallel_for(count, threads, [&](uint64_t lo, uint64_t hi) {
+    for (uint64_t ii = lo; ii < hi; ++ii) {
+      uint64_t i = first + ii;
+      uint64_t b = at(seed ^ 0xB10BULL, i) % static_cast<uint64_t>(blobs);
+      for (int64_t j = 0; j < d; ++j) {
+        int64_t c = static_cast<int64_t>(at(seed ^ 0xCE47E2ULL, b * d + j) >> 49) - 16384;
+        uint64_t r = at(seed, i * d + j);
+        int64_t nsum = static_cast<int64_t>(r & 0xffff) + static_cast<int64_t>((r >> 16) & 0xffff) +
+                       static_cast<int64_t>((r >> 32) & 0xffff) + static_cast<int64_t>(r >> 48) - 131070;
+        int64_t q = c + (nsum >> 5);
+        q = q < -32768 ? -32768 : (q > 32767 ? 32767 : q);
+        out[ii * d + j] = static_cast<float>(q) * 0x1p-12f;
+      }
+    }
+  });
+}
+
+}  // extern "C"

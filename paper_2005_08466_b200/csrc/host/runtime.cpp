@@ -526,6 +526,11 @@ Handle HostContext::enqueue_write_buffer(Handle queue, Handle buffer, std::span<
     fail(ErrorCode::size, "write of " + std::to_string(data.size()) + " bytes at offset " + std::to_string(offset) +
                               " into a " + std::to_string(b.size) + "-byte buffer");
   auto started = Clock::now();
+  // A device whose valid bytes straddle the written range on both sides would
+  // lose one side when trimmed: pull its interval here first.
+  for (auto& [g, o] : b.pieces)
+    if (g != q.gid && o.valid_bytes && o.valid_first < offset && o.valid_first + o.valid_bytes > offset + data.size())
+      impl_->ensure_valid(buffer.id, b, q.gid, o.valid_first, o.valid_bytes, &q);
   Impl::Piece& p = impl_->ensure_alloc(buffer.id, b, q.gid, offset, data.size());
   if (!data.empty()) {
     impl_->trace.record({q.gid, "write_buffer", buffer.id});
@@ -625,6 +630,18 @@ Handle HostContext::enqueue_ndrange_kernel(Handle kernel, std::array<uint64_t, 3
   for (size_t i = 0; i < queues.size(); ++i)
     parts.push_back({impl_->queue(queues[i].id).gid, queues[i].id, bounds[i], bounds[i + 1]});
   return impl_->launch_parts(k, args, global_size, dims, parts, false);
+}
+
+Handle HostContext::enqueue_ndrange_range(Handle queue, Handle kernel, std::array<uint64_t, 3> global_size,
+                                          uint32_t dims, uint64_t row_offset, uint64_t rows) {
+  std::lock_guard lock(impl_->mu);
+  Impl::QueueRec& q = impl_->queue(queue.id);
+  for (uint32_t d = 0; d < dims && d < 3; ++d)
+    if (global_size[d] < 1) fail(ErrorCode::argument, "global_size extents must be >= 1");
+  if (row_offset + rows > global_size[0]) fail(ErrorCode::argument, "sub-range exceeds the global range");
+  std::vector<Arg> args;
+  Impl::KernelRec& k = impl_->bound_kernel(kernel.id, args);
+  return impl_->launch_parts(k, args, global_size, dims, {{q.gid, queue.id, row_offset, row_offset + rows}}, false);
 }
 
 std::pair<int, Handle> HostContext::submit_task(const KernelTask& task) {
@@ -880,6 +897,14 @@ int hcl_ctx_enqueue_ndrange_partitioned(hcl_context* ctx, uint64_t kernel, const
     if (weights) w.assign(weights, weights + nqueues);
     auto ev = ctx->ctx.enqueue_ndrange_kernel(H(HandleKind::kernel, kernel), {global[0], global[1], global[2]}, dims,
                                               qs, w);
+    if (event) *event = ev.id;
+  });
+}
+int hcl_ctx_enqueue_ndrange_range(hcl_context* ctx, uint64_t queue, uint64_t kernel, const uint64_t global[3],
+                                  uint32_t dims, uint64_t row_offset, uint64_t rows, uint64_t* event) {
+  return ctx_guarded([&] {
+    auto ev = ctx->ctx.enqueue_ndrange_range(H(HandleKind::queue, queue), H(HandleKind::kernel, kernel),
+                                             {global[0], global[1], global[2]}, dims, row_offset, rows);
     if (event) *event = ev.id;
   });
 }

@@ -364,7 +364,9 @@ uint64_t launch_gemm_tc(LaunchCtx& c) {
   void* cp = at_byte<uint8_t>(Cb, lo * n * os, rows * n * os, "gemm C");
   if (rows == 0) return 0;
   const int cg = env_int("HCL_GEMM_CG", 2);
-  const bool kmajor = env_int("HCL_GEMM_B_KMAJOR", 0) != 0;
+  // tf32 B goes K-major: an MN-major 32-bit operand needs the 128B_BASE32B
+  // swizzle atom, which this kernel does not stage (measured: zeros)
+  const bool kmajor = TF32 || env_int("HCL_GEMM_B_KMAJOR", 0) != 0;
   const void* b = B.ptr;
   if (kmajor) {  // debug/validation variant: transpose B to N x K first
     void* bt = c.scratch(c.dev, static_cast<size_t>(k * n * es));

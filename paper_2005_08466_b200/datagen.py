@@ -1,0 +1,51 @@
+"""Synthetic inputs (include/hcl_datagen.h): the reference's SplitMix64
+streams, counter based so any row block of any rank is generated directly,
+multithreaded on the host. `out` may be a numpy array or a (pinned) torch CPU
+tensor of the right dtype and size."""
+from __future__ import annotations
+
+import numpy as np
+
+from . import _native as N
+
+
+def _ptr(out):
+    if isinstance(out, np.ndarray):
+        return out.ctypes.data
+    return int(out.data_ptr())
+
+
+def splitmix_at(seed: int, index: int) -> int:
+    return int(N.lib().hcl_gen_splitmix_at(seed, index))
+
+
+def gen_doubles(count: int, seed: int, first: int = 0, out=None, threads: int = 0):
+    out = np.empty(count, np.float64) if out is None else out
+    N.lib().hcl_gen_doubles(_ptr(out), first, count, seed, threads)
+    return out
+
+
+def gen_f32(count: int, seed: int, first: int = 0, out=None, threads: int = 0):
+    out = np.empty(count, np.float32) if out is None else out
+    N.lib().hcl_gen_f32(_ptr(out), first, count, seed, threads)
+    return out
+
+
+def gen_bf16(count: int, seed: int, first: int = 0, out=None, threads: int = 0):
+    """bf16 bit patterns (uint16) of gen_doubles rounded double->f32->bf16."""
+    out = np.empty(count, np.uint16) if out is None else out
+    N.lib().hcl_gen_bf16(_ptr(out), first, count, seed, threads)
+    return out
+
+
+def gen_rmat_edges(scale: int, count: int, seed: int, first: int = 0, threads: int = 0):
+    src = np.empty(count, np.uint32)
+    dst = np.empty(count, np.uint32)
+    N.lib().hcl_gen_rmat_edges(scale, first, count, seed, src.ctypes.data, dst.ctypes.data, threads)
+    return src, dst
+
+
+def gen_kmeans_points(count: int, d: int, blobs: int, seed: int, first: int = 0, out=None, threads: int = 0):
+    out = np.empty(count * d, np.float32) if out is None else out
+    N.lib().hcl_gen_kmeans_points(seed, first, count, d, blobs, _ptr(out), threads)
+    return out

@@ -186,6 +186,15 @@ class HostContext:
                                                           C.byref(ev)))
         return Handle(HandleKind.event, ev.value)
 
+    def enqueue_ndrange_range(self, queue: Handle, kernel: Handle, global_size, dims: int, row_offset: int,
+                              rows: int) -> Handle:
+        """Rows [row_offset, row_offset+rows) of dim 0 on one queue (a rank's part)."""
+        g = (C.c_uint64 * 3)(*global_size)
+        ev = C.c_uint64()
+        check(self._L.hcl_ctx_enqueue_ndrange_range(self._ctx, queue.id, kernel.id, g, dims, row_offset, rows,
+                                                    C.byref(ev)))
+        return Handle(HandleKind.event, ev.value)
+
     def partition_plan(self, kernel: Handle, global_size, queues: Sequence[Handle],
                        weights: Optional[Sequence[int]] = None) -> list[int]:
         g = (C.c_uint64 * 3)(*global_size)

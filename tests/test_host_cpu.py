@@ -17,7 +17,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def header_symbols():
     syms = set()
-    for h in ("hcl_cabi.h", "hcl_host.h"):
+    for h in ("hcl_cabi.h", "hcl_host.h", "hcl_datagen.h"):
         text = open(os.path.join(ROOT, "include", h)).read()
         syms |= set(re.findall(r"^\s*(?:const\s+)?[a-z_0-9]+\s*\*?\s*(hcl_[a-z_0-9]+)\s*\(", text, re.M))
     return syms
@@ -189,3 +189,17 @@ def test_partition_weights_follow_measured_rates():
     assert w[0] == 1 << 20 and abs(w[1] / w[0] - 1 / 3) < 1e-5 and abs(w[2] / w[0] - 2 / 3) < 1e-5
     b = split_ranges(16384, w)
     assert b[1] - b[0] == pytest.approx(16384 / 2, abs=1)
+
+
+def test_product_datagen_matches_oracle_streams():
+    from paper_2005_08466_b200 import datagen as G
+
+    assert (G.gen_doubles(10**5, 42) == O.gen_doubles(10**5, 42)).all()
+    full = O.gen_doubles(300000, 43)
+    assert (G.gen_doubles(1000, 43, first=123456) == full[123456:124456]).all()  # any sub-range
+    assert (G.gen_bf16(300000, 42) == O.gen_bf16(300000, 42)).all()
+    assert (G.gen_f32(1000, 9) == O.gen_doubles(1000, 9).astype(np.float32)).all()
+    s, d = G.gen_rmat_edges(12, 70000, 42, first=5)
+    s2, d2 = O.rmat_edges(12, 5, 70000, 42)
+    assert (s == s2).all() and (d == d2).all()
+    assert (G.gen_kmeans_points(70000, 8, 16, 42, first=3) == O.kmeans_points(42, 3, 70000, 8, 16)).all()
