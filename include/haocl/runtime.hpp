@@ -251,7 +251,8 @@ class HostContext {
                                 uint32_t dims = 1);
   // Partitioned NDRange over several queues (one device each).
   Handle enqueue_ndrange_kernel(Handle kernel, std::array<uint64_t, 3> global_size, uint32_t dims,
-                                const std::vector<Handle>& queues, std::vector<uint64_t> weights = {});
+                                const std::vector<Handle>& queues, std::vector<uint64_t> weights = {},
+                                std::vector<uint64_t> bounds = {});  // explicit row boundaries (parts+1), e.g. nnz-balanced
   // One sub-range [row_offset, row_offset+rows) of dim 0 of the global range on
   // one queue (clEnqueueNDRangeKernel's global_work_offset): the unit a rank
   // runs when the partitioned NDRange spans processes (one process per GPU).

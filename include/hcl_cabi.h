@@ -59,7 +59,9 @@ enum hcl_arg_kind { HCL_ARG_SCALAR = 0, HCL_ARG_IN = 1, HCL_ARG_OUT = 2, HCL_ARG
 enum hcl_part_class {
   HCL_PART_NONE = 0,      /* scalar */
   HCL_PART_REPLICATE = 1, /* whole buffer on every device (GEMM B, PageRank x) */
-  HCL_PART_SPLIT_ROWS = 2 /* row slice [lo,hi) of dim 0 on each device (GEMM A, C) */
+  HCL_PART_SPLIT_ROWS = 2, /* row slice [lo,hi) of dim 0 on each device (GEMM A, C) */
+  HCL_PART_REDUCE_SUM = 3  /* each part produces a full-size int64 partial; the
+                              runtime sums them (k-means centroid sums) */
 };
 
 /* One bound kernel argument, BoundArg (proj/include/haocl/kernels.hpp:44-50). */

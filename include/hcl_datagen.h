@@ -29,6 +29,15 @@ void hcl_gen_rmat_edges(int scale, uint64_t first_edge, uint64_t count, uint64_t
 void hcl_gen_kmeans_points(uint64_t seed, uint64_t first, uint64_t count, int64_t d, int64_t blobs, float* out,
                            int threads);
 
+/* Pull CSR (rows = dst, cols = src ascending, val = 1/outdeg(src)) of the R-MAT
+ * graph with 2^scale vertices and `edges` edges; int32 indices, fp32 values.
+ * row_ptr: 2^scale+1, col_idx/val: edges, outdeg: 2^scale. Returns 0. */
+int hcl_pagerank_csr(int scale, uint64_t edges, uint64_t seed, int32_t* row_ptr, int32_t* col_idx, float* val,
+                     int32_t* outdeg, int threads);
+/* CSR-adaptive row blocks (<= max_nnz per multi-row block); out may be NULL to
+ * count. Returns the number of blocks; out[0..n] are block start rows. */
+int64_t hcl_csr_row_blocks(const int32_t* row_ptr, int64_t rows, int64_t max_nnz, int32_t* out);
+
 #ifdef __cplusplus
 }
 #endif

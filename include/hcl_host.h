@@ -50,10 +50,11 @@ int hcl_ctx_enqueue_read_buffer(hcl_context* ctx, uint64_t queue, uint64_t buffe
 /* enqueue_ndrange_kernel (proj/src/runtime.cpp:516-540). */
 int hcl_ctx_enqueue_ndrange_kernel(hcl_context* ctx, uint64_t queue, uint64_t kernel, const uint64_t global[3],
                                    uint32_t dims, uint64_t* event);
-/* Partitioned NDRange over nqueues queues; weights NULL = scheduler weights. */
+/* Partitioned NDRange over nqueues queues; weights NULL = scheduler weights;
+ * bounds (nqueues+1 row boundaries, e.g. nnz-balanced) NULL = computed split. */
 int hcl_ctx_enqueue_ndrange_partitioned(hcl_context* ctx, uint64_t kernel, const uint64_t global[3], uint32_t dims,
                                         const uint64_t* queues, int nqueues, const uint64_t* weights,
-                                        uint64_t* event);
+                                        const uint64_t* bounds, uint64_t* event);
 /* One sub-range [row_offset, row_offset+rows) of dim 0 on one queue (the part a
  * rank runs when the partitioned NDRange spans processes; OpenCL's global_work_offset). */
 int hcl_ctx_enqueue_ndrange_range(hcl_context* ctx, uint64_t queue, uint64_t kernel, const uint64_t global[3],

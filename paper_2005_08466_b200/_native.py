@@ -74,7 +74,7 @@ HOST = [
                                               C.c_uint64]),
     ("hcl_ctx_enqueue_ndrange_kernel", C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, u64p, C.c_uint32, u64p]),
     ("hcl_ctx_enqueue_ndrange_partitioned", C.c_int, [C.c_void_p, C.c_uint64, u64p, C.c_uint32, u64p, C.c_int,
-                                                      u64p, u64p]),
+                                                      u64p, u64p, u64p]),
     ("hcl_ctx_enqueue_ndrange_range", C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, u64p, C.c_uint32,
                                                 C.c_uint64, C.c_uint64, u64p]),
     ("hcl_ctx_partition_plan", C.c_int, [C.c_void_p, C.c_uint64, u64p, u64p, C.c_int, u64p, u64p]),
@@ -118,6 +118,9 @@ DATAGEN = [
     ("hcl_gen_rmat_edges", None, [C.c_int, C.c_uint64, C.c_uint64, C.c_uint64, C.c_void_p, C.c_void_p, C.c_int]),
     ("hcl_gen_kmeans_points", None, [C.c_uint64, C.c_uint64, C.c_uint64, C.c_int64, C.c_int64, C.c_void_p,
                                      C.c_int]),
+    ("hcl_pagerank_csr", C.c_int, [C.c_int, C.c_uint64, C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                   C.c_int]),
+    ("hcl_csr_row_blocks", C.c_int64, [C.c_void_p, C.c_int64, C.c_int64, C.c_void_p]),
 ]
 
 EXTRA = []  # appended by workload modules

@@ -5,6 +5,7 @@
 // is mix(s + (i+1)*gamma) — so any sub-range (one rank's row block) is
 // generated independently and in parallel, bit-identical to the serial stream.
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstring>
 #include <thread>
@@ -112,6 +113,102 @@ void hcl_gen_kmeans_points(uint64_t seed, uint64_t first, uint64_t count, int64_
       }
     }
   });
+}
+
+// Pull CSR of the R-MAT graph by destination (rows = dst, columns = src
+// ascending, multi-edges kept, val = 1/outdeg(src) in fp32): identical to the
+// oracle's serial counting sorts (oracle/haocl_oracle.c ho_pagerank_csr). Built
+// with a parallel LSD radix sort of 48-bit (dst, src) keys.
+int hcl_pagerank_csr(int scale, uint64_t edges, uint64_t seed, int32_t* row_ptr, int32_t* col_idx, float* val,
+                     int32_t* outdeg, int threads) {
+  if (scale < 1 || scale > 30 || edges >= (1ull << 31)) return 1009;
+  if (threads <= 0) threads = static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
+  const uint64_t v = 1ull << scale;
+  std::vector<uint64_t> keys(edges), tmp(edges);
+  {
+    std::vector<uint32_t> s(edges), d(edges);
+    hcl_gen_rmat_edges(scale, 0, edges, seed, s.data(), d.data(), threads);
+    std::vector<std::atomic<int32_t>> deg(v);
+    parallel_for(v, threads, [&](uint64_t lo, uint64_t hi) {
+      for (uint64_t i = lo; i < hi; ++i) deg[i].store(0, std::memory_order_relaxed);
+    });
+    parallel_for(edges, threads, [&](uint64_t lo, uint64_t hi) {
+      for (uint64_t i = lo; i < hi; ++i) {
+        keys[i] = (static_cast<uint64_t>(d[i]) << 32) | s[i];
+        deg[s[i]].fetch_add(1, std::memory_order_relaxed);
+      }
+    });
+    parallel_for(v, threads, [&](uint64_t lo, uint64_t hi) {
+      for (uint64_t i = lo; i < hi; ++i) outdeg[i] = deg[i].load(std::memory_order_relaxed);
+    });
+  }
+  // LSD radix sort on src (bits 0..scale) then dst (bits 32..32+scale), 16-bit digits
+  std::vector<int> shifts;
+  for (int b = 0; b < scale; b += 16) shifts.push_back(b);
+  for (int b = 0; b < scale; b += 16) shifts.push_back(32 + b);
+  const int T = threads;
+  const uint64_t chunk = (edges + T - 1) / T;
+  std::vector<uint64_t> hist(static_cast<size_t>(T) * 65536);
+  for (int sh : shifts) {
+    std::fill(hist.begin(), hist.end(), 0);
+    std::vector<std::thread> ts;
+    for (int t = 0; t < T; ++t)
+      ts.emplace_back([&, t] {
+        uint64_t lo = t * chunk, hi = std::min(edges, lo + chunk);
+        uint64_t* h = &hist[static_cast<size_t>(t) * 65536];
+        for (uint64_t i = lo; i < hi; ++i) h[(keys[i] >> sh) & 0xffff]++;
+      });
+    for (auto& x : ts) x.join();
+    ts.clear();
+    uint64_t run = 0;  // digit-major, thread-minor exclusive scan -> stable
+    for (int dg = 0; dg < 65536; ++dg)
+      for (int t = 0; t < T; ++t) {
+        uint64_t c = hist[static_cast<size_t>(t) * 65536 + dg];
+        hist[static_cast<size_t>(t) * 65536 + dg] = run;
+        run += c;
+      }
+    for (int t = 0; t < T; ++t)
+      ts.emplace_back([&, t] {
+        uint64_t lo = t * chunk, hi = std::min(edges, lo + chunk);
+        uint64_t* h = &hist[static_cast<size_t>(t) * 65536];
+        for (uint64_t i = lo; i < hi; ++i) tmp[h[(keys[i] >> sh) & 0xffff]++] = keys[i];
+      });
+    for (auto& x : ts) x.join();
+    keys.swap(tmp);
+  }
+  // row_ptr by dst
+  std::vector<int64_t> cnt(v + 1, 0);
+  for (uint64_t i = 0; i < edges; ++i) cnt[(keys[i] >> 32) + 1]++;
+  for (uint64_t i = 0; i < v; ++i) cnt[i + 1] += cnt[i];
+  for (uint64_t i = 0; i <= v; ++i) row_ptr[i] = static_cast<int32_t>(cnt[i]);
+  parallel_for(edges, threads, [&](uint64_t lo, uint64_t hi) {
+    for (uint64_t i = lo; i < hi; ++i) {
+      uint32_t src = static_cast<uint32_t>(keys[i] & 0xffffffffu);
+      col_idx[i] = static_cast<int32_t>(src);
+      val[i] = 1.0f / static_cast<float>(outdeg[src]);
+    }
+  });
+  return 0;
+}
+
+// Row blocks of a CSR for the PageRank SpMV (CSR-adaptive): consecutive rows
+// grouped while their nnz total stays <= max_nnz; a row longer than max_nnz
+// is a block by itself. out[0..count] are block start rows (out[count] = rows).
+// Depends only on row_ptr, so a partitioned launch gives P-invariant results.
+int64_t hcl_csr_row_blocks(const int32_t* row_ptr, int64_t rows, int64_t max_nnz, int32_t* out) {
+  int64_t n = 0;
+  int64_t r = 0;
+  while (r < rows) {
+    if (out) out[n] = static_cast<int32_t>(r);
+    ++n;
+    int64_t start = row_ptr[r];
+    int64_t e = r + 1;
+    if (row_ptr[e] - start <= max_nnz)
+      while (e < rows && row_ptr[e + 1] - start <= max_nnz) ++e;
+    r = e;
+  }
+  if (out) out[n] = static_cast<int32_t>(rows);
+  return n;
 }
 
 }  // extern "C"

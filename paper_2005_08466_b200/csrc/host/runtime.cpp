@@ -306,24 +306,33 @@ struct HostContext::Impl {
             (k.kinds[i] == HCL_ARG_OUT || k.kinds[i] == HCL_ARG_INOUT) && parts.size() > 1)
           fail(ErrorCode::argument, k.name + ": a replicated output cannot be partitioned");
 
-    std::vector<hcl_arg> cargs(n);
+    auto slice = [&](uint32_t i, const Part& part, uint64_t& first, uint64_t& len) {
+      bool split = !whole && k.classes[i] == HCL_PART_SPLIT_ROWS;
+      first = split ? part.lo * row_bytes[i] : 0;
+      len = split ? (part.hi - part.lo) * row_bytes[i] : buffer(args[i].buffer).size;
+    };
+    // 1. stage every part (inputs made valid, outputs allocated) before any launch
     for (const Part& part : parts) {
       if (!whole && part.hi == part.lo) continue;
       QueueRec& q = queue(part.queue);
-      auto staging = Clock::now();
       for (uint32_t i = 0; i < n; ++i) {
-        cargs[i] = hcl_arg{static_cast<uint32_t>(k.kinds[i]), 0, args[i].scalar, args[i].buffer};
         if (!args[i].is_buffer) continue;
         BufferRec& b = buffer(args[i].buffer);
-        bool split = !whole && k.classes[i] == HCL_PART_SPLIT_ROWS;
-        uint64_t first = split ? part.lo * row_bytes[i] : 0;
-        uint64_t len = split ? (part.hi - part.lo) * row_bytes[i] : b.size;
+        uint64_t first, len;
+        slice(i, part, first, len);
         if (k.kinds[i] == HCL_ARG_OUT)
           ensure_alloc(args[i].buffer, b, part.gid, first, len);
         else
           ensure_valid(args[i].buffer, b, part.gid, first, len, &q);
       }
-      add_transfer(&q, 0.0 * ms_since(staging));
+    }
+    // 2. launch every part asynchronously on its device stream
+    std::vector<hcl_arg> cargs(n);
+    for (uint32_t i = 0; i < n; ++i)
+      cargs[i] = hcl_arg{static_cast<uint32_t>(k.kinds[i]), 0, args[i].scalar, args[i].buffer};
+    for (const Part& part : parts) {
+      if (!whole && part.hi == part.lo) continue;
+      QueueRec& q = queue(part.queue);
       scheduler.note_dispatch(part.gid);
       Launch l;
       l.kernel = k.name;
@@ -346,22 +355,72 @@ struct HostContext::Impl {
         check(rc);
       }
       q.pending.push_back(l);
-      // outputs: valid where computed
-      for (uint32_t i = 0; i < n; ++i) {
-        if (!args[i].is_buffer || k.kinds[i] == HCL_ARG_IN) continue;
-        BufferRec& b = buffer(args[i].buffer);
-        bool split = !whole && k.classes[i] == HCL_PART_SPLIT_ROWS;
-        uint64_t first = split ? part.lo * row_bytes[i] : 0;
-        uint64_t len = split ? (part.hi - part.lo) * row_bytes[i] : b.size;
+    }
+    // 3. outputs: the launch produced the bytes U = union of the part slices
+    //    (one interval); older copies of U anywhere are stale, bytes outside U
+    //    keep their validity
+    for (uint32_t i = 0; i < n; ++i) {
+      if (!args[i].is_buffer || k.kinds[i] == HCL_ARG_IN) continue;
+      BufferRec& b = buffer(args[i].buffer);
+      if (!whole && k.classes[i] == HCL_PART_REDUCE_SUM) {
+        // sum the parts' int64 partials onto the first part's device
+        std::vector<int> gids;
+        for (const Part& part : parts)
+          if (part.hi > part.lo) gids.push_back(part.gid);
+        if (gids.empty()) continue;
+        for (size_t a = 0; a < gids.size(); ++a)
+          for (size_t c = a + 1; c < gids.size(); ++c)
+            if (gids[a] == gids[c])
+              fail(ErrorCode::argument, k.name + ": a REDUCE_SUM output needs one device per part");
+        const int g0 = gids[0], d0 = dev_index(g0);
+        const uint64_t id = args[i].buffer;
+        for (size_t a = 1; a < gids.size(); ++a) {
+          uint64_t tmp = new_id();
+          check(hcl_buffer_alloc(d0, tmp, 0, b.size));
+          check(hcl_buffer_copy_peer(d0, tmp, 0, dev_index(gids[a]), id, 0, b.size));
+          trace.record({g0, "copy_peer", id});
+          hcl_arg ra[3] = {{HCL_ARG_INOUT, 0, 0, id}, {HCL_ARG_IN, 0, 0, tmp},
+                           {HCL_ARG_SCALAR, 0, static_cast<int64_t>(b.size / 8), 0}};
+          check(hcl_launch(d0, "reduce_add_i64", ra, 3, nullptr, nullptr, 1, nullptr));
+          check(hcl_buffer_release(d0, tmp));
+        }
+        for (auto& [g, p] : b.pieces) p.valid_bytes = 0;
+        b.pieces[g0].valid_first = 0;
+        b.pieces[g0].valid_bytes = b.size;
+        continue;
+      }
+      uint64_t u0 = UINT64_MAX, u1 = 0;
+      for (const Part& part : parts) {
+        if (!whole && part.hi == part.lo) continue;
+        uint64_t first, len;
+        slice(i, part, first, len);
+        u0 = std::min(u0, first);
+        u1 = std::max(u1, first + len);
+      }
+      if (u1 <= u0) continue;
+      for (auto& [g, p] : b.pieces) {  // old valid minus U (larger side kept)
+        if (!p.valid_bytes) continue;
+        uint64_t vf = p.valid_first, ve = p.valid_first + p.valid_bytes;
+        if (ve <= u0 || vf >= u1) continue;
+        uint64_t left = u0 > vf ? u0 - vf : 0, right = ve > u1 ? ve - u1 : 0;
+        if (left >= right) {
+          p.valid_bytes = left;
+        } else {
+          p.valid_first = u1;
+          p.valid_bytes = right;
+        }
+      }
+      for (const Part& part : parts) {
+        if (!whole && part.hi == part.lo) continue;
+        uint64_t first, len;
+        slice(i, part, first, len);
         Piece& p = b.pieces[part.gid];
-        // a fresh output slice is exactly what this part computed
-        if (!(p.valid_bytes && first <= p.valid_first + p.valid_bytes && p.valid_first <= first + len)) {
+        if (p.valid_bytes && (p.valid_first + p.valid_bytes == first || first + len == p.valid_first))
+          set_valid(p, first, len);
+        else {
           p.valid_first = first;
           p.valid_bytes = len;
-        } else {
-          set_valid(p, first, len);
         }
-        invalidate_others(b, part.gid, first, len);
       }
     }
     for (uint32_t i = 0; i < n; ++i)
@@ -619,11 +678,19 @@ std::vector<uint64_t> HostContext::partition_plan(Handle kernel, std::array<uint
 }
 
 Handle HostContext::enqueue_ndrange_kernel(Handle kernel, std::array<uint64_t, 3> global_size, uint32_t dims,
-                                           const std::vector<Handle>& queues, std::vector<uint64_t> weights) {
+                                           const std::vector<Handle>& queues, std::vector<uint64_t> weights,
+                                           std::vector<uint64_t> bounds) {
   std::lock_guard lock(impl_->mu);
   for (uint32_t d = 0; d < dims && d < 3; ++d)
     if (global_size[d] < 1) fail(ErrorCode::argument, "global_size extents must be >= 1");
-  std::vector<uint64_t> bounds = partition_plan(kernel, global_size, queues, std::move(weights));
+  if (bounds.empty()) {
+    bounds = partition_plan(kernel, global_size, queues, std::move(weights));
+  } else {
+    if (bounds.size() != queues.size() + 1 || bounds.front() != 0 || bounds.back() != global_size[0])
+      fail(ErrorCode::argument, "bounds must hold parts+1 boundaries from 0 to global_size[0]");
+    for (size_t i = 0; i + 1 < bounds.size(); ++i)
+      if (bounds[i] > bounds[i + 1]) fail(ErrorCode::argument, "bounds must be nondecreasing");
+  }
   std::vector<Arg> args;
   Impl::KernelRec& k = impl_->bound_kernel(kernel.id, args);
   std::vector<Impl::Part> parts;
@@ -889,14 +956,16 @@ int hcl_ctx_enqueue_ndrange_kernel(hcl_context* ctx, uint64_t queue, uint64_t ke
   });
 }
 int hcl_ctx_enqueue_ndrange_partitioned(hcl_context* ctx, uint64_t kernel, const uint64_t global[3], uint32_t dims,
-                                        const uint64_t* queues, int nqueues, const uint64_t* weights, uint64_t* event) {
+                                        const uint64_t* queues, int nqueues, const uint64_t* weights,
+                                        const uint64_t* bounds, uint64_t* event) {
   return ctx_guarded([&] {
     std::vector<Handle> qs;
     for (int i = 0; i < nqueues; ++i) qs.push_back(H(HandleKind::queue, queues[i]));
-    std::vector<uint64_t> w;
+    std::vector<uint64_t> w, b;
     if (weights) w.assign(weights, weights + nqueues);
+    if (bounds) b.assign(bounds, bounds + nqueues + 1);
     auto ev = ctx->ctx.enqueue_ndrange_kernel(H(HandleKind::kernel, kernel), {global[0], global[1], global[2]}, dims,
-                                              qs, w);
+                                              qs, w, b);
     if (event) *event = ev.id;
   });
 }

@@ -45,9 +45,9 @@ uint64_t launch_vecadd(LaunchCtx& c) {
   const BufView& A = buffer_arg(c, 0, "vecadd a");
   const BufView& B = buffer_arg(c, 1, "vecadd b");
   const BufView& C = buffer_arg(c, 2, "vecadd c");
-  if (A.first_byte == 0 && A.bytes != static_cast<uint64_t>(n) * 8)
+  if (c.whole && A.bytes != static_cast<uint64_t>(n) * 8)
     fail(ErrorCode::argument, "vecadd: input length mismatch");
-  if (B.first_byte == 0 && B.bytes != static_cast<uint64_t>(n) * 8)
+  if (c.whole && B.bytes != static_cast<uint64_t>(n) * 8)
     fail(ErrorCode::argument, "vecadd: input length mismatch");
   const double* a = at_byte<const double>(A, lo * 8, cnt * 8, "vecadd a");
   const double* b = at_byte<const double>(B, lo * 8, cnt * 8, "vecadd b");
@@ -124,7 +124,7 @@ uint64_t launch_matmul(LaunchCtx& c) {
   const BufView& A = buffer_arg(c, 0, "matmul A");
   const BufView& B = buffer_arg(c, 1, "matmul B");
   const BufView& Cb = buffer_arg(c, 2, "matmul C");
-  if (A.first_byte == 0 && A.bytes != static_cast<uint64_t>(m * k) * 8)
+  if (c.whole && A.bytes != static_cast<uint64_t>(m * k) * 8)
     fail(ErrorCode::argument, "matmul: A size != M*K");
   if (B.first_byte != 0 || B.bytes != static_cast<uint64_t>(k * n) * 8)
     fail(ErrorCode::argument, "matmul: B size != K*N");
@@ -380,7 +380,7 @@ uint64_t launch_knn(LaunchCtx& c) {
   const BufView& Qb = buffer_arg(c, 1, "knn query");
   if (Rf.first_byte != 0 || Rf.bytes != static_cast<uint64_t>(r * d) * 8)
     fail(ErrorCode::argument, "knn: ref size != R*D");
-  if (Qb.first_byte == 0 && Qb.bytes != static_cast<uint64_t>(q * d) * 8)
+  if (c.whole && Qb.bytes != static_cast<uint64_t>(q * d) * 8)
     fail(ErrorCode::argument, "knn: query size != Q*D");
   // NDRange over queries
   uint64_t lo, cnt;

@@ -354,7 +354,7 @@ uint64_t launch_gemm_tc(LaunchCtx& c) {
   const BufView& A = buffer_arg(c, 0, "gemm A");
   const BufView& B = buffer_arg(c, 1, "gemm B");
   const BufView& Cb = buffer_arg(c, 2, "gemm C");
-  if (A.first_byte == 0 && A.bytes != static_cast<uint64_t>(m * k) * es)
+  if (c.whole && A.bytes != static_cast<uint64_t>(m * k) * es)
     fail(ErrorCode::argument, std::string(what) + ": A size != M*K");
   if (B.first_byte != 0 || B.bytes != static_cast<uint64_t>(k * n) * es)
     fail(ErrorCode::argument, std::string(what) + ": B size != K*N");
@@ -468,7 +468,7 @@ uint64_t launch_gemm_f32(LaunchCtx& c) {
   const BufView& A = buffer_arg(c, 0, "gemm_f32 A");
   const BufView& B = buffer_arg(c, 1, "gemm_f32 B");
   const BufView& Cb = buffer_arg(c, 2, "gemm_f32 C");
-  if (A.first_byte == 0 && A.bytes != static_cast<uint64_t>(m * k) * 4)
+  if (c.whole && A.bytes != static_cast<uint64_t>(m * k) * 4)
     fail(ErrorCode::argument, "gemm_f32: A size != M*K");
   if (B.first_byte != 0 || B.bytes != static_cast<uint64_t>(k * n) * 4)
     fail(ErrorCode::argument, "gemm_f32: B size != K*N");

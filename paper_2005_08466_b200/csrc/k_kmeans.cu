@@ -1,5 +1,281 @@
-// placeholder: filled in by the kmeans workload
+// k-means assignment and update (config C4; assignment =
+// the reference's knn with k=1, proj/src/kernels.cpp:195-233).
+//
+// kmeans_assign: dist(x, c_k) = sum_j (c_kj - x_j)^2 in fp32 with every
+//   subtract, multiply and add separately rounded and j ascending, argmin with
+//   strict < so ties keep the smaller k — bit-identical to the oracle
+//   (ho_kmeans_assign). Blackwell's packed FP32x2 instructions (FADD2/FMUL2,
+//   IEEE round-to-nearest per lane) evaluate two centroids per instruction:
+//   each thread owns one point (coordinates duplicated into register pairs) and
+//   streams centroid pairs from shared memory (interleaved [k/2][j][2]).
+// kmeans_accumulate: exact per-cluster sums in 2^-12 fixed point (points are
+//   multiples of 2^-12), int32 shared-memory tables per block flushed with
+//   int64 atomics — integer sums, so the result is independent of order,
+//   blocks and partitions; partial sums of a partitioned launch are combined
+//   by the runtime (REDUCE_SUM class) or by an NCCL allreduce across ranks.
+// kmeans_finalize: c_k = (sum_k * 2^-12) / count_k in fp64, rounded to fp32;
+//   empty clusters keep their centroid.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+
 #include "common.hpp"
+#include "../../include/hcl_cabi.h"
+
 namespace hcl {
-void register_kmeans(std::vector<KernelDef>&) {}
+namespace {
+
+constexpr int KM_D = 32;         // fast-path dimension
+constexpr int KM_KCHUNK = 1024;  // centroids staged per pass (128 KB of smem)
+constexpr int KM_T = 512;
+
+__global__ void __launch_bounds__(KM_T, 1) kmeans_assign32_kernel(const float* __restrict__ pts, int64_t n,
+                                                                 const float* __restrict__ cent, int k,
+                                                                 int32_t* __restrict__ assign) {
+  extern __shared__ float4 cs4[];  // [KM_KCHUNK/2][KM_D/2] of (c_k[j], c_k+1[j], c_k[j+1], c_k+1[j+1])
+  float* cs = reinterpret_cast<float*>(cs4);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t first = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  // all threads of the block walk the same number of points (block-uniform loop)
+  const int64_t iters = (n + stride - 1) / stride;
+  for (int64_t it = 0; it < iters; ++it) {
+    const int64_t i = first + it * stride;
+    const bool active = i < n;
+    float2 xn[KM_D];  // (-x_j, -x_j)
+#pragma unroll
+    for (int j = 0; j < KM_D; j += 4) {
+      float4 v = active ? __ldcs(reinterpret_cast<const float4*>(pts + i * KM_D + j)) : make_float4(0, 0, 0, 0);
+      xn[j] = make_float2(-v.x, -v.x);
+      xn[j + 1] = make_float2(-v.y, -v.y);
+      xn[j + 2] = make_float2(-v.z, -v.z);
+      xn[j + 3] = make_float2(-v.w, -v.w);
+    }
+    float best = 0.f;
+    int bi = 0;
+    for (int k0 = 0; k0 < k; k0 += KM_KCHUNK) {
+      const int kc = min(KM_KCHUNK, k - k0);
+      const int kpairs = (kc + 1) / 2;
+      __syncthreads();
+      for (int e = threadIdx.x; e < kpairs * KM_D; e += blockDim.x) {
+        const int p = e / KM_D, j = e % KM_D;
+        const int ka = k0 + 2 * p, kb = ka + 1;
+        cs[(p * KM_D + j) * 2] = cent[(int64_t)ka * KM_D + j];
+        cs[(p * KM_D + j) * 2 + 1] = kb < k ? cent[(int64_t)kb * KM_D + j] : __int_as_float(0x7f800000);
+      }
+      __syncthreads();
+      for (int p = 0; p < kpairs; ++p) {
+        const float4* row = cs4 + p * (KM_D / 2);
+        float2 s = make_float2(0.f, 0.f);
+        // squares stay scalar FMUL: ptxas contracts mul.rn.f32x2 + add.rn.f32x2
+        // into FFMA2 (single rounding) even under -fmad=false, which would
+        // break bit-exactness with the oracle's rounded multiply-then-add
+#pragma unroll
+        for (int j = 0; j < KM_D; j += 2) {
+          const float4 c = row[j / 2];
+          float2 d0 = __fadd2_rn(make_float2(c.x, c.y), xn[j]);
+          s = __fadd2_rn(s, make_float2(__fmul_rn(d0.x, d0.x), __fmul_rn(d0.y, d0.y)));
+          float2 d1 = __fadd2_rn(make_float2(c.z, c.w), xn[j + 1]);
+          s = __fadd2_rn(s, make_float2(__fmul_rn(d1.x, d1.x), __fmul_rn(d1.y, d1.y)));
+        }
+        const int ka = k0 + 2 * p;
+        if (ka == 0 || s.x < best) { best = s.x; bi = ka; }
+        if (ka + 1 < k && s.y < best) { best = s.y; bi = ka + 1; }
+      }
+    }
+    if (active) assign[i] = bi;
+  }
+}
+
+// Generic D (any <= 256): scalar, same arithmetic order.
+__global__ void __launch_bounds__(256) kmeans_assign_generic_kernel(const float* __restrict__ pts, int64_t n, int d,
+                                                                   const float* __restrict__ cent, int k,
+                                                                   int32_t* __restrict__ assign) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const float* x = pts + i * d;
+  float best = 0.f;
+  int bi = 0;
+  for (int c = 0; c < k; ++c) {
+    const float* m = cent + (int64_t)c * d;
+    float s = 0.f;
+    for (int j = 0; j < d; ++j) {
+      float diff = __fsub_rn(__ldg(m + j), x[j]);
+      s = __fadd_rn(s, __fmul_rn(diff, diff));
+    }
+    if (c == 0 || s < best) { best = s; bi = c; }
+  }
+  assign[i] = bi;
+}
+
+// sums[k*d + j] += x_ij * 4096 (exact integer), counts[k] += 1
+__global__ void __launch_bounds__(1024) kmeans_accumulate_kernel(const float* __restrict__ pts,
+                                                                const int32_t* __restrict__ assign, int64_t n, int d,
+                                                                int k, unsigned long long* __restrict__ sums,
+                                                                unsigned long long* __restrict__ counts,
+                                                                int use_smem) {
+  extern __shared__ int tbl[];  // [k*d] sums + [k] counts, int32 (a block's points cannot overflow)
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nwarps = blockDim.x / 32;
+  if (use_smem) {
+    for (int e = threadIdx.x; e < k * d + k; e += blockDim.x) tbl[e] = 0;
+    __syncthreads();
+  }
+  const int64_t chunk = (n + gridDim.x - 1) / gridDim.x;
+  const int64_t lo = blockIdx.x * chunk, hi = min(n, lo + chunk);
+  for (int64_t i = lo + warp; i < hi; i += nwarps) {
+    const int c = assign[i];
+    for (int j = lane; j < d; j += 32) {
+      int q = __float2int_rz(__fmul_rn(pts[i * d + j], 4096.0f));
+      if (use_smem)
+        atomicAdd(&tbl[c * d + j], q);
+      else
+        atomicAdd(&sums[(int64_t)c * d + j], static_cast<unsigned long long>(static_cast<long long>(q)));
+    }
+    if (lane == 0) {
+      if (use_smem)
+        atomicAdd(&tbl[k * d + c], 1);
+      else
+        atomicAdd(&counts[c], 1ull);
+    }
+  }
+  if (use_smem) {
+    __syncthreads();
+    for (int e = threadIdx.x; e < k * d; e += blockDim.x)
+      if (tbl[e]) atomicAdd(&sums[e], static_cast<unsigned long long>(static_cast<long long>(tbl[e])));
+    for (int e = threadIdx.x; e < k; e += blockDim.x)
+      if (tbl[k * d + e]) atomicAdd(&counts[e], static_cast<unsigned long long>(tbl[k * d + e]));
+  }
+}
+
+__global__ void kmeans_finalize_kernel(const long long* __restrict__ sums, const long long* __restrict__ counts, int k,
+                                       int d, float* __restrict__ cent) {
+  int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= k * d) return;
+  long long cnt = counts[e / d];
+  if (cnt == 0) return;
+  cent[e] = static_cast<float>(__ddiv_rn(__dmul_rn(static_cast<double>(sums[e]), 0x1p-12), static_cast<double>(cnt)));
+}
+
+__global__ void add_i64_kernel(long long* __restrict__ dst, const long long* __restrict__ src, int64_t n) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (; i < n; i += stride) dst[i] += src[i];
+}
+
+// kmeans_assign(points, centroids, assign, N, D, K)
+uint64_t launch_assign(LaunchCtx& c) {
+  int64_t n = scalar_arg(c, 3, "kmeans_assign N");
+  int64_t d = scalar_arg(c, 4, "kmeans_assign D");
+  int64_t k = scalar_arg(c, 5, "kmeans_assign K");
+  if (n < 0 || d < 1 || d > 256 || k < 1 || k > (1 << 24))
+    fail(ErrorCode::argument, "kmeans_assign: need N >= 0, 1 <= D <= 256, 1 <= K");
+  const BufView& P = buffer_arg(c, 0, "kmeans_assign points");
+  const BufView& C = buffer_arg(c, 1, "kmeans_assign centroids");
+  const BufView& A = buffer_arg(c, 2, "kmeans_assign assign");
+  if (C.first_byte != 0 || C.bytes != static_cast<uint64_t>(k * d) * 4)
+    fail(ErrorCode::argument, "kmeans_assign: centroids size != K*D");
+  if (c.whole && P.bytes != static_cast<uint64_t>(n * d) * 4)
+    fail(ErrorCode::argument, "kmeans_assign: points size != N*D");
+  uint64_t lo, rows;
+  sub_range(c, static_cast<uint64_t>(n), lo, rows, "kmeans_assign");
+  const float* pts = at_byte<const float>(P, lo * d * 4, rows * d * 4, "kmeans_assign points");
+  int32_t* as = at_byte<int32_t>(A, lo * 4, rows * 4, "kmeans_assign assign");
+  if (!rows) return 0;
+  const float* cent = reinterpret_cast<const float*>(C.ptr);
+  if (d == KM_D && (reinterpret_cast<uintptr_t>(pts) & 15) == 0) {
+    const size_t smem = static_cast<size_t>(KM_KCHUNK) * KM_D * 4;
+    HCL_CUDA(cudaFuncSetAttribute(kmeans_assign32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem)));
+    int grid = static_cast<int>(std::min<uint64_t>(c.sm_count, ceil_div(rows, KM_T)));
+    kmeans_assign32_kernel<<<grid, KM_T, smem, c.stream>>>(pts, static_cast<int64_t>(rows), cent,
+                                                           static_cast<int>(k), as);
+  } else {
+    kmeans_assign_generic_kernel<<<static_cast<unsigned>(ceil_div(rows, 256)), 256, 0, c.stream>>>(
+        pts, static_cast<int64_t>(rows), static_cast<int>(d), cent, static_cast<int>(k), as);
+  }
+  HCL_LAUNCHED();
+  return 3ull * rows * static_cast<uint64_t>(k) * static_cast<uint64_t>(d);  // 3 flop per term
+}
+
+// kmeans_accumulate(points, assign, sums(int64 K*D), counts(int64 K), N, D, K)
+uint64_t launch_accumulate(LaunchCtx& c) {
+  int64_t n = scalar_arg(c, 4, "kmeans_accumulate N");
+  int64_t d = scalar_arg(c, 5, "kmeans_accumulate D");
+  int64_t k = scalar_arg(c, 6, "kmeans_accumulate K");
+  if (n < 0 || d < 1 || d > 256 || k < 1) fail(ErrorCode::argument, "kmeans_accumulate: bad N/D/K");
+  const BufView& P = buffer_arg(c, 0, "kmeans_accumulate points");
+  const BufView& A = buffer_arg(c, 1, "kmeans_accumulate assign");
+  const BufView& S = buffer_arg(c, 2, "kmeans_accumulate sums");
+  const BufView& Cn = buffer_arg(c, 3, "kmeans_accumulate counts");
+  if (S.first_byte != 0 || S.bytes != static_cast<uint64_t>(k * d) * 8 || Cn.first_byte != 0 ||
+      Cn.bytes != static_cast<uint64_t>(k) * 8)
+    fail(ErrorCode::argument, "kmeans_accumulate: sums must be K*D int64 and counts K int64");
+  uint64_t lo, rows;
+  sub_range(c, static_cast<uint64_t>(n), lo, rows, "kmeans_accumulate");
+  const float* pts = at_byte<const float>(P, lo * d * 4, rows * d * 4, "kmeans_accumulate points");
+  const int32_t* as = at_byte<const int32_t>(A, lo * 4, rows * 4, "kmeans_accumulate assign");
+  HCL_CUDA(cudaMemsetAsync(S.ptr, 0, S.bytes, c.stream));
+  HCL_CUDA(cudaMemsetAsync(Cn.ptr, 0, Cn.bytes, c.stream));
+  if (!rows) return 0;
+  const size_t smem = static_cast<size_t>(k * d + k) * 4;
+  const bool use_smem = smem <= 200 * 1024 && rows > static_cast<uint64_t>(k) * 4;
+  if (use_smem)
+    HCL_CUDA(cudaFuncSetAttribute(kmeans_accumulate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem)));
+  int grid = static_cast<int>(std::min<uint64_t>(static_cast<uint64_t>(c.sm_count) * 2, ceil_div(rows, 1024)));
+  if (use_smem) grid = static_cast<int>(std::min<uint64_t>(c.sm_count, ceil_div(rows, 4096)));
+  grid = std::max(grid, 1);
+  kmeans_accumulate_kernel<<<grid, 1024, use_smem ? smem : 0, c.stream>>>(
+      pts, as, static_cast<int64_t>(rows), static_cast<int>(d), static_cast<int>(k),
+      reinterpret_cast<unsigned long long*>(S.ptr), reinterpret_cast<unsigned long long*>(Cn.ptr), use_smem);
+  HCL_LAUNCHED();
+  return rows * static_cast<uint64_t>(d);
+}
+
+// kmeans_finalize(sums, counts, centroids(inout), K, D)
+uint64_t launch_finalize(LaunchCtx& c) {
+  int64_t k = scalar_arg(c, 3, "kmeans_finalize K");
+  int64_t d = scalar_arg(c, 4, "kmeans_finalize D");
+  const BufView& S = buffer_arg(c, 0, "kmeans_finalize sums");
+  const BufView& Cn = buffer_arg(c, 1, "kmeans_finalize counts");
+  const BufView& Ce = buffer_arg(c, 2, "kmeans_finalize centroids");
+  if (S.bytes != static_cast<uint64_t>(k * d) * 8 || Cn.bytes != static_cast<uint64_t>(k) * 8 ||
+      Ce.bytes != static_cast<uint64_t>(k * d) * 4)
+    fail(ErrorCode::argument, "kmeans_finalize: sizes do not match K and D");
+  kmeans_finalize_kernel<<<static_cast<unsigned>(ceil_div(k * d, 256)), 256, 0, c.stream>>>(
+      reinterpret_cast<const long long*>(S.ptr), reinterpret_cast<const long long*>(Cn.ptr), static_cast<int>(k),
+      static_cast<int>(d), reinterpret_cast<float*>(Ce.ptr));
+  HCL_LAUNCHED();
+  return static_cast<uint64_t>(k * d);
+}
+
+// reduce_add_i64(dst(inout), src, n): dst += src — the runtime's REDUCE_SUM combine step
+uint64_t launch_add_i64(LaunchCtx& c) {
+  int64_t n = scalar_arg(c, 2, "reduce_add_i64 n");
+  const BufView& D = buffer_arg(c, 0, "reduce_add_i64 dst");
+  const BufView& S = buffer_arg(c, 1, "reduce_add_i64 src");
+  if (D.bytes < static_cast<uint64_t>(n) * 8 || S.bytes < static_cast<uint64_t>(n) * 8)
+    fail(ErrorCode::argument, "reduce_add_i64: buffers shorter than n");
+  if (!n) return 0;
+  int grid = static_cast<int>(std::min<uint64_t>(ceil_div(n, 256), c.sm_count * 4));
+  add_i64_kernel<<<grid, 256, 0, c.stream>>>(reinterpret_cast<long long*>(D.ptr),
+                                             reinterpret_cast<const long long*>(S.ptr), n);
+  HCL_LAUNCHED();
+  return static_cast<uint64_t>(n);
+}
+
+uint64_t rows_km(const int64_t* s, uint32_t n) { return static_cast<uint64_t>(s[n == 6 ? 3 : 4]); }
+
+}  // namespace
+
+void register_kmeans(std::vector<KernelDef>& r) {
+  constexpr uint8_t S = HCL_ARG_SCALAR, I = HCL_ARG_IN, O = HCL_ARG_OUT, IO = HCL_ARG_INOUT;
+  constexpr uint8_t N = HCL_PART_NONE, P = HCL_PART_REPLICATE, X = HCL_PART_SPLIT_ROWS, R = HCL_PART_REDUCE_SUM;
+  r.push_back({"b200", "kmeans_assign", {I, I, O, S, S, S}, {X, P, X, N, N, N}, launch_assign, nullptr, rows_km});
+  r.push_back({"b200", "kmeans_accumulate", {I, I, O, O, S, S, S}, {X, X, R, R, N, N, N}, launch_accumulate, nullptr,
+               rows_km});
+  r.push_back({"b200", "kmeans_finalize", {I, I, IO, S, S}, {P, P, P, N, N}, launch_finalize, nullptr, nullptr});
+  r.push_back({"b200", "reduce_add_i64", {IO, I, S}, {P, P, N}, launch_add_i64, nullptr, nullptr});
+}
+
 }  // namespace hcl

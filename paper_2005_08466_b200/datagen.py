@@ -49,3 +49,28 @@ def gen_kmeans_points(count: int, d: int, blobs: int, seed: int, first: int = 0,
     out = np.empty(count * d, np.float32) if out is None else out
     N.lib().hcl_gen_kmeans_points(seed, first, count, d, blobs, _ptr(out), threads)
     return out
+
+
+def pagerank_csr(scale: int, edges: int, seed: int, threads: int = 0):
+    """Pull CSR of the R-MAT graph: (row_ptr int32[V+1], col_idx int32[E],
+    val fp32[E] = 1/outdeg(src), outdeg int32[V])."""
+    v = 1 << scale
+    row_ptr = np.empty(v + 1, np.int32)
+    col_idx = np.empty(edges, np.int32)
+    val = np.empty(edges, np.float32)
+    outdeg = np.empty(v, np.int32)
+    rc = N.lib().hcl_pagerank_csr(scale, edges, seed, row_ptr.ctypes.data, col_idx.ctypes.data, val.ctypes.data,
+                                  outdeg.ctypes.data, threads)
+    if rc:
+        raise N.HaoclError(rc - N.HCL_ERR_BASE, "pagerank_csr: bad arguments")
+    return row_ptr, col_idx, val, outdeg
+
+
+def csr_row_blocks(row_ptr: np.ndarray, max_nnz: int) -> np.ndarray:
+    """CSR-adaptive row blocks: start rows of blocks of <= max_nnz non-zeros
+    (a longer row is its own block); last entry = rows."""
+    rp = np.ascontiguousarray(row_ptr, np.int32)
+    n = int(N.lib().hcl_csr_row_blocks(rp.ctypes.data, len(rp) - 1, max_nnz, None))
+    out = np.empty(n + 1, np.int32)
+    N.lib().hcl_csr_row_blocks(rp.ctypes.data, len(rp) - 1, max_nnz, out.ctypes.data)
+    return out

@@ -1,0 +1,86 @@
+"""k-means over the partitioned NDRange (config C4).
+
+Points are SPLIT_ROWS across the queues; centroids are REPLICATE. Per
+iteration: `kmeans_assign` (exact fp32 distances, bit-identical to the
+reference's knn k=1 semantics) and `kmeans_accumulate` as partitioned
+launches, then `kmeans_finalize` on the first queue. Centroid sums are exact
+int64 fixed point (points are multiples of 2^-12), combined across parts by
+the runtime's REDUCE_SUM class (or an NCCL allreduce across processes), so
+every iteration is bit-identical for any partition.
+"""
+from __future__ import annotations
+
+from typing import Optional, Sequence
+
+import numpy as np
+
+from .runtime import Handle, HostContext
+
+
+class KMeans:
+    def __init__(self, ctx: HostContext, queues: Sequence[Handle], n: int, d: int, k: int,
+                 weights: Optional[Sequence[int]] = None):
+        self.ctx, self.queues, self.n, self.d, self.k = ctx, list(queues), n, d, k
+        self.weights = list(weights) if weights is not None else None
+        mk = ctx.create_buffer
+        self.b_pts = mk(n * d * 4)
+        self.b_cent = mk(k * d * 4)
+        self.b_assign = mk(n * 4)
+        self.b_sums = mk(k * d * 8)
+        self.b_counts = mk(k * 8)
+        prog = ctx.create_program("b200")
+        self.k_assign = ctx.create_kernel(prog, "kmeans_assign")
+        self.k_acc = ctx.create_kernel(prog, "kmeans_accumulate")
+        self.k_fin = ctx.create_kernel(prog, "kmeans_finalize")
+        for j, a in enumerate([self.b_pts, self.b_cent, self.b_assign, n, d, k]):
+            ctx.set_kernel_arg(self.k_assign, j, a)
+        for j, a in enumerate([self.b_pts, self.b_assign, self.b_sums, self.b_counts, n, d, k]):
+            ctx.set_kernel_arg(self.k_acc, j, a)
+        for j, a in enumerate([self.b_sums, self.b_counts, self.b_cent, k, d]):
+            ctx.set_kernel_arg(self.k_fin, j, a)
+
+    def load_points(self, pts: np.ndarray, bounds: Optional[Sequence[int]] = None) -> None:
+        """Scatter each queue's row block of the points straight to its device."""
+        if bounds is None:
+            bounds = self.ctx.partition_plan(self.k_assign, (self.n, 1, 1), self.queues, self.weights)
+        flat = np.ascontiguousarray(pts, np.float32).reshape(-1)
+        for i, q in enumerate(self.queues):
+            lo, hi = bounds[i], bounds[i + 1]
+            if hi > lo:
+                self.ctx.enqueue_write_buffer(q, self.b_pts, flat[lo * self.d:hi * self.d], offset=lo * self.d * 4)
+        self.bounds = list(bounds)
+
+    def set_centroids(self, cent: np.ndarray) -> None:
+        self.ctx.enqueue_write_buffer(self.queues[0], self.b_cent, np.ascontiguousarray(cent, np.float32))
+
+    def iterate(self, iterations: int = 1) -> None:
+        ctx, g = self.ctx, (self.n, 1, 1)
+        for _ in range(iterations):
+            ctx.enqueue_ndrange_partitioned(self.k_assign, g, 1, self.queues, bounds=self.bounds)
+            ctx.enqueue_ndrange_partitioned(self.k_acc, g, 1, self.queues, bounds=self.bounds)
+            ctx.enqueue_ndrange_kernel(self.queues[0], self.k_fin)
+
+    def assign_only(self) -> None:
+        self.ctx.enqueue_ndrange_partitioned(self.k_assign, (self.n, 1, 1), 1, self.queues, bounds=self.bounds)
+
+    def finish(self) -> None:
+        for q in self.queues:
+            self.ctx.finish(q)
+
+    def centroids(self) -> np.ndarray:
+        self.finish()
+        return self.ctx.enqueue_read_buffer(self.queues[0], self.b_cent).view(np.float32).reshape(self.k, self.d)
+
+    def assignments(self) -> np.ndarray:
+        self.finish()
+        return self.ctx.enqueue_read_buffer(self.queues[0], self.b_assign).view(np.int32)
+
+    def sums(self):
+        self.finish()
+        s = self.ctx.enqueue_read_buffer(self.queues[0], self.b_sums).view(np.int64)
+        c = self.ctx.enqueue_read_buffer(self.queues[0], self.b_counts).view(np.int64)
+        return s, c
+
+    def close(self) -> None:
+        for b in (self.b_pts, self.b_cent, self.b_assign, self.b_sums, self.b_counts):
+            self.ctx.release(b)

@@ -176,13 +176,16 @@ class HostContext:
         return Handle(HandleKind.event, ev.value)
 
     def enqueue_ndrange_partitioned(self, kernel: Handle, global_size, dims: int, queues: Sequence[Handle],
-                                    weights: Optional[Sequence[int]] = None) -> Handle:
-        """Partitioned NDRange: split dim 0 of global_size over `queues`."""
+                                    weights: Optional[Sequence[int]] = None,
+                                    bounds: Optional[Sequence[int]] = None) -> Handle:
+        """Partitioned NDRange: split dim 0 of global_size over `queues` (by
+        `weights`, or at explicit row `bounds`, e.g. nnz-balanced ranges)."""
         g = (C.c_uint64 * 3)(*global_size)
         qs = (C.c_uint64 * len(queues))(*[q.id for q in queues])
         w = (C.c_uint64 * len(queues))(*weights) if weights is not None else None
+        b = (C.c_uint64 * (len(queues) + 1))(*[int(x) for x in bounds]) if bounds is not None else None
         ev = C.c_uint64()
-        check(self._L.hcl_ctx_enqueue_ndrange_partitioned(self._ctx, kernel.id, g, dims, qs, len(queues), w,
+        check(self._L.hcl_ctx_enqueue_ndrange_partitioned(self._ctx, kernel.id, g, dims, qs, len(queues), w, b,
                                                           C.byref(ev)))
         return Handle(HandleKind.event, ev.value)
 

@@ -1,0 +1,90 @@
+"""k-means (config C4) parity: assignments bit-exact vs the oracle (the
+reference's knn k=1 semantics in fp32: diff = c - x, ascending d, rounded
+multiply then add, ties to the smaller index), exact int64 sums, centroids
+bit-exact after several iterations, and bit-identical for P in {1, 2, 4}."""
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_2005_08466_b200 import datagen as G
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def queues(ctx):
+    qs = [ctx.create_queue(g) for g in ctx.get_device_ids()[:4]]
+    yield qs
+    for q in qs:
+        ctx.release(q)
+
+
+def oracle_iterations(pts, n, d, k, cent, iters):
+    for _ in range(iters):
+        a = O.kmeans_assign(pts, n, d, cent, k)
+        s, c = O.kmeans_accumulate(pts, n, d, a, k)
+        cent = O.kmeans_finalize(s, c, k, d, cent)
+    return a, s, c, cent
+
+
+@pytest.mark.parametrize("n,d,k", [(20000, 32, 64), (5000, 32, 1030), (3000, 7, 33), (4099, 32, 1)])
+def test_assign_and_update_bitexact(ctx, queues, n, d, k):
+    from paper_2005_08466_b200.kmeans import KMeans
+
+    pts = G.gen_kmeans_points(n, d, max(k, 2), 42)
+    cent0 = pts[: k * d].copy()
+    a_want, s_want, c_want, cent_want = oracle_iterations(pts, n, d, k, cent0, 3)
+    km = KMeans(ctx, queues[:1], n, d, k)
+    km.load_points(pts)
+    km.set_centroids(cent0)
+    km.iterate(2)
+    km.assign_only()
+    km.finish()
+    # after 2 full iterations + assign: assignments of iteration 3
+    got_a = km.assignments()
+    km.iterate(1)
+    s, c = km.sums()
+    cent = km.centroids()
+    km.close()
+    assert (got_a == a_want).all()
+    assert (s == s_want).all() and (c == c_want).all()
+    assert cent.tobytes() == cent_want.reshape(k, d).tobytes()
+
+
+def test_ties_go_to_smaller_index(ctx, queues):
+    from paper_2005_08466_b200.kmeans import KMeans
+
+    d, k, n = 32, 6, 64
+    cent = np.zeros((k, d), np.float32)
+    cent[1] = cent[3] = 1.0  # duplicates: equal distances
+    cent[2] = cent[4] = -1.0
+    cent[5] = 1.0
+    pts = np.zeros((n, d), np.float32)
+    pts[::2] = 1.0
+    pts[1::2] = -1.0
+    km = KMeans(ctx, queues[:1], n, d, k)
+    km.load_points(pts)
+    km.set_centroids(cent)
+    km.assign_only()
+    a = km.assignments()
+    km.close()
+    assert (a[::2] == 1).all() and (a[1::2] == 2).all()
+    assert (a == O.kmeans_assign(pts.ravel(), n, d, cent.ravel(), k)).all()
+
+
+@pytest.mark.parametrize("weights", [None, [3, 1, 2, 2]])
+def test_partition_invariance(ctx, queues, weights):
+    from paper_2005_08466_b200.kmeans import KMeans
+
+    n, d, k = 30000, 32, 128
+    pts = G.gen_kmeans_points(n, d, k, 43)
+    cent0 = pts[: k * d].copy()
+    outs = []
+    for P in (1, 2, 4):
+        km = KMeans(ctx, queues[:P], n, d, k, weights=weights[:P] if weights else None)
+        km.load_points(pts)
+        km.set_centroids(cent0)
+        km.iterate(3)
+        outs.append((km.centroids().tobytes(), km.assignments().tobytes()))
+        km.close()
+    assert outs[0] == outs[1] == outs[2]
