@@ -34,6 +34,10 @@ void hcl_gen_kmeans_points(uint64_t seed, uint64_t first, uint64_t count, int64_
  * row_ptr: 2^scale+1, col_idx/val: edges, outdeg: 2^scale. Returns 0. */
 int hcl_pagerank_csr(int scale, uint64_t edges, uint64_t seed, int32_t* row_ptr, int32_t* col_idx, float* val,
                      int32_t* outdeg, int threads);
+/* Warp work units of the PageRank SpMV: int32x4 {row0,row1,p0,p1} per unit and
+ * {row, first_unit, nchunks} per long row (> warp_nnz). Pass NULL arrays to count. */
+int hcl_pagerank_units(const int32_t* row_ptr, int64_t rows, int64_t warp_nnz, int32_t* units, int32_t* long_rows,
+                       int64_t* n_units, int64_t* n_long);
 /* CSR-adaptive row blocks (<= max_nnz per multi-row block); out may be NULL to
  * count. Returns the number of blocks; out[0..n] are block start rows. */
 int64_t hcl_csr_row_blocks(const int32_t* row_ptr, int64_t rows, int64_t max_nnz, int32_t* out);

@@ -78,7 +78,8 @@ def lib():
         L.ho_rmat_edges.argtypes = [C.c_int, C.c_int64, C.c_int64, C.c_uint64, _u32p, _u32p]
         L.ho_pagerank_csr.argtypes = [C.c_int, C.c_int64, C.c_uint64, _i32p, _i32p, _f32p, _i32p]
         L.ho_spmv_f32.argtypes = [_i32p, _i32p, _f32p, _f32p, C.c_int64, C.c_int64, _f32p]
-        L.ho_pagerank.argtypes = [C.c_int64, _i32p, _i32p, _f32p, _i32p, C.c_int, _f32p]
+        L.ho_pagerank.argtypes = [C.c_int64, _i32p, _i32p, _f32p, _i32p, C.c_int, C.c_int, _f32p]
+        L.ho_spmv_f32_b200.argtypes = [_i32p, _i32p, _f32p, _f32p, C.c_int64, C.c_int64, _f32p]
         L.ho_kmeans_points.argtypes = [C.c_uint64, C.c_int64, C.c_int64, C.c_int64, C.c_int64, _f32p]
         L.ho_kmeans_assign.argtypes = [_f32p, C.c_int64, C.c_int64, _f32p, C.c_int64, _i32p]
         L.ho_kmeans_accumulate.argtypes = [_f32p, C.c_int64, C.c_int64, _i32p, C.c_int64, _i64p, _i64p]
@@ -269,11 +270,21 @@ def spmv_f32(row_ptr, col_idx, val, x, lo: int, hi: int) -> np.ndarray:
     return y
 
 
-def pagerank(row_ptr, col_idx, val, outdeg, iterations: int) -> np.ndarray:
+def spmv_f32_b200(row_ptr, col_idx, val, x, lo: int, hi: int) -> np.ndarray:
+    """fp32 SpMV in the GPU kernel's fixed per-row order (see haocl_oracle.c)."""
+    y = np.empty(hi - lo, np.float32)
+    lib().ho_spmv_f32_b200(_ptr(row_ptr, _i32p), _ptr(col_idx, _i32p), _ptr(val, _f32p),
+                           _ptr(x, _f32p), lo, hi, _ptr(y, _f32p))
+    return y
+
+
+def pagerank(row_ptr, col_idx, val, outdeg, iterations: int, b200_order: bool = False) -> np.ndarray:
+    """PageRank; b200_order=False sums rows in the reference's ascending order,
+    True in the GPU kernel's restated order (bit-exact check)."""
     v = len(row_ptr) - 1
     x = np.empty(v, np.float32)
     lib().ho_pagerank(v, _ptr(row_ptr, _i32p), _ptr(col_idx, _i32p), _ptr(val, _f32p),
-                      _ptr(outdeg, _i32p), iterations, _ptr(x, _f32p))
+                      _ptr(outdeg, _i32p), iterations, int(b200_order), _ptr(x, _f32p))
     return x
 
 

@@ -449,12 +449,51 @@ void ho_spmv_f32(const int32_t* row_ptr, const int32_t* col_idx, const float* va
   }
 }
 
+/* The GPU kernel's fixed per-row summation order (csrc/k_graph.cu), restated
+ * so the CUDA path can be checked bit-for-bit; it depends only on the row's
+ * length, never on the partition. Rows of <= 32 products: ascending (the
+ * reference's order, reference.cpp:22-25). Longer rows: 4096-element chunks;
+ * in a chunk, lane l (0..31) sums elements l, l+32, ... sequentially, then an
+ * xor butterfly (offsets 16, 8, 4, 2, 1) combines the lanes (lane 0's value);
+ * chunk totals are added in chunk order. */
+static float row_sum_b200(const int32_t* col_idx, const float* val, const float* x, int64_t p0, int64_t n) {
+  if (n <= 32) {
+    float s = 0.0f;
+    for (int64_t q = 0; q < n; ++q) s += val[p0 + q] * x[col_idx[p0 + q]];
+    return s;
+  }
+  float total = 0.0f;
+  int first = 1;
+  for (int64_t c0 = 0; c0 < n; c0 += 4096) {
+    int64_t cl = n - c0 < 4096 ? n - c0 : 4096;
+    float v[32], w[32];
+    for (int l = 0; l < 32; ++l) {
+      float s = 0.0f;
+      for (int64_t q = l; q < cl; q += 32) s += val[p0 + c0 + q] * x[col_idx[p0 + c0 + q]];
+      v[l] = s;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      for (int l = 0; l < 32; ++l) w[l] = v[l] + v[l ^ o];
+      for (int l = 0; l < 32; ++l) v[l] = w[l];
+    }
+    total = first ? v[0] : total + v[0];
+    first = 0;
+  }
+  return total;
+}
+
+void ho_spmv_f32_b200(const int32_t* row_ptr, const int32_t* col_idx, const float* val,
+                      const float* x, int64_t lo, int64_t hi, float* y) {
+  for (int64_t i = lo; i < hi; ++i)
+    y[i - lo] = row_sum_b200(col_idx, val, x, row_ptr[i], (int64_t)row_ptr[i + 1] - row_ptr[i]);
+}
+
 /* PageRank (restated; not in the reference). d = 0.85, x0 = 1/V, dangling mass
  * summed exactly in 2^-56 fixed point (order free), then
  *   x_new[i] = base + d * (y[i] + dangling * invV)
  * with every operation individually rounded in fp32. */
 void ho_pagerank(int64_t v, const int32_t* row_ptr, const int32_t* col_idx, const float* val,
-                 const int32_t* outdeg, int iterations, float* x) {
+                 const int32_t* outdeg, int iterations, int b200_order, float* x) {
   const float d = 0.85f;
   const float base = (float)((1.0 - 0.85) / (double)v);
   const float inv_v = (float)(1.0 / (double)v);
@@ -466,7 +505,10 @@ void ho_pagerank(int64_t v, const int32_t* row_ptr, const int32_t* col_idx, cons
       if (outdeg[j] == 0) dsum += (int64_t)(x[j] * 0x1p56f);
     float dangling = (float)((double)dsum * 0x1p-56);
     float t = dangling * inv_v;
-    ho_spmv_f32(row_ptr, col_idx, val, x, 0, v, y);
+    if (b200_order)
+      ho_spmv_f32_b200(row_ptr, col_idx, val, x, 0, v, y);
+    else
+      ho_spmv_f32(row_ptr, col_idx, val, x, 0, v, y);
     for (int64_t i = 0; i < v; ++i) {
       float s = y[i] + t;
       float m = d * s;

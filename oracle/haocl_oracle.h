@@ -68,8 +68,10 @@ int ho_pagerank_csr(int scale, int64_t edges, uint64_t seed, int32_t* row_ptr, i
                     float* val, int32_t* outdeg);
 void ho_spmv_f32(const int32_t* row_ptr, const int32_t* col_idx, const float* val,
                  const float* x, int64_t lo, int64_t hi, float* y);
+void ho_spmv_f32_b200(const int32_t* row_ptr, const int32_t* col_idx, const float* val,
+                      const float* x, int64_t lo, int64_t hi, float* y);
 void ho_pagerank(int64_t v, const int32_t* row_ptr, const int32_t* col_idx, const float* val,
-                 const int32_t* outdeg, int iterations, float* x);
+                 const int32_t* outdeg, int iterations, int b200_order, float* x);
 void ho_kmeans_points(uint64_t seed, int64_t first, int64_t count, int64_t d, int64_t blobs,
                       float* out);
 void ho_kmeans_assign(const float* pts, int64_t n, int64_t d, const float* cent, int64_t k,

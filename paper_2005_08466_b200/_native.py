@@ -121,6 +121,7 @@ DATAGEN = [
     ("hcl_pagerank_csr", C.c_int, [C.c_int, C.c_uint64, C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                    C.c_int]),
     ("hcl_csr_row_blocks", C.c_int64, [C.c_void_p, C.c_int64, C.c_int64, C.c_void_p]),
+    ("hcl_pagerank_units", C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_void_p, C.c_void_p, i64p, i64p]),
 ]
 
 EXTRA = []  # appended by workload modules

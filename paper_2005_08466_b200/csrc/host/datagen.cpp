@@ -191,6 +191,57 @@ int hcl_pagerank_csr(int scale, uint64_t edges, uint64_t seed, int32_t* row_ptr,
   return 0;
 }
 
+// Warp work units of the PageRank SpMV (csrc/k_graph.cu). A unit is
+// {row0, row1, p0, p1}: either consecutive rows with <= warp_nnz products in
+// total (one warp), or one 4096-product chunk of a longer row (row1 = row0+1,
+// [p0,p1) the chunk). Long rows get a fixup entry {row, first_unit, nchunks}:
+// a second pass folds the chunk totals in chunk order. Units are sorted by row
+// and depend only on row_ptr (so every partition sees the same units).
+int hcl_pagerank_units(const int32_t* row_ptr, int64_t rows, int64_t warp_nnz, int32_t* units, int32_t* long_rows,
+                       int64_t* n_units, int64_t* n_long) {
+  if (warp_nnz < 1 || warp_nnz > 4096) return 1009;
+  int64_t nu = 0, nl = 0, r = 0;
+  while (r < rows) {
+    int64_t start = row_ptr[r];
+    int64_t len = row_ptr[r + 1] - start;
+    if (len > warp_nnz) {
+      int64_t nch = (len + 4095) / 4096;
+      if (long_rows) {
+        long_rows[3 * nl] = static_cast<int32_t>(r);
+        long_rows[3 * nl + 1] = static_cast<int32_t>(nu);
+        long_rows[3 * nl + 2] = static_cast<int32_t>(nch);
+      }
+      for (int64_t c = 0; c < nch; ++c) {
+        if (units) {
+          int32_t* u = units + 4 * (nu + c);
+          u[0] = static_cast<int32_t>(r);
+          u[1] = static_cast<int32_t>(r + 1);
+          u[2] = static_cast<int32_t>(start + c * 4096);
+          u[3] = static_cast<int32_t>(std::min<int64_t>(start + (c + 1) * 4096, start + len));
+        }
+      }
+      nu += nch;
+      ++nl;
+      ++r;
+      continue;
+    }
+    int64_t e = r + 1;
+    while (e < rows && row_ptr[e + 1] - start <= warp_nnz) ++e;
+    if (units) {
+      int32_t* u = units + 4 * nu;
+      u[0] = static_cast<int32_t>(r);
+      u[1] = static_cast<int32_t>(e);
+      u[2] = static_cast<int32_t>(start);
+      u[3] = row_ptr[e];
+    }
+    ++nu;
+    r = e;
+  }
+  *n_units = nu;
+  *n_long = nl;
+  return 0;
+}
+
 // Row blocks of a CSR for the PageRank SpMV (CSR-adaptive): consecutive rows
 // grouped while their nnz total stays <= max_nnz; a row longer than max_nnz
 // is a block by itself. out[0..count] are block start rows (out[count] = rows).

@@ -2,18 +2,23 @@
 // a13 spmv_compute iterated, proj/src/kernels.cpp:132-152), int32 indices and
 // fp32 values, HBM-bound.
 //
-// CSR-adaptive schedule: the row-block array (hcl_csr_row_blocks) groups
-// consecutive rows into blocks of <= max_nnz non-zeros; a longer row is a block
-// of its own. A CTA takes one row block at a time:
-//   * multi-row block: the block's products val[p]*x[col[p]] are streamed with
-//     coalesced loads into shared memory, then each thread sums ONE row in
-//     ascending storage order — the reference's order, so these rows are
-//     bit-identical to the fp32 oracle;
-//   * single long row: thread-strided partial sums and a fixed shuffle tree.
-// Row blocks depend only on row_ptr, and a partitioned launch clips them to
-// its row range [lo,hi), so results are bit-identical for every partition P.
-// The PageRank update x' = base + d*(y + dangling/V) is fused into the store,
-// every operation separately rounded (matches oracle ho_pagerank).
+// Warp-granular schedule, no block-wide barriers: the unit array
+// (hcl_pagerank_units) holds, sorted by row,
+//   * multi-row units: consecutive rows with <= warp_nnz products in total. The
+//     warp streams the products val[p]*x[col[p]] (coalesced, 4 loads in flight
+//     per lane) into its own shared-memory slice; then a row of <= 32 products
+//     is summed by one lane in ascending order (the reference's order,
+//     reference.cpp:22-25) and a longer row by the whole warp (lane-strided
+//     partial sums + xor butterfly);
+//   * chunk units: one 4096-product chunk of a longer row, summed by a warp in
+//     the same lane-strided + butterfly order into a per-unit scratch slot; a
+//     fixup pass folds each long row's chunk totals in chunk order.
+// The per-row order depends only on the row's length — restated exactly in the
+// oracle (ho_spmv_f32_b200) — so results are bit-identical to that oracle and
+// identical for every partition P of the NDRange (units are global, a part
+// clips multi-row units to its rows [lo,hi); rows are never split). The
+// PageRank update x' = base + d*(y + dangling/V) is fused into the stores,
+// every operation separately rounded (oracle ho_pagerank).
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -26,182 +31,254 @@ namespace hcl {
 namespace {
 
 constexpr int PR_T = 256;
+constexpr int PR_WARPS = PR_T / 32;
+constexpr int PR_CHUNK = 4096;  // long-row chunk (part of the summation-order definition)
 
+// sum over j with outdeg[j]==0 of trunc(x_j * 2^56): integer, so order free
 __global__ void __launch_bounds__(256) pr_dangling_kernel(const float* __restrict__ x, const int* __restrict__ outdeg,
                                                           int64_t v, unsigned long long* __restrict__ out) {
-  int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   unsigned long long s = 0;
-  for (int64_t i = tid; i < v; i += stride)
-    if (outdeg[i] == 0) s += static_cast<unsigned long long>(__float2ll_rz(__fmul_rn(x[i], 0x1p56f)));
-  // integer sums: any order gives the same bits
+  const int64_t v4 = v / 4;
+  const float4* x4 = reinterpret_cast<const float4*>(x);
+  const int4* d4 = reinterpret_cast<const int4*>(outdeg);
+  for (int64_t i = tid; i < v4; i += 2 * stride) {
+    int4 da = __ldcs(d4 + i);
+    int4 db = i + stride < v4 ? __ldcs(d4 + i + stride) : make_int4(1, 1, 1, 1);
+    float4 xa = __ldcs(x4 + i);
+    float4 xb = i + stride < v4 ? __ldcs(x4 + i + stride) : make_float4(0, 0, 0, 0);
+#define HCL_DANG(dv, xv) \
+  if ((dv) == 0) s += static_cast<unsigned long long>(__float2ll_rz(__fmul_rn((xv), 0x1p56f)))
+    HCL_DANG(da.x, xa.x); HCL_DANG(da.y, xa.y); HCL_DANG(da.z, xa.z); HCL_DANG(da.w, xa.w);
+    HCL_DANG(db.x, xb.x); HCL_DANG(db.y, xb.y); HCL_DANG(db.z, xb.z); HCL_DANG(db.w, xb.w);
+  }
+  for (int64_t i = v4 * 4 + tid; i < v; i += stride) HCL_DANG(outdeg[i], x[i]);
+#undef HCL_DANG
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
   if ((threadIdx.x & 31) == 0 && s) atomicAdd(out, s);
 }
 
-__device__ __forceinline__ int first_block_ending_after(const int* __restrict__ blocks, int n, int row) {
-  // smallest b in [0,n) with blocks[b+1] > row
-  int lo = 0, hi = n;
-  while (lo < hi) {
-    int mid = (lo + hi) >> 1;
-    if (blocks[mid + 1] > row) hi = mid; else lo = mid + 1;
-  }
-  return lo;
+// The CSR arrays stream through once (2 GiB per iteration): keep them out of L1
+// and first in line for L2 eviction, so the gathered x lines stay cached.
+__device__ __forceinline__ int ld_stream(const int* p) {
+  int v;
+  asm volatile("ld.global.nc.L1::no_allocate.b32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ float ld_stream(const float* p) {
+  float v;
+  asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ float ld_x(const float* p) {
+  float v;
+  asm volatile("ld.global.nc.L1::evict_last.f32 %0, [%1];" : "=f"(v) : "l"(p));
+  return v;
+}
+
+__device__ __forceinline__ float butterfly(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = __fadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+struct Update {
+  float base, damp, t;
+};
+
+template <bool UPDATE>
+__device__ __forceinline__ void pr_store(float* __restrict__ y, int r, int lo, float s, const Update& u) {
+  if constexpr (UPDATE)
+    y[r - lo] = __fadd_rn(u.base, __fmul_rn(u.damp, __fadd_rn(s, u.t)));
+  else
+    y[r - lo] = s;
 }
 
 template <bool UPDATE>
-__global__ void __launch_bounds__(PR_T) pr_spmv_kernel(const int* __restrict__ row_ptr, const int* __restrict__ col,
-                                                       const float* __restrict__ val, int64_t nnz_off,
-                                                       const int* __restrict__ blocks, int nblocks,
-                                                       const float* __restrict__ x,
-                                                       const unsigned long long* __restrict__ dsum,
-                                                       float* __restrict__ y, int lo, int hi, float base, float damp,
-                                                       float inv_v, int max_nnz) {
-  extern __shared__ float prod[];
-  __shared__ float wsum[PR_T / 32];
-  const int tid = threadIdx.x;
-  float t = 0.f;
+__device__ __forceinline__ Update pr_update(const unsigned long long* dsum, float base, float damp, float inv_v) {
+  Update u{base, damp, 0.f};
   if constexpr (UPDATE) {
     float dangling = static_cast<float>(static_cast<double>(*dsum) * 0x1p-56);
-    t = __fmul_rn(dangling, inv_v);
+    u.t = __fmul_rn(dangling, inv_v);
   }
-  auto store = [&](int r, float s) {
-    if constexpr (UPDATE)
-      y[r - lo] = __fadd_rn(base, __fmul_rn(damp, __fadd_rn(s, t)));
-    else
-      y[r - lo] = s;
-  };
-  const int b_first = first_block_ending_after(blocks, nblocks, lo);
-  const int b_last = first_block_ending_after(blocks, nblocks, hi - 1) + 1;
+  return u;
+}
+
+// lane-strided partial sums over [p, e) then the butterfly (all lanes hold the total)
+__device__ __forceinline__ float warp_row_sum(const int* __restrict__ colp, const float* __restrict__ valp,
+                                              const float* __restrict__ x, int p, int e, int lane) {
+  float v = 0.f;
+  int q = p + lane;
+  for (; q + 96 < e; q += 128) {
+    int i0 = ld_stream(colp + q), i1 = ld_stream(colp + q + 32), i2 = ld_stream(colp + q + 64), i3 = ld_stream(colp + q + 96);
+    float v0 = ld_stream(valp + q), v1 = ld_stream(valp + q + 32), v2 = ld_stream(valp + q + 64), v3 = ld_stream(valp + q + 96);
+    float x0 = ld_x(x + i0), x1 = ld_x(x + i1), x2 = ld_x(x + i2), x3 = ld_x(x + i3);
+    v = __fadd_rn(v, __fmul_rn(v0, x0));
+    v = __fadd_rn(v, __fmul_rn(v1, x1));
+    v = __fadd_rn(v, __fmul_rn(v2, x2));
+    v = __fadd_rn(v, __fmul_rn(v3, x3));
+  }
+  for (; q < e; q += 32) v = __fadd_rn(v, __fmul_rn(ld_stream(valp + q), ld_x(x + ld_stream(colp + q))));
+  return butterfly(v);
+}
+
+template <bool UPDATE>
+__global__ void __launch_bounds__(PR_T) pr_units_kernel(const int* __restrict__ row_ptr, const int* __restrict__ col,
+                                                        const float* __restrict__ val, int64_t nnz_off,
+                                                        const int4* __restrict__ units, int n_units,
+                                                        const float* __restrict__ x,
+                                                        const unsigned long long* __restrict__ dsum,
+                                                        float* __restrict__ y, int lo, int hi, float base, float damp,
+                                                        float inv_v, int warp_nnz, float* __restrict__ chunk_tot) {
+  extern __shared__ float prod_all[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  float* prod = prod_all + warp * warp_nnz;
+  const Update upd = pr_update<UPDATE>(dsum, base, damp, inv_v);
+  // units overlapping [lo, hi): row1 > lo and row0 < hi (both monotone in u)
+  int a = 0, b = n_units;
+  while (a < b) {
+    int m = (a + b) >> 1;
+    if (__ldg(&units[m].y) > lo) b = m; else a = m + 1;
+  }
+  const int u_first = a;
+  b = n_units;
+  while (a < b) {
+    int m = (a + b) >> 1;
+    if (__ldg(&units[m].x) >= hi) b = m; else a = m + 1;
+  }
+  const int u_last = a;
   const int* colp = col - nnz_off;
   const float* valp = val - nnz_off;
-  for (int b = b_first + blockIdx.x; b < b_last; b += gridDim.x) {
-    const int br0 = blocks[b], br1 = blocks[b + 1];
-    const int r0 = max(br0, lo), r1 = min(br1, hi);
-    const int p0 = row_ptr[r0], p1 = row_ptr[r1];
-    const int n = p1 - p0;
-    if (br1 - br0 == 1 && n > max_nnz) {
-      // long row
-      float s = 0.f;
-      int p = p0 + tid;
-      for (; p + 3 * PR_T < p1; p += 4 * PR_T) {
-        int c0 = __ldg(colp + p), c1 = __ldg(colp + p + PR_T), c2 = __ldg(colp + p + 2 * PR_T), c3 = __ldg(colp + p + 3 * PR_T);
-        float v0 = __ldg(valp + p), v1 = __ldg(valp + p + PR_T), v2 = __ldg(valp + p + 2 * PR_T), v3 = __ldg(valp + p + 3 * PR_T);
-        s = __fadd_rn(s, __fmul_rn(v0, __ldg(x + c0)));
-        s = __fadd_rn(s, __fmul_rn(v1, __ldg(x + c1)));
-        s = __fadd_rn(s, __fmul_rn(v2, __ldg(x + c2)));
-        s = __fadd_rn(s, __fmul_rn(v3, __ldg(x + c3)));
-      }
-      for (; p < p1; p += PR_T) s = __fadd_rn(s, __fmul_rn(__ldg(valp + p), __ldg(x + __ldg(colp + p))));
-      for (int o = 16; o > 0; o >>= 1) s = __fadd_rn(s, __shfl_xor_sync(0xffffffffu, s, o));
-      if ((tid & 31) == 0) wsum[tid >> 5] = s;
-      __syncthreads();
-      if (tid == 0) {
-        float tot = wsum[0];
-        for (int w = 1; w < PR_T / 32; ++w) tot = __fadd_rn(tot, wsum[w]);
-        store(r0, tot);
-      }
-      __syncthreads();
-    } else {
-      int i = tid;
-      for (; i + 3 * PR_T < n; i += 4 * PR_T) {
-        int c0 = __ldg(colp + p0 + i), c1 = __ldg(colp + p0 + i + PR_T), c2 = __ldg(colp + p0 + i + 2 * PR_T),
-            c3 = __ldg(colp + p0 + i + 3 * PR_T);
-        float v0 = __ldg(valp + p0 + i), v1 = __ldg(valp + p0 + i + PR_T), v2 = __ldg(valp + p0 + i + 2 * PR_T),
-              v3 = __ldg(valp + p0 + i + 3 * PR_T);
-        prod[i] = __fmul_rn(v0, __ldg(x + c0));
-        prod[i + PR_T] = __fmul_rn(v1, __ldg(x + c1));
-        prod[i + 2 * PR_T] = __fmul_rn(v2, __ldg(x + c2));
-        prod[i + 3 * PR_T] = __fmul_rn(v3, __ldg(x + c3));
-      }
-      for (; i < n; i += PR_T) prod[i] = __fmul_rn(__ldg(valp + p0 + i), __ldg(x + __ldg(colp + p0 + i)));
-      __syncthreads();
-      for (int r = r0 + tid; r < r1; r += PR_T) {
-        const int q0 = row_ptr[r] - p0, q1 = row_ptr[r + 1] - p0;
-        float s = 0.f;
-        for (int q = q0; q < q1; ++q) s = __fadd_rn(s, prod[q]);
-        store(r, s);
-      }
-      __syncthreads();
+  const int nw = gridDim.x * PR_WARPS;
+  for (int u = u_first + blockIdx.x * PR_WARPS + warp; u < u_last; u += nw) {
+    const int4 U = units[u];
+    if (U.y - U.x == 1 && __ldg(row_ptr + U.x + 1) - __ldg(row_ptr + U.x) > warp_nnz) {
+      // one chunk of a long row
+      const float v = warp_row_sum(colp, valp, x, U.z, U.w, lane);
+      if (lane == 0) chunk_tot[u] = v;
+      continue;
     }
+    const int r0 = max(U.x, lo), r1 = min(U.y, hi);
+    const int p0 = __ldg(row_ptr + r0), n = __ldg(row_ptr + r1) - p0;
+    int i = lane;
+    for (; i + 96 < n; i += 128) {
+      int c0 = ld_stream(colp + p0 + i), c1 = ld_stream(colp + p0 + i + 32), c2 = ld_stream(colp + p0 + i + 64),
+          c3 = ld_stream(colp + p0 + i + 96);
+      float v0 = ld_stream(valp + p0 + i), v1 = ld_stream(valp + p0 + i + 32), v2 = ld_stream(valp + p0 + i + 64),
+            v3 = ld_stream(valp + p0 + i + 96);
+      float x0 = ld_x(x + c0), x1 = ld_x(x + c1), x2 = ld_x(x + c2), x3 = ld_x(x + c3);
+      prod[i] = __fmul_rn(v0, x0);
+      prod[i + 32] = __fmul_rn(v1, x1);
+      prod[i + 64] = __fmul_rn(v2, x2);
+      prod[i + 96] = __fmul_rn(v3, x3);
+    }
+    for (; i < n; i += 32) prod[i] = __fmul_rn(ld_stream(valp + p0 + i), ld_x(x + ld_stream(colp + p0 + i)));
+    __syncwarp();
+    for (int rb = r0; rb < r1; rb += 32) {
+      const int r = rb + lane;
+      const bool in = r < r1;
+      const int q0 = in ? __ldg(row_ptr + r) - p0 : 0;
+      const int len = in ? __ldg(row_ptr + r + 1) - p0 - q0 : 0;
+      if (in && len <= 32) {
+        float s = 0.f;
+        for (int q = q0; q < q0 + len; ++q) s = __fadd_rn(s, prod[q]);
+        pr_store<UPDATE>(y, r, lo, s, upd);
+      }
+      unsigned mask = __ballot_sync(0xffffffffu, in && len > 32);
+      while (mask) {
+        const int j = __ffs(mask) - 1;
+        mask &= mask - 1;
+        const int rq0 = __shfl_sync(0xffffffffu, q0, j), rlen = __shfl_sync(0xffffffffu, len, j);
+        float v = 0.f;
+        for (int q = lane; q < rlen; q += 32) v = __fadd_rn(v, prod[rq0 + q]);
+        v = butterfly(v);
+        if (lane == 0) pr_store<UPDATE>(y, rb + j, lo, v, upd);
+      }
+    }
+    __syncwarp();
   }
 }
 
-struct Graph {
-  const int* row_ptr;
-  const int* col;
-  const float* val;
-  const int* blocks;
-  int64_t v, nnz_off, nblocks, max_nnz;
-};
-
-// args: row_ptr, col, val, blocks, x, ... ; scalars at the end: V, nnz_off, nblocks, max_nnz
-Graph graph_args(LaunchCtx& c, uint32_t s0, const char* what) {
-  Graph g;
-  g.v = scalar_arg(c, s0, what);
-  g.nnz_off = scalar_arg(c, s0 + 1, what);
-  g.nblocks = scalar_arg(c, s0 + 2, what);
-  g.max_nnz = scalar_arg(c, s0 + 3, what);
-  if (g.v < 1 || g.v > INT32_MAX - 1) fail(ErrorCode::argument, std::string(what) + ": V out of range");
-  if (g.max_nnz < 1 || g.max_nnz > 12288) fail(ErrorCode::argument, std::string(what) + ": max_nnz must be in [1, 12288]");
-  const BufView& R = buffer_arg(c, 0, what);
-  if (R.first_byte != 0 || R.bytes != static_cast<uint64_t>(g.v + 1) * 4)
-    fail(ErrorCode::argument, std::string(what) + ": row_ptr must hold V+1 int32");
-  const BufView& B = buffer_arg(c, 3, what);
-  if (B.first_byte != 0 || B.bytes != static_cast<uint64_t>(g.nblocks + 1) * 4)
-    fail(ErrorCode::argument, std::string(what) + ": blocks must hold nblocks+1 int32");
-  const BufView& C = buffer_arg(c, 1, what);
-  const BufView& V = buffer_arg(c, 2, what);
-  if (C.bytes != V.bytes) fail(ErrorCode::argument, std::string(what) + ": col_idx and values differ in size");
-  g.row_ptr = reinterpret_cast<const int*>(R.ptr);
-  g.blocks = reinterpret_cast<const int*>(B.ptr);
-  g.col = reinterpret_cast<const int*>(C.ptr);
-  g.val = reinterpret_cast<const float*>(V.ptr);
-  if (C.first_byte != 0 || V.first_byte != 0)
-    fail(ErrorCode::argument, std::string(what) + ": col_idx/values must be whole buffers (use nnz_off for slices)");
-  return g;
+// long rows: fold the chunk totals in chunk order
+template <bool UPDATE>
+__global__ void pr_fixup_kernel(const int* __restrict__ long_rows, int n_long, const float* __restrict__ chunk_tot,
+                                const unsigned long long* __restrict__ dsum, float* __restrict__ y, int lo, int hi,
+                                float base, float damp, float inv_v) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_long) return;
+  const int row = long_rows[3 * i];
+  if (row < lo || row >= hi) return;
+  const int u0 = long_rows[3 * i + 1], nc = long_rows[3 * i + 2];
+  float total = chunk_tot[u0];
+  for (int c = 1; c < nc; ++c) total = __fadd_rn(total, chunk_tot[u0 + c]);
+  pr_store<UPDATE>(y, row, lo, total, pr_update<UPDATE>(dsum, base, damp, inv_v));
 }
 
+// args: row_ptr col val units long_rows x [dsum] y | V nnz_off n_units n_long warp_nnz
 template <bool UPDATE>
 uint64_t launch_pr(LaunchCtx& c) {
   const char* what = UPDATE ? "pagerank_step" : "pagerank_spmv";
-  // UPDATE: row_ptr col val blocks x dsum xnew | V nnz_off nblocks max_nnz
-  // SPMV  : row_ptr col val blocks x y         | V nnz_off nblocks max_nnz
-  const uint32_t s0 = UPDATE ? 7 : 6;
-  Graph g = graph_args(c, s0, what);
-  const BufView& X = buffer_arg(c, 4, what);
-  if (X.first_byte != 0 || X.bytes != static_cast<uint64_t>(g.v) * 4)
+  const uint32_t iy = UPDATE ? 7 : 6, s0 = iy + 1;
+  const int64_t v = scalar_arg(c, s0, what), nnz_off = scalar_arg(c, s0 + 1, what);
+  const int64_t n_units = scalar_arg(c, s0 + 2, what), n_long = scalar_arg(c, s0 + 3, what);
+  const int64_t warp_nnz = scalar_arg(c, s0 + 4, what);
+  if (v < 1 || v > INT32_MAX - 1) fail(ErrorCode::argument, std::string(what) + ": V out of range");
+  if (warp_nnz < 1 || warp_nnz > PR_CHUNK)
+    fail(ErrorCode::argument, std::string(what) + ": warp_nnz must be in [1, 4096]");
+  const BufView& R = buffer_arg(c, 0, what);
+  const BufView& Cb = buffer_arg(c, 1, what);
+  const BufView& Vb = buffer_arg(c, 2, what);
+  const BufView& U = buffer_arg(c, 3, what);
+  const BufView& L = buffer_arg(c, 4, what);
+  const BufView& X = buffer_arg(c, 5, what);
+  if (R.first_byte != 0 || R.bytes != static_cast<uint64_t>(v + 1) * 4)
+    fail(ErrorCode::argument, std::string(what) + ": row_ptr must hold V+1 int32");
+  if (U.bytes != static_cast<uint64_t>(n_units) * 16 || L.bytes < static_cast<uint64_t>(n_long) * 12)
+    fail(ErrorCode::argument, std::string(what) + ": units / long_rows sizes do not match their counts");
+  if (Cb.bytes != Vb.bytes || Cb.first_byte != 0 || Vb.first_byte != 0)
+    fail(ErrorCode::argument, std::string(what) + ": col_idx/values must be equal whole buffers (nnz_off for slices)");
+  if (X.first_byte != 0 || X.bytes != static_cast<uint64_t>(v) * 4)
     fail(ErrorCode::argument, std::string(what) + ": x must hold V floats");
   const unsigned long long* dsum = nullptr;
   if (UPDATE) {
-    const BufView& D = buffer_arg(c, 5, what);
+    const BufView& D = buffer_arg(c, 6, what);
     if (D.bytes != 8) fail(ErrorCode::argument, std::string(what) + ": dangling sum is one uint64");
     dsum = reinterpret_cast<const unsigned long long*>(D.ptr);
   }
   uint64_t lo, rows;
-  sub_range(c, static_cast<uint64_t>(g.v), lo, rows, what);
-  const BufView& Y = buffer_arg(c, UPDATE ? 6 : 5, what);
-  float* y = at_byte<float>(Y, lo * 4, rows * 4, what);
-  if (!rows) return 0;
-  // host-side checks need the nnz range of [lo, hi): two int32 reads
+  sub_range(c, static_cast<uint64_t>(v), lo, rows, what);
+  float* y = at_byte<float>(buffer_arg(c, iy, what), lo * 4, rows * 4, what);
+  if (!rows || !n_units) return 0;
+  const int* row_ptr = reinterpret_cast<const int*>(R.ptr);
+  // the non-zeros of [lo, hi) must be resident (two int32 reads)
   int rp[2];
-  HCL_CUDA(cudaMemcpyAsync(&rp[0], g.row_ptr + lo, 4, cudaMemcpyDeviceToHost, c.stream));
-  HCL_CUDA(cudaMemcpyAsync(&rp[1], g.row_ptr + lo + rows, 4, cudaMemcpyDeviceToHost, c.stream));
+  HCL_CUDA(cudaMemcpyAsync(&rp[0], row_ptr + lo, 4, cudaMemcpyDeviceToHost, c.stream));
+  HCL_CUDA(cudaMemcpyAsync(&rp[1], row_ptr + lo + rows, 4, cudaMemcpyDeviceToHost, c.stream));
   HCL_CUDA(cudaStreamSynchronize(c.stream));
-  const BufView& C = buffer_arg(c, 1, what);
-  if (rp[0] < g.nnz_off || static_cast<uint64_t>(rp[1] - g.nnz_off) * 4 > C.bytes)
+  if (rp[0] < nnz_off || static_cast<uint64_t>(rp[1] - nnz_off) * 4 > Cb.bytes)
     fail(ErrorCode::argument, std::string(what) + ": col_idx/values do not cover the rows' non-zeros");
-  const size_t smem = static_cast<size_t>(g.max_nnz) * 4;
-  auto kern = pr_spmv_kernel<UPDATE>;
+  float* chunk_tot = static_cast<float*>(c.scratch(c.dev, static_cast<size_t>(n_units) * 4));
+  const float base = static_cast<float>((1.0 - 0.85) / v), damp = 0.85f, inv_v = static_cast<float>(1.0 / v);
+  const size_t smem = static_cast<size_t>(warp_nnz) * 4 * PR_WARPS;
+  auto kern = pr_units_kernel<UPDATE>;
   HCL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   int per_sm = 0;
   HCL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, PR_T, smem));
   const int grid = std::max(1, per_sm) * c.sm_count;
-  kern<<<grid, PR_T, smem, c.stream>>>(g.row_ptr, g.col, g.val, g.nnz_off, g.blocks, static_cast<int>(g.nblocks),
+  kern<<<grid, PR_T, smem, c.stream>>>(row_ptr, reinterpret_cast<const int*>(Cb.ptr),
+                                       reinterpret_cast<const float*>(Vb.ptr), nnz_off,
+                                       reinterpret_cast<const int4*>(U.ptr), static_cast<int>(n_units),
                                        reinterpret_cast<const float*>(X.ptr), dsum, y, static_cast<int>(lo),
-                                       static_cast<int>(lo + rows), static_cast<float>((1.0 - 0.85) / g.v), 0.85f,
-                                       static_cast<float>(1.0 / g.v), static_cast<int>(g.max_nnz));
+                                       static_cast<int>(lo + rows), base, damp, inv_v, static_cast<int>(warp_nnz),
+                                       chunk_tot);
   HCL_LAUNCHED();
+  if (n_long) {
+    pr_fixup_kernel<UPDATE><<<static_cast<unsigned>(ceil_div(n_long, 128)), 128, 0, c.stream>>>(
+        reinterpret_cast<const int*>(L.ptr), static_cast<int>(n_long), chunk_tot, dsum, y, static_cast<int>(lo),
+        static_cast<int>(lo + rows), base, damp, inv_v);
+    HCL_LAUNCHED();
+  }
   return 2ull * static_cast<uint64_t>(rp[1] - rp[0]);
 }
 
@@ -215,7 +292,7 @@ uint64_t launch_pr_dangling(LaunchCtx& c) {
       O.bytes != static_cast<uint64_t>(v) * 4 || D.bytes != 8)
     fail(ErrorCode::argument, "pagerank_dangling: x, outdeg must hold V elements, dsum one uint64");
   HCL_CUDA(cudaMemsetAsync(D.ptr, 0, 8, c.stream));
-  int grid = c.sm_count * 4;
+  int grid = static_cast<int>(std::min<uint64_t>(c.sm_count * 8, ceil_div(v / 8 + 1, 256)));
   pr_dangling_kernel<<<grid, 256, 0, c.stream>>>(reinterpret_cast<const float*>(X.ptr),
                                                  reinterpret_cast<const int*>(O.ptr), v,
                                                  reinterpret_cast<unsigned long long*>(D.ptr));
@@ -223,19 +300,19 @@ uint64_t launch_pr_dangling(LaunchCtx& c) {
   return static_cast<uint64_t>(v);
 }
 
-uint64_t rows_pr(const int64_t* s, uint32_t n) { return static_cast<uint64_t>(s[n == 11 ? 7 : 6]); }
+uint64_t rows_pr(const int64_t* s, uint32_t n) { return static_cast<uint64_t>(s[n == 13 ? 8 : 7]); }
 
 }  // namespace
 
 void register_graph(std::vector<KernelDef>& r) {
   constexpr uint8_t S = HCL_ARG_SCALAR, I = HCL_ARG_IN, O = HCL_ARG_OUT;
   constexpr uint8_t N = HCL_PART_NONE, P = HCL_PART_REPLICATE, X = HCL_PART_SPLIT_ROWS;
-  // y = A x over rows [lo,hi)
-  r.push_back({"b200", "pagerank_spmv", {I, I, I, I, I, O, S, S, S, S}, {P, P, P, P, P, X, N, N, N, N},
+  // y = A x over rows [lo,hi): row_ptr col val units long_rows x y | V nnz_off n_units n_long warp_nnz
+  r.push_back({"b200", "pagerank_spmv", {I, I, I, I, I, I, O, S, S, S, S, S}, {P, P, P, P, P, P, X, N, N, N, N, N},
                launch_pr<false>, nullptr, rows_pr});
-  // x' = (1-d)/V + d (A x + dangling/V) over rows [lo,hi)
-  r.push_back({"b200", "pagerank_step", {I, I, I, I, I, I, O, S, S, S, S}, {P, P, P, P, P, P, X, N, N, N, N},
-               launch_pr<true>, nullptr, rows_pr});
+  // x' = (1-d)/V + d (A x + dangling/V): row_ptr col val units long_rows x dsum x' | V nnz_off n_units n_long warp_nnz
+  r.push_back({"b200", "pagerank_step", {I, I, I, I, I, I, I, O, S, S, S, S, S},
+               {P, P, P, P, P, P, P, X, N, N, N, N, N}, launch_pr<true>, nullptr, rows_pr});
   r.push_back({"b200", "pagerank_dangling", {I, I, O, S}, {P, P, P, N}, launch_pr_dangling, nullptr, nullptr});
 }
 

@@ -66,6 +66,23 @@ def pagerank_csr(scale: int, edges: int, seed: int, threads: int = 0):
     return row_ptr, col_idx, val, outdeg
 
 
+def pagerank_units(row_ptr: np.ndarray, warp_nnz: int):
+    """Warp work units of the PageRank SpMV: (units int32[n,4] {row0,row1,p0,p1},
+    long_rows int32[max(m,1),3] {row, first_unit, nchunks}, m)."""
+    import ctypes as C
+
+    rp = np.ascontiguousarray(row_ptr, np.int32)
+    nu, nl = C.c_int64(), C.c_int64()
+    rc = N.lib().hcl_pagerank_units(rp.ctypes.data, len(rp) - 1, warp_nnz, None, None, C.byref(nu), C.byref(nl))
+    if rc:
+        raise N.HaoclError(rc - N.HCL_ERR_BASE, "pagerank_units: warp_nnz must be in [1, 4096]")
+    units = np.empty((nu.value, 4), np.int32)
+    long_rows = np.empty((max(1, nl.value), 3), np.int32)
+    N.lib().hcl_pagerank_units(rp.ctypes.data, len(rp) - 1, warp_nnz, units.ctypes.data, long_rows.ctypes.data,
+                               C.byref(nu), C.byref(nl))
+    return units, long_rows, nl.value
+
+
 def csr_row_blocks(row_ptr: np.ndarray, max_nnz: int) -> np.ndarray:
     """CSR-adaptive row blocks: start rows of blocks of <= max_nnz non-zeros
     (a longer row is its own block); last entry = rows."""

@@ -1,13 +1,13 @@
 """PageRank over the partitioned NDRange (config C3).
 
 The caller side of the path: the graph lives in HBM as an int32/fp32 pull
-CSR; each iteration runs `pagerank_dangling` (exact fixed-point dangling mass)
-and `pagerank_step` (CSR-adaptive SpMV fused with the PageRank update) as a
-partitioned NDRange over the queues, split at nnz-balanced row boundaries
-(`spmv_partition_ranges`, the reference's kernels.cpp:300-321 generalised to
-weights). The rank vector is the step's SPLIT_ROWS output; the next
-iteration's REPLICATE input gathers it onto every device (peer-to-peer inside
-one process; NCCL allgather across processes, see bench.py).
+CSR plus the SpMV's warp work units; each iteration runs `pagerank_dangling`
+(exact fixed-point dangling mass) and `pagerank_step` (warp-unit SpMV fused
+with the PageRank update) as a partitioned NDRange over the queues, split at
+nnz-balanced row boundaries (`spmv_partition_ranges`, the reference's
+kernels.cpp:300-321 generalised to weights). The rank vector is the step's
+SPLIT_ROWS output; the next iteration's REPLICATE input gathers it onto every
+device (peer-to-peer inside one process; NCCL allgather across processes).
 """
 from __future__ import annotations
 
@@ -15,40 +15,41 @@ from typing import Optional, Sequence
 
 import numpy as np
 
-from .datagen import csr_row_blocks
+from .datagen import pagerank_units
 from .runtime import Handle, HostContext, spmv_partition_ranges
 
-DEFAULT_MAX_NNZ = 4096
+DEFAULT_WARP_NNZ = 1024
 
 
 class PageRank:
     def __init__(self, ctx: HostContext, queues: Sequence[Handle], row_ptr: np.ndarray, col_idx: np.ndarray,
-                 val: np.ndarray, outdeg: np.ndarray, max_nnz: int = DEFAULT_MAX_NNZ,
+                 val: np.ndarray, outdeg: np.ndarray, max_nnz: int = DEFAULT_WARP_NNZ,
                  weights: Optional[Sequence[int]] = None):
         self.ctx, self.queues = ctx, list(queues)
         self.v = len(row_ptr) - 1
         self.nnz = int(row_ptr[-1])
-        self.max_nnz = max_nnz
-        blocks = csr_row_blocks(row_ptr, max_nnz)
-        self.nblocks = len(blocks) - 1
+        self.warp_nnz = max_nnz
+        units, long_rows, n_long = pagerank_units(row_ptr, max_nnz)
+        self.n_units, self.n_long = len(units), n_long
         rp64 = np.ascontiguousarray(row_ptr, np.int64)
         self.bounds = [int(b) for b in spmv_partition_ranges(rp64, len(self.queues), weights)]
         q0 = self.queues[0]
         mk = ctx.create_buffer
-        self.b_rp, self.b_blocks = mk(row_ptr.nbytes), mk(blocks.nbytes)
+        self.b_rp, self.b_units, self.b_long = mk(row_ptr.nbytes), mk(units.nbytes), mk(long_rows.nbytes)
         self.b_col, self.b_val, self.b_deg = mk(col_idx.nbytes), mk(val.nbytes), mk(outdeg.nbytes)
         self.b_x = [mk(self.v * 4), mk(self.v * 4)]
         self.b_dsum = mk(8)
-        for b, a in ((self.b_rp, row_ptr), (self.b_blocks, blocks), (self.b_col, col_idx), (self.b_val, val),
-                     (self.b_deg, outdeg)):
+        for b, a in ((self.b_rp, row_ptr), (self.b_units, units), (self.b_long, long_rows), (self.b_col, col_idx),
+                     (self.b_val, val), (self.b_deg, outdeg)):
             ctx.enqueue_write_buffer(q0, b, np.ascontiguousarray(a))
         prog = ctx.create_program("b200")
         self.k_dang = ctx.create_kernel(prog, "pagerank_dangling")
         self.k_step = [ctx.create_kernel(prog, "pagerank_step") for _ in range(2)]
         self.k_spmv = ctx.create_kernel(prog, "pagerank_spmv")
+        self.tail = [self.v, 0, self.n_units, self.n_long, max_nnz]
         for i, kk in enumerate(self.k_step):  # step i reads x[i], writes x[1-i]
-            for j, a in enumerate([self.b_rp, self.b_col, self.b_val, self.b_blocks, self.b_x[i], self.b_dsum,
-                                   self.b_x[1 - i], self.v, 0, self.nblocks, max_nnz]):
+            for j, a in enumerate([self.b_rp, self.b_col, self.b_val, self.b_units, self.b_long, self.b_x[i],
+                                   self.b_dsum, self.b_x[1 - i]] + self.tail):
                 ctx.set_kernel_arg(kk, j, a)
         for j, a in enumerate([self.b_deg, self.b_dsum, self.v]):
             ctx.set_kernel_arg(self.k_dang, j + 1, a)
@@ -81,8 +82,7 @@ class PageRank:
         ctx = self.ctx
         bx, by = ctx.create_buffer(self.v * 4), ctx.create_buffer(self.v * 4)
         ctx.enqueue_write_buffer(self.queues[0], bx, np.ascontiguousarray(x, np.float32))
-        for j, a in enumerate([self.b_rp, self.b_col, self.b_val, self.b_blocks, bx, by, self.v, 0, self.nblocks,
-                               self.max_nnz]):
+        for j, a in enumerate([self.b_rp, self.b_col, self.b_val, self.b_units, self.b_long, bx, by] + self.tail):
             ctx.set_kernel_arg(self.k_spmv, j, a)
         ctx.enqueue_ndrange_partitioned(self.k_spmv, (self.v, 1, 1), 1, self.queues, bounds=self.bounds)
         self.finish()
@@ -92,5 +92,5 @@ class PageRank:
         return y
 
     def close(self) -> None:
-        for b in (self.b_rp, self.b_blocks, self.b_col, self.b_val, self.b_deg, self.b_dsum, *self.b_x):
+        for b in (self.b_rp, self.b_units, self.b_long, self.b_col, self.b_val, self.b_deg, self.b_dsum, *self.b_x):
             self.ctx.release(b)

@@ -18,7 +18,7 @@ scale = int(os.environ.get("PR_SCALE", "24"))
 t = time.time()
 g = G.pagerank_csr(scale, 16 << scale, 42)
 print(f"csr build {time.time() - t:.1f}s maxrow {np.diff(g[0]).max()} dangling {(g[3] == 0).sum()}", flush=True)
-for mx in (2048, 4096, 8192):
+for mx in (512, 1024, 2048):
     pr = PageRank(ctx, [q], *g, max_nnz=mx)
     pr.reset()
     pr.iterate(3)
