@@ -494,6 +494,12 @@ uint64_t rowbytes_gemm_f32(const int64_t* s, uint32_t, uint32_t i) {
 
 }  // namespace
 
+// shared with the implicit-GEMM conv (k_conv.cu)
+CUtensorMap make_tmap_2d_bf16(const void* base, uint64_t inner, uint64_t outer, uint64_t row_bytes, uint32_t box_inner,
+                              uint32_t box_outer) {
+  return make_tmap(base, false, inner, outer, row_bytes, box_inner, box_outer);
+}
+
 void register_gemm(std::vector<KernelDef>& r) {
   constexpr uint8_t S = HCL_ARG_SCALAR, I = HCL_ARG_IN, O = HCL_ARG_OUT;
   constexpr uint8_t N = HCL_PART_NONE, P = HCL_PART_REPLICATE, X = HCL_PART_SPLIT_ROWS;
