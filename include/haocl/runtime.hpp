@@ -263,6 +263,18 @@ class HostContext {
   std::vector<uint64_t> partition_plan(Handle kernel, std::array<uint64_t, 3> global_size,
                                        const std::vector<Handle>& queues, std::vector<uint64_t> weights = {});
 
+  // ---- collectives across processes (one GPU per rank, NCCL over NVLink) ----
+  // Join the communicator for the queue's device (unique id from rank 0).
+  void init_collectives(Handle queue, int rank, int nranks, const std::vector<uint8_t>& nccl_unique_id);
+  // Rank r holds bytes [bounds[r], bounds[r+1]) of `buffer` on the queue's
+  // device; afterwards every rank holds [bounds[0], bounds[nranks]) (uneven
+  // allgather: PageRank's rank vector).
+  void enqueue_allgather(Handle queue, Handle buffer, const std::vector<uint64_t>& byte_bounds);
+  // Element-wise int64 sum of every rank's copy (k-means centroid sums).
+  void enqueue_allreduce_sum_i64(Handle queue, Handle buffer);
+  // Root's bytes to every rank (GEMM B).
+  void enqueue_broadcast(Handle queue, Handle buffer, int root);
+
   std::pair<int, Handle> submit_task(const KernelTask& task);
   Handle launch_task(Handle queue, const KernelTask& task);
 

@@ -133,6 +133,15 @@ uint64_t hcl_kernel_launch_count(void);
 /* Raw CUDA stream of a device (cudaStream_t as void*), for event timing. */
 int hcl_device_stream(int dev, void** stream);
 
+/* ---- collectives (NCCL over NVLink 5 / NVSwitch, loaded lazily) ---------- */
+int hcl_nccl_unique_id(uint8_t* out, int cap); /* cap >= 128 */
+int hcl_nccl_init(int dev, int nranks, int rank, const uint8_t* id);
+int hcl_nccl_destroy(int dev);
+/* in place: rank r contributes bytes [bounds[r], bounds[r+1]) of the buffer */
+int hcl_allgatherv(int dev, uint64_t buffer_id, const uint64_t* bounds);
+int hcl_allreduce_sum_i64(int dev, uint64_t buffer_id, uint64_t offset, uint64_t count);
+int hcl_broadcast(int dev, uint64_t buffer_id, uint64_t offset, uint64_t bytes, int root);
+
 const char* hcl_last_error(void);
 
 #ifdef __cplusplus

@@ -59,6 +59,13 @@ int hcl_ctx_enqueue_ndrange_partitioned(hcl_context* ctx, uint64_t kernel, const
  * rank runs when the partitioned NDRange spans processes; OpenCL's global_work_offset). */
 int hcl_ctx_enqueue_ndrange_range(hcl_context* ctx, uint64_t queue, uint64_t kernel, const uint64_t global[3],
                                   uint32_t dims, uint64_t row_offset, uint64_t rows, uint64_t* event);
+/* Collectives when the partitioned NDRange spans processes (one GPU per rank,
+ * NCCL over NVLink; the id comes from hcl_nccl_unique_id on rank 0). */
+int hcl_ctx_init_collectives(hcl_context* ctx, uint64_t queue, int rank, int nranks, const uint8_t* nccl_id);
+/* rank r owns bytes [bounds[r], bounds[r+1]); afterwards all ranks hold the union */
+int hcl_ctx_enqueue_allgather(hcl_context* ctx, uint64_t queue, uint64_t buffer, const uint64_t* bounds, int nranks);
+int hcl_ctx_enqueue_allreduce_sum_i64(hcl_context* ctx, uint64_t queue, uint64_t buffer);
+int hcl_ctx_enqueue_broadcast(hcl_context* ctx, uint64_t queue, uint64_t buffer, int root);
 /* The row boundaries (nqueues+1) the partitioned launch would use. */
 int hcl_ctx_partition_plan(hcl_context* ctx, uint64_t kernel, const uint64_t global[3], const uint64_t* queues,
                            int nqueues, const uint64_t* weights, uint64_t* bounds);

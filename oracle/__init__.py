@@ -85,6 +85,7 @@ def lib():
         L.ho_kmeans_accumulate.argtypes = [_f32p, C.c_int64, C.c_int64, _i32p, C.c_int64, _i64p, _i64p]
         L.ho_kmeans_finalize.argtypes = [_i64p, _i64p, C.c_int64, C.c_int64, _f32p]
         L.ho_conv3x3_point.argtypes = [_u16p, _u16p] + [C.c_int64] * 8 + [_f64p]
+        L.ho_conv3x3_rows.argtypes = [_u16p, _u16p] + [C.c_int64] * 7 + [_f64p]
         _lib = L
     return _lib
 
@@ -319,6 +320,13 @@ def conv3x3_point(inp, w, h: int, wd: int, c: int, kout: int, n: int, y: int, x:
     lib().ho_conv3x3_point(_ptr(inp, _u16p), _ptr(w, _u16p), h, wd, c, kout, n, y, x, ko,
                            C.byref(out))
     return out.value
+
+
+def conv3x3_rows(inp, w, h: int, wd: int, c: int, kout: int, n: int, y0: int, y1: int) -> np.ndarray:
+    """fp64 direct conv of output rows [y0, y1) of image n: [y1-y0][wd][kout]."""
+    out = np.empty((y1 - y0) * wd * kout, np.float64)
+    lib().ho_conv3x3_rows(_ptr(inp, _u16p), _ptr(w, _u16p), h, wd, c, kout, n, y0, y1, _ptr(out, _f64p))
+    return out.reshape(y1 - y0, wd, kout)
 
 
 # --------------------------------------------------------------------------

@@ -591,11 +591,32 @@ void ho_kmeans_finalize(const int64_t* sums, const int64_t* counts, int64_t k, i
 
 /* Direct 3x3 conv, stride 1, pad 1, NHWC input, KRSC weights, fp64 accumulate
  * of exact bf16 products in fixed c -> r -> s order. One output element. */
+
 static inline double bf16_to_f64(uint16_t h) {
   uint32_t u = (uint32_t)h << 16;
   float f;
   memcpy(&f, &u, 4);
   return (double)f;
+}
+
+/* Output rows [y0, y1) of image n_img, all K channels, into out[(y - y0)][x][k]
+ * (same fixed c -> r -> s order as ho_conv3x3_point). */
+void ho_conv3x3_rows(const uint16_t* in_bf16, const uint16_t* w_bf16, int64_t h, int64_t w, int64_t c,
+                     int64_t kout, int64_t n_img, int64_t y0, int64_t y1, double* out) {
+  for (int64_t y = y0; y < y1; ++y)
+    for (int64_t x = 0; x < w; ++x)
+      for (int64_t ko = 0; ko < kout; ++ko) {
+        double acc = 0.0;
+        for (int64_t ci = 0; ci < c; ++ci)
+          for (int64_t r = 0; r < 3; ++r)
+            for (int64_t s = 0; s < 3; ++s) {
+              int64_t yy = y + r - 1, xx = x + s - 1;
+              if (yy < 0 || yy >= h || xx < 0 || xx >= w) continue;
+              acc += bf16_to_f64(in_bf16[((n_img * h + yy) * w + xx) * c + ci]) *
+                     bf16_to_f64(w_bf16[((ko * 3 + r) * 3 + s) * c + ci]);
+            }
+        out[((y - y0) * w + x) * kout + ko] = acc;
+      }
 }
 
 void ho_conv3x3_point(const uint16_t* in_bf16, const uint16_t* w_bf16, int64_t h, int64_t w,

@@ -83,6 +83,8 @@ void ho_kmeans_finalize(const int64_t* sums, const int64_t* counts, int64_t k, i
 void ho_conv3x3_point(const uint16_t* in_bf16, const uint16_t* w_bf16, int64_t h, int64_t w,
                       int64_t c, int64_t kout, int64_t n_img, int64_t y, int64_t x, int64_t ko,
                       double* out);
+void ho_conv3x3_rows(const uint16_t* in_bf16, const uint16_t* w_bf16, int64_t h, int64_t w, int64_t c,
+                     int64_t kout, int64_t n_img, int64_t y0, int64_t y1, double* out);
 void ho_gen_bf16(uint16_t* out, size_t count, uint64_t seed);
 
 #ifdef __cplusplus

@@ -55,6 +55,12 @@ CABI = [
     ("hcl_finish", C.c_int, [C.c_int, f64p]),
     ("hcl_kernel_launch_count", C.c_uint64, []),
     ("hcl_device_stream", C.c_int, [C.c_int, C.POINTER(C.c_void_p)]),
+    ("hcl_nccl_unique_id", C.c_int, [u8p, C.c_int]),
+    ("hcl_nccl_init", C.c_int, [C.c_int, C.c_int, C.c_int, u8p]),
+    ("hcl_nccl_destroy", C.c_int, [C.c_int]),
+    ("hcl_allgatherv", C.c_int, [C.c_int, C.c_uint64, u64p]),
+    ("hcl_allreduce_sum_i64", C.c_int, [C.c_int, C.c_uint64, C.c_uint64, C.c_uint64]),
+    ("hcl_broadcast", C.c_int, [C.c_int, C.c_uint64, C.c_uint64, C.c_uint64, C.c_int]),
     ("hcl_last_error", C.c_char_p, []),
 ]
 
@@ -77,6 +83,10 @@ HOST = [
                                                       u64p, u64p, u64p]),
     ("hcl_ctx_enqueue_ndrange_range", C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, u64p, C.c_uint32,
                                                 C.c_uint64, C.c_uint64, u64p]),
+    ("hcl_ctx_init_collectives", C.c_int, [C.c_void_p, C.c_uint64, C.c_int, C.c_int, u8p]),
+    ("hcl_ctx_enqueue_allgather", C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, u64p, C.c_int]),
+    ("hcl_ctx_enqueue_allreduce_sum_i64", C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64]),
+    ("hcl_ctx_enqueue_broadcast", C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_int]),
     ("hcl_ctx_partition_plan", C.c_int, [C.c_void_p, C.c_uint64, u64p, u64p, C.c_int, u64p, u64p]),
     ("hcl_ctx_submit_task", C.c_int, [C.c_void_p, C.c_char_p, u8p, i64p, C.c_int, C.c_char_p, C.c_int, i32p,
                                       u64p]),

@@ -711,6 +711,57 @@ Handle HostContext::enqueue_ndrange_range(Handle queue, Handle kernel, std::arra
   return impl_->launch_parts(k, args, global_size, dims, {{q.gid, queue.id, row_offset, row_offset + rows}}, false);
 }
 
+}  // namespace haocl
+
+extern "C" {
+int hcl_nccl_init(int dev, int nranks, int rank, const uint8_t* id_bytes);
+int hcl_allgatherv(int dev, uint64_t buffer_id, const uint64_t* bounds);
+int hcl_allreduce_sum_i64(int dev, uint64_t buffer_id, uint64_t offset, uint64_t count);
+int hcl_broadcast(int dev, uint64_t buffer_id, uint64_t offset, uint64_t bytes, int root);
+}
+
+namespace haocl {
+
+void HostContext::init_collectives(Handle queue, int rank, int nranks, const std::vector<uint8_t>& id) {
+  std::lock_guard lock(impl_->mu);
+  Impl::QueueRec& q = impl_->queue(queue.id);
+  if (id.size() < 128) fail(ErrorCode::argument, "NCCL unique id is 128 bytes");
+  check(hcl_nccl_init(impl_->dev_index(q.gid), nranks, rank, id.data()));
+}
+
+void HostContext::enqueue_allgather(Handle queue, Handle buffer, const std::vector<uint64_t>& bounds) {
+  std::lock_guard lock(impl_->mu);
+  Impl::QueueRec& q = impl_->queue(queue.id);
+  Impl::BufferRec& b = impl_->buffer(buffer.id);
+  if (bounds.size() < 2 || bounds.back() > b.size) fail(ErrorCode::argument, "allgather bounds exceed the buffer");
+  auto started = Clock::now();
+  Impl::Piece& p = impl_->ensure_alloc(buffer.id, b, q.gid, bounds.front(), bounds.back() - bounds.front());
+  impl_->trace.record({q.gid, "allgather", buffer.id});
+  check(hcl_allgatherv(impl_->dev_index(q.gid), buffer.id, bounds.data()));
+  Impl::set_valid(p, bounds.front(), bounds.back() - bounds.front());
+  impl_->add_transfer(&q, ms_since(started));
+}
+
+void HostContext::enqueue_allreduce_sum_i64(Handle queue, Handle buffer) {
+  std::lock_guard lock(impl_->mu);
+  Impl::QueueRec& q = impl_->queue(queue.id);
+  Impl::BufferRec& b = impl_->buffer(buffer.id);
+  impl_->ensure_valid(buffer.id, b, q.gid, 0, b.size, &q);
+  impl_->trace.record({q.gid, "allreduce", buffer.id});
+  check(hcl_allreduce_sum_i64(impl_->dev_index(q.gid), buffer.id, 0, b.size / 8));
+}
+
+void HostContext::enqueue_broadcast(Handle queue, Handle buffer, int root) {
+  std::lock_guard lock(impl_->mu);
+  Impl::QueueRec& q = impl_->queue(queue.id);
+  Impl::BufferRec& b = impl_->buffer(buffer.id);
+  Impl::Piece& p = impl_->ensure_alloc(buffer.id, b, q.gid, 0, b.size);
+  impl_->trace.record({q.gid, "broadcast", buffer.id});
+  check(hcl_broadcast(impl_->dev_index(q.gid), buffer.id, 0, b.size, root));
+  p.valid_first = 0;
+  p.valid_bytes = b.size;
+}
+
 std::pair<int, Handle> HostContext::submit_task(const KernelTask& task) {
   std::lock_guard lock(impl_->mu);
   Impl::KernelRec k = impl_->temp_kernel(task.kernel_name);
@@ -976,6 +1027,24 @@ int hcl_ctx_enqueue_ndrange_range(hcl_context* ctx, uint64_t queue, uint64_t ker
                                              {global[0], global[1], global[2]}, dims, row_offset, rows);
     if (event) *event = ev.id;
   });
+}
+int hcl_ctx_init_collectives(hcl_context* ctx, uint64_t queue, int rank, int nranks, const uint8_t* id) {
+  return ctx_guarded([&] {
+    ctx->ctx.init_collectives(H(HandleKind::queue, queue), rank, nranks, std::vector<uint8_t>(id, id + 128));
+  });
+}
+int hcl_ctx_enqueue_allgather(hcl_context* ctx, uint64_t queue, uint64_t buffer, const uint64_t* bounds,
+                              int nranks) {
+  return ctx_guarded([&] {
+    ctx->ctx.enqueue_allgather(H(HandleKind::queue, queue), H(HandleKind::buffer, buffer),
+                               std::vector<uint64_t>(bounds, bounds + nranks + 1));
+  });
+}
+int hcl_ctx_enqueue_allreduce_sum_i64(hcl_context* ctx, uint64_t queue, uint64_t buffer) {
+  return ctx_guarded([&] { ctx->ctx.enqueue_allreduce_sum_i64(H(HandleKind::queue, queue), H(HandleKind::buffer, buffer)); });
+}
+int hcl_ctx_enqueue_broadcast(hcl_context* ctx, uint64_t queue, uint64_t buffer, int root) {
+  return ctx_guarded([&] { ctx->ctx.enqueue_broadcast(H(HandleKind::queue, queue), H(HandleKind::buffer, buffer), root); });
 }
 int hcl_ctx_partition_plan(hcl_context* ctx, uint64_t kernel, const uint64_t global[3], const uint64_t* queues,
                            int nqueues, const uint64_t* weights, uint64_t* bounds) {

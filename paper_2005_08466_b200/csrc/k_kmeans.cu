@@ -264,7 +264,49 @@ uint64_t launch_add_i64(LaunchCtx& c) {
   return static_cast<uint64_t>(n);
 }
 
+// Device-side synthetic points, bit-identical to hcl_gen_kmeans_points (host)
+// and oracle ho_kmeans_points: counter-based SplitMix64, so a partitioned
+// launch generates each rank's rows in place.
+__device__ __forceinline__ uint64_t sm_at(uint64_t seed, uint64_t i) {
+  uint64_t z = seed + (i + 1) * 0x9e3779b97f4a7c15ULL;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+
+__global__ void gen_points_kernel(float* __restrict__ out, uint64_t first, uint64_t count, int d, uint64_t blobs,
+                                  uint64_t seed) {
+  const uint64_t total = count * d;
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < total; e += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t i = first + e / d, j = e % d;
+    const uint64_t b = sm_at(seed ^ 0xB10BULL, i) % blobs;
+    const int64_t c = static_cast<int64_t>(sm_at(seed ^ 0xCE47E2ULL, b * d + j) >> 49) - 16384;
+    const uint64_t r = sm_at(seed, i * d + j);
+    const int64_t nsum = static_cast<int64_t>(r & 0xffff) + static_cast<int64_t>((r >> 16) & 0xffff) +
+                         static_cast<int64_t>((r >> 32) & 0xffff) + static_cast<int64_t>(r >> 48) - 131070;
+    int64_t q = c + (nsum >> 5);
+    q = q < -32768 ? -32768 : (q > 32767 ? 32767 : q);
+    out[e] = static_cast<float>(q) * 0x1p-12f;
+  }
+}
+
+// gen_kmeans_points(points(out), N, D, blobs, seed)
+uint64_t launch_gen_points(LaunchCtx& c) {
+  int64_t n = scalar_arg(c, 1, "gen_kmeans_points N"), d = scalar_arg(c, 2, "gen_kmeans_points D");
+  int64_t blobs = scalar_arg(c, 3, "gen_kmeans_points blobs"), seed = scalar_arg(c, 4, "gen_kmeans_points seed");
+  if (n < 0 || d < 1 || blobs < 1) fail(ErrorCode::argument, "gen_kmeans_points: bad N/D/blobs");
+  uint64_t lo, rows;
+  sub_range(c, static_cast<uint64_t>(n), lo, rows, "gen_kmeans_points");
+  float* out = at_byte<float>(buffer_arg(c, 0, "gen_kmeans_points out"), lo * d * 4, rows * d * 4, "gen points");
+  if (!rows) return 0;
+  gen_points_kernel<<<c.sm_count * 16, 256, 0, c.stream>>>(out, lo, rows, static_cast<int>(d),
+                                                           static_cast<uint64_t>(blobs), static_cast<uint64_t>(seed));
+  HCL_LAUNCHED();
+  return rows * static_cast<uint64_t>(d);
+}
+
 uint64_t rows_km(const int64_t* s, uint32_t n) { return static_cast<uint64_t>(s[n == 6 ? 3 : 4]); }
+uint64_t rows_gen(const int64_t* s, uint32_t) { return static_cast<uint64_t>(s[1]); }
 
 }  // namespace
 
@@ -276,6 +318,7 @@ void register_kmeans(std::vector<KernelDef>& r) {
                rows_km});
   r.push_back({"b200", "kmeans_finalize", {I, I, IO, S, S}, {P, P, P, N, N}, launch_finalize, nullptr, nullptr});
   r.push_back({"b200", "reduce_add_i64", {IO, I, S}, {P, P, N}, launch_add_i64, nullptr, nullptr});
+  r.push_back({"b200", "gen_kmeans_points", {O, S, S, S, S}, {X, N, N, N, N}, launch_gen_points, nullptr, rows_gen});
 }
 
 }  // namespace hcl

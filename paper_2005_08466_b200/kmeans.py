@@ -50,6 +50,18 @@ class KMeans:
                 self.ctx.enqueue_write_buffer(q, self.b_pts, flat[lo * self.d:hi * self.d], offset=lo * self.d * 4)
         self.bounds = list(bounds)
 
+    def generate_points(self, seed: int, blobs: int, bounds: Optional[Sequence[int]] = None) -> None:
+        """Generate the synthetic points in HBM (each queue's rows on its device),
+        bit-identical to datagen.gen_kmeans_points."""
+        if bounds is None:
+            bounds = self.ctx.partition_plan(self.k_assign, (self.n, 1, 1), self.queues, self.weights)
+        prog = self.ctx.create_program("b200")
+        kg = self.ctx.create_kernel(prog, "gen_kmeans_points")
+        for j, a in enumerate([self.b_pts, self.n, self.d, blobs, seed]):
+            self.ctx.set_kernel_arg(kg, j, a)
+        self.ctx.enqueue_ndrange_partitioned(kg, (self.n, 1, 1), 1, self.queues, bounds=bounds)
+        self.bounds = list(bounds)
+
     def set_centroids(self, cent: np.ndarray) -> None:
         self.ctx.enqueue_write_buffer(self.queues[0], self.b_cent, np.ascontiguousarray(cent, np.float32))
 

@@ -198,6 +198,27 @@ class HostContext:
                                                     C.byref(ev)))
         return Handle(HandleKind.event, ev.value)
 
+    # -- collectives across processes (one GPU per rank) --------------------
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        buf = (C.c_uint8 * 128)()
+        check(N.lib().hcl_nccl_unique_id(buf, 128))
+        return bytes(buf)
+
+    def init_collectives(self, queue: Handle, rank: int, nranks: int, unique_id: bytes) -> None:
+        ident = (C.c_uint8 * 128)(*unique_id[:128])
+        check(self._L.hcl_ctx_init_collectives(self._ctx, queue.id, rank, nranks, ident))
+
+    def enqueue_allgather(self, queue: Handle, buffer: Handle, byte_bounds: Sequence[int]) -> None:
+        b = (C.c_uint64 * len(byte_bounds))(*[int(x) for x in byte_bounds])
+        check(self._L.hcl_ctx_enqueue_allgather(self._ctx, queue.id, buffer.id, b, len(byte_bounds) - 1))
+
+    def enqueue_allreduce_sum_i64(self, queue: Handle, buffer: Handle) -> None:
+        check(self._L.hcl_ctx_enqueue_allreduce_sum_i64(self._ctx, queue.id, buffer.id))
+
+    def enqueue_broadcast(self, queue: Handle, buffer: Handle, root: int) -> None:
+        check(self._L.hcl_ctx_enqueue_broadcast(self._ctx, queue.id, buffer.id, root))
+
     def partition_plan(self, kernel: Handle, global_size, queues: Sequence[Handle],
                        weights: Optional[Sequence[int]] = None) -> list[int]:
         g = (C.c_uint64 * 3)(*global_size)

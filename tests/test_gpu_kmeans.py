@@ -88,3 +88,15 @@ def test_partition_invariance(ctx, queues, weights):
         outs.append((km.centroids().tobytes(), km.assignments().tobytes()))
         km.close()
     assert outs[0] == outs[1] == outs[2]
+
+
+def test_device_point_generator_matches_host(ctx, queues):
+    from paper_2005_08466_b200.kmeans import KMeans
+
+    n, d, k = 10000, 32, 16
+    km = KMeans(ctx, queues[:3], n, d, k)
+    km.generate_points(42, 1024)
+    km.finish()
+    got = ctx.enqueue_read_buffer(queues[0], km.b_pts).view(np.float32)
+    km.close()
+    assert (got == G.gen_kmeans_points(n, d, 1024, 42)).all()
