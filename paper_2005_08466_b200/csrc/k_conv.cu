@@ -4,23 +4,34 @@
 //   weights : KRSC bf16, [K][3][3][C] = a K x 9C matrix
 //   output  : NHWK, bf16 or fp32, [N][H][W][K]
 // Implicit-GEMM trick: compute outputs on the "virtual" pixel grid of the padded
-// image, p = h*(W+2) + w with w in [0, W+2): then the input pixel read by tap
-// (r,s) is p + r*(W+2) + s — a uniform row shift of the flattened padded input —
-// so every A tile is one plain 2D TMA box of 128 consecutive rows x 64 channels
+// image, p = h*(W+2) + w with w in [0, W+2): the input pixel read by tap (r,s) is
+// then p + r*(W+2) + s — a uniform row shift of the flattened padded input — so
+// an A tile is one plain 2D TMA box of consecutive rows x 64 channels
 // (SWIZZLE_128B, exactly the GEMM's K-major operand). The two junk columns per
 // image row (w >= W) are computed and not stored (0.9% extra MMA work).
+//
 // Kernel structure = csrc/k_gemm.cu: persistent CTA pairs (cta_group::2, UMMA
-// 256 x K x 16), warp 4 TMA producer, warp 5 MMA issuer, warps 0-3 epilogue,
-// 8-stage smem ring, two TMEM accumulators. A pair tile is 256 consecutive
-// virtual pixels of one image; K loop = 9 taps x C/64.
-// The NDRange is the batch: a partitioned launch splits images (SPLIT_ROWS on
-// input and output), weights are REPLICATE.
+// 256 x 128 x 16), a TMA producer warp, an MMA issuer warp, epilogue warps, an
+// smem ring, two TMEM accumulators (2 x 128 columns). A pair tile is 256
+// consecutive virtual pixels of one image.
+//   v2 (C == 64, default): the weights stay resident in shared memory (each CTA
+//     holds its 64 output channels x 9 taps = 72 KB, loaded once), and one A
+//     load per filter row r (136 consecutive padded pixels) feeds the three taps
+//     s = 0,1,2 through descriptors that start s rows (s*128 bytes) further into
+//     the swizzled tile. Measured on B200: the UMMA's 128B swizzle is address
+//     based like TMA's, so the descriptor base-offset field stays 0 (setting it
+//     to the row phase gives wrong results). 8 epilogue warps (two per TMEM lane
+//     quadrant) keep the short K = 576 main loop fed.
+//   v1 (any C multiple of 64): one A and one B TMA load per tap and 64-channel
+//     chunk, 4 epilogue warps.
+// The NDRange is the batch: a partitioned launch splits images (SPLIT_ROWS input
+// and output), weights are REPLICATE.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
-#include <mutex>
+#include <cstdlib>
 #include <string>
 
 #include "common.hpp"
@@ -35,103 +46,178 @@ CUtensorMap make_tmap_2d_bf16(const void* base, uint64_t inner, uint64_t outer, 
 
 namespace {
 
-constexpr int CV_BM = 128;               // pixels per CTA tile
-constexpr int CV_BN = 128;               // output channels (UMMA N)
-constexpr int CV_BNL = CV_BN / 2;        // B rows per CTA
-constexpr int CV_A = CV_BM * 128;        // 16 KB
-constexpr int CV_B = CV_BNL * 128;       // 8 KB
-constexpr int CV_STAGE = CV_A + CV_B;
-constexpr int CV_STAGES = 8;
-constexpr int CV_THREADS = 192;
-constexpr int CV_TMEM = 256;             // 2 accumulators x 128 columns
-constexpr size_t CV_SMEM = static_cast<size_t>(CV_STAGES) * CV_STAGE + 1024 + 256;
+constexpr int CV_BM = 128;          // pixels per CTA tile (TMEM lanes)
+constexpr int CV_BN = 128;          // output channels (UMMA N)
+constexpr int CV_BNL = CV_BN / 2;   // B rows per CTA
+constexpr int CV_TMEM = 256;        // 2 accumulators x 128 columns
+
+// v1
+constexpr int CV1_A = CV_BM * 128;  // 16 KB
+constexpr int CV1_B = CV_BNL * 128; // 8 KB
+constexpr int CV1_STAGE = CV1_A + CV1_B;
+constexpr int CV1_STAGES = 8;
+constexpr int CV1_EPI = 4;          // epilogue warps 0-3, producer 4, MMA 5
+constexpr size_t CV1_SMEM = static_cast<size_t>(CV1_STAGES) * CV1_STAGE + 1024 + 256;
+
+// v2
+constexpr int CV2_AROWS = 136;              // 128 pixels + 2 shifted rows, padded to 8
+constexpr int CV2_A = CV2_AROWS * 128;      // 17 KB
+constexpr int CV2_BTAP = CV_BNL * 128;      // 8 KB per tap per CTA
+constexpr int CV2_B = 9 * CV2_BTAP;         // 72 KB
+constexpr int CV2_STAGES = 8;
+constexpr int CV2_EPI = 8;                  // epilogue warps 0-7, producer 8, MMA 9
+constexpr size_t CV2_SMEM = static_cast<size_t>(CV2_B) + static_cast<size_t>(CV2_STAGES) * CV2_A + 1024 + 256;
+
+// One epilogue warp's share of a finished 128-pixel x 128-channel accumulator:
+// TMEM lane quadrant warp%4 (32 pixels), channel chunks [c0, c1) of 32.
+template <bool OUTF32>
+__device__ __forceinline__ void conv_epilogue(uint32_t tmem_base, int acc, int warp, int c0, int c1, bool ok,
+                                              int64_t opix, void* __restrict__ out) {
+#pragma unroll 1
+  for (int chunk = c0; chunk < c1; ++chunk) {
+    uint32_t r[32];
+    ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>((warp % 4) * 32) << 16) +
+                                static_cast<uint32_t>(acc * CV_BN + chunk * 32),
+                            r);
+    ptx::tmem_ld_wait();
+    if (!ok) continue;
+    if constexpr (OUTF32) {
+      uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<float*>(out) + opix * CV_BN + chunk * 32);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) dst[j] = make_uint4(r[4 * j], r[4 * j + 1], r[4 * j + 2], r[4 * j + 3]);
+    } else {
+      uint32_t pk[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        __nv_bfloat162 b2 = __floats2bfloat162_rn(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1]));
+        pk[j] = *reinterpret_cast<uint32_t*>(&b2);
+      }
+      uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(out) + opix * CV_BN + chunk * 32);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) dst[j] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+    }
+  }
+}
+
+struct ConvGeom {
+  int Wp, m_img, tiles_img, tiles;
+  int64_t img_rows;
+  __device__ ConvGeom(int n_img, int H, int W) {
+    Wp = W + 2;
+    img_rows = static_cast<int64_t>(H + 2) * Wp;
+    m_img = H * Wp;
+    tiles_img = (m_img + 2 * CV_BM - 1) / (2 * CV_BM);
+    tiles = n_img * tiles_img;
+  }
+};
+
+// Epilogue warps' loop over this cluster's tiles (shared by v1 and v2).
+template <bool OUTF32, int EPI>
+__device__ __forceinline__ void conv_epilogue_loop(const ConvGeom& g, int H, int W, uint32_t rank, int warp, int lane,
+                                                   uint32_t tmem_base, uint64_t* tfull, uint64_t* tempty,
+                                                   void* __restrict__ out) {
+  const int cluster = blockIdx.x / 2, nclusters = gridDim.x / 2;
+  const int c0 = EPI == 8 ? (warp / 4) * 2 : 0, c1 = EPI == 8 ? c0 + 2 : 4;
+  int acc = 0;
+  uint32_t acc_phase = 0;
+  for (int t = cluster; t < g.tiles; t += nclusters) {
+    const int n = t / g.tiles_img;
+    const int p = (t % g.tiles_img) * 2 * CV_BM + static_cast<int>(rank) * CV_BM + (warp % 4) * 32 + lane;
+    const int h = p / g.Wp, w = p - h * g.Wp;
+    const bool ok = p < g.m_img && w < W;
+    const int64_t opix = (static_cast<int64_t>(n) * H + h) * W + w;
+    ptx::mbar_wait(&tfull[acc], acc_phase);
+    ptx::tc_fence_after();
+    conv_epilogue<OUTF32>(tmem_base, acc, warp, c0, c1, ok, opix, out);
+    ptx::tc_fence_before();
+    __syncwarp();
+    if (lane == 0) ptx::mbar_arrive_cluster_relaxed(ptx::mapa(ptx::smem_u32(&tempty[acc]), 0));
+    if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+  }
+}
 
 template <bool OUTF32>
-__global__ void __launch_bounds__(CV_THREADS, 1)
-    conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+__global__ void __launch_bounds__((CV1_EPI + 2) * 32, 1)
+    conv3x3_v1_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                       void* __restrict__ out, int n_img, int H, int W, int C) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + CV_STAGES * CV_STAGE);
-  uint64_t* empty = full + CV_STAGES;
-  uint64_t* tfull = empty + CV_STAGES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + CV1_STAGES * CV1_STAGE);
+  uint64_t* empty = full + CV1_STAGES;
+  uint64_t* tfull = empty + CV1_STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  constexpr int PROD = CV1_EPI, MMA = CV1_EPI + 1;
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const uint32_t rank = ptx::cluster_ctarank();
-  const int Wp = W + 2;
-  const int64_t img_rows = static_cast<int64_t>(H + 2) * Wp;  // padded pixels per image
-  const int m_img = H * Wp;                                    // virtual output pixels per image
-  const int tiles_img = (m_img + 2 * CV_BM - 1) / (2 * CV_BM);
-  const int tiles = n_img * tiles_img;
-  const int cb = C / 64;
-  const int nk = 9 * cb;
+  const ConvGeom g(n_img, H, W);
+  const int cb = C / 64, nk = 9 * cb;
 
-  if (warp == 4 && lane == 0) {
+  if (warp == PROD && lane == 0) {
     ptx::prefetch_tmap(&tmA);
     ptx::prefetch_tmap(&tmB);
-    for (int s = 0; s < CV_STAGES; ++s) {
+    for (int s = 0; s < CV1_STAGES; ++s) {
       ptx::mbar_init(&full[s], 1);
       ptx::mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
       ptx::mbar_init(&tfull[a], 1);
-      ptx::mbar_init(&tempty[a], 8);
+      ptx::mbar_init(&tempty[a], 2 * CV1_EPI);
     }
     ptx::fence_mbar_init();
   }
-  if (warp == 5) ptx::tmem_alloc<2>(tmem_slot, CV_TMEM);
+  if (warp == MMA) ptx::tmem_alloc<2>(tmem_slot, CV_TMEM);
   ptx::tc_fence_before();
   ptx::cluster_sync();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   const int cluster = blockIdx.x / 2, nclusters = gridDim.x / 2;
 
-  if (warp == 4) {
+  if (warp == PROD) {
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = cluster; t < tiles; t += nclusters) {
-        const int n = t / tiles_img;
-        const int p0 = (t % tiles_img) * 2 * CV_BM + static_cast<int>(rank) * CV_BM;
-        const int64_t arow = static_cast<int64_t>(n) * img_rows + p0;
+      for (int t = cluster; t < g.tiles; t += nclusters) {
+        const int n = t / g.tiles_img;
+        const int p0 = (t % g.tiles_img) * 2 * CV_BM + static_cast<int>(rank) * CV_BM;
+        const int64_t arow = static_cast<int64_t>(n) * g.img_rows + p0;
         for (int kb = 0; kb < nk; ++kb) {
           const int tap = kb / cb, c0 = (kb % cb) * 64;
           const int r = tap / 3, s = tap % 3;
           ptx::mbar_wait(&empty[stage], phase ^ 1);
-          uint8_t* sa = smem + stage * CV_STAGE;
-          if (rank == 0) ptx::mbar_arrive_expect_tx(&full[stage], CV_STAGE * 2);
+          uint8_t* sa = smem + stage * CV1_STAGE;
+          if (rank == 0) ptx::mbar_arrive_expect_tx(&full[stage], CV1_STAGE * 2);
           const uint32_t bar = ptx::mapa(ptx::smem_u32(&full[stage]), 0);
-          ptx::tma_load_2d_pair(sa, &tmA, bar, c0, static_cast<int>(arow + r * Wp + s));
-          ptx::tma_load_2d_pair(sa + CV_A, &tmB, bar, tap * C + c0, static_cast<int>(rank) * CV_BNL);
-          if (++stage == CV_STAGES) { stage = 0; phase ^= 1; }
+          ptx::tma_load_2d_pair(sa, &tmA, bar, c0, static_cast<int>(arow + r * g.Wp + s));
+          ptx::tma_load_2d_pair(sa + CV1_A, &tmB, bar, tap * C + c0, static_cast<int>(rank) * CV_BNL);
+          if (++stage == CV1_STAGES) { stage = 0; phase ^= 1; }
         }
       }
     }
     __syncwarp();
-  } else if (warp == 5) {
+  } else if (warp == MMA) {
     if (rank == 0 && lane == 0) {
       constexpr uint32_t idesc = ptx::umma_idesc(1, 0, 0, 2 * CV_BM, CV_BN);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int t = cluster; t < tiles; t += nclusters) {
+      for (int t = cluster; t < g.tiles; t += nclusters) {
         ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
         ptx::tc_fence_after();
         const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * CV_BN);
         for (int kb = 0; kb < nk; ++kb) {
           ptx::mbar_wait(&full[stage], phase);
           ptx::tc_fence_after();
-          const uint32_t a_addr = ptx::smem_u32(smem + stage * CV_STAGE);
-          const uint32_t b_addr = a_addr + CV_A;
+          const uint32_t a_addr = ptx::smem_u32(smem + stage * CV1_STAGE);
+          const uint32_t b_addr = a_addr + CV1_A;
 #pragma unroll
           for (int k = 0; k < 4; ++k)
             ptx::mma<2, false>(d_tmem, ptx::umma_desc_sw128(a_addr + k * 32, 16, 1024),
                                ptx::umma_desc_sw128(b_addr + k * 32, 16, 1024), idesc, (kb | k) != 0);
           ptx::mma_commit<2>(&empty[stage]);
-          if (++stage == CV_STAGES) { stage = 0; phase ^= 1; }
+          if (++stage == CV1_STAGES) { stage = 0; phase ^= 1; }
         }
         ptx::mma_commit<2>(&tfull[acc]);
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
@@ -139,50 +225,122 @@ __global__ void __launch_bounds__(CV_THREADS, 1)
     }
     __syncwarp();
   } else {
-    int acc = 0;
-    uint32_t acc_phase = 0;
-    for (int t = cluster; t < tiles; t += nclusters) {
-      const int n = t / tiles_img;
-      const int p = (t % tiles_img) * 2 * CV_BM + static_cast<int>(rank) * CV_BM + warp * 32 + lane;
-      const int h = p / Wp, w = p - h * Wp;
-      const bool ok = p < m_img && w < W;
-      const int64_t opix = (static_cast<int64_t>(n) * H + h) * W + w;
-      ptx::mbar_wait(&tfull[acc], acc_phase);
-      ptx::tc_fence_after();
-#pragma unroll 1
-      for (int chunk = 0; chunk < CV_BN / 32; ++chunk) {
-        uint32_t r[32];
-        ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(warp * 32) << 16) +
-                                    static_cast<uint32_t>(acc * CV_BN + chunk * 32),
-                                r);
-        ptx::tmem_ld_wait();
-        if (!ok) continue;
-        if constexpr (OUTF32) {
-          uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<float*>(out) + opix * CV_BN + chunk * 32);
-#pragma unroll
-          for (int j = 0; j < 8; ++j) dst[j] = make_uint4(r[4 * j], r[4 * j + 1], r[4 * j + 2], r[4 * j + 3]);
-        } else {
-          uint32_t pk[16];
-#pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            __nv_bfloat162 b2 = __floats2bfloat162_rn(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1]));
-            pk[j] = *reinterpret_cast<uint32_t*>(&b2);
-          }
-          uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(out) + opix * CV_BN + chunk * 32);
-#pragma unroll
-          for (int j = 0; j < 4; ++j) dst[j] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
-        }
-      }
-      ptx::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&tempty[acc]), 0));
-      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
-    }
+    conv_epilogue_loop<OUTF32, CV1_EPI>(g, H, W, rank, warp, lane, tmem_base, tfull, tempty, out);
   }
 
   ptx::tc_fence_before();
   ptx::cluster_sync();
-  if (warp == 5) {
+  if (warp == MMA) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc<2>(tmem_base, CV_TMEM);
+  }
+}
+
+template <bool OUTF32>
+__global__ void __launch_bounds__((CV2_EPI + 2) * 32, 1)
+    conv3x3_v2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                      void* __restrict__ out, int n_img, int H, int W) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem_b = smem;
+  uint8_t* smem_a = smem + CV2_B;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_a + CV2_STAGES * CV2_A);
+  uint64_t* empty = full + CV2_STAGES;
+  uint64_t* tfull = empty + CV2_STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint64_t* bfull = tempty + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bfull + 1);
+  constexpr int PROD = CV2_EPI, MMA = CV2_EPI + 1;
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const uint32_t rank = ptx::cluster_ctarank();
+  const ConvGeom g(n_img, H, W);
+
+  if (warp == PROD && lane == 0) {
+    ptx::prefetch_tmap(&tmA);
+    ptx::prefetch_tmap(&tmB);
+    for (int s = 0; s < CV2_STAGES; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      ptx::mbar_init(&tfull[a], 1);
+      ptx::mbar_init(&tempty[a], 2 * CV2_EPI);
+    }
+    ptx::mbar_init(bfull, 1);
+    ptx::fence_mbar_init();
+  }
+  if (warp == MMA) ptx::tmem_alloc<2>(tmem_slot, CV_TMEM);
+  ptx::tc_fence_before();
+  ptx::cluster_sync();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int cluster = blockIdx.x / 2, nclusters = gridDim.x / 2;
+
+  if (warp == PROD) {
+    if (lane == 0) {
+      // resident weights: 9 taps x this CTA's 64 output channels
+      if (rank == 0) ptx::mbar_arrive_expect_tx(bfull, CV2_B * 2);
+      const uint32_t bb = ptx::mapa(ptx::smem_u32(bfull), 0);
+      for (int tap = 0; tap < 9; ++tap)
+        ptx::tma_load_2d_pair(smem_b + tap * CV2_BTAP, &tmB, bb, tap * 64, static_cast<int>(rank) * CV_BNL);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = cluster; t < g.tiles; t += nclusters) {
+        const int n = t / g.tiles_img;
+        const int p0 = (t % g.tiles_img) * 2 * CV_BM + static_cast<int>(rank) * CV_BM;
+        const int64_t arow = static_cast<int64_t>(n) * g.img_rows + p0;
+        for (int r = 0; r < 3; ++r) {
+          ptx::mbar_wait(&empty[stage], phase ^ 1);
+          if (rank == 0) ptx::mbar_arrive_expect_tx(&full[stage], CV2_A * 2);
+          const uint32_t bar = ptx::mapa(ptx::smem_u32(&full[stage]), 0);
+          ptx::tma_load_2d_pair(smem_a + stage * CV2_A, &tmA, bar, 0, static_cast<int>(arow + r * g.Wp));
+          if (++stage == CV2_STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == MMA) {
+    if (rank == 0 && lane == 0) {
+      constexpr uint32_t idesc = ptx::umma_idesc(1, 0, 0, 2 * CV_BM, CV_BN);
+      ptx::mbar_wait(bfull, 0);
+      const uint32_t b_base = ptx::smem_u32(smem_b);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int t = cluster; t < g.tiles; t += nclusters) {
+        ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
+        ptx::tc_fence_after();
+        const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * CV_BN);
+        for (int r = 0; r < 3; ++r) {
+          ptx::mbar_wait(&full[stage], phase);
+          ptx::tc_fence_after();
+          const uint32_t a_addr = ptx::smem_u32(smem_a + stage * CV2_A);
+#pragma unroll
+          for (int s = 0; s < 3; ++s) {
+            const int tap = r * 3 + s;
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              ptx::mma<2, false>(d_tmem, ptx::umma_desc_sw128(a_addr + s * 128 + k * 32, 16, 1024),
+                                 ptx::umma_desc_sw128(b_base + tap * CV2_BTAP + k * 32, 16, 1024), idesc,
+                                 (r | s | k) != 0);
+          }
+          ptx::mma_commit<2>(&empty[stage]);
+          if (++stage == CV2_STAGES) { stage = 0; phase ^= 1; }
+        }
+        ptx::mma_commit<2>(&tfull[acc]);
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+    }
+    __syncwarp();
+  } else {
+    conv_epilogue_loop<OUTF32, CV2_EPI>(g, H, W, rank, warp, lane, tmem_base, tfull, tempty, out);
+  }
+
+  ptx::tc_fence_before();
+  ptx::cluster_sync();
+  if (warp == MMA) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc<2>(tmem_base, CV_TMEM);
   }
@@ -226,16 +384,22 @@ uint64_t launch_conv(LaunchCtx& c) {
   uint8_t* outp = at_byte<uint8_t>(O, lo * img_out, cnt * img_out, "conv3x3 output");
   if (!cnt) return 0;
   const int64_t rows = static_cast<int64_t>(cnt) * (H + 2) * (W + 2);
-  CUtensorMap ta = make_tmap_2d_bf16(in, C, rows, C * 2, 64, CV_BM);
+  const char* mode_env = std::getenv("HCL_CONV_MODE");
+  const bool v2 = C == 64 && !(mode_env && std::atoi(mode_env) == 1);
+  CUtensorMap ta = make_tmap_2d_bf16(in, C, rows, C * 2, 64, v2 ? CV2_AROWS : CV_BM);
   CUtensorMap tb = make_tmap_2d_bf16(Wt.ptr, 9 * C, K, 9 * C * 2, 64, CV_BNL);
-  auto kern = out_f32 ? conv3x3_tc_kernel<true> : conv3x3_tc_kernel<false>;
-  HCL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(CV_SMEM)));
+  void* kern = v2 ? (out_f32 ? reinterpret_cast<void*>(conv3x3_v2_kernel<true>)
+                             : reinterpret_cast<void*>(conv3x3_v2_kernel<false>))
+                  : (out_f32 ? reinterpret_cast<void*>(conv3x3_v1_kernel<true>)
+                             : reinterpret_cast<void*>(conv3x3_v1_kernel<false>));
+  const size_t smem = v2 ? CV2_SMEM : CV1_SMEM;
+  HCL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   const int64_t tiles_img = ceil_div(H * (W + 2), 2 * CV_BM);
   const int64_t clusters = std::min<int64_t>(static_cast<int64_t>(cnt) * tiles_img, c.sm_count / 2);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(static_cast<unsigned>(clusters * 2));
-  cfg.blockDim = dim3(CV_THREADS);
-  cfg.dynamicSmemBytes = CV_SMEM;
+  cfg.blockDim = dim3(((v2 ? CV2_EPI : CV1_EPI) + 2) * 32);
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = c.stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -244,8 +408,10 @@ uint64_t launch_conv(LaunchCtx& c) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  HCL_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, static_cast<void*>(outp), static_cast<int>(cnt), static_cast<int>(H),
-                              static_cast<int>(W), static_cast<int>(C)));
+  void* outv = static_cast<void*>(outp);
+  int cn = static_cast<int>(cnt), hh = static_cast<int>(H), ww = static_cast<int>(W), cc = static_cast<int>(C);
+  void* params[] = {&ta, &tb, &outv, &cn, &hh, &ww, &cc};  // v2 takes the first six
+  HCL_CUDA(cudaLaunchKernelExC(&cfg, kern, params));
   HCL_LAUNCHED();
   return 2ull * cnt * H * W * K * 9 * C;
 }

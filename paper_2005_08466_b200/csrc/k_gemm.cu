@@ -233,10 +233,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) {
-        if constexpr (CG == 2)
-          ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&tempty[acc]), 0));
-        else
-          ptx::mbar_arrive(&tempty[acc]);
+        // relaxed: this barrier only returns the TMEM accumulator (no global-store ordering needed)
+        ptx::mbar_arrive_cluster_relaxed(ptx::mapa(ptx::smem_u32(&tempty[acc]), 0));
       }
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }

@@ -53,6 +53,14 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 
+// Relaxed arrive: no ordering of this thread's prior global stores (the
+// release form waits for them with MEMBAR.GPU). For barriers that only hand a
+// TMEM accumulator back to the MMA warp, whose ordering comes from
+// tcgen05.fence::before_thread_sync + tcgen05.wait::ld.
+__device__ __forceinline__ void mbar_arrive_cluster_relaxed(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   uint32_t addr = smem_u32(bar);
   asm volatile(
@@ -188,6 +196,13 @@ __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t smem_addr, uint32_t
   d |= 1ull << 46;  // version = 1 (Blackwell)
   d |= 2ull << 61;  // layout type SWIZZLE_128B
   return d;
+}
+
+// Same with the 3-bit matrix base offset (bits 49-51): the phase of the
+// swizzle pattern when the start address is not on a 1024-byte boundary.
+__device__ __forceinline__ uint64_t umma_desc_sw128_bo(uint32_t smem_addr, uint32_t lbo, uint32_t sbo,
+                                                       uint32_t base_off) {
+  return umma_desc_sw128(smem_addr, lbo, sbo) | (static_cast<uint64_t>(base_off & 7) << 49);
 }
 
 // Instruction descriptor for kind::f16 / kind::tf32 with fp32 accumulation.
