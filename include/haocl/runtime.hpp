@@ -243,10 +243,16 @@ class HostContext {
   void set_kernel_arg(Handle kernel, uint32_t index, int64_t scalar);
   void set_kernel_arg(Handle kernel, uint32_t index, Handle buffer);
 
-  Handle enqueue_write_buffer(Handle queue, Handle buffer, std::span<const uint8_t> data, uint64_t offset = 0);
+  // blocking = false (OpenCL's blocking_write = CL_FALSE): the copy is queued on
+  // the device's H2D stream, ordered against kernels that use the buffer; the
+  // host memory must stay valid (and should be pinned) until finish(queue).
+  Handle enqueue_write_buffer(Handle queue, Handle buffer, std::span<const uint8_t> data, uint64_t offset = 0,
+                              bool blocking = true);
   std::vector<uint8_t> enqueue_read_buffer(Handle queue, Handle buffer);
   // Read into caller memory (pinned memory gives full PCIe/C2C bandwidth).
-  void enqueue_read_buffer_into(Handle queue, Handle buffer, void* dst, uint64_t offset, uint64_t len);
+  // blocking = false: queued on the D2H stream; dst is valid after finish(queue).
+  void enqueue_read_buffer_into(Handle queue, Handle buffer, void* dst, uint64_t offset, uint64_t len,
+                                bool blocking = true);
   Handle enqueue_ndrange_kernel(Handle queue, Handle kernel, std::array<uint64_t, 3> global_size = {1, 1, 1},
                                 uint32_t dims = 1);
   // Partitioned NDRange over several queues (one device each).

@@ -132,6 +132,12 @@ int hcl_finish(int dev, double* device_ms);
 uint64_t hcl_kernel_launch_count(void);
 /* Raw CUDA stream of a device (cudaStream_t as void*), for event timing. */
 int hcl_device_stream(int dev, void** stream);
+/* Interop with work issued directly on the device's compute stream (e.g. an
+ * external collective): acquire orders the stream after the buffer's pending
+ * copies (write != 0: also after its readers); release records the access so
+ * later copies order after it. Copies run on per-device H2D / D2H streams. */
+int hcl_stream_acquire(int dev, uint64_t id, int write);
+int hcl_stream_release(int dev, uint64_t id, int write);
 
 /* ---- collectives (NCCL over NVLink 5 / NVSwitch, loaded lazily) ---------- */
 int hcl_nccl_unique_id(uint8_t* out, int cap); /* cap >= 128 */

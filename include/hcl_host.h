@@ -47,6 +47,13 @@ int hcl_ctx_enqueue_write_buffer(hcl_context* ctx, uint64_t queue, uint64_t buff
 /* enqueue_read_buffer (proj/src/runtime.cpp:485-514) of [offset, offset+len). */
 int hcl_ctx_enqueue_read_buffer(hcl_context* ctx, uint64_t queue, uint64_t buffer, void* dst, uint64_t offset,
                                 uint64_t len);
+/* Non-blocking variants (OpenCL blocking_write/read = CL_FALSE): queued on the
+ * device's copy streams and ordered against kernels using the buffer; host
+ * memory (pinned for overlap) must stay valid until hcl_ctx_finish. */
+int hcl_ctx_enqueue_write_buffer_async(hcl_context* ctx, uint64_t queue, uint64_t buffer, const void* data,
+                                       uint64_t len, uint64_t offset, uint64_t* event);
+int hcl_ctx_enqueue_read_buffer_async(hcl_context* ctx, uint64_t queue, uint64_t buffer, void* dst, uint64_t offset,
+                                      uint64_t len);
 /* enqueue_ndrange_kernel (proj/src/runtime.cpp:516-540). */
 int hcl_ctx_enqueue_ndrange_kernel(hcl_context* ctx, uint64_t queue, uint64_t kernel, const uint64_t global[3],
                                    uint32_t dims, uint64_t* event);

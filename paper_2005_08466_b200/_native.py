@@ -55,6 +55,8 @@ CABI = [
     ("hcl_finish", C.c_int, [C.c_int, f64p]),
     ("hcl_kernel_launch_count", C.c_uint64, []),
     ("hcl_device_stream", C.c_int, [C.c_int, C.POINTER(C.c_void_p)]),
+    ("hcl_stream_acquire", C.c_int, [C.c_int, C.c_uint64, C.c_int]),
+    ("hcl_stream_release", C.c_int, [C.c_int, C.c_uint64, C.c_int]),
     ("hcl_nccl_unique_id", C.c_int, [u8p, C.c_int]),
     ("hcl_nccl_init", C.c_int, [C.c_int, C.c_int, C.c_int, u8p]),
     ("hcl_nccl_destroy", C.c_int, [C.c_int]),
@@ -78,6 +80,10 @@ HOST = [
                                                C.c_uint64, u64p]),
     ("hcl_ctx_enqueue_read_buffer", C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_void_p, C.c_uint64,
                                               C.c_uint64]),
+    ("hcl_ctx_enqueue_write_buffer_async", C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_void_p, C.c_uint64,
+                                                     C.c_uint64, u64p]),
+    ("hcl_ctx_enqueue_read_buffer_async", C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_void_p, C.c_uint64,
+                                                    C.c_uint64]),
     ("hcl_ctx_enqueue_ndrange_kernel", C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, u64p, C.c_uint32, u64p]),
     ("hcl_ctx_enqueue_ndrange_partitioned", C.c_int, [C.c_void_p, C.c_uint64, u64p, C.c_uint32, u64p, C.c_int,
                                                       u64p, u64p, u64p]),

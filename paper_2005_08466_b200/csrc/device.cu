@@ -60,16 +60,28 @@ void cuda_check(cudaError_t e, const char* what, const char* file, int line) {
 
 namespace {
 
+// Stream-ordered dependency tracking: every allocation remembers the event of
+// its last writer and of its readers per stream, so copies on the H2D / D2H
+// streams overlap kernels on the compute stream while RAW and WAR order holds.
+struct Dep {
+  cudaEvent_t ev = nullptr;
+  cudaStream_t st = nullptr;
+};
+
 struct DevAlloc {
   uint8_t* ptr = nullptr;
   uint64_t first_byte = 0;
   uint64_t bytes = 0;
   bool external = false;
+  Dep last_write;
+  std::vector<Dep> reads;  // at most one per stream
 };
 
 struct Device {
   int ordinal = 0;
-  cudaStream_t stream = nullptr;
+  cudaStream_t stream = nullptr;  // kernels, allocation, peer copies
+  cudaStream_t h2d = nullptr;     // host -> device copies
+  cudaStream_t d2h = nullptr;     // device -> host copies
   int sm_count = 0;
   uint64_t hbm_bytes = 0;
   std::string name;
@@ -77,6 +89,7 @@ struct Device {
   std::unordered_map<uint64_t, DevAlloc> bufs;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> timed;  // since last finish
   std::vector<cudaEvent_t> spare_events;
+  std::vector<cudaEvent_t> spare_sync;  // timing-disabled events for dependencies
   void* scratch = nullptr;
   size_t scratch_bytes = 0;
 
@@ -89,6 +102,54 @@ struct Device {
     cudaEvent_t e;
     HCL_CUDA(cudaEventCreate(&e));
     return e;
+  }
+  cudaEvent_t sync_event() {
+    if (!spare_sync.empty()) {
+      cudaEvent_t e = spare_sync.back();
+      spare_sync.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    HCL_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    return e;
+  }
+  void drop(Dep& d) {
+    if (d.ev) spare_sync.push_back(d.ev);  // waits already enqueued keep their snapshot
+    d = Dep{};
+  }
+  // make `s` wait for the writer (and, for a write, the readers) of `a`
+  void wait_for(DevAlloc& a, cudaStream_t s, bool write) {
+    if (a.last_write.ev && a.last_write.st != s) HCL_CUDA(cudaStreamWaitEvent(s, a.last_write.ev, 0));
+    if (write)
+      for (Dep& r : a.reads)
+        if (r.st != s) HCL_CUDA(cudaStreamWaitEvent(s, r.ev, 0));
+  }
+  // record that an operation on `s` just read / wrote `a`
+  cudaEvent_t note(DevAlloc& a, cudaStream_t s, bool write) {
+    cudaEvent_t e = sync_event();
+    HCL_CUDA(cudaEventRecord(e, s));
+    if (write) {
+      drop(a.last_write);
+      for (Dep& r : a.reads) drop(r);
+      a.reads.clear();
+      a.last_write = Dep{e, s};
+    } else {
+      for (Dep& r : a.reads)
+        if (r.st == s) {  // stream order subsumes the older read
+          drop(r);
+          r = Dep{e, s};
+          return e;
+        }
+      a.reads.push_back(Dep{e, s});
+    }
+    return e;
+  }
+  // before freeing: the compute stream (which frees) waits for every user
+  void retire(DevAlloc& a) {
+    wait_for(a, stream, true);
+    drop(a.last_write);
+    for (Dep& r : a.reads) drop(r);
+    a.reads.clear();
   }
 };
 
@@ -195,6 +256,8 @@ int hcl_init(const int* cuda_ordinals, int n, int* num_devices) {
       d->hbm_bytes = prop.totalGlobalMem;
       d->name = prop.name;
       HCL_CUDA(cudaStreamCreateWithFlags(&d->stream, cudaStreamNonBlocking));
+      HCL_CUDA(cudaStreamCreateWithFlags(&d->h2d, cudaStreamNonBlocking));
+      HCL_CUDA(cudaStreamCreateWithFlags(&d->d2h, cudaStreamNonBlocking));
       g_devices.push_back(std::move(d));
     }
     // NVLink P2P between every pair (NVSwitch: all-to-all).
@@ -281,6 +344,7 @@ int hcl_buffer_alloc(int dev, uint64_t id, uint64_t first_byte, uint64_t bytes) 
     auto it = d.bufs.find(id);
     if (it != d.bufs.end()) {
       if (it->second.first_byte == first_byte && it->second.bytes == bytes) return;
+      d.retire(it->second);
       if (!it->second.external && it->second.ptr) HCL_CUDA(cudaFreeAsync(it->second.ptr, d.stream));
       d.bufs.erase(it);
     }
@@ -291,7 +355,8 @@ int hcl_buffer_alloc(int dev, uint64_t id, uint64_t first_byte, uint64_t bytes) 
       HCL_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&a.ptr), bytes, d.stream));
       HCL_CUDA(cudaMemsetAsync(a.ptr, 0, bytes, d.stream));  // alloc zero-fills (daemon.cpp:21-69)
     }
-    d.bufs.emplace(id, a);
+    auto [pos, ok] = d.bufs.emplace(id, a);
+    if (bytes) d.note(pos->second, d.stream, true);
   });
 }
 
@@ -300,26 +365,41 @@ int hcl_buffer_bind_external(int dev, uint64_t id, void* ptr, uint64_t first_byt
     Device& d = device(dev);
     std::lock_guard<std::mutex> lock(d.mu);
     auto it = d.bufs.find(id);
-    if (it != d.bufs.end() && !it->second.external && it->second.ptr)
-      HCL_CUDA(cudaFreeAsync(it->second.ptr, d.stream));
-    d.bufs[id] = DevAlloc{static_cast<uint8_t*>(ptr), first_byte, bytes, true};
+    if (it != d.bufs.end()) {
+      d.retire(it->second);
+      if (!it->second.external && it->second.ptr) HCL_CUDA(cudaFreeAsync(it->second.ptr, d.stream));
+      d.bufs.erase(it);
+    }
+    DevAlloc a;
+    a.ptr = static_cast<uint8_t*>(ptr);
+    a.first_byte = first_byte;
+    a.bytes = bytes;
+    a.external = true;
+    d.bufs.emplace(id, a);
   });
 }
 
+// Host <-> device copies run on the device's H2D / D2H streams, ordered after
+// the buffer's last writer (and, for a write, its readers); a blocking call
+// waits for its own copy only.
 static int buffer_copy(int dev, uint64_t id, uint64_t offset, void* host, uint64_t len, bool write,
                        bool async) {
   return guarded([&] {
     Device& d = device(dev);
+    // held through a blocking wait: the event must not be recycled meanwhile
     std::lock_guard<std::mutex> lock(d.mu);
     DevAlloc& a = alloc_of(d, id, write ? "write_buffer" : "read_buffer");
     uint8_t* p = range_ptr(a, offset, len, id, write ? "write_buffer" : "read_buffer");
     if (!len) return;
     HCL_CUDA(cudaSetDevice(d.ordinal));
+    cudaStream_t s = write ? d.h2d : d.d2h;
+    d.wait_for(a, s, write);
     if (write)
-      HCL_CUDA(cudaMemcpyAsync(p, host, len, cudaMemcpyHostToDevice, d.stream));
+      HCL_CUDA(cudaMemcpyAsync(p, host, len, cudaMemcpyHostToDevice, s));
     else
-      HCL_CUDA(cudaMemcpyAsync(host, p, len, cudaMemcpyDeviceToHost, d.stream));
-    if (!async) HCL_CUDA(cudaStreamSynchronize(d.stream));
+      HCL_CUDA(cudaMemcpyAsync(host, p, len, cudaMemcpyDeviceToHost, s));
+    cudaEvent_t done = d.note(a, s, write);
+    if (!async) HCL_CUDA(cudaEventSynchronize(done));
   });
 }
 
@@ -341,38 +421,44 @@ int hcl_buffer_copy_peer(int dst_dev, uint64_t dst_id, uint64_t dst_offset, int 
   return guarded([&] {
     Device& dd = device(dst_dev);
     Device& sd = device(src_dev);
-    uint8_t *dp, *sp;
-    {
-      std::lock_guard<std::mutex> lock(dd.mu);
-      dp = range_ptr(alloc_of(dd, dst_id, "copy_peer dst"), dst_offset, len, dst_id, "copy_peer dst");
-    }
-    {
-      std::lock_guard<std::mutex> lock(sd.mu);
-      sp = range_ptr(alloc_of(sd, src_id, "copy_peer src"), src_offset, len, src_id, "copy_peer src");
-    }
+    std::unique_lock<std::mutex> l1(dd.mu, std::defer_lock), l2(sd.mu, std::defer_lock);
+    if (&dd == &sd)
+      l1.lock();
+    else
+      std::lock(l1, l2);
+    DevAlloc& da = alloc_of(dd, dst_id, "copy_peer dst");
+    DevAlloc& sa = alloc_of(sd, src_id, "copy_peer src");
+    uint8_t* dp = range_ptr(da, dst_offset, len, dst_id, "copy_peer dst");
+    uint8_t* sp = range_ptr(sa, src_offset, len, src_id, "copy_peer src");
     if (!len) return;
     if (&dd == &sd) {
       HCL_CUDA(cudaSetDevice(dd.ordinal));
+      dd.wait_for(sa, dd.stream, false);
+      dd.wait_for(da, dd.stream, true);
       HCL_CUDA(cudaMemcpyAsync(dp, sp, len, cudaMemcpyDeviceToDevice, dd.stream));
+      dd.note(sa, dd.stream, false);
+      dd.note(da, dd.stream, true);
       return;
     }
-    // order after everything pending on the source stream, then copy on the
-    // destination stream (NVLink P2P through NVSwitch)
+    // the source's compute stream first waits for the source's writer; the copy
+    // runs on the destination's compute stream (NVLink P2P through NVSwitch)
     HCL_CUDA(cudaSetDevice(sd.ordinal));
-    cudaEvent_t ready;
-    HCL_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+    sd.wait_for(sa, sd.stream, false);
+    cudaEvent_t ready = sd.sync_event();
     HCL_CUDA(cudaEventRecord(ready, sd.stream));
     HCL_CUDA(cudaSetDevice(dd.ordinal));
     HCL_CUDA(cudaStreamWaitEvent(dd.stream, ready, 0));
+    dd.wait_for(da, dd.stream, true);
     HCL_CUDA(cudaMemcpyPeerAsync(dp, dd.ordinal, sp, sd.ordinal, len, dd.stream));
+    dd.note(da, dd.stream, true);
     // the source must not be overwritten before the copy lands
-    cudaEvent_t done;
-    HCL_CUDA(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+    cudaEvent_t done = dd.sync_event();
     HCL_CUDA(cudaEventRecord(done, dd.stream));
     HCL_CUDA(cudaSetDevice(sd.ordinal));
     HCL_CUDA(cudaStreamWaitEvent(sd.stream, done, 0));
-    HCL_CUDA(cudaEventDestroy(ready));
-    HCL_CUDA(cudaEventDestroy(done));
+    sd.note(sa, sd.stream, false);
+    sd.spare_sync.push_back(ready);
+    dd.spare_sync.push_back(done);
   });
 }
 
@@ -383,6 +469,7 @@ int hcl_buffer_release(int dev, uint64_t id) {
     auto it = d.bufs.find(id);
     if (it == d.bufs.end()) return;  // idempotent
     HCL_CUDA(cudaSetDevice(d.ordinal));
+    d.retire(it->second);
     if (!it->second.external && it->second.ptr) HCL_CUDA(cudaFreeAsync(it->second.ptr, d.stream));
     d.bufs.erase(it);
   });
@@ -396,6 +483,24 @@ int hcl_buffer_device_ptr(int dev, uint64_t id, void** ptr, uint64_t* first_byte
     if (ptr) *ptr = a.ptr;
     if (first_byte) *first_byte = a.first_byte;
     if (bytes) *bytes = a.bytes;
+  });
+}
+
+int hcl_stream_acquire(int dev, uint64_t id, int write) {
+  return guarded([&] {
+    Device& d = device(dev);
+    std::lock_guard<std::mutex> lock(d.mu);
+    HCL_CUDA(cudaSetDevice(d.ordinal));
+    d.wait_for(alloc_of(d, id, "stream_acquire"), d.stream, write != 0);
+  });
+}
+
+int hcl_stream_release(int dev, uint64_t id, int write) {
+  return guarded([&] {
+    Device& d = device(dev);
+    std::lock_guard<std::mutex> lock(d.mu);
+    HCL_CUDA(cudaSetDevice(d.ordinal));
+    d.note(alloc_of(d, id, "stream_release"), d.stream, write != 0);
   });
 }
 
@@ -439,11 +544,20 @@ int hcl_launch(int dev, const char* kernel, const hcl_arg* args, uint32_t nargs,
       c.gsize[i] = gsize ? gsize[i] : 1;
     }
     c.scratch = scratch_for;
+    // order after pending copies of the arguments (RAW; WAR for outputs)
+    for (uint32_t i = 0; i < nargs; ++i)
+      if (args[i].kind != HCL_ARG_SCALAR)
+        d.wait_for(alloc_of(d, args[i].buffer_id, kernel), d.stream, args[i].kind != HCL_ARG_IN);
     cudaEvent_t e0 = d.event(), e1 = d.event();
     HCL_CUDA(cudaEventRecord(e0, d.stream));
     uint64_t w = k->launch(c);
     HCL_CUDA(cudaEventRecord(e1, d.stream));
     d.timed.emplace_back(e0, e1);
+    for (uint32_t i = 0; i < nargs; ++i)
+      if (args[i].kind == HCL_ARG_IN) d.note(alloc_of(d, args[i].buffer_id, kernel), d.stream, false);
+    for (uint32_t i = 0; i < nargs; ++i)
+      if (args[i].kind == HCL_ARG_OUT || args[i].kind == HCL_ARG_INOUT)
+        d.note(alloc_of(d, args[i].buffer_id, kernel), d.stream, true);
     if (work_units) *work_units = w;
   });
 }
@@ -453,7 +567,9 @@ int hcl_finish(int dev, double* device_ms) {
     Device& d = device(dev);
     std::lock_guard<std::mutex> lock(d.mu);
     HCL_CUDA(cudaSetDevice(d.ordinal));
+    HCL_CUDA(cudaStreamSynchronize(d.h2d));
     HCL_CUDA(cudaStreamSynchronize(d.stream));
+    HCL_CUDA(cudaStreamSynchronize(d.d2h));
     double total = 0.0;
     for (auto& [a, b] : d.timed) {
       float ms = 0.f;

@@ -576,7 +576,8 @@ void HostContext::set_kernel_arg(Handle kernel, uint32_t index, Handle buffer) {
   impl_->kernel(kernel.id).args[index] = Arg::of_handle(buffer.id);
 }
 
-Handle HostContext::enqueue_write_buffer(Handle queue, Handle buffer, std::span<const uint8_t> data, uint64_t offset) {
+Handle HostContext::enqueue_write_buffer(Handle queue, Handle buffer, std::span<const uint8_t> data, uint64_t offset,
+                                         bool blocking) {
   std::lock_guard lock(impl_->mu);
   Impl::QueueRec& q = impl_->queue(queue.id);
   if (buffer.kind != HandleKind::buffer) fail(ErrorCode::handle, "not a buffer handle");
@@ -593,7 +594,10 @@ Handle HostContext::enqueue_write_buffer(Handle queue, Handle buffer, std::span<
   Impl::Piece& p = impl_->ensure_alloc(buffer.id, b, q.gid, offset, data.size());
   if (!data.empty()) {
     impl_->trace.record({q.gid, "write_buffer", buffer.id});
-    check(hcl_buffer_write(impl_->dev_index(q.gid), buffer.id, offset, data.data(), data.size()));
+    if (blocking)
+      check(hcl_buffer_write(impl_->dev_index(q.gid), buffer.id, offset, data.data(), data.size()));
+    else
+      check(hcl_buffer_write_async(impl_->dev_index(q.gid), buffer.id, offset, data.data(), data.size()));
   }
   Impl::set_valid(p, offset, data.size());
   Impl::invalidate_others(b, q.gid, offset, data.size());
@@ -602,7 +606,8 @@ Handle HostContext::enqueue_write_buffer(Handle queue, Handle buffer, std::span<
   return impl_->new_event();
 }
 
-void HostContext::enqueue_read_buffer_into(Handle queue, Handle buffer, void* dst, uint64_t offset, uint64_t len) {
+void HostContext::enqueue_read_buffer_into(Handle queue, Handle buffer, void* dst, uint64_t offset, uint64_t len,
+                                           bool blocking) {
   std::lock_guard lock(impl_->mu);
   Impl::QueueRec& q = impl_->queue(queue.id);
   if (buffer.kind != HandleKind::buffer) fail(ErrorCode::handle, "not a buffer handle");
@@ -637,7 +642,10 @@ void HostContext::enqueue_read_buffer_into(Handle queue, Handle buffer, void* ds
     }
     uint64_t n = std::min(end, src_end) - pos;
     impl_->trace.record({src, "read_buffer", buffer.id});
-    check(hcl_buffer_read(impl_->dev_index(src), buffer.id, pos, out + (pos - offset), n));
+    if (blocking)
+      check(hcl_buffer_read(impl_->dev_index(src), buffer.id, pos, out + (pos - offset), n));
+    else
+      check(hcl_buffer_read_async(impl_->dev_index(src), buffer.id, pos, out + (pos - offset), n));
     pos += n;
   }
   impl_->add_transfer(&q, ms_since(started));
@@ -995,6 +1003,22 @@ int hcl_ctx_enqueue_read_buffer(hcl_context* ctx, uint64_t queue, uint64_t buffe
                                 uint64_t len) {
   return ctx_guarded([&] {
     ctx->ctx.enqueue_read_buffer_into(H(HandleKind::queue, queue), H(HandleKind::buffer, buffer), dst, offset, len);
+  });
+}
+int hcl_ctx_enqueue_write_buffer_async(hcl_context* ctx, uint64_t queue, uint64_t buffer, const void* data,
+                                       uint64_t len, uint64_t offset, uint64_t* event) {
+  return ctx_guarded([&] {
+    auto ev = ctx->ctx.enqueue_write_buffer(H(HandleKind::queue, queue), H(HandleKind::buffer, buffer),
+                                            std::span<const uint8_t>(static_cast<const uint8_t*>(data), len), offset,
+                                            false);
+    if (event) *event = ev.id;
+  });
+}
+int hcl_ctx_enqueue_read_buffer_async(hcl_context* ctx, uint64_t queue, uint64_t buffer, void* dst, uint64_t offset,
+                                      uint64_t len) {
+  return ctx_guarded([&] {
+    ctx->ctx.enqueue_read_buffer_into(H(HandleKind::queue, queue), H(HandleKind::buffer, buffer), dst, offset, len,
+                                      false);
   });
 }
 int hcl_ctx_enqueue_ndrange_kernel(hcl_context* ctx, uint64_t queue, uint64_t kernel, const uint64_t global[3],

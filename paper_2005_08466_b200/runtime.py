@@ -148,16 +148,20 @@ class HostContext:
             check(self._L.hcl_ctx_set_kernel_arg_i64(self._ctx, kernel.id, index, int(value)))
 
     # -- transfers -------------------------------------------------------
-    def enqueue_write_buffer(self, queue: Handle, buffer: Handle, data, offset: int = 0) -> Handle:
+    def enqueue_write_buffer(self, queue: Handle, buffer: Handle, data, offset: int = 0,
+                             blocking: bool = True) -> Handle:
+        """blocking=False queues the copy on the device's H2D stream (keep `data`
+        alive, ideally pinned, until finish(queue))."""
         ptr, n, keep = _bytes_view(data)
         ev = C.c_uint64()
-        check(self._L.hcl_ctx_enqueue_write_buffer(self._ctx, queue.id, buffer.id, C.c_void_p(ptr), n, offset,
-                                                   C.byref(ev)))
+        fn = self._L.hcl_ctx_enqueue_write_buffer if blocking else self._L.hcl_ctx_enqueue_write_buffer_async
+        check(fn(self._ctx, queue.id, buffer.id, C.c_void_p(ptr), n, offset, C.byref(ev)))
         del keep
         return Handle(HandleKind.event, ev.value)
 
     def enqueue_read_buffer(self, queue: Handle, buffer: Handle, offset: int = 0, length: Optional[int] = None,
-                            out=None) -> np.ndarray:
+                            out=None, blocking: bool = True) -> np.ndarray:
+        """blocking=False queues the copy on the D2H stream; `out` is valid after finish(queue)."""
         if length is None:
             length = self.buffer_size(buffer) - offset
         if out is None:
@@ -165,7 +169,8 @@ class HostContext:
         ptr, n, keep = _bytes_view(out)
         if n < length:
             raise HaoclError(18, "size: output buffer too small")
-        check(self._L.hcl_ctx_enqueue_read_buffer(self._ctx, queue.id, buffer.id, C.c_void_p(ptr), offset, length))
+        fn = self._L.hcl_ctx_enqueue_read_buffer if blocking else self._L.hcl_ctx_enqueue_read_buffer_async
+        check(fn(self._ctx, queue.id, buffer.id, C.c_void_p(ptr), offset, length))
         return out
 
     # -- launches --------------------------------------------------------

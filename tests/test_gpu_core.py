@@ -213,3 +213,32 @@ def test_kernel_launch_counter_advances(ctx, queues):
     before = N.lib().hcl_kernel_launch_count()
     run(ctx, "vecadd", [np.ones(64), np.ones(64), ("out", 64 * 8), 64], [2], queues[:1])
     assert N.lib().hcl_kernel_launch_count() > before
+
+
+def test_async_copies_respect_raw_and_war(ctx, queues):
+    """Non-blocking writes/reads on the copy streams overlap kernels on the
+    compute stream; with two buffer sets reused every other iteration, each
+    result must still match its own inputs (RAW for the kernel, WAR for the
+    overwrite of a buffer the previous-but-one kernel read)."""
+    n = 1 << 20
+    q = queues[0]
+    prog = ctx.create_program("core")
+    sets = []
+    for _ in range(2):
+        k = ctx.create_kernel(prog, "vecadd")
+        a, b, c = (ctx.create_buffer(n * 8) for _ in range(3))
+        for i, v in enumerate([a, b, c, n]):
+            ctx.set_kernel_arg(k, i, v)
+        sets.append((k, a, b, c))
+    ins = [O.gen_doubles(n, 100 + i) for i in range(8)]
+    two = np.full(n, 2.0)
+    outs = [np.empty(n, np.float64) for _ in range(8)]
+    for i in range(8):
+        k, a, b, c = sets[i % 2]
+        ctx.enqueue_write_buffer(q, a, ins[i], blocking=False)
+        ctx.enqueue_write_buffer(q, b, two, blocking=False)
+        ctx.enqueue_ndrange_kernel(q, k)
+        ctx.enqueue_read_buffer(q, c, out=outs[i], blocking=False)
+    ctx.finish(q)
+    for i in range(8):
+        assert (outs[i] == ins[i] + 2.0).all(), i
