@@ -586,9 +586,10 @@ class KMeansW(Workload):
 
     def roofline(self, pk):
         sm = pk.get("sm_max_mhz", 1965.0)
-        # exact SIMT: FADD2 (2 flop) + 2 FMUL + FADD2 per 2 terms -> 1.5 flop per issue slot
-        return ("fp32_simt", 148 * 4 * 32 * 1.5 * sm * 1e6 / 1e12, "TFLOP/s", 1e12,
-                "derived issue-bound rate of the exact FADD2/FMUL mix at max SM clock")
+        # exact (non-FMA) fp32: one add or multiply per lane per clock (FADD2 issues
+        # two lanes' worth but occupies the FP32 pipe twice, measured)
+        return ("fp32_simt", 148 * 128 * sm * 1e6 / 1e12, "TFLOP/s", 1e12,
+                "derived non-FMA fp32 rate (148 SM x 128 lanes x max SM clock)")
 
     def config(self):
         return {"workload": f"k-means iteration (C4): {self.N} points x {self.D} dims, K={self.K}, exact fp32 "
