@@ -19,6 +19,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <cstdlib>
 #include <mutex>
@@ -391,68 +392,96 @@ uint64_t launch_gemm_tc(LaunchCtx& c) {
 }
 
 // ---------------------------------------------------------------------------
-// fp32 SIMT GEMM (exact fp32 products, FFMA accumulate): 128x128 tile per
-// 256-thread block, 8x8 outputs per thread, K panels of 8 double-buffered in
-// shared memory. Used for the fp32 config where TF32 rounding is not wanted.
+// fp32 SIMT GEMM (exact fp32 products, FFMA accumulate in ascending k): BMxBN
+// tile per 256-thread block, TMxTN outputs per thread, K panels of 8
+// double-buffered in shared memory with register-staged prefetch (the next
+// panel's global loads are in flight while the current one is multiplied).
+// A is stored k-major in smem with a 4-float pad so the transposing stores are
+// conflict-free. 128x128 tiles (8x8 per thread) for large problems, 64x64
+// (4x4) when the 128 grid would leave SMs idle (C1: 1024^3 = 64 vs 256 tiles).
 
-constexpr int SG_T = 128, SG_K = 8;
+constexpr int SG_K = 8;
 
+template <int BM, int BN, int TM, int TN>
 __global__ void __launch_bounds__(256) gemm_f32_simt_kernel(const float* __restrict__ A, const float* __restrict__ B,
                                                             float* __restrict__ Cc, int64_t M, int64_t N, int64_t K) {
-  __shared__ __align__(16) float sa[2][SG_K][SG_T];
-  __shared__ __align__(16) float sb[2][SG_K][SG_T];
+  static_assert((BM / TM) * (BN / TN) == 256, "256 threads");
+  constexpr int AP = BM + 4;                      // padded k-row of the A panel
+  constexpr int A_PER = BM * SG_K / 256, B_PER = BN * SG_K / 256;
+  constexpr int RSTEP = BM * 4 / TM, CSTEP = BN * 4 / TN;  // distance between a thread's 4-groups
+  __shared__ __align__(16) float sa[2][SG_K][AP];
+  __shared__ __align__(16) float sb[2][SG_K][BN];
   const int tid = threadIdx.x;
-  const int tx = tid % 16, ty = tid / 16;
-  const int64_t row0 = blockIdx.y * (int64_t)SG_T, col0 = blockIdx.x * (int64_t)SG_T;
-  float acc[8][8];
+  const int tx = tid % (BN / TN), ty = tid / (BN / TN);
+  const int64_t row0 = blockIdx.y * (int64_t)BM, col0 = blockIdx.x * (int64_t)BN;
+  float acc[TM][TN];
 #pragma unroll
-  for (int i = 0; i < 8; ++i)
+  for (int i = 0; i < TM; ++i)
 #pragma unroll
-    for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
-  // loaders: A tile 128 rows x 8 k (4 per thread), B tile 8 k x 128 cols (4 per thread)
-  auto load = [&](int buf, int64_t k0) {
+    for (int j = 0; j < TN; ++j) acc[i][j] = 0.f;
+  float ra[A_PER], rb[B_PER];
+  auto fetch = [&](int64_t k0) {
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
+    for (int e = 0; e < A_PER; ++e) {
       int idx = tid + e * 256;
-      int r = idx / SG_K, kk = idx % SG_K;
-      int64_t gr = row0 + r, gk = k0 + kk;
-      sa[buf][kk][r] = (gr < M && gk < K) ? A[gr * K + gk] : 0.f;
-      int kb = idx / SG_T, cb = idx % SG_T;
-      int64_t gkb = k0 + kb, gc = col0 + cb;
-      sb[buf][kb][cb] = (gkb < K && gc < N) ? B[gkb * N + gc] : 0.f;
+      int64_t gr = row0 + idx / SG_K, gk = k0 + idx % SG_K;
+      ra[e] = (gr < M && gk < K) ? A[gr * K + gk] : 0.f;
+    }
+#pragma unroll
+    for (int e = 0; e < B_PER; ++e) {
+      int idx = tid + e * 256;
+      int64_t gk = k0 + idx / BN, gc = col0 + idx % BN;
+      rb[e] = (gk < K && gc < N) ? B[gk * N + gc] : 0.f;
     }
   };
-  load(0, 0);
+  auto stash = [&](int buf) {
+#pragma unroll
+    for (int e = 0; e < A_PER; ++e) {
+      int idx = tid + e * 256;
+      sa[buf][idx % SG_K][idx / SG_K] = ra[e];
+    }
+#pragma unroll
+    for (int e = 0; e < B_PER; ++e) {
+      int idx = tid + e * 256;
+      sb[buf][idx / BN][idx % BN] = rb[e];
+    }
+  };
+  fetch(0);
+  stash(0);
   __syncthreads();
   int buf = 0;
   for (int64_t k0 = 0; k0 < K; k0 += SG_K) {
-    if (k0 + SG_K < K) load(buf ^ 1, k0 + SG_K);
+    const bool more = k0 + SG_K < K;
+    if (more) fetch(k0 + SG_K);
 #pragma unroll
     for (int kk = 0; kk < SG_K; ++kk) {
-      float av[8], bv[8];
-      float4 a0 = *reinterpret_cast<const float4*>(&sa[buf][kk][ty * 4]);
-      float4 a1 = *reinterpret_cast<const float4*>(&sa[buf][kk][64 + ty * 4]);
-      float4 b0 = *reinterpret_cast<const float4*>(&sb[buf][kk][tx * 4]);
-      float4 b1 = *reinterpret_cast<const float4*>(&sb[buf][kk][64 + tx * 4]);
-      av[0] = a0.x; av[1] = a0.y; av[2] = a0.z; av[3] = a0.w;
-      av[4] = a1.x; av[5] = a1.y; av[6] = a1.z; av[7] = a1.w;
-      bv[0] = b0.x; bv[1] = b0.y; bv[2] = b0.z; bv[3] = b0.w;
-      bv[4] = b1.x; bv[5] = b1.y; bv[6] = b1.z; bv[7] = b1.w;
+      float av[TM], bv[TN];
 #pragma unroll
-      for (int i = 0; i < 8; ++i)
+      for (int g = 0; g < TM / 4; ++g) {
+        float4 v = *reinterpret_cast<const float4*>(&sa[buf][kk][g * RSTEP + ty * 4]);
+        av[g * 4] = v.x; av[g * 4 + 1] = v.y; av[g * 4 + 2] = v.z; av[g * 4 + 3] = v.w;
+      }
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+      for (int g = 0; g < TN / 4; ++g) {
+        float4 v = *reinterpret_cast<const float4*>(&sb[buf][kk][g * CSTEP + tx * 4]);
+        bv[g * 4] = v.x; bv[g * 4 + 1] = v.y; bv[g * 4 + 2] = v.z; bv[g * 4 + 3] = v.w;
+      }
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
     }
+    if (more) stash(buf ^ 1);
     __syncthreads();
     buf ^= 1;
   }
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    int64_t r = row0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + i - 4);
+  for (int i = 0; i < TM; ++i) {
+    int64_t r = row0 + (i / 4) * RSTEP + ty * 4 + i % 4;
     if (r >= M) continue;
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      int64_t cc = col0 + (j < 4 ? tx * 4 + j : 64 + tx * 4 + j - 4);
+    for (int j = 0; j < TN; ++j) {
+      int64_t cc = col0 + (j / 4) * CSTEP + tx * 4 + j % 4;
       if (cc < N) Cc[r * N + cc] = acc[i][j];
     }
   }
@@ -475,9 +504,15 @@ uint64_t launch_gemm_f32(LaunchCtx& c) {
   const float* a = at_byte<const float>(A, lo * k * 4, rows * k * 4, "gemm_f32 A");
   float* cp = at_byte<float>(Cb, lo * n * 4, rows * n * 4, "gemm_f32 C");
   if (rows == 0) return 0;
-  dim3 grid(static_cast<unsigned>(ceil_div(n, SG_T)), static_cast<unsigned>(ceil_div(rows, SG_T)));
-  gemm_f32_simt_kernel<<<grid, 256, 0, c.stream>>>(a, reinterpret_cast<const float*>(B.ptr), cp,
-                                                   static_cast<int64_t>(rows), n, k);
+  const float* bp = reinterpret_cast<const float*>(B.ptr);
+  const int64_t r = static_cast<int64_t>(rows);
+  if (ceil_div(r, 128) * ceil_div(n, 128) >= 2 * static_cast<int64_t>(c.sm_count)) {
+    dim3 grid(static_cast<unsigned>(ceil_div(n, 128)), static_cast<unsigned>(ceil_div(r, 128)));
+    gemm_f32_simt_kernel<128, 128, 8, 8><<<grid, 256, 0, c.stream>>>(a, bp, cp, r, n, k);
+  } else {
+    dim3 grid(static_cast<unsigned>(ceil_div(n, 64)), static_cast<unsigned>(ceil_div(r, 64)));
+    gemm_f32_simt_kernel<64, 64, 4, 4><<<grid, 256, 0, c.stream>>>(a, bp, cp, r, n, k);
+  }
   HCL_LAUNCHED();
   return 2ull * rows * static_cast<uint64_t>(n) * static_cast<uint64_t>(k);
 }
