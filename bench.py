@@ -311,7 +311,7 @@ class GemmF32(Workload):
         import numpy as np
         import torch
 
-        S = self.S
+        self.S = S = int(os.environ.get("BENCH_GEMM_F32_S", self.S))
         self.kernel = os.environ.get("BENCH_GEMM_F32_KERNEL", "gemm_f32")
         self.ctx = ctx = HostContext([self.dist.local])
         self.q = q = ctx.create_queue(0)
@@ -329,10 +329,13 @@ class GemmF32(Workload):
             ctx.set_kernel_arg(self.k, i, v)
         self.step()
         ctx.finish(q)
-        c = ctx.enqueue_read_buffer(q, self.bC).view(np.float32).reshape(S, S).astype(np.float64)
-        a = self.a_host.numpy().astype(np.float64).reshape(S, S)
+        R = S if S <= 2048 else 2  # parity guard rows (all of C1; 2 rows at C2 size)
+        c = ctx.enqueue_read_buffer(q, self.bC, length=R * S * 4).view(np.float32).reshape(R, S).astype(np.float64)
+        a = self.a_host.numpy()[: R * S].astype(np.float64).reshape(R, S)
         b = self.b_host.numpy().astype(np.float64).reshape(S, S)
         self.check = float((np.abs(c - a @ b) / (np.abs(a) @ np.abs(b))).max())
+        tol = 2.0**-10 if self.kernel == "gemm_tf32" else 2.0**-20
+        assert self.check <= tol, f"{self.kernel} parity guard failed: {self.check}"
 
     def step(self):
         self.ctx.enqueue_ndrange_kernel(self.q, self.k, (self.S, self.S, 1), 2)
@@ -357,12 +360,18 @@ class GemmF32(Workload):
         return 2 * self.S * self.S * 4 * self.dist.world, self.S * self.S * 4 * self.dist.world
 
     def roofline(self, pk):
+        if self.kernel == "gemm_tf32":
+            return "tensor", pk["bf16_tflops"] / 2, "TFLOP/s", 1e12, "TF32 tensor peak = MEASURED_PEAKS bf16 / 2"
+        if self.kernel == "gemm_f32x3":
+            return ("tensor", pk["bf16_tflops"] / 6, "TFLOP/s", 1e12,
+                    "3xTF32 effective fp32 peak = MEASURED_PEAKS bf16 / 2 (tf32) / 3 (products)")
         # fp32 FFMA peak: 148 SM x 128 lanes x 2 flop x max clock
         sm = pk.get("sm_max_mhz", 1965.0)
         return "fp32_simt", 148 * 128 * 2 * sm * 1e6 / 1e12, "TFLOP/s", 1e12, "derived FFMA peak at max SM clock"
 
     def config(self):
-        return {"workload": f"fp32 GEMM {self.S}^3 (C1) via the host API on one device ({self.kernel})",
+        cfg = "C1" if self.S == 1024 else "C2 fp32"
+        return {"workload": f"fp32 GEMM {self.S}^3 ({cfg}) via the host API on one device ({self.kernel})",
                 "replicas": self.dist.world, "normwise_err": self.check}
 
     def traffic(self):

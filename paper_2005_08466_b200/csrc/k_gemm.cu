@@ -36,7 +36,7 @@ constexpr int kBM = 128;            // A rows per CTA
 constexpr int kBN = 256;            // tile N (UMMA_N)
 constexpr int kThreads = 192;       // 4 epilogue warps + producer + MMA
 constexpr int kTmemCols = 512;      // 2 accumulators x 256 fp32 columns
-constexpr int kGroupM = 8;          // tile raster group
+constexpr int kGroupM = 8;          // default tile raster group (HCL_GEMM_GROUP overrides)
 
 template <int CG, bool TF32>
 struct Cfg {
@@ -53,12 +53,12 @@ struct Cfg {
 };
 
 struct TileMap {
-  int num_m, num_n;
+  int num_m, num_n, group_m;
   __device__ __forceinline__ void get(int t, int& mt, int& nt) const {
-    int group = kGroupM * num_n;
+    int group = group_m * num_n;
     int g = t / group;
-    int first_m = g * kGroupM;
-    int gm = min(kGroupM, num_m - first_m);
+    int first_m = g * group_m;
+    int gm = min(group_m, num_m - first_m);
     int local = t - g * group;
     mt = first_m + local % gm;
     nt = local / gm;
@@ -68,7 +68,7 @@ struct TileMap {
 template <int CG, bool TF32, bool BMN, bool OUTF32>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                   void* __restrict__ Cout, int M, int N, int K, int64_t ldc) {
+                   void* __restrict__ Cout, int M, int N, int K, int64_t ldc, int group_m) {
   using C = Cfg<CG, TF32>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -100,7 +100,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  const TileMap map{static_cast<int>((M + kBM * CG - 1) / (kBM * CG)), (N + kBN - 1) / kBN};
+  const TileMap map{static_cast<int>((M + kBM * CG - 1) / (kBM * CG)), (N + kBN - 1) / kBN, group_m};
   const int tiles = map.num_m * map.num_n;
   const int cluster = blockIdx.x / CG, nclusters = gridDim.x / CG;
   const int nk = (K + C::kBK - 1) / C::kBK;
@@ -270,6 +270,21 @@ EncodeTiledFn encode_fn() {
   return fn;
 }
 
+int env_int(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  return v ? std::atoi(v) : dflt;
+}
+
+// TMA L2 sector promotion (HCL_GEMM_PROMO 0..3 = none/64B/128B/256B; default 256B)
+CUtensorMapL2promotion l2_promotion() {
+  switch (env_int("HCL_GEMM_PROMO", 3)) {
+    case 0: return CU_TENSOR_MAP_L2_PROMOTION_NONE;
+    case 1: return CU_TENSOR_MAP_L2_PROMOTION_L2_64B;
+    case 2: return CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
+    default: return CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+  }
+}
+
 // 2D row-major tensor [outer][inner] with a SWIZZLE_128B box [box_outer][box_inner].
 CUtensorMap make_tmap(const void* base, bool f32, uint64_t inner, uint64_t outer, uint64_t row_bytes,
                       uint32_t box_inner, uint32_t box_outer) {
@@ -280,7 +295,7 @@ CUtensorMap make_tmap(const void* base, bool f32, uint64_t inner, uint64_t outer
   cuuint32_t estr[2] = {1, 1};
   CUresult r = encode_fn()(&m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
                            const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_SWIZZLE_128B, l2_promotion(),
                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
     fail(ErrorCode::argument, "cuTensorMapEncodeTiled failed (" + std::to_string(static_cast<int>(r)) +
@@ -290,7 +305,7 @@ CUtensorMap make_tmap(const void* base, bool f32, uint64_t inner, uint64_t outer
 
 template <int CG, bool TF32, bool BMN, bool OUTF32>
 void run_gemm(const void* A, const void* B, void* Cp, int64_t M, int64_t N, int64_t K, int64_t ldc,
-              int sm_count, cudaStream_t stream) {
+              int sm_count, cudaStream_t stream, int group_m) {
   using C = Cfg<CG, TF32>;
   const uint64_t es = C::kElem;
   CUtensorMap ta = make_tmap(A, TF32, K, M, K * es, C::kBK, kBM);
@@ -314,7 +329,7 @@ void run_gemm(const void* A, const void* B, void* Cp, int64_t M, int64_t N, int6
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   HCL_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, Cp, static_cast<int>(M), static_cast<int>(N),
-                              static_cast<int>(K), ldc));
+                              static_cast<int>(K), ldc, group_m));
   HCL_LAUNCHED();
 }
 
@@ -329,11 +344,6 @@ __global__ void transpose_kernel(const T* __restrict__ in, T* __restrict__ out, 
   int64_t oc = r0 + threadIdx.x, or0 = blockIdx.x * 32;
   for (int i = threadIdx.y; i < 32; i += 8)
     if (or0 + i < cols && oc < rows) out[(or0 + i) * rows + oc] = tile[threadIdx.x][i];
-}
-
-int env_int(const char* name, int dflt) {
-  const char* v = std::getenv(name);
-  return v ? std::atoi(v) : dflt;
 }
 
 // gemm_bf16(A, B, C, M, K, N, out_f32) and gemm_tf32(A, B, C, M, K, N)
@@ -378,8 +388,9 @@ uint64_t launch_gemm_tc(LaunchCtx& c) {
     b = bt;
   }
   const int64_t M = static_cast<int64_t>(rows);
+  const int group_m = std::max(1, env_int("HCL_GEMM_GROUP", kGroupM));
 #define HCL_GEMM_CASE(CG_, BMN_, OF_) \
-  run_gemm<CG_, TF32, BMN_, OF_>(a, b, cp, M, n, k, n, c.sm_count, c.stream)
+  run_gemm<CG_, TF32, BMN_, OF_>(a, b, cp, M, n, k, n, c.sm_count, c.stream, group_m)
   if (cg == 1) {
     if (kmajor) { if (out_f32) HCL_GEMM_CASE(1, false, true); else HCL_GEMM_CASE(1, false, false); }
     else { if (out_f32) HCL_GEMM_CASE(1, true, true); else HCL_GEMM_CASE(1, true, false); }
@@ -388,6 +399,97 @@ uint64_t launch_gemm_tc(LaunchCtx& c) {
     else { if (out_f32) HCL_GEMM_CASE(2, true, true); else HCL_GEMM_CASE(2, true, false); }
   }
 #undef HCL_GEMM_CASE
+  return 2ull * rows * static_cast<uint64_t>(n) * static_cast<uint64_t>(k);
+}
+
+// ---------------------------------------------------------------------------
+// fp32 GEMM as 3xTF32 on the tensor cores (gemm_f32x3). Each fp32 operand is
+// split x = hi + lo with hi = tf32_rna(x) and lo = x - hi (exact in fp32);
+// C = hi_a*hi_b + hi_a*lo_b + lo_a*hi_b (lo_a*lo_b ~ 2^-22 |a||b| dropped).
+// The three products become ONE K-major TF32 GEMM over K' = 3K:
+//   A'[r] = [hi(a_r) | hi(a_r) | lo(a_r)],  B'^T[n] = [hi(b_n) | lo(b_n) | hi(b_n)]
+// built by two memory-bound split kernels, then the same tcgen05 kernel as
+// gemm_tf32. Accuracy is fp32-product level (<= 2^-20
+// normwise) at ~1/3 of the TF32 tensor rate instead of the FFMA rate.
+
+__device__ __forceinline__ float tf32_hi(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
+// A (rows x K) -> A' (rows x 3K)
+__global__ void split3_rows_kernel(const float4* __restrict__ a, float4* __restrict__ out, int64_t rows, int64_t k4) {
+  const int64_t total = rows * k4;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / k4, c = i - r * k4;
+    float4 v = a[i], h, l;
+    h.x = tf32_hi(v.x); h.y = tf32_hi(v.y); h.z = tf32_hi(v.z); h.w = tf32_hi(v.w);
+    l.x = v.x - h.x; l.y = v.y - h.y; l.z = v.z - h.z; l.w = v.w - h.w;
+    float4* o = out + r * 3 * k4 + c;
+    o[0] = h;
+    o[k4] = h;
+    o[2 * k4] = l;
+  }
+}
+
+// B (K x N, row-major) -> B'^T (N x 3K): transpose through shared memory
+__global__ void split3_cols_kernel(const float* __restrict__ b, float* __restrict__ out, int64_t K, int64_t N) {
+  __shared__ float tile[32][33];
+  const int64_t n0 = blockIdx.x * 32, k0 = blockIdx.y * 32;
+  for (int i = threadIdx.y; i < 32; i += 8) {
+    const int64_t k = k0 + i, n = n0 + threadIdx.x;
+    tile[i][threadIdx.x] = (k < K && n < N) ? b[k * N + n] : 0.f;
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += 8) {
+    const int64_t n = n0 + i, k = k0 + threadIdx.x;
+    if (n < N && k < K) {
+      const float v = tile[threadIdx.x][i], h = tf32_hi(v);
+      float* o = out + n * 3 * K + k;
+      o[0] = h;
+      o[K] = v - h;
+      o[2 * K] = h;
+    }
+  }
+}
+
+// gemm_f32x3(A, B, C, M, K, N): same arguments and classes as gemm_f32
+uint64_t launch_gemm_f32x3(LaunchCtx& c) {
+  int64_t m = scalar_arg(c, 3, "gemm_f32x3 M");
+  int64_t k = scalar_arg(c, 4, "gemm_f32x3 K");
+  int64_t n = scalar_arg(c, 5, "gemm_f32x3 N");
+  if (m < 1 || k < 1 || n < 1) fail(ErrorCode::argument, "gemm_f32x3: dimensions must be >= 1");
+  if (m > INT32_MAX || n > INT32_MAX || 3 * k > INT32_MAX) fail(ErrorCode::argument, "gemm_f32x3: dimension too large");
+  if (k % 4 || n % 4) fail(ErrorCode::argument, "gemm_f32x3: K and N must be multiples of 4 (16-byte TMA row pitch)");
+  const BufView& A = buffer_arg(c, 0, "gemm_f32x3 A");
+  const BufView& B = buffer_arg(c, 1, "gemm_f32x3 B");
+  const BufView& Cb = buffer_arg(c, 2, "gemm_f32x3 C");
+  if (c.whole && A.bytes != static_cast<uint64_t>(m * k) * 4) fail(ErrorCode::argument, "gemm_f32x3: A size != M*K");
+  if (B.first_byte != 0 || B.bytes != static_cast<uint64_t>(k * n) * 4)
+    fail(ErrorCode::argument, "gemm_f32x3: B size != K*N");
+  uint64_t lo, rows;
+  sub_range(c, static_cast<uint64_t>(m), lo, rows, "gemm_f32x3");
+  const float* a = at_byte<const float>(A, lo * k * 4, rows * k * 4, "gemm_f32x3 A");
+  float* cp = at_byte<float>(Cb, lo * n * 4, rows * n * 4, "gemm_f32x3 C");
+  if (rows == 0) return 0;
+  const int64_t r = static_cast<int64_t>(rows);
+  const size_t a3_bytes = static_cast<size_t>(r * 3 * k * 4);
+  uint8_t* s = static_cast<uint8_t*>(c.scratch(c.dev, a3_bytes + static_cast<size_t>(n * 3 * k * 4)));
+  float* a3 = reinterpret_cast<float*>(s);
+  float* b3 = reinterpret_cast<float*>(s + a3_bytes);
+  {
+    const int64_t total = r * (k / 4);
+    const unsigned blocks = static_cast<unsigned>(std::min<int64_t>(ceil_div(total, 256), 64LL * c.sm_count));
+    split3_rows_kernel<<<blocks, 256, 0, c.stream>>>(reinterpret_cast<const float4*>(a), reinterpret_cast<float4*>(a3),
+                                                      r, k / 4);
+    HCL_LAUNCHED();
+    dim3 grid(static_cast<unsigned>(ceil_div(n, 32)), static_cast<unsigned>(ceil_div(k, 32)));
+    split3_cols_kernel<<<grid, dim3(32, 8), 0, c.stream>>>(reinterpret_cast<const float*>(B.ptr), b3, k, n);
+    HCL_LAUNCHED();
+  }
+  const int group_m = std::max(1, env_int("HCL_GEMM_GROUP", kGroupM));
+  run_gemm<2, true, false, true>(a3, b3, cp, r, n, 3 * k, n, c.sm_count, c.stream, group_m);
   return 2ull * rows * static_cast<uint64_t>(n) * static_cast<uint64_t>(k);
 }
 
@@ -541,6 +643,8 @@ void register_gemm(std::vector<KernelDef>& r) {
   r.push_back({"b200", "gemm_tf32", {I, I, O, S, S, S}, {X, P, X, N, N, N}, launch_gemm_tc<true>,
                rowbytes_gemm_f32, rows_gemm});
   r.push_back({"b200", "gemm_f32", {I, I, O, S, S, S}, {X, P, X, N, N, N}, launch_gemm_f32, rowbytes_gemm_f32,
+               rows_gemm});
+  r.push_back({"b200", "gemm_f32x3", {I, I, O, S, S, S}, {X, P, X, N, N, N}, launch_gemm_f32x3, rowbytes_gemm_f32,
                rows_gemm});
 }
 

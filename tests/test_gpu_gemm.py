@@ -4,7 +4,7 @@ err_ij = |C - C64|_ij / (|A| |B|)_ij. Tolerances (stated here, per path):
   bf16 inputs, fp32 out  : 2^-12   (fp32 tensor-core accumulation)
   bf16 inputs, bf16 out  : 2^-8    (adds the bf16 output rounding, 2^-9 rel)
   tf32 (fp32 inputs)     : 2^-10   (1xTF32 products)
-  fp32 SIMT              : 2^-16   (exact fp32 products, fp32 accumulation)
+  fp32 SIMT, 3xTF32      : 2^-20   (fp32-exact-product paths)
 plus bit-identity of C across partitions P in {1,2,4} (P-invariance)."""
 import os
 
@@ -101,18 +101,41 @@ def test_gemm_tf32(ctx, queues, m, n, k):
     assert normwise_err(c, a.astype(np.float64).reshape(m, k), b.astype(np.float64).reshape(k, n)) <= 2.0**-10
 
 
-@pytest.mark.parametrize("m,n,k", [(1024, 1024, 1024), (300, 200, 137)])
+# (2560, 2560, 256) takes the 128x128-tile SIMT kernel, the others the 64x64 one
+@pytest.mark.parametrize("m,n,k", [(1024, 1024, 1024), (300, 200, 137), (2560, 2560, 256)])
 def test_gemm_f32_simt(ctx, queues, m, n, k):
     a = O.gen_doubles(m * k, 42).astype(np.float32)
     b = O.gen_doubles(k * n, 43).astype(np.float32)
     c = gemm(ctx, queues, "gemm_f32", a, b, m, k, n)
-    assert normwise_err(c, a.astype(np.float64).reshape(m, k), b.astype(np.float64).reshape(k, n)) <= 2.0**-16
+    assert normwise_err(c, a.astype(np.float64).reshape(m, k), b.astype(np.float64).reshape(k, n)) <= 2.0**-20
+
+
+@pytest.mark.parametrize("m,n,k", [(1024, 1024, 1024), (300, 200, 136), (512, 264, 4096)])
+def test_gemm_f32x3(ctx, queues, m, n, k):
+    a = O.gen_doubles(m * k, 42).astype(np.float32)
+    b = O.gen_doubles(k * n, 43).astype(np.float32)
+    c = gemm(ctx, queues, "gemm_f32x3", a, b, m, k, n)
+    assert normwise_err(c, a.astype(np.float64).reshape(m, k), b.astype(np.float64).reshape(k, n)) <= 2.0**-20
+
+
+@pytest.mark.parametrize("kernel", ["gemm_f32", "gemm_f32x3", "gemm_tf32"])
+def test_gemm_fp32_partition_invariance(ctx, queues, kernel):
+    m, n, k = 1000, 512, 256
+    a = O.gen_doubles(m * k, 42).astype(np.float32)
+    b = O.gen_doubles(k * n, 43).astype(np.float32)
+    whole = gemm(ctx, queues, kernel, a, b, m, k, n)
+    for P, w in ((2, None), (4, [1, 2, 3, 4])):
+        part = gemm(ctx, queues, kernel, a, b, m, k, n, P=P, weights=w)
+        assert whole.tobytes() == part.tobytes(), (kernel, P)
 
 
 def test_gemm_argument_errors(ctx, queues):
     a = O.gen_bf16(64 * 60, 1)
     with pytest.raises(HaoclError) as e:  # K=60 -> 120-byte rows, not 16-byte aligned
         gemm(ctx, queues, "gemm_bf16", a, O.gen_bf16(60 * 64, 2), 64, 60, 64)
+    assert e.value.name == "argument"
+    with pytest.raises(HaoclError) as e:  # 3xTF32 needs K % 4 == 0
+        gemm(ctx, queues, "gemm_f32x3", np.ones(64 * 62, np.float32), np.ones(62 * 64, np.float32), 64, 62, 64)
     assert e.value.name == "argument"
     with pytest.raises(HaoclError) as e:  # B has the wrong size
         gemm(ctx, queues, "gemm_bf16", O.gen_bf16(64 * 64, 1), O.gen_bf16(64 * 32, 2), 64, 64, 64)
