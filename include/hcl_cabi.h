@@ -60,8 +60,13 @@ enum hcl_part_class {
   HCL_PART_NONE = 0,      /* scalar */
   HCL_PART_REPLICATE = 1, /* whole buffer on every device (GEMM B, PageRank x) */
   HCL_PART_SPLIT_ROWS = 2, /* row slice [lo,hi) of dim 0 on each device (GEMM A, C) */
-  HCL_PART_REDUCE_SUM = 3  /* each part produces a full-size int64 partial; the
+  HCL_PART_REDUCE_SUM = 3, /* each part produces a full-size int64 partial; the
                               runtime sums them (k-means centroid sums) */
+  HCL_PART_MERGE_TOPK = 4  /* each part produces full-size per-query sorted
+                              top-k lists (an index and a distance output); the
+                              runtime folds them pairwise with the kernel's
+                              companion "<name>_merge" (knn reference-set split,
+                              proj/src/bench.cpp:367-447 + kernels.cpp:323-361) */
 };
 
 /* One bound kernel argument, BoundArg (proj/include/haocl/kernels.hpp:44-50). */

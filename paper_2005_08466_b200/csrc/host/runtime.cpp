@@ -359,6 +359,7 @@ struct HostContext::Impl {
     // 3. outputs: the launch produced the bytes U = union of the part slices
     //    (one interval); older copies of U anywhere are stale, bytes outside U
     //    keep their validity
+    bool merged_topk = false;
     for (uint32_t i = 0; i < n; ++i) {
       if (!args[i].is_buffer || k.kinds[i] == HCL_ARG_IN) continue;
       BufferRec& b = buffer(args[i].buffer);
@@ -387,6 +388,55 @@ struct HostContext::Impl {
         for (auto& [g, p] : b.pieces) p.valid_bytes = 0;
         b.pieces[g0].valid_first = 0;
         b.pieces[g0].valid_bytes = b.size;
+        continue;
+      }
+      if (!whole && k.classes[i] == HCL_PART_MERGE_TOPK) {
+        // fold the parts' top-k lists onto the first part's device with the
+        // kernel's "<name>_merge" companion (same arguments + the other part's
+        // index and distance lists), in part order
+        if (merged_topk) continue;  // both MERGE_TOPK outputs are folded together
+        merged_topk = true;
+        std::vector<uint32_t> mi;
+        for (uint32_t j = 0; j < n; ++j)
+          if (args[j].is_buffer && k.classes[j] == HCL_PART_MERGE_TOPK) mi.push_back(j);
+        if (mi.size() != 2) fail(ErrorCode::argument, k.name + ": MERGE_TOPK needs one index and one distance output");
+        std::vector<int> gids;
+        for (const Part& part : parts)
+          if (part.hi > part.lo) gids.push_back(part.gid);
+        if (gids.empty()) continue;
+        for (size_t a = 0; a < gids.size(); ++a)
+          for (size_t c = a + 1; c < gids.size(); ++c)
+            if (gids[a] == gids[c])
+              fail(ErrorCode::argument, k.name + ": a MERGE_TOPK output needs one device per part");
+        const int g0 = gids[0], d0 = dev_index(g0);
+        BufferRec& bi = buffer(args[mi[0]].buffer);
+        BufferRec& bd = buffer(args[mi[1]].buffer);
+        const std::string merge = k.name + "_merge";
+        for (size_t a = 1; a < gids.size(); ++a) {
+          const int da = dev_index(gids[a]);
+          uint64_t ti = new_id(), td = new_id();
+          check(hcl_buffer_alloc(d0, ti, 0, bi.size));
+          check(hcl_buffer_alloc(d0, td, 0, bd.size));
+          check(hcl_buffer_copy_peer(d0, ti, 0, da, args[mi[0]].buffer, 0, bi.size));
+          check(hcl_buffer_copy_peer(d0, td, 0, da, args[mi[1]].buffer, 0, bd.size));
+          trace.record({g0, "copy_peer", args[mi[0]].buffer});
+          trace.record({g0, "copy_peer", args[mi[1]].buffer});
+          std::vector<hcl_arg> margs(cargs);
+          margs[mi[0]].kind = HCL_ARG_INOUT;
+          margs[mi[1]].kind = HCL_ARG_INOUT;
+          margs.push_back(hcl_arg{HCL_ARG_IN, 0, 0, ti});
+          margs.push_back(hcl_arg{HCL_ARG_IN, 0, 0, td});
+          const int rc = hcl_launch(d0, merge.c_str(), margs.data(), static_cast<uint32_t>(margs.size()), nullptr,
+                                    nullptr, 1, nullptr);
+          hcl_buffer_release(d0, ti);
+          hcl_buffer_release(d0, td);
+          check(rc);
+        }
+        for (BufferRec* b2 : {&bi, &bd}) {
+          for (auto& [g, p] : b2->pieces) p.valid_bytes = 0;
+          b2->pieces[g0].valid_first = 0;
+          b2->pieces[g0].valid_bytes = b2->size;
+        }
         continue;
       }
       uint64_t u0 = UINT64_MAX, u1 = 0;

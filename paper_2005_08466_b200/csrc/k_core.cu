@@ -307,9 +307,14 @@ __device__ __forceinline__ bool pair_lt(double da, int ia, double db, int ib) {
   return da < db || (da == db && ia < ib);
 }
 
+// `refp` holds reference rows [idx_base, idx_base + R) of the whole set; the
+// emitted indices are global. Fewer than k candidates (a reference-set part
+// with R < k) pad the list with (+inf, INT32_MAX), which sorts after every
+// real candidate.
 __global__ void __launch_bounds__(KNN_T) knn_f64_kernel(const double* __restrict__ refp,
                                                         const double* __restrict__ query, int64_t R,
-                                                        int64_t D, int k, int32_t* __restrict__ out_idx,
+                                                        int64_t D, int k, int64_t idx_base,
+                                                        int32_t* __restrict__ out_idx,
                                                         double* __restrict__ out_dist) {
   extern __shared__ double sq[];  // D query coords
   __shared__ double hd[KNN_T];
@@ -328,7 +333,7 @@ __global__ void __launch_bounds__(KNN_T) knn_f64_kernel(const double* __restrict
       double diff = __dsub_rn(p[d], sq[d]);
       sum = __dadd_rn(sum, __dmul_rn(diff, diff));
     }
-    int id = static_cast<int>(r);
+    int id = static_cast<int>(idx_base + r);
     if (have < k || pair_lt(sum, id, bd[k - 1], bi[k - 1])) {
       int pos = have < k ? have++ : k - 1;
       while (pos > 0 && pair_lt(sum, id, bd[pos - 1], bi[pos - 1])) {
@@ -395,11 +400,110 @@ uint64_t launch_knn(LaunchCtx& c) {
                                   static_cast<int>(smem)));
   if (cnt) {
     knn_f64_kernel<<<static_cast<unsigned>(cnt), KNN_T, smem, c.stream>>>(
-        reinterpret_cast<const double*>(Rf.ptr), qp, r, d, static_cast<int>(k), oi, od);
+        reinterpret_cast<const double*>(Rf.ptr), qp, r, d, static_cast<int>(k), 0, oi, od);
     HCL_LAUNCHED();
   }
   return static_cast<uint64_t>(d) * r * cnt;
 }
+
+// knn_refsplit(ref, query, R, Q, D, k, idx, dist): the reference's knn
+// partitioning (proj/src/bench.cpp:367-447): the NDRange is the REFERENCE set
+// (dim 0 = R), each part computes every query's top-k over its reference rows
+// [lo, hi) with global indices (the reference adds `lo` on the host, 417-418),
+// and the MERGE_TOPK outputs are folded by knn_refsplit_merge. Launched whole
+// it equals core knn bit-for-bit.
+uint64_t launch_knn_refsplit(LaunchCtx& c) {
+  int64_t r = scalar_arg(c, 2, "knn_refsplit R");
+  int64_t q = scalar_arg(c, 3, "knn_refsplit Q");
+  int64_t d = scalar_arg(c, 4, "knn_refsplit D");
+  int64_t k = scalar_arg(c, 5, "knn_refsplit k");
+  if (r < 1 || q < 1 || d < 1) fail(ErrorCode::argument, "knn_refsplit: R, Q, D must be >= 1");
+  if (k < 1 || k > r) fail(ErrorCode::argument, "knn_refsplit: need 1 <= k <= R");
+  if (k > KNN_MAXK)
+    fail(ErrorCode::argument, "knn_refsplit: the GPU path supports k <= " + std::to_string(KNN_MAXK));
+  if (r > INT32_MAX) fail(ErrorCode::argument, "knn_refsplit: R exceeds int32 indices");
+  const BufView& Rf = buffer_arg(c, 0, "knn_refsplit ref");
+  const BufView& Qb = buffer_arg(c, 1, "knn_refsplit query");
+  if (c.whole && Rf.bytes != static_cast<uint64_t>(r * d) * 8) fail(ErrorCode::argument, "knn_refsplit: ref size != R*D");
+  if (Qb.first_byte != 0 || Qb.bytes != static_cast<uint64_t>(q * d) * 8)
+    fail(ErrorCode::argument, "knn_refsplit: query size != Q*D");
+  uint64_t lo, cnt;
+  sub_range(c, static_cast<uint64_t>(r), lo, cnt, "knn_refsplit");
+  const double* rp = at_byte<const double>(Rf, lo * d * 8, cnt * d * 8, "knn_refsplit ref");
+  int32_t* oi = at_byte<int32_t>(buffer_arg(c, 6, "knn_refsplit idx"), 0, q * k * 4, "knn_refsplit idx");
+  double* od = at_byte<double>(buffer_arg(c, 7, "knn_refsplit dist"), 0, q * k * 8, "knn_refsplit dist");
+  size_t smem = static_cast<size_t>(d) * 8;
+  if (smem > 200 * 1024) fail(ErrorCode::argument, "knn_refsplit: D too large for the GPU path");
+  if (smem > 48 * 1024)
+    HCL_CUDA(cudaFuncSetAttribute(knn_f64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  if (cnt) {
+    knn_f64_kernel<<<static_cast<unsigned>(q), KNN_T, smem, c.stream>>>(rp, reinterpret_cast<const double*>(Qb.ptr),
+                                                                      static_cast<int64_t>(cnt), d, static_cast<int>(k),
+                                                                      static_cast<int64_t>(lo), oi, od);
+    HCL_LAUNCHED();
+  }
+  return static_cast<uint64_t>(d) * cnt * q;
+}
+
+// Fold two per-query sorted top-k lists into the first: the k smallest of the
+// union under the (dist, idx) order -- merge_topk's partial_sort of the pool
+// (proj/src/kernels.cpp:347-358) restricted to two partials, which is
+// associative, so folding parts in order equals the P-way merge. A list that
+// is not sorted raises the reference's contract error (333-340).
+__global__ void knn_merge2_kernel(int32_t* __restrict__ ia, double* __restrict__ da, const int32_t* __restrict__ ib,
+                                  const double* __restrict__ db, int64_t Q, int k, int* __restrict__ bad) {
+  const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (q >= Q) return;
+  int32_t oi[KNN_MAXK];
+  double od[KNN_MAXK];
+  const int32_t* pa = ia + q * k;
+  const double* qa = da + q * k;
+  const int32_t* pb = ib + q * k;
+  const double* qb = db + q * k;
+  for (int i = 1; i < k; ++i)
+    if (pair_lt(qa[i], pa[i], qa[i - 1], pa[i - 1]) || pair_lt(qb[i], pb[i], qb[i - 1], pb[i - 1])) atomicOr(bad, 1);
+  int x = 0, y = 0;
+  for (int o = 0; o < k; ++o) {
+    if (pair_lt(qb[y], pb[y], qa[x], pa[x])) {
+      od[o] = qb[y];
+      oi[o] = pb[y];
+      ++y;
+    } else {
+      od[o] = qa[x];
+      oi[o] = pa[x];
+      ++x;
+    }
+  }
+  for (int o = 0; o < k; ++o) {
+    ia[q * k + o] = oi[o];
+    da[q * k + o] = od[o];
+  }
+}
+
+// knn_refsplit_merge(ref, query, R, Q, D, k, idx, dist, idx2, dist2): the
+// MERGE_TOPK companion (same arguments + the other part's lists).
+uint64_t launch_knn_refsplit_merge(LaunchCtx& c) {
+  int64_t q = scalar_arg(c, 3, "knn merge Q");
+  int64_t k = scalar_arg(c, 5, "knn merge k");
+  if (q < 1 || k < 1 || k > KNN_MAXK) fail(ErrorCode::argument, "knn merge: bad Q or k");
+  int32_t* ia = at_byte<int32_t>(buffer_arg(c, 6, "knn merge idx"), 0, q * k * 4, "knn merge idx");
+  double* da = at_byte<double>(buffer_arg(c, 7, "knn merge dist"), 0, q * k * 8, "knn merge dist");
+  const int32_t* ib = at_byte<const int32_t>(buffer_arg(c, 8, "knn merge idx2"), 0, q * k * 4, "knn merge idx2");
+  const double* db = at_byte<const double>(buffer_arg(c, 9, "knn merge dist2"), 0, q * k * 8, "knn merge dist2");
+  int* bad = static_cast<int*>(c.scratch(c.dev, sizeof(int)));
+  HCL_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), c.stream));
+  knn_merge2_kernel<<<static_cast<unsigned>(ceil_div(q, 128)), 128, 0, c.stream>>>(ia, da, ib, db, q,
+                                                                                 static_cast<int>(k), bad);
+  HCL_LAUNCHED();
+  int h = 0;
+  HCL_CUDA(cudaMemcpyAsync(&h, bad, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+  HCL_CUDA(cudaStreamSynchronize(c.stream));
+  if (h) fail(ErrorCode::contract, "merge_topk: partial not sorted");
+  return static_cast<uint64_t>(q * k);
+}
+
+uint64_t rows_knn_refsplit(const int64_t* s, uint32_t) { return static_cast<uint64_t>(s[2]); }
+uint64_t rowbytes_knn_refsplit(const int64_t* s, uint32_t, uint32_t) { return static_cast<uint64_t>(s[4]) * 8; }
 
 uint64_t rows_matmul(const int64_t* s, uint32_t) { return static_cast<uint64_t>(s[3]); }
 uint64_t rowbytes_matmul(const int64_t* s, uint32_t, uint32_t i) {
@@ -430,6 +534,12 @@ void register_core(std::vector<KernelDef>& r) {
                rowbytes_knn, rows_knn});
   r.push_back({"core", "vecadd", {I, I, O, S}, {X, X, X, N}, launch_vecadd, rowbytes_vecadd,
                rows_vecadd});
+  // the reference-set split of knn (§8(f) 3) and its MERGE_TOPK companion
+  constexpr uint8_t M = HCL_PART_MERGE_TOPK, IO = HCL_ARG_INOUT;
+  r.push_back({"b200", "knn_refsplit", {I, I, S, S, S, S, O, O}, {X, P, N, N, N, N, M, M}, launch_knn_refsplit,
+               rowbytes_knn_refsplit, rows_knn_refsplit});
+  r.push_back({"b200", "knn_refsplit_merge", {I, I, S, S, S, S, IO, IO, I, I}, {P, P, N, N, N, N, P, P, P, P},
+               launch_knn_refsplit_merge, nullptr, nullptr});
 }
 
 }  // namespace hcl
