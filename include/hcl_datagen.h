@@ -38,6 +38,13 @@ int hcl_pagerank_csr(int scale, uint64_t edges, uint64_t seed, int32_t* row_ptr,
  * {row, first_unit, nchunks} per long row (> warp_nnz). Pass NULL arrays to count. */
 int hcl_pagerank_units(const int32_t* row_ptr, int64_t rows, int64_t warp_nnz, int32_t* units, int32_t* long_rows,
                        int64_t* n_units, int64_t* n_long);
+/* Degree-ordered relabelling of a pull CSR: perm[i] = old id of new vertex i
+ * (out-degree descending, ties by id); rows keep their column order (columns
+ * renamed), so per-row SpMV sums are unchanged and results are permuted.
+ * Outputs have the input sizes. Returns 0 or 1000+argument. */
+int hcl_pagerank_relabel(const int32_t* row_ptr, const int32_t* col_idx, const float* val, const int32_t* outdeg,
+                         int64_t v, int32_t* new_row_ptr, int32_t* new_col, float* new_val, int32_t* new_outdeg,
+                         int32_t* perm, int threads);
 /* CSR-adaptive row blocks (<= max_nnz per multi-row block); out may be NULL to
  * count. Returns the number of blocks; out[0..n] are block start rows. */
 int64_t hcl_csr_row_blocks(const int32_t* row_ptr, int64_t rows, int64_t max_nnz, int32_t* out);

@@ -138,6 +138,8 @@ DATAGEN = [
                                    C.c_int]),
     ("hcl_csr_row_blocks", C.c_int64, [C.c_void_p, C.c_int64, C.c_int64, C.c_void_p]),
     ("hcl_pagerank_units", C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_void_p, C.c_void_p, i64p, i64p]),
+    ("hcl_pagerank_relabel", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p,
+                                       C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int]),
 ]
 
 EXTRA = []  # appended by workload modules

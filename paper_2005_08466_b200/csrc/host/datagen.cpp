@@ -262,4 +262,45 @@ int64_t hcl_csr_row_blocks(const int32_t* row_ptr, int64_t rows, int64_t max_nnz
   return n;
 }
 
+// Degree-ordered relabelling of a pull CSR (vertices = rows = columns): new id
+// i is the vertex with the i-th largest out-degree (= how often its rank is
+// gathered), ties by old id. Rows move with their vertex and keep their column
+// ORDER (each old column c becomes inv[c]), so every row's product sequence,
+// and hence the SpMV's per-row summation, is unchanged: results are the old
+// ones permuted (rank_old[perm[i]] = rank_new[i]). The hot sources become one
+// dense prefix of x, which the gathers then find in L1/L2.
+int hcl_pagerank_relabel(const int32_t* row_ptr, const int32_t* col_idx, const float* val, const int32_t* outdeg,
+                         int64_t v, int32_t* new_row_ptr, int32_t* new_col, float* new_val, int32_t* new_outdeg,
+                         int32_t* perm, int threads) {
+  if (v < 1 || v > INT32_MAX) return 1000 + 9;
+  // perm = vertices sorted by (outdeg desc, id asc): counting sort on degree
+  int32_t maxd = 0;
+  for (int64_t i = 0; i < v; ++i) maxd = std::max(maxd, outdeg[i]);
+  std::vector<int64_t> start(static_cast<size_t>(maxd) + 2, 0);
+  for (int64_t i = 0; i < v; ++i) ++start[static_cast<size_t>(maxd - outdeg[i]) + 1];
+  for (size_t d = 1; d < start.size(); ++d) start[d] += start[d - 1];
+  for (int64_t i = 0; i < v; ++i) perm[start[static_cast<size_t>(maxd - outdeg[i])]++] = static_cast<int32_t>(i);
+  std::vector<int32_t> inv(static_cast<size_t>(v));
+  parallel_for(static_cast<uint64_t>(v), threads, [&](uint64_t lo, uint64_t hi) {
+    for (uint64_t i = lo; i < hi; ++i) inv[perm[i]] = static_cast<int32_t>(i);
+  });
+  new_row_ptr[0] = 0;
+  for (int64_t i = 0; i < v; ++i) {
+    const int32_t o = perm[i];
+    new_row_ptr[i + 1] = new_row_ptr[i] + (row_ptr[o + 1] - row_ptr[o]);
+    new_outdeg[i] = outdeg[o];
+  }
+  parallel_for(static_cast<uint64_t>(v), threads, [&](uint64_t lo, uint64_t hi) {
+    for (uint64_t i = lo; i < hi; ++i) {
+      const int32_t o = perm[i];
+      int64_t q = new_row_ptr[i];
+      for (int64_t p = row_ptr[o]; p < row_ptr[o + 1]; ++p, ++q) {
+        new_col[q] = inv[col_idx[p]];
+        new_val[q] = val[p];
+      }
+    }
+  });
+  return 0;
+}
+
 }  // extern "C"

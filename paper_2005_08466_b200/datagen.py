@@ -83,6 +83,23 @@ def pagerank_units(row_ptr: np.ndarray, warp_nnz: int):
     return units, long_rows, nl.value
 
 
+def pagerank_relabel(row_ptr, col_idx, val, outdeg, threads: int = 0):
+    """Degree-ordered relabelling (hcl_pagerank_relabel): returns
+    (row_ptr, col_idx, val, outdeg, perm) of the relabelled graph, perm[i] =
+    old id of new vertex i. Ranks map back as old[perm] = new."""
+    v = len(row_ptr) - 1
+    rp = np.ascontiguousarray(row_ptr, np.int32)
+    ci = np.ascontiguousarray(col_idx, np.int32)
+    va = np.ascontiguousarray(val, np.float32)
+    od = np.ascontiguousarray(outdeg, np.int32)
+    out = (np.empty_like(rp), np.empty_like(ci), np.empty_like(va), np.empty_like(od), np.empty(v, np.int32))
+    rc = N.lib().hcl_pagerank_relabel(rp.ctypes.data, ci.ctypes.data, va.ctypes.data, od.ctypes.data, v,
+                                      *(a.ctypes.data for a in out), threads)
+    if rc:
+        raise N.HaoclError(rc - N.HCL_ERR_BASE, "pagerank_relabel: bad arguments")
+    return out
+
+
 def csr_row_blocks(row_ptr: np.ndarray, max_nnz: int) -> np.ndarray:
     """CSR-adaptive row blocks: start rows of blocks of <= max_nnz non-zeros
     (a longer row is its own block); last entry = rows."""

@@ -15,7 +15,7 @@ from typing import Optional, Sequence
 
 import numpy as np
 
-from .datagen import pagerank_units
+from .datagen import pagerank_relabel, pagerank_units
 from .runtime import Handle, HostContext, spmv_partition_ranges
 
 DEFAULT_WARP_NNZ = 1024
@@ -24,8 +24,14 @@ DEFAULT_WARP_NNZ = 1024
 class PageRank:
     def __init__(self, ctx: HostContext, queues: Sequence[Handle], row_ptr: np.ndarray, col_idx: np.ndarray,
                  val: np.ndarray, outdeg: np.ndarray, max_nnz: int = DEFAULT_WARP_NNZ,
-                 weights: Optional[Sequence[int]] = None):
+                 weights: Optional[Sequence[int]] = None, relabel: bool = False):
+        """relabel: store the graph degree-ordered (hcl_pagerank_relabel) so the
+        hot ranks form a dense prefix of x; per-row sums are unchanged, and
+        ranks()/spmv() map results back to the caller's vertex ids."""
         self.ctx, self.queues = ctx, list(queues)
+        self.perm = None
+        if relabel:
+            row_ptr, col_idx, val, outdeg, self.perm = pagerank_relabel(row_ptr, col_idx, val, outdeg)
         self.v = len(row_ptr) - 1
         self.nnz = int(row_ptr[-1])
         self.warp_nnz = max_nnz
@@ -75,18 +81,26 @@ class PageRank:
 
     def ranks(self) -> np.ndarray:
         self.finish()
-        return self.ctx.enqueue_read_buffer(self.queues[0], self.b_x[self.cur]).view(np.float32)
+        return self._to_caller(self.ctx.enqueue_read_buffer(self.queues[0], self.b_x[self.cur]).view(np.float32))
+
+    def _to_caller(self, r: np.ndarray) -> np.ndarray:
+        if self.perm is None:
+            return r
+        out = np.empty_like(r)
+        out[self.perm] = r
+        return out
 
     def spmv(self, x: np.ndarray) -> np.ndarray:
         """One y = A x through the partitioned pagerank_spmv kernel."""
         ctx = self.ctx
         bx, by = ctx.create_buffer(self.v * 4), ctx.create_buffer(self.v * 4)
-        ctx.enqueue_write_buffer(self.queues[0], bx, np.ascontiguousarray(x, np.float32))
+        x = np.ascontiguousarray(x, np.float32)
+        ctx.enqueue_write_buffer(self.queues[0], bx, x if self.perm is None else x[self.perm])
         for j, a in enumerate([self.b_rp, self.b_col, self.b_val, self.b_units, self.b_long, bx, by] + self.tail):
             ctx.set_kernel_arg(self.k_spmv, j, a)
         ctx.enqueue_ndrange_partitioned(self.k_spmv, (self.v, 1, 1), 1, self.queues, bounds=self.bounds)
         self.finish()
-        y = ctx.enqueue_read_buffer(self.queues[0], by).view(np.float32).copy()
+        y = self._to_caller(ctx.enqueue_read_buffer(self.queues[0], by).view(np.float32).copy())
         ctx.release(bx)
         ctx.release(by)
         return y

@@ -118,3 +118,31 @@ def test_pagerank_uneven_weights(ctx, queues, graph):
     pr.close()
     rp, ci, val, deg = graph
     assert got == O.pagerank(rp, ci, val, deg, 5, b200_order=True).tobytes()
+
+
+def test_relabel_preserves_results_cpu(graph):
+    """Degree-ordered relabelling keeps every row's product sequence: the
+    restated-order oracle on the relabelled graph equals the original, permuted."""
+    rp, ci, val, deg = graph
+    rp2, ci2, val2, deg2, perm = G.pagerank_relabel(rp, ci, val, deg)
+    assert sorted(perm.tolist()) == list(range(len(rp) - 1))
+    assert (np.diff(deg2) <= 0).all() and (deg2 == deg[perm]).all()
+    r = O.pagerank(rp, ci, val, deg, 7, b200_order=True)
+    r2 = O.pagerank(rp2, ci2, val2, deg2, 7, b200_order=True)
+    assert r2.tobytes() == r[perm].tobytes()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("P,weights", [(1, None), (4, [1, 2, 3, 4])])
+def test_pagerank_relabelled(ctx, queues, graph, P, weights):
+    from paper_2005_08466_b200.pagerank import PageRank
+
+    rp, ci, val, deg = graph
+    pr = PageRank(ctx, queues[:P], *graph, max_nnz=512, weights=weights, relabel=True)
+    x = O.gen_doubles(len(rp) - 1, 7).astype(np.float32) + 1.5
+    assert pr.spmv(x).tobytes() == O.spmv_f32_b200(rp, ci, val, x, 0, len(rp) - 1).tobytes()
+    pr.reset()
+    pr.iterate(20)
+    got = pr.ranks().tobytes()
+    pr.close()
+    assert got == O.pagerank(rp, ci, val, deg, 20, b200_order=True).tobytes()
