@@ -416,7 +416,7 @@ class PageRankW(Workload):
         t0 = time.perf_counter()
         rp, ci, val, deg = G.pagerank_csr(self.scale, self.e, 42)
         # degree-ordered vertex ids (per-row sums unchanged; tests/test_gpu_pagerank.py)
-        self.relabel = os.environ.get("BENCH_PR_RELABEL", "1") == "1"
+        self.relabel = os.environ.get("BENCH_PR_RELABEL", "0") == "1"
         if self.relabel:
             rp, ci, val, deg, _ = G.pagerank_relabel(rp, ci, val, deg)
         ctx.add_data_creation_ms((time.perf_counter() - t0) * 1e3)

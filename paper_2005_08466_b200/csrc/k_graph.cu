@@ -21,9 +21,7 @@
 // every operation separately rounded (oracle ho_pagerank).
 #include <cuda_runtime.h>
 
-#include <algorithm>
 #include <cstdint>
-#include <cstdlib>
 #include <string>
 
 #include "common.hpp"
@@ -32,6 +30,8 @@
 namespace hcl {
 namespace {
 
+constexpr int PR_T = 256;
+constexpr int PR_WARPS = PR_T / 32;
 constexpr int PR_CHUNK = 4096;  // long-row chunk (part of the summation-order definition)
 
 // sum over j with outdeg[j]==0 of trunc(x_j * 2^56): integer, so order free
@@ -105,50 +105,35 @@ __device__ __forceinline__ Update pr_update(const unsigned long long* dsum, floa
   return u;
 }
 
-// x gather through the block's shared-memory copy of the hot prefix x[0, hot)
-// (with degree-ordered vertex ids the most gathered ranks; hcl_pagerank_relabel)
-struct XSrc {
-  const float* __restrict__ x;
-  const float* sx;
-  int hot;
-  __device__ __forceinline__ float operator()(int c) const { return c < hot ? sx[c] : ld_x(x + c); }
-};
-
 // lane-strided partial sums over [p, e) then the butterfly (all lanes hold the total)
 __device__ __forceinline__ float warp_row_sum(const int* __restrict__ colp, const float* __restrict__ valp,
-                                              const XSrc& gx, int p, int e, int lane) {
+                                              const float* __restrict__ x, int p, int e, int lane) {
   float v = 0.f;
   int q = p + lane;
   for (; q + 96 < e; q += 128) {
     int i0 = ld_stream(colp + q), i1 = ld_stream(colp + q + 32), i2 = ld_stream(colp + q + 64), i3 = ld_stream(colp + q + 96);
     float v0 = ld_stream(valp + q), v1 = ld_stream(valp + q + 32), v2 = ld_stream(valp + q + 64), v3 = ld_stream(valp + q + 96);
-    float x0 = gx(i0), x1 = gx(i1), x2 = gx(i2), x3 = gx(i3);
+    float x0 = ld_x(x + i0), x1 = ld_x(x + i1), x2 = ld_x(x + i2), x3 = ld_x(x + i3);
     v = __fadd_rn(v, __fmul_rn(v0, x0));
     v = __fadd_rn(v, __fmul_rn(v1, x1));
     v = __fadd_rn(v, __fmul_rn(v2, x2));
     v = __fadd_rn(v, __fmul_rn(v3, x3));
   }
-  for (; q < e; q += 32) v = __fadd_rn(v, __fmul_rn(ld_stream(valp + q), gx(ld_stream(colp + q))));
+  for (; q < e; q += 32) v = __fadd_rn(v, __fmul_rn(ld_stream(valp + q), ld_x(x + ld_stream(colp + q))));
   return butterfly(v);
 }
 
-template <bool UPDATE, int NT>
-__global__ void __launch_bounds__(NT) pr_units_kernel(const int* __restrict__ row_ptr, const int* __restrict__ col,
+template <bool UPDATE>
+__global__ void __launch_bounds__(PR_T) pr_units_kernel(const int* __restrict__ row_ptr, const int* __restrict__ col,
                                                         const float* __restrict__ val, int64_t nnz_off,
                                                         const int4* __restrict__ units, int n_units,
                                                         const float* __restrict__ x,
                                                         const unsigned long long* __restrict__ dsum,
                                                         float* __restrict__ y, int lo, int hi, float base, float damp,
-                                                        float inv_v, int warp_nnz, float* __restrict__ chunk_tot,
-                                                        int hot) {
-  extern __shared__ __align__(16) float smem_f[];
+                                                        float inv_v, int warp_nnz, float* __restrict__ chunk_tot) {
+  extern __shared__ float prod_all[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int hot_pad = (hot + 3) & ~3;
-  float* prod = smem_f + hot_pad + warp * warp_nnz;
-  for (int i = threadIdx.x; i < hot_pad / 4; i += NT)
-    reinterpret_cast<float4*>(smem_f)[i] = __ldg(reinterpret_cast<const float4*>(x) + i);
-  if (hot) __syncthreads();
-  const XSrc gx{x, smem_f, hot};
+  float* prod = prod_all + warp * warp_nnz;
   const Update upd = pr_update<UPDATE>(dsum, base, damp, inv_v);
   // units overlapping [lo, hi): row1 > lo and row0 < hi (both monotone in u)
   int a = 0, b = n_units;
@@ -165,13 +150,12 @@ __global__ void __launch_bounds__(NT) pr_units_kernel(const int* __restrict__ ro
   const int u_last = a;
   const int* colp = col - nnz_off;
   const float* valp = val - nnz_off;
-  constexpr int WARPS = NT / 32;
-  const int nw = gridDim.x * WARPS;
-  for (int u = u_first + blockIdx.x * WARPS + warp; u < u_last; u += nw) {
+  const int nw = gridDim.x * PR_WARPS;
+  for (int u = u_first + blockIdx.x * PR_WARPS + warp; u < u_last; u += nw) {
     const int4 U = units[u];
     if (U.y - U.x == 1 && __ldg(row_ptr + U.x + 1) - __ldg(row_ptr + U.x) > warp_nnz) {
       // one chunk of a long row
-      const float v = warp_row_sum(colp, valp, gx, U.z, U.w, lane);
+      const float v = warp_row_sum(colp, valp, x, U.z, U.w, lane);
       if (lane == 0) chunk_tot[u] = v;
       continue;
     }
@@ -183,13 +167,13 @@ __global__ void __launch_bounds__(NT) pr_units_kernel(const int* __restrict__ ro
           c3 = ld_stream(colp + p0 + i + 96);
       float v0 = ld_stream(valp + p0 + i), v1 = ld_stream(valp + p0 + i + 32), v2 = ld_stream(valp + p0 + i + 64),
             v3 = ld_stream(valp + p0 + i + 96);
-      float x0 = gx(c0), x1 = gx(c1), x2 = gx(c2), x3 = gx(c3);
+      float x0 = ld_x(x + c0), x1 = ld_x(x + c1), x2 = ld_x(x + c2), x3 = ld_x(x + c3);
       prod[i] = __fmul_rn(v0, x0);
       prod[i + 32] = __fmul_rn(v1, x1);
       prod[i + 64] = __fmul_rn(v2, x2);
       prod[i + 96] = __fmul_rn(v3, x3);
     }
-    for (; i < n; i += 32) prod[i] = __fmul_rn(ld_stream(valp + p0 + i), gx(ld_stream(colp + p0 + i)));
+    for (; i < n; i += 32) prod[i] = __fmul_rn(ld_stream(valp + p0 + i), ld_x(x + ld_stream(colp + p0 + i)));
     __syncwarp();
     for (int rb = r0; rb < r1; rb += 32) {
       const int r = rb + lane;
@@ -229,11 +213,6 @@ __global__ void pr_fixup_kernel(const int* __restrict__ long_rows, int n_long, c
   float total = chunk_tot[u0];
   for (int c = 1; c < nc; ++c) total = __fadd_rn(total, chunk_tot[u0 + c]);
   pr_store<UPDATE>(y, row, lo, total, pr_update<UPDATE>(dsum, base, damp, inv_v));
-}
-
-int env_int_pr(const char* name, int dflt) {
-  const char* e = std::getenv(name);
-  return e ? std::atoi(e) : dflt;
 }
 
 // args: row_ptr col val units long_rows x [dsum] y | V nnz_off n_units n_long warp_nnz
@@ -281,28 +260,18 @@ uint64_t launch_pr(LaunchCtx& c) {
     fail(ErrorCode::argument, std::string(what) + ": col_idx/values do not cover the rows' non-zeros");
   float* chunk_tot = static_cast<float*>(c.scratch(c.dev, static_cast<size_t>(n_units) * 4));
   const float base = static_cast<float>((1.0 - 0.85) / v), damp = 0.85f, inv_v = static_cast<float>(1.0 / v);
-  // block shape and hot-prefix cache (HCL_PR_NT = 256 | 1024 threads per
-  // block, HCL_PR_HOT = cached x entries, -1 = all the shared memory left)
-  const int nt = env_int_pr("HCL_PR_NT", 256) == 1024 ? 1024 : 256;
-  const size_t prod_bytes = static_cast<size_t>(warp_nnz) * 4 * (nt / 32);
-  int64_t hot = env_int_pr("HCL_PR_HOT", 0);
-  constexpr size_t kSmemMax = 227 * 1024;
-  if (prod_bytes > kSmemMax) fail(ErrorCode::argument, std::string(what) + ": warp_nnz too large for the block");
-  if (hot < 0) hot = static_cast<int64_t>((kSmemMax - prod_bytes) / 4) & ~int64_t(3);
-  hot = std::min<int64_t>(hot, v) & ~int64_t(3);
-  const size_t smem = prod_bytes + static_cast<size_t>(hot) * 4;
-  if (smem > kSmemMax) fail(ErrorCode::argument, std::string(what) + ": HCL_PR_HOT too large");
-  auto kern = nt == 1024 ? pr_units_kernel<UPDATE, 1024> : pr_units_kernel<UPDATE, 256>;
+  const size_t smem = static_cast<size_t>(warp_nnz) * 4 * PR_WARPS;
+  auto kern = pr_units_kernel<UPDATE>;
   HCL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   int per_sm = 0;
-  HCL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nt, smem));
+  HCL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, PR_T, smem));
   const int grid = std::max(1, per_sm) * c.sm_count;
-  kern<<<grid, nt, smem, c.stream>>>(row_ptr, reinterpret_cast<const int*>(Cb.ptr),
-                                     reinterpret_cast<const float*>(Vb.ptr), nnz_off,
-                                     reinterpret_cast<const int4*>(U.ptr), static_cast<int>(n_units),
-                                     reinterpret_cast<const float*>(X.ptr), dsum, y, static_cast<int>(lo),
-                                     static_cast<int>(lo + rows), base, damp, inv_v, static_cast<int>(warp_nnz),
-                                     chunk_tot, static_cast<int>(hot));
+  kern<<<grid, PR_T, smem, c.stream>>>(row_ptr, reinterpret_cast<const int*>(Cb.ptr),
+                                       reinterpret_cast<const float*>(Vb.ptr), nnz_off,
+                                       reinterpret_cast<const int4*>(U.ptr), static_cast<int>(n_units),
+                                       reinterpret_cast<const float*>(X.ptr), dsum, y, static_cast<int>(lo),
+                                       static_cast<int>(lo + rows), base, damp, inv_v, static_cast<int>(warp_nnz),
+                                       chunk_tot);
   HCL_LAUNCHED();
   if (n_long) {
     pr_fixup_kernel<UPDATE><<<static_cast<unsigned>(ceil_div(n_long, 128)), 128, 0, c.stream>>>(
