@@ -420,7 +420,7 @@ class PageRankW(Workload):
         if self.relabel:
             rp, ci, val, deg, _ = G.pagerank_relabel(rp, ci, val, deg)
         ctx.add_data_creation_ms((time.perf_counter() - t0) * 1e3)
-        self.wn = wn = int(os.environ.get("BENCH_PR_WARP_NNZ", "512"))
+        self.wn = wn = int(os.environ.get("BENCH_PR_WARP_NNZ", "64"))
         units, long_rows, n_long = G.pagerank_units(rp, wn)
         self.bounds = [int(x) for x in spmv_partition_ranges(rp.astype(np.int64), d.world)]
         lo, hi = self.bounds[d.rank], self.bounds[d.rank + 1]

@@ -18,7 +18,7 @@ import numpy as np
 from .datagen import pagerank_relabel, pagerank_units
 from .runtime import Handle, HostContext, spmv_partition_ranges
 
-DEFAULT_WARP_NNZ = 1024
+DEFAULT_WARP_NNZ = 64  # measured best at scale 24 (profiles/r01_pagerank_experiments.txt)
 
 
 class PageRank:
