@@ -292,6 +292,10 @@ class HostContext {
   void add_data_creation_ms(double ms);
   MessageTrace& trace();
   Scheduler& scheduler();
+  // SM budget of a (logical) device: its kernels size their grids to `sms`
+  // SMs, and the scheduler's model relative_throughput becomes sms/SM count
+  // (emulated heterogeneous devices on one GPU; hcl_device_set_sm_budget)
+  void set_device_sm_budget(int global_device_id, int sms);
   uint64_t buffer_size(Handle buffer) const;
   int queue_device(Handle queue) const;
   // Device pointer of a buffer's resident slice on a device (for zero-copy interop).

@@ -86,6 +86,13 @@ int hcl_device_count(int* n);
 /* type: 1 = gpu (wire::DeviceType, proj/include/haocl/wire.hpp:44) */
 int hcl_device_info(int dev, int* type, double* relative_throughput, int* sm_count,
                     uint64_t* hbm_bytes, char* name, int name_cap);
+/* SM budget of a logical device: the persistent kernels size their grids to
+ * `sms` (even, 2..the GPU's SM count) instead of the whole GPU, so several
+ * logical devices on one GPU run concurrently at different rates -- an
+ * emulated heterogeneous node set for the rate-proportional split (the
+ * reference's DeviceProfile.relative_throughput, proj/src/scheduler.cpp:38-48).
+ * relative_throughput becomes sms / SM count; sms <= 0 restores the whole GPU. */
+int hcl_device_set_sm_budget(int dev, int sms);
 
 /* ---- registry (query_registry; proj/src/api.cpp:93-117) ---------------- */
 /* Kernel names of a bundle as a comma-separated list; arities per kernel. */

@@ -101,6 +101,8 @@ int hcl_ctx_sched_rate(hcl_context* ctx, int global_id, const char* kernel, doub
 int hcl_ctx_sched_schedule(hcl_context* ctx, const char* kernel, const char* policy, int explicit_device,
                            double work_units, uint64_t in_bytes, uint64_t out_bytes, int* chosen);
 int hcl_ctx_sched_set_model(hcl_context* ctx, int global_id, double relative_throughput);
+/* SM budget of a logical device (hcl_device_set_sm_budget) + scheduler model update. */
+int hcl_ctx_set_sm_budget(hcl_context* ctx, int global_id, int sms);
 int hcl_ctx_sched_partition_weights(hcl_context* ctx, const char* kernel, const int* gids, int n,
                                     uint64_t* weights);
 

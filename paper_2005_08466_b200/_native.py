@@ -39,6 +39,7 @@ CABI = [
     ("hcl_init", C.c_int, [i32p, C.c_int, i32p]),
     ("hcl_device_count", C.c_int, [i32p]),
     ("hcl_device_info", C.c_int, [C.c_int, i32p, f64p, i32p, u64p, C.c_char_p, C.c_int]),
+    ("hcl_device_set_sm_budget", C.c_int, [C.c_int, C.c_int]),
     ("hcl_query_registry", C.c_int, [C.c_char_p, C.c_char_p, C.c_int, C.POINTER(C.c_uint32), C.c_int, i32p]),
     ("hcl_kernel_signature", C.c_int, [C.c_char_p, C.c_char_p, u8p, u8p, C.c_int, i32p]),
     ("hcl_buffer_alloc", C.c_int, [C.c_int, C.c_uint64, C.c_uint64, C.c_uint64]),
@@ -109,6 +110,7 @@ HOST = [
     ("hcl_ctx_sched_schedule", C.c_int, [C.c_void_p, C.c_char_p, C.c_char_p, C.c_int, C.c_double, C.c_uint64,
                                          C.c_uint64, i32p]),
     ("hcl_ctx_sched_set_model", C.c_int, [C.c_void_p, C.c_int, C.c_double]),
+    ("hcl_ctx_set_sm_budget", C.c_int, [C.c_void_p, C.c_int, C.c_int]),
     ("hcl_ctx_sched_partition_weights", C.c_int, [C.c_void_p, C.c_char_p, i32p, C.c_int, u64p]),
     ("hcl_split_ranges", C.c_int, [C.c_uint64, u64p, C.c_int, u64p]),
     ("hcl_spmv_partition_ranges", C.c_int, [C.c_int64, i64p, C.c_int64, u64p, i64p]),

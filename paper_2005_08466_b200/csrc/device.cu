@@ -82,7 +82,8 @@ struct Device {
   cudaStream_t stream = nullptr;  // kernels, allocation, peer copies
   cudaStream_t h2d = nullptr;     // host -> device copies
   cudaStream_t d2h = nullptr;     // device -> host copies
-  int sm_count = 0;
+  int sm_count = 0;      // SM budget the kernels size their grids to
+  int sm_physical = 0;   // the GPU's SM count
   uint64_t hbm_bytes = 0;
   std::string name;
   std::mutex mu;
@@ -252,7 +253,7 @@ int hcl_init(const int* cuda_ordinals, int n, int* num_devices) {
       if (prop.major != 10)
         fail(ErrorCode::precondition, std::string("device ") + prop.name +
                                           " is not sm_100 (Blackwell B200); this library is built for sm_100a only");
-      d->sm_count = prop.multiProcessorCount;
+      d->sm_count = d->sm_physical = prop.multiProcessorCount;
       d->hbm_bytes = prop.totalGlobalMem;
       d->name = prop.name;
       HCL_CUDA(cudaStreamCreateWithFlags(&d->stream, cudaStreamNonBlocking));
@@ -276,6 +277,20 @@ int hcl_init(const int* cuda_ordinals, int n, int* num_devices) {
   });
 }
 
+int hcl_device_set_sm_budget(int dev, int sms) {
+  return guarded([&] {
+    Device& d = device(dev);
+    std::lock_guard<std::mutex> lock(d.mu);
+    if (sms <= 0) {  // reset to the whole GPU
+      d.sm_count = d.sm_physical;
+      return;
+    }
+    if (sms < 2 || sms > d.sm_physical)
+      fail(ErrorCode::argument, "SM budget must be in [2, " + std::to_string(d.sm_physical) + "]");
+    d.sm_count = sms & ~1;  // CTA pairs
+  });
+}
+
 int hcl_device_count(int* n) {
   return guarded([&] {
     std::lock_guard<std::mutex> lock(g_devices_mu);
@@ -288,7 +303,7 @@ int hcl_device_info(int dev, int* type, double* relative_throughput, int* sm_cou
   return guarded([&] {
     Device& d = device(dev);
     if (type) *type = 1;  // wire::DeviceType::gpu
-    if (relative_throughput) *relative_throughput = 1.0;
+    if (relative_throughput) *relative_throughput = static_cast<double>(d.sm_count) / d.sm_physical;
     if (sm_count) *sm_count = d.sm_count;
     if (hbm_bytes) *hbm_bytes = d.hbm_bytes;
     if (name && name_cap > 0) {

@@ -948,6 +948,19 @@ void HostContext::add_data_creation_ms(double ms) {
 MessageTrace& HostContext::trace() { return impl_->trace; }
 Scheduler& HostContext::scheduler() { return impl_->scheduler; }
 
+void HostContext::set_device_sm_budget(int gid, int sms) {
+  std::lock_guard lock(impl_->mu);
+  const int dev = impl_->dev_index(gid);
+  check(hcl_device_set_sm_budget(dev, sms));
+  double rel = 1.0;
+  check(hcl_device_info(dev, nullptr, &rel, nullptr, nullptr, nullptr, 0));
+  auto st = impl_->scheduler.snapshot();
+  std::vector<std::pair<int, DeviceModel>> devs;
+  for (auto& d : st.devices)
+    devs.push_back({d.global_id, d.global_id == gid ? DeviceModel{d.model.type, rel} : d.model});
+  impl_->scheduler.sync_devices(devs);
+}
+
 uint64_t HostContext::buffer_size(Handle buffer) const {
   std::lock_guard lock(impl_->mu);
   if (buffer.kind != HandleKind::buffer) fail(ErrorCode::handle, "not a buffer handle");
@@ -1201,6 +1214,9 @@ int hcl_ctx_sched_schedule(hcl_context* ctx, const char* kernel, const char* pol
     t.placement = (policy && *policy) ? haocl::Placement::auto_with(policy) : haocl::Placement::explicit_on(explicit_device);
     *chosen = ctx->ctx.scheduler().schedule(t, haocl::TaskEstimate{work, in_bytes, out_bytes});
   });
+}
+int hcl_ctx_set_sm_budget(hcl_context* ctx, int gid, int sms) {
+  return ctx_guarded([&] { ctx->ctx.set_device_sm_budget(gid, sms); });
 }
 int hcl_ctx_sched_set_model(hcl_context* ctx, int gid, double relative_throughput) {
   return ctx_guarded([&] {

@@ -297,6 +297,11 @@ class HostContext:
     def set_relative_throughput(self, gid: int, rel: float) -> None:
         check(self._L.hcl_ctx_sched_set_model(self._ctx, gid, rel))
 
+    def set_sm_budget(self, gid: int, sms: int) -> None:
+        """Give logical device `gid` a budget of `sms` SMs (its kernels size their
+        grids to it; the scheduler model becomes sms / SM count)."""
+        check(self._L.hcl_ctx_set_sm_budget(self._ctx, gid, sms))
+
     def partition_weights(self, kernel: str, gids: Sequence[int]) -> list[int]:
         g = (C.c_int * len(gids))(*gids)
         w = (C.c_uint64 * len(gids))()

@@ -242,3 +242,24 @@ def test_async_copies_respect_raw_and_war(ctx, queues):
     ctx.finish(q)
     for i in range(8):
         assert (outs[i] == ins[i] + 2.0).all(), i
+
+
+def test_sm_budget_emulated_heterogeneity(ctx, queues):
+    """A logical device with an SM budget sizes its grids to it (slower, same
+    results) and the scheduler's model follows (relative_throughput)."""
+    gids = ctx.get_device_ids()
+    m = n = k = 2048
+    a = O.gen_bf16(m * k, 42)
+    b = O.gen_bf16(k * n, 43)
+    outs = {}
+    try:
+        ctx.set_sm_budget(gids[1], 16)
+        with pytest.raises(HaoclError) as e:
+            ctx.set_sm_budget(gids[1], 100000)
+        assert e.value.name == "argument"
+        for qi in (0, 1):
+            res = run(ctx, "gemm_bf16", [a, b, ("out", m * n * 4), m, k, n, 1], [2], [queues[qi]], bundle="b200")
+            outs[qi] = res[2].tobytes()
+    finally:
+        ctx.set_sm_budget(gids[1], 0)
+    assert outs[0] == outs[1]
