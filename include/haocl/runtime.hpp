@@ -255,7 +255,10 @@ class HostContext {
                                 bool blocking = true);
   Handle enqueue_ndrange_kernel(Handle queue, Handle kernel, std::array<uint64_t, 3> global_size = {1, 1, 1},
                                 uint32_t dims = 1);
-  // Partitioned NDRange over several queues (one device each).
+  // Partitioned NDRange over several queues (one device each). No weights and
+  // no bounds: the split follows the scheduler's EMA-profiled rates per
+  // (device, kernel), with 2% hysteresis so profiling noise does not move
+  // shards between devices on every launch.
   Handle enqueue_ndrange_kernel(Handle kernel, std::array<uint64_t, 3> global_size, uint32_t dims,
                                 const std::vector<Handle>& queues, std::vector<uint64_t> weights = {},
                                 std::vector<uint64_t> bounds = {});  // explicit row boundaries (parts+1), e.g. nnz-balanced

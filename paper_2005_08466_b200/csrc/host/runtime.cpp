@@ -103,6 +103,8 @@ struct HostContext::Impl {
     uint32_t arity = 0;
     std::vector<uint8_t> kinds, classes;
     std::map<uint32_t, Arg> args;
+    // last rate-driven split (hysteresis against EMA noise moving shards)
+    std::vector<uint64_t> last_bounds, last_queues;
   };
 
   GlobalDeviceMap device_map;
@@ -742,7 +744,27 @@ Handle HostContext::enqueue_ndrange_kernel(Handle kernel, std::array<uint64_t, 3
   for (uint32_t d = 0; d < dims && d < 3; ++d)
     if (global_size[d] < 1) fail(ErrorCode::argument, "global_size extents must be >= 1");
   if (bounds.empty()) {
+    const bool profiled = weights.empty();
     bounds = partition_plan(kernel, global_size, queues, std::move(weights));
+    if (profiled) {
+      // Rate-driven split: keep the previous boundaries unless some boundary
+      // moves by more than 2% of the range -- EMA noise must not migrate
+      // shards between devices on every launch.
+      Impl::KernelRec& kr = impl_->kernel(kernel.id);
+      std::vector<uint64_t> qids;
+      for (const Handle& h : queues) qids.push_back(h.id);
+      if (kr.last_queues == qids && kr.last_bounds.size() == bounds.size() && kr.last_bounds.back() == bounds.back()) {
+        const uint64_t tol = std::max<uint64_t>(1, global_size[0] / 50);
+        bool small = true;
+        for (size_t i = 0; i < bounds.size(); ++i) {
+          const uint64_t d = bounds[i] > kr.last_bounds[i] ? bounds[i] - kr.last_bounds[i] : kr.last_bounds[i] - bounds[i];
+          if (d > tol) small = false;
+        }
+        if (small) bounds = kr.last_bounds;
+      }
+      kr.last_bounds = bounds;
+      kr.last_queues = qids;
+    }
   } else {
     if (bounds.size() != queues.size() + 1 || bounds.front() != 0 || bounds.back() != global_size[0])
       fail(ErrorCode::argument, "bounds must hold parts+1 boundaries from 0 to global_size[0]");

@@ -263,3 +263,44 @@ def test_sm_budget_emulated_heterogeneity(ctx, queues):
     finally:
         ctx.set_sm_budget(gids[1], 0)
     assert outs[0] == outs[1]
+
+
+def test_rate_driven_split(ctx, queues):
+    """Partitioned launches without weights follow the EMA-profiled rates
+    (Scheduler::partition_weights, proj/src/scheduler.cpp:136-149 generalised):
+    a device with a quarter of the SMs ends up with well under half the rows,
+    and the output equals the whole launch bit-for-bit."""
+    gids = ctx.get_device_ids()
+    m, n, k = 8192, 2048, 2048
+    a = O.gen_bf16(m * k, 5)
+    b = O.gen_bf16(k * n, 6)
+    prog = ctx.create_program("b200")
+    kh = ctx.create_kernel(prog, "gemm_bf16")
+    ba, bb, bc = ctx.create_buffer(a.nbytes), ctx.create_buffer(b.nbytes), ctx.create_buffer(m * n * 4)
+    qs = [queues[2], queues[3]]
+    try:
+        ctx.set_sm_budget(gids[2], 120)
+        ctx.set_sm_budget(gids[3], 28)
+        ctx.enqueue_write_buffer(qs[0], ba, a)
+        ctx.enqueue_write_buffer(qs[0], bb, b)
+        for i, v in enumerate([ba, bb, bc, m, k, n, 1]):
+            ctx.set_kernel_arg(kh, i, v)
+        plan0 = ctx.partition_plan(kh, (m, n, 1), qs)
+        for _ in range(4):
+            for _ in range(3):
+                ctx.enqueue_ndrange_partitioned(kh, (m, n, 1), 2, qs)
+            for q in qs:
+                ctx.finish(q)
+        plan = ctx.partition_plan(kh, (m, n, 1), qs)
+        got = ctx.enqueue_read_buffer(qs[0], bc).tobytes()
+        ctx.enqueue_ndrange_kernel(queues[0], kh, (m, n, 1), 2)
+        ctx.finish(queues[0])
+        whole = ctx.enqueue_read_buffer(queues[0], bc).tobytes()
+    finally:
+        ctx.set_sm_budget(gids[2], 0)
+        ctx.set_sm_budget(gids[3], 0)
+        for h in (ba, bb, bc, kh, prog):
+            ctx.release(h)
+    assert plan0[1] > m * 0.7  # model: 120 vs 28 SMs
+    assert plan[1] > m * 0.65, plan  # profiled rates agree
+    assert got == whole
