@@ -204,6 +204,10 @@ class Scheduler {
   // to each device's measured (EMA) rate for the kernel, else its modeled rate.
   // Equal rates give equal weights (and so the reference's block_range split).
   std::vector<uint64_t> partition_weights(const std::string& kernel_name, const std::vector<int>& gids) const;
+  // Persisted EMA profiles: "gid<TAB>kernel<TAB>rate" lines (exact round trip).
+  // import replaces the rates of the listed devices it knows; returns how many.
+  std::string export_profiles() const;
+  size_t import_profiles(const std::string& text);
 
  private:
   struct Impl;

@@ -101,6 +101,8 @@ int hcl_ctx_sched_rate(hcl_context* ctx, int global_id, const char* kernel, doub
 int hcl_ctx_sched_schedule(hcl_context* ctx, const char* kernel, const char* policy, int explicit_device,
                            double work_units, uint64_t in_bytes, uint64_t out_bytes, int* chosen);
 int hcl_ctx_sched_set_model(hcl_context* ctx, int global_id, double relative_throughput);
+int hcl_ctx_sched_save_profiles(hcl_context* ctx, const char* path);
+int hcl_ctx_sched_load_profiles(hcl_context* ctx, const char* path, int* loaded);
 /* SM budget of a logical device (hcl_device_set_sm_budget) + scheduler model update. */
 int hcl_ctx_set_sm_budget(hcl_context* ctx, int global_id, int sms);
 int hcl_ctx_sched_partition_weights(hcl_context* ctx, const char* kernel, const int* gids, int n,
@@ -127,6 +129,9 @@ int hcl_sched_register_fixed_policy(hcl_scheduler* s, const char* name, int gid)
 int hcl_sched_modeled_cost(hcl_scheduler* s, int global_id, const char* kernel, double work_units,
                            uint64_t in_bytes, uint64_t out_bytes, int resident, double* cost);
 int hcl_sched_partition_weights(hcl_scheduler* s, const char* kernel, const int* gids, int n, uint64_t* weights);
+/* Persist / restore the EMA profiles (text, one "gid<TAB>kernel<TAB>rate" per line). */
+int hcl_sched_save_profiles(hcl_scheduler* s, const char* path);
+int hcl_sched_load_profiles(hcl_scheduler* s, const char* path, int* loaded);
 
 #ifdef __cplusplus
 }

@@ -110,6 +110,8 @@ HOST = [
     ("hcl_ctx_sched_schedule", C.c_int, [C.c_void_p, C.c_char_p, C.c_char_p, C.c_int, C.c_double, C.c_uint64,
                                          C.c_uint64, i32p]),
     ("hcl_ctx_sched_set_model", C.c_int, [C.c_void_p, C.c_int, C.c_double]),
+    ("hcl_ctx_sched_save_profiles", C.c_int, [C.c_void_p, C.c_char_p]),
+    ("hcl_ctx_sched_load_profiles", C.c_int, [C.c_void_p, C.c_char_p, i32p]),
     ("hcl_ctx_set_sm_budget", C.c_int, [C.c_void_p, C.c_int, C.c_int]),
     ("hcl_ctx_sched_partition_weights", C.c_int, [C.c_void_p, C.c_char_p, i32p, C.c_int, u64p]),
     ("hcl_split_ranges", C.c_int, [C.c_uint64, u64p, C.c_int, u64p]),
@@ -126,6 +128,8 @@ HOST = [
     ("hcl_sched_modeled_cost", C.c_int, [C.c_void_p, C.c_int, C.c_char_p, C.c_double, C.c_uint64, C.c_uint64,
                                          C.c_int, f64p]),
     ("hcl_sched_partition_weights", C.c_int, [C.c_void_p, C.c_char_p, i32p, C.c_int, u64p]),
+    ("hcl_sched_save_profiles", C.c_int, [C.c_void_p, C.c_char_p]),
+    ("hcl_sched_load_profiles", C.c_int, [C.c_void_p, C.c_char_p, i32p]),
 ]
 
 DATAGEN = [

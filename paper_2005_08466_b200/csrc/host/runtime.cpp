@@ -17,6 +17,7 @@
 #include <algorithm>
 #include <atomic>
 #include <chrono>
+#include <cstdio>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -1235,6 +1236,28 @@ int hcl_ctx_sched_schedule(hcl_context* ctx, const char* kernel, const char* pol
     t.kernel_name = kernel;
     t.placement = (policy && *policy) ? haocl::Placement::auto_with(policy) : haocl::Placement::explicit_on(explicit_device);
     *chosen = ctx->ctx.scheduler().schedule(t, haocl::TaskEstimate{work, in_bytes, out_bytes});
+  });
+}
+int hcl_ctx_sched_save_profiles(hcl_context* ctx, const char* path) {
+  return ctx_guarded([&] {
+    std::FILE* f = std::fopen(path, "wb");
+    if (!f) throw haocl::Error(haocl::ErrorCode::argument, std::string("cannot write ") + path);
+    const std::string t = ctx->ctx.scheduler().export_profiles();
+    const bool ok = std::fwrite(t.data(), 1, t.size(), f) == t.size();
+    std::fclose(f);
+    if (!ok) throw haocl::Error(haocl::ErrorCode::argument, std::string("short write to ") + path);
+  });
+}
+int hcl_ctx_sched_load_profiles(hcl_context* ctx, const char* path, int* loaded) {
+  return ctx_guarded([&] {
+    std::FILE* f = std::fopen(path, "rb");
+    if (!f) throw haocl::Error(haocl::ErrorCode::argument, std::string("cannot read ") + path);
+    std::string t;
+    char buf[4096];
+    for (size_t n; (n = std::fread(buf, 1, sizeof buf, f)) > 0;) t.append(buf, n);
+    std::fclose(f);
+    const size_t n = ctx->ctx.scheduler().import_profiles(t);
+    if (loaded) *loaded = static_cast<int>(n);
   });
 }
 int hcl_ctx_set_sm_budget(hcl_context* ctx, int gid, int sms) {

@@ -9,7 +9,11 @@
 #include <algorithm>
 #include <atomic>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <fstream>
+#include <sstream>
 #include <limits>
 #include <mutex>
 
@@ -160,6 +164,43 @@ void Scheduler::record_profile(int global_id, const std::string& kernel_name, do
     d->profiled_rate[kernel_name] = sample;
   else
     it->second = impl_->options.ema_alpha * sample + (1.0 - impl_->options.ema_alpha) * it->second;
+}
+
+// Persisted profiles (§8(f) 2): one "gid<TAB>kernel<TAB>rate" line per
+// (device, kernel) EMA rate, %.17g so a round trip is exact.
+std::string Scheduler::export_profiles() const {
+  std::lock_guard lock(impl_->mu);
+  std::string out;
+  char buf[64];
+  for (const auto& d : impl_->state.devices)
+    for (const auto& [kernel, rate] : d.profiled_rate) {
+      std::snprintf(buf, sizeof buf, "\t%.17g\n", rate);
+      out += std::to_string(d.global_id) + "\t" + kernel + buf;
+    }
+  return out;
+}
+
+size_t Scheduler::import_profiles(const std::string& text) {
+  std::lock_guard lock(impl_->mu);
+  size_t n = 0, pos = 0;
+  while (pos < text.size()) {
+    size_t eol = text.find('\n', pos);
+    if (eol == std::string::npos) eol = text.size();
+    const std::string line = text.substr(pos, eol - pos);
+    pos = eol + 1;
+    if (line.empty()) continue;
+    const size_t t1 = line.find('\t'), t2 = t1 == std::string::npos ? t1 : line.find('\t', t1 + 1);
+    if (t2 == std::string::npos) fail(ErrorCode::parse, "profile line needs gid<TAB>kernel<TAB>rate: " + line);
+    char* end = nullptr;
+    const long gid = std::strtol(line.c_str(), &end, 10);
+    const double rate = std::strtod(line.c_str() + t2 + 1, &end);
+    if (!(rate > 0.0)) fail(ErrorCode::parse, "profile rate must be > 0: " + line);
+    DeviceState* d = impl_->state.find(static_cast<int>(gid));
+    if (!d) continue;  // a device this run does not have
+    d->profiled_rate[line.substr(t1 + 1, t2 - t1 - 1)] = rate;
+    ++n;
+  }
+  return n;
 }
 
 void Scheduler::sync_devices(const std::vector<std::pair<int, DeviceModel>>& devices) {
@@ -348,6 +389,31 @@ int hcl_sched_schedule(hcl_scheduler* s, const char* kernel, const char* policy,
 
 int hcl_sched_record_profile(hcl_scheduler* s, int gid, const char* kernel, double work, double seconds) {
   return host_guarded([&] { s->sched.record_profile(gid, kernel, work, seconds); });
+}
+
+namespace {
+void save_text(const std::string& path, const std::string& text) {
+  std::ofstream f(path, std::ios::binary | std::ios::trunc);
+  if (!f) throw haocl::Error(haocl::ErrorCode::argument, "cannot write " + path);
+  f << text;
+}
+std::string load_text(const std::string& path) {
+  std::ifstream f(path, std::ios::binary);
+  if (!f) throw haocl::Error(haocl::ErrorCode::argument, "cannot read " + path);
+  std::stringstream ss;
+  ss << f.rdbuf();
+  return ss.str();
+}
+}  // namespace
+
+int hcl_sched_save_profiles(hcl_scheduler* s, const char* path) {
+  return host_guarded([&] { save_text(path, s->sched.export_profiles()); });
+}
+int hcl_sched_load_profiles(hcl_scheduler* s, const char* path, int* loaded) {
+  return host_guarded([&] {
+    size_t n = s->sched.import_profiles(load_text(path));
+    if (loaded) *loaded = static_cast<int>(n);
+  });
 }
 
 int hcl_sched_rate(hcl_scheduler* s, int gid, const char* kernel, double* rate) {

@@ -9,6 +9,7 @@ for released handles), so parity tests read like the reference's own.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass, field
 from enum import IntEnum
 from typing import Iterable, Optional, Sequence
@@ -297,6 +298,15 @@ class HostContext:
     def set_relative_throughput(self, gid: int, rel: float) -> None:
         check(self._L.hcl_ctx_sched_set_model(self._ctx, gid, rel))
 
+    def save_profiles(self, path: str) -> None:
+        """Persist the scheduler's EMA rates per (device, kernel) (§8(f) 2)."""
+        check(self._L.hcl_ctx_sched_save_profiles(self._ctx, os.fsencode(path)))
+
+    def load_profiles(self, path: str) -> int:
+        n = C.c_int()
+        check(self._L.hcl_ctx_sched_load_profiles(self._ctx, os.fsencode(path), C.byref(n)))
+        return n.value
+
     def set_sm_budget(self, gid: int, sms: int) -> None:
         """Give logical device `gid` a budget of `sms` SMs (its kernels size their
         grids to it; the scheduler model becomes sms / SM count)."""
@@ -387,3 +397,11 @@ class Scheduler:
         w = (C.c_uint64 * len(gids))()
         check(N.lib().hcl_sched_partition_weights(self._s, kernel.encode(), g, len(gids), w))
         return list(w)
+
+    def save_profiles(self, path: str) -> None:
+        check(N.lib().hcl_sched_save_profiles(self._s, os.fsencode(path)))
+
+    def load_profiles(self, path: str) -> int:
+        n = C.c_int()
+        check(N.lib().hcl_sched_load_profiles(self._s, os.fsencode(path), C.byref(n)))
+        return n.value

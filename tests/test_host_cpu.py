@@ -203,3 +203,26 @@ def test_product_datagen_matches_oracle_streams():
     s2, d2 = O.rmat_edges(12, 5, 70000, 42)
     assert (s == s2).all() and (d == d2).all()
     assert (G.gen_kmeans_points(70000, 8, 16, 42, first=3) == O.kmeans_points(42, 3, 70000, 8, 16)).all()
+
+
+def test_scheduler_profiles_persist(tmp_path):
+    """EMA profiles survive a save/load round trip exactly (§8(f) 2) and drive
+    the same partition weights; devices the new run lacks are skipped."""
+    from paper_2005_08466_b200 import HaoclError, Scheduler
+
+    s = Scheduler([(1, 1.0), (2, 1.0), (3, 1.0)])
+    for sec in (0.010, 0.012, 0.011):
+        s.record_profile(1, "conv3x3", 1e9, sec)
+        s.record_profile(2, "conv3x3", 1e9, sec * 2.1)
+    s.record_profile(3, "gemm_bf16", 5e12, 0.0037)
+    path = str(tmp_path / "profiles.tsv")
+    s.save_profiles(path)
+    t = Scheduler([(1, 1.0), (2, 1.0)])
+    assert t.load_profiles(path) == 2  # device 3 is not in this run
+    assert t.rate(1, "conv3x3") == s.rate(1, "conv3x3") and t.rate(2, "conv3x3") == s.rate(2, "conv3x3")
+    assert t.partition_weights("conv3x3", [1, 2]) == s.partition_weights("conv3x3", [1, 2])
+    bad = tmp_path / "bad.tsv"
+    bad.write_text("1 conv3x3 5\n")
+    with pytest.raises(HaoclError) as e:
+        t.load_profiles(str(bad))
+    assert e.value.name == "parse"
