@@ -33,6 +33,10 @@ def ctx():
         pytest.skip("needs a GPU")
     from paper_2005_08466_b200 import HostContext
 
-    c = HostContext([0, 0, 0, 0])
+    # on a multi-GPU box the other GPUs are appended as devices 4.. (one per
+    # GPU) for tests/test_gpu_multi.py; the first four stay logical devices of GPU 0
+    ordinals = [0, 0, 0, 0] + list(range(1, torch.cuda.device_count()))
+    c = HostContext(ordinals)
+    c.cuda_ordinals = ordinals
     yield c
     c.close()
