@@ -137,8 +137,8 @@ int hcl_nccl_init(int dev, int nranks, int rank, const uint8_t* id_bytes) {
     std::memcpy(&id, id_bytes, sizeof(id));
     void* s = nullptr;
     hcl_check(hcl_device_stream(dev, &s));  // validates dev
-    int ord = 0;
-    cudaGetDevice(&ord);
+    int ord = 0;  // ncclCommInitRank binds the current device
+    if (cudaStreamGetDevice(static_cast<cudaStream_t>(s), &ord) == cudaSuccess) cudaSetDevice(ord);
     ncclComm_t comm;
     nccl_check(nccl().commInitRank(&comm, nranks, id, rank), "ncclCommInitRank");
     g_comms[dev] = comm;

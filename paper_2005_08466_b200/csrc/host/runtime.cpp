@@ -343,6 +343,9 @@ struct HostContext::Impl {
       int dev = dev_index(part.gid);
       void* stream = nullptr;
       check(hcl_device_stream(dev, &stream));
+      // the events must belong to the stream's GPU (several GPUs per process)
+      int ordinal = 0;
+      if (cudaStreamGetDevice(static_cast<cudaStream_t>(stream), &ordinal) == cudaSuccess) cudaSetDevice(ordinal);
       cudaEventCreate(&l.start);
       cudaEventCreate(&l.stop);
       cudaEventRecord(l.start, static_cast<cudaStream_t>(stream));
