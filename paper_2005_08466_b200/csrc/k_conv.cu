@@ -43,6 +43,8 @@ namespace hcl {
 // from k_gemm.cu
 CUtensorMap make_tmap_2d_bf16(const void* base, uint64_t inner, uint64_t outer, uint64_t row_bytes, uint32_t box_inner,
                               uint32_t box_outer);
+CUtensorMap make_tmap_4d_bf16(const void* base, const uint64_t dims[4], const uint64_t strides[3],
+                              const uint32_t box[4]);
 
 namespace {
 
@@ -64,9 +66,16 @@ constexpr int CV2_AROWS = 136;              // 128 pixels + 2 shifted rows, padd
 constexpr int CV2_A = CV2_AROWS * 128;      // 17 KB
 constexpr int CV2_BTAP = CV_BNL * 128;      // 8 KB per tap per CTA
 constexpr int CV2_B = 9 * CV2_BTAP;         // 72 KB
-constexpr int CV2_STAGES = 8;
 constexpr int CV2_EPI = 8;                  // epilogue warps 0-7, producer 8, MMA 9
-constexpr size_t CV2_SMEM = static_cast<size_t>(CV2_B) + static_cast<size_t>(CV2_STAGES) * CV2_A + 1024 + 256;
+constexpr int CV2_OSTAGE = 32 * 128;        // per epilogue warp: 32 pixels x 64 bf16 channels (TMA-store staging)
+// bf16 output stages its tiles in shared memory for TMA stores (6 A stages);
+// fp32 output stores directly from registers (8 A stages)
+template <bool OUTF32>
+struct CV2Cfg {
+  static constexpr int kStages = OUTF32 ? 8 : 6;
+  static constexpr size_t kObytes = OUTF32 ? 0 : static_cast<size_t>(CV2_EPI) * CV2_OSTAGE;
+  static constexpr size_t kSmem = static_cast<size_t>(CV2_B) + static_cast<size_t>(kStages) * CV2_A + kObytes + 1024 + 256;
+};
 
 // One epilogue warp's share of a finished 128-pixel x 128-channel accumulator:
 // TMEM lane quadrant warp%4 (32 pixels), channel chunks [c0, c1) of 32.
@@ -112,10 +121,12 @@ struct ConvGeom {
 };
 
 // Epilogue warps' loop over this cluster's tiles (shared by v1 and v2).
+// epi_mode (HCL_CONV_EPI, diagnostics only): 0 normal, 1 skip TMEM loads and
+// stores, 2 TMEM loads without stores -- separates MMA, TMEM-read and store costs
 template <bool OUTF32, int EPI>
 __device__ __forceinline__ void conv_epilogue_loop(const ConvGeom& g, int H, int W, uint32_t rank, int warp, int lane,
                                                    uint32_t tmem_base, uint64_t* tfull, uint64_t* tempty,
-                                                   void* __restrict__ out) {
+                                                   void* __restrict__ out, int epi_mode) {
   const int cluster = blockIdx.x / 2, nclusters = gridDim.x / 2;
   const int c0 = EPI == 8 ? (warp / 4) * 2 : 0, c1 = EPI == 8 ? c0 + 2 : 4;
   int acc = 0;
@@ -124,11 +135,11 @@ __device__ __forceinline__ void conv_epilogue_loop(const ConvGeom& g, int H, int
     const int n = t / g.tiles_img;
     const int p = (t % g.tiles_img) * 2 * CV_BM + static_cast<int>(rank) * CV_BM + (warp % 4) * 32 + lane;
     const int h = p / g.Wp, w = p - h * g.Wp;
-    const bool ok = p < g.m_img && w < W;
+    const bool ok = p < g.m_img && w < W && epi_mode == 0;
     const int64_t opix = (static_cast<int64_t>(n) * H + h) * W + w;
     ptx::mbar_wait(&tfull[acc], acc_phase);
     ptx::tc_fence_after();
-    conv_epilogue<OUTF32>(tmem_base, acc, warp, c0, c1, ok, opix, out);
+    if (epi_mode != 1) conv_epilogue<OUTF32>(tmem_base, acc, warp, c0, c1, ok, opix, out);
     ptx::tc_fence_before();
     __syncwarp();
     if (lane == 0) ptx::mbar_arrive_cluster_relaxed(ptx::mapa(ptx::smem_u32(&tempty[acc]), 0));
@@ -136,10 +147,70 @@ __device__ __forceinline__ void conv_epilogue_loop(const ConvGeom& g, int H, int
   }
 }
 
+// bf16 epilogue through shared memory and TMA stores (v2): each epilogue warp
+// owns 32 consecutive virtual pixels (TMEM lane quadrant warp%4) x 64 output
+// channels (warp/4). It releases the accumulator right after its TMEM loads,
+// writes its 32 x 128-byte rows SWIZZLE_128B-swizzled into a private 4 KB
+// buffer, and one lane stores them with one or two 4D TMA boxes [1,1,32,64]
+// of the N x H x W x K output: a group that wraps into the next image row
+// takes a second box at w - Wp, and the padding columns (w >= W) and rows past
+// the image (h >= H) are out of bounds, so TMA skips them.
+__device__ __forceinline__ void conv_epilogue_loop_tma(const ConvGeom& g, int H, uint32_t rank, int warp, int lane,
+                                                       uint32_t tmem_base, uint64_t* tfull, uint64_t* tempty,
+                                                       const CUtensorMap* tmO, uint8_t* obuf, int epi_mode) {
+  const int cluster = blockIdx.x / 2, nclusters = gridDim.x / 2;
+  const int half = warp / 4;
+  int acc = 0;
+  uint32_t acc_phase = 0;
+  for (int t = cluster; t < g.tiles; t += nclusters) {
+    const int n = t / g.tiles_img;
+    const int p = (t % g.tiles_img) * 2 * CV_BM + static_cast<int>(rank) * CV_BM + (warp % 4) * 32;
+    ptx::mbar_wait(&tfull[acc], acc_phase);
+    ptx::tc_fence_after();
+    uint32_t r0[32], r1[32];
+    if (epi_mode != 1) {
+      const uint32_t ta = tmem_base + (static_cast<uint32_t>((warp % 4) * 32) << 16) +
+                          static_cast<uint32_t>(acc * CV_BN + half * 64);
+      ptx::tmem_ld_32x32b_x32(ta, r0);
+      ptx::tmem_ld_32x32b_x32(ta + 32, r1);
+      ptx::tmem_ld_wait();
+    }
+    ptx::tc_fence_before();
+    __syncwarp();
+    if (lane == 0) ptx::mbar_arrive_cluster_relaxed(ptx::mapa(ptx::smem_u32(&tempty[acc]), 0));
+    if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    if (epi_mode != 0) continue;
+    if (lane == 0) ptx::bulk_wait_read0();  // the previous store has read this buffer
+    __syncwarp();
+    uint32_t pk[32];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      __nv_bfloat162 a = __floats2bfloat162_rn(__uint_as_float(r0[2 * j]), __uint_as_float(r0[2 * j + 1]));
+      __nv_bfloat162 b = __floats2bfloat162_rn(__uint_as_float(r1[2 * j]), __uint_as_float(r1[2 * j + 1]));
+      pk[j] = *reinterpret_cast<uint32_t*>(&a);
+      pk[16 + j] = *reinterpret_cast<uint32_t*>(&b);
+    }
+    uint8_t* row = obuf + lane * 128;
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      *reinterpret_cast<uint4*>(row + ((j ^ (lane & 7)) << 4)) =
+          make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+    ptx::fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+      const int h = p / g.Wp, w = p - h * g.Wp;
+      if (h < H) ptx::tma_store_4d(tmO, obuf, half * 64, w, h, n);
+      if (w + 32 > g.Wp && h + 1 < H) ptx::tma_store_4d(tmO, obuf, half * 64, w - g.Wp, h + 1, n);
+      ptx::bulk_commit();
+    }
+  }
+  if (lane == 0) ptx::bulk_wait0();
+}
+
 template <bool OUTF32>
 __global__ void __launch_bounds__((CV1_EPI + 2) * 32, 1)
     conv3x3_v1_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                      void* __restrict__ out, int n_img, int H, int W, int C) {
+                      void* __restrict__ out, int n_img, int H, int W, int C, int epi_mode) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + CV1_STAGES * CV1_STAGE);
@@ -225,7 +296,7 @@ __global__ void __launch_bounds__((CV1_EPI + 2) * 32, 1)
     }
     __syncwarp();
   } else {
-    conv_epilogue_loop<OUTF32, CV1_EPI>(g, H, W, rank, warp, lane, tmem_base, tfull, tempty, out);
+    conv_epilogue_loop<OUTF32, CV1_EPI>(g, H, W, rank, warp, lane, tmem_base, tfull, tempty, out, epi_mode);
   }
 
   ptx::tc_fence_before();
@@ -239,12 +310,15 @@ __global__ void __launch_bounds__((CV1_EPI + 2) * 32, 1)
 template <bool OUTF32>
 __global__ void __launch_bounds__((CV2_EPI + 2) * 32, 1)
     conv3x3_v2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                      void* __restrict__ out, int n_img, int H, int W) {
+                      const __grid_constant__ CUtensorMap tmO, void* __restrict__ out, int n_img, int H, int W,
+                      int epi_mode) {
+  constexpr int CV2_STAGES = CV2Cfg<OUTF32>::kStages;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* smem_b = smem;
   uint8_t* smem_a = smem + CV2_B;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem_a + CV2_STAGES * CV2_A);
+  uint8_t* smem_o = smem_a + CV2_STAGES * CV2_A;  // 1024-aligned (72 KB + 6 x 17 KB)
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_o + CV2Cfg<OUTF32>::kObytes);
   uint64_t* empty = full + CV2_STAGES;
   uint64_t* tfull = empty + CV2_STAGES;
   uint64_t* tempty = tfull + 2;
@@ -259,6 +333,7 @@ __global__ void __launch_bounds__((CV2_EPI + 2) * 32, 1)
   if (warp == PROD && lane == 0) {
     ptx::prefetch_tmap(&tmA);
     ptx::prefetch_tmap(&tmB);
+    if constexpr (!OUTF32) ptx::prefetch_tmap(&tmO);
     for (int s = 0; s < CV2_STAGES; ++s) {
       ptx::mbar_init(&full[s], 1);
       ptx::mbar_init(&empty[s], 1);
@@ -301,10 +376,14 @@ __global__ void __launch_bounds__((CV2_EPI + 2) * 32, 1)
     }
     __syncwarp();
   } else if (warp == MMA) {
-    if (rank == 0 && lane == 0) {
+    if (rank == 0) {
+      // the whole warp runs the issue loop (uniform operands, elect.sync inside
+      // the MMA asm); descriptors are the base descriptors plus compile-time
+      // offsets in 16-byte units (the start-address field, bits 0-13)
       constexpr uint32_t idesc = ptx::umma_idesc(1, 0, 0, 2 * CV_BM, CV_BN);
       ptx::mbar_wait(bfull, 0);
-      const uint32_t b_base = ptx::smem_u32(smem_b);
+      const uint64_t bdesc0 = ptx::umma_desc_sw128(ptx::smem_u32(smem_b), 16, 1024);
+      const uint64_t adesc0 = ptx::umma_desc_sw128(ptx::smem_u32(smem_a), 16, 1024);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
@@ -316,26 +395,30 @@ __global__ void __launch_bounds__((CV2_EPI + 2) * 32, 1)
         for (int r = 0; r < 3; ++r) {
           ptx::mbar_wait(&full[stage], phase);
           ptx::tc_fence_after();
-          const uint32_t a_addr = ptx::smem_u32(smem_a + stage * CV2_A);
+          const uint64_t adesc = adesc0 + static_cast<uint64_t>((stage * CV2_A) >> 4);
 #pragma unroll
           for (int s = 0; s < 3; ++s) {
             const int tap = r * 3 + s;
 #pragma unroll
             for (int k = 0; k < 4; ++k)
-              ptx::mma<2, false>(d_tmem, ptx::umma_desc_sw128(a_addr + s * 128 + k * 32, 16, 1024),
-                                 ptx::umma_desc_sw128(b_base + tap * CV2_BTAP + k * 32, 16, 1024), idesc,
-                                 (r | s | k) != 0);
+              ptx::mma_elect<2, false>(d_tmem, adesc + static_cast<uint64_t>((s * 128 + k * 32) >> 4),
+                                       bdesc0 + static_cast<uint64_t>((tap * CV2_BTAP + k * 32) >> 4), idesc,
+                                       (r | s | k) != 0);
           }
-          ptx::mma_commit<2>(&empty[stage]);
+          ptx::mma_commit_elect<2>(&empty[stage]);
           if (++stage == CV2_STAGES) { stage = 0; phase ^= 1; }
         }
-        ptx::mma_commit<2>(&tfull[acc]);
+        ptx::mma_commit_elect<2>(&tfull[acc]);
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
     }
     __syncwarp();
   } else {
-    conv_epilogue_loop<OUTF32, CV2_EPI>(g, H, W, rank, warp, lane, tmem_base, tfull, tempty, out);
+    if constexpr (OUTF32)
+      conv_epilogue_loop<OUTF32, CV2_EPI>(g, H, W, rank, warp, lane, tmem_base, tfull, tempty, out, epi_mode);
+    else
+      conv_epilogue_loop_tma(g, H, rank, warp, lane, tmem_base, tfull, tempty, &tmO, smem_o + warp * CV2_OSTAGE,
+                             epi_mode);
   }
 
   ptx::tc_fence_before();
@@ -392,7 +475,16 @@ uint64_t launch_conv(LaunchCtx& c) {
                              : reinterpret_cast<void*>(conv3x3_v2_kernel<false>))
                   : (out_f32 ? reinterpret_cast<void*>(conv3x3_v1_kernel<true>)
                              : reinterpret_cast<void*>(conv3x3_v1_kernel<false>));
-  const size_t smem = v2 ? CV2_SMEM : CV1_SMEM;
+  const size_t smem = v2 ? (out_f32 ? CV2Cfg<true>::kSmem : CV2Cfg<false>::kSmem) : CV1_SMEM;
+  // bf16 output tensor N x H x W x K for the v2 TMA-store epilogue
+  CUtensorMap to{};
+  if (v2 && !out_f32) {
+    const uint64_t od[4] = {static_cast<uint64_t>(K), static_cast<uint64_t>(W), static_cast<uint64_t>(H), cnt};
+    const uint64_t os[3] = {static_cast<uint64_t>(K) * 2, static_cast<uint64_t>(W) * K * 2,
+                            static_cast<uint64_t>(H) * W * K * 2};
+    const uint32_t ob[4] = {64, 32, 1, 1};
+    to = make_tmap_4d_bf16(outp, od, os, ob);
+  }
   HCL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   const int64_t tiles_img = ceil_div(H * (W + 2), 2 * CV_BM);
   const int64_t clusters = std::min<int64_t>(static_cast<int64_t>(cnt) * tiles_img, c.sm_count / 2);
@@ -410,8 +502,11 @@ uint64_t launch_conv(LaunchCtx& c) {
   cfg.numAttrs = 1;
   void* outv = static_cast<void*>(outp);
   int cn = static_cast<int>(cnt), hh = static_cast<int>(H), ww = static_cast<int>(W), cc = static_cast<int>(C);
-  void* params[] = {&ta, &tb, &outv, &cn, &hh, &ww, &cc};  // v2 takes the first six
-  HCL_CUDA(cudaLaunchKernelExC(&cfg, kern, params));
+  const char* epi_env = std::getenv("HCL_CONV_EPI");
+  int epi_mode = epi_env ? std::atoi(epi_env) : 0;
+  void* params_v1[] = {&ta, &tb, &outv, &cn, &hh, &ww, &cc, &epi_mode};
+  void* params_v2[] = {&ta, &tb, &to, &outv, &cn, &hh, &ww, &epi_mode};
+  HCL_CUDA(cudaLaunchKernelExC(&cfg, kern, v2 ? params_v2 : params_v1));
   HCL_LAUNCHED();
   return 2ull * cnt * H * W * K * 9 * C;
 }

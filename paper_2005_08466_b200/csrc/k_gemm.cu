@@ -153,8 +153,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncwarp();
   } else if (warp == 5) {
     // ---------------- MMA issuer (leader CTA) ----------------
-    if (rank == 0 && lane == 0) {
+    if (rank == 0) {
+      // whole warp issues (uniform operands; elect.sync inside the asm);
+      // descriptors = stage-0 descriptors + offsets in 16-byte units
       constexpr uint32_t idesc = ptx::umma_idesc(TF32 ? 2 : 1, 0, BMN ? 1 : 0, kBM * CG, kBN);
+      const uint32_t a0 = ptx::smem_u32(smem);
+      const uint64_t adesc0 = ptx::umma_desc_sw128(a0, 16, 1024);
+      const uint64_t bdesc0 = BMN ? ptx::umma_desc_sw128(a0 + C::kABytes, C::kBK * 128, 1024)
+                                  : ptx::umma_desc_sw128(a0 + C::kABytes, 16, 1024);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
@@ -166,22 +172,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int kb = 0; kb < nk; ++kb) {
           ptx::mbar_wait(&full[stage], phase);
           ptx::tc_fence_after();
-          const uint32_t a_addr = ptx::smem_u32(smem + stage * C::kStage);
-          const uint32_t b_addr = a_addr + C::kABytes;
+          const uint64_t so = static_cast<uint64_t>((stage * C::kStage) >> 4);
 #pragma unroll
           for (int k = 0; k < C::kBK / C::kUK; ++k) {
-            const uint64_t adesc = ptx::umma_desc_sw128(a_addr + k * 32, 16, 1024);
-            uint64_t bdesc;
-            if constexpr (BMN)
-              bdesc = ptx::umma_desc_sw128(b_addr + k * (C::kUK / 8) * 1024, C::kBK * 128, 1024);
-            else
-              bdesc = ptx::umma_desc_sw128(b_addr + k * 32, 16, 1024);
-            ptx::mma<CG, TF32>(d_tmem, adesc, bdesc, idesc, (kb | k) != 0);
+            const uint64_t adesc = adesc0 + so + static_cast<uint64_t>((k * 32) >> 4);
+            const uint64_t bdesc = bdesc0 + so + static_cast<uint64_t>((BMN ? k * (C::kUK / 8) * 1024 : k * 32) >> 4);
+            ptx::mma_elect<CG, TF32>(d_tmem, adesc, bdesc, idesc, (kb | k) != 0);
           }
-          ptx::mma_commit<CG>(&empty[stage]);  // frees the smem slot when these MMAs finish
+          ptx::mma_commit_elect<CG>(&empty[stage]);  // frees the smem slot when these MMAs finish
           if (++stage == C::kStages) { stage = 0; phase ^= 1; }
         }
-        ptx::mma_commit<CG>(&tfull[acc]);  // accumulator ready for the epilogue
+        ptx::mma_commit_elect<CG>(&tfull[acc]);  // accumulator ready for the epilogue
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
     }
@@ -673,6 +674,23 @@ uint64_t rowbytes_gemm_f32(const int64_t* s, uint32_t, uint32_t i) {
 CUtensorMap make_tmap_2d_bf16(const void* base, uint64_t inner, uint64_t outer, uint64_t row_bytes, uint32_t box_inner,
                               uint32_t box_outer) {
   return make_tmap(base, false, inner, outer, row_bytes, box_inner, box_outer);
+}
+
+// 4D bf16 tensor (dims[0] innermost), SWIZZLE_128B box; strides[i] = byte
+// pitch of dimension i+1. Out-of-bounds box elements are skipped by stores.
+CUtensorMap make_tmap_4d_bf16(const void* base, const uint64_t dims[4], const uint64_t strides[3],
+                              const uint32_t box[4]) {
+  CUtensorMap m;
+  cuuint64_t d[4] = {dims[0], dims[1], dims[2], dims[3]};
+  cuuint64_t s[3] = {strides[0], strides[1], strides[2]};
+  cuuint32_t b[4] = {box[0], box[1], box[2], box[3]};
+  cuuint32_t e[4] = {1, 1, 1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), d, s, b, e,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    fail(ErrorCode::argument, "cuTensorMapEncodeTiled (4D) failed (" + std::to_string(static_cast<int>(r)) + ")");
+  return m;
 }
 
 void register_gemm(std::vector<KernelDef>& r) {

@@ -99,6 +99,27 @@ __device__ __forceinline__ void tma_load_2d_pair(void* smem, const CUtensorMap* 
       : "memory");
 }
 
+// ---- TMA stores (smem -> global, bulk-group completion) --------------------
+
+// generic-proxy smem writes -> visible to the async proxy (before a TMA store)
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ void tma_store_4d(const CUtensorMap* m, const void* smem, int c0, int c1, int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(
+          reinterpret_cast<uint64_t>(m)),
+      "r"(smem_u32(smem)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+// the smem source of every committed store has been read (buffer reusable)
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+// every committed store has completed
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
 // ---- tcgen05 ---------------------------------------------------------------
 
 template <int CG>
@@ -149,6 +170,41 @@ __device__ __forceinline__ void mma(uint32_t d_tmem, uint64_t adesc, uint64_t bd
         "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
         "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+// Warp-collective forms: the whole (converged) warp calls them with
+// warp-uniform operands and elect.sync picks the issuing lane inside the asm,
+// so the operands stay in uniform registers -- no per-MMA R2UR waterfall loop,
+// which at 64-cycle N=128 MMAs is what limits issue (profiles/r01_conv_ncu_summary.txt).
+template <int CG, bool TF32>
+__device__ __forceinline__ void mma_elect(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                          uint32_t accumulate) {
+#define HCL_MMA_ELECT(KIND, G)                                                                   \
+  asm volatile(                                                                                  \
+      "{\n\t.reg .pred e, p;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"       \
+      "@e tcgen05.mma.cta_group::" #G ".kind::" #KIND " [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem), \
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate))
+  if constexpr (CG == 1 && !TF32) HCL_MMA_ELECT(f16, 1);
+  else if constexpr (CG == 2 && !TF32) HCL_MMA_ELECT(f16, 2);
+  else if constexpr (CG == 1 && TF32) HCL_MMA_ELECT(tf32, 1);
+  else HCL_MMA_ELECT(tf32, 2);
+#undef HCL_MMA_ELECT
+}
+
+template <int CG>
+__device__ __forceinline__ void mma_commit_elect(uint64_t* bar) {
+  if constexpr (CG == 1)
+    asm volatile(
+        "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_u32(bar))
+        : "memory");
+  else
+    asm volatile(
+        "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}" ::"r"(
+            smem_u32(bar)),
+        "h"(static_cast<uint16_t>(0x3))
+        : "memory");
 }
 
 // Arrive on `bar` (same smem offset in every CTA of `mask`) when all prior
