@@ -151,13 +151,14 @@ __device__ __forceinline__ void conv_epilogue_loop(const ConvGeom& g, int H, int
 // owns 32 consecutive virtual pixels (TMEM lane quadrant warp%4) x 64 output
 // channels (warp/4). It releases the accumulator right after its TMEM loads,
 // writes its 32 x 128-byte rows SWIZZLE_128B-swizzled into a private 4 KB
-// buffer, and one lane stores them with one or two 4D TMA boxes [1,1,32,64]
-// of the N x H x W x K output: a group that wraps into the next image row
-// takes a second box at w - Wp, and the padding columns (w >= W) and rows past
-// the image (h >= H) are out of bounds, so TMA skips them.
-__device__ __forceinline__ void conv_epilogue_loop_tma(const ConvGeom& g, int H, uint32_t rank, int warp, int lane,
-                                                       uint32_t tmem_base, uint64_t* tfull, uint64_t* tempty,
-                                                       const CUtensorMap* tmO, uint8_t* obuf, int epi_mode) {
+// buffer, and one lane stores them with a 4D TMA box [1,1,32,64]
+// of the N x H x W x K output; a group that wraps into the next image row
+// stores its wrapped lanes directly from registers; the padding columns
+// (w >= W) and rows past the image (h >= H) are out of bounds, so TMA skips them.
+__device__ __forceinline__ void conv_epilogue_loop_tma(const ConvGeom& g, int H, int W, uint32_t rank, int warp,
+                                                       int lane, uint32_t tmem_base, uint64_t* tfull,
+                                                       uint64_t* tempty, const CUtensorMap* tmO, uint8_t* obuf,
+                                                       void* __restrict__ out, int epi_mode) {
   const int cluster = blockIdx.x / 2, nclusters = gridDim.x / 2;
   const int half = warp / 4;
   int acc = 0;
@@ -197,11 +198,20 @@ __device__ __forceinline__ void conv_epilogue_loop_tma(const ConvGeom& g, int H,
           make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
     ptx::fence_proxy_async_smem();
     __syncwarp();
+    const int h = p / g.Wp, w = p - h * g.Wp;
     if (lane == 0) {
-      const int h = p / g.Wp, w = p - h * g.Wp;
       if (h < H) ptx::tma_store_4d(tmO, obuf, half * 64, w, h, n);
-      if (w + 32 > g.Wp && h + 1 < H) ptx::tma_store_4d(tmO, obuf, half * 64, w - g.Wp, h + 1, n);
       ptx::bulk_commit();
+    }
+    // a group that wraps into the next image row: those lanes store their
+    // 128 bytes directly (TMA box starts cannot be negative)
+    const int j0 = g.Wp - w;
+    if (lane >= j0 && h + 1 < H) {
+      uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(out) +
+                                            ((static_cast<int64_t>(n) * H + h + 1) * W + (lane - j0)) * CV_BN +
+                                            half * 64);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) dst[j] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
     }
   }
   if (lane == 0) ptx::bulk_wait0();
@@ -417,8 +427,8 @@ __global__ void __launch_bounds__((CV2_EPI + 2) * 32, 1)
     if constexpr (OUTF32)
       conv_epilogue_loop<OUTF32, CV2_EPI>(g, H, W, rank, warp, lane, tmem_base, tfull, tempty, out, epi_mode);
     else
-      conv_epilogue_loop_tma(g, H, rank, warp, lane, tmem_base, tfull, tempty, &tmO, smem_o + warp * CV2_OSTAGE,
-                             epi_mode);
+      conv_epilogue_loop_tma(g, H, W, rank, warp, lane, tmem_base, tfull, tempty, &tmO, smem_o + warp * CV2_OSTAGE,
+                             out, epi_mode);
   }
 
   ptx::tc_fence_before();

@@ -47,7 +47,8 @@ def run(ctx, queues, n, h, wd, c, k, out_f32, P=1, weights=None):
     return xb, wb, got
 
 
-@pytest.mark.parametrize("n,h,wd,c,out_f32", [(2, 16, 16, 64, True), (3, 7, 37, 128, True), (2, 12, 30, 64, False)])
+@pytest.mark.parametrize("n,h,wd,c,out_f32", [(2, 16, 16, 64, True), (3, 7, 37, 128, True), (2, 12, 30, 64, False),
+                                             (3, 9, 50, 64, False), (2, 5, 224, 64, False)])
 def test_conv_matches_fp64_reference(ctx, queues, n, h, wd, c, out_f32):
     k = 128
     xb, wb, got = run(ctx, queues, n, h, wd, c, k, out_f32)
