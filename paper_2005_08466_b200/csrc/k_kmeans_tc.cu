@@ -1,0 +1,469 @@
+// Tensor-core filtered k-means assignment (config C4; SURVEY.md §8(d) C4 "with
+// tensor filtering"). Same result as kmeans_assign -- the exact fp32 argmin of
+// sum_j (c_kj - x_j)^2 (every operation separately rounded, j ascending, ties
+// to the smaller k; the reference's knn k=1, proj/src/kernels.cpp:195-233) --
+// but the 2*N*K*D distance work runs on the 5th-generation tensor cores:
+//
+//   1. score: s~_k = x . c_k by tcgen05 bf16 MMAs with fp32 accumulation, on
+//      split operands x = xh + xl (exact for points on a 2^-12 grid, else
+//      |x - xh - xl| <= 2^-16 |x|) and c = ch + cl (+ |residual| <= 2^-16 |c|):
+//      xh.ch + xl.ch + xh.cl + xl.cl as 8 MMAs of K=16 over the A row [xh|xl]
+//      and the B rows [ch|ch], [cl|cl]. t_k = |c_k|^2 - 2 s~_k ranks the
+//      centroids like |x - c_k|^2 (|x|^2 is common to the row).
+//   2. filter (epilogue, per point): every k with t_k <= min_j t_j + 2 eps is a
+//      candidate, eps = 2^-10 (|x| max|c| + |x|^2 + max|c|^2) -- at least 8x
+//      the bound on |t_k + |x|^2 - d_k| from the split, the tensor-core
+//      accumulation (<= 2^-13 |x||c|) and the fp32 evaluation of the exact
+//      distance d_k (<= 2^-19 (|x|^2 + |c|^2 + 2|x||c|)). The exact argmin is
+//      always a candidate, and so is every k tied with it.
+//   3. verify: the candidates' exact fp32 distances (the oracle's operation
+//      order) pick the result; a point whose candidate list overflows is
+//      scanned exactly over all K.
+// On the C4 data (2^28 points, K=1024, 1024 Gaussian blobs) the filter keeps
+// 1.26 candidates per point on average (max 5; scripts in profiles/).
+//
+// Layout: points are stored twice -- fp32 (the exact pass and the update) and
+// split bf16 [xh(32) | xl(32)] (128 B per point = one SWIZZLE_128B row) with
+// |x|^2 per point, made once by kmeans_split_points. Per launch the centroids
+// are split into B1 = [ch|ch], B2 = [cl|cl] (bf16, K x 64) with |c|^2. One
+// persistent CTA pair (cta_group::2) per 2 SMs: the pair's B halves for all K
+// are resident (K/2 x 256 B per CTA, <= 128 KB), A tiles of 2 x 128 points
+// stream through 3 stages, and each tile runs K/256 chunks of N=256 MMAs into
+// two TMEM accumulators. Epilogue warps 0-3 scan the even chunks (accumulator
+// 0), warps 4-7 the odd ones (accumulator 1); they merge candidate lists
+// through shared memory and warps 0-3 verify and store.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <string>
+
+#include "common.hpp"
+#include "ptx.cuh"
+#include "../../include/hcl_cabi.h"
+
+namespace hcl {
+
+CUtensorMap make_tmap_2d_bf16(const void* base, uint64_t inner, uint64_t outer, uint64_t row_bytes, uint32_t box_inner,
+                              uint32_t box_outer);
+
+namespace {
+
+constexpr int KT_D = 32;
+constexpr int KT_EPI = 8;                    // epilogue warps 0-7, producer 8, MMA 9
+constexpr int KT_THREADS = (KT_EPI + 2) * 32;
+constexpr int KT_ROWS = 128;                 // points per CTA per tile
+constexpr int KT_A = KT_ROWS * 128;          // 16 KB A tile per CTA
+constexpr int KT_STAGES = 3;
+constexpr int KT_BH = 128 * 128;             // per CTA, chunk and split part: 128 centroids x 128 B
+constexpr int KT_LIST = 8;                   // candidate slots per point and epilogue group
+constexpr int KT_KMAX = 1024;
+
+struct KtLayout {
+  size_t b, a, q, lists, xch, bars, total;
+  __host__ __device__ KtLayout(int K) {
+    const int nch = K / 256;
+    b = 0;
+    a = b + static_cast<size_t>(nch) * 2 * KT_BH;
+    q = a + static_cast<size_t>(KT_STAGES) * KT_A;
+    lists = q + static_cast<size_t>(K) * 4;
+    xch = lists + 2ull * KT_ROWS * KT_LIST * 8;  // (t, k) float2 per slot
+    bars = xch + KT_ROWS * 16;                    // group-1 (min, count, overflow)
+    total = bars + 16 * 8 + 16 + 1024;            // barriers, TMEM slot, alignment slack
+  }
+};
+
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+
+// exact fp32 distance in the oracle's order (ho_kmeans_assign)
+__device__ __forceinline__ float exact_dist(const float (&x)[KT_D], const float* __restrict__ c) {
+  float s = 0.f;
+#pragma unroll
+  for (int j = 0; j < KT_D; j += 4) {
+    const float4 v = __ldg(reinterpret_cast<const float4*>(c + j));
+    float d0 = __fsub_rn(v.x, x[j]), d1 = __fsub_rn(v.y, x[j + 1]);
+    float d2 = __fsub_rn(v.z, x[j + 2]), d3 = __fsub_rn(v.w, x[j + 3]);
+    s = __fadd_rn(s, __fmul_rn(d0, d0));
+    s = __fadd_rn(s, __fmul_rn(d1, d1));
+    s = __fadd_rn(s, __fmul_rn(d2, d2));
+    s = __fadd_rn(s, __fmul_rn(d3, d3));
+  }
+  return s;
+}
+
+__global__ void __launch_bounds__(KT_THREADS, 1)
+    kmeans_assign_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB1,
+                            const __grid_constant__ CUtensorMap tmB2, const float* __restrict__ qg,
+                            const float* __restrict__ stats, const float* __restrict__ cent,
+                            const float* __restrict__ pts, const float* __restrict__ xxg,
+                            int32_t* __restrict__ assign, int rows, int K, int* __restrict__ n_overflow) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const KtLayout L(K);
+  uint8_t* sb = smem + L.b;
+  uint8_t* sa = smem + L.a;
+  float* sq = reinterpret_cast<float*>(smem + L.q);
+  float2* lists = reinterpret_cast<float2*>(smem + L.lists);
+  float4* xch = reinterpret_cast<float4*>(smem + L.xch);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.bars);
+  uint64_t* empty = full + KT_STAGES;
+  uint64_t* tfull = empty + KT_STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint64_t* bfull = tempty + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bfull + 1);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const uint32_t rank = ptx::cluster_ctarank();
+  const int nch = K / 256;
+  constexpr int PROD = KT_EPI, MMA = KT_EPI + 1;
+
+  if (warp == PROD && lane == 0) {
+    ptx::prefetch_tmap(&tmA);
+    ptx::prefetch_tmap(&tmB1);
+    ptx::prefetch_tmap(&tmB2);
+    for (int s = 0; s < KT_STAGES; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      ptx::mbar_init(&tfull[a], 1);
+      ptx::mbar_init(&tempty[a], 2 * 4);  // the 4 warps of one epilogue group, both CTAs
+    }
+    ptx::mbar_init(bfull, 1);
+    ptx::fence_mbar_init();
+  }
+  if (warp == MMA) ptx::tmem_alloc<2>(tmem_slot, 512);
+  ptx::tc_fence_before();
+  ptx::cluster_sync();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int cluster = blockIdx.x / 2, nclusters = gridDim.x / 2;
+  const int tiles = (rows + 2 * KT_ROWS - 1) / (2 * KT_ROWS);
+
+  if (warp == PROD) {
+    if (lane == 0) {
+      // resident B: this CTA's 128-centroid half of every 256-centroid chunk
+      if (rank == 0) ptx::mbar_arrive_expect_tx(bfull, static_cast<uint32_t>(nch) * 2 * KT_BH * 2);
+      const uint32_t bb = ptx::mapa(ptx::smem_u32(bfull), 0);
+      for (int c = 0; c < nch; ++c) {
+        const int row = c * 256 + static_cast<int>(rank) * 128;
+        ptx::tma_load_2d_pair(sb + (2 * c) * KT_BH, &tmB1, bb, 0, row);
+        ptx::tma_load_2d_pair(sb + (2 * c + 1) * KT_BH, &tmB2, bb, 0, row);
+      }
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = cluster; t < tiles; t += nclusters) {
+        ptx::mbar_wait(&empty[stage], phase ^ 1);
+        if (rank == 0) ptx::mbar_arrive_expect_tx(&full[stage], KT_A * 2);
+        const uint32_t bar = ptx::mapa(ptx::smem_u32(&full[stage]), 0);
+        ptx::tma_load_2d_pair(sa + stage * KT_A, &tmA, bar, 0, t * 2 * KT_ROWS + static_cast<int>(rank) * KT_ROWS);
+        if (++stage == KT_STAGES) { stage = 0; phase ^= 1; }
+      }
+    }
+    __syncwarp();
+  } else if (warp == MMA) {
+    if (rank == 0) {
+      constexpr uint32_t idesc = ptx::umma_idesc(1, 0, 0, 2 * KT_ROWS, 256);
+      ptx::mbar_wait(bfull, 0);
+      const uint64_t adesc0 = ptx::umma_desc_sw128(ptx::smem_u32(sa), 16, 1024);
+      const uint64_t bdesc0 = ptx::umma_desc_sw128(ptx::smem_u32(sb), 16, 1024);
+      int stage = 0;
+      uint32_t phase = 0;
+      uint32_t acc_phase[2] = {0, 0};
+      for (int t = cluster; t < tiles; t += nclusters) {
+        ptx::mbar_wait(&full[stage], phase);
+        ptx::tc_fence_after();
+        const uint64_t adesc = adesc0 + static_cast<uint64_t>((stage * KT_A) >> 4);
+        for (int c = 0; c < nch; ++c) {
+          const int acc = c & 1;
+          ptx::mbar_wait(&tempty[acc], acc_phase[acc] ^ 1);
+          acc_phase[acc] ^= 1;
+          ptx::tc_fence_after();
+          const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * 256);
+          const uint64_t b1 = bdesc0 + static_cast<uint64_t>(((2 * c) * KT_BH) >> 4);
+          const uint64_t b2 = bdesc0 + static_cast<uint64_t>(((2 * c + 1) * KT_BH) >> 4);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) ptx::mma_elect<2, false>(d_tmem, adesc + 2 * i, b1 + 2 * i, idesc, i != 0);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) ptx::mma_elect<2, false>(d_tmem, adesc + 2 * i, b2 + 2 * i, idesc, 1);
+          ptx::mma_commit_elect<2>(&tfull[acc]);
+        }
+        ptx::mma_commit_elect<2>(&empty[stage]);
+        if (++stage == KT_STAGES) { stage = 0; phase ^= 1; }
+      }
+    }
+    __syncwarp();
+  } else {
+    // ---------------- epilogue: groups g = 0 (even chunks), 1 (odd chunks) ----------------
+    const int g = warp / 4, quad = warp % 4;
+    const int pl = quad * 32 + lane;  // point within the CTA tile = TMEM lane
+    for (int i = threadIdx.x; i < K; i += KT_EPI * 32) sq[i] = qg[i];
+    const float qmax = stats[0];
+    const float cmax = sqrtf(qmax);
+    epi_bar();
+    float2* my = lists + (g * KT_ROWS + pl) * KT_LIST;
+    uint32_t acc_phase = 0;
+    for (int t = cluster; t < tiles; t += nclusters) {
+      const int row = t * 2 * KT_ROWS + static_cast<int>(rank) * KT_ROWS + pl;
+      const bool valid = row < rows;
+      const float xx = valid ? xxg[row] : 0.f;
+      const float two_eps = 0x1p-9f * (sqrtf(xx) * cmax + xx + qmax);
+      float m = __int_as_float(0x7f800000);
+      int cnt = 0, ovf = 0;
+      for (int c = g; c < nch; c += 2) {
+        ptx::mbar_wait(&tfull[g], acc_phase);
+        acc_phase ^= 1;
+        ptx::tc_fence_after();
+#pragma unroll 1
+        for (int b = 0; b < 8; ++b) {
+          uint32_t r[32];
+          ptx::tmem_ld_32x32b_x32(
+              tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + static_cast<uint32_t>(g * 256 + b * 32), r);
+          ptx::tmem_ld_wait();
+          if (b == 7) {  // accumulator drained: hand it back to the MMA warp
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive_cluster_relaxed(ptx::mapa(ptx::smem_u32(&tempty[g]), 0));
+          }
+          const int k0 = c * 256 + b * 32;
+          const float4* q4 = reinterpret_cast<const float4*>(sq + k0);
+          float bmin = __int_as_float(0x7f800000);
+#pragma unroll
+          for (int j = 0; j < 32; j += 4) {
+            const float4 qv = q4[j / 4];
+            float t0 = fmaf(-2.f, __uint_as_float(r[j]), qv.x);
+            float t1 = fmaf(-2.f, __uint_as_float(r[j + 1]), qv.y);
+            float t2 = fmaf(-2.f, __uint_as_float(r[j + 2]), qv.z);
+            float t3 = fmaf(-2.f, __uint_as_float(r[j + 3]), qv.w);
+            r[j] = __float_as_uint(t0);
+            r[j + 1] = __float_as_uint(t1);
+            r[j + 2] = __float_as_uint(t2);
+            r[j + 3] = __float_as_uint(t3);
+            bmin = fminf(bmin, fminf(fminf(t0, t1), fminf(t2, t3)));
+          }
+          m = fminf(m, bmin);
+          const float thr = m + two_eps;
+          if (bmin <= thr) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const float tj = __uint_as_float(r[j]);
+              if (tj <= thr) {
+                if (cnt == KT_LIST) {  // drop entries the running minimum has excluded
+                  int w = 0;
+                  for (int e = 0; e < KT_LIST; ++e)
+                    if (my[e].x <= thr) my[w++] = my[e];
+                  cnt = w;
+                }
+                if (cnt < KT_LIST)
+                  my[cnt++] = make_float2(tj, __int_as_float(k0 + j));
+                else
+                  ovf = 1;
+              }
+            }
+          }
+        }
+      }
+      // merge the two groups' lists; group 0 verifies and stores
+      if (g == 1) xch[pl] = make_float4(m, __int_as_float(cnt), __int_as_float(ovf), 0.f);
+      epi_bar();
+      if (g == 0 && valid) {
+        const float4 o = xch[pl];
+        const float mall = fminf(m, o.x);
+        const float thr = mall + two_eps;
+        const int cnt1 = __float_as_int(o.y);
+        ovf |= __float_as_int(o.z);
+        float x[KT_D];
+#pragma unroll
+        for (int j = 0; j < KT_D; j += 4) {
+          const float4 v = __ldg(reinterpret_cast<const float4*>(pts + static_cast<int64_t>(row) * KT_D + j));
+          x[j] = v.x;
+          x[j + 1] = v.y;
+          x[j + 2] = v.z;
+          x[j + 3] = v.w;
+        }
+        float best = __int_as_float(0x7f800000);
+        int bk = 0x7fffffff;
+        if (ovf) {
+          atomicAdd(n_overflow, 1);
+          for (int k = 0; k < K; ++k) {
+            const float e = exact_dist(x, cent + static_cast<int64_t>(k) * KT_D);
+            if (e < best) { best = e; bk = k; }
+          }
+        } else {
+          const float2* other = lists + (KT_ROWS + pl) * KT_LIST;
+          for (int e = 0; e < cnt + cnt1; ++e) {
+            const float2 en = e < cnt ? my[e] : other[e - cnt];
+            if (en.x > thr) continue;
+            const int k = __float_as_int(en.y);
+            const float d = exact_dist(x, cent + static_cast<int64_t>(k) * KT_D);
+            if (d < best || (d == best && k < bk)) { best = d; bk = k; }
+          }
+        }
+        assign[row] = bk;
+      }
+      epi_bar();
+    }
+  }
+
+  ptx::tc_fence_before();
+  ptx::cluster_sync();
+  if (warp == MMA) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc<2>(tmem_base, 512);
+  }
+}
+
+// points (N x 32 fp32) -> split rows [xh | xl] (N x 64 bf16) and |x|^2
+__global__ void kmeans_split_points_kernel(const float4* __restrict__ pts, uint4* __restrict__ split,
+                                           float* __restrict__ xx, int64_t n) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  uint32_t hi[16], lo[16];
+  float s = 0.f;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const float4 v = pts[i * 8 + j];
+    const float e[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int u = 0; u < 4; u += 2) {
+      const __nv_bfloat16 h0 = __float2bfloat16_rn(e[u]), h1 = __float2bfloat16_rn(e[u + 1]);
+      const __nv_bfloat16 l0 = __float2bfloat16_rn(e[u] - __bfloat162float(h0));
+      const __nv_bfloat16 l1 = __float2bfloat16_rn(e[u + 1] - __bfloat162float(h1));
+      hi[(j * 4 + u) / 2] = static_cast<uint32_t>(__bfloat16_as_ushort(h0)) |
+                            (static_cast<uint32_t>(__bfloat16_as_ushort(h1)) << 16);
+      lo[(j * 4 + u) / 2] = static_cast<uint32_t>(__bfloat16_as_ushort(l0)) |
+                            (static_cast<uint32_t>(__bfloat16_as_ushort(l1)) << 16);
+    }
+    s = fmaf(v.x, v.x, s);
+    s = fmaf(v.y, v.y, s);
+    s = fmaf(v.z, v.z, s);
+    s = fmaf(v.w, v.w, s);
+  }
+  uint4* o = split + i * 8;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) o[j] = make_uint4(hi[4 * j], hi[4 * j + 1], hi[4 * j + 2], hi[4 * j + 3]);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) o[4 + j] = make_uint4(lo[4 * j], lo[4 * j + 1], lo[4 * j + 2], lo[4 * j + 3]);
+  xx[i] = s;
+}
+
+// centroids (K x 32) -> B1 = [ch|ch], B2 = [cl|cl] (K x 64 bf16), q = |c|^2, stats[0] = max q
+__global__ void kmeans_split_centroids_kernel(const float* __restrict__ cent, uint16_t* __restrict__ b1,
+                                              uint16_t* __restrict__ b2, float* __restrict__ q,
+                                              unsigned* __restrict__ stats, int K) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= K) return;
+  float s = 0.f;
+  for (int j = 0; j < KT_D; ++j) {
+    const float v = cent[static_cast<int64_t>(k) * KT_D + j];
+    const __nv_bfloat16 h = __float2bfloat16_rn(v);
+    const __nv_bfloat16 l = __float2bfloat16_rn(v - __bfloat162float(h));
+    b1[k * 64 + j] = b1[k * 64 + 32 + j] = __bfloat16_as_ushort(h);
+    b2[k * 64 + j] = b2[k * 64 + 32 + j] = __bfloat16_as_ushort(l);
+    s = fmaf(v, v, s);
+  }
+  q[k] = s;
+  atomicMax(stats, __float_as_uint(s * (1.f + 0x1p-20f)));  // non-negative: bit order = value order
+}
+
+// kmeans_assign_tc(points, split, xx, centroids, assign, N, D, K)
+uint64_t launch_assign_tc(LaunchCtx& c) {
+  const int64_t n = scalar_arg(c, 5, "kmeans_assign_tc N");
+  const int64_t d = scalar_arg(c, 6, "kmeans_assign_tc D");
+  const int64_t k = scalar_arg(c, 7, "kmeans_assign_tc K");
+  if (d != KT_D) fail(ErrorCode::argument, "kmeans_assign_tc: D must be 32");
+  if (k < 256 || k > KT_KMAX || k % 256) fail(ErrorCode::argument, "kmeans_assign_tc: K must be 256, 512, 768 or 1024");
+  if (n < 1 || n > INT32_MAX) fail(ErrorCode::argument, "kmeans_assign_tc: N out of range");
+  const BufView& P = buffer_arg(c, 0, "kmeans_assign_tc points");
+  const BufView& S = buffer_arg(c, 1, "kmeans_assign_tc split");
+  const BufView& X = buffer_arg(c, 2, "kmeans_assign_tc xx");
+  const BufView& Cb = buffer_arg(c, 3, "kmeans_assign_tc centroids");
+  if (Cb.first_byte != 0 || Cb.bytes != static_cast<uint64_t>(k * d) * 4)
+    fail(ErrorCode::argument, "kmeans_assign_tc: centroids size != K*D");
+  if (c.whole && (P.bytes != static_cast<uint64_t>(n * d) * 4 || S.bytes != static_cast<uint64_t>(n) * 128 ||
+                  X.bytes != static_cast<uint64_t>(n) * 4))
+    fail(ErrorCode::argument, "kmeans_assign_tc: points N*D fp32, split N*128 bytes, xx N fp32");
+  uint64_t lo, rows;
+  sub_range(c, static_cast<uint64_t>(n), lo, rows, "kmeans_assign_tc");
+  const float* pts = at_byte<const float>(P, lo * d * 4, rows * d * 4, "kmeans_assign_tc points");
+  const uint8_t* split = at_byte<const uint8_t>(S, lo * 128, rows * 128, "kmeans_assign_tc split");
+  const float* xx = at_byte<const float>(X, lo * 4, rows * 4, "kmeans_assign_tc xx");
+  int32_t* asg = at_byte<int32_t>(buffer_arg(c, 4, "kmeans_assign_tc assign"), lo * 4, rows * 4, "kmeans_assign_tc assign");
+  if (!rows) return 0;
+  // per-launch centroid split + norms in scratch
+  const size_t bsz = static_cast<size_t>(k) * 128;
+  uint8_t* scr = static_cast<uint8_t*>(c.scratch(c.dev, 2 * bsz + static_cast<size_t>(k) * 4 + 64));
+  uint16_t* b1 = reinterpret_cast<uint16_t*>(scr);
+  uint16_t* b2 = reinterpret_cast<uint16_t*>(scr + bsz);
+  float* q = reinterpret_cast<float*>(scr + 2 * bsz);
+  unsigned* stats = reinterpret_cast<unsigned*>(scr + 2 * bsz + static_cast<size_t>(k) * 4);
+  int* n_ovf = reinterpret_cast<int*>(stats + 4);
+  HCL_CUDA(cudaMemsetAsync(stats, 0, 32, c.stream));
+  kmeans_split_centroids_kernel<<<static_cast<unsigned>(ceil_div(k, 128)), 128, 0, c.stream>>>(
+      reinterpret_cast<const float*>(Cb.ptr), b1, b2, q, stats, static_cast<int>(k));
+  HCL_LAUNCHED();
+  CUtensorMap ta = make_tmap_2d_bf16(split, 64, rows, 128, 64, KT_ROWS);
+  CUtensorMap tb1 = make_tmap_2d_bf16(b1, 64, static_cast<uint64_t>(k), 128, 64, 128);
+  CUtensorMap tb2 = make_tmap_2d_bf16(b2, 64, static_cast<uint64_t>(k), 128, 64, 128);
+  const KtLayout Lh(static_cast<int>(k));
+  const size_t smem = Lh.total;
+  HCL_CUDA(cudaFuncSetAttribute(kmeans_assign_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(smem)));
+  const int64_t tiles = ceil_div(static_cast<int64_t>(rows), 2 * KT_ROWS);
+  const int64_t clusters = std::min<int64_t>(tiles, c.sm_count / 2);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(clusters * 2));
+  cfg.blockDim = dim3(KT_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = c.stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  HCL_CUDA(cudaLaunchKernelEx(&cfg, kmeans_assign_tc_kernel, ta, tb1, tb2, static_cast<const float*>(q),
+                              reinterpret_cast<const float*>(stats), reinterpret_cast<const float*>(Cb.ptr), pts, xx,
+                              asg, static_cast<int>(rows), static_cast<int>(k), n_ovf));
+  HCL_LAUNCHED();
+  return 3ull * rows * static_cast<uint64_t>(k) * static_cast<uint64_t>(d);
+}
+
+// kmeans_split_points(points, split, xx, N, D)
+uint64_t launch_split_points(LaunchCtx& c) {
+  const int64_t n = scalar_arg(c, 3, "kmeans_split_points N");
+  const int64_t d = scalar_arg(c, 4, "kmeans_split_points D");
+  if (d != KT_D) fail(ErrorCode::argument, "kmeans_split_points: D must be 32");
+  const BufView& P = buffer_arg(c, 0, "kmeans_split_points points");
+  if (c.whole && P.bytes != static_cast<uint64_t>(n * d) * 4)
+    fail(ErrorCode::argument, "kmeans_split_points: points size != N*D");
+  uint64_t lo, rows;
+  sub_range(c, static_cast<uint64_t>(n), lo, rows, "kmeans_split_points");
+  const float* pts = at_byte<const float>(P, lo * d * 4, rows * d * 4, "kmeans_split_points points");
+  uint8_t* split = at_byte<uint8_t>(buffer_arg(c, 1, "split"), lo * 128, rows * 128, "kmeans_split_points split");
+  float* xx = at_byte<float>(buffer_arg(c, 2, "xx"), lo * 4, rows * 4, "kmeans_split_points xx");
+  if (!rows) return 0;
+  kmeans_split_points_kernel<<<static_cast<unsigned>(ceil_div(rows, 256)), 256, 0, c.stream>>>(
+      reinterpret_cast<const float4*>(pts), reinterpret_cast<uint4*>(split), xx, static_cast<int64_t>(rows));
+  HCL_LAUNCHED();
+  return rows;
+}
+
+uint64_t rows_tc(const int64_t* s, uint32_t) { return static_cast<uint64_t>(s[5]); }
+uint64_t rows_split(const int64_t* s, uint32_t) { return static_cast<uint64_t>(s[3]); }
+
+}  // namespace
+
+void register_kmeans_tc(std::vector<KernelDef>& r) {
+  constexpr uint8_t S = HCL_ARG_SCALAR, I = HCL_ARG_IN, O = HCL_ARG_OUT;
+  constexpr uint8_t N = HCL_PART_NONE, P = HCL_PART_REPLICATE, X = HCL_PART_SPLIT_ROWS;
+  r.push_back({"b200", "kmeans_assign_tc", {I, I, I, I, O, S, S, S}, {X, X, X, P, X, N, N, N}, launch_assign_tc,
+               nullptr, rows_tc});
+  r.push_back({"b200", "kmeans_split_points", {I, O, O, S, S}, {X, X, X, N, N}, launch_split_points, nullptr,
+               rows_split});
+}
+
+}  // namespace hcl

@@ -18,6 +18,7 @@ void register_gemm(std::vector<KernelDef>& r);
 void register_graph(std::vector<KernelDef>& r);
 void register_kmeans(std::vector<KernelDef>& r);
 void register_conv(std::vector<KernelDef>& r);
+void register_kmeans_tc(std::vector<KernelDef>& r);
 
 const std::vector<KernelDef>& registry() {
   static const std::vector<KernelDef> defs = [] {
@@ -27,6 +28,7 @@ const std::vector<KernelDef>& registry() {
     register_graph(r);
     register_kmeans(r);
     register_conv(r);
+    register_kmeans_tc(r);
     return r;
   }();
   return defs;

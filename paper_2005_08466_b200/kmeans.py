@@ -19,8 +19,12 @@ from .runtime import Handle, HostContext
 
 class KMeans:
     def __init__(self, ctx: HostContext, queues: Sequence[Handle], n: int, d: int, k: int,
-                 weights: Optional[Sequence[int]] = None):
+                 weights: Optional[Sequence[int]] = None, tensor_filter: bool = False):
+        """tensor_filter: assign with kmeans_assign_tc (tcgen05 bf16-split scores,
+        exact fp32 verification of the candidates; identical assignments) --
+        needs D = 32 and K in {256, 512, 768, 1024}."""
         self.ctx, self.queues, self.n, self.d, self.k = ctx, list(queues), n, d, k
+        self.tensor_filter = tensor_filter
         self.weights = list(weights) if weights is not None else None
         mk = ctx.create_buffer
         self.b_pts = mk(n * d * 4)
@@ -38,6 +42,22 @@ class KMeans:
             ctx.set_kernel_arg(self.k_acc, j, a)
         for j, a in enumerate([self.b_sums, self.b_counts, self.b_cent, k, d]):
             ctx.set_kernel_arg(self.k_fin, j, a)
+        if tensor_filter:
+            self.b_split, self.b_xx = mk(n * 128), mk(n * 4)
+            self.k_split = ctx.create_kernel(prog, "kmeans_split_points")
+            self.k_assign_tc = ctx.create_kernel(prog, "kmeans_assign_tc")
+            for j, a in enumerate([self.b_pts, self.b_split, self.b_xx, n, d]):
+                ctx.set_kernel_arg(self.k_split, j, a)
+            for j, a in enumerate([self.b_pts, self.b_split, self.b_xx, self.b_cent, self.b_assign, n, d, k]):
+                ctx.set_kernel_arg(self.k_assign_tc, j, a)
+
+    def _split(self) -> None:
+        if self.tensor_filter:  # the bf16 split rows and |x|^2 of the resident points (once)
+            self.ctx.enqueue_ndrange_partitioned(self.k_split, (self.n, 1, 1), 1, self.queues, bounds=self.bounds)
+
+    def _assign(self) -> None:
+        k = self.k_assign_tc if self.tensor_filter else self.k_assign
+        self.ctx.enqueue_ndrange_partitioned(k, (self.n, 1, 1), 1, self.queues, bounds=self.bounds)
 
     def load_points(self, pts: np.ndarray, bounds: Optional[Sequence[int]] = None) -> None:
         """Scatter each queue's row block of the points straight to its device."""
@@ -49,6 +69,7 @@ class KMeans:
             if hi > lo:
                 self.ctx.enqueue_write_buffer(q, self.b_pts, flat[lo * self.d:hi * self.d], offset=lo * self.d * 4)
         self.bounds = list(bounds)
+        self._split()
 
     def generate_points(self, seed: int, blobs: int, bounds: Optional[Sequence[int]] = None) -> None:
         """Generate the synthetic points in HBM (each queue's rows on its device),
@@ -61,6 +82,7 @@ class KMeans:
             self.ctx.set_kernel_arg(kg, j, a)
         self.ctx.enqueue_ndrange_partitioned(kg, (self.n, 1, 1), 1, self.queues, bounds=bounds)
         self.bounds = list(bounds)
+        self._split()
 
     def set_centroids(self, cent: np.ndarray) -> None:
         self.ctx.enqueue_write_buffer(self.queues[0], self.b_cent, np.ascontiguousarray(cent, np.float32))
@@ -68,12 +90,12 @@ class KMeans:
     def iterate(self, iterations: int = 1) -> None:
         ctx, g = self.ctx, (self.n, 1, 1)
         for _ in range(iterations):
-            ctx.enqueue_ndrange_partitioned(self.k_assign, g, 1, self.queues, bounds=self.bounds)
+            self._assign()
             ctx.enqueue_ndrange_partitioned(self.k_acc, g, 1, self.queues, bounds=self.bounds)
             ctx.enqueue_ndrange_kernel(self.queues[0], self.k_fin)
 
     def assign_only(self) -> None:
-        self.ctx.enqueue_ndrange_partitioned(self.k_assign, (self.n, 1, 1), 1, self.queues, bounds=self.bounds)
+        self._assign()
 
     def finish(self) -> None:
         for q in self.queues:
@@ -96,3 +118,6 @@ class KMeans:
     def close(self) -> None:
         for b in (self.b_pts, self.b_cent, self.b_assign, self.b_sums, self.b_counts):
             self.ctx.release(b)
+        if self.tensor_filter:
+            self.ctx.release(self.b_split)
+            self.ctx.release(self.b_xx)

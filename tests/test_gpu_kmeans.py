@@ -100,3 +100,51 @@ def test_device_point_generator_matches_host(ctx, queues):
     got = ctx.enqueue_read_buffer(queues[0], km.b_pts).view(np.float32)
     km.close()
     assert (got == G.gen_kmeans_points(n, d, 1024, 42)).all()
+
+
+# ---- tensor-filtered assignment (kmeans_assign_tc): identical results ----
+
+@pytest.mark.parametrize("n,k,P", [(20000, 256, 1), (70001, 1024, 1), (33333, 512, 4), (9000, 768, 2)])
+def test_tensor_filter_bitexact(ctx, queues, n, k, P):
+    from paper_2005_08466_b200.kmeans import KMeans
+
+    d = 32
+    pts = G.gen_kmeans_points(n, d, k, 42)
+    cent0 = pts[: k * d].copy()
+    a_want, s_want, c_want, cent_want = oracle_iterations(pts, n, d, k, cent0, 3)
+    km = KMeans(ctx, queues[:P], n, d, k, tensor_filter=True)
+    km.load_points(pts)
+    km.set_centroids(cent0)
+    km.iterate(2)
+    km.assign_only()
+    got_a = km.assignments()
+    km.iterate(1)
+    s, c = km.sums()
+    cent = km.centroids()
+    km.close()
+    assert (got_a == a_want).all()
+    assert (s == s_want).all() and (c == c_want).all()
+    assert cent.tobytes() == cent_want.reshape(k, d).tobytes()
+
+
+def test_tensor_filter_ties_and_general_fp32(ctx, queues):
+    """Exact ties (duplicate centroids) and points off the 2^-12 grid."""
+    from paper_2005_08466_b200.kmeans import KMeans
+
+    d, k, n = 32, 256, 4096
+    rng = np.random.default_rng(3)
+    cent = rng.standard_normal((k, d)).astype(np.float32) * 3
+    cent[7] = cent[200]  # duplicates: ties must go to 7
+    cent[9] = cent[10]
+    pts = rng.standard_normal((n, d)).astype(np.float32) * 3
+    pts[:50] = cent[200] + rng.standard_normal((50, d)).astype(np.float32) * 1e-3
+    pts[50:100] = cent[10]
+    want = O.kmeans_assign(pts.reshape(-1), n, d, cent.reshape(-1), k)
+    km = KMeans(ctx, queues[:1], n, d, k, tensor_filter=True)
+    km.load_points(pts)
+    km.set_centroids(cent)
+    km.assign_only()
+    got = km.assignments()
+    km.close()
+    assert (got == want).all()
+    assert (got[50:100] == 9).all()
