@@ -552,12 +552,17 @@ class KMeansW(Workload):
         self.q = q = ctx.create_queue(0)
         b = split_ranges(self.N, [1] * d.world)
         self.lo, self.rows = b[d.rank], b[d.rank + 1] - b[d.rank]
-        self.km = km = KMeans(ctx, [q], self.N, self.D, self.K)
+        # tensor-filtered assignment (kmeans_assign_tc: tcgen05 split-bf16 scores + exact fp32
+        # verification, identical assignments); BENCH_KM_TC=0 selects the exact SIMT kernel
+        self.tc = os.environ.get("BENCH_KM_TC", "1") == "1"
+        self.km = km = KMeans(ctx, [q], self.N, self.D, self.K, tensor_filter=self.tc)
         # this rank's rows of the point set, generated in HBM (counter-based SplitMix64)
         kg = ctx.create_kernel(ctx.create_program("b200"), "gen_kmeans_points")
         for j, a in enumerate([km.b_pts, self.N, self.D, self.K, 42]):
             ctx.set_kernel_arg(kg, j, a)
         ctx.enqueue_ndrange_range(q, kg, (self.N, 1, 1), 1, self.lo, self.rows)
+        if self.tc:  # bf16 split rows + |x|^2 of the resident points, once
+            ctx.enqueue_ndrange_range(q, km.k_split, (self.N, 1, 1), 1, self.lo, self.rows)
         ctx.finish(q)
         from paper_2005_08466_b200 import datagen as G
 
@@ -570,7 +575,8 @@ class KMeansW(Workload):
 
     def _assign(self):
         c = self.ctx
-        c.enqueue_ndrange_range(self.q, self.km.k_assign, (self.N, 1, 1), 1, self.lo, self.rows)
+        k = self.km.k_assign_tc if self.tc else self.km.k_assign
+        c.enqueue_ndrange_range(self.q, k, (self.N, 1, 1), 1, self.lo, self.rows)
 
     def step(self):
         c, q, km = self.ctx, self.q, self.km
@@ -585,6 +591,8 @@ class KMeansW(Workload):
         return self._assign
 
     def dominant_work(self):
+        if self.tc:  # tensor work actually issued: 4 split products x D per (point, centroid)
+            return 2.0 * self.rows * self.K * 4 * self.D
         return 3.0 * self.rows * self.K * self.D
 
     def e2e_step(self):
@@ -600,6 +608,9 @@ class KMeansW(Workload):
         return self.K * self.D * 4 * self.dist.world, self.K * self.D * 4 * self.dist.world
 
     def roofline(self, pk):
+        if self.tc:
+            return ("tensor", pk["bf16_tflops"], "TFLOP/s", 1e12,
+                    "MEASURED_PEAKS.json bf16_tflops; achieved = split-bf16 MMA flops issued (2 N K 4D)")
         sm = pk.get("sm_max_mhz", 1965.0)
         # exact (non-FMA) fp32: one add or multiply per lane per clock (FADD2 issues
         # two lanes' worth but occupies the FP32 pipe twice, measured)
@@ -609,6 +620,8 @@ class KMeansW(Workload):
     def config(self):
         return {"workload": f"k-means iteration (C4): {self.N} points x {self.D} dims, K={self.K}, exact fp32 "
                             f"assignment (3 flop/term), int64 sums, points split over {self.dist.world} rank(s)",
+                "assign_kernel": "kmeans_assign_tc (tcgen05 split-bf16 filter + exact fp32 verify)" if self.tc
+                else "kmeans_assign (exact fp32 SIMT)",
                 "points": "SplitMix64 blobs, multiples of 2^-12, generated in HBM"}
 
     def traffic(self):

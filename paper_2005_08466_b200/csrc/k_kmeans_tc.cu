@@ -216,13 +216,17 @@ __global__ void __launch_bounds__(KT_THREADS, 1)
         ptx::mbar_wait(&tfull[g], acc_phase);
         acc_phase ^= 1;
         ptx::tc_fence_after();
-#pragma unroll 1
+        const uint32_t tbase =
+            tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + static_cast<uint32_t>(g * 256);
+        uint32_t r[2][32];
+        ptx::tmem_ld_32x32b_x32(tbase, r[0]);
+        ptx::tmem_ld_wait();
+#pragma unroll
         for (int b = 0; b < 8; ++b) {
-          uint32_t r[32];
-          ptx::tmem_ld_32x32b_x32(
-              tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + static_cast<uint32_t>(g * 256 + b * 32), r);
-          ptx::tmem_ld_wait();
-          if (b == 7) {  // accumulator drained: hand it back to the MMA warp
+          uint32_t (&cur)[32] = r[b & 1];
+          if (b < 7) {
+            ptx::tmem_ld_32x32b_x32(tbase + (b + 1) * 32, r[(b + 1) & 1]);  // next batch in flight
+          } else {  // accumulator drained: hand it back to the MMA warp
             ptx::tc_fence_before();
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive_cluster_relaxed(ptx::mapa(ptx::smem_u32(&tempty[g]), 0));
@@ -233,36 +237,41 @@ __global__ void __launch_bounds__(KT_THREADS, 1)
 #pragma unroll
           for (int j = 0; j < 32; j += 4) {
             const float4 qv = q4[j / 4];
-            float t0 = fmaf(-2.f, __uint_as_float(r[j]), qv.x);
-            float t1 = fmaf(-2.f, __uint_as_float(r[j + 1]), qv.y);
-            float t2 = fmaf(-2.f, __uint_as_float(r[j + 2]), qv.z);
-            float t3 = fmaf(-2.f, __uint_as_float(r[j + 3]), qv.w);
-            r[j] = __float_as_uint(t0);
-            r[j + 1] = __float_as_uint(t1);
-            r[j + 2] = __float_as_uint(t2);
-            r[j + 3] = __float_as_uint(t3);
+            const float t0 = fmaf(-2.f, __uint_as_float(cur[j]), qv.x);
+            const float t1 = fmaf(-2.f, __uint_as_float(cur[j + 1]), qv.y);
+            const float t2 = fmaf(-2.f, __uint_as_float(cur[j + 2]), qv.z);
+            const float t3 = fmaf(-2.f, __uint_as_float(cur[j + 3]), qv.w);
+            cur[j] = __float_as_uint(t0);
+            cur[j + 1] = __float_as_uint(t1);
+            cur[j + 2] = __float_as_uint(t2);
+            cur[j + 3] = __float_as_uint(t3);
             bmin = fminf(bmin, fminf(fminf(t0, t1), fminf(t2, t3)));
           }
           m = fminf(m, bmin);
           const float thr = m + two_eps;
-          if (bmin <= thr) {
+          // branch-free candidate mask; the (rare) appends loop over its bits
+          uint32_t mask = 0;
 #pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              const float tj = __uint_as_float(r[j]);
-              if (tj <= thr) {
-                if (cnt == KT_LIST) {  // drop entries the running minimum has excluded
-                  int w = 0;
-                  for (int e = 0; e < KT_LIST; ++e)
-                    if (my[e].x <= thr) my[w++] = my[e];
-                  cnt = w;
-                }
-                if (cnt < KT_LIST)
-                  my[cnt++] = make_float2(tj, __int_as_float(k0 + j));
-                else
-                  ovf = 1;
-              }
+          for (int j = 0; j < 32; ++j) mask |= (__uint_as_float(cur[j]) <= thr ? 1u : 0u) << j;
+          while (mask) {
+            const int j = __ffs(mask) - 1;
+            mask &= mask - 1;
+            float tj = 0.f;
+#pragma unroll
+            for (int u = 0; u < 32; ++u)
+              if (u == j) tj = __uint_as_float(cur[u]);
+            if (cnt == KT_LIST) {  // drop entries the running minimum has excluded
+              int w = 0;
+              for (int e = 0; e < KT_LIST; ++e)
+                if (my[e].x <= thr) my[w++] = my[e];
+              cnt = w;
             }
+            if (cnt < KT_LIST)
+              my[cnt++] = make_float2(tj, __int_as_float(k0 + j));
+            else
+              ovf = 1;
           }
+          if (b < 7) ptx::tmem_ld_wait();
         }
       }
       // merge the two groups' lists; group 0 verifies and stores
