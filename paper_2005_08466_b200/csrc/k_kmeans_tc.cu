@@ -62,7 +62,7 @@ constexpr int KT_LIST = 8;                   // candidate slots per point and ep
 constexpr int KT_KMAX = 1024;
 
 struct KtLayout {
-  size_t b, a, q, lists, xch, bars, total;
+  size_t b, a, q, lists, xch, vq, bars, total;
   __host__ __device__ KtLayout(int K) {
     const int nch = K / 256;
     b = 0;
@@ -70,7 +70,8 @@ struct KtLayout {
     q = a + static_cast<size_t>(KT_STAGES) * KT_A;
     lists = q + static_cast<size_t>(K) * 4;
     xch = lists + 2ull * KT_ROWS * KT_LIST * 8;  // (t, k) float2 per slot
-    bars = xch + KT_ROWS * 16;                    // group-1 (min, count, overflow)
+    vq = xch + KT_ROWS * 16;                      // group-1 (min, count, overflow)
+    bars = vq + 4ull * 32 * 2 * KT_LIST * 8;      // verification queues of warps 0-3
     total = bars + 16 * 8 + 16 + 1024;            // barriers, TMEM slot, alignment slack
   }
 };
@@ -107,6 +108,7 @@ __global__ void __launch_bounds__(KT_THREADS, 1)
   float* sq = reinterpret_cast<float*>(smem + L.q);
   float2* lists = reinterpret_cast<float2*>(smem + L.lists);
   float4* xch = reinterpret_cast<float4*>(smem + L.xch);
+  int2* vq = reinterpret_cast<int2*>(smem + L.vq);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.bars);
   uint64_t* empty = full + KT_STAGES;
   uint64_t* tfull = empty + KT_STAGES;
@@ -277,40 +279,88 @@ __global__ void __launch_bounds__(KT_THREADS, 1)
       // merge the two groups' lists; group 0 verifies and stores
       if (g == 1) xch[pl] = make_float4(m, __int_as_float(cnt), __int_as_float(ovf), 0.f);
       epi_bar();
-      if (g == 0 && valid) {
+      if (g == 0) {
+        // final filter of both lists; a single survivor is the exact argmin as
+        // it stands (no distance needed); points with several survivors queue
+        // their (point, centroid) pairs so the whole warp evaluates them at once
         const float4 o = xch[pl];
-        const float mall = fminf(m, o.x);
-        const float thr = mall + two_eps;
+        const float thr = fminf(m, o.x) + two_eps;
         const int cnt1 = __float_as_int(o.y);
         ovf |= __float_as_int(o.z);
-        float x[KT_D];
-#pragma unroll
-        for (int j = 0; j < KT_D; j += 4) {
-          const float4 v = __ldg(reinterpret_cast<const float4*>(pts + static_cast<int64_t>(row) * KT_D + j));
-          x[j] = v.x;
-          x[j + 1] = v.y;
-          x[j + 2] = v.z;
-          x[j + 3] = v.w;
-        }
-        float best = __int_as_float(0x7f800000);
-        int bk = 0x7fffffff;
-        if (ovf) {
-          atomicAdd(n_overflow, 1);
-          for (int k = 0; k < K; ++k) {
-            const float e = exact_dist(x, cent + static_cast<int64_t>(k) * KT_D);
-            if (e < best) { best = e; bk = k; }
-          }
-        } else {
-          const float2* other = lists + (KT_ROWS + pl) * KT_LIST;
+        const float2* other = lists + (KT_ROWS + pl) * KT_LIST;
+        int nc = 0, k1 = 0;
+        if (valid && !ovf)
           for (int e = 0; e < cnt + cnt1; ++e) {
             const float2 en = e < cnt ? my[e] : other[e - cnt];
-            if (en.x > thr) continue;
-            const int k = __float_as_int(en.y);
-            const float d = exact_dist(x, cent + static_cast<int64_t>(k) * KT_D);
-            if (d < best || (d == best && k < bk)) { best = d; bk = k; }
+            if (en.x <= thr) {
+              ++nc;
+              k1 = __float_as_int(en.y);
+            }
+          }
+        const int nq = nc >= 2 ? nc : 0;
+        int off = nq;  // inclusive warp scan of the queue counts
+#pragma unroll
+        for (int sft = 1; sft < 32; sft <<= 1) {
+          const int v = __shfl_up_sync(0xffffffffu, off, sft);
+          if (lane >= sft) off += v;
+        }
+        const int total = __shfl_sync(0xffffffffu, off, 31);
+        off -= nq;
+        int2* wq = vq + quad * (32 * 2 * KT_LIST);
+        if (nq) {
+          int w = off;
+          for (int e = 0; e < cnt + cnt1; ++e) {
+            const float2 en = e < cnt ? my[e] : other[e - cnt];
+            if (en.x <= thr) wq[w++] = make_int2(__float_as_int(en.y) | (lane << 16), 0);
           }
         }
-        assign[row] = bk;
+        __syncwarp();
+        const int row0 = row - lane;
+        for (int i = lane; i < total; i += 32) {
+          const int2 e = wq[i];
+          const int p = e.x >> 16, k = e.x & 0xffff;
+          float x[KT_D];
+#pragma unroll
+          for (int j = 0; j < KT_D; j += 4) {
+            const float4 v = __ldg(reinterpret_cast<const float4*>(pts + static_cast<int64_t>(row0 + p) * KT_D + j));
+            x[j] = v.x;
+            x[j + 1] = v.y;
+            x[j + 2] = v.z;
+            x[j + 3] = v.w;
+          }
+          wq[i].y = __float_as_int(exact_dist(x, cent + static_cast<int64_t>(k) * KT_D));
+        }
+        __syncwarp();
+        if (valid) {
+          int bk = k1;
+          if (ovf) {  // candidate list overflowed: exact scan over all K (rare)
+            atomicAdd(n_overflow, 1);
+            float x[KT_D];
+#pragma unroll
+            for (int j = 0; j < KT_D; j += 4) {
+              const float4 v = __ldg(reinterpret_cast<const float4*>(pts + static_cast<int64_t>(row) * KT_D + j));
+              x[j] = v.x;
+              x[j + 1] = v.y;
+              x[j + 2] = v.z;
+              x[j + 3] = v.w;
+            }
+            float best = __int_as_float(0x7f800000);
+            for (int k = 0; k < K; ++k) {
+              const float e = exact_dist(x, cent + static_cast<int64_t>(k) * KT_D);
+              if (e < best) { best = e; bk = k; }
+            }
+          } else if (nq) {
+            float best = __int_as_float(0x7f800000);
+            bk = 0x7fffffff;
+            for (int i = off; i < off + nq; ++i) {
+              const int2 e = wq[i];
+              const float d = __int_as_float(e.y);
+              const int k = e.x & 0xffff;
+              if (d < best || (d == best && k < bk)) { best = d; bk = k; }
+            }
+          }
+          assign[row] = bk;
+        }
       }
       epi_bar();
     }
