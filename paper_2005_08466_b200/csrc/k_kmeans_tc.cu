@@ -255,13 +255,12 @@ __global__ void __launch_bounds__(KT_THREADS, 1)
           uint32_t mask = 0;
 #pragma unroll
           for (int j = 0; j < 32; ++j) mask |= (__uint_as_float(cur[j]) <= thr ? 1u : 0u) << j;
+          // entries carry their batch minimum, a lower bound of their t (no
+          // dynamic register indexing): an entry whose batch minimum exceeds the
+          // final threshold is certainly stale; the rest are verified exactly
           while (mask) {
             const int j = __ffs(mask) - 1;
             mask &= mask - 1;
-            float tj = 0.f;
-#pragma unroll
-            for (int u = 0; u < 32; ++u)
-              if (u == j) tj = __uint_as_float(cur[u]);
             if (cnt == KT_LIST) {  // drop entries the running minimum has excluded
               int w = 0;
               for (int e = 0; e < KT_LIST; ++e)
@@ -269,7 +268,7 @@ __global__ void __launch_bounds__(KT_THREADS, 1)
               cnt = w;
             }
             if (cnt < KT_LIST)
-              my[cnt++] = make_float2(tj, __int_as_float(k0 + j));
+              my[cnt++] = make_float2(bmin, __int_as_float(k0 + j));
             else
               ovf = 1;
           }
@@ -280,8 +279,8 @@ __global__ void __launch_bounds__(KT_THREADS, 1)
       if (g == 1) xch[pl] = make_float4(m, __int_as_float(cnt), __int_as_float(ovf), 0.f);
       epi_bar();
       if (g == 0) {
-        // final filter of both lists; a single survivor is the exact argmin as
-        // it stands (no distance needed); points with several survivors queue
+        // final filter of both lists (by batch minimum); a single survivor is
+        // the exact argmin as it stands (no distance needed); points with several survivors queue
         // their (point, centroid) pairs so the whole warp evaluates them at once
         const float4 o = xch[pl];
         const float thr = fminf(m, o.x) + two_eps;
