@@ -28,10 +28,11 @@
 // are split into B1 = [ch|ch], B2 = [cl|cl] (bf16, K x 64) with |c|^2. One
 // persistent CTA pair (cta_group::2) per 2 SMs: the pair's B halves for all K
 // are resident (K/2 x 256 B per CTA, <= 128 KB), A tiles of 2 x 128 points
-// stream through 3 stages, and each tile runs K/256 chunks of N=256 MMAs into
-// two TMEM accumulators. Epilogue warps 0-3 scan the even chunks (accumulator
-// 0), warps 4-7 the odd ones (accumulator 1); they merge candidate lists
-// through shared memory and warps 0-3 verify and store.
+// stream through 2 stages, and each tile runs K/256 chunks of N=256 MMAs into
+// two TMEM accumulators. Scan warps 0-3 take the even chunks (accumulator 0),
+// warps 4-7 the odd ones (accumulator 1), and hand each tile's candidate lists
+// (double-buffered in shared memory, mbarrier handshakes) to verify warps 8-11,
+// which filter, check exactly and store while the scan runs on.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -52,14 +53,18 @@ CUtensorMap make_tmap_2d_bf16(const void* base, uint64_t inner, uint64_t outer, 
 namespace {
 
 constexpr int KT_D = 32;
-constexpr int KT_EPI = 8;                    // epilogue warps 0-7, producer 8, MMA 9
-constexpr int KT_THREADS = (KT_EPI + 2) * 32;
+constexpr int KT_SCAN = 8;                   // scan warps 0-7 (TMEM scores -> candidate lists)
+constexpr int KT_VER = 4;                    // verify warps 8-11 (exact fp32 check, store)
+constexpr int KT_PROD = KT_SCAN + KT_VER;    // TMA producer warp 12, MMA warp 13
+constexpr int KT_MMA = KT_PROD + 1;
+constexpr int KT_THREADS = (KT_MMA + 1) * 32;
 constexpr int KT_ROWS = 128;                 // points per CTA per tile
 constexpr int KT_A = KT_ROWS * 128;          // 16 KB A tile per CTA
-constexpr int KT_STAGES = 3;
+constexpr int KT_STAGES = 2;
 constexpr int KT_BH = 128 * 128;             // per CTA, chunk and split part: 128 centroids x 128 B
-constexpr int KT_LIST = 8;                   // candidate slots per point and epilogue group
+constexpr int KT_LIST = 8;                   // candidate slots per point and scan group
 constexpr int KT_KMAX = 1024;
+constexpr int KT_LBUF = 2 * KT_ROWS * KT_LIST;  // float2 slots of one tile's lists (both groups)
 
 struct KtLayout {
   size_t b, a, q, lists, xch, vq, bars, total;
@@ -69,9 +74,9 @@ struct KtLayout {
     a = b + static_cast<size_t>(nch) * 2 * KT_BH;
     q = a + static_cast<size_t>(KT_STAGES) * KT_A;
     lists = q + static_cast<size_t>(K) * 4;
-    xch = lists + 2ull * KT_ROWS * KT_LIST * 8;  // (t, k) float2 per slot
-    vq = xch + KT_ROWS * 16;                      // group-1 (min, count, overflow)
-    bars = vq + 4ull * 32 * 2 * KT_LIST * 8;      // verification queues of warps 0-3
+    xch = lists + 2ull * KT_LBUF * 8;             // 2 buffers x (bmin, k) float2 slots
+    vq = xch + 2ull * 2 * KT_ROWS * 16;           // 2 buffers x 2 groups x (min, count, overflow)
+    bars = vq + static_cast<size_t>(KT_VER) * 32 * 2 * KT_LIST * 8;  // verify queues
     total = bars + 16 * 8 + 16 + 1024;            // barriers, TMEM slot, alignment slack
   }
 };
@@ -113,15 +118,16 @@ __global__ void __launch_bounds__(KT_THREADS, 1)
   uint64_t* empty = full + KT_STAGES;
   uint64_t* tfull = empty + KT_STAGES;
   uint64_t* tempty = tfull + 2;
-  uint64_t* bfull = tempty + 2;
+  uint64_t* lfull = tempty + 2;   // [2] scan -> verify: a tile's candidate lists are complete
+  uint64_t* lempty = lfull + 2;   // [2] verify -> scan: list buffer free again
+  uint64_t* bfull = lempty + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bfull + 1);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const uint32_t rank = ptx::cluster_ctarank();
   const int nch = K / 256;
-  constexpr int PROD = KT_EPI, MMA = KT_EPI + 1;
 
-  if (warp == PROD && lane == 0) {
+  if (warp == KT_PROD && lane == 0) {
     ptx::prefetch_tmap(&tmA);
     ptx::prefetch_tmap(&tmB1);
     ptx::prefetch_tmap(&tmB2);
@@ -131,12 +137,14 @@ __global__ void __launch_bounds__(KT_THREADS, 1)
     }
     for (int a = 0; a < 2; ++a) {
       ptx::mbar_init(&tfull[a], 1);
-      ptx::mbar_init(&tempty[a], 2 * 4);  // the 4 warps of one epilogue group, both CTAs
+      ptx::mbar_init(&tempty[a], 2 * 4);  // the 4 warps of one scan group, both CTAs
+      ptx::mbar_init(&lfull[a], KT_SCAN);
+      ptx::mbar_init(&lempty[a], KT_VER);
     }
     ptx::mbar_init(bfull, 1);
     ptx::fence_mbar_init();
   }
-  if (warp == MMA) ptx::tmem_alloc<2>(tmem_slot, 512);
+  if (warp == KT_MMA) ptx::tmem_alloc<2>(tmem_slot, 512);
   ptx::tc_fence_before();
   ptx::cluster_sync();
   ptx::tc_fence_after();
@@ -144,7 +152,7 @@ __global__ void __launch_bounds__(KT_THREADS, 1)
   const int cluster = blockIdx.x / 2, nclusters = gridDim.x / 2;
   const int tiles = (rows + 2 * KT_ROWS - 1) / (2 * KT_ROWS);
 
-  if (warp == PROD) {
+  if (warp == KT_PROD) {
     if (lane == 0) {
       // resident B: this CTA's 128-centroid half of every 256-centroid chunk
       if (rank == 0) ptx::mbar_arrive_expect_tx(bfull, static_cast<uint32_t>(nch) * 2 * KT_BH * 2);
@@ -165,23 +173,27 @@ __global__ void __launch_bounds__(KT_THREADS, 1)
       }
     }
     __syncwarp();
-  } else if (warp == MMA) {
+  } else if (warp == KT_MMA) {
     if (rank == 0) {
       constexpr uint32_t idesc = ptx::umma_idesc(1, 0, 0, 2 * KT_ROWS, 256);
       ptx::mbar_wait(bfull, 0);
       const uint64_t adesc0 = ptx::umma_desc_sw128(ptx::smem_u32(sa), 16, 1024);
       const uint64_t bdesc0 = ptx::umma_desc_sw128(ptx::smem_u32(sb), 16, 1024);
       int stage = 0;
-      uint32_t phase = 0;
-      uint32_t acc_phase[2] = {0, 0};
+      uint32_t phase = 0, ph0 = 0, ph1 = 0;
       for (int t = cluster; t < tiles; t += nclusters) {
         ptx::mbar_wait(&full[stage], phase);
         ptx::tc_fence_after();
         const uint64_t adesc = adesc0 + static_cast<uint64_t>((stage * KT_A) >> 4);
         for (int c = 0; c < nch; ++c) {
           const int acc = c & 1;
-          ptx::mbar_wait(&tempty[acc], acc_phase[acc] ^ 1);
-          acc_phase[acc] ^= 1;
+          if (acc == 0) {
+            ptx::mbar_wait(&tempty[0], ph0 ^ 1);
+            ph0 ^= 1;
+          } else {
+            ptx::mbar_wait(&tempty[1], ph1 ^ 1);
+            ph1 ^= 1;
+          }
           ptx::tc_fence_after();
           const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * 256);
           const uint64_t b1 = bdesc0 + static_cast<uint64_t>(((2 * c) * KT_BH) >> 4);
@@ -197,23 +209,26 @@ __global__ void __launch_bounds__(KT_THREADS, 1)
       }
     }
     __syncwarp();
-  } else {
-    // ---------------- epilogue: groups g = 0 (even chunks), 1 (odd chunks) ----------------
+  } else if (warp < KT_SCAN) {
+    // ---------------- scan: groups g = 0 (even chunks), 1 (odd chunks) ----------------
     const int g = warp / 4, quad = warp % 4;
     const int pl = quad * 32 + lane;  // point within the CTA tile = TMEM lane
-    for (int i = threadIdx.x; i < K; i += KT_EPI * 32) sq[i] = qg[i];
+    for (int i = threadIdx.x; i < K; i += KT_SCAN * 32) sq[i] = qg[i];
     const float qmax = stats[0];
     const float cmax = sqrtf(qmax);
     epi_bar();
-    float2* my = lists + (g * KT_ROWS + pl) * KT_LIST;
     uint32_t acc_phase = 0;
-    for (int t = cluster; t < tiles; t += nclusters) {
+    int it = 0;
+    for (int t = cluster; t < tiles; t += nclusters, ++it) {
+      const int buf = it & 1;
       const int row = t * 2 * KT_ROWS + static_cast<int>(rank) * KT_ROWS + pl;
       const bool valid = row < rows;
-      const float xx = valid ? xxg[row] : 0.f;
+      const float xx = valid ? __ldg(xxg + row) : 0.f;
       const float two_eps = 0x1p-9f * (sqrtf(xx) * cmax + xx + qmax);
       float m = __int_as_float(0x7f800000);
       int cnt = 0, ovf = 0;
+      ptx::mbar_wait(&lempty[buf], ((it >> 1) & 1) ^ 1);  // the verify warps are done with this buffer
+      float2* my = lists + buf * KT_LBUF + (g * KT_ROWS + pl) * KT_LIST;
       for (int c = g; c < nch; c += 2) {
         ptx::mbar_wait(&tfull[g], acc_phase);
         acc_phase ^= 1;
@@ -251,13 +266,13 @@ __global__ void __launch_bounds__(KT_THREADS, 1)
           }
           m = fminf(m, bmin);
           const float thr = m + two_eps;
-          // branch-free candidate mask; the (rare) appends loop over its bits
+          // branch-free candidate mask; the (rare) appends loop over its bits.
+          // Entries carry their batch minimum, a lower bound of their t (no
+          // dynamic register indexing): an entry whose batch minimum exceeds the
+          // final threshold is certainly stale; the rest are verified exactly.
           uint32_t mask = 0;
 #pragma unroll
           for (int j = 0; j < 32; ++j) mask |= (__uint_as_float(cur[j]) <= thr ? 1u : 0u) << j;
-          // entries carry their batch minimum, a lower bound of their t (no
-          // dynamic register indexing): an entry whose batch minimum exceeds the
-          // final threshold is certainly stale; the rest are verified exactly
           while (mask) {
             const int j = __ffs(mask) - 1;
             mask &= mask - 1;
@@ -275,99 +290,110 @@ __global__ void __launch_bounds__(KT_THREADS, 1)
           if (b < 7) ptx::tmem_ld_wait();
         }
       }
-      // merge the two groups' lists; group 0 verifies and stores
-      if (g == 1) xch[pl] = make_float4(m, __int_as_float(cnt), __int_as_float(ovf), 0.f);
-      epi_bar();
-      if (g == 0) {
-        // final filter of both lists (by batch minimum); a single survivor is
-        // the exact argmin as it stands (no distance needed); points with several survivors queue
-        // their (point, centroid) pairs so the whole warp evaluates them at once
-        const float4 o = xch[pl];
-        const float thr = fminf(m, o.x) + two_eps;
-        const int cnt1 = __float_as_int(o.y);
-        ovf |= __float_as_int(o.z);
-        const float2* other = lists + (KT_ROWS + pl) * KT_LIST;
-        int nc = 0, k1 = 0;
-        if (valid && !ovf)
-          for (int e = 0; e < cnt + cnt1; ++e) {
-            const float2 en = e < cnt ? my[e] : other[e - cnt];
-            if (en.x <= thr) {
-              ++nc;
-              k1 = __float_as_int(en.y);
-            }
+      xch[(buf * 2 + g) * KT_ROWS + pl] = make_float4(m, __int_as_float(cnt), __int_as_float(ovf), two_eps);
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&lfull[buf]);
+    }
+  } else if (warp < KT_SCAN + KT_VER) {
+    // ---------------- verify: final filter, exact check of multi-candidate points, store ----------------
+    const int vw = warp - KT_SCAN;
+    const int pl = vw * 32 + lane;
+    int2* wq = vq + vw * (32 * 2 * KT_LIST);
+    int it = 0;
+    for (int t = cluster; t < tiles; t += nclusters, ++it) {
+      const int buf = it & 1;
+      const int row = t * 2 * KT_ROWS + static_cast<int>(rank) * KT_ROWS + pl;
+      const bool valid = row < rows;
+      ptx::mbar_wait(&lfull[buf], (it >> 1) & 1);
+      const float4 o0 = xch[(buf * 2 + 0) * KT_ROWS + pl];
+      const float4 o1 = xch[(buf * 2 + 1) * KT_ROWS + pl];
+      const float thr = fminf(o0.x, o1.x) + o0.w;
+      const int cnt0 = __float_as_int(o0.y), cnt1 = __float_as_int(o1.y);
+      const int ovf = __float_as_int(o0.z) | __float_as_int(o1.z);
+      const float2* l0 = lists + buf * KT_LBUF + pl * KT_LIST;
+      const float2* l1 = lists + buf * KT_LBUF + (KT_ROWS + pl) * KT_LIST;
+      // a single survivor is the exact argmin as it stands; points with several
+      // survivors queue their (point, centroid) pairs for the whole warp
+      int nc = 0, k1 = 0;
+      if (valid && !ovf)
+        for (int e = 0; e < cnt0 + cnt1; ++e) {
+          const float2 en = e < cnt0 ? l0[e] : l1[e - cnt0];
+          if (en.x <= thr) {
+            ++nc;
+            k1 = __float_as_int(en.y);
           }
-        const int nq = nc >= 2 ? nc : 0;
-        int off = nq;  // inclusive warp scan of the queue counts
+        }
+      const int nq = nc >= 2 ? nc : 0;
+      int off = nq;  // inclusive warp scan of the queue counts
 #pragma unroll
-        for (int sft = 1; sft < 32; sft <<= 1) {
-          const int v = __shfl_up_sync(0xffffffffu, off, sft);
-          if (lane >= sft) off += v;
+      for (int sft = 1; sft < 32; sft <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, off, sft);
+        if (lane >= sft) off += v;
+      }
+      const int total = __shfl_sync(0xffffffffu, off, 31);
+      off -= nq;
+      if (nq) {
+        int w = off;
+        for (int e = 0; e < cnt0 + cnt1; ++e) {
+          const float2 en = e < cnt0 ? l0[e] : l1[e - cnt0];
+          if (en.x <= thr) wq[w++] = make_int2(__float_as_int(en.y) | (lane << 16), 0);
         }
-        const int total = __shfl_sync(0xffffffffu, off, 31);
-        off -= nq;
-        int2* wq = vq + quad * (32 * 2 * KT_LIST);
-        if (nq) {
-          int w = off;
-          for (int e = 0; e < cnt + cnt1; ++e) {
-            const float2 en = e < cnt ? my[e] : other[e - cnt];
-            if (en.x <= thr) wq[w++] = make_int2(__float_as_int(en.y) | (lane << 16), 0);
-          }
+      }
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&lempty[buf]);  // lists consumed (the queue is private)
+      const int row0 = row - lane;
+      for (int i = lane; i < total; i += 32) {
+        const int2 e = wq[i];
+        const int p = e.x >> 16, k = e.x & 0xffff;
+        float x[KT_D];
+#pragma unroll
+        for (int j = 0; j < KT_D; j += 4) {
+          const float4 v = __ldg(reinterpret_cast<const float4*>(pts + static_cast<int64_t>(row0 + p) * KT_D + j));
+          x[j] = v.x;
+          x[j + 1] = v.y;
+          x[j + 2] = v.z;
+          x[j + 3] = v.w;
         }
-        __syncwarp();
-        const int row0 = row - lane;
-        for (int i = lane; i < total; i += 32) {
-          const int2 e = wq[i];
-          const int p = e.x >> 16, k = e.x & 0xffff;
+        wq[i].y = __float_as_int(exact_dist(x, cent + static_cast<int64_t>(k) * KT_D));
+      }
+      __syncwarp();
+      if (valid) {
+        int bk = k1;
+        if (ovf) {  // candidate list overflowed: exact scan over all K (rare)
+          atomicAdd(n_overflow, 1);
           float x[KT_D];
 #pragma unroll
           for (int j = 0; j < KT_D; j += 4) {
-            const float4 v = __ldg(reinterpret_cast<const float4*>(pts + static_cast<int64_t>(row0 + p) * KT_D + j));
+            const float4 v = __ldg(reinterpret_cast<const float4*>(pts + static_cast<int64_t>(row) * KT_D + j));
             x[j] = v.x;
             x[j + 1] = v.y;
             x[j + 2] = v.z;
             x[j + 3] = v.w;
           }
-          wq[i].y = __float_as_int(exact_dist(x, cent + static_cast<int64_t>(k) * KT_D));
-        }
-        __syncwarp();
-        if (valid) {
-          int bk = k1;
-          if (ovf) {  // candidate list overflowed: exact scan over all K (rare)
-            atomicAdd(n_overflow, 1);
-            float x[KT_D];
-#pragma unroll
-            for (int j = 0; j < KT_D; j += 4) {
-              const float4 v = __ldg(reinterpret_cast<const float4*>(pts + static_cast<int64_t>(row) * KT_D + j));
-              x[j] = v.x;
-              x[j + 1] = v.y;
-              x[j + 2] = v.z;
-              x[j + 3] = v.w;
-            }
-            float best = __int_as_float(0x7f800000);
-            for (int k = 0; k < K; ++k) {
-              const float e = exact_dist(x, cent + static_cast<int64_t>(k) * KT_D);
-              if (e < best) { best = e; bk = k; }
-            }
-          } else if (nq) {
-            float best = __int_as_float(0x7f800000);
-            bk = 0x7fffffff;
-            for (int i = off; i < off + nq; ++i) {
-              const int2 e = wq[i];
-              const float d = __int_as_float(e.y);
-              const int k = e.x & 0xffff;
-              if (d < best || (d == best && k < bk)) { best = d; bk = k; }
-            }
+          float best = __int_as_float(0x7f800000);
+          for (int k = 0; k < K; ++k) {
+            const float e = exact_dist(x, cent + static_cast<int64_t>(k) * KT_D);
+            if (e < best) { best = e; bk = k; }
           }
-          assign[row] = bk;
+        } else if (nq) {
+          float best = __int_as_float(0x7f800000);
+          bk = 0x7fffffff;
+          for (int i = off; i < off + nq; ++i) {
+            const int2 e = wq[i];
+            const float d = __int_as_float(e.y);
+            const int k = e.x & 0xffff;
+            if (d < best || (d == best && k < bk)) { best = d; bk = k; }
+          }
         }
+        assign[row] = bk;
       }
-      epi_bar();
+      __syncwarp();
     }
   }
 
   ptx::tc_fence_before();
   ptx::cluster_sync();
-  if (warp == MMA) {
+  if (warp == KT_MMA) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc<2>(tmem_base, 512);
   }
