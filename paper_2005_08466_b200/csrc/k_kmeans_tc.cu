@@ -29,8 +29,8 @@
 // persistent CTA pair (cta_group::2) per 2 SMs: the pair's B halves for all K
 // are resident (K/2 x 256 B per CTA, <= 128 KB), A tiles of 2 x 128 points
 // stream through 2 stages, and each tile runs K/256 chunks of N=256 MMAs into
-// two TMEM accumulators. Scan warps 0-3 take the even chunks (accumulator 0),
-// warps 4-7 the odd ones (accumulator 1), and hand each tile's candidate lists
+// two TMEM accumulators. Scan warps 0-3 take columns 0-127 of every chunk,
+// warps 4-7 columns 128-255, and hand each tile's candidate lists
 // (double-buffered in shared memory, mbarrier handshakes) to verify warps 8-11,
 // which filter, check exactly and store while the scan runs on.
 #include <cuda.h>
@@ -137,7 +137,7 @@ __global__ void __launch_bounds__(KT_THREADS, 1)
     }
     for (int a = 0; a < 2; ++a) {
       ptx::mbar_init(&tfull[a], 1);
-      ptx::mbar_init(&tempty[a], 2 * 4);  // the 4 warps of one scan group, both CTAs
+      ptx::mbar_init(&tempty[a], 2 * KT_SCAN);  // every scan warp, both CTAs
       ptx::mbar_init(&lfull[a], KT_SCAN);
       ptx::mbar_init(&lempty[a], KT_VER);
     }
@@ -210,14 +210,14 @@ __global__ void __launch_bounds__(KT_THREADS, 1)
     }
     __syncwarp();
   } else if (warp < KT_SCAN) {
-    // ---------------- scan: groups g = 0 (even chunks), 1 (odd chunks) ----------------
+    // ---------------- scan: group g = column half g of every chunk ----------------
     const int g = warp / 4, quad = warp % 4;
     const int pl = quad * 32 + lane;  // point within the CTA tile = TMEM lane
     for (int i = threadIdx.x; i < K; i += KT_SCAN * 32) sq[i] = qg[i];
     const float qmax = stats[0];
     const float cmax = sqrtf(qmax);
     epi_bar();
-    uint32_t acc_phase = 0;
+    uint32_t ph0 = 0, ph1 = 0;
     int it = 0;
     for (int t = cluster; t < tiles; t += nclusters, ++it) {
       const int buf = it & 1;
@@ -229,26 +229,32 @@ __global__ void __launch_bounds__(KT_THREADS, 1)
       int cnt = 0, ovf = 0;
       ptx::mbar_wait(&lempty[buf], ((it >> 1) & 1) ^ 1);  // the verify warps are done with this buffer
       float2* my = lists + buf * KT_LBUF + (g * KT_ROWS + pl) * KT_LIST;
-      for (int c = g; c < nch; c += 2) {
-        ptx::mbar_wait(&tfull[g], acc_phase);
-        acc_phase ^= 1;
+      for (int c = 0; c < nch; ++c) {
+        const int acc = c & 1;
+        if (acc == 0) {
+          ptx::mbar_wait(&tfull[0], ph0);
+          ph0 ^= 1;
+        } else {
+          ptx::mbar_wait(&tfull[1], ph1);
+          ph1 ^= 1;
+        }
         ptx::tc_fence_after();
-        const uint32_t tbase =
-            tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + static_cast<uint32_t>(g * 256);
+        const uint32_t tbase = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) +
+                               static_cast<uint32_t>(acc * 256 + g * 128);
         uint32_t r[2][32];
         ptx::tmem_ld_32x32b_x32(tbase, r[0]);
         ptx::tmem_ld_wait();
 #pragma unroll
-        for (int b = 0; b < 8; ++b) {
+        for (int b = 0; b < 4; ++b) {
           uint32_t (&cur)[32] = r[b & 1];
-          if (b < 7) {
+          if (b < 3) {
             ptx::tmem_ld_32x32b_x32(tbase + (b + 1) * 32, r[(b + 1) & 1]);  // next batch in flight
-          } else {  // accumulator drained: hand it back to the MMA warp
+          } else {  // our half of the accumulator drained: hand it back to the MMA warp
             ptx::tc_fence_before();
             __syncwarp();
-            if (lane == 0) ptx::mbar_arrive_cluster_relaxed(ptx::mapa(ptx::smem_u32(&tempty[g]), 0));
+            if (lane == 0) ptx::mbar_arrive_cluster_relaxed(ptx::mapa(ptx::smem_u32(&tempty[acc]), 0));
           }
-          const int k0 = c * 256 + b * 32;
+          const int k0 = c * 256 + g * 128 + b * 32;
           const float4* q4 = reinterpret_cast<const float4*>(sq + k0);
           float bmin = __int_as_float(0x7f800000);
 #pragma unroll
@@ -287,7 +293,7 @@ __global__ void __launch_bounds__(KT_THREADS, 1)
             else
               ovf = 1;
           }
-          if (b < 7) ptx::tmem_ld_wait();
+          if (b < 3) ptx::tmem_ld_wait();
         }
       }
       xch[(buf * 2 + g) * KT_ROWS + pl] = make_float4(m, __int_as_float(cnt), __int_as_float(ovf), two_eps);
