@@ -39,6 +39,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include <string>
 
 #include "common.hpp"
@@ -104,7 +105,10 @@ __global__ void __launch_bounds__(KT_THREADS, 1)
                             const __grid_constant__ CUtensorMap tmB2, const float* __restrict__ qg,
                             const float* __restrict__ stats, const float* __restrict__ cent,
                             const float* __restrict__ pts, const float* __restrict__ xxg,
-                            int32_t* __restrict__ assign, int rows, int K, int* __restrict__ n_overflow) {
+                            int32_t* __restrict__ assign, int rows, int K, int* __restrict__ n_overflow,
+                            int dbg) {
+  // dbg (HCL_KM_DBG, diagnostics only; wrong results): bit 0 skips the exact
+  // verification, bit 1 the candidate masks, bit 2 the whole verify stage
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const KtLayout L(K);
@@ -256,7 +260,7 @@ __global__ void __launch_bounds__(KT_THREADS, 1)
           }
           const int k0 = c * 256 + g * 128 + b * 32;
           const float4* q4 = reinterpret_cast<const float4*>(sq + k0);
-          float bmin = __int_as_float(0x7f800000);
+          float g4[8];  // minima of the 8 groups of 4 columns
 #pragma unroll
           for (int j = 0; j < 32; j += 4) {
             const float4 qv = q4[j / 4];
@@ -268,30 +272,49 @@ __global__ void __launch_bounds__(KT_THREADS, 1)
             cur[j + 1] = __float_as_uint(t1);
             cur[j + 2] = __float_as_uint(t2);
             cur[j + 3] = __float_as_uint(t3);
-            bmin = fminf(bmin, fminf(fminf(t0, t1), fminf(t2, t3)));
+            g4[j / 4] = fminf(fminf(t0, t1), fminf(t2, t3));
           }
+          const float bmin = fminf(fminf(fminf(g4[0], g4[1]), fminf(g4[2], g4[3])),
+                                   fminf(fminf(g4[4], g4[5]), fminf(g4[6], g4[7])));
           m = fminf(m, bmin);
           const float thr = m + two_eps;
-          // branch-free candidate mask; the (rare) appends loop over its bits.
-          // Entries carry their batch minimum, a lower bound of their t (no
-          // dynamic register indexing): an entry whose batch minimum exceeds the
-          // final threshold is certainly stale; the rest are verified exactly.
+          // candidate groups by their minima (8 tests per batch); the rare hits
+          // test their 4 columns with static register indices and append (t, k)
           uint32_t mask = 0;
+          if (!(dbg & 2)) {
 #pragma unroll
-          for (int j = 0; j < 32; ++j) mask |= (__uint_as_float(cur[j]) <= thr ? 1u : 0u) << j;
+            for (int i = 0; i < 8; ++i) mask |= (g4[i] <= thr ? 1u : 0u) << i;
+          }
           while (mask) {
-            const int j = __ffs(mask) - 1;
+            const int i = __ffs(mask) - 1;
             mask &= mask - 1;
-            if (cnt == KT_LIST) {  // drop entries the running minimum has excluded
-              int w = 0;
-              for (int e = 0; e < KT_LIST; ++e)
-                if (my[e].x <= thr) my[w++] = my[e];
-              cnt = w;
+            float tv[4];
+            switch (i) {
+#define HCL_KT_CASE(I)                                                   \
+  case I:                                                                \
+    tv[0] = __uint_as_float(cur[4 * I]);                                 \
+    tv[1] = __uint_as_float(cur[4 * I + 1]);                             \
+    tv[2] = __uint_as_float(cur[4 * I + 2]);                             \
+    tv[3] = __uint_as_float(cur[4 * I + 3]);                             \
+    break;
+              HCL_KT_CASE(0) HCL_KT_CASE(1) HCL_KT_CASE(2) HCL_KT_CASE(3)
+              HCL_KT_CASE(4) HCL_KT_CASE(5) HCL_KT_CASE(6) default: HCL_KT_CASE(7)
+#undef HCL_KT_CASE
             }
-            if (cnt < KT_LIST)
-              my[cnt++] = make_float2(bmin, __int_as_float(k0 + j));
-            else
-              ovf = 1;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              if (!(tv[u] <= thr)) continue;
+              if (cnt == KT_LIST) {  // drop entries the running minimum has excluded
+                int w = 0;
+                for (int e = 0; e < KT_LIST; ++e)
+                  if (my[e].x <= thr) my[w++] = my[e];
+                cnt = w;
+              }
+              if (cnt < KT_LIST)
+                my[cnt++] = make_float2(tv[u], __int_as_float(k0 + 4 * i + u));
+              else
+                ovf = 1;
+            }
           }
           if (b < 3) ptx::tmem_ld_wait();
         }
@@ -311,6 +334,11 @@ __global__ void __launch_bounds__(KT_THREADS, 1)
       const int row = t * 2 * KT_ROWS + static_cast<int>(rank) * KT_ROWS + pl;
       const bool valid = row < rows;
       ptx::mbar_wait(&lfull[buf], (it >> 1) & 1);
+      if (dbg & 4) {
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&lempty[buf]);
+        continue;
+      }
       const float4 o0 = xch[(buf * 2 + 0) * KT_ROWS + pl];
       const float4 o1 = xch[(buf * 2 + 1) * KT_ROWS + pl];
       const float thr = fminf(o0.x, o1.x) + o0.w;
@@ -329,7 +357,7 @@ __global__ void __launch_bounds__(KT_THREADS, 1)
             k1 = __float_as_int(en.y);
           }
         }
-      const int nq = nc >= 2 ? nc : 0;
+      const int nq = (nc >= 2 && !(dbg & 1)) ? nc : 0;
       int off = nq;  // inclusive warp scan of the queue counts
 #pragma unroll
       for (int sft = 1; sft < 32; sft <<= 1) {
@@ -515,9 +543,11 @@ uint64_t launch_assign_tc(LaunchCtx& c) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  const char* dbg_env = std::getenv("HCL_KM_DBG");
+  const int dbg = dbg_env ? std::atoi(dbg_env) : 0;
   HCL_CUDA(cudaLaunchKernelEx(&cfg, kmeans_assign_tc_kernel, ta, tb1, tb2, static_cast<const float*>(q),
                               reinterpret_cast<const float*>(stats), reinterpret_cast<const float*>(Cb.ptr), pts, xx,
-                              asg, static_cast<int>(rows), static_cast<int>(k), n_ovf));
+                              asg, static_cast<int>(rows), static_cast<int>(k), n_ovf, dbg));
   HCL_LAUNCHED();
   return 3ull * rows * static_cast<uint64_t>(k) * static_cast<uint64_t>(d);
 }
