@@ -260,7 +260,7 @@ __global__ void __launch_bounds__(KT_THREADS, 1)
           }
           const int k0 = c * 256 + g * 128 + b * 32;
           const float4* q4 = reinterpret_cast<const float4*>(sq + k0);
-          float g4[8];  // minima of the 8 groups of 4 columns
+          float bmin = __int_as_float(0x7f800000);
 #pragma unroll
           for (int j = 0; j < 32; j += 4) {
             const float4 qv = q4[j / 4];
@@ -272,49 +272,32 @@ __global__ void __launch_bounds__(KT_THREADS, 1)
             cur[j + 1] = __float_as_uint(t1);
             cur[j + 2] = __float_as_uint(t2);
             cur[j + 3] = __float_as_uint(t3);
-            g4[j / 4] = fminf(fminf(t0, t1), fminf(t2, t3));
+            bmin = fminf(bmin, fminf(fminf(t0, t1), fminf(t2, t3)));
           }
-          const float bmin = fminf(fminf(fminf(g4[0], g4[1]), fminf(g4[2], g4[3])),
-                                   fminf(fminf(g4[4], g4[5]), fminf(g4[6], g4[7])));
           m = fminf(m, bmin);
           const float thr = m + two_eps;
-          // candidate groups by their minima (8 tests per batch); the rare hits
-          // test their 4 columns with static register indices and append (t, k)
+          // branch-free candidate mask; the (rare) appends loop over its bits.
+          // Entries carry their batch minimum, a lower bound of their t (no
+          // dynamic register indexing): an entry whose batch minimum exceeds the
+          // final threshold is certainly stale; the rest are verified exactly.
           uint32_t mask = 0;
           if (!(dbg & 2)) {
 #pragma unroll
-            for (int i = 0; i < 8; ++i) mask |= (g4[i] <= thr ? 1u : 0u) << i;
+            for (int j = 0; j < 32; ++j) mask |= (__uint_as_float(cur[j]) <= thr ? 1u : 0u) << j;
           }
           while (mask) {
-            const int i = __ffs(mask) - 1;
+            const int j = __ffs(mask) - 1;
             mask &= mask - 1;
-            float tv[4];
-            switch (i) {
-#define HCL_KT_CASE(I)                                                   \
-  case I:                                                                \
-    tv[0] = __uint_as_float(cur[4 * I]);                                 \
-    tv[1] = __uint_as_float(cur[4 * I + 1]);                             \
-    tv[2] = __uint_as_float(cur[4 * I + 2]);                             \
-    tv[3] = __uint_as_float(cur[4 * I + 3]);                             \
-    break;
-              HCL_KT_CASE(0) HCL_KT_CASE(1) HCL_KT_CASE(2) HCL_KT_CASE(3)
-              HCL_KT_CASE(4) HCL_KT_CASE(5) HCL_KT_CASE(6) default: HCL_KT_CASE(7)
-#undef HCL_KT_CASE
+            if (cnt == KT_LIST) {  // drop entries the running minimum has excluded
+              int w = 0;
+              for (int e = 0; e < KT_LIST; ++e)
+                if (my[e].x <= thr) my[w++] = my[e];
+              cnt = w;
             }
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              if (!(tv[u] <= thr)) continue;
-              if (cnt == KT_LIST) {  // drop entries the running minimum has excluded
-                int w = 0;
-                for (int e = 0; e < KT_LIST; ++e)
-                  if (my[e].x <= thr) my[w++] = my[e];
-                cnt = w;
-              }
-              if (cnt < KT_LIST)
-                my[cnt++] = make_float2(tv[u], __int_as_float(k0 + 4 * i + u));
-              else
-                ovf = 1;
-            }
+            if (cnt < KT_LIST)
+              my[cnt++] = make_float2(bmin, __int_as_float(k0 + j));
+            else
+              ovf = 1;
           }
           if (b < 3) ptx::tmem_ld_wait();
         }
