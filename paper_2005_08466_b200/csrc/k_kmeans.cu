@@ -122,6 +122,39 @@ __global__ void __launch_bounds__(1024) kmeans_accumulate_kernel(const float* __
   }
   const int64_t chunk = (n + gridDim.x - 1) / gridDim.x;
   const int64_t lo = blockIdx.x * chunk, hi = min(n, lo + chunk);
+  if (use_smem && d == 32) {
+    // D = 32: lane = dimension; 8 points per warp iteration so the loads of
+    // the next points are in flight together (the loop is latency-bound
+    // otherwise). A cluster row is flushed to the int64 totals whenever its
+    // block-local count reaches 2^15, so |int32 sum| <= (2^15 + 32) * 2^15 < 2^31
+    // for any data (points on the 2^-12 grid in [-8, 8)).
+    constexpr int U = 8;
+    for (int64_t base = lo + static_cast<int64_t>(warp) * U; base < hi; base += static_cast<int64_t>(nwarps) * U) {
+      int cs[U], qs[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t i = base + u;
+        cs[u] = i < hi ? __ldg(assign + i) : -1;
+        qs[u] = i < hi ? __float2int_rz(__fmul_rn(__ldg(pts + i * 32 + lane), 4096.0f)) : 0;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int c = cs[u];
+        if (c < 0) continue;
+        atomicAdd(&tbl[c * 32 + lane], qs[u]);
+        int old = 0;
+        if (lane == 0) old = atomicAdd(&tbl[k * 32 + c], 1);
+        old = __shfl_sync(0xffffffffu, old, 0);
+        if (old + 1 == (1 << 15)) {
+          __syncwarp();
+          const int v = atomicExch(&tbl[c * 32 + lane], 0);
+          atomicAdd(&sums[static_cast<int64_t>(c) * 32 + lane],
+                    static_cast<unsigned long long>(static_cast<long long>(v)));
+          if (lane == 0) atomicAdd(&counts[c], static_cast<unsigned long long>(atomicExch(&tbl[k * 32 + c], 0)));
+        }
+      }
+    }
+  } else
   for (int64_t i = lo + warp; i < hi; i += nwarps) {
     const int c = assign[i];
     for (int j = lane; j < d; j += 32) {

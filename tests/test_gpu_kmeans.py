@@ -148,3 +148,24 @@ def test_tensor_filter_ties_and_general_fp32(ctx, queues):
     km.close()
     assert (got == want).all()
     assert (got[50:100] == 9).all()
+
+
+def test_accumulate_many_points_one_cluster(ctx, queues):
+    """Block-local int32 sums are flushed before they can overflow: 5M copies of
+    the largest grid point in one cluster (int64 sums far beyond 2^31)."""
+    from paper_2005_08466_b200.kmeans import KMeans
+
+    n, d, k = 5_000_000, 32, 2
+    pts = np.full((n, d), 8.0 - 2.0**-12, np.float32)
+    pts[::2, ::2] = -8.0
+    cent = np.stack([np.full(d, 7.0, np.float32), np.full(d, -100.0, np.float32)])
+    a = O.kmeans_assign(pts.reshape(-1), n, d, cent.reshape(-1), k)
+    s_want, c_want = O.kmeans_accumulate(pts.reshape(-1), n, d, a, k)
+    km = KMeans(ctx, queues[:1], n, d, k)
+    km.load_points(pts)
+    km.set_centroids(cent)
+    km.iterate(1)
+    s, c = km.sums()
+    km.close()
+    assert (c == c_want).all() and (s == s_want).all()
+    assert c_want[0] == n and abs(int(s_want[1])) > 2**31
