@@ -371,6 +371,136 @@ __global__ void __launch_bounds__(KNN_T) knn_f64_kernel(const double* __restrict
   }
 }
 
+// k > 32 (up to KNN_LARGE_MAXK): one 256-thread block per query keeps the
+// running top-k sorted in shared memory. Each tile of 256 references is
+// scored (same exact order), the candidates below the current k-th pair are
+// compacted and bitonic-sorted, and the two sorted runs are merged by rank
+// (pairs are distinct: indices are unique), so the result is the k smallest
+// under (dist, idx) exactly as the reference's partial_sort.
+constexpr int KNN_LT = 256, KNN_LARGE_MAXK = 4096;
+
+__device__ __forceinline__ int rank_lt(const double* d, const int* ix, int n, double vd, int vi) {
+  int lo = 0, hi = n;  // number of elements < (vd, vi)
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (pair_lt(d[mid], ix[mid], vd, vi)) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+__global__ void __launch_bounds__(KNN_LT) knn_large_kernel(const double* __restrict__ refp,
+                                                          const double* __restrict__ query, int64_t R, int64_t D,
+                                                          int k, int64_t idx_base, int32_t* __restrict__ out_idx,
+                                                          double* __restrict__ out_dist) {
+  extern __shared__ __align__(16) uint8_t kl_smem[];
+  double* bd = reinterpret_cast<double*>(kl_smem);          // k
+  double* od = bd + k;                                       // k
+  double* cd = od + k;                                       // KNN_LT
+  double* sq = cd + KNN_LT;                                  // D
+  int* bi = reinterpret_cast<int*>(sq + D);                  // k
+  int* oi = bi + k;                                          // k
+  int* ci = oi + k;                                          // KNN_LT
+  __shared__ int n_cand;
+  const int64_t q = blockIdx.x;
+  const int t = threadIdx.x;
+  for (int64_t d = t; d < D; d += KNN_LT) sq[d] = query[q * D + d];
+  int cur = 0;
+  __syncthreads();
+  for (int64_t r0 = 0; r0 < R; r0 += KNN_LT) {
+    const int64_t r = r0 + t;
+    double dist = __longlong_as_double(0x7ff0000000000000LL);
+    int id = 0x7fffffff;
+    if (r < R) {
+      const double* p = refp + r * D;
+      double sum = 0.0;
+      for (int64_t d = 0; d < D; ++d) {
+        const double diff = __dsub_rn(p[d], sq[d]);
+        sum = __dadd_rn(sum, __dmul_rn(diff, diff));
+      }
+      dist = sum;
+      id = static_cast<int>(idx_base + r);
+    }
+    const bool pass = r < R && (cur < k || pair_lt(dist, id, bd[k - 1], bi[k - 1]));
+    if (t == 0) n_cand = 0;
+    __syncthreads();
+    if (pass) {
+      const int slot = atomicAdd(&n_cand, 1);
+      cd[slot] = dist;
+      ci[slot] = id;
+    }
+    __syncthreads();
+    const int nc = n_cand;
+    __syncthreads();        // every thread has read n_cand before thread 0 resets it
+    if (nc == 0) continue;  // uniform
+    // bitonic sort of the candidates (padded to a power of two with +inf)
+    int np = 1;
+    while (np < nc) np <<= 1;
+    for (int i = nc + t; i < np; i += KNN_LT) {
+      cd[i] = __longlong_as_double(0x7ff0000000000000LL);
+      ci[i] = 0x7fffffff;
+    }
+    __syncthreads();
+    for (int size = 2; size <= np; size <<= 1)
+      for (int stride = size >> 1; stride > 0; stride >>= 1) {
+        for (int i = t; i < np; i += KNN_LT) {
+          const int j = i ^ stride;
+          if (j > i) {
+            const bool up = (i & size) == 0;
+            if (pair_lt(cd[j], ci[j], cd[i], ci[i]) == up) {
+              const double td = cd[i];
+              const int ti = ci[i];
+              cd[i] = cd[j];
+              ci[i] = ci[j];
+              cd[j] = td;
+              ci[j] = ti;
+            }
+          }
+        }
+        __syncthreads();
+      }
+    // merge the sorted runs by rank into od/oi, keep the first k
+    for (int i = t; i < cur; i += KNN_LT) {
+      const int pos = i + rank_lt(cd, ci, nc, bd[i], bi[i]);
+      if (pos < k) {
+        od[pos] = bd[i];
+        oi[pos] = bi[i];
+      }
+    }
+    for (int j = t; j < nc; j += KNN_LT) {
+      const int pos = j + rank_lt(bd, bi, cur, cd[j], ci[j]);
+      if (pos < k) {
+        od[pos] = cd[j];
+        oi[pos] = ci[j];
+      }
+    }
+    __syncthreads();
+    cur = min(k, cur + nc);
+    for (int i = t; i < cur; i += KNN_LT) {
+      bd[i] = od[i];
+      bi[i] = oi[i];
+    }
+    __syncthreads();
+  }
+  for (int i = t; i < k; i += KNN_LT) {
+    out_dist[q * k + i] = i < cur ? bd[i] : __longlong_as_double(0x7ff0000000000000LL);
+    out_idx[q * k + i] = i < cur ? bi[i] : 0x7fffffff;
+  }
+}
+
+void launch_knn_large(LaunchCtx& c, const double* refp, const double* qp, int64_t r, int64_t d, int64_t k,
+                      int64_t idx_base, int64_t nq, int32_t* oi, double* od) {
+  if (k > KNN_LARGE_MAXK)
+    fail(ErrorCode::argument, "knn: the GPU path supports k <= " + std::to_string(KNN_LARGE_MAXK));
+  const size_t smem = static_cast<size_t>(2 * k + KNN_LT + d) * 8 + static_cast<size_t>(2 * k + KNN_LT) * 4;
+  if (smem > 220 * 1024) fail(ErrorCode::argument, "knn: k and D too large for the GPU path");
+  if (smem > 48 * 1024)
+    HCL_CUDA(cudaFuncSetAttribute(knn_large_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem)));
+  knn_large_kernel<<<static_cast<unsigned>(nq), KNN_LT, smem, c.stream>>>(refp, qp, r, d, static_cast<int>(k),
+                                                                          idx_base, oi, od);
+  HCL_LAUNCHED();
+}
+
 uint64_t launch_knn(LaunchCtx& c) {
   int64_t r = scalar_arg(c, 2, "knn R");
   int64_t q = scalar_arg(c, 3, "knn Q");
@@ -378,8 +508,6 @@ uint64_t launch_knn(LaunchCtx& c) {
   int64_t k = scalar_arg(c, 5, "knn k");
   if (r < 1 || q < 1 || d < 1) fail(ErrorCode::argument, "knn: R, Q, D must be >= 1");
   if (k < 1 || k > r) fail(ErrorCode::argument, "knn: need 1 <= k <= R");
-  if (k > KNN_MAXK)
-    fail(ErrorCode::argument, "knn: the GPU path supports k <= " + std::to_string(KNN_MAXK));
   if (r > INT32_MAX) fail(ErrorCode::argument, "knn: R exceeds int32 indices");
   const BufView& Rf = buffer_arg(c, 0, "knn ref");
   const BufView& Qb = buffer_arg(c, 1, "knn query");
@@ -393,6 +521,10 @@ uint64_t launch_knn(LaunchCtx& c) {
   const double* qp = at_byte<const double>(Qb, lo * d * 8, cnt * d * 8, "knn query");
   int32_t* oi = at_byte<int32_t>(buffer_arg(c, 6, "knn idx"), lo * k * 4, cnt * k * 4, "knn idx");
   double* od = at_byte<double>(buffer_arg(c, 7, "knn dist"), lo * k * 8, cnt * k * 8, "knn dist");
+  if (k > KNN_MAXK) {
+    if (cnt) launch_knn_large(c, reinterpret_cast<const double*>(Rf.ptr), qp, r, d, k, 0, cnt, oi, od);
+    return static_cast<uint64_t>(d) * r * cnt;
+  }
   size_t smem = static_cast<size_t>(d) * 8;
   if (smem > 200 * 1024) fail(ErrorCode::argument, "knn: D too large for the GPU path");
   if (smem > 48 * 1024)
@@ -419,8 +551,6 @@ uint64_t launch_knn_refsplit(LaunchCtx& c) {
   int64_t k = scalar_arg(c, 5, "knn_refsplit k");
   if (r < 1 || q < 1 || d < 1) fail(ErrorCode::argument, "knn_refsplit: R, Q, D must be >= 1");
   if (k < 1 || k > r) fail(ErrorCode::argument, "knn_refsplit: need 1 <= k <= R");
-  if (k > KNN_MAXK)
-    fail(ErrorCode::argument, "knn_refsplit: the GPU path supports k <= " + std::to_string(KNN_MAXK));
   if (r > INT32_MAX) fail(ErrorCode::argument, "knn_refsplit: R exceeds int32 indices");
   const BufView& Rf = buffer_arg(c, 0, "knn_refsplit ref");
   const BufView& Qb = buffer_arg(c, 1, "knn_refsplit query");
@@ -432,6 +562,11 @@ uint64_t launch_knn_refsplit(LaunchCtx& c) {
   const double* rp = at_byte<const double>(Rf, lo * d * 8, cnt * d * 8, "knn_refsplit ref");
   int32_t* oi = at_byte<int32_t>(buffer_arg(c, 6, "knn_refsplit idx"), 0, q * k * 4, "knn_refsplit idx");
   double* od = at_byte<double>(buffer_arg(c, 7, "knn_refsplit dist"), 0, q * k * 8, "knn_refsplit dist");
+  if (k > KNN_MAXK) {
+    if (cnt) launch_knn_large(c, rp, reinterpret_cast<const double*>(Qb.ptr), static_cast<int64_t>(cnt), d, k,
+                              static_cast<int64_t>(lo), q, oi, od);
+    return static_cast<uint64_t>(d) * cnt * q;
+  }
   size_t smem = static_cast<size_t>(d) * 8;
   if (smem > 200 * 1024) fail(ErrorCode::argument, "knn_refsplit: D too large for the GPU path");
   if (smem > 48 * 1024)
@@ -480,20 +615,77 @@ __global__ void knn_merge2_kernel(int32_t* __restrict__ ia, double* __restrict__
   }
 }
 
+// k > 32: one block per query merges the two sorted lists by rank in shared memory
+__global__ void __launch_bounds__(KNN_LT) knn_merge2_large_kernel(int32_t* __restrict__ ia, double* __restrict__ da,
+                                                                 const int32_t* __restrict__ ib,
+                                                                 const double* __restrict__ db, int k,
+                                                                 int* __restrict__ bad) {
+  extern __shared__ __align__(16) uint8_t km_smem[];
+  double* ad = reinterpret_cast<double*>(km_smem);
+  double* bdd = ad + k;
+  int* ai = reinterpret_cast<int*>(bdd + k);
+  int* bii = ai + k;
+  const int64_t q = blockIdx.x;
+  const int t = threadIdx.x;
+  for (int i = t; i < k; i += KNN_LT) {
+    ad[i] = da[q * k + i];
+    ai[i] = ia[q * k + i];
+    bdd[i] = db[q * k + i];
+    bii[i] = ib[q * k + i];
+  }
+  __syncthreads();
+  for (int i = t + 1; i < k; i += KNN_LT)
+    if (pair_lt(ad[i], ai[i], ad[i - 1], ai[i - 1]) || pair_lt(bdd[i], bii[i], bdd[i - 1], bii[i - 1])) atomicOr(bad, 1);
+  // equal pairs (padding) rank a before b; distinct real pairs have distinct ranks
+  for (int i = t; i < k; i += KNN_LT) {
+    int lo = 0, hi = k;  // b elements strictly below a[i]
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (pair_lt(bdd[mid], bii[mid], ad[i], ai[i])) lo = mid + 1; else hi = mid;
+    }
+    const int pos = i + lo;
+    if (pos < k) {
+      da[q * k + pos] = ad[i];
+      ia[q * k + pos] = ai[i];
+    }
+  }
+  for (int j = t; j < k; j += KNN_LT) {
+    int lo = 0, hi = k;  // a elements at or below b[j]
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (!pair_lt(bdd[j], bii[j], ad[mid], ai[mid])) lo = mid + 1; else hi = mid;
+    }
+    const int pos = j + lo;
+    if (pos < k) {
+      da[q * k + pos] = bdd[j];
+      ia[q * k + pos] = bii[j];
+    }
+  }
+}
+
 // knn_refsplit_merge(ref, query, R, Q, D, k, idx, dist, idx2, dist2): the
 // MERGE_TOPK companion (same arguments + the other part's lists).
 uint64_t launch_knn_refsplit_merge(LaunchCtx& c) {
   int64_t q = scalar_arg(c, 3, "knn merge Q");
   int64_t k = scalar_arg(c, 5, "knn merge k");
-  if (q < 1 || k < 1 || k > KNN_MAXK) fail(ErrorCode::argument, "knn merge: bad Q or k");
+  if (q < 1 || k < 1 || k > KNN_LARGE_MAXK) fail(ErrorCode::argument, "knn merge: bad Q or k");
   int32_t* ia = at_byte<int32_t>(buffer_arg(c, 6, "knn merge idx"), 0, q * k * 4, "knn merge idx");
   double* da = at_byte<double>(buffer_arg(c, 7, "knn merge dist"), 0, q * k * 8, "knn merge dist");
   const int32_t* ib = at_byte<const int32_t>(buffer_arg(c, 8, "knn merge idx2"), 0, q * k * 4, "knn merge idx2");
   const double* db = at_byte<const double>(buffer_arg(c, 9, "knn merge dist2"), 0, q * k * 8, "knn merge dist2");
   int* bad = static_cast<int*>(c.scratch(c.dev, sizeof(int)));
   HCL_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), c.stream));
-  knn_merge2_kernel<<<static_cast<unsigned>(ceil_div(q, 128)), 128, 0, c.stream>>>(ia, da, ib, db, q,
+  if (k <= KNN_MAXK) {
+    knn_merge2_kernel<<<static_cast<unsigned>(ceil_div(q, 128)), 128, 0, c.stream>>>(ia, da, ib, db, q,
+                                                                                   static_cast<int>(k), bad);
+  } else {
+    const size_t smem = static_cast<size_t>(k) * 24;
+    if (smem > 48 * 1024)
+      HCL_CUDA(cudaFuncSetAttribute(knn_merge2_large_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(smem)));
+    knn_merge2_large_kernel<<<static_cast<unsigned>(q), KNN_LT, smem, c.stream>>>(ia, da, ib, db,
                                                                                  static_cast<int>(k), bad);
+  }
   HCL_LAUNCHED();
   int h = 0;
   HCL_CUDA(cudaMemcpyAsync(&h, bad, sizeof(int), cudaMemcpyDeviceToHost, c.stream));

@@ -304,3 +304,40 @@ def test_rate_driven_split(ctx, queues):
     assert plan0[1] > m * 0.7  # model: 120 vs 28 SMs
     assert plan[1] > m * 0.65, plan  # profiled rates agree
     assert got == whole
+
+
+def test_zero_weight_parts_are_skipped(ctx, queues, golden):
+    """Parts with no rows launch nothing and leave the output intact."""
+    n = 512
+    a = O.gen_doubles(n * n, 42)
+    b = O.gen_doubles(n * n, 43)
+    out = run(ctx, "matmul", [a, b, ("out", n * n * 8), n, n, n], [2], queues, global_rows=n, partitioned=True,
+              weights=[0, 1, 0, 3])
+    assert h(O.fnv1a(out[2])) == golden["digests"]["matmul_512"]
+
+
+def test_buffers_beyond_4gib(ctx, queues):
+    """The reference caps a read at one 4 GiB frame (wire.cpp:337-338); here
+    buffers, offsets, peer copies and partial reads are 64-bit: vecadd over
+    4.8 GB operands split over four devices, read back at offsets > 4 GiB."""
+    n = 600_000_000
+    a = O.gen_doubles(n, 42)
+    b = O.gen_doubles(n, 43)
+    prog = ctx.create_program("core")
+    k = ctx.create_kernel(prog, "vecadd")
+    ba, bb, bc = (ctx.create_buffer(n * 8) for _ in range(3))
+    try:
+        ctx.enqueue_write_buffer(queues[0], ba, a)
+        ctx.enqueue_write_buffer(queues[0], bb, b)
+        for i, v in enumerate([ba, bb, bc, n]):
+            ctx.set_kernel_arg(k, i, v)
+        ctx.enqueue_ndrange_partitioned(k, (n, 1, 1), 1, queues, [1, 2, 3, 4])
+        for q in queues:
+            ctx.finish(q)
+        for lo in (0, (1 << 32) // 8 - 3, n - 1000):  # straddles the 4 GiB offset and the part boundaries
+            got = ctx.enqueue_read_buffer(queues[1], bc, offset=lo * 8, length=8000).view(np.float64)
+            want = a[lo:lo + 1000] + b[lo:lo + 1000]
+            assert got.tobytes() == want.tobytes(), lo
+    finally:
+        for hnd in (ba, bb, bc, k, prog):
+            ctx.release(hnd)

@@ -100,3 +100,19 @@ def test_knn_refsplit_errors(ctx, queues):
         run(ctx, "knn_refsplit", [rf, q, 10, 3, 2, 2, ("out", 3 * 2 * 4), ("out", 3 * 2 * 8)], [6, 7],
             [queues[0], queues[0]], global_rows=10, partitioned=True, bundle="b200")
     assert e.value.name == "argument"
+
+
+@pytest.mark.parametrize("R,Q,D,K", [(5000, 40, 16, 100), (700, 9, 5, 700), (3000, 17, 8, 33)])
+@pytest.mark.parametrize("P,weights", [(1, None), (4, [3, 1, 2, 5])])
+def test_knn_large_k(ctx, queues, R, Q, D, K, P, weights):
+    """k > 32 (a block-wide sorted top-k; up to 4096): both the query-split core
+    knn and the reference-set split equal the reference's ref::knn."""
+    rf = O.gen_doubles(R * D, 11)
+    rf[7 * D:8 * D] = rf[2 * D:3 * D]  # a tie
+    q = O.gen_doubles(Q * D, 12)
+    ei, ed = O.knn(rf, q, R, Q, D, K)
+    idx, dist = knn_refsplit(ctx, queues, rf, q, R, Q, D, K, P, weights)
+    assert idx.tolist() == ei.tolist() and dist.tobytes() == ed.tobytes()
+    core = run(ctx, "knn", [rf, q, R, Q, D, K, ("out", Q * K * 4), ("out", Q * K * 8)], [6, 7], queues[:P],
+               global_rows=Q, partitioned=P > 1)
+    assert core[6].view(np.int32).tolist() == ei.tolist() and core[7].tobytes() == ed.tobytes()
