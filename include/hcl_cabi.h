@@ -160,6 +160,14 @@ int hcl_allgatherv(int dev, uint64_t buffer_id, const uint64_t* bounds);
 int hcl_allreduce_sum_i64(int dev, uint64_t buffer_id, uint64_t offset, uint64_t count);
 int hcl_broadcast(int dev, uint64_t buffer_id, uint64_t offset, uint64_t bytes, int root);
 
+/* In-process collective across this process's devices over NVLink peer
+ * copies: devs[i] holds buffer buf_ids[i]. op 0 broadcast
+ * count elements from devs[root]; op 1 allgather (device i contributes
+ * elements [i*count, (i+1)*count)); op 2 allreduce sum in device order (bit-
+ * identical on every device). dtype 0 int64, 1 fp64, 2 fp32. */
+int hcl_collective(int op, const int* devs, int ndev, const uint64_t* buf_ids, uint64_t count, int dtype,
+                   int root);
+
 const char* hcl_last_error(void);
 
 #ifdef __cplusplus

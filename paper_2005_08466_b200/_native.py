@@ -39,6 +39,7 @@ CABI = [
     ("hcl_init", C.c_int, [i32p, C.c_int, i32p]),
     ("hcl_device_count", C.c_int, [i32p]),
     ("hcl_device_info", C.c_int, [C.c_int, i32p, f64p, i32p, u64p, C.c_char_p, C.c_int]),
+    ("hcl_collective", C.c_int, [C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_uint64, C.c_int, C.c_int]),
     ("hcl_device_set_sm_budget", C.c_int, [C.c_int, C.c_int]),
     ("hcl_query_registry", C.c_int, [C.c_char_p, C.c_char_p, C.c_int, C.POINTER(C.c_uint32), C.c_int, i32p]),
     ("hcl_kernel_signature", C.c_int, [C.c_char_p, C.c_char_p, u8p, u8p, C.c_int, i32p]),

@@ -7,6 +7,8 @@
 // becomes an asynchronous kernel launch bracketed by CUDA events.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <atomic>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -206,6 +208,20 @@ void* scratch_for(int dev, size_t bytes) {
     d.scratch_bytes = bytes;
   }
   return d.scratch;
+}
+
+template <typename T>
+__global__ void local_add_kernel(T* __restrict__ dst, const T* __restrict__ src, uint64_t n) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    dst[i] = dst[i] + src[i];
+}
+
+std::atomic<uint64_t> g_coll_tmp{0};
+uint64_t coll_tmp_id() { return 0xC011'0000'0000'0000ULL | g_coll_tmp.fetch_add(1); }
+
+// a nested C-ABI call's failure back into an exception (its message is in g_last_error)
+void check_rc(int rc) {
+  if (rc != HCL_OK) fail(static_cast<ErrorCode>(rc - HCL_ERR_BASE), g_last_error);
 }
 
 }  // namespace
@@ -574,6 +590,67 @@ int hcl_launch(int dev, const char* kernel, const hcl_arg* args, uint32_t nargs,
       if (args[i].kind == HCL_ARG_OUT || args[i].kind == HCL_ARG_INOUT)
         d.note(alloc_of(d, args[i].buffer_id, kernel), d.stream, true);
     if (work_units) *work_units = w;
+  });
+}
+
+// In-process collective over NVLink peer copies (SURVEY.md §8(b)'s proposed
+// hcl_collective): devs[i] holds buffer buf_ids[i].
+//   op 0 broadcast:  bytes [0, count*es) of devs[root] to every device
+//   op 1 allgather:  device i contributes elements [i*count, (i+1)*count)
+//   op 2 allreduce:  element-wise sum in device order (0, 1, ..., ndev-1) on the
+//                    root, then broadcast -- deterministic and bit-identical on
+//                    every device; dtype 0 int64, 1 fp64, 2 fp32
+int hcl_collective(int op, const int* devs, int ndev, const uint64_t* buf_ids, uint64_t count, int dtype, int root) {
+  return guarded([&] {
+    if (ndev < 1 || !devs || !buf_ids) fail(ErrorCode::argument, "collective: need at least one device");
+    if (dtype < 0 || dtype > 2) fail(ErrorCode::argument, "collective: dtype must be 0 (i64), 1 (f64) or 2 (f32)");
+    if (root < 0 || root >= ndev) fail(ErrorCode::argument, "collective: root out of range");
+    const uint64_t es = dtype == 2 ? 4 : 8, bytes = count * es;
+    if (op == 0) {
+      for (int i = 0; i < ndev; ++i)
+        if (i != root) check_rc(hcl_buffer_copy_peer(devs[i], buf_ids[i], 0, devs[root], buf_ids[root], 0, bytes));
+    } else if (op == 1) {
+      for (int j = 0; j < ndev; ++j)
+        for (int i = 0; i < ndev; ++i)
+          if (i != j)
+            check_rc(hcl_buffer_copy_peer(devs[i], buf_ids[i], j * bytes, devs[j], buf_ids[j], j * bytes, bytes));
+    } else if (op == 2) {
+      const int rd = devs[root];
+      const uint64_t acc = coll_tmp_id(), tmp = coll_tmp_id();
+      check_rc(hcl_buffer_alloc(rd, acc, 0, bytes));
+      check_rc(hcl_buffer_alloc(rd, tmp, 0, bytes));
+      check_rc(hcl_buffer_copy_peer(rd, acc, 0, devs[0], buf_ids[0], 0, bytes));
+      for (int i = 1; i < ndev; ++i) {
+        check_rc(hcl_buffer_copy_peer(rd, tmp, 0, devs[i], buf_ids[i], 0, bytes));
+        Device& d = device(rd);
+        std::lock_guard<std::mutex> lock(d.mu);
+        HCL_CUDA(cudaSetDevice(d.ordinal));
+        DevAlloc& aa = alloc_of(d, acc, "collective");
+        DevAlloc& ta = alloc_of(d, tmp, "collective");
+        d.wait_for(aa, d.stream, true);
+        d.wait_for(ta, d.stream, false);
+        const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(ceil_div(count, 256), 8ull * d.sm_count));
+        if (count) {
+          if (dtype == 0)
+            local_add_kernel<long long><<<grid, 256, 0, d.stream>>>(reinterpret_cast<long long*>(aa.ptr),
+                                                                    reinterpret_cast<const long long*>(ta.ptr), count);
+          else if (dtype == 1)
+            local_add_kernel<double><<<grid, 256, 0, d.stream>>>(reinterpret_cast<double*>(aa.ptr),
+                                                                 reinterpret_cast<const double*>(ta.ptr), count);
+          else
+            local_add_kernel<float><<<grid, 256, 0, d.stream>>>(reinterpret_cast<float*>(aa.ptr),
+                                                                reinterpret_cast<const float*>(ta.ptr), count);
+          HCL_LAUNCHED();
+        }
+        d.note(aa, d.stream, true);
+        d.note(ta, d.stream, false);
+      }
+      for (int i = 0; i < ndev; ++i) check_rc(hcl_buffer_copy_peer(devs[i], buf_ids[i], 0, rd, acc, 0, bytes));
+      check_rc(hcl_buffer_release(rd, acc));
+      check_rc(hcl_buffer_release(rd, tmp));
+    } else {
+      fail(ErrorCode::argument, "collective: op must be 0 (broadcast), 1 (allgather) or 2 (allreduce)");
+    }
   });
 }
 

@@ -341,3 +341,52 @@ def test_buffers_beyond_4gib(ctx, queues):
     finally:
         for hnd in (ba, bb, bc, k, prog):
             ctx.release(hnd)
+
+
+def test_in_process_collective_c_abi(ctx, queues):
+    """hcl_collective across the four logical devices of the
+    session: allreduce in device order (bit-identical everywhere), allgather,
+    broadcast; raw C-ABI calls on device-level buffer ids."""
+    import ctypes as C
+
+    from paper_2005_08466_b200 import _native as N
+
+    L = N.lib()
+    ndev, cnt = 4, 1000
+    devs = (C.c_int * ndev)(0, 1, 2, 3)
+    ids = (C.c_uint64 * ndev)(*[0x7700_0000 + i for i in range(ndev)])
+    rng = np.random.default_rng(5)
+    parts = [rng.standard_normal(cnt * ndev) * 10.0**rng.integers(-8, 17, cnt * ndev) for _ in range(ndev)]
+
+    def put(arrs):
+        for i, a in enumerate(arrs):
+            assert L.hcl_buffer_alloc(i, ids[i], 0, a.nbytes) == 0
+            assert L.hcl_buffer_write(i, ids[i], 0, a.ctypes.data, a.nbytes) == 0
+
+    def get(i, nbytes, dt):
+        out = np.empty(nbytes // np.dtype(dt).itemsize, dt)
+        assert L.hcl_buffer_read(i, ids[i], 0, out.ctypes.data, nbytes) == 0
+        return out
+
+    try:
+        put([p.astype(np.float64) for p in parts])
+        assert L.hcl_collective(2, devs, ndev, ids, cnt * ndev, 1, 2) == 0  # allreduce f64, root 2
+        want = ((parts[0] + parts[1]) + parts[2]) + parts[3]
+        for i in range(ndev):
+            assert get(i, cnt * ndev * 8, np.float64).tobytes() == want.tobytes()
+        ints = [np.arange(cnt * ndev, dtype=np.int64) * (i + 1) for i in range(ndev)]
+        put(ints)
+        assert L.hcl_collective(1, devs, ndev, ids, cnt, 0, 0) == 0  # allgather: device i owns slice i
+        want = np.concatenate([ints[i][i * cnt:(i + 1) * cnt] for i in range(ndev)])
+        for i in range(ndev):
+            assert (get(i, cnt * ndev * 8, np.int64) == want).all()
+        fl = [np.full(cnt, i + 0.5, np.float32) for i in range(ndev)]
+        put(fl)
+        assert L.hcl_collective(0, devs, ndev, ids, cnt, 2, 3) == 0  # broadcast f32 from device 3
+        for i in range(ndev):
+            assert (get(i, cnt * 4, np.float32) == 3.5).all()
+        rc = L.hcl_collective(2, devs, ndev, ids, cnt, 7, 0)
+        assert rc == 1000 + 9  # argument
+    finally:
+        for i in range(ndev):
+            L.hcl_buffer_release(i, ids[i])
