@@ -75,7 +75,7 @@ struct KtLayout {
     a = b + static_cast<size_t>(nch) * 2 * KT_BH;
     q = a + static_cast<size_t>(KT_STAGES) * KT_A;
     lists = q + static_cast<size_t>(K) * 4;
-    xch = lists + 2ull * KT_LBUF * 8;             // 2 buffers x (t, k) float2 slots
+    xch = lists + 2ull * KT_LBUF * 8;             // 2 buffers x (bmin, k) float2 slots
     vq = xch + 2ull * 2 * KT_ROWS * 16;           // 2 buffers x 2 groups x (min, count, overflow)
     bars = vq + static_cast<size_t>(KT_VER) * 32 * 2 * KT_LIST * 8;  // verify queues
     total = bars + 16 * 8 + 16 + 1024;            // barriers, TMEM slot, alignment slack
@@ -276,28 +276,28 @@ __global__ void __launch_bounds__(KT_THREADS, 1)
           }
           m = fminf(m, bmin);
           const float thr = m + two_eps;
-          // candidate test per column with a warp vote: the append block is
-          // entered only for the (few) columns some lane's point keeps, so a
-          // score costs a compare plus 1/32 of a vote -- the divergent
-          // per-lane mask (FSETP + SEL + LOP per score) cost three times more
+          // branch-free candidate mask; the (rare) appends loop over its bits.
+          // Entries carry their batch minimum, a lower bound of their t (no
+          // dynamic register indexing): an entry whose batch minimum exceeds the
+          // final threshold is certainly stale; the rest are verified exactly.
+          uint32_t mask = 0;
           if (!(dbg & 2)) {
 #pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              const float tj = __uint_as_float(cur[j]);
-              const bool hit = tj <= thr;
-              if (__ballot_sync(0xffffffffu, hit) && hit) {
-                if (cnt == KT_LIST) {  // drop entries the running minimum has excluded
-                  int w = 0;
-                  for (int e = 0; e < KT_LIST; ++e)
-                    if (my[e].x <= thr) my[w++] = my[e];
-                  cnt = w;
-                }
-                if (cnt < KT_LIST)
-                  my[cnt++] = make_float2(tj, __int_as_float(k0 + j));
-                else
-                  ovf = 1;
-              }
+            for (int j = 0; j < 32; ++j) mask |= (__uint_as_float(cur[j]) <= thr ? 1u : 0u) << j;
+          }
+          while (mask) {
+            const int j = __ffs(mask) - 1;
+            mask &= mask - 1;
+            if (cnt == KT_LIST) {  // drop entries the running minimum has excluded
+              int w = 0;
+              for (int e = 0; e < KT_LIST; ++e)
+                if (my[e].x <= thr) my[w++] = my[e];
+              cnt = w;
             }
+            if (cnt < KT_LIST)
+              my[cnt++] = make_float2(bmin, __int_as_float(k0 + j));
+            else
+              ovf = 1;
           }
           if (b < 3) ptx::tmem_ld_wait();
         }
