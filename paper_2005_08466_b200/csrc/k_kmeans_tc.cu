@@ -260,7 +260,7 @@ __global__ void __launch_bounds__(KT_THREADS, 1)
           }
           const int k0 = c * 256 + g * 128 + b * 32;
           const float4* q4 = reinterpret_cast<const float4*>(sq + k0);
-          float bmin = __int_as_float(0x7f800000);
+          float g4[8];  // independent group minima: a shallow dependency tree, not a 32-long chain
 #pragma unroll
           for (int j = 0; j < 32; j += 4) {
             const float4 qv = q4[j / 4];
@@ -272,18 +272,27 @@ __global__ void __launch_bounds__(KT_THREADS, 1)
             cur[j + 1] = __float_as_uint(t1);
             cur[j + 2] = __float_as_uint(t2);
             cur[j + 3] = __float_as_uint(t3);
-            bmin = fminf(bmin, fminf(fminf(t0, t1), fminf(t2, t3)));
+            g4[j / 4] = fminf(fminf(t0, t1), fminf(t2, t3));
           }
+          const float bmin = fminf(fminf(fminf(g4[0], g4[1]), fminf(g4[2], g4[3])),
+                                   fminf(fminf(g4[4], g4[5]), fminf(g4[6], g4[7])));
           m = fminf(m, bmin);
           const float thr = m + two_eps;
-          // branch-free candidate mask; the (rare) appends loop over its bits.
-          // Entries carry their batch minimum, a lower bound of their t (no
-          // dynamic register indexing): an entry whose batch minimum exceeds the
-          // final threshold is certainly stale; the rest are verified exactly.
+          // branch-free candidate mask (four independent partial masks); the
+          // (rare) appends loop over its bits. Entries carry their batch
+          // minimum, a lower bound of their t (no dynamic register indexing):
+          // an entry whose batch minimum exceeds the final threshold is
+          // certainly stale; the rest are verified exactly.
           uint32_t mask = 0;
           if (!(dbg & 2)) {
+            uint32_t pm[4] = {0, 0, 0, 0};
 #pragma unroll
-            for (int j = 0; j < 32; ++j) mask |= (__uint_as_float(cur[j]) <= thr ? 1u : 0u) << j;
+            for (int j = 0; j < 32; ++j) pm[j & 3] |= (__uint_as_float(cur[j]) <= thr ? 1u : 0u) << j;
+            mask = (pm[0] | pm[1]) | (pm[2] | pm[3]);
+            if (dbg & 8) {  // diagnostics: build the mask but skip the appends
+              ovf |= mask == 0x5a5a5a5au;
+              mask = 0;
+            }
           }
           while (mask) {
             const int j = __ffs(mask) - 1;
