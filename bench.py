@@ -211,6 +211,12 @@ class GemmBf16(Workload):
         got = (c2.astype(np.uint32) << 16).view(np.float32).astype(np.float64).reshape(2, S)
         self.check = float((np.abs(got - ref) / scale).max())
         assert self.check <= 2.0**-8, f"gemm parity guard failed: {self.check}"
+        if d.world > 1:  # B reaches the GPUs as 1/N slices over each rank's PCIe + an NVLink allgather
+            from paper_2005_08466_b200 import HostContext as HC
+
+            uid = d.bcast_bytes(HC.nccl_unique_id() if d.rank == 0 else None)
+            ctx.init_collectives(q, d.rank, d.world, uid)
+            self.kb = split_ranges(S, [1] * d.world)
         self.e2e_setup()
 
     def step(self):
@@ -249,7 +255,13 @@ class GemmBf16(Workload):
         self.e2e_i += 1
         k, bA, bB, bC = self.sets[s]
         ctx.enqueue_write_buffer(q, bA, self.a_host, offset=self.lo * S * 2, blocking=False)
-        ctx.enqueue_write_buffer(q, bB, self.b_host, blocking=False)
+        if self.dist.world == 1:
+            ctx.enqueue_write_buffer(q, bB, self.b_host, blocking=False)
+        else:  # this rank's K-rows of B from host, the rest from the peers over NVLink
+            r, kb = self.dist.rank, self.kb
+            ctx.enqueue_write_buffer(q, bB, self.b_host[kb[r] * S:kb[r + 1] * S], offset=kb[r] * S * 2,
+                                     blocking=False)
+            ctx.enqueue_allgather(q, bB, [x * S * 2 for x in kb])
         ctx.enqueue_ndrange_range(q, k, (S, S, 1), 2, self.lo, self.rows)
         ctx.enqueue_read_buffer(q, bC, offset=self.lo * S * 2, length=self.rows * S * 2, out=self.c_hosts[s],
                                 blocking=False)
@@ -258,8 +270,8 @@ class GemmBf16(Workload):
         return 2.0 * self.S**3
 
     def e2e_bytes(self):
-        S, W = self.S, self.dist.world
-        return S * S * 2 + W * S * S * 2, S * S * 2
+        S = self.S  # all ranks together: A once, B once (sliced + NVLink allgather), C once
+        return 2 * S * S * 2, S * S * 2
 
     def roofline(self, pk):
         return "tensor", pk["bf16_tflops"], "TFLOP/s", 1e12, "MEASURED_PEAKS.json bf16_tflops (burst)"
@@ -268,7 +280,9 @@ class GemmBf16(Workload):
         return {"workload": f"gemm_bf16 {self.S}^3 (C2), NDRange rows split row-block over {self.dist.world} rank(s), "
                             "B replicated, fp32 accumulate, bf16 C",
                 "rows_per_rank": self.rows, "kernel": "tcgen05 cta_group::2 256x256 tiles, TMA, 2 TMEM accumulators",
-                "l2": "inputs 1 GiB > 126 MB L2; no flush", "parity_rows_normwise_err": self.check}
+                "l2": "inputs 1 GiB > 126 MB L2; no flush", "parity_rows_normwise_err": self.check,
+                "e2e_inputs": "per step: A rows per rank H2D; B as 1/N K-row slices H2D per rank + NCCL allgather "
+                              "over NVLink (N>1); C rows D2H; double-buffered, non-blocking copies"}
 
     def traffic(self):
         prof = os.path.join(ROOT, "profiles", "gemm_bf16_ncu.json")
