@@ -848,7 +848,11 @@ def run_b200(args):
         wl.ctx.finish(wl.q)
         dom_ms = d0.elapsed_time(d1) / args.steps
 
-    # e2e through the public API with host buffers
+    # e2e through the public API with host buffers (untimed warm-up first: the
+    # first collectives set up NCCL's peer channels)
+    for _ in range(min(args.warmup, 2)):
+        wl.e2e_step()
+    wl.ctx.finish(wl.q)
     dist.barrier()
     t0 = time.perf_counter()
     for _ in range(args.steps):
