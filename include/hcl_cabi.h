@@ -150,6 +150,11 @@ int hcl_device_stream(int dev, void** stream);
  * later copies order after it. Copies run on per-device H2D / D2H streams. */
 int hcl_stream_acquire(int dev, uint64_t id, int write);
 int hcl_stream_release(int dev, uint64_t id, int write);
+/* The same for the device's collective stream: NCCL work issued there
+ * overlaps kernels on the compute stream, ordered per buffer. */
+int hcl_comm_stream(int dev, void** stream);
+int hcl_comm_acquire(int dev, uint64_t id, int write);
+int hcl_comm_release(int dev, uint64_t id, int write);
 
 /* ---- collectives (NCCL over NVLink 5 / NVSwitch, loaded lazily) ---------- */
 int hcl_nccl_unique_id(uint8_t* out, int cap); /* cap >= 128 */

@@ -39,6 +39,9 @@ CABI = [
     ("hcl_init", C.c_int, [i32p, C.c_int, i32p]),
     ("hcl_device_count", C.c_int, [i32p]),
     ("hcl_device_info", C.c_int, [C.c_int, i32p, f64p, i32p, u64p, C.c_char_p, C.c_int]),
+    ("hcl_comm_stream", C.c_int, [C.c_int, C.POINTER(C.c_void_p)]),
+    ("hcl_comm_acquire", C.c_int, [C.c_int, C.c_uint64, C.c_int]),
+    ("hcl_comm_release", C.c_int, [C.c_int, C.c_uint64, C.c_int]),
     ("hcl_collective", C.c_int, [C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_uint64, C.c_int, C.c_int]),
     ("hcl_device_set_sm_budget", C.c_int, [C.c_int, C.c_int]),
     ("hcl_query_registry", C.c_int, [C.c_char_p, C.c_char_p, C.c_int, C.POINTER(C.c_uint32), C.c_int, i32p]),

@@ -84,6 +84,7 @@ struct Device {
   cudaStream_t stream = nullptr;  // kernels, allocation, peer copies
   cudaStream_t h2d = nullptr;     // host -> device copies
   cudaStream_t d2h = nullptr;     // device -> host copies
+  cudaStream_t comm = nullptr;    // NCCL collectives (overlap the compute stream)
   int sm_count = 0;      // SM budget the kernels size their grids to
   int sm_physical = 0;   // the GPU's SM count
   uint64_t hbm_bytes = 0;
@@ -275,6 +276,7 @@ int hcl_init(const int* cuda_ordinals, int n, int* num_devices) {
       HCL_CUDA(cudaStreamCreateWithFlags(&d->stream, cudaStreamNonBlocking));
       HCL_CUDA(cudaStreamCreateWithFlags(&d->h2d, cudaStreamNonBlocking));
       HCL_CUDA(cudaStreamCreateWithFlags(&d->d2h, cudaStreamNonBlocking));
+      HCL_CUDA(cudaStreamCreateWithFlags(&d->comm, cudaStreamNonBlocking));
       g_devices.push_back(std::move(d));
     }
     // NVLink P2P between every pair (NVSwitch: all-to-all).
@@ -526,6 +528,28 @@ int hcl_stream_acquire(int dev, uint64_t id, int write) {
   });
 }
 
+int hcl_comm_stream(int dev, void** stream) {
+  return guarded([&] { *stream = device(dev).comm; });
+}
+
+int hcl_comm_acquire(int dev, uint64_t id, int write) {
+  return guarded([&] {
+    Device& d = device(dev);
+    std::lock_guard<std::mutex> lock(d.mu);
+    HCL_CUDA(cudaSetDevice(d.ordinal));
+    d.wait_for(alloc_of(d, id, "comm_acquire"), d.comm, write != 0);
+  });
+}
+
+int hcl_comm_release(int dev, uint64_t id, int write) {
+  return guarded([&] {
+    Device& d = device(dev);
+    std::lock_guard<std::mutex> lock(d.mu);
+    HCL_CUDA(cudaSetDevice(d.ordinal));
+    d.note(alloc_of(d, id, "comm_release"), d.comm, write != 0);
+  });
+}
+
 int hcl_stream_release(int dev, uint64_t id, int write) {
   return guarded([&] {
     Device& d = device(dev);
@@ -661,6 +685,7 @@ int hcl_finish(int dev, double* device_ms) {
     HCL_CUDA(cudaSetDevice(d.ordinal));
     HCL_CUDA(cudaStreamSynchronize(d.h2d));
     HCL_CUDA(cudaStreamSynchronize(d.stream));
+    HCL_CUDA(cudaStreamSynchronize(d.comm));
     HCL_CUDA(cudaStreamSynchronize(d.d2h));
     double total = 0.0;
     for (auto& [a, b] : d.timed) {

@@ -111,9 +111,9 @@ uint8_t* buffer_base(int dev, uint64_t id, uint64_t need_first, uint64_t need_le
   return static_cast<uint8_t*>(p) - first;  // logical byte 0
 }
 
-cudaStream_t stream_of(int dev) {
+cudaStream_t stream_of(int dev) {  // the device's collective stream
   void* s = nullptr;
-  hcl_check(hcl_device_stream(dev, &s));
+  hcl_check(hcl_comm_stream(dev, &s));
   return static_cast<cudaStream_t>(s);
 }
 
@@ -164,7 +164,7 @@ int hcl_allgatherv(int dev, uint64_t buffer_id, const uint64_t* bounds) {
     auto [rank, nranks] = g_rank[dev];
     uint8_t* base = buffer_base(dev, buffer_id, bounds[0], bounds[nranks] - bounds[0]);
     cudaStream_t st = stream_of(dev);
-    hcl_check(hcl_stream_acquire(dev, buffer_id, 1));
+    hcl_check(hcl_comm_acquire(dev, buffer_id, 1));
     nccl_check(nccl().groupStart(), "ncclGroupStart");
     for (int r = 0; r < nranks; ++r) {
       size_t n = bounds[r + 1] - bounds[r];
@@ -172,7 +172,7 @@ int hcl_allgatherv(int dev, uint64_t buffer_id, const uint64_t* bounds) {
       nccl_check(nccl().broadcast(base + bounds[r], base + bounds[r], n, ncclUint8, r, comm, st), "ncclBroadcast");
     }
     nccl_check(nccl().groupEnd(), "ncclGroupEnd");
-    hcl_check(hcl_stream_release(dev, buffer_id, 1));
+    hcl_check(hcl_comm_release(dev, buffer_id, 1));
   });
 }
 
@@ -181,10 +181,10 @@ int hcl_allreduce_sum_i64(int dev, uint64_t buffer_id, uint64_t offset, uint64_t
   return guarded([&] {
     ncclComm_t comm = comm_of(dev);
     uint8_t* base = buffer_base(dev, buffer_id, offset, count * 8);
-    hcl_check(hcl_stream_acquire(dev, buffer_id, 1));
+    hcl_check(hcl_comm_acquire(dev, buffer_id, 1));
     nccl_check(nccl().allReduce(base + offset, base + offset, count, ncclInt64, ncclSum, comm, stream_of(dev)),
                "ncclAllReduce");
-    hcl_check(hcl_stream_release(dev, buffer_id, 1));
+    hcl_check(hcl_comm_release(dev, buffer_id, 1));
   });
 }
 
@@ -192,10 +192,10 @@ int hcl_broadcast(int dev, uint64_t buffer_id, uint64_t offset, uint64_t bytes, 
   return guarded([&] {
     ncclComm_t comm = comm_of(dev);
     uint8_t* base = buffer_base(dev, buffer_id, offset, bytes);
-    hcl_check(hcl_stream_acquire(dev, buffer_id, 1));
+    hcl_check(hcl_comm_acquire(dev, buffer_id, 1));
     nccl_check(nccl().broadcast(base + offset, base + offset, bytes, ncclUint8, root, comm, stream_of(dev)),
                "ncclBroadcast");
-    hcl_check(hcl_stream_release(dev, buffer_id, 1));
+    hcl_check(hcl_comm_release(dev, buffer_id, 1));
   });
 }
 
