@@ -92,6 +92,7 @@ class HostContext:
 
     def __init__(self, cuda_ordinals: Optional[Sequence[int]] = None,
                  scheduler: Optional[SchedulerOptions] = None):
+        """HostContext::init (proj/src/runtime.cpp:317-374): CUDA devices instead of a cluster file."""
         L = N.lib()
         self._L = L
         ords = list(cuda_ordinals or [])
@@ -114,6 +115,7 @@ class HostContext:
 
     # -- devices ---------------------------------------------------------
     def get_device_ids(self) -> list[int]:
+        """proj/src/runtime.cpp:378-383."""
         ids = (C.c_int * 64)()
         n = C.c_int()
         check(self._L.hcl_ctx_get_device_ids(self._ctx, ids, 64, C.byref(n)))
@@ -121,26 +123,31 @@ class HostContext:
 
     # -- objects ---------------------------------------------------------
     def create_queue(self, global_device_id: int, user_id: str = "default", shared: bool = True) -> Handle:
+        """proj/src/runtime.cpp:385-399."""
         q = C.c_uint64()
         check(self._L.hcl_ctx_create_queue(self._ctx, global_device_id, user_id.encode(), int(shared), C.byref(q)))
         return Handle(HandleKind.queue, q.value)
 
     def create_buffer(self, size: int) -> Handle:
+        """proj/src/runtime.cpp:401-406 (lazy: placed on first use)."""
         b = C.c_uint64()
         check(self._L.hcl_ctx_create_buffer(self._ctx, size, C.byref(b)))
         return Handle(HandleKind.buffer, b.value)
 
     def create_program(self, bundle: str) -> Handle:
+        """proj/src/runtime.cpp:408-417 (query_registry of a bundle)."""
         p = C.c_uint64()
         check(self._L.hcl_ctx_create_program(self._ctx, bundle.encode(), C.byref(p)))
         return Handle(HandleKind.program, p.value)
 
     def create_kernel(self, program: Handle, kernel_name: str) -> Handle:
+        """proj/src/runtime.cpp:419-435 (name error 10 for unknown kernels)."""
         k = C.c_uint64()
         check(self._L.hcl_ctx_create_kernel(self._ctx, program.id, kernel_name.encode(), C.byref(k)))
         return Handle(HandleKind.kernel, k.value)
 
     def set_kernel_arg(self, kernel: Handle, index: int, value) -> None:
+        """proj/src/runtime.cpp:437-446 (int -> i64 scalar, Handle -> buffer)."""
         if isinstance(value, Handle):
             if value.kind != HandleKind.buffer:
                 raise HaoclError(16, "handle: argument is not a buffer handle")
@@ -151,8 +158,9 @@ class HostContext:
     # -- transfers -------------------------------------------------------
     def enqueue_write_buffer(self, queue: Handle, buffer: Handle, data, offset: int = 0,
                              blocking: bool = True) -> Handle:
-        """blocking=False queues the copy on the device's H2D stream (keep `data`
-        alive, ideally pinned, until finish(queue))."""
+        """proj/src/runtime.cpp:448-483 (size error 18 past the end). blocking=False
+        queues the copy on the device's H2D stream (keep `data` alive, ideally
+        pinned, until finish(queue))."""
         ptr, n, keep = _bytes_view(data)
         ev = C.c_uint64()
         fn = self._L.hcl_ctx_enqueue_write_buffer if blocking else self._L.hcl_ctx_enqueue_write_buffer_async
@@ -162,7 +170,7 @@ class HostContext:
 
     def enqueue_read_buffer(self, queue: Handle, buffer: Handle, offset: int = 0, length: Optional[int] = None,
                             out=None, blocking: bool = True) -> np.ndarray:
-        """blocking=False queues the copy on the D2H stream; `out` is valid after finish(queue)."""
+        """proj/src/runtime.cpp:485-514 (gathers the buffer's shards). blocking=False queues the copy on the D2H stream; `out` is valid after finish(queue)."""
         if length is None:
             length = self.buffer_size(buffer) - offset
         if out is None:
@@ -176,6 +184,7 @@ class HostContext:
 
     # -- launches --------------------------------------------------------
     def enqueue_ndrange_kernel(self, queue: Handle, kernel: Handle, global_size=(1, 1, 1), dims: int = 1) -> Handle:
+        """proj/src/runtime.cpp:516-540: the whole range on one queue."""
         g = (C.c_uint64 * 3)(*global_size)
         ev = C.c_uint64()
         check(self._L.hcl_ctx_enqueue_ndrange_kernel(self._ctx, queue.id, kernel.id, g, dims, C.byref(ev)))
@@ -184,7 +193,9 @@ class HostContext:
     def enqueue_ndrange_partitioned(self, kernel: Handle, global_size, dims: int, queues: Sequence[Handle],
                                     weights: Optional[Sequence[int]] = None,
                                     bounds: Optional[Sequence[int]] = None) -> Handle:
-        """Partitioned NDRange: split dim 0 of global_size over `queues` (by
+        """The bench layer's partitioning moved into the runtime (run_matmul /
+        run_spmv / run_knn, proj/src/bench.cpp:147-447; block_range 31-33).
+        Partitioned NDRange: split dim 0 of global_size over `queues` (by
         `weights`, or at explicit row `bounds`, e.g. nnz-balanced ranges)."""
         g = (C.c_uint64 * 3)(*global_size)
         qs = (C.c_uint64 * len(queues))(*[q.id for q in queues])
@@ -227,6 +238,9 @@ class HostContext:
 
     def partition_plan(self, kernel: Handle, global_size, queues: Sequence[Handle],
                        weights: Optional[Sequence[int]] = None) -> list[int]:
+        """Row boundaries a partitioned launch would use: split_ranges of the
+        weights (block_range for equal ones, proj/src/bench.cpp:31-33) or of the
+        scheduler's EMA rates (proj/src/scheduler.cpp:136-149)."""
         g = (C.c_uint64 * 3)(*global_size)
         qs = (C.c_uint64 * len(queues))(*[q.id for q in queues])
         w = (C.c_uint64 * len(queues))(*weights) if weights is not None else None
@@ -235,6 +249,7 @@ class HostContext:
         return list(out)
 
     def submit_task(self, task: KernelTask) -> tuple[int, Handle]:
+        """proj/src/runtime.cpp:542-594 (scheduler placement)."""
         n = len(task.args)
         isb = (C.c_uint8 * max(1, n))()
         vals = (C.c_int64 * max(1, n))()
@@ -251,15 +266,18 @@ class HostContext:
         return chosen.value, Handle(HandleKind.event, ev.value)
 
     def finish(self, queue: Handle) -> TimingFragment:
+        """proj/src/runtime.cpp:606-616 (CUDA-event compute time, EMA profiles)."""
         t, c, m = C.c_double(), C.c_double(), C.c_double()
         check(self._L.hcl_ctx_finish(self._ctx, queue.id, C.byref(t), C.byref(c), C.byref(m)))
         return TimingFragment(t.value, c.value, m.value)
 
     def release(self, handle: Handle) -> None:
+        """proj/src/runtime.cpp:618-666."""
         check(self._L.hcl_ctx_release(self._ctx, int(handle.kind), handle.id))
 
     # -- observability ---------------------------------------------------
     def breakdown(self) -> TimingBreakdown:
+        """proj/src/runtime.cpp:668-671."""
         out = (C.c_double * 5)()
         check(self._L.hcl_ctx_breakdown(self._ctx, out))
         return TimingBreakdown(*list(out))
