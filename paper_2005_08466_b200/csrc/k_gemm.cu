@@ -9,7 +9,8 @@
 // Kernel structure (one persistent CTA pair per two SMs, cta_group::2):
 //   warp 4      TMA producer: A tile 128 x 128B and B tile (256/CG) x 128B per
 //               stage into a 6-deep SWIZZLE_128B smem ring (mbarrier full/empty)
-//   warp 5      MMA issuer (leader CTA, one thread): tcgen05.mma 256x256xK into
+//   warp 5      MMA issuer (leader CTA; the whole warp runs the loop and
+//               elect.sync picks the issuing lane): tcgen05.mma 256x256xK into
 //               one of two TMEM accumulators (2 x 256 columns = all 512)
 //   warps 0-3   epilogue: tcgen05.ld 32x32b -> registers -> bf16/fp32 -> HBM,
 //               overlapped with the next tile's main loop (TMEM double buffer)
@@ -649,9 +650,20 @@ uint64_t launch_gemm_f32(LaunchCtx& c) {
   if (rows == 0) return 0;
   const float* bp = reinterpret_cast<const float*>(B.ptr);
   const int64_t r = static_cast<int64_t>(rows);
-  if (ceil_div(r, 128) * ceil_div(n, 128) >= 2 * static_cast<int64_t>(c.sm_count)) {
+  // tile: 128x128 (8x8 per thread) when the grid fills the GPU twice, else
+  // 128x64 (8x4) when it still covers most SMs (C1 1024^2: 128 blocks),
+  // else 64x64 (4x4); HCL_SIMT_TILE=0|1|2 forces one (every shape computes
+  // each output with the same FMA chain, so results are identical)
+  const int64_t sms = c.sm_count;
+  int tile = env_int("HCL_SIMT_TILE", -1);
+  if (tile < 0 || tile > 2)
+    tile = ceil_div(r, 128) * ceil_div(n, 128) >= 2 * sms ? 0 : ceil_div(r, 128) * ceil_div(n, 64) >= (3 * sms) / 4 ? 1 : 2;
+  if (tile == 0) {
     dim3 grid(static_cast<unsigned>(ceil_div(n, 128)), static_cast<unsigned>(ceil_div(r, 128)));
     gemm_f32_simt_kernel<128, 128, 8, 8><<<grid, 256, 0, c.stream>>>(a, bp, cp, r, n, k);
+  } else if (tile == 1) {
+    dim3 grid(static_cast<unsigned>(ceil_div(n, 64)), static_cast<unsigned>(ceil_div(r, 128)));
+    gemm_f32_simt_kernel<128, 64, 8, 4><<<grid, 256, 0, c.stream>>>(a, bp, cp, r, n, k);
   } else {
     dim3 grid(static_cast<unsigned>(ceil_div(n, 64)), static_cast<unsigned>(ceil_div(r, 64)));
     gemm_f32_simt_kernel<64, 64, 4, 4><<<grid, 256, 0, c.stream>>>(a, bp, cp, r, n, k);

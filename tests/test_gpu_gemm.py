@@ -174,3 +174,14 @@ def test_gemm_argument_errors(ctx, queues):
     with pytest.raises(HaoclError) as e:  # B has the wrong size
         gemm(ctx, queues, "gemm_bf16", O.gen_bf16(64 * 64, 1), O.gen_bf16(64 * 32, 2), 64, 64, 64)
     assert e.value.name == "argument"
+
+
+def test_gemm_f32_simt_tiles_bit_identical(ctx, queues, monkeypatch):
+    m, n, k = 700, 520, 300
+    a = O.gen_doubles(m * k, 42).astype(np.float32)
+    b = O.gen_doubles(k * n, 43).astype(np.float32)
+    outs = []
+    for t in "012":
+        monkeypatch.setenv("HCL_SIMT_TILE", t)
+        outs.append(gemm(ctx, queues, "gemm_f32", a, b, m, k, n).tobytes())
+    assert outs[0] == outs[1] == outs[2]
