@@ -537,14 +537,14 @@ uint64_t launch_gemm_f32x3(LaunchCtx& c) {
 
 // ---------------------------------------------------------------------------
 // fp32 SIMT GEMM (exact fp32 products, FFMA accumulate in ascending k): BMxBN
-// tile per 256-thread block, TMxTN outputs per thread, K panels of 8
+// tile per 256-thread block, TMxTN outputs per thread, K panels of 16
 // double-buffered in shared memory with register-staged prefetch (the next
 // panel's global loads are in flight while the current one is multiplied).
 // A is stored k-major in smem with a 4-float pad so the transposing stores are
 // conflict-free. 128x128 tiles (8x8 per thread) for large problems, 64x64
 // (4x4) when the 128 grid would leave SMs idle (C1: 1024^3 = 64 vs 256 tiles).
 
-constexpr int SG_K = 8;
+constexpr int SG_K = 16;  // k per smem panel: 16 keeps a panel of FFMA work ahead of the global-load latency
 
 template <int BM, int BN, int TM, int TN>
 __global__ void __launch_bounds__(256) gemm_f32_simt_kernel(const float* __restrict__ A, const float* __restrict__ B,
