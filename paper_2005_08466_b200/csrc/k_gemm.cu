@@ -277,6 +277,19 @@ EncodeTiledFn encode_fn() {
   return fn;
 }
 
+// A (rows x cols) -> At (cols x pitch), pitch >= rows
+__global__ void transpose_pitched_kernel(const float* __restrict__ in, float* __restrict__ out, int64_t rows,
+                                         int64_t cols, int64_t pitch) {
+  __shared__ float tile[32][33];
+  const int64_t c = blockIdx.x * 32 + threadIdx.x, r0 = blockIdx.y * 32;
+  for (int i = threadIdx.y; i < 32; i += 8)
+    if (r0 + i < rows && c < cols) tile[i][threadIdx.x] = in[(r0 + i) * cols + c];
+  __syncthreads();
+  const int64_t oc = r0 + threadIdx.x, or0 = blockIdx.x * 32;
+  for (int i = threadIdx.y; i < 32; i += 8)
+    if (or0 + i < cols && oc < rows) out[(or0 + i) * pitch + oc] = tile[threadIdx.x][i];
+}
+
 int env_int(const char* name, int dflt) {
   const char* v = std::getenv(name);
   return v ? std::atoi(v) : dflt;
@@ -631,6 +644,123 @@ __global__ void __launch_bounds__(256) gemm_f32_simt_kernel(const float* __restr
   }
 }
 
+// Multistage variant (N % 4 == 0): A is first transposed to At (K x rows,
+// pitch padded to 4 floats) so both operand tiles are contiguous k-rows, copied
+// with 16-byte cp.async (zero-filled past the edges) into a 3-stage ring; the
+// register tile and the FFMA chain per output are those of gemm_f32_simt_kernel
+// (k ascending), so results are bit-identical to it.
+constexpr int MS_K = 16, MS_STAGES = 3;
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(ptx::smem_u32(smem)), "l"(gmem),
+               "r"(src_bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+template <int BM, int BN, int TM, int TN>
+__global__ void __launch_bounds__(256) gemm_f32_ms_kernel(const float* __restrict__ At, int64_t lda,
+                                                          const float* __restrict__ B, float* __restrict__ Cc,
+                                                          int64_t M, int64_t N, int64_t K) {
+  static_assert((BM / TM) * (BN / TN) == 256, "256 threads");
+  constexpr int RSTEP = BM * 4 / TM, CSTEP = BN * 4 / TN;
+  constexpr int A_CH = MS_K * BM / 4, B_CH = MS_K * BN / 4;  // 16-byte chunks per stage
+  extern __shared__ __align__(16) float ms_smem[];
+  float* sa = ms_smem;                          // [stage][MS_K][BM]
+  float* sb = ms_smem + MS_STAGES * MS_K * BM;  // [stage][MS_K][BN]
+  const int tid = threadIdx.x;
+  const int tx = tid % (BN / TN), ty = tid / (BN / TN);
+  const int64_t row0 = blockIdx.y * (int64_t)BM, col0 = blockIdx.x * (int64_t)BN;
+  const int nk = static_cast<int>((K + MS_K - 1) / MS_K);
+  auto issue = [&](int stage, int kt) {
+    const int64_t k0 = static_cast<int64_t>(kt) * MS_K;
+    for (int ch = tid; ch < A_CH; ch += 256) {
+      const int kk = ch / (BM / 4), m4 = (ch % (BM / 4)) * 4;
+      const int64_t gk = k0 + kk, gm = row0 + m4;
+      const int64_t rem = M - gm;
+      const int bytes = gk < K ? static_cast<int>(rem >= 4 ? 4 : (rem > 0 ? rem : 0)) * 4 : 0;
+      cp_async16(sa + (stage * MS_K + kk) * BM + m4, bytes ? At + gk * lda + gm : At, bytes);
+    }
+    for (int ch = tid; ch < B_CH; ch += 256) {
+      const int kk = ch / (BN / 4), n4 = (ch % (BN / 4)) * 4;
+      const int64_t gk = k0 + kk, gn = col0 + n4;
+      const int64_t rem = N - gn;
+      const int bytes = gk < K ? static_cast<int>(rem >= 4 ? 4 : (rem > 0 ? rem : 0)) * 4 : 0;
+      cp_async16(sb + (stage * MS_K + kk) * BN + n4, bytes ? B + gk * N + gn : B, bytes);
+    }
+  };
+  float acc[TM][TN];
+#pragma unroll
+  for (int i = 0; i < TM; ++i)
+#pragma unroll
+    for (int j = 0; j < TN; ++j) acc[i][j] = 0.f;
+#pragma unroll
+  for (int st = 0; st < MS_STAGES - 1; ++st) {
+    if (st < nk) issue(st, st);
+    cp_async_commit();
+  }
+  for (int kt = 0; kt < nk; ++kt) {
+    cp_async_wait<MS_STAGES - 2>();
+    __syncthreads();
+    const int nxt = kt + MS_STAGES - 1;
+    if (nxt < nk) issue(nxt % MS_STAGES, nxt);
+    cp_async_commit();
+    const float* a = sa + (kt % MS_STAGES) * MS_K * BM;
+    const float* b = sb + (kt % MS_STAGES) * MS_K * BN;
+#pragma unroll
+    for (int kk = 0; kk < MS_K; ++kk) {
+      float av[TM], bv[TN];
+#pragma unroll
+      for (int g = 0; g < TM / 4; ++g) {
+        const float4 v = *reinterpret_cast<const float4*>(a + kk * BM + g * RSTEP + ty * 4);
+        av[g * 4] = v.x; av[g * 4 + 1] = v.y; av[g * 4 + 2] = v.z; av[g * 4 + 3] = v.w;
+      }
+#pragma unroll
+      for (int g = 0; g < TN / 4; ++g) {
+        const float4 v = *reinterpret_cast<const float4*>(b + kk * BN + g * CSTEP + tx * 4);
+        bv[g * 4] = v.x; bv[g * 4 + 1] = v.y; bv[g * 4 + 2] = v.z; bv[g * 4 + 3] = v.w;
+      }
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+    }
+  }
+  cp_async_wait<0>();
+#pragma unroll
+  for (int i = 0; i < TM; ++i) {
+    const int64_t r = row0 + (i / 4) * RSTEP + ty * 4 + i % 4;
+    if (r >= M) continue;
+#pragma unroll
+    for (int g = 0; g < TN / 4; ++g) {
+      const int64_t cc = col0 + g * CSTEP + tx * 4;
+      if (cc + 3 < N) {
+        *reinterpret_cast<float4*>(Cc + r * N + cc) =
+            make_float4(acc[i][g * 4], acc[i][g * 4 + 1], acc[i][g * 4 + 2], acc[i][g * 4 + 3]);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (cc + j < N) Cc[r * N + cc + j] = acc[i][g * 4 + j];
+      }
+    }
+  }
+}
+
+template <int BM, int BN, int TM, int TN>
+void run_gemm_f32_ms(const float* At, int64_t lda, const float* b, float* cp, int64_t r, int64_t n, int64_t k,
+                     cudaStream_t stream) {
+  const size_t smem = static_cast<size_t>(MS_STAGES) * MS_K * (BM + BN) * 4;
+  auto kern = gemm_f32_ms_kernel<BM, BN, TM, TN>;
+  HCL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  dim3 grid(static_cast<unsigned>(ceil_div(n, BN)), static_cast<unsigned>(ceil_div(r, BM)));
+  kern<<<grid, 256, smem, stream>>>(At, lda, b, cp, r, n, k);
+  HCL_LAUNCHED();
+}
+
 uint64_t launch_gemm_f32(LaunchCtx& c) {
   int64_t m = scalar_arg(c, 3, "gemm_f32 M");
   int64_t k = scalar_arg(c, 4, "gemm_f32 K");
@@ -658,6 +788,18 @@ uint64_t launch_gemm_f32(LaunchCtx& c) {
   int tile = env_int("HCL_SIMT_TILE", -1);
   if (tile < 0 || tile > 2)
     tile = ceil_div(r, 128) * ceil_div(n, 128) >= 2 * sms ? 0 : ceil_div(r, 128) * ceil_div(n, 64) >= (3 * sms) / 4 ? 1 : 2;
+  if (n % 4 == 0 && env_int("HCL_SIMT_MS", 1)) {
+    // multistage path: At = A^T (K x rows, pitch rounded up to 4 floats)
+    const int64_t lda = (r + 3) / 4 * 4;
+    float* at = static_cast<float*>(c.scratch(c.dev, static_cast<size_t>(k * lda) * 4));
+    dim3 tg(static_cast<unsigned>(ceil_div(k, 32)), static_cast<unsigned>(ceil_div(r, 32)));
+    transpose_pitched_kernel<<<tg, dim3(32, 8), 0, c.stream>>>(a, at, r, k, lda);
+    HCL_LAUNCHED();
+    if (tile == 0) run_gemm_f32_ms<128, 128, 8, 8>(at, lda, bp, cp, r, n, k, c.stream);
+    else if (tile == 1) run_gemm_f32_ms<128, 64, 8, 4>(at, lda, bp, cp, r, n, k, c.stream);
+    else run_gemm_f32_ms<64, 64, 4, 4>(at, lda, bp, cp, r, n, k, c.stream);
+    return 2ull * rows * static_cast<uint64_t>(n) * static_cast<uint64_t>(k);
+  }
   if (tile == 0) {
     dim3 grid(static_cast<unsigned>(ceil_div(n, 128)), static_cast<unsigned>(ceil_div(r, 128)));
     gemm_f32_simt_kernel<128, 128, 8, 8><<<grid, 256, 0, c.stream>>>(a, bp, cp, r, n, k);

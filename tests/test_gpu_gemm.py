@@ -177,11 +177,15 @@ def test_gemm_argument_errors(ctx, queues):
 
 
 def test_gemm_f32_simt_tiles_bit_identical(ctx, queues, monkeypatch):
-    m, n, k = 700, 520, 300
+    m, n, k = 701, 520, 301  # ragged M and K; N % 4 == 0 takes the multistage path
     a = O.gen_doubles(m * k, 42).astype(np.float32)
     b = O.gen_doubles(k * n, 43).astype(np.float32)
     outs = []
-    for t in "012":
-        monkeypatch.setenv("HCL_SIMT_TILE", t)
-        outs.append(gemm(ctx, queues, "gemm_f32", a, b, m, k, n).tobytes())
-    assert outs[0] == outs[1] == outs[2]
+    for ms in "01":  # register-prefetch kernel and the cp.async multistage kernel
+        monkeypatch.setenv("HCL_SIMT_MS", ms)
+        for t in "012":
+            monkeypatch.setenv("HCL_SIMT_TILE", t)
+            outs.append(gemm(ctx, queues, "gemm_f32", a, b, m, k, n).tobytes())
+    assert all(o == outs[0] for o in outs)
+    a64, b64 = a.astype(np.float64).reshape(m, k), b.astype(np.float64).reshape(k, n)
+    assert normwise_err(np.frombuffer(outs[0], np.float32).reshape(m, n), a64, b64) <= 2.0**-20
