@@ -781,13 +781,13 @@ uint64_t launch_gemm_f32(LaunchCtx& c) {
   const float* bp = reinterpret_cast<const float*>(B.ptr);
   const int64_t r = static_cast<int64_t>(rows);
   // tile: 128x128 (8x8 per thread) when the grid fills the GPU twice, else
-  // 128x64 (8x4) when it still covers most SMs (C1 1024^2: 128 blocks),
-  // else 64x64 (4x4); HCL_SIMT_TILE=0|1|2 forces one (every shape computes
-  // each output with the same FMA chain, so results are identical)
+  // 64x64 (4x4); 128x64 (8x4) is available; HCL_SIMT_TILE=0|1|2 forces one
+  // (every shape computes each output with the same FMA chain, so results
+  // are identical)
   const int64_t sms = c.sm_count;
   int tile = env_int("HCL_SIMT_TILE", -1);
   if (tile < 0 || tile > 2)
-    tile = ceil_div(r, 128) * ceil_div(n, 128) >= 2 * sms ? 0 : ceil_div(r, 128) * ceil_div(n, 64) >= (3 * sms) / 4 ? 1 : 2;
+    tile = ceil_div(r, 128) * ceil_div(n, 128) >= 2 * sms ? 0 : 2;  // 1024^3: 64x64 measured best (24.5 TF)
   if (n % 4 == 0 && env_int("HCL_SIMT_MS", 1)) {
     // multistage path: At = A^T (K x rows, pitch rounded up to 4 floats)
     const int64_t lda = (r + 3) / 4 * 4;
