@@ -339,7 +339,9 @@ void run_gemm(const void* A, const void* B, void* Cp, int64_t M, int64_t N, int6
   // per launch: the attribute is per device context and launches may target several GPUs
   HCL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(C::kSmem)));
   const int64_t tiles = ceil_div(M, kBM * CG) * ceil_div(N, BN);
-  const int64_t clusters = std::min<int64_t>(tiles, sm_count / CG);
+  // HCL_GEMM_PERSIST=0: one cluster per tile, launched in raster order, so the
+  // hardware keeps the running tiles a compact window (experiment)
+  const int64_t clusters = env_int("HCL_GEMM_PERSIST", 1) ? std::min<int64_t>(tiles, sm_count / CG) : tiles;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(static_cast<unsigned>(clusters * CG));
   cfg.blockDim = dim3(kThreads);
