@@ -41,10 +41,13 @@ constexpr int kGroupM = 8;          // default tile raster group (HCL_GEMM_GROUP
 // Tile shapes: (CG, BN) = (2, 256) for large problems (256x256 UMMA per CTA
 // pair); (2, 128) and (1, 64) when the 256-wide grid would leave SMs idle
 // (C1: a 1024^2 output is only 16 pair tiles at 256x256, 128 CTA tiles at 128x64).
-template <int CG, bool TF32, int BN>
+// ONE: one tile per CTA pair -- a single TMEM accumulator and ~100 KB of
+// stages, so two pairs share each SM pair and one's epilogue overlaps the
+// other's main loop (the persistent schedule double-buffers TMEM instead).
+template <int CG, bool TF32, int BN, bool ONE = false>
 struct Cfg {
   static constexpr int kBN = BN;                 // tile N (UMMA_N)
-  static constexpr int kTmemCols = 2 * BN;       // 2 accumulators x BN fp32 columns
+  static constexpr int kTmemCols = ONE ? BN : 2 * BN;  // accumulators x BN fp32 columns
   static constexpr int kElem = TF32 ? 4 : 2;
   static constexpr int kBK = 128 / kElem;        // one 128-byte swizzle row of K
   static constexpr int kUK = 32 / kElem;         // K per tcgen05.mma
@@ -52,7 +55,8 @@ struct Cfg {
   static constexpr int kABytes = kBM * 128;
   static constexpr int kBBytes = kBNLocal * 128;
   static constexpr int kStage = kABytes + kBBytes;
-  static constexpr int kStages = (200 * 1024) / kStage < 8 ? (200 * 1024) / kStage : 8;
+  static constexpr int kBudget = ONE ? 100 * 1024 : 200 * 1024;
+  static constexpr int kStages = kBudget / kStage < 8 ? kBudget / kStage : 8;
   static constexpr int kMNAtom = 128 / kElem;    // MN elements per swizzle atom row
   static constexpr size_t kSmem = static_cast<size_t>(kStages) * kStage + 1024 + 256;
 };
@@ -70,11 +74,11 @@ struct TileMap {
   }
 };
 
-template <int CG, bool TF32, bool BMN, bool OUTF32, int BN>
+template <int CG, bool TF32, bool BMN, bool OUTF32, int BN, bool ONE>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    void* __restrict__ Cout, int M, int N, int K, int64_t ldc, int group_m) {
-  using C = Cfg<CG, TF32, BN>;
+  using C = Cfg<CG, TF32, BN, ONE>;
   constexpr int kBN = C::kBN;
   static_assert(!BMN || C::kBNLocal % C::kMNAtom == 0, "MN-major B needs whole 128-byte atoms per CTA");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -327,16 +331,16 @@ CUtensorMap make_tmap(const void* base, bool f32, uint64_t inner, uint64_t outer
   return m;
 }
 
-template <int CG, bool TF32, bool BMN, bool OUTF32, int BN = 256>
+template <int CG, bool TF32, bool BMN, bool OUTF32, int BN = 256, bool ONE = false>
 void run_gemm(const void* A, const void* B, void* Cp, int64_t M, int64_t N, int64_t K, int64_t ldc,
               int sm_count, cudaStream_t stream, int group_m) {
-  using C = Cfg<CG, TF32, BN>;
+  using C = Cfg<CG, TF32, BN, ONE>;
   const uint64_t es = C::kElem;
   const CUtensorMapL2promotion promo = l2_promotion();
   CUtensorMap ta = make_tmap(A, TF32, K, M, K * es, C::kBK, kBM, promo);
   CUtensorMap tb = BMN ? make_tmap(B, TF32, N, K, N * es, C::kMNAtom, C::kBK, promo)
                        : make_tmap(B, TF32, K, N, K * es, C::kBK, C::kBNLocal, promo);
-  auto kern = gemm_tc_kernel<CG, TF32, BMN, OUTF32, BN>;
+  auto kern = gemm_tc_kernel<CG, TF32, BMN, OUTF32, BN, ONE>;
   // per launch: the attribute is per device context and launches may target several GPUs
   HCL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(C::kSmem)));
   const int64_t tiles = ceil_div(M, kBM * CG) * ceil_div(N, BN);
@@ -347,7 +351,7 @@ void run_gemm(const void* A, const void* B, void* Cp, int64_t M, int64_t N, int6
   // and 1.23 GHz for persistent CTA pairs walking strided tile lists, whose
   // drift spreads the live panels over several waves (profiles/r01_gemm_sweep.txt).
   // HCL_GEMM_PERSIST=1 selects the persistent schedule.
-  const int64_t clusters = env_int("HCL_GEMM_PERSIST", 0) ? std::min<int64_t>(tiles, sm_count / CG) : tiles;
+  const int64_t clusters = !ONE && env_int("HCL_GEMM_PERSIST", 0) ? std::min<int64_t>(tiles, sm_count / CG) : tiles;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(static_cast<unsigned>(clusters * CG));
   cfg.blockDim = dim3(kThreads);
@@ -401,7 +405,12 @@ void dispatch_shape(int shape, const void* a, const void* b, void* cp, int64_t M
     case 1: run_gemm<1, TF32, BMN, OUTF32, 256>(a, b, cp, M, n, k, n, c.sm_count, c.stream, group_m); break;
     case 2: run_gemm<2, TF32, BMN, OUTF32, 128>(a, b, cp, M, n, k, n, c.sm_count, c.stream, group_m); break;
     case 3: run_gemm<1, TF32, BMN, OUTF32, 64>(a, b, cp, M, n, k, n, c.sm_count, c.stream, group_m); break;
-    default: run_gemm<2, TF32, BMN, OUTF32, 256>(a, b, cp, M, n, k, n, c.sm_count, c.stream, group_m); break;
+    default:
+      if (env_int("HCL_GEMM_PERSIST", 0) || env_int("HCL_GEMM_ONE", 1) == 0)
+        run_gemm<2, TF32, BMN, OUTF32, 256>(a, b, cp, M, n, k, n, c.sm_count, c.stream, group_m);
+      else
+        run_gemm<2, TF32, BMN, OUTF32, 256, true>(a, b, cp, M, n, k, n, c.sm_count, c.stream, group_m);
+      break;
   }
 }
 

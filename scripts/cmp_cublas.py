@@ -29,8 +29,9 @@ for _ in range(3):
     ctx.enqueue_ndrange_kernel(q, k, (S, S, 1), 2)
 torch.cuda.synchronize()
 ctx.finish(q)
-def ours(persist):
+def ours(persist, one=1):
     os.environ["HCL_GEMM_PERSIST"] = str(persist)
+    os.environ["HCL_GEMM_ONE"] = str(one)
     t = time.perf_counter()
     for _ in range(REPS):
         ctx.enqueue_ndrange_kernel(q, k, (S, S, 1), 2)
@@ -49,7 +50,8 @@ def cublas():
 
 f = 2 * S**3
 for rnd in range(int(os.environ.get("CMP_ROUNDS", "3"))):
-    order = [("cuBLAS", cublas), ("persistent", lambda: ours(1)), ("one tile per cluster", lambda: ours(0))]
+    order = [("cuBLAS", cublas), ("persistent", lambda: ours(1)), ("one tile, 2 acc", lambda: ours(0, 0)),
+             ("one tile, 2 pairs/SM", lambda: ours(0, 1))]
     if rnd % 2:
         order.reverse()
     res = {name: fn() for name, fn in order}
