@@ -88,6 +88,7 @@ struct LaunchCtx {
   int dev = 0;
   cudaStream_t stream = nullptr;
   int sm_count = 148;
+  bool sm_budgeted = false;  // sm_count is a budget below the GPU's SM count (hcl_device_set_sm_budget)
   const LaunchArg* args = nullptr;
   uint32_t nargs = 0;
   uint64_t goff[3] = {0, 0, 0};

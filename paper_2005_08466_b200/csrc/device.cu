@@ -590,6 +590,7 @@ int hcl_launch(int dev, const char* kernel, const hcl_arg* args, uint32_t nargs,
     c.dev = dev;
     c.stream = d.stream;
     c.sm_count = d.sm_count;
+    c.sm_budgeted = d.sm_count < d.sm_physical;
     c.args = la.data();
     c.nargs = nargs;
     c.dims = dims ? dims : 1;

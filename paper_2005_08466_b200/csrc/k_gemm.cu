@@ -333,7 +333,7 @@ CUtensorMap make_tmap(const void* base, bool f32, uint64_t inner, uint64_t outer
 
 template <int CG, bool TF32, bool BMN, bool OUTF32, int BN = 256, bool ONE = false>
 void run_gemm(const void* A, const void* B, void* Cp, int64_t M, int64_t N, int64_t K, int64_t ldc,
-              int sm_count, cudaStream_t stream, int group_m) {
+              int sm_count, cudaStream_t stream, int group_m, bool persistent) {
   using C = Cfg<CG, TF32, BN, ONE>;
   const uint64_t es = C::kElem;
   const CUtensorMapL2promotion promo = l2_promotion();
@@ -350,8 +350,9 @@ void run_gemm(const void* A, const void* B, void* Cp, int64_t M, int64_t N, int6
   // 9.8 GB DRAM reads per launch and 1.40 GHz under the power cap, vs 18.4 GB
   // and 1.23 GHz for persistent CTA pairs walking strided tile lists, whose
   // drift spreads the live panels over several waves (profiles/r01_gemm_sweep.txt).
-  // HCL_GEMM_PERSIST=1 selects the persistent schedule.
-  const int64_t clusters = !ONE && env_int("HCL_GEMM_PERSIST", 0) ? std::min<int64_t>(tiles, sm_count / CG) : tiles;
+  // The persistent schedule (HCL_GEMM_PERSIST=1) is also what an SM budget
+  // needs: its grid is sized to the budget (emulated heterogeneous devices).
+  const int64_t clusters = !ONE && persistent ? std::min<int64_t>(tiles, sm_count / CG) : tiles;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(static_cast<unsigned>(clusters * CG));
   cfg.blockDim = dim3(kThreads);
@@ -401,15 +402,16 @@ int pick_shape(int64_t M, int64_t N, int sm_count) {
 template <bool TF32, bool BMN, bool OUTF32>
 void dispatch_shape(int shape, const void* a, const void* b, void* cp, int64_t M, int64_t n, int64_t k,
                     const LaunchCtx& c, int group_m) {
+  const bool persist = c.sm_budgeted || env_int("HCL_GEMM_PERSIST", 0) != 0;
   switch (shape) {
-    case 1: run_gemm<1, TF32, BMN, OUTF32, 256>(a, b, cp, M, n, k, n, c.sm_count, c.stream, group_m); break;
-    case 2: run_gemm<2, TF32, BMN, OUTF32, 128>(a, b, cp, M, n, k, n, c.sm_count, c.stream, group_m); break;
-    case 3: run_gemm<1, TF32, BMN, OUTF32, 64>(a, b, cp, M, n, k, n, c.sm_count, c.stream, group_m); break;
+    case 1: run_gemm<1, TF32, BMN, OUTF32, 256>(a, b, cp, M, n, k, n, c.sm_count, c.stream, group_m, persist); break;
+    case 2: run_gemm<2, TF32, BMN, OUTF32, 128>(a, b, cp, M, n, k, n, c.sm_count, c.stream, group_m, persist); break;
+    case 3: run_gemm<1, TF32, BMN, OUTF32, 64>(a, b, cp, M, n, k, n, c.sm_count, c.stream, group_m, persist); break;
     default:
-      if (env_int("HCL_GEMM_PERSIST", 0) || env_int("HCL_GEMM_ONE", 1) == 0)
-        run_gemm<2, TF32, BMN, OUTF32, 256>(a, b, cp, M, n, k, n, c.sm_count, c.stream, group_m);
+      if (persist || env_int("HCL_GEMM_ONE", 1) == 0)
+        run_gemm<2, TF32, BMN, OUTF32, 256>(a, b, cp, M, n, k, n, c.sm_count, c.stream, group_m, persist);
       else
-        run_gemm<2, TF32, BMN, OUTF32, 256, true>(a, b, cp, M, n, k, n, c.sm_count, c.stream, group_m);
+        run_gemm<2, TF32, BMN, OUTF32, 256, true>(a, b, cp, M, n, k, n, c.sm_count, c.stream, group_m, false);
       break;
   }
 }
