@@ -459,6 +459,19 @@ class PageRankW(Workload):
                 ctx.set_kernel_arg(self.k_step[i], j, a)
         for j, a in enumerate([self.b_deg, self.b_dsum, self.v]):
             ctx.set_kernel_arg(self.k_dang, j + 1, a)
+        # implicit values (default): pagerank_prep folds val = 1/outdeg into xs, the
+        # step gathers xs (bit-identical products, no 1 GB value stream per iteration)
+        self.implicit = os.environ.get("BENCH_PR_IMPLICIT", "1") == "1"
+        if self.implicit:
+            self.b_xs = mk(self.v * 4)
+            self.k_prep = ctx.create_kernel(prog, "pagerank_prep")
+            self.k_stepi = [ctx.create_kernel(prog, "pagerank_step_implicit") for _ in range(2)]
+            for i in range(2):
+                for j, a in enumerate([self.b_rp, self.b_col, self.b_u, self.b_l, self.b_xs, self.b_dsum,
+                                       self.b_x[1 - i], self.v, p0, len(units), n_long, wn]):
+                    ctx.set_kernel_arg(self.k_stepi[i], j, a)
+            for j, a in enumerate([self.b_deg, self.b_dsum, self.b_xs, self.v]):
+                ctx.set_kernel_arg(self.k_prep, j + 1, a)
         if d.world > 1:
             uid = d.bcast_bytes(HostContext.nccl_unique_id() if d.rank == 0 else None)
             ctx.init_collectives(q, d.rank, d.world, uid)
@@ -480,12 +493,17 @@ class PageRankW(Workload):
         self.cur = 0
 
     def spmv(self):
-        self.ctx.enqueue_ndrange_range(self.q, self.k_step[self.cur], (self.v, 1, 1), 1, self.lo, self.rows)
+        k = self.k_stepi[self.cur] if self.implicit else self.k_step[self.cur]
+        self.ctx.enqueue_ndrange_range(self.q, k, (self.v, 1, 1), 1, self.lo, self.rows)
 
     def step(self):
         ctx, q = self.ctx, self.q
-        ctx.set_kernel_arg(self.k_dang, 0, self.b_x[self.cur])
-        ctx.enqueue_ndrange_kernel(q, self.k_dang)
+        if self.implicit:
+            ctx.set_kernel_arg(self.k_prep, 0, self.b_x[self.cur])
+            ctx.enqueue_ndrange_kernel(q, self.k_prep)
+        else:
+            ctx.set_kernel_arg(self.k_dang, 0, self.b_x[self.cur])
+            ctx.enqueue_ndrange_kernel(q, self.k_dang)
         self.spmv()
         if self.dist.world > 1:
             ctx.enqueue_allgather(q, self.b_x[1 - self.cur], self.byte_bounds)
@@ -495,7 +513,9 @@ class PageRankW(Workload):
         return self.spmv
 
     def dominant_work(self):
-        return self.nnz_local * 8.0 + (self.rows + 1) * 4 + self.rows * 4 * 2
+        # bytes the kernel must move: col (+ val unless implicit), row_ptr, x and y
+        per_nnz = 4.0 if self.implicit else 8.0
+        return self.nnz_local * per_nnz + (self.rows + 1) * 4 + self.rows * 4 * 2
 
     def e2e_step(self):
         # one iteration with the rank vector from host and the rank's slice back
@@ -516,6 +536,9 @@ class PageRankW(Workload):
     def config(self):
         return {"workload": f"PageRank iteration (C3): R-MAT scale {self.scale}, {self.e} edges, int32/fp32 pull CSR, "
                             f"nnz-balanced rows over {self.dist.world} rank(s), rank allgather",
+                "values": "implicit: val = 1/outdeg(src) folded into xs by pagerank_prep (bit-identical products); "
+                          "bytes are counted per the CSR definition (nnz*8 + ...)" if self.implicit
+                else "explicit fp32 value stream",
                 "vertex_ids": "out-degree ordered (hcl_pagerank_relabel; per-row sums unchanged)" if self.relabel
                 else "R-MAT ids", "warp_nnz": self.wn,
                 "algorithmic_bytes_per_iteration": self.work_per_step(), "rank_sum_err": self.check,

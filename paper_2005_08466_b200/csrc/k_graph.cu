@@ -106,24 +106,35 @@ __device__ __forceinline__ Update pr_update(const unsigned long long* dsum, floa
 }
 
 // lane-strided partial sums over [p, e) then the butterfly (all lanes hold the total)
+// IMP: the values are implicit -- x holds xs = val(src) * x(src) (pagerank_prep),
+// so a product is one gather; the same rounded product as val[p] * x[col[p]].
+template <bool IMP>
+__device__ __forceinline__ float product(const float* __restrict__ valp, const float* __restrict__ x, int q, int c) {
+  if constexpr (IMP)
+    return ld_x(x + c);
+  else
+    return __fmul_rn(ld_stream(valp + q), ld_x(x + c));
+}
+
+template <bool IMP>
 __device__ __forceinline__ float warp_row_sum(const int* __restrict__ colp, const float* __restrict__ valp,
                                               const float* __restrict__ x, int p, int e, int lane) {
   float v = 0.f;
   int q = p + lane;
   for (; q + 96 < e; q += 128) {
     int i0 = ld_stream(colp + q), i1 = ld_stream(colp + q + 32), i2 = ld_stream(colp + q + 64), i3 = ld_stream(colp + q + 96);
-    float v0 = ld_stream(valp + q), v1 = ld_stream(valp + q + 32), v2 = ld_stream(valp + q + 64), v3 = ld_stream(valp + q + 96);
-    float x0 = ld_x(x + i0), x1 = ld_x(x + i1), x2 = ld_x(x + i2), x3 = ld_x(x + i3);
-    v = __fadd_rn(v, __fmul_rn(v0, x0));
-    v = __fadd_rn(v, __fmul_rn(v1, x1));
-    v = __fadd_rn(v, __fmul_rn(v2, x2));
-    v = __fadd_rn(v, __fmul_rn(v3, x3));
+    const float p0 = product<IMP>(valp, x, q, i0), p1 = product<IMP>(valp, x, q + 32, i1);
+    const float p2 = product<IMP>(valp, x, q + 64, i2), p3 = product<IMP>(valp, x, q + 96, i3);
+    v = __fadd_rn(v, p0);
+    v = __fadd_rn(v, p1);
+    v = __fadd_rn(v, p2);
+    v = __fadd_rn(v, p3);
   }
-  for (; q < e; q += 32) v = __fadd_rn(v, __fmul_rn(ld_stream(valp + q), ld_x(x + ld_stream(colp + q))));
+  for (; q < e; q += 32) v = __fadd_rn(v, product<IMP>(valp, x, q, ld_stream(colp + q)));
   return butterfly(v);
 }
 
-template <bool UPDATE>
+template <bool UPDATE, bool IMP>
 __global__ void __launch_bounds__(PR_T) pr_units_kernel(const int* __restrict__ row_ptr, const int* __restrict__ col,
                                                         const float* __restrict__ val, int64_t nnz_off,
                                                         const int4* __restrict__ units, int n_units,
@@ -155,7 +166,7 @@ __global__ void __launch_bounds__(PR_T) pr_units_kernel(const int* __restrict__ 
     const int4 U = units[u];
     if (U.y - U.x == 1 && __ldg(row_ptr + U.x + 1) - __ldg(row_ptr + U.x) > warp_nnz) {
       // one chunk of a long row
-      const float v = warp_row_sum(colp, valp, x, U.z, U.w, lane);
+      const float v = warp_row_sum<IMP>(colp, valp, x, U.z, U.w, lane);
       if (lane == 0) chunk_tot[u] = v;
       continue;
     }
@@ -165,15 +176,14 @@ __global__ void __launch_bounds__(PR_T) pr_units_kernel(const int* __restrict__ 
     for (; i + 96 < n; i += 128) {
       int c0 = ld_stream(colp + p0 + i), c1 = ld_stream(colp + p0 + i + 32), c2 = ld_stream(colp + p0 + i + 64),
           c3 = ld_stream(colp + p0 + i + 96);
-      float v0 = ld_stream(valp + p0 + i), v1 = ld_stream(valp + p0 + i + 32), v2 = ld_stream(valp + p0 + i + 64),
-            v3 = ld_stream(valp + p0 + i + 96);
-      float x0 = ld_x(x + c0), x1 = ld_x(x + c1), x2 = ld_x(x + c2), x3 = ld_x(x + c3);
-      prod[i] = __fmul_rn(v0, x0);
-      prod[i + 32] = __fmul_rn(v1, x1);
-      prod[i + 64] = __fmul_rn(v2, x2);
-      prod[i + 96] = __fmul_rn(v3, x3);
+      const float q0 = product<IMP>(valp, x, p0 + i, c0), q1 = product<IMP>(valp, x, p0 + i + 32, c1);
+      const float q2 = product<IMP>(valp, x, p0 + i + 64, c2), q3 = product<IMP>(valp, x, p0 + i + 96, c3);
+      prod[i] = q0;
+      prod[i + 32] = q1;
+      prod[i + 64] = q2;
+      prod[i + 96] = q3;
     }
-    for (; i < n; i += 32) prod[i] = __fmul_rn(ld_stream(valp + p0 + i), ld_x(x + ld_stream(colp + p0 + i)));
+    for (; i < n; i += 32) prod[i] = product<IMP>(valp, x, p0 + i, ld_stream(colp + p0 + i));
     __syncwarp();
     for (int rb = r0; rb < r1; rb += 32) {
       const int r = rb + lane;
@@ -216,10 +226,12 @@ __global__ void pr_fixup_kernel(const int* __restrict__ long_rows, int n_long, c
 }
 
 // args: row_ptr col val units long_rows x [dsum] y | V nnz_off n_units n_long warp_nnz
-template <bool UPDATE>
+// (IMP: no val argument; x is xs from pagerank_prep)
+template <bool UPDATE, bool IMP = false>
 uint64_t launch_pr(LaunchCtx& c) {
-  const char* what = UPDATE ? "pagerank_step" : "pagerank_spmv";
-  const uint32_t iy = UPDATE ? 7 : 6, s0 = iy + 1;
+  const char* what = IMP ? "pagerank_step_implicit" : UPDATE ? "pagerank_step" : "pagerank_spmv";
+  constexpr uint32_t o = IMP ? 1 : 0;  // argument shift when there is no val buffer
+  const uint32_t iy = (UPDATE ? 7 : 6) - o, s0 = iy + 1;
   const int64_t v = scalar_arg(c, s0, what), nnz_off = scalar_arg(c, s0 + 1, what);
   const int64_t n_units = scalar_arg(c, s0 + 2, what), n_long = scalar_arg(c, s0 + 3, what);
   const int64_t warp_nnz = scalar_arg(c, s0 + 4, what);
@@ -228,10 +240,10 @@ uint64_t launch_pr(LaunchCtx& c) {
     fail(ErrorCode::argument, std::string(what) + ": warp_nnz must be in [1, 4096]");
   const BufView& R = buffer_arg(c, 0, what);
   const BufView& Cb = buffer_arg(c, 1, what);
-  const BufView& Vb = buffer_arg(c, 2, what);
-  const BufView& U = buffer_arg(c, 3, what);
-  const BufView& L = buffer_arg(c, 4, what);
-  const BufView& X = buffer_arg(c, 5, what);
+  const BufView& Vb = IMP ? Cb : buffer_arg(c, 2, what);
+  const BufView& U = buffer_arg(c, 3 - o, what);
+  const BufView& L = buffer_arg(c, 4 - o, what);
+  const BufView& X = buffer_arg(c, 5 - o, what);
   if (R.first_byte != 0 || R.bytes != static_cast<uint64_t>(v + 1) * 4)
     fail(ErrorCode::argument, std::string(what) + ": row_ptr must hold V+1 int32");
   if (U.bytes != static_cast<uint64_t>(n_units) * 16 || L.bytes < static_cast<uint64_t>(n_long) * 12)
@@ -242,7 +254,7 @@ uint64_t launch_pr(LaunchCtx& c) {
     fail(ErrorCode::argument, std::string(what) + ": x must hold V floats");
   const unsigned long long* dsum = nullptr;
   if (UPDATE) {
-    const BufView& D = buffer_arg(c, 6, what);
+    const BufView& D = buffer_arg(c, 6 - o, what);
     if (D.bytes != 8) fail(ErrorCode::argument, std::string(what) + ": dangling sum is one uint64");
     dsum = reinterpret_cast<const unsigned long long*>(D.ptr);
   }
@@ -261,13 +273,13 @@ uint64_t launch_pr(LaunchCtx& c) {
   float* chunk_tot = static_cast<float*>(c.scratch(c.dev, static_cast<size_t>(n_units) * 4));
   const float base = static_cast<float>((1.0 - 0.85) / v), damp = 0.85f, inv_v = static_cast<float>(1.0 / v);
   const size_t smem = static_cast<size_t>(warp_nnz) * 4 * PR_WARPS;
-  auto kern = pr_units_kernel<UPDATE>;
+  auto kern = pr_units_kernel<UPDATE, IMP>;
   HCL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   int per_sm = 0;
   HCL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, PR_T, smem));
   const int grid = std::max(1, per_sm) * c.sm_count;
   kern<<<grid, PR_T, smem, c.stream>>>(row_ptr, reinterpret_cast<const int*>(Cb.ptr),
-                                       reinterpret_cast<const float*>(Vb.ptr), nnz_off,
+                                       IMP ? nullptr : reinterpret_cast<const float*>(Vb.ptr), nnz_off,
                                        reinterpret_cast<const int4*>(U.ptr), static_cast<int>(n_units),
                                        reinterpret_cast<const float*>(X.ptr), dsum, y, static_cast<int>(lo),
                                        static_cast<int>(lo + rows), base, damp, inv_v, static_cast<int>(warp_nnz),
@@ -280,6 +292,47 @@ uint64_t launch_pr(LaunchCtx& c) {
     HCL_LAUNCHED();
   }
   return 2ull * static_cast<uint64_t>(rp[1] - rp[0]);
+}
+
+// xs[i] = val(i) * x[i], val(i) = 1/outdeg(i) rounded to fp32 exactly as the CSR
+// builder stores it (hcl_pagerank_csr), 0 for dangling vertices; fused with the
+// dangling sum. With xs the SpMV's products are single gathers, bit-identical
+// to val[p] * x[col[p]], and the 4-byte-per-edge value stream disappears.
+__global__ void __launch_bounds__(256) pr_prep_kernel(const float* __restrict__ x, const int* __restrict__ outdeg,
+                                                      int64_t v, float* __restrict__ xs,
+                                                      unsigned long long* __restrict__ out) {
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  unsigned long long s = 0;
+  for (int64_t i = tid; i < v; i += stride) {
+    const int d = __ldcs(outdeg + i);
+    const float xi = __ldcs(x + i);
+    if (d == 0) s += static_cast<unsigned long long>(__float2ll_rz(__fmul_rn(xi, 0x1p56f)));
+    xs[i] = d ? __fmul_rn(__fdiv_rn(1.0f, static_cast<float>(d)), xi) : 0.f;
+  }
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0 && s) atomicAdd(out, s);
+}
+
+// pagerank_prep(x, outdeg, dsum, xs, V)
+uint64_t launch_pr_prep(LaunchCtx& c) {
+  int64_t v = scalar_arg(c, 4, "pagerank_prep V");
+  const BufView& X = buffer_arg(c, 0, "pagerank_prep x");
+  const BufView& O = buffer_arg(c, 1, "pagerank_prep outdeg");
+  const BufView& D = buffer_arg(c, 2, "pagerank_prep dsum");
+  const BufView& XS = buffer_arg(c, 3, "pagerank_prep xs");
+  if (X.first_byte != 0 || X.bytes != static_cast<uint64_t>(v) * 4 || O.first_byte != 0 ||
+      O.bytes != static_cast<uint64_t>(v) * 4 || D.bytes != 8 || XS.first_byte != 0 ||
+      XS.bytes != static_cast<uint64_t>(v) * 4)
+    fail(ErrorCode::argument, "pagerank_prep: x, outdeg, xs must hold V elements, dsum one uint64");
+  HCL_CUDA(cudaMemsetAsync(D.ptr, 0, 8, c.stream));
+  int grid = static_cast<int>(std::min<uint64_t>(c.sm_count * 8, ceil_div(v, 256)));
+  pr_prep_kernel<<<grid, 256, 0, c.stream>>>(reinterpret_cast<const float*>(X.ptr),
+                                             reinterpret_cast<const int*>(O.ptr), v,
+                                             reinterpret_cast<float*>(XS.ptr),
+                                             reinterpret_cast<unsigned long long*>(D.ptr));
+  HCL_LAUNCHED();
+  return static_cast<uint64_t>(v);
 }
 
 // pagerank_dangling(x, outdeg, dsum, V): dsum = sum over outdeg==0 of x in 2^-56 fixed point
@@ -301,6 +354,7 @@ uint64_t launch_pr_dangling(LaunchCtx& c) {
 }
 
 uint64_t rows_pr(const int64_t* s, uint32_t n) { return static_cast<uint64_t>(s[n == 13 ? 8 : 7]); }
+uint64_t rows_pr_imp(const int64_t* s, uint32_t) { return static_cast<uint64_t>(s[7]); }
 
 }  // namespace
 
@@ -314,6 +368,11 @@ void register_graph(std::vector<KernelDef>& r) {
   r.push_back({"b200", "pagerank_step", {I, I, I, I, I, I, I, O, S, S, S, S, S},
                {P, P, P, P, P, P, P, X, N, N, N, N, N}, launch_pr<true>, nullptr, rows_pr});
   r.push_back({"b200", "pagerank_dangling", {I, I, O, S}, {P, P, P, N}, launch_pr_dangling, nullptr, nullptr});
+  // implicit values (val = 1/outdeg(src)): pagerank_prep(x, outdeg, dsum, xs, V), then
+  // pagerank_step_implicit(row_ptr col units long_rows xs dsum x' | V nnz_off n_units n_long warp_nnz)
+  r.push_back({"b200", "pagerank_prep", {I, I, O, O, S}, {P, P, P, P, N}, launch_pr_prep, nullptr, nullptr});
+  r.push_back({"b200", "pagerank_step_implicit", {I, I, I, I, I, I, O, S, S, S, S, S},
+               {P, P, P, P, P, P, X, N, N, N, N, N}, launch_pr<true, true>, nullptr, rows_pr_imp});
 }
 
 }  // namespace hcl

@@ -24,10 +24,13 @@ DEFAULT_WARP_NNZ = 64  # measured best at scale 24 (profiles/r01_pagerank_experi
 class PageRank:
     def __init__(self, ctx: HostContext, queues: Sequence[Handle], row_ptr: np.ndarray, col_idx: np.ndarray,
                  val: np.ndarray, outdeg: np.ndarray, max_nnz: int = DEFAULT_WARP_NNZ,
-                 weights: Optional[Sequence[int]] = None, relabel: bool = False):
+                 weights: Optional[Sequence[int]] = None, relabel: bool = False, implicit: bool = True):
         """relabel: store the graph degree-ordered (hcl_pagerank_relabel) so the
         hot ranks form a dense prefix of x; per-row sums are unchanged, and
-        ranks()/spmv() map results back to the caller's vertex ids."""
+        ranks()/spmv() map results back to the caller's vertex ids. implicit: the
+        iteration uses pagerank_prep + pagerank_step_implicit (values folded into
+        xs = x/outdeg, bit-identical products, no value stream)."""
+        self.implicit = implicit
         self.ctx, self.queues = ctx, list(queues)
         self.perm = None
         if relabel:
@@ -59,6 +62,16 @@ class PageRank:
                 ctx.set_kernel_arg(kk, j, a)
         for j, a in enumerate([self.b_deg, self.b_dsum, self.v]):
             ctx.set_kernel_arg(self.k_dang, j + 1, a)
+        if implicit:
+            self.b_xs = mk(self.v * 4)
+            self.k_prep = ctx.create_kernel(prog, "pagerank_prep")
+            self.k_stepi = [ctx.create_kernel(prog, "pagerank_step_implicit") for _ in range(2)]
+            for i, kk in enumerate(self.k_stepi):  # reads xs (from x[i]), writes x[1-i]
+                for j, a in enumerate([self.b_rp, self.b_col, self.b_units, self.b_long, self.b_xs, self.b_dsum,
+                                       self.b_x[1 - i]] + self.tail):
+                    ctx.set_kernel_arg(kk, j, a)
+            for j, a in enumerate([self.b_deg, self.b_dsum, self.b_xs, self.v]):
+                ctx.set_kernel_arg(self.k_prep, j + 1, a)
         self.cur = 0
 
     def reset(self) -> None:
@@ -69,10 +82,15 @@ class PageRank:
     def iterate(self, iterations: int) -> None:
         ctx = self.ctx
         for _ in range(iterations):
-            ctx.set_kernel_arg(self.k_dang, 0, self.b_x[self.cur])
-            ctx.enqueue_ndrange_kernel(self.queues[0], self.k_dang)
-            ctx.enqueue_ndrange_partitioned(self.k_step[self.cur], (self.v, 1, 1), 1, self.queues,
-                                            bounds=self.bounds)
+            if self.implicit:
+                ctx.set_kernel_arg(self.k_prep, 0, self.b_x[self.cur])
+                ctx.enqueue_ndrange_kernel(self.queues[0], self.k_prep)
+                step = self.k_stepi[self.cur]
+            else:
+                ctx.set_kernel_arg(self.k_dang, 0, self.b_x[self.cur])
+                ctx.enqueue_ndrange_kernel(self.queues[0], self.k_dang)
+                step = self.k_step[self.cur]
+            ctx.enqueue_ndrange_partitioned(step, (self.v, 1, 1), 1, self.queues, bounds=self.bounds)
             self.cur = 1 - self.cur
 
     def finish(self) -> None:
@@ -108,3 +126,5 @@ class PageRank:
     def close(self) -> None:
         for b in (self.b_rp, self.b_units, self.b_long, self.b_col, self.b_val, self.b_deg, self.b_dsum, *self.b_x):
             self.ctx.release(b)
+        if self.implicit:
+            self.ctx.release(self.b_xs)

@@ -146,3 +146,21 @@ def test_pagerank_relabelled(ctx, queues, graph, P, weights):
     got = pr.ranks().tobytes()
     pr.close()
     assert got == O.pagerank(rp, ci, val, deg, 20, b200_order=True).tobytes()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("P", [1, 3])
+def test_implicit_values_bit_identical(ctx, queues, graph, P):
+    """pagerank_prep + pagerank_step_implicit (values folded into xs = x/outdeg)
+    equals the explicit-value step and the restated-order oracle bit-for-bit."""
+    from paper_2005_08466_b200.pagerank import PageRank
+
+    rp, ci, val, deg = graph
+    out = []
+    for implicit in (False, True):
+        pr = PageRank(ctx, queues[:P], *graph, max_nnz=64, implicit=implicit)
+        pr.reset()
+        pr.iterate(20)
+        out.append(pr.ranks().tobytes())
+        pr.close()
+    assert out[0] == out[1] == O.pagerank(rp, ci, val, deg, 20, b200_order=True).tobytes()
