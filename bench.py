@@ -513,9 +513,9 @@ class PageRankW(Workload):
         return self.spmv
 
     def dominant_work(self):
-        # bytes the kernel must move: col (+ val unless implicit), row_ptr, x and y
-        per_nnz = 4.0 if self.implicit else 8.0
-        return self.nnz_local * per_nnz + (self.rows + 1) * 4 + self.rows * 4 * 2
+        # SURVEY.md §8(d) algorithmic bytes of the CSR formulation (nnz*8 + (V+1)*4 + 2*V*4), also
+        # with implicit values (which move nnz*4 fewer bytes for the same work)
+        return self.nnz_local * 8.0 + (self.rows + 1) * 4 + self.rows * 4 * 2
 
     def e2e_step(self):
         # one iteration with the rank vector from host and the rank's slice back
