@@ -161,8 +161,6 @@ __device__ __forceinline__ void conv_epilogue_loop_tma(const ConvGeom& g, int H,
                                                        void* __restrict__ out, int epi_mode) {
   const int cluster = blockIdx.x / 2, nclusters = gridDim.x / 2;
   const int half = warp / 4;
-  const bool epi_hint = (epi_mode & 4) == 0;  // HCL_CONV_EPI=4: plain stores (no L2 evict_first hint)
-  epi_mode &= 3;
   int acc = 0;
   uint32_t acc_phase = 0;
   for (int t = cluster; t < g.tiles; t += nclusters) {
@@ -202,12 +200,7 @@ __device__ __forceinline__ void conv_epilogue_loop_tma(const ConvGeom& g, int H,
     __syncwarp();
     const int h = p / g.Wp, w = p - h * g.Wp;
     if (lane == 0) {
-      if (h < H) {
-        if (epi_hint)
-          ptx::tma_store_4d_hint(tmO, obuf, half * 64, w, h, n, ptx::policy_evict_first());
-        else
-          ptx::tma_store_4d(tmO, obuf, half * 64, w, h, n);
-      }
+      if (h < H) ptx::tma_store_4d(tmO, obuf, half * 64, w, h, n);
       ptx::bulk_commit();
     }
     // a group that wraps into the next image row: those lanes store their
