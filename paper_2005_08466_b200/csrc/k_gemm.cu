@@ -58,7 +58,11 @@ struct Cfg {
   static constexpr int kBudget = ONE ? 100 * 1024 : 200 * 1024;
   static constexpr int kStages = kBudget / kStage < 8 ? kBudget / kStage : 8;
   static constexpr int kMNAtom = 128 / kElem;    // MN elements per swizzle atom row
-  static constexpr size_t kSmem = static_cast<size_t>(kStages) * kStage + 1024 + 256;
+  // bf16 C through shared memory + TMA stores (ONE): 4 warps x 32 rows x 64 B
+  static constexpr bool kTmaC = ONE && !TF32;
+  static constexpr int kCStage = 32 * 64;
+  static constexpr size_t kCBytes = kTmaC ? 4 * kCStage : 0;
+  static constexpr size_t kSmem = static_cast<size_t>(kStages) * kStage + kCBytes + 1024 + 256;
 };
 
 struct TileMap {
@@ -77,13 +81,15 @@ struct TileMap {
 template <int CG, bool TF32, bool BMN, bool OUTF32, int BN, bool ONE>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                   void* __restrict__ Cout, int M, int N, int K, int64_t ldc, int group_m) {
+                   const __grid_constant__ CUtensorMap tmC, void* __restrict__ Cout, int M, int N, int K,
+                   int64_t ldc, int group_m) {
   using C = Cfg<CG, TF32, BN, ONE>;
   constexpr int kBN = C::kBN;
   static_assert(!BMN || C::kBNLocal % C::kMNAtom == 0, "MN-major B needs whole 128-byte atoms per CTA");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStage);
+  uint8_t* cstage = smem + C::kStages * C::kStage;  // 1024-aligned (stages are 16/32 KB)
+  uint64_t* full = reinterpret_cast<uint64_t*>(cstage + C::kCBytes);
   uint64_t* empty = full + C::kStages;
   uint64_t* tfull = empty + C::kStages;
   uint64_t* tempty = tfull + 2;
@@ -212,7 +218,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::tmem_ld_32x32b_x32(taddr, r);
         ptx::tmem_ld_wait();
         const int col0 = nt * kBN + chunk * 32;
-        if (!row_ok || col0 >= N) continue;
+        if constexpr (C::kTmaC && !OUTF32) {
+          if (col0 >= N) continue;  // warp-uniform; TMA clips rows >= M
+        } else {
+          if (!row_ok || col0 >= N) continue;
+        }
         if constexpr (OUTF32) {
           float* dst = reinterpret_cast<float*>(Cout) + row * ldc + col0;
           if (col0 + 32 <= N && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
@@ -223,6 +233,28 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int j = 0; j < 32; ++j)
               if (col0 + j < N) dst[j] = __uint_as_float(r[j]);
+          }
+        } else if constexpr (OUTF32 == false && Cfg<CG, TF32, BN, ONE>::kTmaC) {
+          // SWIZZLE_64B staging: row = lane, 16-byte chunk j at j ^ ((row >> 1) & 3);
+          // TMA clips rows >= M and columns >= N
+          uint32_t p[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            __nv_bfloat162 h = __floats2bfloat162_rn(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1]));
+            p[j] = *reinterpret_cast<uint32_t*>(&h);
+          }
+          uint8_t* buf = cstage + warp * C::kCStage;
+          if (lane == 0) ptx::bulk_wait_read0();  // the previous chunk's store has read the buffer
+          __syncwarp();
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            *reinterpret_cast<uint4*>(buf + lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4)) =
+                make_uint4(p[4 * j], p[4 * j + 1], p[4 * j + 2], p[4 * j + 3]);
+          ptx::fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            ptx::tma_store_2d(&tmC, buf, col0, static_cast<int>(row - lane));
+            ptx::bulk_commit();
           }
         } else {
           __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(Cout) + row * ldc + col0;
@@ -253,6 +285,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   }
 
+  if constexpr (C::kTmaC)
+    if (warp < 4 && lane == 0) ptx::bulk_wait0();
   ptx::tc_fence_before();
   if constexpr (CG == 2) ptx::cluster_sync(); else __syncthreads();
   if (warp == 5) {
@@ -340,6 +374,17 @@ void run_gemm(const void* A, const void* B, void* Cp, int64_t M, int64_t N, int6
   CUtensorMap ta = make_tmap(A, TF32, K, M, K * es, C::kBK, kBM, promo);
   CUtensorMap tb = BMN ? make_tmap(B, TF32, N, K, N * es, C::kMNAtom, C::kBK, promo)
                        : make_tmap(B, TF32, K, N, K * es, C::kBK, C::kBNLocal, promo);
+  CUtensorMap tc{};
+  if constexpr (C::kTmaC && !OUTF32) {  // C (M x N bf16), box 32 x 32, SWIZZLE_64B
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(N), static_cast<cuuint64_t>(M)};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(ldc) * 2};
+    cuuint32_t box[2] = {32, 32};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = encode_fn()(&tc, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Cp, dims, strides, box, estr,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                             CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) fail(ErrorCode::argument, "cuTensorMapEncodeTiled (C) failed");
+  }
   auto kern = gemm_tc_kernel<CG, TF32, BMN, OUTF32, BN, ONE>;
   // per launch: the attribute is per device context and launches may target several GPUs
   HCL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(C::kSmem)));
@@ -365,7 +410,7 @@ void run_gemm(const void* A, const void* B, void* Cp, int64_t M, int64_t N, int6
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  HCL_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, Cp, static_cast<int>(M), static_cast<int>(N),
+  HCL_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, tc, Cp, static_cast<int>(M), static_cast<int>(N),
                               static_cast<int>(K), ldc, group_m));
   HCL_LAUNCHED();
 }
