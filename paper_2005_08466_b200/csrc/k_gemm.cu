@@ -82,7 +82,7 @@ template <int CG, bool TF32, bool BMN, bool OUTF32, int BN, bool ONE>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmC, void* __restrict__ Cout, int M, int N, int K,
-                   int64_t ldc, int group_m) {
+                   int64_t ldc, int group_m, int tma_c) {
   using C = Cfg<CG, TF32, BN, ONE>;
   constexpr int kBN = C::kBN;
   static_assert(!BMN || C::kBNLocal % C::kMNAtom == 0, "MN-major B needs whole 128-byte atoms per CTA");
@@ -218,7 +218,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::tmem_ld_32x32b_x32(taddr, r);
         ptx::tmem_ld_wait();
         const int col0 = nt * kBN + chunk * 32;
-        if constexpr (C::kTmaC && !OUTF32) {
+        if (C::kTmaC && !OUTF32 && tma_c) {
           if (col0 >= N) continue;  // warp-uniform; TMA clips rows >= M
         } else {
           if (!row_ok || col0 >= N) continue;
@@ -234,7 +234,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int j = 0; j < 32; ++j)
               if (col0 + j < N) dst[j] = __uint_as_float(r[j]);
           }
-        } else if constexpr (OUTF32 == false && Cfg<CG, TF32, BN, ONE>::kTmaC) {
+        } else if (Cfg<CG, TF32, BN, ONE>::kTmaC && tma_c) {
           // SWIZZLE_64B staging: row = lane, 16-byte chunk j at j ^ ((row >> 1) & 3);
           // TMA clips rows >= M and columns >= N
           uint32_t p[16];
@@ -286,7 +286,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 
   if constexpr (C::kTmaC)
-    if (warp < 4 && lane == 0) ptx::bulk_wait0();
+    if (tma_c && warp < 4 && lane == 0) ptx::bulk_wait0();
   ptx::tc_fence_before();
   if constexpr (CG == 2) ptx::cluster_sync(); else __syncthreads();
   if (warp == 5) {
@@ -375,7 +375,8 @@ void run_gemm(const void* A, const void* B, void* Cp, int64_t M, int64_t N, int6
   CUtensorMap tb = BMN ? make_tmap(B, TF32, N, K, N * es, C::kMNAtom, C::kBK, promo)
                        : make_tmap(B, TF32, K, N, K * es, C::kBK, C::kBNLocal, promo);
   CUtensorMap tc{};
-  if constexpr (C::kTmaC && !OUTF32) {  // C (M x N bf16), box 32 x 32, SWIZZLE_64B
+  const int tma_c = C::kTmaC && !OUTF32 && env_int("HCL_GEMM_TMAC", 1) ? 1 : 0;
+  if (tma_c) {  // C (M x N bf16), box 32 x 32, SWIZZLE_64B
     cuuint64_t dims[2] = {static_cast<cuuint64_t>(N), static_cast<cuuint64_t>(M)};
     cuuint64_t strides[1] = {static_cast<cuuint64_t>(ldc) * 2};
     cuuint32_t box[2] = {32, 32};
@@ -411,7 +412,7 @@ void run_gemm(const void* A, const void* B, void* Cp, int64_t M, int64_t N, int6
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   HCL_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, tc, Cp, static_cast<int>(M), static_cast<int>(N),
-                              static_cast<int>(K), ldc, group_m));
+                              static_cast<int>(K), ldc, group_m, tma_c));
   HCL_LAUNCHED();
 }
 

@@ -29,9 +29,10 @@ for _ in range(3):
     ctx.enqueue_ndrange_kernel(q, k, (S, S, 1), 2)
 torch.cuda.synchronize()
 ctx.finish(q)
-def ours(persist, one=1):
+def ours(persist, one=1, tmac=1):
     os.environ["HCL_GEMM_PERSIST"] = str(persist)
     os.environ["HCL_GEMM_ONE"] = str(one)
+    os.environ["HCL_GEMM_TMAC"] = str(tmac)
     t = time.perf_counter()
     for _ in range(REPS):
         ctx.enqueue_ndrange_kernel(q, k, (S, S, 1), 2)
@@ -49,9 +50,9 @@ def cublas():
 
 
 f = 2 * S**3
-for rnd in range(int(os.environ.get("CMP_ROUNDS", "3"))):
-    order = [("cuBLAS", cublas), ("persistent", lambda: ours(1)), ("one tile, 2 acc", lambda: ours(0, 0)),
-             ("one tile, 2 pairs/SM", lambda: ours(0, 1))]
+for rnd in range(int(os.environ.get("CMP_ROUNDS", "4"))):
+    order = [("cuBLAS", cublas), ("2 pairs/SM + TMA C", lambda: ours(0, 1, 1)),
+             ("2 pairs/SM, direct C", lambda: ours(0, 1, 0))]
     if rnd % 2:
         order.reverse()
     res = {name: fn() for name, fn in order}
