@@ -75,6 +75,9 @@ struct BufView {
   uint8_t* ptr = nullptr;
   uint64_t first_byte = 0;
   uint64_t bytes = 0;
+  // changes with every write through this library (copies, peer copies, kernel
+  // outputs); 0 for externally bound memory (never assumed unchanged)
+  uint64_t version = 0;
 };
 
 struct LaunchArg {

@@ -75,9 +75,12 @@ struct DevAlloc {
   uint64_t first_byte = 0;
   uint64_t bytes = 0;
   bool external = false;
+  uint64_t version = 0;  // bumped on every tracked write (BufView::version)
   Dep last_write;
   std::vector<Dep> reads;  // at most one per stream
 };
+
+std::atomic<uint64_t> g_write_version{0};
 
 struct Device {
   int ordinal = 0;
@@ -133,6 +136,7 @@ struct Device {
     cudaEvent_t e = sync_event();
     HCL_CUDA(cudaEventRecord(e, s));
     if (write) {
+      if (!a.external) a.version = g_write_version.fetch_add(1) + 1;
       drop(a.last_write);
       for (Dep& r : a.reads) drop(r);
       a.reads.clear();
@@ -583,7 +587,7 @@ int hcl_launch(int dev, const char* kernel, const hcl_arg* args, uint32_t nargs,
       la[i].id = args[i].buffer_id;
       if (!is_scalar) {
         DevAlloc& a = alloc_of(d, args[i].buffer_id, kernel);
-        la[i].buf = BufView{a.ptr, a.first_byte, a.bytes};
+        la[i].buf = BufView{a.ptr, a.first_byte, a.bytes, a.version};
       }
     }
     LaunchCtx c;

@@ -22,6 +22,10 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <tuple>
+#include <mutex>
+#include <map>
+#include <cstdlib>
 #include <string>
 
 #include "common.hpp"
@@ -225,6 +229,39 @@ __global__ void pr_fixup_kernel(const int* __restrict__ long_rows, int n_long, c
   pr_store<UPDATE>(y, row, lo, total, pr_update<UPDATE>(dsum, base, damp, inv_v));
 }
 
+// validated (row_ptr version, slice) -> row_ptr[lo], row_ptr[hi]
+struct PrCheckKey {
+  int dev;
+  const void* ptr;
+  uint64_t version, lo, rows, col_bytes;
+  int64_t nnz_off;
+  bool operator<(const PrCheckKey& o) const {
+    return std::tie(dev, ptr, version, lo, rows, col_bytes, nnz_off) <
+           std::tie(o.dev, o.ptr, o.version, o.lo, o.rows, o.col_bytes, o.nnz_off);
+  }
+};
+std::mutex g_pr_check_mu;
+std::map<PrCheckKey, std::pair<int, int>> g_pr_check;
+
+bool pr_check_cached(int dev, const BufView& R, uint64_t lo, uint64_t rows, uint64_t col_bytes, int64_t nnz_off,
+                     int (&rp)[2]) {
+  if (R.version == 0) return false;
+  std::lock_guard<std::mutex> lock(g_pr_check_mu);
+  auto it = g_pr_check.find({dev, R.ptr, R.version, lo, rows, col_bytes, nnz_off});
+  if (it == g_pr_check.end()) return false;
+  rp[0] = it->second.first;
+  rp[1] = it->second.second;
+  return true;
+}
+
+void pr_check_store(int dev, const BufView& R, uint64_t lo, uint64_t rows, uint64_t col_bytes, int64_t nnz_off,
+                    const int (&rp)[2]) {
+  if (R.version == 0) return;
+  std::lock_guard<std::mutex> lock(g_pr_check_mu);
+  if (g_pr_check.size() > 4096) g_pr_check.clear();
+  g_pr_check[{dev, R.ptr, R.version, lo, rows, col_bytes, nnz_off}] = {rp[0], rp[1]};
+}
+
 // args: row_ptr col val units long_rows x [dsum] y | V nnz_off n_units n_long warp_nnz
 // (IMP: no val argument; x is xs from pagerank_prep)
 template <bool UPDATE, bool IMP = false>
@@ -263,13 +300,18 @@ uint64_t launch_pr(LaunchCtx& c) {
   float* y = at_byte<float>(buffer_arg(c, iy, what), lo * 4, rows * 4, what);
   if (!rows || !n_units) return 0;
   const int* row_ptr = reinterpret_cast<const int*>(R.ptr);
-  // the non-zeros of [lo, hi) must be resident (two int32 reads)
+  // the non-zeros of [lo, hi) must be resident: two int32 reads of row_ptr with a
+  // host round trip -- done once per (row_ptr contents, slice) and cached by
+  // the buffer's write version, so iterations do not stall the stream
   int rp[2];
-  HCL_CUDA(cudaMemcpyAsync(&rp[0], row_ptr + lo, 4, cudaMemcpyDeviceToHost, c.stream));
-  HCL_CUDA(cudaMemcpyAsync(&rp[1], row_ptr + lo + rows, 4, cudaMemcpyDeviceToHost, c.stream));
-  HCL_CUDA(cudaStreamSynchronize(c.stream));
-  if (rp[0] < nnz_off || static_cast<uint64_t>(rp[1] - nnz_off) * 4 > Cb.bytes)
-    fail(ErrorCode::argument, std::string(what) + ": col_idx/values do not cover the rows' non-zeros");
+  if (!pr_check_cached(c.dev, R, lo, rows, Cb.bytes, nnz_off, rp)) {
+    HCL_CUDA(cudaMemcpyAsync(&rp[0], row_ptr + lo, 4, cudaMemcpyDeviceToHost, c.stream));
+    HCL_CUDA(cudaMemcpyAsync(&rp[1], row_ptr + lo + rows, 4, cudaMemcpyDeviceToHost, c.stream));
+    HCL_CUDA(cudaStreamSynchronize(c.stream));
+    if (rp[0] < nnz_off || static_cast<uint64_t>(rp[1] - nnz_off) * 4 > Cb.bytes)
+      fail(ErrorCode::argument, std::string(what) + ": col_idx/values do not cover the rows' non-zeros");
+    pr_check_store(c.dev, R, lo, rows, Cb.bytes, nnz_off, rp);
+  }
   float* chunk_tot = static_cast<float*>(c.scratch(c.dev, static_cast<size_t>(n_units) * 4));
   const float base = static_cast<float>((1.0 - 0.85) / v), damp = 0.85f, inv_v = static_cast<float>(1.0 / v);
   const size_t smem = static_cast<size_t>(warp_nnz) * 4 * PR_WARPS;

@@ -164,3 +164,38 @@ def test_implicit_values_bit_identical(ctx, queues, graph, P):
         out.append(pr.ranks().tobytes())
         pr.close()
     assert out[0] == out[1] == O.pagerank(rp, ci, val, deg, 20, b200_order=True).tobytes()
+
+
+@pytest.mark.gpu
+def test_step_rejects_short_col_buffer_and_revalidates(ctx, queues, graph):
+    """The row_ptr coverage check (cached per row_ptr write version) still
+    rejects a col/val slice that does not cover the rows, and a rewritten
+    row_ptr is validated again."""
+    from paper_2005_08466_b200 import HaoclError
+    from paper_2005_08466_b200.datagen import pagerank_units
+
+    rp, ci, val, deg = graph
+    v, nnz = len(rp) - 1, int(rp[-1])
+    units, long_rows, n_long = pagerank_units(rp, 64)
+    prog = ctx.create_program("b200")
+    k = ctx.create_kernel(prog, "pagerank_spmv")
+    q = queues[0]
+    mk = ctx.create_buffer
+    b_rp, b_u, b_l = mk(rp.nbytes), mk(units.nbytes), mk(long_rows.nbytes)
+    b_col, b_val = mk((nnz - 8) * 4), mk((nnz - 8) * 4)  # 8 non-zeros short
+    b_x, b_y = mk(v * 4), mk(v * 4)
+    for b, a in ((b_rp, rp), (b_u, units), (b_l, long_rows), (b_col, ci[: nnz - 8]), (b_val, val[: nnz - 8]),
+                 (b_x, np.ones(v, np.float32))):
+        ctx.enqueue_write_buffer(q, b, a)
+    for j, a in enumerate([b_rp, b_col, b_val, b_u, b_l, b_x, b_y, v, 0, len(units), n_long, 64]):
+        ctx.set_kernel_arg(k, j, a)
+    with pytest.raises(HaoclError) as e:
+        ctx.enqueue_ndrange_kernel(q, k, (v, 1, 1), 1)
+    assert e.value.name == "argument"
+    rp2 = rp.copy()
+    rp2[1:] = np.minimum(rp2[1:], nnz - 8)  # now consistent with the short slice
+    ctx.enqueue_write_buffer(q, b_rp, rp2)
+    ctx.enqueue_ndrange_kernel(q, k, (v, 1, 1), 1)  # revalidated against the new contents: accepted
+    ctx.finish(q)
+    for b in (b_rp, b_u, b_l, b_col, b_val, b_x, b_y, k, prog):
+        ctx.release(b)
