@@ -628,8 +628,8 @@ class KMeansW(Workload):
         return self._assign
 
     def dominant_work(self):
-        if self.tc:  # tensor work actually issued: 4 split products x D per (point, centroid)
-            return 2.0 * self.rows * self.K * 4 * self.D
+        if self.tc:  # tensor work actually issued: 3 split products x D per (point, centroid)
+            return 2.0 * self.rows * self.K * 3 * self.D
         return 3.0 * self.rows * self.K * self.D
 
     def e2e_step(self):
@@ -647,7 +647,7 @@ class KMeansW(Workload):
     def roofline(self, pk):
         if self.tc:
             return ("tensor", pk["bf16_tflops"], "TFLOP/s", 1e12,
-                    "MEASURED_PEAKS.json bf16_tflops; achieved = split-bf16 MMA flops issued (2 N K 4D)")
+                    "MEASURED_PEAKS.json bf16_tflops; achieved = split-bf16 MMA flops issued (2 N K 3D)")
         sm = pk.get("sm_max_mhz", 1965.0)
         # exact (non-FMA) fp32: one add or multiply per lane per clock (FADD2 issues
         # two lanes' worth but occupies the FP32 pipe twice, measured)

@@ -25,7 +25,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++20", "-Xcompiler", "-fPIC,-O3", "--expt-relaxed-constexpr",
-         "-I" + INCLUDE, "-I" + CSRC, "-Xptxas", "-warn-spills"]
+         "-I" + INCLUDE, "-I" + CSRC, "-Xptxas", "-warn-spills"] + os.environ.get("HCL_NVCC_EXTRA", "").split()
 
 
 def sources():

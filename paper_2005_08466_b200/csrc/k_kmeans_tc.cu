@@ -7,20 +7,24 @@
 //   1. score: s~_k = x . c_k by tcgen05 bf16 MMAs with fp32 accumulation, on
 //      split operands x = xh + xl (exact for points on a 2^-12 grid, else
 //      |x - xh - xl| <= 2^-16 |x|) and c = ch + cl (+ |residual| <= 2^-16 |c|):
-//      xh.ch + xl.ch + xh.cl + xl.cl as 8 MMAs of K=16 over the A row [xh|xl]
-//      and the B rows [ch|ch], [cl|cl]. t_k = |c_k|^2 - 2 s~_k ranks the
-//      centroids like |x - c_k|^2 (|x|^2 is common to the row).
+//      xh.ch + xl.ch + xh.cl as 6 MMAs of K=16 over the A row [xh|xl] and the
+//      B rows [ch|ch] (4) and [cl|..] (2; xl.cl, <= 2^-18 |x||c|, is dropped).
+//      t_k = |c_k|^2 - 2 s~_k ranks the centroids like |x - c_k|^2 (|x|^2 is
+//      common to the row).
 //   2. filter (epilogue, per point): every k with t_k <= min_j t_j + 2 eps is a
-//      candidate, eps = 2^-10 (|x| max|c| + |x|^2 + max|c|^2) -- at least 8x
-//      the bound on |t_k + |x|^2 - d_k| from the split, the tensor-core
-//      accumulation (<= 2^-13 |x||c|) and the fp32 evaluation of the exact
+//      candidate, eps = 2^-10 (|x| max|c| + |x|^2 + max|c|^2) -- at least 7x
+//      the bound on |t_k + |x|^2 - d_k| from the split and the dropped term,
+//      the tensor-core accumulation (<= 2^-13 |x||c|) and the fp32 evaluation of the exact
 //      distance d_k (<= 2^-19 (|x|^2 + |c|^2 + 2|x||c|)). The exact argmin is
 //      always a candidate, and so is every k tied with it.
 //   3. verify: the candidates' exact fp32 distances (the oracle's operation
-//      order) pick the result; a point whose candidate list overflows is
-//      scanned exactly over all K.
+//      order) pick the result; a point whose candidate list overflows (or
+//      with more than KT_QCAP survivors) is scanned exactly over all K by
+//      the whole verify warp.
 // On the C4 data (2^28 points, K=1024, 1024 Gaussian blobs) the filter keeps
-// 1.26 candidates per point on average (max 5; scripts in profiles/).
+// 1.26 candidates per point on average (max 5; scripts in profiles/); at 2^26
+// points 22% of the points keep several (0.48 exact checks per point) and
+// ~900 overflow (HCL_KM_DBG=16 prints these counts).
 //
 // Layout: points are stored twice -- fp32 (the exact pass and the update) and
 // split bf16 [xh(32) | xl(32)] (128 B per point = one SWIZZLE_128B row) with
@@ -28,17 +32,22 @@
 // are split into B1 = [ch|ch], B2 = [cl|cl] (bf16, K x 64) with |c|^2. One
 // persistent CTA pair (cta_group::2) per 2 SMs: the pair's B halves for all K
 // are resident (K/2 x 256 B per CTA, <= 128 KB), A tiles of 2 x 128 points
-// stream through 2 stages, and each tile runs K/256 chunks of N=256 MMAs into
-// two TMEM accumulators. Scan warps 0-3 take columns 0-127 of every chunk,
-// warps 4-7 columns 128-255, and hand each tile's candidate lists
-// (double-buffered in shared memory, mbarrier handshakes) to verify warps 8-11,
-// which filter, check exactly and store while the scan runs on.
+// stream through 2 stages, and each tile runs K/KT_CW chunks of N=KT_CW MMAs
+// into 512/KT_CW TMEM accumulators. KT_GROUPS groups of 4 scan warps each take
+// a KT_CW/KT_GROUPS column slice of every chunk (score, running minimum,
+// candidate mask; one list entry per batch of 32 columns with candidates)
+// and hand each tile's lists (double-buffered in shared memory, mbarrier
+// handshakes) to the verify warps -- two sets of 4, one per list buffer --
+// which filter, check exactly and store while the scan runs on. Measured on
+// 2^26 points, K=1024 (scripts/gpu_km4.sh): 4 groups x 4 slots, N=256: 20.2 ms;
+// 2 groups x 8 slots: 24.5 ms; N=128 chunks: 22.0 ms.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 #include <string>
 
@@ -54,35 +63,57 @@ CUtensorMap make_tmap_2d_bf16(const void* base, uint64_t inner, uint64_t outer, 
 namespace {
 
 constexpr int KT_D = 32;
-constexpr int KT_SCAN = 8;                   // scan warps 0-7 (TMEM scores -> candidate lists)
-constexpr int KT_VER = 4;                    // verify warps 8-11 (exact fp32 check, store)
-constexpr int KT_PROD = KT_SCAN + KT_VER;    // TMA producer warp 12, MMA warp 13
+#ifndef HCL_KT_GROUPS
+#define HCL_KT_GROUPS 4
+#endif
+#ifndef HCL_KT_CW
+#define HCL_KT_CW 256
+#endif
+constexpr int KT_CW = HCL_KT_CW;             // centroids per chunk (MMA N); TMEM holds 512 / KT_CW accumulators
+constexpr int KT_NACC = 512 / KT_CW;
+constexpr int KT_GROUPS = HCL_KT_GROUPS;     // scan groups: column slices of every chunk
+constexpr int KT_SCAN = 4 * KT_GROUPS;       // scan warps (TMEM scores -> candidate lists)
+constexpr int KT_VER = 8;                    // verify warps: two sets of 4, one per list buffer
+constexpr int KT_QCAP = 8;                   // queued exact checks per point (more: full scan)
+constexpr int KT_PROD = KT_SCAN + KT_VER;    // TMA producer warp, then the MMA warp
+constexpr int KT_GCOLS = KT_CW / KT_GROUPS;  // columns per group per chunk
+static_assert(KT_GCOLS >= 32 && KT_GCOLS % 32 == 0, "scan groups take whole 32-column batches");
 constexpr int KT_MMA = KT_PROD + 1;
 constexpr int KT_THREADS = (KT_MMA + 1) * 32;
 constexpr int KT_ROWS = 128;                 // points per CTA per tile
 constexpr int KT_A = KT_ROWS * 128;          // 16 KB A tile per CTA
 constexpr int KT_STAGES = 2;
-constexpr int KT_BH = 128 * 128;             // per CTA, chunk and split part: 128 centroids x 128 B
-constexpr int KT_LIST = 8;                   // candidate slots per point and scan group
+constexpr int KT_BH = (KT_CW / 2) * 128;     // per CTA, chunk and split part: KT_CW / 2 centroids x 128 B
+#ifndef HCL_KT_LIST
+#define HCL_KT_LIST (16 / HCL_KT_GROUPS)
+#endif
+constexpr int KT_LIST = HCL_KT_LIST;         // candidate slots per point and scan group
 constexpr int KT_KMAX = 1024;
-constexpr int KT_LBUF = 2 * KT_ROWS * KT_LIST;  // float2 slots of one tile's lists (both groups)
+static_assert((KT_KMAX / KT_CW) * (KT_GCOLS / 32) <= 16, "list keys carry a 4-bit batch index");
+constexpr int KT_LBUF = KT_GROUPS * KT_ROWS * KT_LIST;  // float2 slots of one tile's lists (all groups)
 
 struct KtLayout {
   size_t b, a, q, lists, xch, vq, bars, total;
   __host__ __device__ KtLayout(int K) {
-    const int nch = K / 256;
+    const int nch = K / KT_CW;
     b = 0;
     a = b + static_cast<size_t>(nch) * 2 * KT_BH;
     q = a + static_cast<size_t>(KT_STAGES) * KT_A;
     lists = q + static_cast<size_t>(K) * 4;
-    xch = lists + 2ull * KT_LBUF * 8;             // 2 buffers x (bmin, k) float2 slots
-    vq = xch + 2ull * 2 * KT_ROWS * 16;           // 2 buffers x 2 groups x (min, count, overflow)
-    bars = vq + static_cast<size_t>(KT_VER) * 32 * 2 * KT_LIST * 8;  // verify queues
+    xch = lists + 2ull * KT_LBUF * 8;             // 2 buffers x (t, k) float2 slots
+    vq = xch + 2ull * KT_GROUPS * KT_ROWS * 8 + 2ull * KT_ROWS * 4;  // 2 bufs x groups x (min, count|ovf) + 2 eps
+    bars = vq + static_cast<size_t>(KT_VER) * 32 * KT_QCAP * 8;  // verify queues
     total = bars + 16 * 8 + 16 + 1024;            // barriers, TMEM slot, alignment slack
   }
 };
 
-__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+// first centroid of a list entry's batch: batch index (low 4 key bits) within scan group g
+__device__ __forceinline__ int entry_k0(uint32_t key, int g) {
+  const int bi = static_cast<int>(key & 0xfu);
+  return (bi / (KT_GCOLS / 32)) * KT_CW + g * KT_GCOLS + (bi % (KT_GCOLS / 32)) * 32;
+}
+
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, %0;" ::"n"(KT_SCAN * 32) : "memory"); }
 
 // exact fp32 distance in the oracle's order (ho_kmeans_assign)
 __device__ __forceinline__ float exact_dist(const float (&x)[KT_D], const float* __restrict__ c) {
@@ -116,20 +147,21 @@ __global__ void __launch_bounds__(KT_THREADS, 1)
   uint8_t* sa = smem + L.a;
   float* sq = reinterpret_cast<float*>(smem + L.q);
   float2* lists = reinterpret_cast<float2*>(smem + L.lists);
-  float4* xch = reinterpret_cast<float4*>(smem + L.xch);
+  float2* xch = reinterpret_cast<float2*>(smem + L.xch);              // [buf][group][point] (min, count|ovf<<16)
+  float* xeps = reinterpret_cast<float*>(xch + 2 * KT_GROUPS * KT_ROWS);  // [buf][point] 2 eps
   int2* vq = reinterpret_cast<int2*>(smem + L.vq);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.bars);
   uint64_t* empty = full + KT_STAGES;
   uint64_t* tfull = empty + KT_STAGES;
-  uint64_t* tempty = tfull + 2;
-  uint64_t* lfull = tempty + 2;   // [2] scan -> verify: a tile's candidate lists are complete
+  uint64_t* tempty = tfull + KT_NACC;
+  uint64_t* lfull = tempty + KT_NACC;   // [2] scan -> verify: a tile's candidate lists are complete
   uint64_t* lempty = lfull + 2;   // [2] verify -> scan: list buffer free again
   uint64_t* bfull = lempty + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bfull + 1);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const uint32_t rank = ptx::cluster_ctarank();
-  const int nch = K / 256;
+  const int nch = K / KT_CW;
 
   if (warp == KT_PROD && lane == 0) {
     ptx::prefetch_tmap(&tmA);
@@ -139,11 +171,13 @@ __global__ void __launch_bounds__(KT_THREADS, 1)
       ptx::mbar_init(&full[s], 1);
       ptx::mbar_init(&empty[s], 1);
     }
-    for (int a = 0; a < 2; ++a) {
+    for (int a = 0; a < KT_NACC; ++a) {
       ptx::mbar_init(&tfull[a], 1);
       ptx::mbar_init(&tempty[a], 2 * KT_SCAN);  // every scan warp, both CTAs
+    }
+    for (int a = 0; a < 2; ++a) {
       ptx::mbar_init(&lfull[a], KT_SCAN);
-      ptx::mbar_init(&lempty[a], KT_VER);
+      ptx::mbar_init(&lempty[a], KT_VER / 2);
     }
     ptx::mbar_init(bfull, 1);
     ptx::fence_mbar_init();
@@ -158,11 +192,11 @@ __global__ void __launch_bounds__(KT_THREADS, 1)
 
   if (warp == KT_PROD) {
     if (lane == 0) {
-      // resident B: this CTA's 128-centroid half of every 256-centroid chunk
+      // resident B: this CTA's half of every chunk's centroids
       if (rank == 0) ptx::mbar_arrive_expect_tx(bfull, static_cast<uint32_t>(nch) * 2 * KT_BH * 2);
       const uint32_t bb = ptx::mapa(ptx::smem_u32(bfull), 0);
       for (int c = 0; c < nch; ++c) {
-        const int row = c * 256 + static_cast<int>(rank) * 128;
+        const int row = c * KT_CW + static_cast<int>(rank) * (KT_CW / 2);
         ptx::tma_load_2d_pair(sb + (2 * c) * KT_BH, &tmB1, bb, 0, row);
         ptx::tma_load_2d_pair(sb + (2 * c + 1) * KT_BH, &tmB2, bb, 0, row);
       }
@@ -179,34 +213,30 @@ __global__ void __launch_bounds__(KT_THREADS, 1)
     __syncwarp();
   } else if (warp == KT_MMA) {
     if (rank == 0) {
-      constexpr uint32_t idesc = ptx::umma_idesc(1, 0, 0, 2 * KT_ROWS, 256);
+      constexpr uint32_t idesc = ptx::umma_idesc(1, 0, 0, 2 * KT_ROWS, KT_CW);
       ptx::mbar_wait(bfull, 0);
       const uint64_t adesc0 = ptx::umma_desc_sw128(ptx::smem_u32(sa), 16, 1024);
       const uint64_t bdesc0 = ptx::umma_desc_sw128(ptx::smem_u32(sb), 16, 1024);
       int stage = 0;
-      uint32_t phase = 0, ph0 = 0, ph1 = 0;
+      uint32_t phase = 0, tph = 0;  // tph: phase bit per accumulator
+      int acc = 0;
       for (int t = cluster; t < tiles; t += nclusters) {
         ptx::mbar_wait(&full[stage], phase);
         ptx::tc_fence_after();
         const uint64_t adesc = adesc0 + static_cast<uint64_t>((stage * KT_A) >> 4);
         for (int c = 0; c < nch; ++c) {
-          const int acc = c & 1;
-          if (acc == 0) {
-            ptx::mbar_wait(&tempty[0], ph0 ^ 1);
-            ph0 ^= 1;
-          } else {
-            ptx::mbar_wait(&tempty[1], ph1 ^ 1);
-            ph1 ^= 1;
-          }
+          ptx::mbar_wait(&tempty[acc], ((tph >> acc) & 1) ^ 1);
+          tph ^= 1u << acc;
           ptx::tc_fence_after();
-          const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * 256);
+          const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * KT_CW);
           const uint64_t b1 = bdesc0 + static_cast<uint64_t>(((2 * c) * KT_BH) >> 4);
           const uint64_t b2 = bdesc0 + static_cast<uint64_t>(((2 * c + 1) * KT_BH) >> 4);
 #pragma unroll
           for (int i = 0; i < 4; ++i) ptx::mma_elect<2, false>(d_tmem, adesc + 2 * i, b1 + 2 * i, idesc, i != 0);
 #pragma unroll
-          for (int i = 0; i < 4; ++i) ptx::mma_elect<2, false>(d_tmem, adesc + 2 * i, b2 + 2 * i, idesc, 1);
+          for (int i = 0; i < 2; ++i) ptx::mma_elect<2, false>(d_tmem, adesc + 2 * i, b2 + 2 * i, idesc, 1);
           ptx::mma_commit_elect<2>(&tfull[acc]);
+          if (++acc == KT_NACC) acc = 0;
         }
         ptx::mma_commit_elect<2>(&empty[stage]);
         if (++stage == KT_STAGES) { stage = 0; phase ^= 1; }
@@ -214,15 +244,16 @@ __global__ void __launch_bounds__(KT_THREADS, 1)
     }
     __syncwarp();
   } else if (warp < KT_SCAN) {
-    // ---------------- scan: group g = column half g of every chunk ----------------
+    // ---------------- scan: group g = column slice g of every chunk ----------------
     const int g = warp / 4, quad = warp % 4;
     const int pl = quad * 32 + lane;  // point within the CTA tile = TMEM lane
     for (int i = threadIdx.x; i < K; i += KT_SCAN * 32) sq[i] = qg[i];
+    const uint32_t sq_s = ptx::smem_u32(sq);
     const float qmax = stats[0];
     const float cmax = sqrtf(qmax);
     epi_bar();
-    uint32_t ph0 = 0, ph1 = 0;
-    int it = 0;
+    uint32_t tph = 0;  // phase bit per accumulator
+    int acc = 0, it = 0;
     for (int t = cluster; t < tiles; t += nclusters, ++it) {
       const int buf = it & 1;
       const int row = t * 2 * KT_ROWS + static_cast<int>(rank) * KT_ROWS + pl;
@@ -234,36 +265,30 @@ __global__ void __launch_bounds__(KT_THREADS, 1)
       ptx::mbar_wait(&lempty[buf], ((it >> 1) & 1) ^ 1);  // the verify warps are done with this buffer
       float2* my = lists + buf * KT_LBUF + (g * KT_ROWS + pl) * KT_LIST;
       for (int c = 0; c < nch; ++c) {
-        const int acc = c & 1;
-        if (acc == 0) {
-          ptx::mbar_wait(&tfull[0], ph0);
-          ph0 ^= 1;
-        } else {
-          ptx::mbar_wait(&tfull[1], ph1);
-          ph1 ^= 1;
-        }
+        ptx::mbar_wait(&tfull[acc], (tph >> acc) & 1);
+        tph ^= 1u << acc;
         ptx::tc_fence_after();
         const uint32_t tbase = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) +
-                               static_cast<uint32_t>(acc * 256 + g * 128);
-        uint32_t r[2][32];
-        ptx::tmem_ld_32x32b_x32(tbase, r[0]);
-        ptx::tmem_ld_wait();
+                               static_cast<uint32_t>(acc * KT_CW + g * KT_GCOLS);
 #pragma unroll
-        for (int b = 0; b < 4; ++b) {
-          uint32_t (&cur)[32] = r[b & 1];
-          if (b < 3) {
-            ptx::tmem_ld_32x32b_x32(tbase + (b + 1) * 32, r[(b + 1) & 1]);  // next batch in flight
-          } else {  // our half of the accumulator drained: hand it back to the MMA warp
+        for (int b = 0; b < KT_GCOLS / 32; ++b) {
+          uint32_t cur[32];
+          ptx::tmem_ld_32x32b_x32(tbase + b * 32, cur);
+          ptx::tmem_ld_wait();
+          if (b == KT_GCOLS / 32 - 1) {  // our slice of the accumulator drained: hand it back
             ptx::tc_fence_before();
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive_cluster_relaxed(ptx::mapa(ptx::smem_u32(&tempty[acc]), 0));
           }
-          const int k0 = c * 256 + g * 128 + b * 32;
-          const float4* q4 = reinterpret_cast<const float4*>(sq + k0);
-          float g4[8];  // independent group minima: a shallow dependency tree, not a 32-long chain
+          const int k0 = c * KT_CW + g * KT_GCOLS + b * 32;
+          const uint32_t q_s = sq_s + static_cast<uint32_t>(k0) * 4;
+          float g4[8];  // independent group minima (a shallow dependency tree)
 #pragma unroll
           for (int j = 0; j < 32; j += 4) {
-            const float4 qv = q4[j / 4];
+            float4 qv;
+            asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                         : "=f"(qv.x), "=f"(qv.y), "=f"(qv.z), "=f"(qv.w)
+                         : "r"(q_s + j * 4));
             const float t0 = fmaf(-2.f, __uint_as_float(cur[j]), qv.x);
             const float t1 = fmaf(-2.f, __uint_as_float(cur[j + 1]), qv.y);
             const float t2 = fmaf(-2.f, __uint_as_float(cur[j + 2]), qv.z);
@@ -278,77 +303,116 @@ __global__ void __launch_bounds__(KT_THREADS, 1)
                                    fminf(fminf(g4[4], g4[5]), fminf(g4[6], g4[7])));
           m = fminf(m, bmin);
           const float thr = m + two_eps;
-          // branch-free candidate mask (four independent partial masks); the
-          // (rare) appends loop over its bits. Entries carry their batch
-          // minimum, a lower bound of their t (no dynamic register indexing):
-          // an entry whose batch minimum exceeds the final threshold is
-          // certainly stale; the rest are verified exactly.
-          uint32_t mask = 0;
+          // candidate mask: set.le gives exact 1.0/0.0 flags (one ALU op per
+          // score) that FFMAs (the FMA pipe) weigh by 2^j into exact integers
+          // below 2^24, read back from the float bits. A batch with candidates
+          // appends ONE entry (key, mask): the key is a lower bound of the
+          // batch minimum (so of every candidate's t) carrying the batch
+          // index in its low 4 bits -- an entry whose key exceeds the final
+          // threshold is certainly stale; the rest are verified exactly.
           if (!(dbg & 2)) {
-            uint32_t pm[4] = {0, 0, 0, 0};
+            float acc[4] = {0x1p23f, 0.f, 0x1p23f, 0.f};  // 2^23 + bits 0-15 / 2^23 + bits 16-31
 #pragma unroll
-            for (int j = 0; j < 32; ++j) pm[j & 3] |= (__uint_as_float(cur[j]) <= thr ? 1u : 0u) << j;
-            mask = (pm[0] | pm[1]) | (pm[2] | pm[3]);
+            for (int j = 0; j < 32; ++j) {
+              float f;
+              asm("set.le.f32.f32 %0, %1, %2;" : "=f"(f) : "f"(__uint_as_float(cur[j])), "f"(thr));
+              acc[(j >> 4) * 2 + (j & 1)] = fmaf(f, static_cast<float>(1u << (j & 15)), acc[(j >> 4) * 2 + (j & 1)]);
+            }
+            const uint32_t lo = __float_as_uint(acc[0] + acc[1]), hi = __float_as_uint(acc[2] + acc[3]);
+            uint32_t mask = __byte_perm(lo, hi, 0x5410);
             if (dbg & 8) {  // diagnostics: build the mask but skip the appends
               ovf |= mask == 0x5a5a5a5au;
               mask = 0;
             }
-          }
-          while (mask) {
-            const int j = __ffs(mask) - 1;
-            mask &= mask - 1;
-            if (cnt == KT_LIST) {  // drop entries the running minimum has excluded
-              int w = 0;
-              for (int e = 0; e < KT_LIST; ++e)
-                if (my[e].x <= thr) my[w++] = my[e];
-              cnt = w;
+            if (mask) {
+              if (cnt == KT_LIST) {  // drop entries the running minimum has excluded
+                int w = 0;
+#pragma unroll
+                for (int e = 0; e < KT_LIST; ++e) {
+                  const float2 en = my[e];
+                  if (en.x <= thr) my[w++] = en;
+                }
+                cnt = w;
+              }
+              if (cnt < KT_LIST) {
+                const float lb = bmin - (fabsf(bmin) * 0x1p-16f + 0x1p-100f);  // < bmin by >= 8 ulps
+                const uint32_t key = (__float_as_uint(lb) & ~0xfu) | static_cast<uint32_t>(c * (KT_GCOLS / 32) + b);
+                my[cnt++] = make_float2(__uint_as_float(key), __uint_as_float(mask));
+              } else {
+                ovf = 1;
+              }
             }
-            if (cnt < KT_LIST)
-              my[cnt++] = make_float2(bmin, __int_as_float(k0 + j));
-            else
-              ovf = 1;
           }
-          if (b < 3) ptx::tmem_ld_wait();
         }
+        if (++acc == KT_NACC) acc = 0;
       }
-      xch[(buf * 2 + g) * KT_ROWS + pl] = make_float4(m, __int_as_float(cnt), __int_as_float(ovf), two_eps);
+      xch[(buf * KT_GROUPS + g) * KT_ROWS + pl] = make_float2(m, __int_as_float(cnt | (ovf << 16)));
+      if (g == 0) xeps[buf * KT_ROWS + pl] = two_eps;
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&lfull[buf]);
     }
   } else if (warp < KT_SCAN + KT_VER) {
     // ---------------- verify: final filter, exact check of multi-candidate points, store ----------------
-    const int vw = warp - KT_SCAN;
-    const int pl = vw * 32 + lane;
-    int2* wq = vq + vw * (32 * 2 * KT_LIST);
-    int it = 0;
-    for (int t = cluster; t < tiles; t += nclusters, ++it) {
-      const int buf = it & 1;
+    // set vset = vw / 4 takes the tiles of list buffer vset (every other tile)
+    const int vw = warp - KT_SCAN, vset = vw / 4;
+    const int pl = (vw % 4) * 32 + lane;
+    int2* wq = vq + vw * (32 * KT_QCAP);
+    int it = vset;
+    for (int t = cluster + vset * nclusters; t < tiles; t += 2 * nclusters, it += 2) {
+      const int buf = vset;
       const int row = t * 2 * KT_ROWS + static_cast<int>(rank) * KT_ROWS + pl;
       const bool valid = row < rows;
+      if (lane == 0 && t + 2 * nclusters < tiles) {  // next tile's fp32 rows of this warp -> L2
+        const int64_t nrow = static_cast<int64_t>(t + 2 * nclusters) * 2 * KT_ROWS + rank * KT_ROWS + (vw % 4) * 32;
+        const int64_t nr = rows - nrow < 32 ? rows - nrow : 32;
+        if (nr > 0) ptx::bulk_prefetch_l2(pts + nrow * KT_D, static_cast<uint32_t>(nr * KT_D * 4));
+      }
       ptx::mbar_wait(&lfull[buf], (it >> 1) & 1);
       if (dbg & 4) {
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(&lempty[buf]);
         continue;
       }
-      const float4 o0 = xch[(buf * 2 + 0) * KT_ROWS + pl];
-      const float4 o1 = xch[(buf * 2 + 1) * KT_ROWS + pl];
-      const float thr = fminf(o0.x, o1.x) + o0.w;
-      const int cnt0 = __float_as_int(o0.y), cnt1 = __float_as_int(o1.y);
-      const int ovf = __float_as_int(o0.z) | __float_as_int(o1.z);
-      const float2* l0 = lists + buf * KT_LBUF + pl * KT_LIST;
-      const float2* l1 = lists + buf * KT_LBUF + (KT_ROWS + pl) * KT_LIST;
+      float mall = __int_as_float(0x7f800000);
+      int ovf = 0, cnts[KT_GROUPS];
+#pragma unroll
+      for (int gg = 0; gg < KT_GROUPS; ++gg) {
+        const float2 o = xch[(buf * KT_GROUPS + gg) * KT_ROWS + pl];
+        mall = fminf(mall, o.x);
+        cnts[gg] = __float_as_int(o.y) & 0xffff;
+        ovf |= __float_as_int(o.y) >> 16;
+      }
+      const float thr = mall + xeps[buf * KT_ROWS + pl];
+      const float2* lbase = lists + buf * KT_LBUF + pl * KT_LIST;
+      // all list entries at once (independent shared loads), stale ones masked off
+      float2 ent[KT_GROUPS * KT_LIST];
+#pragma unroll
+      for (int gg = 0; gg < KT_GROUPS; ++gg)
+#pragma unroll
+        for (int e = 0; e < KT_LIST; ++e) {
+          float2 en = make_float2(0.f, 0.f);
+          if (e < cnts[gg]) en = lbase[gg * KT_ROWS * KT_LIST + e];
+          if (!(en.x <= thr)) en.y = 0.f;  // mask 0: no candidates
+          ent[gg * KT_LIST + e] = en;
+        }
       // a single survivor is the exact argmin as it stands; points with several
       // survivors queue their (point, centroid) pairs for the whole warp
       int nc = 0, k1 = 0;
       if (valid && !ovf)
-        for (int e = 0; e < cnt0 + cnt1; ++e) {
-          const float2 en = e < cnt0 ? l0[e] : l1[e - cnt0];
-          if (en.x <= thr) {
-            ++nc;
-            k1 = __float_as_int(en.y);
+#pragma unroll
+        for (int gg = 0; gg < KT_GROUPS; ++gg)
+#pragma unroll
+          for (int e = 0; e < KT_LIST; ++e) {
+            const uint32_t mk = __float_as_uint(ent[gg * KT_LIST + e].y);
+            if (mk) {
+              nc += __popc(mk);
+              k1 = entry_k0(__float_as_uint(ent[gg * KT_LIST + e].x), gg) + __ffs(mk) - 1;
+            }
           }
-        }
+      if (nc > KT_QCAP) {  // more survivors than its queue share: full scan
+        ovf = 1;
+        nc = 0;
+      }
       const int nq = (nc >= 2 && !(dbg & 1)) ? nc : 0;
       int off = nq;  // inclusive warp scan of the queue counts
 #pragma unroll
@@ -358,12 +422,23 @@ __global__ void __launch_bounds__(KT_THREADS, 1)
       }
       const int total = __shfl_sync(0xffffffffu, off, 31);
       off -= nq;
+      if (dbg & 16) {  // diagnostics: queued exact checks, multi-candidate points
+        const uint32_t multi = __ballot_sync(0xffffffffu, nq > 0);
+        if (lane == 0) {
+          atomicAdd(n_overflow + 1, total);
+          atomicAdd(n_overflow + 2, __popc(multi));
+        }
+      }
       if (nq) {
         int w = off;
-        for (int e = 0; e < cnt0 + cnt1; ++e) {
-          const float2 en = e < cnt0 ? l0[e] : l1[e - cnt0];
-          if (en.x <= thr) wq[w++] = make_int2(__float_as_int(en.y) | (lane << 16), 0);
-        }
+#pragma unroll
+        for (int gg = 0; gg < KT_GROUPS; ++gg)
+#pragma unroll
+          for (int e = 0; e < KT_LIST; ++e) {
+            const int k0 = entry_k0(__float_as_uint(ent[gg * KT_LIST + e].x), gg);
+            for (uint32_t mk = __float_as_uint(ent[gg * KT_LIST + e].y); mk; mk &= mk - 1)
+              wq[w++] = make_int2((k0 + __ffs(mk) - 1) | (lane << 16), 0);
+          }
       }
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&lempty[buf]);  // lists consumed (the queue is private)
@@ -383,24 +458,40 @@ __global__ void __launch_bounds__(KT_THREADS, 1)
         wq[i].y = __float_as_int(exact_dist(x, cent + static_cast<int64_t>(k) * KT_D));
       }
       __syncwarp();
+      // points whose candidate list overflowed: exact scan over all K, the
+      // whole warp sharing one point (lane-strided centroids, then a warp
+      // argmin with the lowest index on ties)
+      int okb = -1;
+      for (uint32_t om = __ballot_sync(0xffffffffu, valid && ovf); om; om &= om - 1) {
+        const int p = __ffs(om) - 1;
+        float x[KT_D];
+#pragma unroll
+        for (int j = 0; j < KT_D; j += 4) {
+          const float4 v = __ldg(reinterpret_cast<const float4*>(pts + static_cast<int64_t>(row0 + p) * KT_D + j));
+          x[j] = v.x;
+          x[j + 1] = v.y;
+          x[j + 2] = v.z;
+          x[j + 3] = v.w;
+        }
+        float best = __int_as_float(0x7f800000);
+        int bkk = 0x7fffffff;
+        for (int k = lane; k < K; k += 32) {
+          const float e = exact_dist(x, cent + static_cast<int64_t>(k) * KT_D);
+          if (e < best) { best = e; bkk = k; }
+        }
+#pragma unroll
+        for (int sft = 16; sft; sft >>= 1) {
+          const float ob = __shfl_xor_sync(0xffffffffu, best, sft);
+          const int ok = __shfl_xor_sync(0xffffffffu, bkk, sft);
+          if (ob < best || (ob == best && ok < bkk)) { best = ob; bkk = ok; }
+        }
+        if (lane == p) okb = bkk;
+      }
       if (valid) {
         int bk = k1;
-        if (ovf) {  // candidate list overflowed: exact scan over all K (rare)
+        if (ovf) {  // candidate list overflowed (rare): the warp scan above
           atomicAdd(n_overflow, 1);
-          float x[KT_D];
-#pragma unroll
-          for (int j = 0; j < KT_D; j += 4) {
-            const float4 v = __ldg(reinterpret_cast<const float4*>(pts + static_cast<int64_t>(row) * KT_D + j));
-            x[j] = v.x;
-            x[j + 1] = v.y;
-            x[j + 2] = v.z;
-            x[j + 3] = v.w;
-          }
-          float best = __int_as_float(0x7f800000);
-          for (int k = 0; k < K; ++k) {
-            const float e = exact_dist(x, cent + static_cast<int64_t>(k) * KT_D);
-            if (e < best) { best = e; bk = k; }
-          }
+          bk = okb;
         } else if (nq) {
           float best = __int_as_float(0x7f800000);
           bk = 0x7fffffff;
@@ -515,8 +606,8 @@ uint64_t launch_assign_tc(LaunchCtx& c) {
       reinterpret_cast<const float*>(Cb.ptr), b1, b2, q, stats, static_cast<int>(k));
   HCL_LAUNCHED();
   CUtensorMap ta = make_tmap_2d_bf16(split, 64, rows, 128, 64, KT_ROWS);
-  CUtensorMap tb1 = make_tmap_2d_bf16(b1, 64, static_cast<uint64_t>(k), 128, 64, 128);
-  CUtensorMap tb2 = make_tmap_2d_bf16(b2, 64, static_cast<uint64_t>(k), 128, 64, 128);
+  CUtensorMap tb1 = make_tmap_2d_bf16(b1, 64, static_cast<uint64_t>(k), 128, 64, KT_CW / 2);
+  CUtensorMap tb2 = make_tmap_2d_bf16(b2, 64, static_cast<uint64_t>(k), 128, 64, KT_CW / 2);
   const KtLayout Lh(static_cast<int>(k));
   const size_t smem = Lh.total;
   HCL_CUDA(cudaFuncSetAttribute(kmeans_assign_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -541,6 +632,13 @@ uint64_t launch_assign_tc(LaunchCtx& c) {
                               reinterpret_cast<const float*>(stats), reinterpret_cast<const float*>(Cb.ptr), pts, xx,
                               asg, static_cast<int>(rows), static_cast<int>(k), n_ovf, dbg));
   HCL_LAUNCHED();
+  if (dbg & 16) {  // diagnostics: report list overflows of this launch
+    int h[3] = {0, 0, 0};
+    HCL_CUDA(cudaMemcpyAsync(h, n_ovf, 12, cudaMemcpyDeviceToHost, c.stream));
+    HCL_CUDA(cudaStreamSynchronize(c.stream));
+    std::fprintf(stderr, "kmeans_assign_tc: %d list overflows, %d queued exact checks, %d multi-candidate points in %lld points\n",
+                 h[0], h[1], h[2], static_cast<long long>(rows));
+  }
   return 3ull * rows * static_cast<uint64_t>(k) * static_cast<uint64_t>(d);
 }
 
