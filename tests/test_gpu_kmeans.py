@@ -169,3 +169,30 @@ def test_accumulate_many_points_one_cluster(ctx, queues):
     km.close()
     assert (c == c_want).all() and (s == s_want).all()
     assert c_want[0] == n and abs(int(s_want[1])) > 2**31
+
+
+def test_full_size_c4_sampled_parity(ctx, queues):
+    """SURVEY.md §8(d) C4 at full size: 2^28 points generated in HBM, K = 1024,
+    initial centroids = the first K points, one full iteration, then the
+    tensor-filtered assignment of 2^16 sampled points (64 seeded blocks of 1024)
+    recomputed by the oracle against the GPU's centroids, bit-exactly."""
+    from paper_2005_08466_b200.kmeans import KMeans
+
+    n, d, k = 1 << 28, 32, 1024
+    km = KMeans(ctx, queues[:1], n, d, k, tensor_filter=True)
+    try:
+        km.generate_points(42, k)
+        km.set_centroids(G.gen_kmeans_points(k, d, k, 42))
+        km.iterate(1)
+        cent = km.centroids().reshape(-1)
+        _, counts = km.sums()
+        assert int(counts.sum()) == n
+        km.assign_only()
+        got = km.assignments()
+    finally:
+        km.close()
+    rng = np.random.default_rng(7)
+    for off in rng.choice(n // 1024, 64, replace=False) * 1024:
+        pts = G.gen_kmeans_points(1024, d, k, 42, first=int(off))
+        want = O.kmeans_assign(pts, 1024, d, cent, k)
+        assert (got[off:off + 1024] == want).all(), off
