@@ -71,3 +71,41 @@ def test_conv_partition_invariance(ctx, queues, P, weights):
     _, _, whole = run(ctx, queues, n, h, wd, c, k, True)
     _, _, part = run(ctx, queues, n, h, wd, c, k, True, P=P, weights=weights)
     assert whole.tobytes() == part.tobytes()
+
+
+def test_conv_full_c5_sampled(ctx, queues):
+    """SURVEY.md §8(d) C5 at full size (batch 256, 224 x 224, 64 -> 128, bf16
+    output): 4096 seeded output points -- a quarter of them on the padded
+    border -- against the C oracle's fp64 direct conv of the same bf16 inputs."""
+    from paper_2005_08466_b200.conv import Conv3x3
+
+    n, h, wd, c, k = 256, 224, 224, 64, 128
+    xb = O.gen_bf16(n * h * wd * c, 42)
+    wb = O.gen_bf16(k * 9 * c, 43)
+    cv = Conv3x3(ctx, queues[:1], n, h, wd, c, k, out_f32=False)
+    try:
+        cv.load(xb.reshape(n, h, wd, c), wb.reshape(k, 3, 3, c))
+        cv.run()
+        cv.finish()
+        raw = ctx.enqueue_read_buffer(queues[0], cv.b_out).view(np.uint16)
+    finally:
+        cv.close()
+    rng = np.random.default_rng(5)
+    m = 4096
+    ni, yi, xi, ki = (rng.integers(0, v, m) for v in (n, h, wd, k))
+    edge = rng.integers(0, 4, m)  # first quarter: pin y or x to a border
+    yi[: m // 8] = np.where(edge[: m // 8] & 1, h - 1, 0)
+    xi[m // 8: m // 4] = np.where(edge[m // 8: m // 4] & 1, wd - 1, 0)
+    x = xb.reshape(n, h, wd, c)  # bf16 bits; converted per patch
+    w = np.abs(O.bf16_to_f32(wb).reshape(k, 3, 3, c).astype(np.float64))
+    for i, y, xx, ko in zip(ni, yi, xi, ki):
+        i, y, xx, ko = int(i), int(y), int(xx), int(ko)
+        got = float(O.bf16_to_f32(raw[((i * h + y) * wd + xx) * k + ko: ((i * h + y) * wd + xx) * k + ko + 1])[0])
+        want = O.conv3x3_point(xb, wb, h, wd, c, k, i, y, xx, ko)
+        scale = 0.0
+        for r in range(3):
+            for s in range(3):
+                yy, xs = y + r - 1, xx + s - 1
+                if 0 <= yy < h and 0 <= xs < wd:
+                    scale += float(np.abs(O.bf16_to_f32(x[i, yy, xs]).astype(np.float64)) @ w[ko, r, s])
+        assert abs(got - want) <= 2.0**-8 * max(scale, 1e-30), (i, y, xx, ko, got, want)

@@ -189,3 +189,23 @@ def test_gemm_f32_simt_tiles_bit_identical(ctx, queues, monkeypatch):
     assert all(o == outs[0] for o in outs)
     a64, b64 = a.astype(np.float64).reshape(m, k), b.astype(np.float64).reshape(k, n)
     assert normwise_err(np.frombuffer(outs[0], np.float32).reshape(m, n), a64, b64) <= 2.0**-20
+
+
+@pytest.mark.parametrize("kernel,out_f32,tol", [("gemm_bf16", True, 2.0**-12), ("gemm_bf16", False, 2.0**-8),
+                                                ("gemm_f32x3", True, 2.0**-17), ("gemm_f32", True, 2.0**-20)])
+def test_gemm_full_c2_sampled(ctx, queues, kernel, out_f32, tol):
+    """SURVEY.md §8(d) C2 at full size (16384^3, A seed 42, B seed 43): 4096
+    seeded (i, j) entries -- a 64 x 64 grid of rows and columns -- against fp64
+    dot products of the same rounded inputs, with the path's normwise tolerance."""
+    s = 16384
+    if kernel == "gemm_bf16":
+        a, b = O.gen_bf16(s * s, 42), O.gen_bf16(s * s, 43)
+        af, bf = O.bf16_to_f32(a).reshape(s, s), O.bf16_to_f32(b).reshape(s, s)
+    else:
+        a, b = O.gen_doubles(s * s, 42).astype(np.float32), O.gen_doubles(s * s, 43).astype(np.float32)
+        af, bf = a.reshape(s, s), b.reshape(s, s)
+    c = gemm(ctx, queues, kernel, a, b, s, s, s, out_f32=out_f32)
+    rng = np.random.default_rng(11)
+    ii, jj = np.sort(rng.choice(s, 64, replace=False)), np.sort(rng.choice(s, 64, replace=False))
+    a64, b64 = af[ii].astype(np.float64), bf[:, jj].astype(np.float64)
+    assert normwise_err(c[np.ix_(ii, jj)], a64, b64) <= tol
