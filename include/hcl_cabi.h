@@ -173,6 +173,19 @@ int hcl_broadcast(int dev, uint64_t buffer_id, uint64_t offset, uint64_t bytes, 
 int hcl_collective(int op, const int* devs, int ndev, const uint64_t* buf_ids, uint64_t count, int dtype,
                    int root);
 
+/* ---- remote-node path ------------------------------ */
+/* Serve this process's logical devices (hcl_init) to remote hosts over the
+ * HaoCL wire protocol: HCL1 frames on TCP `message_port` and message_port+1
+ * (data), the daemon side of proj/src/daemon.cpp + net.cpp (Ping/Pong,
+ * DeviceIdRequest, DataTransfer/DataAck, the five forwarded ApiCalls,
+ * Shutdown). Buffers stay resident in HBM between calls. hcl_node_start
+ * returns once both ports listen; hcl_node_wait blocks until a Shutdown
+ * message (or hcl_node_stop from another thread); hcl_node_stop drains the
+ * connections and frees the daemon. */
+int hcl_node_start(const char* host, int message_port, void** node);
+int hcl_node_wait(void* node);
+int hcl_node_stop(void* node);
+
 const char* hcl_last_error(void);
 
 #ifdef __cplusplus

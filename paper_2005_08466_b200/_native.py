@@ -43,6 +43,9 @@ CABI = [
     ("hcl_comm_acquire", C.c_int, [C.c_int, C.c_uint64, C.c_int]),
     ("hcl_comm_release", C.c_int, [C.c_int, C.c_uint64, C.c_int]),
     ("hcl_collective", C.c_int, [C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_uint64, C.c_int, C.c_int]),
+    ("hcl_node_start", C.c_int, [C.c_char_p, C.c_int, C.POINTER(C.c_void_p)]),
+    ("hcl_node_wait", C.c_int, [C.c_void_p]),
+    ("hcl_node_stop", C.c_int, [C.c_void_p]),
     ("hcl_device_set_sm_budget", C.c_int, [C.c_int, C.c_int]),
     ("hcl_query_registry", C.c_int, [C.c_char_p, C.c_char_p, C.c_int, C.POINTER(C.c_uint32), C.c_int, i32p]),
     ("hcl_kernel_signature", C.c_int, [C.c_char_p, C.c_char_p, u8p, u8p, C.c_int, i32p]),

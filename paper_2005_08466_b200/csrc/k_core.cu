@@ -295,6 +295,53 @@ uint64_t launch_spmv_compute(LaunchCtx& c) {
 }
 
 // ---------------------------------------------------------------------------
+// bfs — proj/src/kernels.cpp:154-193. Level-synchronous: pass L visits every
+// vertex of level L-1 and claims each unseen neighbour with a CAS, so every
+// vertex gets its unique BFS level (-1 when unreachable) under any schedule --
+// the same levels as the reference's CAS frontier loop. One pass per level;
+// the host stops after a pass that claims nothing.
+
+__global__ void __launch_bounds__(256) bfs_level_kernel(const int64_t* __restrict__ row_ptr,
+                                                        const int64_t* __restrict__ col_idx, int64_t vertices,
+                                                        int32_t level, int32_t* __restrict__ levels,
+                                                        int* __restrict__ claimed) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int any = 0;
+  for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < vertices; u += stride) {
+    if (levels[u] != level - 1) continue;
+    for (int64_t p = row_ptr[u], e = row_ptr[u + 1]; p < e; ++p) {
+      const int64_t v = __ldg(col_idx + p);
+      if (levels[v] == -1 && atomicCAS(levels + v, -1, level) == -1) any = 1;
+    }
+  }
+  if (__syncthreads_or(any) && threadIdx.x == 0) atomicOr(claimed, 1);
+}
+
+uint64_t launch_bfs(LaunchCtx& c) {
+  Csr64 s = csr_view(c, 0, 1, 2, -1, "bfs");
+  const int64_t source = scalar_arg(c, 3, "bfs source");
+  if (source < 0 || source >= s.rows) fail(ErrorCode::argument, "bfs: source out of range");
+  const BufView& L = buffer_arg(c, 4, "bfs levels");
+  int32_t* levels = at_byte<int32_t>(L, 0, static_cast<uint64_t>(s.rows) * 4, "bfs levels");
+  HCL_CUDA(cudaMemsetAsync(levels, 0xff, static_cast<size_t>(s.rows) * 4, c.stream));
+  const int32_t zero = 0;
+  HCL_CUDA(cudaMemcpyAsync(levels + source, &zero, 4, cudaMemcpyHostToDevice, c.stream));
+  int* claimed = static_cast<int*>(c.scratch(c.dev, 64));
+  const unsigned blocks = static_cast<unsigned>(std::max<int64_t>(
+      1, std::min<int64_t>(ceil_div(s.rows, 256), static_cast<int64_t>(c.sm_count) * 8)));
+  for (int32_t level = 1;; ++level) {
+    HCL_CUDA(cudaMemsetAsync(claimed, 0, 4, c.stream));
+    bfs_level_kernel<<<blocks, 256, 0, c.stream>>>(s.row_ptr, s.col_idx, s.rows, level, levels, claimed);
+    HCL_LAUNCHED();
+    int h = 0;
+    HCL_CUDA(cudaMemcpyAsync(&h, claimed, 4, cudaMemcpyDeviceToHost, c.stream));
+    HCL_CUDA(cudaStreamSynchronize(c.stream));
+    if (!h) break;
+  }
+  return static_cast<uint64_t>(s.nnz);
+}
+
+// ---------------------------------------------------------------------------
 // knn — proj/src/kernels.cpp:195-233. One 128-thread block per query; each
 // thread keeps a sorted top-k of its strided reference subset under the
 // (dist, idx) order, then the block merges the 128 lists k times by a
@@ -722,6 +769,7 @@ void register_core(std::vector<KernelDef>& r) {
                nullptr});
   r.push_back({"core", "spmv_compute", {I, I, I, I, I, S, S, O}, {P, P, P, P, P, N, N, P},
                launch_spmv_compute, nullptr, nullptr});
+  r.push_back({"core", "bfs", {I, I, I, S, O}, {P, P, P, N, P}, launch_bfs, nullptr, nullptr});
   r.push_back({"core", "knn", {I, I, S, S, S, S, O, O}, {P, X, N, N, N, N, X, X}, launch_knn,
                rowbytes_knn, rows_knn});
   r.push_back({"core", "vecadd", {I, I, O, S}, {X, X, X, N}, launch_vecadd, rowbytes_vecadd,

@@ -85,6 +85,31 @@ def test_vecadd_digest(ctx, queues, golden, n, P):
     assert h(O.fnv1a(out[2])) == golden["digests"][f"vecadd_{n}"]
 
 
+@pytest.mark.parametrize("V,E", [(1000, 10**4), (10**5, 10**6)])
+def test_bfs_digest(ctx, queues, golden, V, E):
+    """bfs (proj/src/kernels.cpp:154-193; whole range only, as bench.cpp:539-540):
+    levels bit-identical to the reference digest, and to the oracle from
+    another source (unreachable vertices stay -1)."""
+    rp, ci = O.gen_graph(V, E, 42)
+    hdr = np.array([V, V], np.int64)
+    out = run(ctx, "bfs", [hdr, rp, ci, 0, ("out", V * 4)], [4], queues[:1])
+    assert h(O.fnv1a(out[4])) == golden["digests"][f"bfs_{V}v{E}e"]
+    out = run(ctx, "bfs", [hdr, rp, ci, V // 3, ("out", V * 4)], [4], queues[:1])
+    assert (out[4].view(np.int32) == O.bfs(rp, ci, V // 3)).all()
+
+
+def test_bfs_unreachable_and_errors(ctx, queues):
+    # two components: 0-1-2 and 3-4; source 4 reaches only 3
+    rp = np.array([0, 1, 3, 4, 5, 6], np.int64)
+    ci = np.array([1, 0, 2, 1, 4, 3], np.int64)
+    hdr = np.array([5, 5], np.int64)
+    out = run(ctx, "bfs", [hdr, rp, ci, 4, ("out", 20)], [4], queues[:1])[4].view(np.int32)
+    assert out.tolist() == [-1, -1, -1, 1, 0]
+    with pytest.raises(HaoclError) as e:
+        run(ctx, "bfs", [hdr, rp, ci, 5, ("out", 20)], [4], queues[:1])
+    assert e.value.name == "argument"
+
+
 @pytest.mark.parametrize("r,c,d", [(100, 100, 0.1), (10**4, 10**4, 1e-3), (10**5, 10**5, 1e-4)])
 def test_spmv_two_stage_digest(ctx, queues, golden, r, c, d):
     """The reference bench's two-stage SpMV (proj/src/bench.cpp:210-321): stage 1
