@@ -11,7 +11,7 @@
 // haocl::bench::run_benchmark -- the unmodified reference path: seeded inputs,
 // block_range partitioning over the parts, per-part buffers and launches, and
 // in-process oracle verification -- and prints the RunReport JSON.
-// Keys: m k n rows cols density vertices edges knn_r knn_q knn_d knn_k length seed.
+// Keys: m k n rows cols density vertices edges knn_r knn_q knn_d knn_k length seed type.
 
 #include <cstdlib>
 #include <iostream>
@@ -28,9 +28,12 @@ int main(int argc, char** argv) {
     return 2;
   }
   const int port = std::atoi(argv[1]), ndev = std::atoi(argv[2]);
+  std::string type = "gpu";  // type=cpu to drive the reference's own daemon (ref_node)
+  for (int i = 5; i < argc; ++i)
+    if (std::string(argv[i]).rfind("type=", 0) == 0) type = std::string(argv[i]).substr(5);
   std::ostringstream conf;
   conf << "host 127.0.0.1:" << (port + 50) << "\n";
-  for (int d = 0; d < ndev; ++d) conf << "node n0 127.0.0.1:" << port << " gpu 1.0\n";
+  for (int d = 0; d < ndev; ++d) conf << "node n0 127.0.0.1:" << port << " " << type << " 1.0\n";
   haocl::bench::BenchParams p;
   p.benchmark = argv[3];
   p.partition = std::atoi(argv[4]);

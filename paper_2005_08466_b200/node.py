@@ -15,6 +15,7 @@ from __future__ import annotations
 
 import argparse
 import ctypes as C
+import os
 from typing import Optional, Sequence
 
 from . import _native as N
@@ -61,6 +62,9 @@ def main(argv=None) -> None:
     ap.add_argument("--port", type=int, required=True, help="message port (data port = port + 1)")
     ap.add_argument("--devices", default="0", help="comma-separated CUDA ordinals served as local devices")
     a = ap.parse_args(argv)
+    # load every kernel when the devices are set up, not inside the first
+    # launch (whose node-reported compute time would include the module load)
+    os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
     d = NodeDaemon(a.port, a.host, [int(x) for x in a.devices.split(",") if x != ""])
     print(f"haocl node: serving {a.devices} on {a.host}:{a.port}/{a.port + 1}", flush=True)
     try:
