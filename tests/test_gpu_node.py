@@ -67,3 +67,48 @@ def test_reference_host_drives_b200_node(node, golden, bench, args, key, parts):
     assert report["result_digest"].lower() == golden["digests"][key]
     assert report["partition"] == parts and len(report["devices"]) == ndev
     assert all(d.endswith(":gpu") for d in report["devices"])
+
+
+def _vecadd(c, call_id, dev, a, b, out, n):
+    return c.call(call_id, "launch_kernel",
+                  [(W.STRING, "vecadd"), (W.STRING, "default"), (W.I32, 1), (W.I32, dev), (W.I32, 1),
+                   (W.I64, n), (W.I64, 1), (W.I64, 1), (W.I32, 4),
+                   (W.HANDLE, a), (W.HANDLE, b), (W.HANDLE, out), (W.I64, n)])
+
+
+def test_residency_peer_staging_and_invalidation(node):
+    """HBM residency of the daemon's buffers: an output feeds a launch on the
+    other device (peer copy, never read back), a rewritten input invalidates
+    the resident copies, and read_buffer returns the newest bytes."""
+    import numpy as np
+
+    port, _ = node
+    n = 1 << 16
+    rng = np.random.default_rng(1)
+    a, b, a2 = (rng.standard_normal(n) for _ in range(3))
+    m, d = W.Conn(port), W.Conn(port + 1)
+
+    def put(cid, bid, arr):
+        m.call(cid, "alloc_buffer", [(W.HANDLE, bid), (W.I64, arr.nbytes)])
+        raw = arr.tobytes()
+        for off in range(0, len(raw), 1 << 18):  # 256 KiB chunks, last one acknowledged
+            d.send(W.frame(W.DATA, cid * 100 + off // (1 << 18), W.data_chunk(bid, off, len(raw), raw[off:off + (1 << 18)])))
+        kind, _, body = d.recv_frame()
+        assert kind == W.ACK
+
+    put(1, 101, a)
+    put(2, 102, b)
+    for bid in (103, 104):
+        m.call(3, "alloc_buffer", [(W.HANDLE, bid), (W.I64, n * 8)])
+    res = _vecadd(m, 4, 0, 101, 102, 103, n)  # c = a + b on device 0
+    assert res[2] == n  # work units = n (kernels.cpp:296)
+    _vecadd(m, 5, 1, 103, 101, 104, n)         # e = c + a on device 1: c staged by peer copy
+    e = np.frombuffer(d.call(6, "read_buffer", [(W.HANDLE, 104)])[0], np.float64)
+    assert (e == (a + b) + a).all()
+    put(7, 101, a2)                             # rewrite a: device copies are stale now
+    _vecadd(m, 8, 0, 101, 102, 103, n)
+    c = np.frombuffer(d.call(9, "read_buffer", [(W.HANDLE, 103)])[0], np.float64)
+    assert (c == a2 + b).all()
+    for bid in (101, 102, 103, 104):
+        m.call(10, "release_object", [(W.HANDLE, bid)])
+    m.close(), d.close()
