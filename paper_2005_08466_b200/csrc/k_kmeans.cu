@@ -18,9 +18,11 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <string>
 
 #include "common.hpp"
+#include "ptx.cuh"
 #include "../../include/hcl_cabi.h"
 
 namespace hcl {
@@ -180,6 +182,95 @@ __global__ void __launch_bounds__(1024) kmeans_accumulate_kernel(const float* __
   }
 }
 
+// D = 32, points streamed through shared memory by 1D bulk copies (TMA): one
+// elected thread keeps AC_STAGES chunks of AC_CHUNK points (and their
+// assignments) in flight per SM, so the HBM stream does not depend on how
+// many loads the warps keep outstanding; the warps add each staged point into
+// the block's int32 table (lane = dimension, conflict-free, one shared atomic
+// per point) and count the chunk's assignments 32 at a time.
+constexpr int AC_CHUNK = 192, AC_STAGES = 3, AC_FLUSH = 64;
+static_assert(AC_FLUSH * AC_CHUNK < (1 << 15), "rows must stay below 2^16 points between flushes");
+constexpr int AC_STAGE_BYTES = AC_CHUNK * 128 + AC_CHUNK * 4;
+
+__global__ void __launch_bounds__(1024) kmeans_accumulate32_bulk_kernel(const float* __restrict__ pts,
+                                                                       const int32_t* __restrict__ assign,
+                                                                       int64_t n, int k,
+                                                                       unsigned long long* __restrict__ sums,
+                                                                       unsigned long long* __restrict__ counts) {
+  extern __shared__ __align__(128) uint8_t ac_smem[];
+  int* tbl = reinterpret_cast<int*>(ac_smem);  // [k*32] sums + [k] counts
+  const size_t tbl_bytes = (static_cast<size_t>(k) * 33 * 4 + 127) & ~size_t(127);
+  uint8_t* stage0 = ac_smem + tbl_bytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(stage0 + AC_STAGES * AC_STAGE_BYTES);
+  uint64_t* empty = full + AC_STAGES;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nwarps = blockDim.x / 32;
+  for (int e = threadIdx.x; e < k * 33; e += blockDim.x) tbl[e] = 0;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < AC_STAGES; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&empty[s], nwarps);
+    }
+    ptx::fence_mbar_init();
+  }
+  __syncthreads();
+  // this block's range, in whole chunks (the host hands the tail to the other kernel)
+  const int64_t nchunks = n / AC_CHUNK;
+  const int64_t per = (nchunks + gridDim.x - 1) / gridDim.x;
+  const int64_t c0 = blockIdx.x * per, c1 = min(nchunks, c0 + per);
+  if (threadIdx.x == 0) {  // producer: prime the ring
+    for (int64_t ch = c0; ch < min(c1, c0 + AC_STAGES); ++ch) {
+      const int s = static_cast<int>((ch - c0) % AC_STAGES);
+      uint8_t* st = stage0 + s * AC_STAGE_BYTES;
+      ptx::mbar_arrive_expect_tx(&full[s], AC_STAGE_BYTES);
+      ptx::bulk_load(st, pts + ch * AC_CHUNK * 32, AC_CHUNK * 128, &full[s]);
+      ptx::bulk_load(st + AC_CHUNK * 128, assign + ch * AC_CHUNK, AC_CHUNK * 4, &full[s]);
+    }
+  }
+  for (int64_t ch = c0; ch < c1; ++ch) {
+    const int64_t it = ch - c0;
+    const int s = static_cast<int>(it % AC_STAGES);
+    const uint32_t ph = static_cast<uint32_t>((it / AC_STAGES) & 1);
+    ptx::mbar_wait(&full[s], ph);
+    const float* sp = reinterpret_cast<const float*>(stage0 + s * AC_STAGE_BYTES);
+    const int* sa = reinterpret_cast<const int*>(stage0 + s * AC_STAGE_BYTES + AC_CHUNK * 128);
+    if (warp < AC_CHUNK / 32) atomicAdd(&tbl[k * 32 + sa[warp * 32 + lane]], 1);  // counts: 32 points per atomic
+    for (int p = warp; p < AC_CHUNK; p += nwarps)
+      atomicAdd(&tbl[sa[p] * 32 + lane], __float2int_rz(__fmul_rn(sp[p * 32 + lane], 4096.0f)));
+    __syncwarp();
+    if (lane == 0) ptx::mbar_arrive(&empty[s]);
+    if (threadIdx.x == 0 && ch + AC_STAGES < c1) {  // refill this stage once every warp is done with it
+      ptx::mbar_wait(&empty[s], ph);
+      uint8_t* st = stage0 + s * AC_STAGE_BYTES;
+      const int64_t nx = ch + AC_STAGES;
+      ptx::mbar_arrive_expect_tx(&full[s], AC_STAGE_BYTES);
+      ptx::bulk_load(st, pts + nx * AC_CHUNK * 32, AC_CHUNK * 128, &full[s]);
+      ptx::bulk_load(st + AC_CHUNK * 128, assign + nx * AC_CHUNK, AC_CHUNK * 4, &full[s]);
+    }
+    // int32 overflow guard: |q| <= 2^15, so a row is exact while its block-local
+    // count stays below 2^16. Rows past 2^15 are flushed every AC_FLUSH chunks
+    // (at most AC_FLUSH * AC_CHUNK < 2^15 more points in between).
+    if ((it + 1) % AC_FLUSH == 0) {
+      __syncthreads();
+      for (int r = threadIdx.x; r < k; r += blockDim.x)
+        if (tbl[k * 32 + r] >= (1 << 15)) {
+          for (int j = 0; j < 32; ++j) {
+            atomicAdd(&sums[static_cast<int64_t>(r) * 32 + j],
+                      static_cast<unsigned long long>(static_cast<long long>(tbl[r * 32 + j])));
+            tbl[r * 32 + j] = 0;
+          }
+          atomicAdd(&counts[r], static_cast<unsigned long long>(tbl[k * 32 + r]));
+          tbl[k * 32 + r] = 0;
+        }
+      __syncthreads();
+    }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < k * 32; e += blockDim.x)
+    if (tbl[e]) atomicAdd(&sums[e], static_cast<unsigned long long>(static_cast<long long>(tbl[e])));
+  for (int e = threadIdx.x; e < k; e += blockDim.x)
+    if (tbl[k * 32 + e]) atomicAdd(&counts[e], static_cast<unsigned long long>(tbl[k * 32 + e]));
+}
+
 __global__ void kmeans_finalize_kernel(const long long* __restrict__ sums, const long long* __restrict__ counts, int k,
                                        int d, float* __restrict__ cent) {
   int e = blockIdx.x * blockDim.x + threadIdx.x;
@@ -250,6 +341,27 @@ uint64_t launch_accumulate(LaunchCtx& c) {
   HCL_CUDA(cudaMemsetAsync(S.ptr, 0, S.bytes, c.stream));
   HCL_CUDA(cudaMemsetAsync(Cn.ptr, 0, Cn.bytes, c.stream));
   if (!rows) return 0;
+  const uint64_t work = rows * static_cast<uint64_t>(d);
+  const size_t bulk_smem = ((static_cast<size_t>(k) * 33 * 4 + 127) & ~size_t(127)) +
+                           AC_STAGES * AC_STAGE_BYTES + 2 * AC_STAGES * 8;
+  const char* bulk_env = std::getenv("HCL_KM_ACC_BULK");  // 0: the register-pipelined kernel only
+  const bool bulk = (bulk_env ? std::atoi(bulk_env) != 0 : true) && d == 32 && bulk_smem <= 227 * 1024 &&
+                    rows >= static_cast<uint64_t>(AC_CHUNK) && (reinterpret_cast<uintptr_t>(pts) & 15) == 0 &&
+                    (reinterpret_cast<uintptr_t>(as) & 15) == 0;
+  if (bulk) {  // whole chunks streamed by TMA; the < AC_CHUNK-point tail by the kernel below
+    HCL_CUDA(cudaFuncSetAttribute(kmeans_accumulate32_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(bulk_smem)));
+    const int bgrid = static_cast<int>(std::min<uint64_t>(c.sm_count, rows / AC_CHUNK));
+    kmeans_accumulate32_bulk_kernel<<<bgrid, 1024, bulk_smem, c.stream>>>(
+        pts, as, static_cast<int64_t>(rows), static_cast<int>(k), reinterpret_cast<unsigned long long*>(S.ptr),
+        reinterpret_cast<unsigned long long*>(Cn.ptr));
+    HCL_LAUNCHED();
+    const uint64_t done = rows / AC_CHUNK * AC_CHUNK;
+    pts += done * 32;
+    as += done;
+    rows -= done;
+    if (!rows) return work;
+  }
   const size_t smem = static_cast<size_t>(k * d + k) * 4;
   const bool use_smem = smem <= 200 * 1024 && rows > static_cast<uint64_t>(k) * 4;
   if (use_smem)
@@ -262,7 +374,7 @@ uint64_t launch_accumulate(LaunchCtx& c) {
       pts, as, static_cast<int64_t>(rows), static_cast<int>(d), static_cast<int>(k),
       reinterpret_cast<unsigned long long*>(S.ptr), reinterpret_cast<unsigned long long*>(Cn.ptr), use_smem);
   HCL_LAUNCHED();
-  return rows * static_cast<uint64_t>(d);
+  return work;
 }
 
 // kmeans_finalize(sums, counts, centroids(inout), K, D)
