@@ -164,6 +164,9 @@ int hcl_nccl_destroy(int dev);
 int hcl_allgatherv(int dev, uint64_t buffer_id, const uint64_t* bounds);
 int hcl_allreduce_sum_i64(int dev, uint64_t buffer_id, uint64_t offset, uint64_t count);
 int hcl_broadcast(int dev, uint64_t buffer_id, uint64_t offset, uint64_t bytes, int root);
+/* Stream-ordered barrier on the device's kernel stream (a one-element NCCL
+ * allreduce): later kernels start after every rank's earlier kernels finished. */
+int hcl_nccl_barrier(int dev);
 
 /* In-process collective across this process's devices over NVLink peer
  * copies: devs[i] holds buffer buf_ids[i]. op 0 broadcast
@@ -172,6 +175,14 @@ int hcl_broadcast(int dev, uint64_t buffer_id, uint64_t offset, uint64_t bytes, 
  * identical on every device). dtype 0 int64, 1 fp64, 2 fp32. */
 int hcl_collective(int op, const int* devs, int ndev, const uint64_t* buf_ids, uint64_t count, int dtype,
                    int root);
+
+/* ---- cross-process peer buffers (fused exchange kernels) -------------- */
+/* Allocate buffer `id` on `dev` IPC-exportable (cudaMalloc, zero-filled) and
+ * return its 64-byte CUDA IPC handle; another process maps it with
+ * hcl_buffer_open_shared as a buffer of its own device, and kernels there
+ * store into it over NVLink (pagerank_step_exchange). */
+int hcl_buffer_alloc_shared(int dev, uint64_t id, uint64_t bytes, uint8_t* ipc_handle);
+int hcl_buffer_open_shared(int dev, uint64_t id, const uint8_t* ipc_handle, uint64_t bytes);
 
 /* ---- remote-node path ------------------------------ */
 /* Serve this process's logical devices (hcl_init) to remote hosts over the

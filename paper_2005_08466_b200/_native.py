@@ -71,6 +71,9 @@ CABI = [
     ("hcl_allgatherv", C.c_int, [C.c_int, C.c_uint64, u64p]),
     ("hcl_allreduce_sum_i64", C.c_int, [C.c_int, C.c_uint64, C.c_uint64, C.c_uint64]),
     ("hcl_broadcast", C.c_int, [C.c_int, C.c_uint64, C.c_uint64, C.c_uint64, C.c_int]),
+    ("hcl_nccl_barrier", C.c_int, [C.c_int]),
+    ("hcl_buffer_alloc_shared", C.c_int, [C.c_int, C.c_uint64, C.c_uint64, C.c_void_p]),
+    ("hcl_buffer_open_shared", C.c_int, [C.c_int, C.c_uint64, C.c_void_p, C.c_uint64]),
     ("hcl_last_error", C.c_char_p, []),
 ]
 

@@ -75,6 +75,7 @@ struct DevAlloc {
   uint64_t first_byte = 0;
   uint64_t bytes = 0;
   bool external = false;
+  uint8_t mem = 0;       // 0 stream-ordered pool, 1 cudaMalloc (IPC-exportable), 2 IPC-mapped peer memory
   uint64_t version = 0;  // bumped on every tracked write (BufView::version)
   Dep last_write;
   std::vector<Dep> reads;  // at most one per stream
@@ -160,6 +161,20 @@ struct Device {
     a.reads.clear();
   }
 };
+
+// free an allocation after d.retire(a) (the device stream then follows every use)
+void free_alloc(Device& d, DevAlloc& a) {
+  if (!a.ptr) return;
+  if (a.mem == 1 || a.mem == 2) {  // not stream-ordered: wait for the uses first
+    HCL_CUDA(cudaStreamSynchronize(d.stream));
+    if (a.mem == 1)
+      HCL_CUDA(cudaFree(a.ptr));
+    else
+      HCL_CUDA(cudaIpcCloseMemHandle(a.ptr));
+  } else if (!a.external) {
+    HCL_CUDA(cudaFreeAsync(a.ptr, d.stream));
+  }
+}
 
 std::mutex g_devices_mu;
 std::vector<std::unique_ptr<Device>> g_devices;
@@ -382,7 +397,7 @@ int hcl_buffer_alloc(int dev, uint64_t id, uint64_t first_byte, uint64_t bytes) 
     if (it != d.bufs.end()) {
       if (it->second.first_byte == first_byte && it->second.bytes == bytes) return;
       d.retire(it->second);
-      if (!it->second.external && it->second.ptr) HCL_CUDA(cudaFreeAsync(it->second.ptr, d.stream));
+      free_alloc(d, it->second);
       d.bufs.erase(it);
     }
     DevAlloc a;
@@ -404,7 +419,7 @@ int hcl_buffer_bind_external(int dev, uint64_t id, void* ptr, uint64_t first_byt
     auto it = d.bufs.find(id);
     if (it != d.bufs.end()) {
       d.retire(it->second);
-      if (!it->second.external && it->second.ptr) HCL_CUDA(cudaFreeAsync(it->second.ptr, d.stream));
+      free_alloc(d, it->second);
       d.bufs.erase(it);
     }
     DevAlloc a;
@@ -412,6 +427,56 @@ int hcl_buffer_bind_external(int dev, uint64_t id, void* ptr, uint64_t first_byt
     a.first_byte = first_byte;
     a.bytes = bytes;
     a.external = true;
+    d.bufs.emplace(id, a);
+  });
+}
+
+// Cross-process buffers (fused exchange kernels over NVLink):
+// a cudaMalloc allocation whose IPC handle other processes map as peer memory.
+int hcl_buffer_alloc_shared(int dev, uint64_t id, uint64_t bytes, uint8_t* ipc_handle) {
+  return guarded([&] {
+    if (!ipc_handle || !bytes) fail(ErrorCode::argument, "hcl_buffer_alloc_shared: need a handle slot and bytes > 0");
+    Device& d = device(dev);
+    std::lock_guard<std::mutex> lock(d.mu);
+    HCL_CUDA(cudaSetDevice(d.ordinal));
+    auto it = d.bufs.find(id);
+    if (it != d.bufs.end()) {
+      d.retire(it->second);
+      free_alloc(d, it->second);
+      d.bufs.erase(it);
+    }
+    DevAlloc a;
+    a.bytes = bytes;
+    a.mem = 1;
+    HCL_CUDA(cudaMalloc(reinterpret_cast<void**>(&a.ptr), bytes));
+    HCL_CUDA(cudaMemsetAsync(a.ptr, 0, bytes, d.stream));
+    cudaIpcMemHandle_t h;
+    HCL_CUDA(cudaIpcGetMemHandle(&h, a.ptr));
+    std::memcpy(ipc_handle, &h, sizeof(h));
+    auto [pos, ok] = d.bufs.emplace(id, a);
+    d.note(pos->second, d.stream, true);
+  });
+}
+
+int hcl_buffer_open_shared(int dev, uint64_t id, const uint8_t* ipc_handle, uint64_t bytes) {
+  return guarded([&] {
+    if (!ipc_handle) fail(ErrorCode::argument, "hcl_buffer_open_shared: handle is NULL");
+    Device& d = device(dev);
+    std::lock_guard<std::mutex> lock(d.mu);
+    HCL_CUDA(cudaSetDevice(d.ordinal));
+    auto it = d.bufs.find(id);
+    if (it != d.bufs.end()) {
+      d.retire(it->second);
+      free_alloc(d, it->second);
+      d.bufs.erase(it);
+    }
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, ipc_handle, sizeof(h));
+    DevAlloc a;
+    a.bytes = bytes;
+    a.mem = 2;
+    a.external = true;  // another process's memory: writes to it are not versioned here
+    HCL_CUDA(cudaIpcOpenMemHandle(reinterpret_cast<void**>(&a.ptr), h, cudaIpcMemLazyEnablePeerAccess));
     d.bufs.emplace(id, a);
   });
 }
@@ -507,7 +572,7 @@ int hcl_buffer_release(int dev, uint64_t id) {
     if (it == d.bufs.end()) return;  // idempotent
     HCL_CUDA(cudaSetDevice(d.ordinal));
     d.retire(it->second);
-    if (!it->second.external && it->second.ptr) HCL_CUDA(cudaFreeAsync(it->second.ptr, d.stream));
+    free_alloc(d, it->second);
     d.bufs.erase(it);
   });
 }

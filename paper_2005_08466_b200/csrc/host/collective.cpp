@@ -188,6 +188,27 @@ int hcl_allreduce_sum_i64(int dev, uint64_t buffer_id, uint64_t offset, uint64_t
   });
 }
 
+// Stream-ordered barrier across the communicator's ranks on the device's
+// kernel stream: a one-element allreduce. Kernels enqueued after it start only
+// once every rank's kernels before it have finished -- the ordering a fused
+// exchange kernel needs (its NVLink stores into peer buffers must land before
+// any rank reads them in the next step).
+int hcl_nccl_barrier(int dev) {
+  return guarded([&] {
+    ncclComm_t comm = comm_of(dev);
+    void* s = nullptr;
+    hcl_check(hcl_device_stream(dev, &s));
+    static std::map<int, void*> scratch;
+    void*& p = scratch[dev];
+    if (!p) {
+      int ord = 0;
+      if (cudaStreamGetDevice(static_cast<cudaStream_t>(s), &ord) == cudaSuccess) cudaSetDevice(ord);
+      if (cudaMalloc(&p, 8) != cudaSuccess) fail(haocl::ErrorCode::internal, "hcl_nccl_barrier: cudaMalloc");
+    }
+    nccl_check(nccl().allReduce(p, p, 1, ncclInt64, ncclSum, comm, static_cast<cudaStream_t>(s)), "ncclAllReduce");
+  });
+}
+
 int hcl_broadcast(int dev, uint64_t buffer_id, uint64_t offset, uint64_t bytes, int root) {
   return guarded([&] {
     ncclComm_t comm = comm_of(dev);

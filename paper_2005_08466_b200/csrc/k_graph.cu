@@ -99,6 +99,35 @@ __device__ __forceinline__ void pr_store(float* __restrict__ y, int r, int lo, f
     y[r - lo] = s;
 }
 
+// Fused exchange (pagerank_step_exchange): every row result is also stored
+// into the next-iteration rank vector of each peer device (NVLink stores into
+// peer / IPC-mapped memory), replacing the allgather that would follow.
+constexpr int PR_MAX_PEERS = 7;
+struct Fanout {
+  float* p[PR_MAX_PEERS];
+  int n;
+};
+
+__device__ __forceinline__ Fanout load_fanout(const unsigned long long* peers, int n) {
+  Fanout f;
+  f.n = n;
+#pragma unroll
+  for (int k = 0; k < PR_MAX_PEERS; ++k) f.p[k] = k < n ? reinterpret_cast<float*>(__ldg(peers + k)) : nullptr;
+  return f;
+}
+
+template <bool UPDATE, bool XCH>
+__device__ __forceinline__ void pr_store_x(float* __restrict__ y, int r, int lo, float s, const Update& u,
+                                           const Fanout& f) {
+  pr_store<UPDATE>(y, r, lo, s, u);
+  if constexpr (XCH) {
+    const float v = y[r - lo];
+#pragma unroll
+    for (int k = 0; k < PR_MAX_PEERS; ++k)
+      if (k < f.n) f.p[k][r] = v;
+  }
+}
+
 template <bool UPDATE>
 __device__ __forceinline__ Update pr_update(const unsigned long long* dsum, float base, float damp, float inv_v) {
   Update u{base, damp, 0.f};
@@ -138,18 +167,21 @@ __device__ __forceinline__ float warp_row_sum(const int* __restrict__ colp, cons
   return butterfly(v);
 }
 
-template <bool UPDATE, bool IMP>
+template <bool UPDATE, bool IMP, bool XCH = false>
 __global__ void __launch_bounds__(PR_T) pr_units_kernel(const int* __restrict__ row_ptr, const int* __restrict__ col,
                                                         const float* __restrict__ val, int64_t nnz_off,
                                                         const int4* __restrict__ units, int n_units,
                                                         const float* __restrict__ x,
                                                         const unsigned long long* __restrict__ dsum,
                                                         float* __restrict__ y, int lo, int hi, float base, float damp,
-                                                        float inv_v, int warp_nnz, float* __restrict__ chunk_tot) {
+                                                        float inv_v, int warp_nnz, float* __restrict__ chunk_tot,
+                                                        const unsigned long long* __restrict__ peers, int n_peers) {
   extern __shared__ float prod_all[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   float* prod = prod_all + warp * warp_nnz;
   const Update upd = pr_update<UPDATE>(dsum, base, damp, inv_v);
+  Fanout fo{};
+  if constexpr (XCH) fo = load_fanout(peers, n_peers);
   // units overlapping [lo, hi): row1 > lo and row0 < hi (both monotone in u)
   int a = 0, b = n_units;
   while (a < b) {
@@ -197,7 +229,7 @@ __global__ void __launch_bounds__(PR_T) pr_units_kernel(const int* __restrict__ 
       if (in && len <= 32) {
         float s = 0.f;
         for (int q = q0; q < q0 + len; ++q) s = __fadd_rn(s, prod[q]);
-        pr_store<UPDATE>(y, r, lo, s, upd);
+        pr_store_x<UPDATE, XCH>(y, r, lo, s, upd, fo);
       }
       unsigned mask = __ballot_sync(0xffffffffu, in && len > 32);
       while (mask) {
@@ -207,26 +239,33 @@ __global__ void __launch_bounds__(PR_T) pr_units_kernel(const int* __restrict__ 
         float v = 0.f;
         for (int q = lane; q < rlen; q += 32) v = __fadd_rn(v, prod[rq0 + q]);
         v = butterfly(v);
-        if (lane == 0) pr_store<UPDATE>(y, rb + j, lo, v, upd);
+        if (lane == 0) pr_store_x<UPDATE, XCH>(y, rb + j, lo, v, upd, fo);
       }
     }
     __syncwarp();
   }
+  if constexpr (XCH) __threadfence_system();  // peer stores visible before the barrier that follows
 }
 
 // long rows: fold the chunk totals in chunk order
-template <bool UPDATE>
+template <bool UPDATE, bool XCH = false>
 __global__ void pr_fixup_kernel(const int* __restrict__ long_rows, int n_long, const float* __restrict__ chunk_tot,
                                 const unsigned long long* __restrict__ dsum, float* __restrict__ y, int lo, int hi,
-                                float base, float damp, float inv_v) {
+                                float base, float damp, float inv_v, const unsigned long long* __restrict__ peers,
+                                int n_peers) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n_long) return;
-  const int row = long_rows[3 * i];
-  if (row < lo || row >= hi) return;
-  const int u0 = long_rows[3 * i + 1], nc = long_rows[3 * i + 2];
-  float total = chunk_tot[u0];
-  for (int c = 1; c < nc; ++c) total = __fadd_rn(total, chunk_tot[u0 + c]);
-  pr_store<UPDATE>(y, row, lo, total, pr_update<UPDATE>(dsum, base, damp, inv_v));
+  if (i < n_long) {
+    const int row = long_rows[3 * i];
+    if (row >= lo && row < hi) {
+      const int u0 = long_rows[3 * i + 1], nc = long_rows[3 * i + 2];
+      float total = chunk_tot[u0];
+      for (int c = 1; c < nc; ++c) total = __fadd_rn(total, chunk_tot[u0 + c]);
+      Fanout fo{};
+      if constexpr (XCH) fo = load_fanout(peers, n_peers);
+      pr_store_x<UPDATE, XCH>(y, row, lo, total, pr_update<UPDATE>(dsum, base, damp, inv_v), fo);
+    }
+  }
+  if constexpr (XCH) __threadfence_system();
 }
 
 // validated (row_ptr version, slice) -> row_ptr[lo], row_ptr[hi]
@@ -264,9 +303,10 @@ void pr_check_store(int dev, const BufView& R, uint64_t lo, uint64_t rows, uint6
 
 // args: row_ptr col val units long_rows x [dsum] y | V nnz_off n_units n_long warp_nnz
 // (IMP: no val argument; x is xs from pagerank_prep)
-template <bool UPDATE, bool IMP = false>
+template <bool UPDATE, bool IMP = false, bool XCH = false>
 uint64_t launch_pr(LaunchCtx& c) {
-  const char* what = IMP ? "pagerank_step_implicit" : UPDATE ? "pagerank_step" : "pagerank_spmv";
+  const char* what = XCH ? "pagerank_step_exchange"
+                         : IMP ? "pagerank_step_implicit" : UPDATE ? "pagerank_step" : "pagerank_spmv";
   constexpr uint32_t o = IMP ? 1 : 0;  // argument shift when there is no val buffer
   const uint32_t iy = (UPDATE ? 7 : 6) - o, s0 = iy + 1;
   const int64_t v = scalar_arg(c, s0, what), nnz_off = scalar_arg(c, s0 + 1, what);
@@ -295,6 +335,15 @@ uint64_t launch_pr(LaunchCtx& c) {
     if (D.bytes != 8) fail(ErrorCode::argument, std::string(what) + ": dangling sum is one uint64");
     dsum = reinterpret_cast<const unsigned long long*>(D.ptr);
   }
+  const unsigned long long* peers = nullptr;
+  int n_peers = 0;
+  if (XCH) {  // peers buffer (device addresses of the peers' next rank vectors) and their count
+    n_peers = static_cast<int>(scalar_arg(c, s0 + 6, what));
+    const BufView& PB = buffer_arg(c, s0 + 5, what);
+    if (n_peers < 0 || n_peers > PR_MAX_PEERS || PB.first_byte != 0 || PB.bytes < static_cast<uint64_t>(n_peers) * 8)
+      fail(ErrorCode::argument, std::string(what) + ": peers must list 0..7 device addresses");
+    peers = reinterpret_cast<const unsigned long long*>(PB.ptr);
+  }
   uint64_t lo, rows;
   sub_range(c, static_cast<uint64_t>(v), lo, rows, what);
   float* y = at_byte<float>(buffer_arg(c, iy, what), lo * 4, rows * 4, what);
@@ -315,7 +364,7 @@ uint64_t launch_pr(LaunchCtx& c) {
   float* chunk_tot = static_cast<float*>(c.scratch(c.dev, static_cast<size_t>(n_units) * 4));
   const float base = static_cast<float>((1.0 - 0.85) / v), damp = 0.85f, inv_v = static_cast<float>(1.0 / v);
   const size_t smem = static_cast<size_t>(warp_nnz) * 4 * PR_WARPS;
-  auto kern = pr_units_kernel<UPDATE, IMP>;
+  auto kern = pr_units_kernel<UPDATE, IMP, XCH>;
   HCL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   int per_sm = 0;
   HCL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, PR_T, smem));
@@ -325,12 +374,12 @@ uint64_t launch_pr(LaunchCtx& c) {
                                        reinterpret_cast<const int4*>(U.ptr), static_cast<int>(n_units),
                                        reinterpret_cast<const float*>(X.ptr), dsum, y, static_cast<int>(lo),
                                        static_cast<int>(lo + rows), base, damp, inv_v, static_cast<int>(warp_nnz),
-                                       chunk_tot);
+                                       chunk_tot, peers, n_peers);
   HCL_LAUNCHED();
   if (n_long) {
-    pr_fixup_kernel<UPDATE><<<static_cast<unsigned>(ceil_div(n_long, 128)), 128, 0, c.stream>>>(
+    pr_fixup_kernel<UPDATE, XCH><<<static_cast<unsigned>(ceil_div(n_long, 128)), 128, 0, c.stream>>>(
         reinterpret_cast<const int*>(L.ptr), static_cast<int>(n_long), chunk_tot, dsum, y, static_cast<int>(lo),
-        static_cast<int>(lo + rows), base, damp, inv_v);
+        static_cast<int>(lo + rows), base, damp, inv_v, peers, n_peers);
     HCL_LAUNCHED();
   }
   return 2ull * static_cast<uint64_t>(rp[1] - rp[0]);
@@ -415,6 +464,11 @@ void register_graph(std::vector<KernelDef>& r) {
   r.push_back({"b200", "pagerank_prep", {I, I, O, O, S}, {P, P, P, P, N}, launch_pr_prep, nullptr, nullptr});
   r.push_back({"b200", "pagerank_step_implicit", {I, I, I, I, I, I, O, S, S, S, S, S},
                {P, P, P, P, P, P, X, N, N, N, N, N}, launch_pr<true, true>, nullptr, rows_pr_imp});
+  // the implicit step fused with the rank-vector exchange: also stores each row into the
+  // peers' x' (peers = device addresses, uint64[n_peers]):
+  // row_ptr col units long_rows xs dsum x' | V nnz_off n_units n_long warp_nnz | peers n_peers
+  r.push_back({"b200", "pagerank_step_exchange", {I, I, I, I, I, I, O, S, S, S, S, S, I, S},
+               {P, P, P, P, P, P, X, N, N, N, N, N, P, N}, launch_pr<true, true, true>, nullptr, rows_pr_imp});
 }
 
 }  // namespace hcl

@@ -217,3 +217,90 @@ def test_pagerank_full_c3(ctx, queues):
     want = O.pagerank(rp, ci, val, deg, 20, b200_order=True)
     assert got.tobytes() == want.tobytes()
     assert abs(float(got.astype(np.float64).sum()) - 1.0) <= 1e-3
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("P", [2, 4])
+def test_step_exchange_fused_allgather(ctx, queues, graph, P):
+    """pagerank_step_exchange: each device computes its nnz-balanced row range
+    and stores every row into its own AND its peers' next rank vectors (here
+    logical devices of one process; across processes the peers are IPC-mapped
+    buffers, bench.py). After 20 iterations with only a per-iteration barrier,
+    every device holds the full rank vector, bit-identical to the
+    restated-order oracle -- no allgather ran."""
+    import ctypes as C
+
+    from paper_2005_08466_b200 import _native as N
+    from paper_2005_08466_b200.datagen import pagerank_units
+    from paper_2005_08466_b200.runtime import spmv_partition_ranges
+
+    L = N.lib()
+    rp, ci, val, deg = graph
+    v = len(rp) - 1
+    units, long_rows, n_long = pagerank_units(rp, 64)
+    bounds = [int(b) for b in spmv_partition_ranges(rp.astype(np.int64), P)]
+    base = 0x7800_0000
+    ids = {}
+
+    def bid(dev, name):
+        return ids.setdefault((dev, name), base + len(ids))
+
+    def put(dev, name, arr):
+        arr = np.ascontiguousarray(arr)
+        i = bid(dev, name)
+        N.check(L.hcl_buffer_alloc(dev, i, 0, arr.nbytes))
+        N.check(L.hcl_buffer_write(dev, i, 0, arr.ctypes.data, arr.nbytes))
+
+    def ptr(dev, name):
+        p = C.c_void_p()
+        N.check(L.hcl_buffer_device_ptr(dev, bid(dev, name), C.byref(p), None, None))
+        return p.value
+
+    def launch(dev, kernel, args, lo=None, rows=None):
+        a = (N.HclArg * len(args))()
+        for j, (kind, x) in enumerate(args):
+            a[j].kind = kind
+            if kind == 0:
+                a[j].scalar = x
+            else:
+                a[j].buffer_id = x
+        w = C.c_uint64()
+        if lo is None:
+            N.check(L.hcl_launch(dev, kernel.encode(), a, len(args), None, None, 1, C.byref(w)))
+        else:
+            go, gs = (C.c_uint64 * 3)(lo, 0, 0), (C.c_uint64 * 3)(rows, 1, 1)
+            N.check(L.hcl_launch(dev, kernel.encode(), a, len(args), go, gs, 1, C.byref(w)))
+
+    x0 = np.full(v, np.float32(1.0 / v), np.float32)
+    try:
+        for d in range(P):
+            for name, arr in (("rp", rp), ("col", ci), ("units", units), ("long", long_rows), ("deg", deg),
+                              ("x0", x0), ("x1", np.zeros(v, np.float32)), ("xs", np.zeros(v, np.float32)),
+                              ("dsum", np.zeros(1, np.uint64))):
+                put(d, name, arr)
+        for d in range(P):  # peers' next vectors, for each parity
+            for i in range(2):
+                put(d, f"peers{i}", np.array([ptr(e, f"x{i}") for e in range(P) if e != d], np.uint64))
+        I_, O_, S_ = 1, 2, 0
+        cur = 0
+        for _ in range(20):
+            for d in range(P):
+                launch(d, "pagerank_prep", [(I_, bid(d, f"x{cur}")), (I_, bid(d, "deg")), (O_, bid(d, "dsum")),
+                                            (O_, bid(d, "xs")), (S_, v)])
+                nxt = 1 - cur
+                launch(d, "pagerank_step_exchange",
+                       [(I_, bid(d, "rp")), (I_, bid(d, "col")), (I_, bid(d, "units")), (I_, bid(d, "long")),
+                        (I_, bid(d, "xs")), (I_, bid(d, "dsum")), (O_, bid(d, f"x{nxt}")), (S_, v), (S_, 0),
+                        (S_, len(units)), (S_, n_long), (S_, 64), (I_, bid(d, f"peers{nxt}")), (S_, P - 1)],
+                       lo=bounds[d], rows=bounds[d + 1] - bounds[d])
+            for d in range(P):  # the barrier: every device's stores have landed
+                N.check(L.hcl_finish(d, None))
+            cur = 1 - cur
+        want = O.pagerank(rp, ci, val, deg, 20, b200_order=True)
+        for d in range(P):
+            got = np.empty(v, np.float32)
+            N.check(L.hcl_buffer_read(d, bid(d, f"x{cur}"), 0, got.ctypes.data, v * 4))
+            assert got.tobytes() == want.tobytes(), d
+    finally:
+        for (d, _), i in ids.items():
+            L.hcl_buffer_release(d, i)
