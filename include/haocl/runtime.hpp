@@ -287,6 +287,16 @@ class HostContext {
   void enqueue_allreduce_sum_i64(Handle queue, Handle buffer);
   // Root's bytes to every rank (GEMM B).
   void enqueue_broadcast(Handle queue, Handle buffer, int root);
+  // Fused-exchange plumbing (one process per GPU): back
+  // `buffer` on the queue's device with IPC-exportable memory and return its
+  // 64-byte handle; map a peer rank's handle on the queue's device and return
+  // the mapped device address (kernels such as pagerank_step_exchange store
+  // into it over NVLink); a stream-ordered barrier across the communicator,
+  // after which `completed` buffers are whole on the queue's device (the
+  // peers' stores filled the rows this rank did not write).
+  std::vector<uint8_t> share_buffer(Handle queue, Handle buffer);
+  uint64_t open_shared_buffer(Handle queue, const std::vector<uint8_t>& ipc_handle, uint64_t bytes);
+  void enqueue_barrier(Handle queue, const std::vector<Handle>& completed = {});
 
   std::pair<int, Handle> submit_task(const KernelTask& task);
   Handle launch_task(Handle queue, const KernelTask& task);

@@ -73,6 +73,15 @@ int hcl_ctx_init_collectives(hcl_context* ctx, uint64_t queue, int rank, int nra
 int hcl_ctx_enqueue_allgather(hcl_context* ctx, uint64_t queue, uint64_t buffer, const uint64_t* bounds, int nranks);
 int hcl_ctx_enqueue_allreduce_sum_i64(hcl_context* ctx, uint64_t queue, uint64_t buffer);
 int hcl_ctx_enqueue_broadcast(hcl_context* ctx, uint64_t queue, uint64_t buffer, int root);
+/* Fused-exchange plumbing (HostContext::share_buffer / open_shared_buffer /
+ * enqueue_barrier): 64-byte CUDA IPC handle of a buffer backed on the queue's
+ * device; a peer's handle mapped on the queue's device (its device address);
+ * a stream-ordered barrier across the NCCL communicator after which the
+ * `completed` buffers count as whole on the queue's device. */
+int hcl_ctx_share_buffer(hcl_context* ctx, uint64_t queue, uint64_t buffer, uint8_t* ipc_handle);
+int hcl_ctx_open_shared_buffer(hcl_context* ctx, uint64_t queue, const uint8_t* ipc_handle, uint64_t bytes,
+                               uint64_t* device_address);
+int hcl_ctx_enqueue_barrier(hcl_context* ctx, uint64_t queue, const uint64_t* completed, int n);
 /* The row boundaries (nqueues+1) the partitioned launch would use. */
 int hcl_ctx_partition_plan(hcl_context* ctx, uint64_t kernel, const uint64_t global[3], const uint64_t* queues,
                            int nqueues, const uint64_t* weights, uint64_t* bounds);

@@ -450,6 +450,7 @@ int hcl_buffer_alloc_shared(int dev, uint64_t id, uint64_t bytes, uint8_t* ipc_h
     a.mem = 1;
     HCL_CUDA(cudaMalloc(reinterpret_cast<void**>(&a.ptr), bytes));
     HCL_CUDA(cudaMemsetAsync(a.ptr, 0, bytes, d.stream));
+    HCL_CUDA(cudaStreamSynchronize(d.stream));  // zeroed before any peer can store into it
     cudaIpcMemHandle_t h;
     HCL_CUDA(cudaIpcGetMemHandle(&h, a.ptr));
     std::memcpy(ipc_handle, &h, sizeof(h));

@@ -123,6 +123,7 @@ struct HostContext::Impl {
   TimingBreakdown timings;
 
   uint64_t new_id() { return next_handle.fetch_add(1); }
+  std::vector<std::pair<int, uint64_t>> mapped;  // (device, id) of IPC-mapped peer buffers
 
   Handle new_event() {
     uint64_t id = new_id();
@@ -516,6 +517,7 @@ HostContext::HostContext(HostContext&&) noexcept = default;
 HostContext& HostContext::operator=(HostContext&&) noexcept = default;
 HostContext::~HostContext() {
   if (!impl_) return;
+  for (auto& [dev, id] : impl_->mapped) hcl_buffer_release(dev, id);
   for (auto& [id, b] : impl_->buffers)
     for (auto& [g, p] : b.pieces)
       if (p.allocated) hcl_buffer_release(impl_->dev_index(g), id);
@@ -824,6 +826,47 @@ void HostContext::enqueue_allgather(Handle queue, Handle buffer, const std::vect
   check(hcl_allgatherv(impl_->dev_index(q.gid), buffer.id, bounds.data()));
   Impl::set_valid(p, bounds.front(), bounds.back() - bounds.front());
   impl_->add_transfer(&q, ms_since(started));
+}
+
+std::vector<uint8_t> HostContext::share_buffer(Handle queue, Handle buffer) {
+  std::lock_guard lock(impl_->mu);
+  Impl::QueueRec& q = impl_->queue(queue.id);
+  Impl::BufferRec& b = impl_->buffer(buffer.id);
+  std::vector<uint8_t> h(64);
+  check(hcl_buffer_alloc_shared(impl_->dev_index(q.gid), buffer.id, b.size, h.data()));
+  Impl::Piece& p = b.pieces[q.gid];  // zero-filled, whole buffer, nothing written yet
+  p.allocated = true;
+  p.alloc_first = 0;
+  p.alloc_bytes = b.size;
+  p.valid_bytes = 0;
+  impl_->trace.record({q.gid, "alloc_buffer", buffer.id});
+  return h;
+}
+
+uint64_t HostContext::open_shared_buffer(Handle queue, const std::vector<uint8_t>& ipc_handle, uint64_t bytes) {
+  std::lock_guard lock(impl_->mu);
+  Impl::QueueRec& q = impl_->queue(queue.id);
+  if (ipc_handle.size() < 64) fail(ErrorCode::argument, "open_shared_buffer: IPC handles are 64 bytes");
+  const int dev = impl_->dev_index(q.gid);
+  const uint64_t id = impl_->new_id() | (1ull << 61);  // device-level mapping, outside the buffer table
+  check(hcl_buffer_open_shared(dev, id, ipc_handle.data(), bytes));
+  impl_->mapped.push_back({dev, id});
+  void* p = nullptr;
+  check(hcl_buffer_device_ptr(dev, id, &p, nullptr, nullptr));
+  return reinterpret_cast<uint64_t>(p);
+}
+
+void HostContext::enqueue_barrier(Handle queue, const std::vector<Handle>& completed) {
+  std::lock_guard lock(impl_->mu);
+  Impl::QueueRec& q = impl_->queue(queue.id);
+  impl_->trace.record({q.gid, "barrier", 0});
+  check(hcl_nccl_barrier(impl_->dev_index(q.gid)));
+  for (const Handle& h : completed) {
+    Impl::BufferRec& b = impl_->buffer(h.id);
+    Impl::Piece& p = impl_->ensure_alloc(h.id, b, q.gid, 0, b.size);
+    Impl::set_valid(p, 0, b.size);
+    Impl::invalidate_others(b, q.gid, 0, b.size);
+  }
 }
 
 void HostContext::enqueue_allreduce_sum_i64(Handle queue, Handle buffer) {
@@ -1155,6 +1198,26 @@ int hcl_ctx_enqueue_allgather(hcl_context* ctx, uint64_t queue, uint64_t buffer,
 }
 int hcl_ctx_enqueue_allreduce_sum_i64(hcl_context* ctx, uint64_t queue, uint64_t buffer) {
   return ctx_guarded([&] { ctx->ctx.enqueue_allreduce_sum_i64(H(HandleKind::queue, queue), H(HandleKind::buffer, buffer)); });
+}
+int hcl_ctx_share_buffer(hcl_context* ctx, uint64_t queue, uint64_t buffer, uint8_t* ipc_handle) {
+  return ctx_guarded([&] {
+    auto h = ctx->ctx.share_buffer(H(HandleKind::queue, queue), H(HandleKind::buffer, buffer));
+    std::memcpy(ipc_handle, h.data(), h.size());
+  });
+}
+int hcl_ctx_open_shared_buffer(hcl_context* ctx, uint64_t queue, const uint8_t* ipc_handle, uint64_t bytes,
+                               uint64_t* device_address) {
+  return ctx_guarded([&] {
+    *device_address = ctx->ctx.open_shared_buffer(H(HandleKind::queue, queue),
+                                                  std::vector<uint8_t>(ipc_handle, ipc_handle + 64), bytes);
+  });
+}
+int hcl_ctx_enqueue_barrier(hcl_context* ctx, uint64_t queue, const uint64_t* completed, int n) {
+  return ctx_guarded([&] {
+    std::vector<Handle> bs;
+    for (int i = 0; i < n; ++i) bs.push_back(H(HandleKind::buffer, completed[i]));
+    ctx->ctx.enqueue_barrier(H(HandleKind::queue, queue), bs);
+  });
 }
 int hcl_ctx_enqueue_broadcast(hcl_context* ctx, uint64_t queue, uint64_t buffer, int root) {
   return ctx_guarded([&] { ctx->ctx.enqueue_broadcast(H(HandleKind::queue, queue), H(HandleKind::buffer, buffer), root); });

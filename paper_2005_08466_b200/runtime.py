@@ -233,6 +233,28 @@ class HostContext:
     def enqueue_allreduce_sum_i64(self, queue: Handle, buffer: Handle) -> None:
         check(self._L.hcl_ctx_enqueue_allreduce_sum_i64(self._ctx, queue.id, buffer.id))
 
+    def share_buffer(self, queue: Handle, buffer: Handle) -> bytes:
+        """Back `buffer` on the queue's device with IPC-exportable memory (zero-filled);
+        returns its 64-byte CUDA IPC handle for the other ranks (fused exchange kernels)."""
+        h = (C.c_uint8 * 64)()
+        check(self._L.hcl_ctx_share_buffer(self._ctx, queue.id, buffer.id, h))
+        return bytes(h)
+
+    def open_shared_buffer(self, queue: Handle, ipc_handle: bytes, nbytes: int) -> int:
+        """Map a peer rank's shared buffer on the queue's device; returns its device
+        address (what pagerank_step_exchange's peers list holds)."""
+        h = (C.c_uint8 * 64)(*ipc_handle[:64])
+        addr = C.c_uint64()
+        check(self._L.hcl_ctx_open_shared_buffer(self._ctx, queue.id, h, nbytes, C.byref(addr)))
+        return addr.value
+
+    def enqueue_barrier(self, queue: Handle, completed: Sequence[Handle] = ()) -> None:
+        """Stream-ordered barrier across the NCCL communicator (init_collectives);
+        afterwards the `completed` buffers count as whole on the queue's device
+        (peer ranks stored the rows this rank did not write)."""
+        ids = (C.c_uint64 * max(1, len(completed)))(*[b.id for b in completed])
+        check(self._L.hcl_ctx_enqueue_barrier(self._ctx, queue.id, ids, len(completed)))
+
     def enqueue_broadcast(self, queue: Handle, buffer: Handle, root: int) -> None:
         check(self._L.hcl_ctx_enqueue_broadcast(self._ctx, queue.id, buffer.id, root))
 
