@@ -517,50 +517,75 @@ class PageRankW(Workload):
             uid = d.bcast_bytes(HostContext.nccl_unique_id() if d.rank == 0 else None)
             ctx.init_collectives(q, d.rank, d.world, uid)
         self.byte_bounds = [4 * b for b in self.bounds]
-        # N > 1: the step kernel itself stores every row into all ranks' next rank
-        # vectors over NVLink (IPC-mapped peer buffers) and a stream-ordered barrier
-        # replaces the allgather (BENCH_PR_EXCHANGE=0: NCCL allgather after the step)
-        self.exchange = d.world > 1 and self.implicit and os.environ.get("BENCH_PR_EXCHANGE", "1") == "1"
-        if self.exchange:
-            mine = b"".join(ctx.share_buffer(q, self.b_x[i]) for i in range(2))
-            handles = d.allgather_bytes(mine)
+        # fused step (default with implicit values, any N): pagerank_step_exchange writes
+        # the rank's rows of x', the next gather input xs' = fl(1/outdeg) x' for those rows
+        # into this rank's AND every peer's xs' (IPC-mapped peer buffers, NVLink stores)
+        # and its dangling partial; an allreduce of the dangling sums is the only
+        # collective (and the step barrier). No prep pass, no rank-vector allgather.
+        # BENCH_PR_EXCHANGE=0: prep + step + NCCL allgather (the unfused baseline).
+        self.fused = self.implicit and os.environ.get("BENCH_PR_EXCHANGE", "1") == "1"
+        if self.fused:
+            self.b_xs2 = [mk(self.v * 4), mk(self.v * 4)]
+            handles = d.allgather_bytes(b"".join(ctx.share_buffer(q, b) for b in self.b_xs2)) if d.world > 1 else None
+            self.b_dsum2 = [mk(8), mk(8)]
             self.b_peers, self.k_stepx = [], [ctx.create_kernel(prog, "pagerank_step_exchange") for _ in range(2)]
             for i in range(2):
-                addrs = np.array([ctx.open_shared_buffer(q, handles[r][64 * i:64 * (i + 1)], self.v * 4)
-                                  for r in range(d.world) if r != d.rank], np.uint64)
-                bp = mk(addrs.nbytes)
-                ctx.enqueue_write_buffer(q, bp, addrs)
+                addrs = [ctx.open_shared_buffer(q, handles[r][64 * i:64 * (i + 1)], self.v * 4)
+                         for r in range(d.world) if r != d.rank] if d.world > 1 else []
+                arr = np.array(addrs or [0], np.uint64)
+                bp = mk(arr.nbytes)
+                ctx.enqueue_write_buffer(q, bp, arr)
                 self.b_peers.append(bp)
-            for i in range(2):  # reads xs (from x[i]), writes x[1-i] here and on every peer
-                for j, a in enumerate([self.b_rp, self.b_col, self.b_u, self.b_l, self.b_xs, self.b_dsum,
-                                       self.b_x[1 - i], self.v, p0, len(units), n_long, wn, self.b_peers[1 - i],
-                                       d.world - 1]):
+            for i in range(2):  # reads xs[i], dsum[i]; writes x rows, xs[1-i] (here + peers), dsum[1-i]
+                for j, a in enumerate([self.b_rp, self.b_col, self.b_u, self.b_l, self.b_xs2[i], self.b_dsum2[i],
+                                       self.b_x[0], self.v, p0, len(units), n_long, wn, self.b_peers[1 - i],
+                                       d.world - 1, self.b_deg, self.b_xs2[1 - i], self.b_dsum2[1 - i]]):
                     ctx.set_kernel_arg(self.k_stepx[i], j, a)
+            self.k_prep0 = ctx.create_kernel(prog, "pagerank_prep")  # x0 -> xs[0], dsum[0]
+            for j, a in enumerate([self.b_x[0], self.b_deg, self.b_dsum2[0], self.b_xs2[0], self.v]):
+                ctx.set_kernel_arg(self.k_prep0, j, a)
         import torch
 
         self.x0 = torch.full((self.v,), 1.0 / self.v, dtype=torch.float32).pin_memory()
         self.r_host = torch.empty(self.rows, dtype=torch.float32, pin_memory=True)
+        # parity guard (the full 20-iteration oracle check is in tests/): one step's rows
+        # sum to 1 over the ranks; the fused step equals prep + step + allgather bit for bit
+        fused = self.fused
+        self.fused = False
         self.reset()
-        # parity guard: one iteration vs the restated-order oracle is in tests/; here a sum check
         self.step()
         ctx.finish(q)
-        x = ctx.enqueue_read_buffer(q, self.b_x[self.cur]).view(np.float32).copy()
-        self.check = float(abs(x.astype(np.float64).sum() - 1.0))
-        if self.exchange:  # the fused exchange must leave the allgather's bytes on every rank
-            self.exchange = False
+        ref = ctx.enqueue_read_buffer(q, self.b_x[self.cur]).view(np.float32).copy()
+        self.check = float(abs(d.allsum(float(ref[lo:hi].astype(np.float64).sum())) - 1.0))
+        self.fused = fused
+        if self.fused:
             d.barrier()
             self.reset()
             self.step()
             ctx.finish(q)
-            ref = ctx.enqueue_read_buffer(q, self.b_x[self.cur]).view(np.float32)
-            assert ref.tobytes() == x.tobytes(), "pagerank_step_exchange differs from step + allgather"
-            self.exchange = True
+            d.barrier()
+            x = ctx.enqueue_read_buffer(q, self.b_x[0], offset=lo * 4, length=self.rows * 4).view(np.float32)
+            assert x.tobytes() == ref[lo:hi].tobytes(), "pagerank_step_exchange rows differ from step + allgather"
+            # its xs' must be prep(x') over all rows (the peers' stores included)
+            xs_f = ctx.enqueue_read_buffer(q, self.b_xs2[self.cur]).view(np.float32).copy()
+            ctx.enqueue_write_buffer(q, self.b_x[1], ref)
+            ctx.set_kernel_arg(self.k_prep, 0, self.b_x[1])
+            ctx.enqueue_ndrange_kernel(q, self.k_prep)
+            ctx.finish(q)
+            xs_r = ctx.enqueue_read_buffer(q, self.b_xs).view(np.float32)
+            assert xs_r.tobytes() == xs_f.tobytes(), "pagerank_step_exchange xs' differs from prep(allgathered x')"
             d.barrier()
         self.reset()
 
     def reset(self):
-        self.ctx.enqueue_write_buffer(self.q, self.b_x[0], self.x0)
+        ctx, q = self.ctx, self.q
+        if self.fused:
+            ctx.finish(q)  # the previous step's collective: no peer store is still landing
+            self.dist.barrier()
+        ctx.enqueue_write_buffer(q, self.b_x[0], self.x0)
         self.cur = 0
+        if self.fused:
+            ctx.enqueue_ndrange_kernel(q, self.k_prep0)
 
     def spmv(self):
         k = self.k_stepi[self.cur] if self.implicit else self.k_step[self.cur]
@@ -568,19 +593,21 @@ class PageRankW(Workload):
 
     def step(self):
         ctx, q = self.ctx, self.q
+        if self.fused:
+            ctx.enqueue_ndrange_range(q, self.k_stepx[self.cur], (self.v, 1, 1), 1, self.lo, self.rows)
+            if self.dist.world > 1:  # the one collective; the next step's kernel waits on it (reads dsum')
+                ctx.enqueue_allreduce_sum_i64(q, self.b_dsum2[1 - self.cur])
+            self.cur = 1 - self.cur
+            return
         if self.implicit:
             ctx.set_kernel_arg(self.k_prep, 0, self.b_x[self.cur])
             ctx.enqueue_ndrange_kernel(q, self.k_prep)
         else:
             ctx.set_kernel_arg(self.k_dang, 0, self.b_x[self.cur])
             ctx.enqueue_ndrange_kernel(q, self.k_dang)
-        if self.exchange:
-            ctx.enqueue_ndrange_range(q, self.k_stepx[self.cur], (self.v, 1, 1), 1, self.lo, self.rows)
-            ctx.enqueue_barrier(q, [self.b_x[1 - self.cur]])
-        else:
-            self.spmv()
-            if self.dist.world > 1:
-                ctx.enqueue_allgather(q, self.b_x[1 - self.cur], self.byte_bounds)
+        self.spmv()
+        if self.dist.world > 1:
+            ctx.enqueue_allgather(q, self.b_x[1 - self.cur], self.byte_bounds)
         self.cur = 1 - self.cur
 
     def dominant(self):
@@ -594,8 +621,11 @@ class PageRankW(Workload):
     def e2e_step(self):
         # one iteration with the rank vector from host and the rank's slice back
         ctx, q = self.ctx, self.q
-        if self.exchange:  # the previous step's barrier: no peer store is still landing in b_x[cur]
-            ctx.finish(q)
+        if self.fused:
+            self.reset()  # x0 from host (+ its gather input)
+            self.step()
+            ctx.enqueue_read_buffer(q, self.b_x[0], offset=self.lo * 4, length=self.rows * 4, out=self.r_host)
+            return
         ctx.enqueue_write_buffer(q, self.b_x[self.cur], self.x0)
         self.step()
         ctx.enqueue_read_buffer(q, self.b_x[self.cur], offset=self.lo * 4, length=self.rows * 4, out=self.r_host)
@@ -611,7 +641,9 @@ class PageRankW(Workload):
 
     def config(self):
         return {"workload": f"PageRank iteration (C3): R-MAT scale {self.scale}, {self.e} edges, int32/fp32 pull CSR, "
-                            f"nnz-balanced rows over {self.dist.world} rank(s), rank allgather",
+                            f"nnz-balanced rows over {self.dist.world} rank(s), " + (
+                                "fused step: x' rows + next gather input xs' stored to every rank over NVLink, "
+                                "dangling-sum allreduce" if self.fused else "prep + step + rank allgather"),
                 "values": "implicit: val = 1/outdeg(src) folded into xs by pagerank_prep (bit-identical products); "
                           "bytes are counted per the CSR definition (nnz*8 + ...)" if self.implicit
                 else "explicit fp32 value stream",

@@ -99,18 +99,26 @@ __device__ __forceinline__ void pr_store(float* __restrict__ y, int r, int lo, f
     y[r - lo] = s;
 }
 
-// Fused exchange (pagerank_step_exchange): every row result is also stored
-// into the next-iteration rank vector of each peer device (NVLink stores into
-// peer / IPC-mapped memory), replacing the allgather that would follow.
+// Fused step (pagerank_step_exchange): besides x'[r], each row also yields the
+// next iteration's gather input xs'[r] = fl(1/outdeg(r)) * x'[r] (what
+// pagerank_prep computes, bit for bit), stored into this device's xs' and
+// into every peer's xs' (NVLink stores into peer / IPC-mapped memory), and
+// dangling rows add x'[r] to dsum' (2^-56 fixed point, order-free). The
+// separate prep pass and the rank-vector allgather disappear; an allreduce
+// of dsum' is the only collective, and it doubles as the step barrier.
 constexpr int PR_MAX_PEERS = 7;
 struct Fanout {
   float* p[PR_MAX_PEERS];
   int n;
+  float* xs;            // this device's xs'
+  const int* outdeg;
 };
 
-__device__ __forceinline__ Fanout load_fanout(const unsigned long long* peers, int n) {
+__device__ __forceinline__ Fanout load_fanout(const unsigned long long* peers, int n, float* xs, const int* outdeg) {
   Fanout f;
   f.n = n;
+  f.xs = xs;
+  f.outdeg = outdeg;
 #pragma unroll
   for (int k = 0; k < PR_MAX_PEERS; ++k) f.p[k] = k < n ? reinterpret_cast<float*>(__ldg(peers + k)) : nullptr;
   return f;
@@ -118,14 +126,26 @@ __device__ __forceinline__ Fanout load_fanout(const unsigned long long* peers, i
 
 template <bool UPDATE, bool XCH>
 __device__ __forceinline__ void pr_store_x(float* __restrict__ y, int r, int lo, float s, const Update& u,
-                                           const Fanout& f) {
+                                           const Fanout& f, unsigned long long& dang) {
   pr_store<UPDATE>(y, r, lo, s, u);
   if constexpr (XCH) {
     const float v = y[r - lo];
+    const int d = __ldg(f.outdeg + r);
+    const float xs = d ? __fmul_rn(__fdiv_rn(1.0f, static_cast<float>(d)), v) : 0.f;
+    f.xs[r] = xs;
 #pragma unroll
     for (int k = 0; k < PR_MAX_PEERS; ++k)
-      if (k < f.n) f.p[k][r] = v;
+      if (k < f.n) f.p[k][r] = xs;
+    if (d == 0) dang += static_cast<unsigned long long>(__float2ll_rz(__fmul_rn(v, 0x1p56f)));
   }
+}
+
+// end of an exchange kernel: the block's dangling partial into dsum', and the
+// peer stores made visible system-wide before the allreduce that follows
+__device__ __forceinline__ void pr_exchange_flush(unsigned long long dang, unsigned long long* dsum_next) {
+  for (int o = 16; o > 0; o >>= 1) dang += __shfl_xor_sync(0xffffffffu, dang, o);
+  if ((threadIdx.x & 31) == 0 && dang) atomicAdd(dsum_next, dang);
+  __threadfence_system();
 }
 
 template <bool UPDATE>
@@ -175,13 +195,16 @@ __global__ void __launch_bounds__(PR_T) pr_units_kernel(const int* __restrict__ 
                                                         const unsigned long long* __restrict__ dsum,
                                                         float* __restrict__ y, int lo, int hi, float base, float damp,
                                                         float inv_v, int warp_nnz, float* __restrict__ chunk_tot,
-                                                        const unsigned long long* __restrict__ peers, int n_peers) {
+                                                        const unsigned long long* __restrict__ peers, int n_peers,
+                                                        const int* __restrict__ outdeg, float* __restrict__ xs_next,
+                                                        unsigned long long* __restrict__ dsum_next) {
   extern __shared__ float prod_all[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   float* prod = prod_all + warp * warp_nnz;
   const Update upd = pr_update<UPDATE>(dsum, base, damp, inv_v);
   Fanout fo{};
-  if constexpr (XCH) fo = load_fanout(peers, n_peers);
+  unsigned long long dang = 0;
+  if constexpr (XCH) fo = load_fanout(peers, n_peers, xs_next, outdeg);
   // units overlapping [lo, hi): row1 > lo and row0 < hi (both monotone in u)
   int a = 0, b = n_units;
   while (a < b) {
@@ -229,7 +252,7 @@ __global__ void __launch_bounds__(PR_T) pr_units_kernel(const int* __restrict__ 
       if (in && len <= 32) {
         float s = 0.f;
         for (int q = q0; q < q0 + len; ++q) s = __fadd_rn(s, prod[q]);
-        pr_store_x<UPDATE, XCH>(y, r, lo, s, upd, fo);
+        pr_store_x<UPDATE, XCH>(y, r, lo, s, upd, fo, dang);
       }
       unsigned mask = __ballot_sync(0xffffffffu, in && len > 32);
       while (mask) {
@@ -239,12 +262,12 @@ __global__ void __launch_bounds__(PR_T) pr_units_kernel(const int* __restrict__ 
         float v = 0.f;
         for (int q = lane; q < rlen; q += 32) v = __fadd_rn(v, prod[rq0 + q]);
         v = butterfly(v);
-        if (lane == 0) pr_store_x<UPDATE, XCH>(y, rb + j, lo, v, upd, fo);
+        if (lane == 0) pr_store_x<UPDATE, XCH>(y, rb + j, lo, v, upd, fo, dang);
       }
     }
     __syncwarp();
   }
-  if constexpr (XCH) __threadfence_system();  // peer stores visible before the barrier that follows
+  if constexpr (XCH) pr_exchange_flush(dang, dsum_next);
 }
 
 // long rows: fold the chunk totals in chunk order
@@ -252,8 +275,10 @@ template <bool UPDATE, bool XCH = false>
 __global__ void pr_fixup_kernel(const int* __restrict__ long_rows, int n_long, const float* __restrict__ chunk_tot,
                                 const unsigned long long* __restrict__ dsum, float* __restrict__ y, int lo, int hi,
                                 float base, float damp, float inv_v, const unsigned long long* __restrict__ peers,
-                                int n_peers) {
+                                int n_peers, const int* __restrict__ outdeg, float* __restrict__ xs_next,
+                                unsigned long long* __restrict__ dsum_next) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned long long dang = 0;
   if (i < n_long) {
     const int row = long_rows[3 * i];
     if (row >= lo && row < hi) {
@@ -261,11 +286,11 @@ __global__ void pr_fixup_kernel(const int* __restrict__ long_rows, int n_long, c
       float total = chunk_tot[u0];
       for (int c = 1; c < nc; ++c) total = __fadd_rn(total, chunk_tot[u0 + c]);
       Fanout fo{};
-      if constexpr (XCH) fo = load_fanout(peers, n_peers);
-      pr_store_x<UPDATE, XCH>(y, row, lo, total, pr_update<UPDATE>(dsum, base, damp, inv_v), fo);
+      if constexpr (XCH) fo = load_fanout(peers, n_peers, xs_next, outdeg);
+      pr_store_x<UPDATE, XCH>(y, row, lo, total, pr_update<UPDATE>(dsum, base, damp, inv_v), fo, dang);
     }
   }
-  if constexpr (XCH) __threadfence_system();
+  if constexpr (XCH) pr_exchange_flush(dang, dsum_next);
 }
 
 // validated (row_ptr version, slice) -> row_ptr[lo], row_ptr[hi]
@@ -337,12 +362,25 @@ uint64_t launch_pr(LaunchCtx& c) {
   }
   const unsigned long long* peers = nullptr;
   int n_peers = 0;
-  if (XCH) {  // peers buffer (device addresses of the peers' next rank vectors) and their count
+  const int* outdeg = nullptr;
+  float* xs_next = nullptr;
+  unsigned long long* dsum_next = nullptr;
+  if (XCH) {  // peers (device addresses of the peers' xs'), their count, outdeg, xs', dsum'
     n_peers = static_cast<int>(scalar_arg(c, s0 + 6, what));
     const BufView& PB = buffer_arg(c, s0 + 5, what);
     if (n_peers < 0 || n_peers > PR_MAX_PEERS || PB.first_byte != 0 || PB.bytes < static_cast<uint64_t>(n_peers) * 8)
       fail(ErrorCode::argument, std::string(what) + ": peers must list 0..7 device addresses");
     peers = reinterpret_cast<const unsigned long long*>(PB.ptr);
+    const BufView& OD = buffer_arg(c, s0 + 7, what);
+    const BufView& XN = buffer_arg(c, s0 + 8, what);
+    const BufView& DN = buffer_arg(c, s0 + 9, what);
+    if (OD.first_byte != 0 || OD.bytes != static_cast<uint64_t>(v) * 4 || XN.first_byte != 0 ||
+        XN.bytes != static_cast<uint64_t>(v) * 4 || DN.bytes != 8)
+      fail(ErrorCode::argument, std::string(what) + ": outdeg and xs' must hold V elements, dsum' one uint64");
+    outdeg = reinterpret_cast<const int*>(OD.ptr);
+    xs_next = reinterpret_cast<float*>(XN.ptr);
+    dsum_next = reinterpret_cast<unsigned long long*>(DN.ptr);
+    HCL_CUDA(cudaMemsetAsync(dsum_next, 0, 8, c.stream));
   }
   uint64_t lo, rows;
   sub_range(c, static_cast<uint64_t>(v), lo, rows, what);
@@ -374,12 +412,12 @@ uint64_t launch_pr(LaunchCtx& c) {
                                        reinterpret_cast<const int4*>(U.ptr), static_cast<int>(n_units),
                                        reinterpret_cast<const float*>(X.ptr), dsum, y, static_cast<int>(lo),
                                        static_cast<int>(lo + rows), base, damp, inv_v, static_cast<int>(warp_nnz),
-                                       chunk_tot, peers, n_peers);
+                                       chunk_tot, peers, n_peers, outdeg, xs_next, dsum_next);
   HCL_LAUNCHED();
   if (n_long) {
     pr_fixup_kernel<UPDATE, XCH><<<static_cast<unsigned>(ceil_div(n_long, 128)), 128, 0, c.stream>>>(
         reinterpret_cast<const int*>(L.ptr), static_cast<int>(n_long), chunk_tot, dsum, y, static_cast<int>(lo),
-        static_cast<int>(lo + rows), base, damp, inv_v, peers, n_peers);
+        static_cast<int>(lo + rows), base, damp, inv_v, peers, n_peers, outdeg, xs_next, dsum_next);
     HCL_LAUNCHED();
   }
   return 2ull * static_cast<uint64_t>(rp[1] - rp[0]);
@@ -464,11 +502,12 @@ void register_graph(std::vector<KernelDef>& r) {
   r.push_back({"b200", "pagerank_prep", {I, I, O, O, S}, {P, P, P, P, N}, launch_pr_prep, nullptr, nullptr});
   r.push_back({"b200", "pagerank_step_implicit", {I, I, I, I, I, I, O, S, S, S, S, S},
                {P, P, P, P, P, P, X, N, N, N, N, N}, launch_pr<true, true>, nullptr, rows_pr_imp});
-  // the implicit step fused with the rank-vector exchange: also stores each row into the
-  // peers' x' (peers = device addresses, uint64[n_peers]):
-  // row_ptr col units long_rows xs dsum x' | V nnz_off n_units n_long warp_nnz | peers n_peers
-  r.push_back({"b200", "pagerank_step_exchange", {I, I, I, I, I, I, O, S, S, S, S, S, I, S},
-               {P, P, P, P, P, P, X, N, N, N, N, N, P, N}, launch_pr<true, true, true>, nullptr, rows_pr_imp});
+  // the implicit step fused with the next prep and the exchange: x' rows, xs' rows here and on
+  // every peer (peers = device addresses of their xs', uint64[n_peers]), dangling partial dsum':
+  // row_ptr col units long_rows xs dsum x' | V nnz_off n_units n_long warp_nnz | peers n_peers outdeg xs' dsum'
+  r.push_back({"b200", "pagerank_step_exchange", {I, I, I, I, I, I, O, S, S, S, S, S, I, S, I, O, O},
+               {P, P, P, P, P, P, X, N, N, N, N, N, P, N, P, P, P}, launch_pr<true, true, true>, nullptr,
+               rows_pr_imp});
 }
 
 }  // namespace hcl

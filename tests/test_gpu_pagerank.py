@@ -220,14 +220,15 @@ def test_pagerank_full_c3(ctx, queues):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("P", [2, 4])
-def test_step_exchange_fused_allgather(ctx, queues, graph, P):
+@pytest.mark.parametrize("P", [1, 2, 4])
+def test_step_exchange_fused(ctx, queues, graph, P):
     """pagerank_step_exchange: each device computes its nnz-balanced row range
-    and stores every row into its own AND its peers' next rank vectors (here
-    logical devices of one process; across processes the peers are IPC-mapped
-    buffers, bench.py). After 20 iterations with only a per-iteration barrier,
-    every device holds the full rank vector, bit-identical to the
-    restated-order oracle -- no allgather ran."""
+    of x' and, for those rows, the next gather input xs' = fl(1/outdeg) x'
+    (what pagerank_prep computes) into its own AND its peers' xs' (here logical
+    devices of one process; across processes IPC-mapped peer buffers, bench.py),
+    plus its dangling partial. The only collective is an allreduce of the
+    dangling sums. After 20 iterations the rows are bit-identical to the
+    restated-order oracle -- no prep pass, no allgather."""
     import ctypes as C
 
     from paper_2005_08466_b200 import _native as N
@@ -265,42 +266,47 @@ def test_step_exchange_fused_allgather(ctx, queues, graph, P):
             else:
                 a[j].buffer_id = x
         w = C.c_uint64()
-        if lo is None:
-            N.check(L.hcl_launch(dev, kernel.encode(), a, len(args), None, None, 1, C.byref(w)))
-        else:
-            go, gs = (C.c_uint64 * 3)(lo, 0, 0), (C.c_uint64 * 3)(rows, 1, 1)
-            N.check(L.hcl_launch(dev, kernel.encode(), a, len(args), go, gs, 1, C.byref(w)))
+        go, gs = ((C.c_uint64 * 3)(lo, 0, 0), (C.c_uint64 * 3)(rows, 1, 1)) if lo is not None else (None, None)
+        N.check(L.hcl_launch(dev, kernel.encode(), a, len(args), go, gs, 1, C.byref(w)))
 
+    I_, O_, S_ = 1, 2, 0
     x0 = np.full(v, np.float32(1.0 / v), np.float32)
     try:
         for d in range(P):
             for name, arr in (("rp", rp), ("col", ci), ("units", units), ("long", long_rows), ("deg", deg),
-                              ("x0", x0), ("x1", np.zeros(v, np.float32)), ("xs", np.zeros(v, np.float32)),
-                              ("dsum", np.zeros(1, np.uint64))):
+                              ("x", x0), ("xs0", np.zeros(v, np.float32)), ("xs1", np.zeros(v, np.float32)),
+                              ("dsum0", np.zeros(1, np.uint64)), ("dsum1", np.zeros(1, np.uint64))):
                 put(d, name, arr)
-        for d in range(P):  # peers' next vectors, for each parity
+        for d in range(P):  # peers' xs' for each parity
             for i in range(2):
-                put(d, f"peers{i}", np.array([ptr(e, f"x{i}") for e in range(P) if e != d], np.uint64))
-        I_, O_, S_ = 1, 2, 0
+                put(d, f"peers{i}", np.array([ptr(e, f"xs{i}") for e in range(P) if e != d] or [0], np.uint64))
+            # iteration 0's gather input, once: xs0 = prep(x0), dsum0 = its dangling sum
+            launch(d, "pagerank_prep", [(I_, bid(d, "x")), (I_, bid(d, "deg")), (O_, bid(d, "dsum0")),
+                                        (O_, bid(d, "xs0")), (S_, v)])
+        devs = (C.c_int * P)(*range(P))
         cur = 0
         for _ in range(20):
+            nxt = 1 - cur
             for d in range(P):
-                launch(d, "pagerank_prep", [(I_, bid(d, f"x{cur}")), (I_, bid(d, "deg")), (O_, bid(d, "dsum")),
-                                            (O_, bid(d, "xs")), (S_, v)])
-                nxt = 1 - cur
                 launch(d, "pagerank_step_exchange",
                        [(I_, bid(d, "rp")), (I_, bid(d, "col")), (I_, bid(d, "units")), (I_, bid(d, "long")),
-                        (I_, bid(d, "xs")), (I_, bid(d, "dsum")), (O_, bid(d, f"x{nxt}")), (S_, v), (S_, 0),
-                        (S_, len(units)), (S_, n_long), (S_, 64), (I_, bid(d, f"peers{nxt}")), (S_, P - 1)],
+                        (I_, bid(d, f"xs{cur}")), (I_, bid(d, f"dsum{cur}")), (O_, bid(d, "x")), (S_, v), (S_, 0),
+                        (S_, len(units)), (S_, n_long), (S_, 64), (I_, bid(d, f"peers{nxt}")), (S_, P - 1),
+                        (I_, bid(d, "deg")), (O_, bid(d, f"xs{nxt}")), (O_, bid(d, f"dsum{nxt}"))],
                        lo=bounds[d], rows=bounds[d + 1] - bounds[d])
-            for d in range(P):  # the barrier: every device's stores have landed
+            for d in range(P):  # every device's stores have landed
                 N.check(L.hcl_finish(d, None))
-            cur = 1 - cur
+            if P > 1:  # the one collective: allreduce of the dangling partials
+                dids = (C.c_uint64 * P)(*[bid(d, f"dsum{nxt}") for d in range(P)])
+                N.check(L.hcl_collective(2, devs, P, dids, 1, 0, 0))
+            cur = nxt
         want = O.pagerank(rp, ci, val, deg, 20, b200_order=True)
+        got = np.empty(v, np.float32)
         for d in range(P):
-            got = np.empty(v, np.float32)
-            N.check(L.hcl_buffer_read(d, bid(d, f"x{cur}"), 0, got.ctypes.data, v * 4))
-            assert got.tobytes() == want.tobytes(), d
+            part = np.empty(v, np.float32)
+            N.check(L.hcl_buffer_read(d, bid(d, "x"), 0, part.ctypes.data, v * 4))
+            got[bounds[d]:bounds[d + 1]] = part[bounds[d]:bounds[d + 1]]
+        assert got.tobytes() == want.tobytes()
     finally:
         for (d, _), i in ids.items():
             L.hcl_buffer_release(d, i)
