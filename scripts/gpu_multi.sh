@@ -3,7 +3,7 @@
 mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1
 N=${NGPU:-2}
-timeout -s KILL 900 python -m pytest tests -q -m gpu -x > gpurun_out/multi_tests.log 2>&1; echo tests=$?
+timeout -s KILL 1500 python -m pytest tests -q -m gpu -x > gpurun_out/multi_tests.log 2>&1; echo tests=$?
 TR="python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 29511"
 timeout -s KILL 600 $TR bench.py --gpus $N --steps 20 --warmup 5 > gpurun_out/multi_gemm.json 2> gpurun_out/multi_gemm.err; echo gemm=$?
 timeout -s KILL 600 $TR bench.py --gpus $N --workload pagerank --steps 10 --warmup 3 > gpurun_out/multi_pr.json 2> gpurun_out/multi_pr.err; echo pr=$?
