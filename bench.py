@@ -201,6 +201,19 @@ class Workload:
     def __init__(self, args, dist: Dist):
         self.args, self.dist = args, dist
 
+    # dram__bytes_read.sum + dram__bytes_write.sum of the dominant kernel from one
+    # `ncu --set full` capture of this workload at N=1 (profiles/ncu_traffic.json);
+    # per-launch traffic at other N (or other kernels) is not measured -> null
+    traffic_key = None
+
+    def traffic(self):
+        prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        if self.dist.world != 1 or not self.traffic_key or not os.path.exists(prof):
+            return None
+        with open(prof) as f:
+            e = json.load(f).get(self.traffic_key)
+        return e.get("dram_bytes_per_launch") if e else None
+
     # device handles of the runtime (set in setup)
     def stream(self):
         from paper_2005_08466_b200 import _native as N
@@ -368,6 +381,7 @@ class GemmF32(Workload):
 
         self.S = S = int(os.environ.get("BENCH_GEMM_F32_S", self.S))
         self.kernel = os.environ.get("BENCH_GEMM_F32_KERNEL", "gemm_f32")
+        self.traffic_key = f"{self.kernel}_{S}"
         self.ctx = ctx = HostContext([self.dist.local])
         self.q = q = ctx.create_queue(0)
         self.a_host = torch.empty(S * S, dtype=torch.float32, pin_memory=True)
@@ -428,9 +442,6 @@ class GemmF32(Workload):
         cfg = "C1" if self.S == 1024 else "C2 fp32"
         return {"workload": f"fp32 GEMM {self.S}^3 ({cfg}) via the host API on one device ({self.kernel})",
                 "replicas": self.dist.world, "normwise_err": self.check}
-
-    def traffic(self):
-        return None
 
     @staticmethod
     def reference_sampler():
@@ -524,6 +535,7 @@ class PageRankW(Workload):
         # collective (and the step barrier). No prep pass, no rank-vector allgather.
         # BENCH_PR_EXCHANGE=0: prep + step + NCCL allgather (the unfused baseline).
         self.fused = self.implicit and os.environ.get("BENCH_PR_EXCHANGE", "1") == "1"
+        self.traffic_key = f"pagerank_step_exchange_scale{self.scale}" if self.fused and not self.relabel else None
         if self.fused:
             self.b_xs2 = [mk(self.v * 4), mk(self.v * 4)]
             handles = d.allgather_bytes(b"".join(ctx.share_buffer(q, b) for b in self.b_xs2)) if d.world > 1 else None
@@ -610,8 +622,11 @@ class PageRankW(Workload):
             ctx.enqueue_allgather(q, self.b_x[1 - self.cur], self.byte_bounds)
         self.cur = 1 - self.cur
 
+    def step_kernel(self):  # the fused step's kernel alone (no collective): the dominant launch
+        self.ctx.enqueue_ndrange_range(self.q, self.k_stepx[self.cur], (self.v, 1, 1), 1, self.lo, self.rows)
+
     def dominant(self):
-        return self.spmv
+        return self.step_kernel if self.fused else self.spmv
 
     def dominant_work(self):
         # SURVEY.md §8(d) algorithmic bytes of the CSR formulation (nnz*8 + (V+1)*4 + 2*V*4), also
@@ -651,9 +666,6 @@ class PageRankW(Workload):
                 else "R-MAT ids", "warp_nnz": self.wn,
                 "algorithmic_bytes_per_iteration": self.work_per_step(), "rank_sum_err": self.check,
                 "l2": "2.35 GB streamed per iteration > L2"}
-
-    def traffic(self):
-        return None
 
     @staticmethod
     def reference_sampler():
@@ -700,6 +712,7 @@ class KMeansW(Workload):
         # tensor-filtered assignment (kmeans_assign_tc: tcgen05 split-bf16 scores + exact fp32
         # verification, identical assignments); BENCH_KM_TC=0 selects the exact SIMT kernel
         self.tc = os.environ.get("BENCH_KM_TC", "1") == "1"
+        self.traffic_key = f"kmeans_assign_tc_n{self.N}" if self.tc else None
         self.km = km = KMeans(ctx, [q], self.N, self.D, self.K, tensor_filter=self.tc)
         # this rank's rows of the point set, generated in HBM (counter-based SplitMix64)
         kg = ctx.create_kernel(ctx.create_program("b200"), "gen_kmeans_points")
@@ -769,9 +782,6 @@ class KMeansW(Workload):
                 else "kmeans_assign (exact fp32 SIMT)",
                 "points": "SplitMix64 blobs, multiples of 2^-12, generated in HBM"}
 
-    def traffic(self):
-        return None
-
     @staticmethod
     def reference_sampler():
         import oracle as O
@@ -805,6 +815,7 @@ class ConvW(Workload):
 
         d = self.dist
         self.N = int(os.environ.get("BENCH_CONV_N", self.N))
+        self.traffic_key = f"conv3x3_n{self.N}"
         self.ctx = ctx = HostContext([d.local])
         self.q = q = ctx.create_queue(0)
         b = split_ranges(self.N, [1] * d.world)
@@ -870,9 +881,6 @@ class ConvW(Workload):
         return {"workload": f"conv3x3 (C5): batch {self.N}, {self.H}x{self.W}x{self.C} -> {self.K}, stride 1 pad 1, "
                             f"bf16 in/out, fp32 accumulate, batch split over {self.dist.world} rank(s)",
                 "layout": "padded NHWC input, KRSC weights, NHWK output"}
-
-    def traffic(self):
-        return None
 
     @staticmethod
     def reference_sampler():

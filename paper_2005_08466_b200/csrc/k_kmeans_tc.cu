@@ -362,11 +362,6 @@ __global__ void __launch_bounds__(KT_THREADS, 1)
       const int buf = vset;
       const int row = t * 2 * KT_ROWS + static_cast<int>(rank) * KT_ROWS + pl;
       const bool valid = row < rows;
-      if (lane == 0 && t + 2 * nclusters < tiles) {  // next tile's fp32 rows of this warp -> L2
-        const int64_t nrow = static_cast<int64_t>(t + 2 * nclusters) * 2 * KT_ROWS + rank * KT_ROWS + (vw % 4) * 32;
-        const int64_t nr = rows - nrow < 32 ? rows - nrow : 32;
-        if (nr > 0) ptx::bulk_prefetch_l2(pts + nrow * KT_D, static_cast<uint32_t>(nr * KT_D * 4));
-      }
       ptx::mbar_wait(&lfull[buf], (it >> 1) & 1);
       if (dbg & 4) {
         __syncwarp();
