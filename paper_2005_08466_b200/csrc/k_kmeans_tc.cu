@@ -4,19 +4,23 @@
 // to the smaller k; the reference's knn k=1, proj/src/kernels.cpp:195-233) --
 // but the 2*N*K*D distance work runs on the 5th-generation tensor cores:
 //
-//   1. score: s~_k = x . c_k by tcgen05 bf16 MMAs with fp32 accumulation, on
-//      split operands x = xh + xl (exact for points on a 2^-12 grid, else
-//      |x - xh - xl| <= 2^-16 |x|) and c = ch + cl (+ |residual| <= 2^-16 |c|):
-//      xh.ch + xl.ch + xh.cl as 6 MMAs of K=16 over the A row [xh|xl] and the
-//      B rows [ch|ch] (4) and [cl|..] (2; xl.cl, <= 2^-18 |x||c|, is dropped).
-//      t_k = |c_k|^2 - 2 s~_k ranks the centroids like |x - c_k|^2 (|x|^2 is
-//      common to the row).
+//   1. score: t~_k = |c_k|^2 - 2 x . c_k straight out of the tensor core:
+//      tcgen05 bf16 MMAs with fp32 accumulation on split operands x = xh + xl
+//      (exact for points on a 2^-12 grid, else |x - xh - xl| <= 2^-16 |x|)
+//      and c = ch + cl (+ |residual| <= 2^-16 |c|): -2(xh.ch + xl.ch + xh.cl)
+//      as 6 MMAs of K=16 over the A row [xh|xl] and the B rows [-2ch|-2ch]
+//      (4) and [-2cl|..] (2; xl.cl, <= 2^-18 |x||c|, is dropped), plus one
+//      K=16 MMA of a constant "ones" A tile against B2's second half
+//      [qh, ql, 0...] (|c|^2 as bf16 hi + lo, |error| <= 2^-17 |c|^2). t_k
+//      ranks the centroids like |x - c_k|^2 (|x|^2 is common to the row); the
+//      scan reads it from TMEM with no per-score arithmetic.
 //   2. filter (epilogue, per point): every k with t_k <= min_j t_j + 2 eps is a
-//      candidate, eps = 2^-10 (|x| max|c| + |x|^2 + max|c|^2) -- at least 7x
-//      the bound on |t_k + |x|^2 - d_k| from the split and the dropped term,
-//      the tensor-core accumulation (<= 2^-13 |x||c|) and the fp32 evaluation of the exact
-//      distance d_k (<= 2^-19 (|x|^2 + |c|^2 + 2|x||c|)). The exact argmin is
-//      always a candidate, and so is every k tied with it.
+//      candidate, eps = 2^-10 (|x| max|c| + |x|^2 + max|c|^2) -- at least 4x
+//      the bound on |t_k + |x|^2 - d_k| from the splits and the dropped term,
+//      the tensor-core accumulation (<= 2^-13 (|x||c| + |c|^2)) and the fp32
+//      evaluation of the exact distance d_k (<= 2^-19 (|x|^2 + |c|^2 +
+//      2|x||c|)). The exact argmin is always a candidate, and so is every k
+//      tied with it.
 //   3. verify: the candidates' exact fp32 distances (the oracle's operation
 //      order) pick the result; a point whose candidate list overflows (or
 //      with more than KT_QCAP survivors) is scanned exactly over all K by
@@ -29,7 +33,7 @@
 // Layout: points are stored twice -- fp32 (the exact pass and the update) and
 // split bf16 [xh(32) | xl(32)] (128 B per point = one SWIZZLE_128B row) with
 // |x|^2 per point, made once by kmeans_split_points. Per launch the centroids
-// are split into B1 = [ch|ch], B2 = [cl|cl] (bf16, K x 64) with |c|^2. One
+// are split into B1 = [-2ch|-2ch], B2 = [-2cl|qh,ql,0..] (bf16, K x 64). One
 // persistent CTA pair (cta_group::2) per 2 SMs: the pair's B halves for all K
 // are resident (K/2 x 256 B per CTA, <= 128 KB), A tiles of 2 x 128 points
 // stream through 2 stages, and each tile runs K/KT_CW chunks of N=KT_CW MMAs
@@ -39,8 +43,9 @@
 // and hand each tile's lists (double-buffered in shared memory, mbarrier
 // handshakes) to the verify warps -- two sets of 4, one per list buffer --
 // which filter, check exactly and store while the scan runs on. Measured on
-// 2^26 points, K=1024 (scripts/gpu_km4.sh): 4 groups x 4 slots, N=256: 20.2 ms;
-// 2 groups x 8 slots: 24.5 ms; N=128 chunks: 22.0 ms.
+// 2^26 points, K=1024 (scripts/gpu_km4.sh, gpu_km7.sh): 4 groups x 4 slots,
+// N=256: 20.2 ms, 17.2 ms with |c|^2 folded into the MMA; 2 groups x 8 slots:
+// 24.5 ms; N=128 chunks: 22.0 ms.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -99,7 +104,7 @@ struct KtLayout {
     b = 0;
     a = b + static_cast<size_t>(nch) * 2 * KT_BH;
     q = a + static_cast<size_t>(KT_STAGES) * KT_A;
-    lists = q + static_cast<size_t>(K) * 4;
+    lists = q + 4096;  // q: the constant "ones" A tile of the |c|^2 MMA (128 rows x 16 bf16, no swizzle)
     xch = lists + 2ull * KT_LBUF * 8;             // 2 buffers x (t, k) float2 slots
     vq = xch + 2ull * KT_GROUPS * KT_ROWS * 8 + 2ull * KT_ROWS * 4;  // 2 bufs x groups x (min, count|ovf) + 2 eps
     bars = vq + static_cast<size_t>(KT_VER) * 32 * KT_QCAP * 8;  // verify queues
@@ -133,7 +138,7 @@ __device__ __forceinline__ float exact_dist(const float (&x)[KT_D], const float*
 
 __global__ void __launch_bounds__(KT_THREADS, 1)
     kmeans_assign_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB1,
-                            const __grid_constant__ CUtensorMap tmB2, const float* __restrict__ qg,
+                            const __grid_constant__ CUtensorMap tmB2, const float* __restrict__ /*q: unused*/,
                             const float* __restrict__ stats, const float* __restrict__ cent,
                             const float* __restrict__ pts, const float* __restrict__ xxg,
                             int32_t* __restrict__ assign, int rows, int K, int* __restrict__ n_overflow,
@@ -145,7 +150,7 @@ __global__ void __launch_bounds__(KT_THREADS, 1)
   const KtLayout L(K);
   uint8_t* sb = smem + L.b;
   uint8_t* sa = smem + L.a;
-  float* sq = reinterpret_cast<float*>(smem + L.q);
+  uint32_t* ones = reinterpret_cast<uint32_t*>(smem + L.q);
   float2* lists = reinterpret_cast<float2*>(smem + L.lists);
   float2* xch = reinterpret_cast<float2*>(smem + L.xch);              // [buf][group][point] (min, count|ovf<<16)
   float* xeps = reinterpret_cast<float*>(xch + 2 * KT_GROUPS * KT_ROWS);  // [buf][point] 2 eps
@@ -183,6 +188,10 @@ __global__ void __launch_bounds__(KT_THREADS, 1)
     ptx::fence_mbar_init();
   }
   if (warp == KT_MMA) ptx::tmem_alloc<2>(tmem_slot, 512);
+  // every 16-byte core-matrix row = bf16 [1, 1, 0 x 6]: A(m, k) = 1 for k % 8 in {0, 1},
+  // against B2 columns 32.. = [qh, ql, 0 ...] (identical core matrices: layout-proof)
+  for (int i = threadIdx.x; i < 1024; i += blockDim.x) ones[i] = (i & 3) == 0 ? 0x3F803F80u : 0u;
+  ptx::fence_proxy_async_smem();
   ptx::tc_fence_before();
   ptx::cluster_sync();
   ptx::tc_fence_after();
@@ -217,6 +226,7 @@ __global__ void __launch_bounds__(KT_THREADS, 1)
       ptx::mbar_wait(bfull, 0);
       const uint64_t adesc0 = ptx::umma_desc_sw128(ptx::smem_u32(sa), 16, 1024);
       const uint64_t bdesc0 = ptx::umma_desc_sw128(ptx::smem_u32(sb), 16, 1024);
+      const uint64_t ones_desc = ptx::umma_desc_noswz(ptx::smem_u32(ones), 128, 256);
       int stage = 0;
       uint32_t phase = 0, tph = 0;  // tph: phase bit per accumulator
       int acc = 0;
@@ -235,6 +245,7 @@ __global__ void __launch_bounds__(KT_THREADS, 1)
           for (int i = 0; i < 4; ++i) ptx::mma_elect<2, false>(d_tmem, adesc + 2 * i, b1 + 2 * i, idesc, i != 0);
 #pragma unroll
           for (int i = 0; i < 2; ++i) ptx::mma_elect<2, false>(d_tmem, adesc + 2 * i, b2 + 2 * i, idesc, 1);
+          ptx::mma_elect<2, false>(d_tmem, ones_desc, b2 + 4, idesc, 1);  // + |c|^2 (B2 k-step 2)
           ptx::mma_commit_elect<2>(&tfull[acc]);
           if (++acc == KT_NACC) acc = 0;
         }
@@ -247,8 +258,6 @@ __global__ void __launch_bounds__(KT_THREADS, 1)
     // ---------------- scan: group g = column slice g of every chunk ----------------
     const int g = warp / 4, quad = warp % 4;
     const int pl = quad * 32 + lane;  // point within the CTA tile = TMEM lane
-    for (int i = threadIdx.x; i < K; i += KT_SCAN * 32) sq[i] = qg[i];
-    const uint32_t sq_s = ptx::smem_u32(sq);
     const float qmax = stats[0];
     const float cmax = sqrtf(qmax);
     epi_bar();
@@ -281,22 +290,11 @@ __global__ void __launch_bounds__(KT_THREADS, 1)
             if (lane == 0) ptx::mbar_arrive_cluster_relaxed(ptx::mapa(ptx::smem_u32(&tempty[acc]), 0));
           }
           const int k0 = c * KT_CW + g * KT_GCOLS + b * 32;
-          const uint32_t q_s = sq_s + static_cast<uint32_t>(k0) * 4;
-          float g4[8];  // independent group minima (a shallow dependency tree)
+          float g4[8];  // independent group minima (a shallow dependency tree); the MMA already added |c|^2
 #pragma unroll
           for (int j = 0; j < 32; j += 4) {
-            float4 qv;
-            asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
-                         : "=f"(qv.x), "=f"(qv.y), "=f"(qv.z), "=f"(qv.w)
-                         : "r"(q_s + j * 4));
-            const float t0 = fmaf(-2.f, __uint_as_float(cur[j]), qv.x);
-            const float t1 = fmaf(-2.f, __uint_as_float(cur[j + 1]), qv.y);
-            const float t2 = fmaf(-2.f, __uint_as_float(cur[j + 2]), qv.z);
-            const float t3 = fmaf(-2.f, __uint_as_float(cur[j + 3]), qv.w);
-            cur[j] = __float_as_uint(t0);
-            cur[j + 1] = __float_as_uint(t1);
-            cur[j + 2] = __float_as_uint(t2);
-            cur[j + 3] = __float_as_uint(t3);
+            const float t0 = __uint_as_float(cur[j]), t1 = __uint_as_float(cur[j + 1]);
+            const float t2 = __uint_as_float(cur[j + 2]), t3 = __uint_as_float(cur[j + 3]);
             g4[j / 4] = fminf(fminf(t0, t1), fminf(t2, t3));
           }
           const float bmin = fminf(fminf(fminf(g4[0], g4[1]), fminf(g4[2], g4[3])),
@@ -556,10 +554,18 @@ __global__ void kmeans_split_centroids_kernel(const float* __restrict__ cent, ui
     const float v = cent[static_cast<int64_t>(k) * KT_D + j];
     const __nv_bfloat16 h = __float2bfloat16_rn(v);
     const __nv_bfloat16 l = __float2bfloat16_rn(v - __bfloat162float(h));
-    b1[k * 64 + j] = b1[k * 64 + 32 + j] = __bfloat16_as_ushort(h);
-    b2[k * 64 + j] = b2[k * 64 + 32 + j] = __bfloat16_as_ushort(l);
+    // -2c: exact in bf16 (a power-of-two scale), so the MMA accumulates -2 x.c directly
+    b1[k * 64 + j] = b1[k * 64 + 32 + j] = __bfloat16_as_ushort(__hmul(h, __float2bfloat16_rn(-2.f)));
+    b2[k * 64 + j] = __bfloat16_as_ushort(__hmul(l, __float2bfloat16_rn(-2.f)));
     s = fmaf(v, v, s);
   }
+  // B2's second half carries |c|^2 as bf16 hi + lo (|error| <= 2^-17 |c|^2) for the
+  // ones-column MMA: the accumulator then holds t = |c|^2 - 2 x.c itself
+  const __nv_bfloat16 qh = __float2bfloat16_rn(s);
+  const __nv_bfloat16 ql = __float2bfloat16_rn(s - __bfloat162float(qh));
+  b2[k * 64 + 32] = __bfloat16_as_ushort(qh);
+  b2[k * 64 + 33] = __bfloat16_as_ushort(ql);
+  for (int j = 34; j < 64; ++j) b2[k * 64 + j] = 0;
   q[k] = s;
   atomicMax(stats, __float_as_uint(s * (1.f + 0x1p-20f)));  // non-negative: bit order = value order
 }

@@ -276,6 +276,17 @@ __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t smem_addr, uint32_t
   return d;
 }
 
+// K-major SWIZZLE_NONE (interleaved 8-row x 16-byte core matrices): LBO = byte
+// stride between core matrices adjacent in K, SBO = between 8-row groups.
+__device__ __forceinline__ uint64_t umma_desc_noswz(uint32_t smem_addr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((smem_addr >> 4) & 0x3FFF);
+  d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFF) << 16;
+  d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFF) << 32;
+  d |= 1ull << 46;  // version = 1 (Blackwell); layout type 0 = SWIZZLE_NONE
+  return d;
+}
+
 // Same with the 3-bit matrix base offset (bits 49-51): the phase of the
 // swizzle pattern when the start address is not on a 1024-byte boundary.
 __device__ __forceinline__ uint64_t umma_desc_sw128_bo(uint32_t smem_addr, uint32_t lbo, uint32_t sbo,
