@@ -749,8 +749,8 @@ class KMeansW(Workload):
         return self._assign
 
     def dominant_work(self):
-        if self.tc:  # tensor work actually issued: 3 split products x D per (point, centroid)
-            return 2.0 * self.rows * self.K * 3 * self.D
+        if self.tc:  # tensor work actually issued per (point, centroid): 3 split products x D + the K=16 |c|^2 MMA
+            return 2.0 * self.rows * self.K * (3 * self.D + 16)
         return 3.0 * self.rows * self.K * self.D
 
     def e2e_step(self):
@@ -768,7 +768,7 @@ class KMeansW(Workload):
     def roofline(self, pk):
         if self.tc:
             return ("tensor", pk["bf16_tflops"], "TFLOP/s", 1e12,
-                    "MEASURED_PEAKS.json bf16_tflops; achieved = split-bf16 MMA flops issued (2 N K 3D)")
+                    "MEASURED_PEAKS.json bf16_tflops; achieved = bf16 MMA flops issued (2 N K (3D + 16))")
         sm = pk.get("sm_max_mhz", 1965.0)
         # exact (non-FMA) fp32: one add or multiply per lane per clock (FADD2 issues
         # two lanes' worth but occupies the FP32 pipe twice, measured)
