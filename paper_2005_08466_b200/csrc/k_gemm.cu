@@ -82,7 +82,10 @@ template <int CG, bool TF32, bool BMN, bool OUTF32, int BN, bool ONE>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmC, void* __restrict__ Cout, int M, int N, int K,
-                   int64_t ldc, int group_m, int tma_c) {
+                   int64_t ldc, int group_m, int tma_c, int ksplit) {
+  // ksplit > 1 (fp32 output only): work unit t = (tile, K slice t / tiles); slice s
+  // accumulates k-blocks [nk*s/ksplit, nk*(s+1)/ksplit) into C + s*M*ldc (a workspace
+  // the launcher reduces in slice order)
   using C = Cfg<CG, TF32, BN, ONE>;
   constexpr int kBN = C::kBN;
   static_assert(!BMN || C::kBNLocal % C::kMNAtom == 0, "MN-major B needs whole 128-byte atoms per CTA");
@@ -119,6 +122,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const TileMap map{static_cast<int>((M + kBM * CG - 1) / (kBM * CG)), (N + kBN - 1) / kBN, group_m};
   const int tiles = map.num_m * map.num_n;
+  const int units = tiles * ksplit;
   const int cluster = blockIdx.x / CG, nclusters = gridDim.x / CG;
   const int nk = (K + C::kBK - 1) / C::kBK;
 
@@ -127,12 +131,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = cluster; t < tiles; t += nclusters) {
+      for (int t = cluster; t < units; t += nclusters) {
         int mt, nt;
-        map.get(t, mt, nt);
+        map.get(t % tiles, mt, nt);
+        const int sp = t / tiles;
+        const int kb0 = static_cast<int>(static_cast<int64_t>(nk) * sp / ksplit);
+        const int kb1 = static_cast<int>(static_cast<int64_t>(nk) * (sp + 1) / ksplit);
         const int m0 = mt * kBM * CG + static_cast<int>(rank) * kBM;
         const int n0 = nt * kBN + static_cast<int>(rank) * C::kBNLocal;
-        for (int kb = 0; kb < nk; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           ptx::mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * C::kStage;
           uint8_t* sb = sa + C::kABytes;
@@ -177,11 +184,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int t = cluster; t < tiles; t += nclusters) {
+      for (int t = cluster; t < units; t += nclusters) {
+        const int sp = t / tiles;
+        const int kb0 = static_cast<int>(static_cast<int64_t>(nk) * sp / ksplit);
+        const int kb1 = static_cast<int>(static_cast<int64_t>(nk) * (sp + 1) / ksplit);
         ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
         ptx::tc_fence_after();
         const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * kBN);
-        for (int kb = 0; kb < nk; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           ptx::mbar_wait(&full[stage], phase);
           ptx::tc_fence_after();
           const uint64_t so = static_cast<uint64_t>((stage * C::kStage) >> 4);
@@ -189,7 +199,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int k = 0; k < C::kBK / C::kUK; ++k) {
             const uint64_t adesc = adesc0 + so + static_cast<uint64_t>((k * 32) >> 4);
             const uint64_t bdesc = bdesc0 + so + static_cast<uint64_t>((BMN ? k * (C::kUK / 8) * 1024 : k * 32) >> 4);
-            ptx::mma_elect<CG, TF32>(d_tmem, adesc, bdesc, idesc, (kb | k) != 0);
+            ptx::mma_elect<CG, TF32>(d_tmem, adesc, bdesc, idesc, (kb != kb0) | (k != 0));
           }
           ptx::mma_commit_elect<CG>(&empty[stage]);  // frees the smem slot when these MMAs finish
           if (++stage == C::kStages) { stage = 0; phase ^= 1; }
@@ -203,9 +213,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ---------------- epilogue warps 0-3 ----------------
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int t = cluster; t < tiles; t += nclusters) {
+    for (int t = cluster; t < units; t += nclusters) {
       int mt, nt;
-      map.get(t, mt, nt);
+      map.get(t % tiles, mt, nt);
+      const int64_t slice = static_cast<int64_t>(t / tiles) * M * ldc;  // 0 unless ksplit > 1
       ptx::mbar_wait(&tfull[acc], acc_phase);
       ptx::tc_fence_after();
       const int64_t row = static_cast<int64_t>(mt) * kBM * CG + rank * kBM + warp * 32 + lane;
@@ -224,7 +235,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (!row_ok || col0 >= N) continue;
         }
         if constexpr (OUTF32) {
-          float* dst = reinterpret_cast<float*>(Cout) + row * ldc + col0;
+          float* dst = reinterpret_cast<float*>(Cout) + slice + row * ldc + col0;
           if (col0 + 32 <= N && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
 #pragma unroll
             for (int j = 0; j < 8; ++j)
@@ -367,7 +378,7 @@ CUtensorMap make_tmap(const void* base, bool f32, uint64_t inner, uint64_t outer
 
 template <int CG, bool TF32, bool BMN, bool OUTF32, int BN = 256, bool ONE = false>
 void run_gemm(const void* A, const void* B, void* Cp, int64_t M, int64_t N, int64_t K, int64_t ldc,
-              int sm_count, cudaStream_t stream, int group_m, bool persistent) {
+              int sm_count, cudaStream_t stream, int group_m, bool persistent, int ksplit = 1) {
   using C = Cfg<CG, TF32, BN, ONE>;
   const uint64_t es = C::kElem;
   const CUtensorMapL2promotion promo = l2_promotion();
@@ -389,7 +400,7 @@ void run_gemm(const void* A, const void* B, void* Cp, int64_t M, int64_t N, int6
   auto kern = gemm_tc_kernel<CG, TF32, BMN, OUTF32, BN, ONE>;
   // per launch: the attribute is per device context and launches may target several GPUs
   HCL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(C::kSmem)));
-  const int64_t tiles = ceil_div(M, kBM * CG) * ceil_div(N, BN);
+  const int64_t tiles = ceil_div(M, kBM * CG) * ceil_div(N, BN) * ksplit;
   // One cluster per tile (default): the hardware launches clusters in raster
   // order as SMs free up, so the running tiles stay a compact window of the
   // grouped raster and L2 serves the panel re-reads. Measured at 16384^3:
@@ -412,7 +423,7 @@ void run_gemm(const void* A, const void* B, void* Cp, int64_t M, int64_t N, int6
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   HCL_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, tc, Cp, static_cast<int>(M), static_cast<int>(N),
-                              static_cast<int>(K), ldc, group_m, tma_c));
+                              static_cast<int>(K), ldc, group_m, tma_c, ksplit));
   HCL_LAUNCHED();
 }
 
@@ -432,14 +443,14 @@ __global__ void transpose_kernel(const T* __restrict__ in, T* __restrict__ out, 
 // Tile shape with the smallest estimated time: waves x (BN + 32), i.e. the
 // per-SM work of a tile (128 x BN) plus a fixed per-tile cost (prologue,
 // pipeline fill, epilogue tail) in column units.
-int pick_shape(int64_t M, int64_t N, int sm_count) {
+int pick_shape(int64_t M, int64_t N, int sm_count, int ksplit = 1) {
   static constexpr int kCG[4] = {2, 1, 2, 1}, kBNs[4] = {256, 256, 128, 64};
   int best = 0;
   int64_t best_t = INT64_MAX;
   for (int i : {0, 2, 3}) {
-    const int64_t tiles = ceil_div(M, kBM * kCG[i]) * ceil_div(N, kBNs[i]);
-    const int64_t clusters = std::max<int64_t>(1, std::min<int64_t>(tiles, sm_count / kCG[i]));
-    const int64_t t = ceil_div(tiles, clusters) * (kBNs[i] + 32);
+    const int64_t units = ceil_div(M, kBM * kCG[i]) * ceil_div(N, kBNs[i]) * ksplit;
+    const int64_t clusters = std::max<int64_t>(1, std::min<int64_t>(units, sm_count / kCG[i]));
+    const int64_t t = ceil_div(units, clusters) * (kBNs[i] + 32);
     if (t < best_t) { best_t = t; best = i; }
   }
   return best;
@@ -447,18 +458,42 @@ int pick_shape(int64_t M, int64_t N, int sm_count) {
 
 template <bool TF32, bool BMN, bool OUTF32>
 void dispatch_shape(int shape, const void* a, const void* b, void* cp, int64_t M, int64_t n, int64_t k,
-                    const LaunchCtx& c, int group_m) {
+                    const LaunchCtx& c, int group_m, int ksplit = 1) {
   const bool persist = c.sm_budgeted || env_int("HCL_GEMM_PERSIST", 0) != 0;
   switch (shape) {
-    case 1: run_gemm<1, TF32, BMN, OUTF32, 256>(a, b, cp, M, n, k, n, c.sm_count, c.stream, group_m, persist); break;
-    case 2: run_gemm<2, TF32, BMN, OUTF32, 128>(a, b, cp, M, n, k, n, c.sm_count, c.stream, group_m, persist); break;
-    case 3: run_gemm<1, TF32, BMN, OUTF32, 64>(a, b, cp, M, n, k, n, c.sm_count, c.stream, group_m, persist); break;
+    case 1:
+      run_gemm<1, TF32, BMN, OUTF32, 256>(a, b, cp, M, n, k, n, c.sm_count, c.stream, group_m, persist, ksplit);
+      break;
+    case 2:
+      run_gemm<2, TF32, BMN, OUTF32, 128>(a, b, cp, M, n, k, n, c.sm_count, c.stream, group_m, persist, ksplit);
+      break;
+    case 3:
+      run_gemm<1, TF32, BMN, OUTF32, 64>(a, b, cp, M, n, k, n, c.sm_count, c.stream, group_m, persist, ksplit);
+      break;
     default:
       if (persist || env_int("HCL_GEMM_ONE", 1) == 0)
-        run_gemm<2, TF32, BMN, OUTF32, 256>(a, b, cp, M, n, k, n, c.sm_count, c.stream, group_m, persist);
+        run_gemm<2, TF32, BMN, OUTF32, 256>(a, b, cp, M, n, k, n, c.sm_count, c.stream, group_m, persist, ksplit);
       else
-        run_gemm<2, TF32, BMN, OUTF32, 256, true>(a, b, cp, M, n, k, n, c.sm_count, c.stream, group_m, false);
+        run_gemm<2, TF32, BMN, OUTF32, 256, true>(a, b, cp, M, n, k, n, c.sm_count, c.stream, group_m, false,
+                                                  ksplit);
       break;
+  }
+}
+
+// C = sum over the ksplit workspace slices, in slice order (deterministic)
+__global__ void __launch_bounds__(256) ksplit_reduce_kernel(const float4* __restrict__ ws, float4* __restrict__ out,
+                                                            int64_t n4, int ksplit) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += stride) {
+    float4 a = ws[i];
+    for (int s = 1; s < ksplit; ++s) {
+      const float4 b = ws[s * n4 + i];
+      a.x = __fadd_rn(a.x, b.x);
+      a.y = __fadd_rn(a.y, b.y);
+      a.z = __fadd_rn(a.z, b.z);
+      a.w = __fadd_rn(a.w, b.w);
+    }
+    out[i] = a;
   }
 }
 
@@ -592,10 +627,19 @@ uint64_t launch_gemm_f32x3(LaunchCtx& c) {
   float* cp = at_byte<float>(Cb, lo * n * 4, rows * n * 4, "gemm_f32x3 C");
   if (rows == 0) return 0;
   const int64_t r = static_cast<int64_t>(rows);
+  // optional K split (HCL_GEMM_KSPLIT = slices; a function of N and K only, so every row
+  // partition of one GEMM sums in the same order; slices reduced in order). Measured at
+  // C1 (1024^3): 51 us per launch unsplit, 52 us with 2 slices, 58 us with 4 -- the split
+  // kernels and launch gaps dominate at this size, so the default is unsplit.
+  const int64_t nkb = ceil_div(3 * k, 32);
+  const int ksplit = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(env_int("HCL_GEMM_KSPLIT", 1), nkb)));
   const size_t a3_bytes = static_cast<size_t>(r * 3 * k * 4);
-  uint8_t* s = static_cast<uint8_t*>(c.scratch(c.dev, a3_bytes + static_cast<size_t>(n * 3 * k * 4)));
+  const size_t b3_bytes = static_cast<size_t>(n * 3 * k * 4);
+  const size_t ws_bytes = ksplit > 1 ? static_cast<size_t>(ksplit) * r * n * 4 : 0;
+  uint8_t* s = static_cast<uint8_t*>(c.scratch(c.dev, a3_bytes + b3_bytes + ws_bytes));
   float* a3 = reinterpret_cast<float*>(s);
   float* b3 = reinterpret_cast<float*>(s + a3_bytes);
+  float* ws = reinterpret_cast<float*>(s + a3_bytes + b3_bytes);
   {
     const int64_t total = r * (k / 4);
     const unsigned blocks = static_cast<unsigned>(std::min<int64_t>(ceil_div(total, 256), 64LL * c.sm_count));
@@ -608,8 +652,15 @@ uint64_t launch_gemm_f32x3(LaunchCtx& c) {
   }
   const int group_m = std::max(1, env_int("HCL_GEMM_GROUP", kGroupM));
   int shape = env_int("HCL_GEMM_SHAPE", -1);
-  if (shape < 0 || shape > 3) shape = pick_shape(r, n, c.sm_count);
-  dispatch_shape<true, false, true>(shape, a3, b3, cp, r, n, 3 * k, c, group_m);
+  if (shape < 0 || shape > 3) shape = pick_shape(r, n, c.sm_count, ksplit);
+  dispatch_shape<true, false, true>(shape, a3, b3, ksplit > 1 ? ws : cp, r, n, 3 * k, c, group_m, ksplit);
+  if (ksplit > 1) {
+    const int64_t n4 = r * n / 4;  // N % 4 == 0
+    const unsigned blocks = static_cast<unsigned>(std::min<int64_t>(ceil_div(n4, 256), 8LL * c.sm_count));
+    ksplit_reduce_kernel<<<blocks, 256, 0, c.stream>>>(reinterpret_cast<const float4*>(ws),
+                                                       reinterpret_cast<float4*>(cp), n4, ksplit);
+    HCL_LAUNCHED();
+  }
   return 2ull * rows * static_cast<uint64_t>(n) * static_cast<uint64_t>(k);
 }
 
