@@ -209,3 +209,16 @@ def test_gemm_full_c2_sampled(ctx, queues, kernel, out_f32, tol):
     ii, jj = np.sort(rng.choice(s, 64, replace=False)), np.sort(rng.choice(s, 64, replace=False))
     a64, b64 = af[ii].astype(np.float64), bf[:, jj].astype(np.float64)
     assert normwise_err(c[np.ix_(ii, jj)], a64, b64) <= tol
+
+
+def test_gemm_f32x3_ksplit(ctx, queues, monkeypatch):
+    """Optional K split (HCL_GEMM_KSPLIT): slices summed in order -- within the
+    3xTF32 tolerance and bit-identical across row partitions."""
+    monkeypatch.setenv("HCL_GEMM_KSPLIT", "4")
+    m, n, k = 1024, 512, 1024
+    a = O.gen_doubles(m * k, 42).astype(np.float32)
+    b = O.gen_doubles(k * n, 43).astype(np.float32)
+    whole = gemm(ctx, queues, "gemm_f32x3", a, b, m, k, n)
+    assert normwise_err(whole, a.astype(np.float64).reshape(m, k), b.astype(np.float64).reshape(k, n)) <= 2.0**-17
+    part = gemm(ctx, queues, "gemm_f32x3", a, b, m, k, n, P=4, weights=[1, 2, 3, 4])
+    assert whole.tobytes() == part.tobytes()
