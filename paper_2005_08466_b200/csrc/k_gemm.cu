@@ -559,7 +559,7 @@ uint64_t launch_gemm_tc(LaunchCtx& c) {
 // C = hi_a*hi_b + hi_a*lo_b + lo_a*hi_b (lo_a*lo_b ~ 2^-22 |a||b| dropped).
 // The three products become ONE K-major TF32 GEMM over K' = 3K:
 //   A'[r] = [hi(a_r) | hi(a_r) | lo(a_r)],  B'^T[n] = [hi(b_n) | lo(b_n) | hi(b_n)]
-// built by two memory-bound split kernels, then the same tcgen05 kernel as
+// built by one memory-bound split launch (A rows and B columns), then the same tcgen05 kernel as
 // gemm_tf32. The split products are exact, but the tensor core's fp32
 // accumulation truncates per MMA, so the measured normwise error is ~2^-19 at
 // K=1024 and ~2^-17 at K=16384 (SIMT gemm_f32: ~2^-22) -- at 1/3 of the TF32
@@ -571,35 +571,40 @@ __device__ __forceinline__ float tf32_hi(float x) {
   return __uint_as_float(r);
 }
 
-// A (rows x K) -> A' (rows x 3K)
-__global__ void split3_rows_kernel(const float4* __restrict__ a, float4* __restrict__ out, int64_t rows, int64_t k4) {
-  const int64_t total = rows * k4;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = i / k4, c = i - r * k4;
-    float4 v = a[i], h, l;
-    h.x = tf32_hi(v.x); h.y = tf32_hi(v.y); h.z = tf32_hi(v.z); h.w = tf32_hi(v.w);
-    l.x = v.x - h.x; l.y = v.y - h.y; l.z = v.z - h.z; l.w = v.w - h.w;
-    float4* o = out + r * 3 * k4 + c;
-    o[0] = h;
-    o[k4] = h;
-    o[2 * k4] = l;
+// Both splits in one launch (small GEMMs are launch-bound): blocks [0, a_blocks)
+// split A's rows, the rest transpose-split B in 32x32 tiles (256 threads = 32 x 8)
+__global__ void __launch_bounds__(256) split3_both_kernel(const float4* __restrict__ a, float4* __restrict__ a3,
+                                                          int64_t rows, int64_t k4, int a_blocks,
+                                                          const float* __restrict__ b, float* __restrict__ b3,
+                                                          int64_t K, int64_t N, int gx) {
+  if (static_cast<int>(blockIdx.x) < a_blocks) {
+    const int64_t total = rows * k4;
+    for (int64_t i = blockIdx.x * 256ll + threadIdx.x; i < total; i += static_cast<int64_t>(a_blocks) * 256) {
+      const int64_t r = i / k4, c = i - r * k4;
+      float4 v = a[i], h, l;
+      h.x = tf32_hi(v.x); h.y = tf32_hi(v.y); h.z = tf32_hi(v.z); h.w = tf32_hi(v.w);
+      l.x = v.x - h.x; l.y = v.y - h.y; l.z = v.z - h.z; l.w = v.w - h.w;
+      float4* o = a3 + r * 3 * k4 + c;
+      o[0] = h;
+      o[k4] = h;
+      o[2 * k4] = l;
+    }
+    return;
   }
-}
-
-// B (K x N, row-major) -> B'^T (N x 3K): transpose through shared memory
-__global__ void split3_cols_kernel(const float* __restrict__ b, float* __restrict__ out, int64_t K, int64_t N) {
   __shared__ float tile[32][33];
-  const int64_t n0 = blockIdx.x * 32, k0 = blockIdx.y * 32;
-  for (int i = threadIdx.y; i < 32; i += 8) {
-    const int64_t k = k0 + i, n = n0 + threadIdx.x;
-    tile[i][threadIdx.x] = (k < K && n < N) ? b[k * N + n] : 0.f;
+  const int bid = static_cast<int>(blockIdx.x) - a_blocks;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int64_t n0 = static_cast<int64_t>(bid % gx) * 32, k0 = static_cast<int64_t>(bid / gx) * 32;
+  for (int i = ty; i < 32; i += 8) {
+    const int64_t k = k0 + i, n = n0 + tx;
+    tile[i][tx] = (k < K && n < N) ? b[k * N + n] : 0.f;
   }
   __syncthreads();
-  for (int i = threadIdx.y; i < 32; i += 8) {
-    const int64_t n = n0 + i, k = k0 + threadIdx.x;
+  for (int i = ty; i < 32; i += 8) {
+    const int64_t n = n0 + i, k = k0 + tx;
     if (n < N && k < K) {
-      const float v = tile[threadIdx.x][i], h = tf32_hi(v);
-      float* o = out + n * 3 * K + k;
+      const float v = tile[tx][i], h = tf32_hi(v);
+      float* o = b3 + n * 3 * K + k;
       o[0] = h;
       o[K] = v - h;
       o[2 * K] = h;
@@ -642,12 +647,12 @@ uint64_t launch_gemm_f32x3(LaunchCtx& c) {
   float* ws = reinterpret_cast<float*>(s + a3_bytes + b3_bytes);
   {
     const int64_t total = r * (k / 4);
-    const unsigned blocks = static_cast<unsigned>(std::min<int64_t>(ceil_div(total, 256), 64LL * c.sm_count));
-    split3_rows_kernel<<<blocks, 256, 0, c.stream>>>(reinterpret_cast<const float4*>(a), reinterpret_cast<float4*>(a3),
-                                                      r, k / 4);
-    HCL_LAUNCHED();
-    dim3 grid(static_cast<unsigned>(ceil_div(n, 32)), static_cast<unsigned>(ceil_div(k, 32)));
-    split3_cols_kernel<<<grid, dim3(32, 8), 0, c.stream>>>(reinterpret_cast<const float*>(B.ptr), b3, k, n);
+    const int a_blocks = static_cast<int>(std::min<int64_t>(ceil_div(total, 256), 64LL * c.sm_count));
+    const int gx = static_cast<int>(ceil_div(n, 32));
+    const int64_t b_blocks = static_cast<int64_t>(gx) * ceil_div(k, 32);
+    split3_both_kernel<<<static_cast<unsigned>(a_blocks + b_blocks), 256, 0, c.stream>>>(
+        reinterpret_cast<const float4*>(a), reinterpret_cast<float4*>(a3), r, k / 4, a_blocks,
+        reinterpret_cast<const float*>(B.ptr), b3, k, n, gx);
     HCL_LAUNCHED();
   }
   const int group_m = std::max(1, env_int("HCL_GEMM_GROUP", kGroupM));
