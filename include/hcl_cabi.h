@@ -62,6 +62,14 @@ enum hcl_part_class {
   HCL_PART_SPLIT_ROWS = 2, /* row slice [lo,hi) of dim 0 on each device (GEMM A, C) */
   HCL_PART_REDUCE_SUM = 3, /* each part produces a full-size int64 partial; the
                               runtime sums them (k-means centroid sums) */
+  HCL_PART_EXCHANGE = 5,  /* full-size output on every part's device: each part's
+                              kernel writes its rows into ALL copies through the
+                              PEERS list (pagerank_step_exchange); afterwards the
+                              buffer is whole on every participating device */
+  HCL_PART_PEERS = 6,     /* input the runtime fills per part (multi-part launches):
+                              uint64 device addresses of the EXCHANGE output's copies
+                              on the other parts' devices; the next argument is
+                              their count (parts - 1) */
   HCL_PART_MERGE_TOPK = 4  /* each part produces full-size per-query sorted
                               top-k lists (an index and a distance output); the
                               runtime folds them pairwise with the kernel's

@@ -330,7 +330,44 @@ struct HostContext::Impl {
           ensure_valid(args[i].buffer, b, part.gid, first, len, &q);
       }
     }
+    // 1b. EXCHANGE / PEERS: each part's kernel stores its rows into every part's copy
+    //     of the EXCHANGE output; its PEERS input lists the other copies' addresses
+    std::vector<const Part*> live;
+    for (const Part& part : parts)
+      if (whole || part.hi > part.lo) live.push_back(&part);
+    int xi = -1;
+    for (uint32_t i = 0; i < n; ++i)
+      if (args[i].is_buffer && k.classes[i] == HCL_PART_EXCHANGE) {
+        if (xi >= 0) fail(ErrorCode::argument, k.name + ": one EXCHANGE output per kernel");
+        xi = static_cast<int>(i);
+      }
+    const bool exchange = xi >= 0 && live.size() > 1;
+    if (exchange) {
+      for (size_t a = 0; a < live.size(); ++a)
+        for (size_t c = a + 1; c < live.size(); ++c)
+          if (live[a]->gid == live[c]->gid)
+            fail(ErrorCode::argument, k.name + ": an EXCHANGE output needs one device per part");
+      for (uint32_t i = 0; i < n; ++i) {
+        if (!args[i].is_buffer || k.classes[i] != HCL_PART_PEERS) continue;
+        if (i + 1 >= n || args[i + 1].is_buffer || args[i + 1].scalar != static_cast<int64_t>(live.size() - 1))
+          fail(ErrorCode::argument, k.name + ": the PEERS count argument must equal parts - 1");
+        BufferRec& pb = buffer(args[i].buffer);
+        if (pb.size < 8 * (live.size() - 1)) fail(ErrorCode::size, k.name + ": PEERS buffer too small");
+        for (const Part* p : live) {
+          std::vector<uint64_t> addrs;
+          for (const Part* o : live) {
+            if (o == p) continue;
+            void* ptr = nullptr;
+            check(hcl_buffer_device_ptr(dev_index(o->gid), args[xi].buffer, &ptr, nullptr, nullptr));
+            addrs.push_back(reinterpret_cast<uint64_t>(ptr));
+          }
+          check(hcl_buffer_write(dev_index(p->gid), args[i].buffer, 0, addrs.data(), addrs.size() * 8));
+          set_valid(pb.pieces[p->gid], 0, pb.size);  // per-device contents: the others stay valid too
+        }
+      }
+    }
     // 2. launch every part asynchronously on its device stream
+    std::vector<std::pair<cudaStream_t, cudaEvent_t>> part_done;
     std::vector<hcl_arg> cargs(n);
     for (uint32_t i = 0; i < n; ++i)
       cargs[i] = hcl_arg{static_cast<uint32_t>(k.kinds[i]), 0, args[i].scalar, args[i].buffer};
@@ -355,6 +392,7 @@ struct HostContext::Impl {
       trace.record({part.gid, "launch_kernel", 0});
       int rc = hcl_launch(dev, k.name.c_str(), cargs.data(), n, goff, whole ? nullptr : gsz, dims, &l.work);
       cudaEventRecord(l.stop, static_cast<cudaStream_t>(stream));
+      part_done.emplace_back(static_cast<cudaStream_t>(stream), l.stop);
       scheduler.note_complete(part.gid);
       if (rc != HCL_OK) {
         cudaEventDestroy(l.start);
@@ -363,6 +401,12 @@ struct HostContext::Impl {
       }
       q.pending.push_back(l);
     }
+    // 2b. EXCHANGE: every part wrote into every copy, so each device's stream
+    //     waits for all parts before anything later touches the output there
+    if (exchange)
+      for (auto& [st, ev_own] : part_done)
+        for (auto& [st2, ev] : part_done)
+          if (ev != ev_own) cudaStreamWaitEvent(st, ev, 0);
     // 3. outputs: the launch produced the bytes U = union of the part slices
     //    (one interval); older copies of U anywhere are stale, bytes outside U
     //    keep their validity
@@ -395,6 +439,14 @@ struct HostContext::Impl {
         for (auto& [g, p] : b.pieces) p.valid_bytes = 0;
         b.pieces[g0].valid_first = 0;
         b.pieces[g0].valid_bytes = b.size;
+        continue;
+      }
+      if (k.classes[i] == HCL_PART_EXCHANGE) {  // whole on every participating device
+        for (auto& [g, p] : b.pieces) p.valid_bytes = 0;
+        for (const Part* p : live) {
+          b.pieces[p->gid].valid_first = 0;
+          b.pieces[p->gid].valid_bytes = b.size;
+        }
         continue;
       }
       if (!whole && k.classes[i] == HCL_PART_MERGE_TOPK) {

@@ -505,8 +505,9 @@ void register_graph(std::vector<KernelDef>& r) {
   // the implicit step fused with the next prep and the exchange: x' rows, xs' rows here and on
   // every peer (peers = device addresses of their xs', uint64[n_peers]), dangling partial dsum':
   // row_ptr col units long_rows xs dsum x' | V nnz_off n_units n_long warp_nnz | peers n_peers outdeg xs' dsum'
+  constexpr uint8_t XG = HCL_PART_EXCHANGE, PR = HCL_PART_PEERS, RS = HCL_PART_REDUCE_SUM;
   r.push_back({"b200", "pagerank_step_exchange", {I, I, I, I, I, I, O, S, S, S, S, S, I, S, I, O, O},
-               {P, P, P, P, P, P, X, N, N, N, N, N, P, N, P, P, P}, launch_pr<true, true, true>, nullptr,
+               {P, P, P, P, P, P, X, N, N, N, N, N, PR, N, P, XG, RS}, launch_pr<true, true, true>, nullptr,
                rows_pr_imp});
 }
 

@@ -24,13 +24,19 @@ DEFAULT_WARP_NNZ = 64  # measured best at scale 24 (profiles/r01_pagerank_experi
 class PageRank:
     def __init__(self, ctx: HostContext, queues: Sequence[Handle], row_ptr: np.ndarray, col_idx: np.ndarray,
                  val: np.ndarray, outdeg: np.ndarray, max_nnz: int = DEFAULT_WARP_NNZ,
-                 weights: Optional[Sequence[int]] = None, relabel: bool = False, implicit: bool = True):
+                 weights: Optional[Sequence[int]] = None, relabel: bool = False, implicit: bool = True,
+                 fused: bool = False):
         """relabel: store the graph degree-ordered (hcl_pagerank_relabel) so the
         hot ranks form a dense prefix of x; per-row sums are unchanged, and
         ranks()/spmv() map results back to the caller's vertex ids. implicit: the
         iteration uses pagerank_prep + pagerank_step_implicit (values folded into
         xs = x/outdeg, bit-identical products, no value stream)."""
         self.implicit = implicit
+        # fused: one partitioned pagerank_step_exchange per iteration -- each part writes its
+        # rows of x', the next gather input xs' into EVERY device's copy (EXCHANGE output,
+        # NVLink stores through the runtime-filled PEERS list) and its dangling partial
+        # (REDUCE_SUM); no prep pass and no copies of the rank vector between iterations
+        self.fused = fused and implicit
         self.ctx, self.queues = ctx, list(queues)
         self.perm = None
         if relabel:
@@ -72,16 +78,36 @@ class PageRank:
                     ctx.set_kernel_arg(kk, j, a)
             for j, a in enumerate([self.b_deg, self.b_dsum, self.b_xs, self.v]):
                 ctx.set_kernel_arg(self.k_prep, j + 1, a)
+        if self.fused:
+            P = len(self.queues)
+            self.b_xs2, self.b_dsum2 = [mk(self.v * 4), mk(self.v * 4)], [mk(8), mk(8)]
+            self.b_peers = mk(8 * max(1, P - 1))
+            self.k_prep0 = ctx.create_kernel(prog, "pagerank_prep")
+            for j, a in enumerate([self.b_x[0], self.b_deg, self.b_dsum2[0], self.b_xs2[0], self.v]):
+                ctx.set_kernel_arg(self.k_prep0, j, a)
+            self.k_stepx = [ctx.create_kernel(prog, "pagerank_step_exchange") for _ in range(2)]
+            for i, kk in enumerate(self.k_stepx):  # reads xs[i], dsum[i]; writes x rows, xs[1-i], dsum[1-i]
+                for j, a in enumerate([self.b_rp, self.b_col, self.b_units, self.b_long, self.b_xs2[i],
+                                       self.b_dsum2[i], self.b_x[0]] + self.tail +
+                                      [self.b_peers, P - 1, self.b_deg, self.b_xs2[1 - i], self.b_dsum2[1 - i]]):
+                    ctx.set_kernel_arg(kk, j, a)
         self.cur = 0
 
     def reset(self) -> None:
         x0 = np.full(self.v, np.float32(1.0 / self.v), np.float32)
         self.ctx.enqueue_write_buffer(self.queues[0], self.b_x[0], x0)
         self.cur = 0
+        if self.fused:  # iteration 0's gather input and dangling sum
+            self.ctx.enqueue_ndrange_kernel(self.queues[0], self.k_prep0)
 
     def iterate(self, iterations: int) -> None:
         ctx = self.ctx
         for _ in range(iterations):
+            if self.fused:
+                ctx.enqueue_ndrange_partitioned(self.k_stepx[self.cur], (self.v, 1, 1), 1, self.queues,
+                                                bounds=self.bounds)
+                self.cur = 1 - self.cur
+                continue
             if self.implicit:
                 ctx.set_kernel_arg(self.k_prep, 0, self.b_x[self.cur])
                 ctx.enqueue_ndrange_kernel(self.queues[0], self.k_prep)
@@ -99,7 +125,8 @@ class PageRank:
 
     def ranks(self) -> np.ndarray:
         self.finish()
-        return self._to_caller(self.ctx.enqueue_read_buffer(self.queues[0], self.b_x[self.cur]).view(np.float32))
+        bx = self.b_x[0] if self.fused else self.b_x[self.cur]
+        return self._to_caller(self.ctx.enqueue_read_buffer(self.queues[0], bx).view(np.float32))
 
     def _to_caller(self, r: np.ndarray) -> np.ndarray:
         if self.perm is None:
@@ -128,3 +155,6 @@ class PageRank:
             self.ctx.release(b)
         if self.implicit:
             self.ctx.release(self.b_xs)
+        if self.fused:
+            for b in (*self.b_xs2, *self.b_dsum2, self.b_peers):
+                self.ctx.release(b)
