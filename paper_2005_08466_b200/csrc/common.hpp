@@ -62,9 +62,11 @@ void cuda_check(cudaError_t e, const char* what, const char* file, int line);
 // Counts every CUDA kernel this library launches (the bench reports it as
 // gpu_launches). Kernel launch sites use HCL_LAUNCHED() right after <<<>>>.
 extern std::atomic<uint64_t> g_kernel_launches;
+extern thread_local uint64_t t_kernel_launches;  // this thread's share (graph capture counts)
 #define HCL_LAUNCHED()                                            \
   do {                                                            \
     ::hcl::g_kernel_launches.fetch_add(1, std::memory_order_relaxed); \
+    ++::hcl::t_kernel_launches;                                   \
     HCL_CUDA(cudaGetLastError());                                 \
   } while (0)
 
@@ -133,6 +135,9 @@ struct KernelDef {
   LaunchFn launch;
   RowBytesFn row_bytes;  // may be null when no SPLIT_ROWS argument
   RowsFn rows;           // may be null (then dim 0 must be given)
+  // the launch function only enqueues stream work (no host syncs): repeated
+  // identical launches are captured once into a CUDA graph and replayed
+  bool graphable = false;
 };
 
 const std::vector<KernelDef>& registry();

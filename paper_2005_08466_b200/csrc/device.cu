@@ -11,6 +11,7 @@
 #include <atomic>
 #include <cstring>
 #include <memory>
+#include <cstdlib>
 #include <mutex>
 #include <string>
 #include <unordered_map>
@@ -22,6 +23,7 @@
 namespace hcl {
 
 std::atomic<uint64_t> g_kernel_launches{0};
+thread_local uint64_t t_kernel_launches = 0;
 
 const char* error_code_name(ErrorCode code) {
   switch (code) {
@@ -70,6 +72,13 @@ struct Dep {
   cudaStream_t st = nullptr;
 };
 
+struct GraphEntry {
+  cudaGraphExec_t exec = nullptr;
+  uint64_t work = 0;
+  uint64_t kernels = 0;  // kernel launches captured (counted again at every replay)
+  bool seen = false;
+};
+
 struct DevAlloc {
   uint8_t* ptr = nullptr;
   uint64_t first_byte = 0;
@@ -100,6 +109,7 @@ struct Device {
   std::vector<cudaEvent_t> spare_sync;  // timing-disabled events for dependencies
   void* scratch = nullptr;
   size_t scratch_bytes = 0;
+  std::unordered_map<std::string, GraphEntry> graphs;  // captured launches (KernelDef::graphable)
 
   cudaEvent_t event() {
     if (!spare_events.empty()) {
@@ -218,6 +228,45 @@ uint8_t* range_ptr(DevAlloc& a, uint64_t offset, uint64_t len, uint64_t id, cons
                               std::to_string(a.first_byte + a.bytes) + ") of buffer " +
                               std::to_string(id));
   return a.ptr + (offset - a.first_byte);
+}
+
+bool graphs_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("HCL_GRAPH");
+    return !e || std::atoi(e) != 0;
+  }();
+  return on;
+}
+
+// Everything a graphable launch function's enqueued work depends on: the kernel,
+// arguments (device addresses and extents, scalars), the range, the device's SM
+// budget and scratch, and the launch-shaping environment knobs.
+std::string graph_key(const KernelDef* k, const std::vector<LaunchArg>& la, const LaunchCtx& c, const Device& d) {
+  std::string key;
+  auto put = [&key](const void* p, size_t n) { key.append(static_cast<const char*>(p), n); };
+  put(&k, sizeof(k));
+  for (const LaunchArg& a : la) {
+    put(&a.kind, sizeof(a.kind));
+    put(&a.scalar, sizeof(a.scalar));
+    put(&a.buf.ptr, sizeof(a.buf.ptr));
+    put(&a.buf.first_byte, sizeof(a.buf.first_byte));
+    put(&a.buf.bytes, sizeof(a.buf.bytes));
+  }
+  put(c.goff, sizeof(c.goff));
+  put(c.gsize, sizeof(c.gsize));
+  put(&c.dims, sizeof(c.dims));
+  put(&c.whole, sizeof(c.whole));
+  put(&d.sm_count, sizeof(d.sm_count));
+  put(&d.scratch, sizeof(d.scratch));
+  put(&d.scratch_bytes, sizeof(d.scratch_bytes));
+  for (const char* v : {"HCL_GEMM_SHAPE", "HCL_GEMM_CG", "HCL_GEMM_B_KMAJOR", "HCL_GEMM_GROUP", "HCL_GEMM_PROMO",
+                        "HCL_GEMM_TMAC", "HCL_GEMM_ONE", "HCL_GEMM_PERSIST", "HCL_GEMM_KSPLIT", "HCL_SIMT_MS",
+                        "HCL_SIMT_TILE"}) {
+    const char* e = std::getenv(v);
+    key += '|';
+    if (e) key += e;
+  }
+  return key;
 }
 
 void* scratch_for(int dev, size_t bytes) {
@@ -676,7 +725,40 @@ int hcl_launch(int dev, const char* kernel, const hcl_arg* args, uint32_t nargs,
         d.wait_for(alloc_of(d, args[i].buffer_id, kernel), d.stream, args[i].kind != HCL_ARG_IN);
     cudaEvent_t e0 = d.event(), e1 = d.event();
     HCL_CUDA(cudaEventRecord(e0, d.stream));
-    uint64_t w = k->launch(c);
+    uint64_t w = 0;
+    if (k->graphable && graphs_enabled()) {
+      // the second identical launch is captured into a CUDA graph, later ones replay it
+      // (same kernels, same work -- only the per-kernel launch gaps go)
+      GraphEntry& ge = d.graphs[graph_key(k, la, c, d)];
+      if (ge.exec) {
+        HCL_CUDA(cudaGraphLaunch(ge.exec, d.stream));
+        g_kernel_launches += ge.kernels;  // the replay launches the captured kernels again
+        w = ge.work;
+      } else if (ge.seen) {
+        HCL_CUDA(cudaStreamBeginCapture(d.stream, cudaStreamCaptureModeThreadLocal));
+        cudaGraph_t g = nullptr;
+        const uint64_t k0 = t_kernel_launches;
+        try {
+          w = k->launch(c);
+        } catch (...) {
+          cudaStreamEndCapture(d.stream, &g);
+          if (g) cudaGraphDestroy(g);
+          throw;
+        }
+        HCL_CUDA(cudaStreamEndCapture(d.stream, &g));
+        const cudaError_t ie = cudaGraphInstantiate(&ge.exec, g, 0);
+        cudaGraphDestroy(g);
+        HCL_CUDA(ie);
+        HCL_CUDA(cudaGraphLaunch(ge.exec, d.stream));
+        ge.work = w;
+        ge.kernels = t_kernel_launches - k0;  // counted once at capture = this launch
+      } else {
+        w = k->launch(c);
+        ge.seen = true;
+      }
+    } else {
+      w = k->launch(c);
+    }
     HCL_CUDA(cudaEventRecord(e1, d.stream));
     d.timed.emplace_back(e0, e1);
     for (uint32_t i = 0; i < nargs; ++i)

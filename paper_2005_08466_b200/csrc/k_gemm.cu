@@ -972,13 +972,13 @@ void register_gemm(std::vector<KernelDef>& r) {
   constexpr uint8_t S = HCL_ARG_SCALAR, I = HCL_ARG_IN, O = HCL_ARG_OUT;
   constexpr uint8_t N = HCL_PART_NONE, P = HCL_PART_REPLICATE, X = HCL_PART_SPLIT_ROWS;
   r.push_back({"b200", "gemm_bf16", {I, I, O, S, S, S, S}, {X, P, X, N, N, N, N}, launch_gemm_tc<false>,
-               rowbytes_gemm_bf16, rows_gemm});
+               rowbytes_gemm_bf16, rows_gemm, true});
   r.push_back({"b200", "gemm_tf32", {I, I, O, S, S, S}, {X, P, X, N, N, N}, launch_gemm_tc<true>,
-               rowbytes_gemm_f32, rows_gemm});
+               rowbytes_gemm_f32, rows_gemm, true});
   r.push_back({"b200", "gemm_f32", {I, I, O, S, S, S}, {X, P, X, N, N, N}, launch_gemm_f32, rowbytes_gemm_f32,
-               rows_gemm});
+               rows_gemm, true});
   r.push_back({"b200", "gemm_f32x3", {I, I, O, S, S, S}, {X, P, X, N, N, N}, launch_gemm_f32x3, rowbytes_gemm_f32,
-               rows_gemm});
+               rows_gemm, true});
 }
 
 }  // namespace hcl
