@@ -26,7 +26,7 @@
 //      with more than KT_QCAP survivors) is scanned exactly over all K by
 //      the whole verify warp.
 // On the C4 data (2^28 points, K=1024, 1024 Gaussian blobs) the filter keeps
-// 1.26 candidates per point on average (max 5; scripts in profiles/); at 2^26
+// 1.26 candidates per point on average (max 5; profiles/r01_kmeans_tc.txt); at 2^26
 // points 22% of the points keep several (0.48 exact checks per point) and
 // ~900 overflow (HCL_KM_DBG=16 prints these counts).
 //
@@ -92,7 +92,7 @@ constexpr int KT_BH = (KT_CW / 2) * 128;     // per CTA, chunk and split part: K
 #ifndef HCL_KT_LIST
 #define HCL_KT_LIST (16 / HCL_KT_GROUPS)
 #endif
-constexpr int KT_LIST = HCL_KT_LIST;         // candidate slots per point and scan group
+constexpr int KT_LIST = HCL_KT_LIST;         // list entries (32-column batches with candidates) per point and scan group
 constexpr int KT_KMAX = 1024;
 static_assert((KT_KMAX / KT_CW) * (KT_GCOLS / 32) <= 16, "list keys carry a 4-bit batch index");
 constexpr int KT_LBUF = KT_GROUPS * KT_ROWS * KT_LIST;  // float2 slots of one tile's lists (all groups)
@@ -105,7 +105,7 @@ struct KtLayout {
     a = b + static_cast<size_t>(nch) * 2 * KT_BH;
     q = a + static_cast<size_t>(KT_STAGES) * KT_A;
     lists = q + 4096;  // q: the constant "ones" A tile of the |c|^2 MMA (128 rows x 16 bf16, no swizzle)
-    xch = lists + 2ull * KT_LBUF * 8;             // 2 buffers x (t, k) float2 slots
+    xch = lists + 2ull * KT_LBUF * 8;             // 2 buffers x (key | batch index, mask) float2 entries
     vq = xch + 2ull * KT_GROUPS * KT_ROWS * 8 + 2ull * KT_ROWS * 4;  // 2 bufs x groups x (min, count|ovf) + 2 eps
     bars = vq + static_cast<size_t>(KT_VER) * 32 * KT_QCAP * 8;  // verify queues
     total = bars + 16 * 8 + 16 + 1024;            // barriers, TMEM slot, alignment slack
