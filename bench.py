@@ -548,10 +548,12 @@ class PageRankW(Workload):
                 bp = mk(arr.nbytes)
                 ctx.enqueue_write_buffer(q, bp, arr)
                 self.b_peers.append(bp)
+            self.b_inv = mk(self.v * 4)  # fl(1/outdeg), computed once per graph
+            ctx.enqueue_write_buffer(q, self.b_inv, G.pagerank_inv_outdeg(deg))
             for i in range(2):  # reads xs[i], dsum[i]; writes x rows, xs[1-i] (here + peers), dsum[1-i]
                 for j, a in enumerate([self.b_rp, self.b_col, self.b_u, self.b_l, self.b_xs2[i], self.b_dsum2[i],
                                        self.b_x[0], self.v, p0, len(units), n_long, wn, self.b_peers[1 - i],
-                                       d.world - 1, self.b_deg, self.b_xs2[1 - i], self.b_dsum2[1 - i]]):
+                                       d.world - 1, self.b_inv, self.b_xs2[1 - i], self.b_dsum2[1 - i]]):
                     ctx.set_kernel_arg(self.k_stepx[i], j, a)
             self.k_prep0 = ctx.create_kernel(prog, "pagerank_prep")  # x0 -> xs[0], dsum[0]
             for j, a in enumerate([self.b_x[0], self.b_deg, self.b_dsum2[0], self.b_xs2[0], self.v]):

@@ -101,7 +101,7 @@ __device__ __forceinline__ void pr_store(float* __restrict__ y, int r, int lo, f
 
 // Fused step (pagerank_step_exchange): besides x'[r], each row also yields the
 // next iteration's gather input xs'[r] = fl(1/outdeg(r)) * x'[r] (what
-// pagerank_prep computes, bit for bit), stored into this device's xs' and
+// pagerank_prep computes, bit for bit; the reciprocals come precomputed), stored into this device's xs' and
 // into every peer's xs' (NVLink stores into peer / IPC-mapped memory), and
 // dangling rows add x'[r] to dsum' (2^-56 fixed point, order-free). The
 // separate prep pass and the rank-vector allgather disappear; an allreduce
@@ -111,14 +111,14 @@ struct Fanout {
   float* p[PR_MAX_PEERS];
   int n;
   float* xs;            // this device's xs'
-  const int* outdeg;
+  const float* inv;     // fl(1/outdeg), 0 for dangling vertices
 };
 
-__device__ __forceinline__ Fanout load_fanout(const unsigned long long* peers, int n, float* xs, const int* outdeg) {
+__device__ __forceinline__ Fanout load_fanout(const unsigned long long* peers, int n, float* xs, const float* inv) {
   Fanout f;
   f.n = n;
   f.xs = xs;
-  f.outdeg = outdeg;
+  f.inv = inv;
 #pragma unroll
   for (int k = 0; k < PR_MAX_PEERS; ++k) f.p[k] = k < n ? reinterpret_cast<float*>(__ldg(peers + k)) : nullptr;
   return f;
@@ -130,13 +130,13 @@ __device__ __forceinline__ void pr_store_x(float* __restrict__ y, int r, int lo,
   pr_store<UPDATE>(y, r, lo, s, u);
   if constexpr (XCH) {
     const float v = y[r - lo];
-    const int d = __ldg(f.outdeg + r);
-    const float xs = d ? __fmul_rn(__fdiv_rn(1.0f, static_cast<float>(d)), v) : 0.f;
+    const float inv = __ldg(f.inv + r);  // the division is done once per graph, not per step
+    const float xs = __fmul_rn(inv, v);
     f.xs[r] = xs;
 #pragma unroll
     for (int k = 0; k < PR_MAX_PEERS; ++k)
       if (k < f.n) f.p[k][r] = xs;
-    if (d == 0) dang += static_cast<unsigned long long>(__float2ll_rz(__fmul_rn(v, 0x1p56f)));
+    if (inv == 0.f) dang += static_cast<unsigned long long>(__float2ll_rz(__fmul_rn(v, 0x1p56f)));
   }
 }
 
@@ -196,7 +196,7 @@ __global__ void __launch_bounds__(PR_T) pr_units_kernel(const int* __restrict__ 
                                                         float* __restrict__ y, int lo, int hi, float base, float damp,
                                                         float inv_v, int warp_nnz, float* __restrict__ chunk_tot,
                                                         const unsigned long long* __restrict__ peers, int n_peers,
-                                                        const int* __restrict__ outdeg, float* __restrict__ xs_next,
+                                                        const float* __restrict__ inv_outdeg, float* __restrict__ xs_next,
                                                         unsigned long long* __restrict__ dsum_next) {
   extern __shared__ float prod_all[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -204,7 +204,7 @@ __global__ void __launch_bounds__(PR_T) pr_units_kernel(const int* __restrict__ 
   const Update upd = pr_update<UPDATE>(dsum, base, damp, inv_v);
   Fanout fo{};
   unsigned long long dang = 0;
-  if constexpr (XCH) fo = load_fanout(peers, n_peers, xs_next, outdeg);
+  if constexpr (XCH) fo = load_fanout(peers, n_peers, xs_next, inv_outdeg);
   // units overlapping [lo, hi): row1 > lo and row0 < hi (both monotone in u)
   int a = 0, b = n_units;
   while (a < b) {
@@ -275,7 +275,7 @@ template <bool UPDATE, bool XCH = false>
 __global__ void pr_fixup_kernel(const int* __restrict__ long_rows, int n_long, const float* __restrict__ chunk_tot,
                                 const unsigned long long* __restrict__ dsum, float* __restrict__ y, int lo, int hi,
                                 float base, float damp, float inv_v, const unsigned long long* __restrict__ peers,
-                                int n_peers, const int* __restrict__ outdeg, float* __restrict__ xs_next,
+                                int n_peers, const float* __restrict__ inv_outdeg, float* __restrict__ xs_next,
                                 unsigned long long* __restrict__ dsum_next) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   unsigned long long dang = 0;
@@ -286,7 +286,7 @@ __global__ void pr_fixup_kernel(const int* __restrict__ long_rows, int n_long, c
       float total = chunk_tot[u0];
       for (int c = 1; c < nc; ++c) total = __fadd_rn(total, chunk_tot[u0 + c]);
       Fanout fo{};
-      if constexpr (XCH) fo = load_fanout(peers, n_peers, xs_next, outdeg);
+      if constexpr (XCH) fo = load_fanout(peers, n_peers, xs_next, inv_outdeg);
       pr_store_x<UPDATE, XCH>(y, row, lo, total, pr_update<UPDATE>(dsum, base, damp, inv_v), fo, dang);
     }
   }
@@ -362,10 +362,10 @@ uint64_t launch_pr(LaunchCtx& c) {
   }
   const unsigned long long* peers = nullptr;
   int n_peers = 0;
-  const int* outdeg = nullptr;
+  const float* inv_outdeg = nullptr;
   float* xs_next = nullptr;
   unsigned long long* dsum_next = nullptr;
-  if (XCH) {  // peers (device addresses of the peers' xs'), their count, outdeg, xs', dsum'
+  if (XCH) {  // peers (device addresses of the peers' xs'), their count, inv_outdeg, xs', dsum'
     n_peers = static_cast<int>(scalar_arg(c, s0 + 6, what));
     const BufView& PB = buffer_arg(c, s0 + 5, what);
     if (n_peers < 0 || n_peers > PR_MAX_PEERS || PB.first_byte != 0 || PB.bytes < static_cast<uint64_t>(n_peers) * 8)
@@ -376,8 +376,8 @@ uint64_t launch_pr(LaunchCtx& c) {
     const BufView& DN = buffer_arg(c, s0 + 9, what);
     if (OD.first_byte != 0 || OD.bytes != static_cast<uint64_t>(v) * 4 || XN.first_byte != 0 ||
         XN.bytes != static_cast<uint64_t>(v) * 4 || DN.bytes != 8)
-      fail(ErrorCode::argument, std::string(what) + ": outdeg and xs' must hold V elements, dsum' one uint64");
-    outdeg = reinterpret_cast<const int*>(OD.ptr);
+      fail(ErrorCode::argument, std::string(what) + ": inv_outdeg and xs' must hold V elements, dsum' one uint64");
+    inv_outdeg = reinterpret_cast<const float*>(OD.ptr);
     xs_next = reinterpret_cast<float*>(XN.ptr);
     dsum_next = reinterpret_cast<unsigned long long*>(DN.ptr);
     HCL_CUDA(cudaMemsetAsync(dsum_next, 0, 8, c.stream));
@@ -412,12 +412,12 @@ uint64_t launch_pr(LaunchCtx& c) {
                                        reinterpret_cast<const int4*>(U.ptr), static_cast<int>(n_units),
                                        reinterpret_cast<const float*>(X.ptr), dsum, y, static_cast<int>(lo),
                                        static_cast<int>(lo + rows), base, damp, inv_v, static_cast<int>(warp_nnz),
-                                       chunk_tot, peers, n_peers, outdeg, xs_next, dsum_next);
+                                       chunk_tot, peers, n_peers, inv_outdeg, xs_next, dsum_next);
   HCL_LAUNCHED();
   if (n_long) {
     pr_fixup_kernel<UPDATE, XCH><<<static_cast<unsigned>(ceil_div(n_long, 128)), 128, 0, c.stream>>>(
         reinterpret_cast<const int*>(L.ptr), static_cast<int>(n_long), chunk_tot, dsum, y, static_cast<int>(lo),
-        static_cast<int>(lo + rows), base, damp, inv_v, peers, n_peers, outdeg, xs_next, dsum_next);
+        static_cast<int>(lo + rows), base, damp, inv_v, peers, n_peers, inv_outdeg, xs_next, dsum_next);
     HCL_LAUNCHED();
   }
   return 2ull * static_cast<uint64_t>(rp[1] - rp[0]);
@@ -504,7 +504,8 @@ void register_graph(std::vector<KernelDef>& r) {
                {P, P, P, P, P, P, X, N, N, N, N, N}, launch_pr<true, true>, nullptr, rows_pr_imp});
   // the implicit step fused with the next prep and the exchange: x' rows, xs' rows here and on
   // every peer (peers = device addresses of their xs', uint64[n_peers]), dangling partial dsum':
-  // row_ptr col units long_rows xs dsum x' | V nnz_off n_units n_long warp_nnz | peers n_peers outdeg xs' dsum'
+  // row_ptr col units long_rows xs dsum x' | V nnz_off n_units n_long warp_nnz | peers n_peers inv_outdeg xs' dsum'
+  // (inv_outdeg = fl(1/outdeg) as fp32, 0 for dangling vertices: datagen.pagerank_inv_outdeg)
   constexpr uint8_t XG = HCL_PART_EXCHANGE, PR = HCL_PART_PEERS, RS = HCL_PART_REDUCE_SUM;
   r.push_back({"b200", "pagerank_step_exchange", {I, I, I, I, I, I, O, S, S, S, S, S, I, S, I, O, O},
                {P, P, P, P, P, P, X, N, N, N, N, N, PR, N, P, XG, RS}, launch_pr<true, true, true>, nullptr,

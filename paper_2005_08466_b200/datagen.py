@@ -108,3 +108,14 @@ def csr_row_blocks(row_ptr: np.ndarray, max_nnz: int) -> np.ndarray:
     out = np.empty(n + 1, np.int32)
     N.lib().hcl_csr_row_blocks(rp.ctypes.data, len(rp) - 1, max_nnz, out.ctypes.data)
     return out
+
+
+def pagerank_inv_outdeg(outdeg: np.ndarray) -> np.ndarray:
+    """fp32 fl(1/outdeg) per vertex, 0 for dangling vertices: the reciprocal the CSR
+    builder stores as val (IEEE round-to-nearest division, as __fdiv_rn), computed
+    once per graph for pagerank_step_exchange."""
+    d = np.asarray(outdeg, np.int32)
+    inv = np.zeros(len(d), np.float32)
+    nz = d > 0
+    inv[nz] = np.float32(1.0) / d[nz].astype(np.float32)
+    return inv

@@ -15,7 +15,7 @@ from typing import Optional, Sequence
 
 import numpy as np
 
-from .datagen import pagerank_relabel, pagerank_units
+from .datagen import pagerank_inv_outdeg, pagerank_relabel, pagerank_units
 from .runtime import Handle, HostContext, spmv_partition_ranges
 
 DEFAULT_WARP_NNZ = 64  # measured best at scale 24 (profiles/r01_pagerank_experiments.txt)
@@ -81,6 +81,8 @@ class PageRank:
         if self.fused:
             P = len(self.queues)
             self.b_xs2, self.b_dsum2 = [mk(self.v * 4), mk(self.v * 4)], [mk(8), mk(8)]
+            self.b_inv = mk(self.v * 4)
+            ctx.enqueue_write_buffer(q0, self.b_inv, pagerank_inv_outdeg(outdeg))
             self.b_peers = mk(8 * max(1, P - 1))
             self.k_prep0 = ctx.create_kernel(prog, "pagerank_prep")
             for j, a in enumerate([self.b_x[0], self.b_deg, self.b_dsum2[0], self.b_xs2[0], self.v]):
@@ -89,7 +91,7 @@ class PageRank:
             for i, kk in enumerate(self.k_stepx):  # reads xs[i], dsum[i]; writes x rows, xs[1-i], dsum[1-i]
                 for j, a in enumerate([self.b_rp, self.b_col, self.b_units, self.b_long, self.b_xs2[i],
                                        self.b_dsum2[i], self.b_x[0]] + self.tail +
-                                      [self.b_peers, P - 1, self.b_deg, self.b_xs2[1 - i], self.b_dsum2[1 - i]]):
+                                      [self.b_peers, P - 1, self.b_inv, self.b_xs2[1 - i], self.b_dsum2[1 - i]]):
                     ctx.set_kernel_arg(kk, j, a)
         self.cur = 0
 
@@ -156,5 +158,5 @@ class PageRank:
         if self.implicit:
             self.ctx.release(self.b_xs)
         if self.fused:
-            for b in (*self.b_xs2, *self.b_dsum2, self.b_peers):
+            for b in (*self.b_xs2, *self.b_dsum2, self.b_peers, self.b_inv):
                 self.ctx.release(b)

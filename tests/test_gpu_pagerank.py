@@ -30,6 +30,15 @@ def test_product_csr_matches_oracle(graph):
     assert val.tobytes() == val2.tobytes()
 
 
+def test_inv_outdeg_matches_csr_values(graph):
+    """The fused step's precomputed reciprocals are the CSR's stored values
+    (val[p] = fl(1/outdeg(col[p]))) bit for bit, 0 exactly for dangling vertices."""
+    rp, ci, val, deg = graph
+    inv = G.pagerank_inv_outdeg(deg)
+    assert inv[ci].tobytes() == val.tobytes()
+    assert ((inv == 0) == (deg == 0)).all()
+
+
 def test_row_blocks_properties(graph):
     rp = graph[0]
     for mx in (1, 16, 300, 4096):
@@ -274,6 +283,7 @@ def test_step_exchange_fused(ctx, queues, graph, P):
     try:
         for d in range(P):
             for name, arr in (("rp", rp), ("col", ci), ("units", units), ("long", long_rows), ("deg", deg),
+                              ("inv", G.pagerank_inv_outdeg(deg)),
                               ("x", x0), ("xs0", np.zeros(v, np.float32)), ("xs1", np.zeros(v, np.float32)),
                               ("dsum0", np.zeros(1, np.uint64)), ("dsum1", np.zeros(1, np.uint64))):
                 put(d, name, arr)
@@ -292,7 +302,7 @@ def test_step_exchange_fused(ctx, queues, graph, P):
                        [(I_, bid(d, "rp")), (I_, bid(d, "col")), (I_, bid(d, "units")), (I_, bid(d, "long")),
                         (I_, bid(d, f"xs{cur}")), (I_, bid(d, f"dsum{cur}")), (O_, bid(d, "x")), (S_, v), (S_, 0),
                         (S_, len(units)), (S_, n_long), (S_, 64), (I_, bid(d, f"peers{nxt}")), (S_, P - 1),
-                        (I_, bid(d, "deg")), (O_, bid(d, f"xs{nxt}")), (O_, bid(d, f"dsum{nxt}"))],
+                        (I_, bid(d, "inv")), (O_, bid(d, f"xs{nxt}")), (O_, bid(d, f"dsum{nxt}"))],
                        lo=bounds[d], rows=bounds[d + 1] - bounds[d])
             for d in range(P):  # every device's stores have landed
                 N.check(L.hcl_finish(d, None))
