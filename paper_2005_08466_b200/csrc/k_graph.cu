@@ -92,11 +92,11 @@ struct Update {
 };
 
 template <bool UPDATE>
-__device__ __forceinline__ void pr_store(float* __restrict__ y, int r, int lo, float s, const Update& u) {
-  if constexpr (UPDATE)
-    y[r - lo] = __fadd_rn(u.base, __fmul_rn(u.damp, __fadd_rn(s, u.t)));
-  else
-    y[r - lo] = s;
+__device__ __forceinline__ float pr_store(float* __restrict__ y, int r, int lo, float s, const Update& u) {
+  float v = s;
+  if constexpr (UPDATE) v = __fadd_rn(u.base, __fmul_rn(u.damp, __fadd_rn(s, u.t)));
+  y[r - lo] = v;
+  return v;
 }
 
 // Fused step (pagerank_step_exchange): besides x'[r], each row also yields the
@@ -127,9 +127,8 @@ __device__ __forceinline__ Fanout load_fanout(const unsigned long long* peers, i
 template <bool UPDATE, bool XCH>
 __device__ __forceinline__ void pr_store_x(float* __restrict__ y, int r, int lo, float s, const Update& u,
                                            const Fanout& f, unsigned long long& dang) {
-  pr_store<UPDATE>(y, r, lo, s, u);
+  const float v = pr_store<UPDATE>(y, r, lo, s, u);
   if constexpr (XCH) {
-    const float v = y[r - lo];
     const float inv = __ldg(f.inv + r);  // the division is done once per graph, not per step
     const float xs = __fmul_rn(inv, v);
     f.xs[r] = xs;
