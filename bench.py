@@ -488,7 +488,16 @@ class PageRankW(Workload):
         ctx.add_data_creation_ms((time.perf_counter() - t0) * 1e3)
         self.wn = wn = int(os.environ.get("BENCH_PR_WARP_NNZ", "64"))
         units, long_rows, n_long = G.pagerank_units(rp, wn)
-        self.bounds = [int(x) for x in spmv_partition_ranges(rp.astype(np.int64), d.world)]
+        # rows balanced on a cost model, not on nnz alone: with the fused step every row also
+        # costs its x'/xs' stores (one per rank). Measured per rank at N=4 (BENCH_PR_RANK_TIMES=1):
+        # nnz-balanced ranges take 0.40 / 0.43 / 0.49 / 0.61 ms (0.45M .. 9.4M rows of equal nnz);
+        # cost(row) = nnz + BENCH_PR_ROW_COST * N gives 3.59 (0) / 3.81 (1.0) / 4.02 (1.5) /
+        # 4.22 (2.2) / 4.25 (2.8) TB/s at N=4 and 2.81 (1.0) / 2.98 (2.2) TB/s at N=2
+        fused_step = (os.environ.get("BENCH_PR_IMPLICIT", "1") == "1"
+                      and os.environ.get("BENCH_PR_EXCHANGE", "1") == "1")
+        row_cost = float(os.environ.get("BENCH_PR_ROW_COST", "2.5")) * (d.world if fused_step else 0)
+        cum = rp.astype(np.int64) + np.round(row_cost * np.arange(len(rp))).astype(np.int64)
+        self.bounds = [int(x) for x in spmv_partition_ranges(cum, d.world)]
         lo, hi = self.bounds[d.rank], self.bounds[d.rank + 1]
         self.lo, self.rows = lo, hi - lo
         p0, p1 = int(rp[lo]), int(rp[hi])
@@ -590,6 +599,20 @@ class PageRankW(Workload):
             assert xs_r.tobytes() == xs_f.tobytes(), "pagerank_step_exchange xs' differs from prep(allgathered x')"
             d.barrier()
         self.reset()
+        if os.environ.get("BENCH_PR_RANK_TIMES") == "1" and self.fused:  # diagnostics: per-rank kernel time
+            import torch
+
+            st = self.stream()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            for _ in range(10):
+                self.step_kernel()
+            e1.record(st)
+            ctx.finish(q)
+            print(f"rank {d.rank}: rows {self.rows} nnz {self.nnz_local} fused kernel "
+                  f"{e0.elapsed_time(e1) / 10:.4f} ms", file=sys.stderr, flush=True)
+            d.barrier()
+            self.reset()
 
     def reset(self):
         ctx, q = self.ctx, self.q
