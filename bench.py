@@ -492,10 +492,13 @@ class PageRankW(Workload):
         # costs its x'/xs' stores (one per rank). Measured per rank at N=4 (BENCH_PR_RANK_TIMES=1):
         # nnz-balanced ranges take 0.40 / 0.43 / 0.49 / 0.61 ms (0.45M .. 9.4M rows of equal nnz);
         # cost(row) = nnz + BENCH_PR_ROW_COST * N gives 3.59 (0) / 3.81 (1.0) / 4.02 (1.5) /
-        # 4.22 (2.2) / 4.25 (2.8) TB/s at N=4 and 2.81 (1.0) / 2.98 (2.2) TB/s at N=2
+        # 4.22 (2.2) / 4.25 (2.8) TB/s at N=4 and 2.81 (1.0) / 2.98 (2.2) TB/s at N=2. A
+        # least-squares refit from the ranks' measured times (t = a*nnz + b*rows) landed on
+        # ~10 nnz per row at N=4 and no faster split: the residual imbalance is not linear
+        # in (nnz, rows) -- gather locality differs between the hub rows and the tail
         fused_step = (os.environ.get("BENCH_PR_IMPLICIT", "1") == "1"
                       and os.environ.get("BENCH_PR_EXCHANGE", "1") == "1")
-        row_cost = float(os.environ.get("BENCH_PR_ROW_COST", "2.5")) * (d.world if fused_step else 0)
+        self.row_cost = row_cost = float(os.environ.get("BENCH_PR_ROW_COST", "2.5")) * (d.world if fused_step else 0)
         cum = rp.astype(np.int64) + np.round(row_cost * np.arange(len(rp))).astype(np.int64)
         self.bounds = [int(x) for x in spmv_partition_ranges(cum, d.world)]
         lo, hi = self.bounds[d.rank], self.bounds[d.rank + 1]
@@ -600,18 +603,8 @@ class PageRankW(Workload):
             d.barrier()
         self.reset()
         if os.environ.get("BENCH_PR_RANK_TIMES") == "1" and self.fused:  # diagnostics: per-rank kernel time
-            import torch
-
-            st = self.stream()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(st)
-            for _ in range(10):
-                self.step_kernel()
-            e1.record(st)
-            ctx.finish(q)
             print(f"rank {d.rank}: rows {self.rows} nnz {self.nnz_local} fused kernel "
-                  f"{e0.elapsed_time(e1) / 10:.4f} ms", file=sys.stderr, flush=True)
-            d.barrier()
+                  f"{self.rank_kernel_ms():.4f} ms", file=sys.stderr, flush=True)
             self.reset()
 
     def reset(self):
@@ -646,6 +639,21 @@ class PageRankW(Workload):
         if self.dist.world > 1:
             ctx.enqueue_allgather(q, self.b_x[1 - self.cur], self.byte_bounds)
         self.cur = 1 - self.cur
+
+    def rank_kernel_ms(self, n=10):
+        """This rank's fused-kernel time (CUDA events, n launches after a reset)."""
+        import torch
+
+        self.reset()
+        st = self.stream()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        for _ in range(n):
+            self.step_kernel()
+        e1.record(st)
+        self.ctx.finish(self.q)
+        self.dist.barrier()
+        return e0.elapsed_time(e1) / n
 
     def step_kernel(self):  # the fused step's kernel alone (no collective): the dominant launch
         self.ctx.enqueue_ndrange_range(self.q, self.k_stepx[self.cur], (self.v, 1, 1), 1, self.lo, self.rows)
@@ -690,6 +698,7 @@ class PageRankW(Workload):
                 "vertex_ids": "out-degree ordered (hcl_pagerank_relabel; per-row sums unchanged)" if self.relabel
                 else "R-MAT ids", "warp_nnz": self.wn,
                 "algorithmic_bytes_per_iteration": self.work_per_step(), "rank_sum_err": self.check,
+                "row_cost_nnz_per_row": self.row_cost,
                 "l2": "2.35 GB streamed per iteration > L2"}
 
     @staticmethod
