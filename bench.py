@@ -206,6 +206,10 @@ class Workload:
     # per-launch traffic at other N (or other kernels) is not measured -> null
     traffic_key = None
 
+    def l2_flush_bytes(self):
+        """Bytes to write between timed steps when the inputs fit in L2 (0: inputs > L2)."""
+        return 0
+
     def traffic(self):
         prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
         if self.dist.world != 1 or not self.traffic_key or not os.path.exists(prof):
@@ -438,10 +442,16 @@ class GemmF32(Workload):
         sm = pk.get("sm_max_mhz", 1965.0)
         return "fp32_simt", 148 * 128 * 2 * sm * 1e6 / 1e12, "TFLOP/s", 1e12, "derived FFMA peak at max SM clock"
 
+    def l2_flush_bytes(self):
+        # A, B and C (3 * S^2 * 4 bytes) fit in the 126 MB L2 up to S ~ 3000
+        return 256 << 20 if 3 * self.S * self.S * 4 < (126 << 20) else 0
+
     def config(self):
         cfg = "C1" if self.S == 1024 else "C2 fp32"
         return {"workload": f"fp32 GEMM {self.S}^3 ({cfg}) via the host API on one device ({self.kernel})",
-                "replicas": self.dist.world, "normwise_err": self.check}
+                "replicas": self.dist.world, "normwise_err": self.check,
+                "l2": ("inputs fit in L2: 256 MB flush write before every timed step, per-step CUDA events"
+                       if self.l2_flush_bytes() else f"inputs {3 * self.S * self.S * 4 >> 20} MB > L2; no flush")}
 
     @staticmethod
     def reference_sampler():
@@ -814,7 +824,8 @@ class KMeansW(Workload):
                             f"assignment (3 flop/term), int64 sums, points split over {self.dist.world} rank(s)",
                 "assign_kernel": "kmeans_assign_tc (tcgen05 split-bf16 filter + exact fp32 verify)" if self.tc
                 else "kmeans_assign (exact fp32 SIMT)",
-                "points": "SplitMix64 blobs, multiples of 2^-12, generated in HBM"}
+                "points": "SplitMix64 blobs, multiples of 2^-12, generated in HBM",
+                "l2": f"points {self.N * self.D * 4 >> 30} GiB > L2; no flush"}
 
     @staticmethod
     def reference_sampler():
@@ -914,7 +925,9 @@ class ConvW(Workload):
     def config(self):
         return {"workload": f"conv3x3 (C5): batch {self.N}, {self.H}x{self.W}x{self.C} -> {self.K}, stride 1 pad 1, "
                             f"bf16 in/out, fp32 accumulate, batch split over {self.dist.world} rank(s)",
-                "layout": "padded NHWC input, KRSC weights, NHWK output"}
+                "layout": "padded NHWC input, KRSC weights, NHWK output",
+                "l2": f"input {self.N * (self.H + 2) * (self.W + 2) * self.C * 2 >> 20} MB and output "
+                      f"{self.N * self.H * self.W * self.K * 2 >> 20} MB > L2; no flush"}
 
     @staticmethod
     def reference_sampler():
@@ -997,11 +1010,25 @@ def run_b200(args):
     if sampler:
         sampler.mark()
     launches0 = N.lib().hcl_kernel_launch_count()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(args.steps):
-        wl.step()
-    e1.record(stream)
+    flush = wl.l2_flush_bytes()
+    if flush:
+        # inputs smaller than L2: every timed step starts from a flushed L2 (a write
+        # larger than L2 on the same stream, outside the per-step event pairs)
+        fbuf = torch.empty(flush // 4, dtype=torch.float32, device=torch.device("cuda", dist.local))
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(args.steps)]
+        for a, b in evs:
+            with torch.cuda.stream(stream):
+                fbuf.zero_()
+            a.record(stream)
+            wl.step()
+            b.record(stream)
+    else:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            wl.step()
+        e1.record(stream)
     wl.ctx.finish(wl.q)
     dist.barrier()
     launches = N.lib().hcl_kernel_launch_count() - launches0
@@ -1017,7 +1044,7 @@ def run_b200(args):
         need_hold = dist.allmax(1.0 if (sampler and sampler.count() < 3 and hold_ms < 3000) else 0.0) > 0
     if sampler:
         sampler.end()
-    dev_ms = e0.elapsed_time(e1)
+    dev_ms = sum(a.elapsed_time(b) for a, b in evs) if flush else e0.elapsed_time(e1)
     ms_max = dist.allmax(dev_ms)
     launches_total = int(dist.allsum(launches))
 
