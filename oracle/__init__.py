@@ -456,3 +456,28 @@ def ref_execute(kernel: str, args, out_caps, threads: int = 1):
                             threads, C.byref(work))
     res = {i: outs[i][: int(lens[i])] for i in outs}
     return rc, int(work.value), res
+
+
+def ref_pagerank(row_ptr, col_idx, outdeg, iterations: int, d: float = 0.85, threads: int = 0) -> np.ndarray:
+    """PageRank iterated on the REFERENCE LIBRARY's spmv_compute (fp64 values,
+    int64 CSR: proj/src/kernels.cpp:132-152 through kernels::execute), with the
+    damping, teleport and dangling mass applied here in fp64:
+    x' = (1-d)/V + d (A x + dangling(x)/V), A_vu = 1/outdeg(u), x0 = 1/V."""
+    import os
+
+    v = len(row_ptr) - 1
+    hdr = np.array([v, v], np.int64)
+    rp64 = np.ascontiguousarray(row_ptr, np.int64)
+    ci64 = np.ascontiguousarray(col_idx, np.int64)
+    deg = np.asarray(outdeg)
+    val64 = 1.0 / deg[col_idx].astype(np.float64)
+    x = np.full(v, 1.0 / v)
+    for _ in range(iterations):
+        dang = float(x[deg == 0].sum())
+        rc, _, out = ref_execute("spmv_compute", [("in", hdr), ("in", rp64), ("in", ci64), ("in", val64), ("in", x),
+                                                  ("s", 0), ("s", v), ("out", None)], {7: v * 8},
+                                 threads=threads or os.cpu_count() or 1)
+        if rc != 0:
+            raise RuntimeError(f"reference spmv_compute failed: {rc}")
+        x = (1.0 - d) / v + d * (out[7].view(np.float64) + dang / v)
+    return x

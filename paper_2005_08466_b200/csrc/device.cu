@@ -834,21 +834,30 @@ int hcl_collective(int op, const int* devs, int ndev, const uint64_t* buf_ids, u
 int hcl_finish(int dev, double* device_ms) {
   return guarded([&] {
     Device& d = device(dev);
-    std::lock_guard<std::mutex> lock(d.mu);
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> timed;
+    {
+      std::lock_guard<std::mutex> lock(d.mu);
+      timed.swap(d.timed);
+    }
+    // the streams are fixed for the device's lifetime: synchronize them without
+    // the device lock so other threads keep issuing work meanwhile
     HCL_CUDA(cudaSetDevice(d.ordinal));
     HCL_CUDA(cudaStreamSynchronize(d.h2d));
     HCL_CUDA(cudaStreamSynchronize(d.stream));
     HCL_CUDA(cudaStreamSynchronize(d.comm));
     HCL_CUDA(cudaStreamSynchronize(d.d2h));
     double total = 0.0;
-    for (auto& [a, b] : d.timed) {
+    for (auto& [a, b] : timed) {
       float ms = 0.f;
+      HCL_CUDA(cudaEventSynchronize(b));
       HCL_CUDA(cudaEventElapsedTime(&ms, a, b));
       total += ms;
+    }
+    std::lock_guard<std::mutex> lock(d.mu);
+    for (auto& [a, b] : timed) {
       d.spare_events.push_back(a);
       d.spare_events.push_back(b);
     }
-    d.timed.clear();
     if (device_ms) *device_ms = total;
   });
 }

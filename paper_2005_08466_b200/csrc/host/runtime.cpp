@@ -20,6 +20,7 @@
 #include <cstdio>
 #include <cstring>
 #include <map>
+#include <memory>
 #include <mutex>
 #include <set>
 
@@ -71,9 +72,62 @@ void MessageTrace::clear() {
 }
 
 struct HostContext::Impl {
+  // Disjoint, non-adjacent byte intervals [first, end) kept in a sorted map.
+  struct Ranges {
+    std::map<uint64_t, uint64_t> m;  // first -> end
+    bool empty() const { return m.empty(); }
+    void clear() { m.clear(); }
+    void add(uint64_t first, uint64_t len) {
+      if (!len) return;
+      uint64_t f = first, e = first + len;
+      auto it = m.upper_bound(f);
+      if (it != m.begin()) {
+        auto pv = std::prev(it);
+        if (pv->second >= f) it = pv;  // overlaps or touches the previous interval
+      }
+      while (it != m.end() && it->first <= e) {
+        f = std::min(f, it->first);
+        e = std::max(e, it->second);
+        it = m.erase(it);
+      }
+      m.emplace(f, e);
+    }
+    void sub(uint64_t first, uint64_t len) {
+      if (!len) return;
+      const uint64_t f = first, e = first + len;
+      auto it = m.upper_bound(f);
+      if (it != m.begin() && std::prev(it)->second > f) --it;
+      while (it != m.end() && it->first < e) {
+        const uint64_t a = it->first, b = it->second;
+        it = m.erase(it);
+        if (a < f) m.emplace(a, f);
+        if (b > e) {
+          m.emplace(e, b);
+          break;
+        }
+      }
+    }
+    // end of the interval holding `pos`, or 0 when no interval holds it
+    uint64_t holds(uint64_t pos) const {
+      auto it = m.upper_bound(pos);
+      if (it == m.begin()) return 0;
+      --it;
+      return pos < it->second ? it->second : 0;
+    }
+    bool covers(uint64_t first, uint64_t len) const {
+      if (!len) return true;
+      const uint64_t e = holds(first);
+      return e && e >= first + len;
+    }
+    // first interval start strictly after `pos` (UINT64_MAX if none)
+    uint64_t next_start(uint64_t pos) const {
+      auto it = m.upper_bound(pos);
+      return it == m.end() ? UINT64_MAX : it->first;
+    }
+  };
   struct Piece {
     uint64_t alloc_first = 0, alloc_bytes = 0;
-    uint64_t valid_first = 0, valid_bytes = 0;  // one valid interval inside the allocation
+    Ranges valid;  // valid byte intervals inside the allocation
     bool allocated = false;
   };
   struct BufferRec {
@@ -92,6 +146,9 @@ struct HostContext::Impl {
     bool shared = true;
     double transfer_ms = 0.0, compute_ms = 0.0, modeled_ms = 0.0;
     std::vector<Launch> pending;
+    // serializes finish() per queue; the table lock is never held across a
+    // device synchronization (the reference's per-queue mutex, runtime.cpp:60-64)
+    std::shared_ptr<std::mutex> op_mu = std::make_shared<std::mutex>();
   };
   struct ProgramRec {
     std::string bundle;
@@ -172,17 +229,17 @@ struct HostContext::Impl {
       nf = std::min(nf, p.alloc_first);
       ne = std::max(ne, p.alloc_first + p.alloc_bytes);
     }
-    if (p.allocated && p.valid_bytes) {
-      // preserve valid bytes through a temporary buffer on the same device
-      uint64_t tmp = new_id();
-      check(hcl_buffer_alloc(dev, tmp, p.valid_first, p.valid_bytes));
-      check(hcl_buffer_copy_peer(dev, tmp, p.valid_first, dev, id, p.valid_first, p.valid_bytes));
+    if (p.allocated && !p.valid.empty()) {
+      // preserve every valid interval through a temporary buffer on the same device
+      const uint64_t tmp = new_id(), of = p.alloc_first;
+      check(hcl_buffer_alloc(dev, tmp, of, p.alloc_bytes));
+      for (auto& [a, e] : p.valid.m) check(hcl_buffer_copy_peer(dev, tmp, a, dev, id, a, e - a));
       check(hcl_buffer_alloc(dev, id, nf, ne - nf));
-      check(hcl_buffer_copy_peer(dev, id, p.valid_first, dev, tmp, p.valid_first, p.valid_bytes));
+      for (auto& [a, e] : p.valid.m) check(hcl_buffer_copy_peer(dev, id, a, dev, tmp, a, e - a));
       check(hcl_buffer_release(dev, tmp));
     } else {
       check(hcl_buffer_alloc(dev, id, nf, ne - nf));
-      p.valid_bytes = 0;
+      p.valid.clear();
     }
     trace.record({gid, "alloc_buffer", id});
     p.allocated = true;
@@ -191,74 +248,48 @@ struct HostContext::Impl {
     return p;
   }
 
-  static void set_valid(Piece& p, uint64_t first, uint64_t len) {
-    if (!len) return;
-    if (p.valid_bytes && first <= p.valid_first + p.valid_bytes && p.valid_first <= first + len) {
-      uint64_t f = std::min(first, p.valid_first);
-      uint64_t e = std::max(first + len, p.valid_first + p.valid_bytes);
-      p.valid_first = f;
-      p.valid_bytes = e - f;
-    } else {
-      p.valid_first = first;
-      p.valid_bytes = len;
-    }
-  }
+  static void set_valid(Piece& p, uint64_t first, uint64_t len) { p.valid.add(first, len); }
 
   // Other devices' copies of [first, first+len) are stale after a write there.
   static void invalidate_others(BufferRec& b, int gid, uint64_t first, uint64_t len) {
-    uint64_t e = first + len;
-    for (auto& [g, p] : b.pieces) {
-      if (g == gid || !p.valid_bytes) continue;
-      uint64_t vf = p.valid_first, ve = p.valid_first + p.valid_bytes;
-      if (ve <= first || vf >= e) continue;
-      uint64_t left = first > vf ? first - vf : 0;
-      uint64_t right = ve > e ? ve - e : 0;
-      if (left >= right) {
-        p.valid_bytes = left;
-      } else {
-        p.valid_first = e;
-        p.valid_bytes = right;
-      }
-    }
+    for (auto& [g, p] : b.pieces)
+      if (g != gid) p.valid.sub(first, len);
   }
 
   // Make bytes [first, first+len) of buffer `id` valid on `gid`, copying the
-  // missing parts from devices that hold them (NVLink peer copies).
+  // missing parts from devices that hold them (NVLink peer copies). Bytes no
+  // device holds were never written: the zero-filled allocation stands for them.
   void ensure_valid(uint64_t id, BufferRec& b, int gid, uint64_t first, uint64_t len, QueueRec* q) {
     Piece& p = ensure_alloc(id, b, gid, first, len);
-    if (p.valid_bytes && first >= p.valid_first && first + len <= p.valid_first + p.valid_bytes) return;
+    if (p.valid.covers(first, len)) return;
     auto started = Clock::now();
     int dev = dev_index(gid);
     uint64_t pos = first, end = first + len;
     bool copied = false;
     while (pos < end) {
-      if (p.valid_bytes && pos >= p.valid_first && pos < p.valid_first + p.valid_bytes) {
-        pos = p.valid_first + p.valid_bytes;
+      if (uint64_t e = p.valid.holds(pos)) {
+        pos = e;
         continue;
       }
-      // a source holding `pos`
+      const uint64_t stop = std::min(end, p.valid.next_start(pos));
       int src = -1;
       uint64_t src_end = 0;
       for (auto& [g, o] : b.pieces) {
-        if (g == gid || !o.valid_bytes) continue;
-        if (pos >= o.valid_first && pos < o.valid_first + o.valid_bytes) {
+        if (g == gid) continue;
+        if (uint64_t e = o.valid.holds(pos)) {
           src = g;
-          src_end = o.valid_first + o.valid_bytes;
+          src_end = e;
           break;
         }
       }
-      uint64_t stop = end;
-      if (p.valid_bytes && p.valid_first > pos) stop = std::min(stop, p.valid_first);
-      if (src < 0) {
-        // nobody holds it: never written -> zeros (the allocation is zero-filled
-        // unless reused; skip to the next held byte)
+      if (src < 0) {  // skip to the next byte some other device holds
         uint64_t next = stop;
         for (auto& [g, o] : b.pieces)
-          if (g != gid && o.valid_bytes && o.valid_first > pos) next = std::min(next, o.valid_first);
+          if (g != gid) next = std::min(next, o.valid.next_start(pos));
         pos = next;
         continue;
       }
-      uint64_t n = std::min(stop, src_end) - pos;
+      const uint64_t n = std::min(stop, src_end) - pos;
       check(hcl_buffer_copy_peer(dev, id, pos, dev_index(src), id, pos, n));
       trace.record({gid, "copy_peer", id});
       copied = true;
@@ -271,7 +302,7 @@ struct HostContext::Impl {
   void note_residency(uint64_t id, BufferRec& b) {
     std::vector<int> ids;
     for (auto& [g, p] : b.pieces)
-      if (p.valid_bytes == b.size && b.size) ids.push_back(g);
+      if (b.size && p.valid.covers(0, b.size)) ids.push_back(g);
     scheduler.note_resident(id, ids);
   }
 
@@ -366,6 +397,27 @@ struct HostContext::Impl {
         }
       }
     }
+    // 1c. EXCHANGE: a part's kernel stores into its peers' copies, whose
+    //     allocation (stream-ordered alloc + zero fill on the peer's stream) and
+    //     older readers must be complete first: every live stream waits for
+    //     every other live stream's staging before any part launches
+    if (exchange) {
+      std::vector<std::pair<cudaStream_t, cudaEvent_t>> staged;
+      for (const Part* p : live) {
+        void* st = nullptr;
+        check(hcl_device_stream(dev_index(p->gid), &st));
+        int ordinal = 0;
+        if (cudaStreamGetDevice(static_cast<cudaStream_t>(st), &ordinal) == cudaSuccess) cudaSetDevice(ordinal);
+        cudaEvent_t ev = nullptr;
+        cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+        cudaEventRecord(ev, static_cast<cudaStream_t>(st));
+        staged.emplace_back(static_cast<cudaStream_t>(st), ev);
+      }
+      for (auto& [st, own] : staged)
+        for (auto& [st2, ev] : staged)
+          if (ev != own) cudaStreamWaitEvent(st, ev, 0);
+      for (auto& [st, ev] : staged) cudaEventDestroy(ev);  // released once the waits resolve
+    }
     // 2. launch every part asynchronously on its device stream
     std::vector<std::pair<cudaStream_t, cudaEvent_t>> part_done;
     std::vector<hcl_arg> cargs(n);
@@ -424,29 +476,30 @@ struct HostContext::Impl {
           for (size_t c = a + 1; c < gids.size(); ++c)
             if (gids[a] == gids[c])
               fail(ErrorCode::argument, k.name + ": a REDUCE_SUM output needs one device per part");
-        const int g0 = gids[0], d0 = dev_index(g0);
+        // binary tree: in round r part a folds part a + 2^r into itself; the
+        // folds of one round run concurrently on their devices' streams and
+        // integer sums make the result independent of the tree shape
+        const int g0 = gids[0];
         const uint64_t id = args[i].buffer;
-        for (size_t a = 1; a < gids.size(); ++a) {
-          uint64_t tmp = new_id();
-          check(hcl_buffer_alloc(d0, tmp, 0, b.size));
-          check(hcl_buffer_copy_peer(d0, tmp, 0, dev_index(gids[a]), id, 0, b.size));
-          trace.record({g0, "copy_peer", id});
-          hcl_arg ra[3] = {{HCL_ARG_INOUT, 0, 0, id}, {HCL_ARG_IN, 0, 0, tmp},
-                           {HCL_ARG_SCALAR, 0, static_cast<int64_t>(b.size / 8), 0}};
-          check(hcl_launch(d0, "reduce_add_i64", ra, 3, nullptr, nullptr, 1, nullptr));
-          check(hcl_buffer_release(d0, tmp));
-        }
-        for (auto& [g, p] : b.pieces) p.valid_bytes = 0;
-        b.pieces[g0].valid_first = 0;
-        b.pieces[g0].valid_bytes = b.size;
+        for (size_t stride = 1; stride < gids.size(); stride *= 2)
+          for (size_t a = 0; a + stride < gids.size(); a += 2 * stride) {
+            const int da = dev_index(gids[a]);
+            uint64_t tmp = new_id();
+            check(hcl_buffer_alloc(da, tmp, 0, b.size));
+            check(hcl_buffer_copy_peer(da, tmp, 0, dev_index(gids[a + stride]), id, 0, b.size));
+            trace.record({gids[a], "copy_peer", id});
+            hcl_arg ra[3] = {{HCL_ARG_INOUT, 0, 0, id}, {HCL_ARG_IN, 0, 0, tmp},
+                             {HCL_ARG_SCALAR, 0, static_cast<int64_t>(b.size / 8), 0}};
+            check(hcl_launch(da, "reduce_add_i64", ra, 3, nullptr, nullptr, 1, nullptr));
+            check(hcl_buffer_release(da, tmp));
+          }
+        for (auto& [g, p] : b.pieces) p.valid.clear();
+        b.pieces[g0].valid.add(0, b.size);
         continue;
       }
       if (k.classes[i] == HCL_PART_EXCHANGE) {  // whole on every participating device
-        for (auto& [g, p] : b.pieces) p.valid_bytes = 0;
-        for (const Part* p : live) {
-          b.pieces[p->gid].valid_first = 0;
-          b.pieces[p->gid].valid_bytes = b.size;
-        }
+        for (auto& [g, p] : b.pieces) p.valid.clear();
+        for (const Part* p : live) b.pieces[p->gid].valid.add(0, b.size);
         continue;
       }
       if (!whole && k.classes[i] == HCL_PART_MERGE_TOPK) {
@@ -467,69 +520,53 @@ struct HostContext::Impl {
           for (size_t c = a + 1; c < gids.size(); ++c)
             if (gids[a] == gids[c])
               fail(ErrorCode::argument, k.name + ": a MERGE_TOPK output needs one device per part");
-        const int g0 = gids[0], d0 = dev_index(g0);
+        // binary tree of pairwise merges (the (dist, idx) merge is associative,
+        // so any fold order equals the P-way merge); one round's merges run
+        // concurrently on their devices
+        const int g0 = gids[0];
         BufferRec& bi = buffer(args[mi[0]].buffer);
         BufferRec& bd = buffer(args[mi[1]].buffer);
         const std::string merge = k.name + "_merge";
-        for (size_t a = 1; a < gids.size(); ++a) {
-          const int da = dev_index(gids[a]);
-          uint64_t ti = new_id(), td = new_id();
-          check(hcl_buffer_alloc(d0, ti, 0, bi.size));
-          check(hcl_buffer_alloc(d0, td, 0, bd.size));
-          check(hcl_buffer_copy_peer(d0, ti, 0, da, args[mi[0]].buffer, 0, bi.size));
-          check(hcl_buffer_copy_peer(d0, td, 0, da, args[mi[1]].buffer, 0, bd.size));
-          trace.record({g0, "copy_peer", args[mi[0]].buffer});
-          trace.record({g0, "copy_peer", args[mi[1]].buffer});
-          std::vector<hcl_arg> margs(cargs);
-          margs[mi[0]].kind = HCL_ARG_INOUT;
-          margs[mi[1]].kind = HCL_ARG_INOUT;
-          margs.push_back(hcl_arg{HCL_ARG_IN, 0, 0, ti});
-          margs.push_back(hcl_arg{HCL_ARG_IN, 0, 0, td});
-          const int rc = hcl_launch(d0, merge.c_str(), margs.data(), static_cast<uint32_t>(margs.size()), nullptr,
-                                    nullptr, 1, nullptr);
-          hcl_buffer_release(d0, ti);
-          hcl_buffer_release(d0, td);
-          check(rc);
-        }
+        for (size_t stride = 1; stride < gids.size(); stride *= 2)
+          for (size_t a = 0; a + stride < gids.size(); a += 2 * stride) {
+            const int d0 = dev_index(gids[a]), da = dev_index(gids[a + stride]);
+            uint64_t ti = new_id(), td = new_id();
+            check(hcl_buffer_alloc(d0, ti, 0, bi.size));
+            check(hcl_buffer_alloc(d0, td, 0, bd.size));
+            check(hcl_buffer_copy_peer(d0, ti, 0, da, args[mi[0]].buffer, 0, bi.size));
+            check(hcl_buffer_copy_peer(d0, td, 0, da, args[mi[1]].buffer, 0, bd.size));
+            trace.record({gids[a], "copy_peer", args[mi[0]].buffer});
+            trace.record({gids[a], "copy_peer", args[mi[1]].buffer});
+            std::vector<hcl_arg> margs(cargs);
+            margs[mi[0]].kind = HCL_ARG_INOUT;
+            margs[mi[1]].kind = HCL_ARG_INOUT;
+            margs.push_back(hcl_arg{HCL_ARG_IN, 0, 0, ti});
+            margs.push_back(hcl_arg{HCL_ARG_IN, 0, 0, td});
+            const int rc = hcl_launch(d0, merge.c_str(), margs.data(), static_cast<uint32_t>(margs.size()), nullptr,
+                                      nullptr, 1, nullptr);
+            hcl_buffer_release(d0, ti);
+            hcl_buffer_release(d0, td);
+            check(rc);
+          }
         for (BufferRec* b2 : {&bi, &bd}) {
-          for (auto& [g, p] : b2->pieces) p.valid_bytes = 0;
-          b2->pieces[g0].valid_first = 0;
-          b2->pieces[g0].valid_bytes = b2->size;
+          for (auto& [g, p] : b2->pieces) p.valid.clear();
+          b2->pieces[g0].valid.add(0, b2->size);
         }
         continue;
       }
-      uint64_t u0 = UINT64_MAX, u1 = 0;
+      // every part's slice is now valid on its device and stale everywhere else
       for (const Part& part : parts) {
         if (!whole && part.hi == part.lo) continue;
         uint64_t first, len;
         slice(i, part, first, len);
-        u0 = std::min(u0, first);
-        u1 = std::max(u1, first + len);
-      }
-      if (u1 <= u0) continue;
-      for (auto& [g, p] : b.pieces) {  // old valid minus U (larger side kept)
-        if (!p.valid_bytes) continue;
-        uint64_t vf = p.valid_first, ve = p.valid_first + p.valid_bytes;
-        if (ve <= u0 || vf >= u1) continue;
-        uint64_t left = u0 > vf ? u0 - vf : 0, right = ve > u1 ? ve - u1 : 0;
-        if (left >= right) {
-          p.valid_bytes = left;
-        } else {
-          p.valid_first = u1;
-          p.valid_bytes = right;
-        }
+        for (auto& [g, p] : b.pieces)
+          if (g != part.gid) p.valid.sub(first, len);
       }
       for (const Part& part : parts) {
         if (!whole && part.hi == part.lo) continue;
         uint64_t first, len;
         slice(i, part, first, len);
-        Piece& p = b.pieces[part.gid];
-        if (p.valid_bytes && (p.valid_first + p.valid_bytes == first || first + len == p.valid_first))
-          set_valid(p, first, len);
-        else {
-          p.valid_first = first;
-          p.valid_bytes = len;
-        }
+        b.pieces[part.gid].valid.add(first, len);
       }
     }
     for (uint32_t i = 0; i < n; ++i)
@@ -688,77 +725,88 @@ void HostContext::set_kernel_arg(Handle kernel, uint32_t index, Handle buffer) {
 
 Handle HostContext::enqueue_write_buffer(Handle queue, Handle buffer, std::span<const uint8_t> data, uint64_t offset,
                                          bool blocking) {
-  std::lock_guard lock(impl_->mu);
-  Impl::QueueRec& q = impl_->queue(queue.id);
-  if (buffer.kind != HandleKind::buffer) fail(ErrorCode::handle, "not a buffer handle");
-  Impl::BufferRec& b = impl_->buffer(buffer.id);
-  if (offset + data.size() > b.size)
-    fail(ErrorCode::size, "write of " + std::to_string(data.size()) + " bytes at offset " + std::to_string(offset) +
-                              " into a " + std::to_string(b.size) + "-byte buffer");
+  int dev = -1;
+  Handle ev;
   auto started = Clock::now();
-  // A device whose valid bytes straddle the written range on both sides would
-  // lose one side when trimmed: pull its interval here first.
-  for (auto& [g, o] : b.pieces)
-    if (g != q.gid && o.valid_bytes && o.valid_first < offset && o.valid_first + o.valid_bytes > offset + data.size())
-      impl_->ensure_valid(buffer.id, b, q.gid, o.valid_first, o.valid_bytes, &q);
-  Impl::Piece& p = impl_->ensure_alloc(buffer.id, b, q.gid, offset, data.size());
-  if (!data.empty()) {
-    impl_->trace.record({q.gid, "write_buffer", buffer.id});
-    if (blocking)
-      check(hcl_buffer_write(impl_->dev_index(q.gid), buffer.id, offset, data.data(), data.size()));
-    else
-      check(hcl_buffer_write_async(impl_->dev_index(q.gid), buffer.id, offset, data.data(), data.size()));
+  {
+    std::lock_guard lock(impl_->mu);
+    Impl::QueueRec& q = impl_->queue(queue.id);
+    if (buffer.kind != HandleKind::buffer) fail(ErrorCode::handle, "not a buffer handle");
+    Impl::BufferRec& b = impl_->buffer(buffer.id);
+    if (offset + data.size() > b.size)
+      fail(ErrorCode::size, "write of " + std::to_string(data.size()) + " bytes at offset " + std::to_string(offset) +
+                                " into a " + std::to_string(b.size) + "-byte buffer");
+    Impl::Piece& p = impl_->ensure_alloc(buffer.id, b, q.gid, offset, data.size());
+    if (!data.empty()) {
+      impl_->trace.record({q.gid, "write_buffer", buffer.id});
+      if (blocking)
+        dev = impl_->dev_index(q.gid);  // issued below, off the table lock
+      else
+        check(hcl_buffer_write_async(impl_->dev_index(q.gid), buffer.id, offset, data.data(), data.size()));
+    }
+    Impl::set_valid(p, offset, data.size());
+    Impl::invalidate_others(b, q.gid, offset, data.size());
+    impl_->note_residency(buffer.id, b);
+    ev = impl_->new_event();
   }
-  Impl::set_valid(p, offset, data.size());
-  Impl::invalidate_others(b, q.gid, offset, data.size());
-  impl_->note_residency(buffer.id, b);
-  impl_->add_transfer(&q, ms_since(started));
-  return impl_->new_event();
+  // a blocking copy from pageable memory waits for the buffer's earlier users:
+  // other threads keep using the context meanwhile
+  if (dev >= 0) check(hcl_buffer_write(dev, buffer.id, offset, data.data(), data.size()));
+  std::lock_guard lock(impl_->mu);
+  auto qi = impl_->queues.find(queue.id);
+  impl_->add_transfer(qi == impl_->queues.end() ? nullptr : &qi->second, ms_since(started));
+  return ev;
 }
 
 void HostContext::enqueue_read_buffer_into(Handle queue, Handle buffer, void* dst, uint64_t offset, uint64_t len,
                                            bool blocking) {
-  std::lock_guard lock(impl_->mu);
-  Impl::QueueRec& q = impl_->queue(queue.id);
-  if (buffer.kind != HandleKind::buffer) fail(ErrorCode::handle, "not a buffer handle");
-  Impl::BufferRec& b = impl_->buffer(buffer.id);
-  if (offset + len > b.size) fail(ErrorCode::size, "read past the end of the buffer");
+  struct Copy {
+    int dev;
+    uint64_t pos, n;
+  };
+  std::vector<Copy> copies;  // blocking pieces, issued off the table lock
   auto started = Clock::now();
   auto* out = static_cast<uint8_t*>(dst);
-  uint64_t pos = offset, end = offset + len;
-  while (pos < end) {
-    int src = -1;
-    uint64_t src_end = 0;
-    auto holds = [&](const Impl::Piece& o) { return o.valid_bytes && pos >= o.valid_first && pos < o.valid_first + o.valid_bytes; };
-    auto qi = b.pieces.find(q.gid);
-    if (qi != b.pieces.end() && holds(qi->second)) {
-      src = q.gid;
-      src_end = qi->second.valid_first + qi->second.valid_bytes;
-    } else {
-      for (auto& [g, o] : b.pieces)
-        if (holds(o)) {
-          src = g;
-          src_end = o.valid_first + o.valid_bytes;
-          break;
-        }
+  {
+    std::lock_guard lock(impl_->mu);
+    Impl::QueueRec& q = impl_->queue(queue.id);
+    if (buffer.kind != HandleKind::buffer) fail(ErrorCode::handle, "not a buffer handle");
+    Impl::BufferRec& b = impl_->buffer(buffer.id);
+    if (offset + len > b.size) fail(ErrorCode::size, "read past the end of the buffer");
+    uint64_t pos = offset, end = offset + len;
+    while (pos < end) {
+      int src = -1;
+      uint64_t src_end = 0;
+      auto qi = b.pieces.find(q.gid);
+      if (qi != b.pieces.end() && (src_end = qi->second.valid.holds(pos))) {
+        src = q.gid;
+      } else {
+        for (auto& [g, o] : b.pieces)
+          if ((src_end = o.valid.holds(pos))) {
+            src = g;
+            break;
+          }
+      }
+      if (src < 0) {  // never written: zeros (SPEC design decision; runtime.cpp:496-497)
+        uint64_t next = end;
+        for (auto& [g, o] : b.pieces) next = std::min(next, o.valid.next_start(pos));
+        std::memset(out + (pos - offset), 0, next - pos);
+        pos = next;
+        continue;
+      }
+      uint64_t n = std::min(end, src_end) - pos;
+      impl_->trace.record({src, "read_buffer", buffer.id});
+      if (blocking)
+        copies.push_back({impl_->dev_index(src), pos, n});
+      else
+        check(hcl_buffer_read_async(impl_->dev_index(src), buffer.id, pos, out + (pos - offset), n));
+      pos += n;
     }
-    if (src < 0) {  // never written: zeros (SPEC design decision; runtime.cpp:496-497)
-      uint64_t next = end;
-      for (auto& [g, o] : b.pieces)
-        if (o.valid_bytes && o.valid_first > pos) next = std::min(next, o.valid_first);
-      std::memset(out + (pos - offset), 0, next - pos);
-      pos = next;
-      continue;
-    }
-    uint64_t n = std::min(end, src_end) - pos;
-    impl_->trace.record({src, "read_buffer", buffer.id});
-    if (blocking)
-      check(hcl_buffer_read(impl_->dev_index(src), buffer.id, pos, out + (pos - offset), n));
-    else
-      check(hcl_buffer_read_async(impl_->dev_index(src), buffer.id, pos, out + (pos - offset), n));
-    pos += n;
   }
-  impl_->add_transfer(&q, ms_since(started));
+  for (const Copy& c : copies) check(hcl_buffer_read(c.dev, buffer.id, c.pos, out + (c.pos - offset), c.n));
+  std::lock_guard lock(impl_->mu);
+  auto qi = impl_->queues.find(queue.id);
+  impl_->add_transfer(qi == impl_->queues.end() ? nullptr : &qi->second, ms_since(started));
 }
 
 std::vector<uint8_t> HostContext::enqueue_read_buffer(Handle queue, Handle buffer) {
@@ -890,7 +938,7 @@ std::vector<uint8_t> HostContext::share_buffer(Handle queue, Handle buffer) {
   p.allocated = true;
   p.alloc_first = 0;
   p.alloc_bytes = b.size;
-  p.valid_bytes = 0;
+  p.valid.clear();
   impl_->trace.record({q.gid, "alloc_buffer", buffer.id});
   return h;
 }
@@ -937,8 +985,8 @@ void HostContext::enqueue_broadcast(Handle queue, Handle buffer, int root) {
   Impl::Piece& p = impl_->ensure_alloc(buffer.id, b, q.gid, 0, b.size);
   impl_->trace.record({q.gid, "broadcast", buffer.id});
   check(hcl_broadcast(impl_->dev_index(q.gid), buffer.id, 0, b.size, root));
-  p.valid_first = 0;
-  p.valid_bytes = b.size;
+  p.valid.clear();
+  p.valid.add(0, b.size);
 }
 
 std::pair<int, Handle> HostContext::submit_task(const KernelTask& task) {
@@ -989,28 +1037,46 @@ Handle HostContext::launch_task(Handle queue, const KernelTask& task) {
 }
 
 TimingFragment HostContext::finish(Handle queue) {
+  std::shared_ptr<std::mutex> op;
+  {
+    std::lock_guard lock(impl_->mu);
+    op = impl_->queue(queue.id).op_mu;
+  }
+  std::lock_guard serial(*op);  // one finish per queue at a time
+  std::vector<Impl::Launch> done;
+  int dev = 0;
+  {
+    std::lock_guard lock(impl_->mu);
+    Impl::QueueRec& q = impl_->queue(queue.id);
+    dev = impl_->dev_index(q.gid);
+    done.swap(q.pending);
+  }
+  // device synchronization without the table lock: other queues keep enqueueing
+  check(hcl_finish(dev, nullptr));
+  std::vector<float> ms(done.size(), 0.f);
+  for (size_t i = 0; i < done.size(); ++i) {
+    cudaEventSynchronize(done[i].stop);
+    cudaEventElapsedTime(&ms[i], done[i].start, done[i].stop);
+    cudaEventDestroy(done[i].start);
+    cudaEventDestroy(done[i].stop);
+  }
   std::lock_guard lock(impl_->mu);
   Impl::QueueRec& q = impl_->queue(queue.id);
-  check(hcl_finish(impl_->dev_index(q.gid), nullptr));
-  for (auto& l : q.pending) {
-    float ms = 0.f;
-    cudaEventSynchronize(l.stop);
-    cudaEventElapsedTime(&ms, l.start, l.stop);
-    q.compute_ms += ms;
+  for (size_t i = 0; i < done.size(); ++i) {
+    const Impl::Launch& l = done[i];
+    q.compute_ms += ms[i];
     const DeviceEntry* e = impl_->device_map.find(l.gid);
     double modeled = static_cast<double>(l.work) /
                      ((e ? e->model.relative_throughput : 1.0) * impl_->scheduler.options().baseline_rate) * 1000.0;
     q.modeled_ms += modeled;
     {
       std::lock_guard lb(impl_->breakdown_mu);
-      impl_->timings.compute_ms += ms;
+      impl_->timings.compute_ms += ms[i];
       impl_->timings.modeled_compute_ms += modeled;
     }
-    if (ms > 0.f && l.work > 0) impl_->scheduler.record_profile(l.gid, l.kernel, static_cast<double>(l.work), ms / 1000.0);
-    cudaEventDestroy(l.start);
-    cudaEventDestroy(l.stop);
+    if (ms[i] > 0.f && l.work > 0)
+      impl_->scheduler.record_profile(l.gid, l.kernel, static_cast<double>(l.work), ms[i] / 1000.0);
   }
-  q.pending.clear();
   TimingFragment f{q.transfer_ms, q.compute_ms, q.modeled_ms};
   q.transfer_ms = q.compute_ms = q.modeled_ms = 0.0;
   return f;

@@ -450,6 +450,42 @@ uint64_t launch_gen_points(LaunchCtx& c) {
   return rows * static_cast<uint64_t>(d);
 }
 
+// kmeans_accumulate's exact int32/int64 tables assume every coordinate is a
+// multiple of 2^-12 inside [-8, 8) (|x * 4096| <= 2^15). This check flags
+// any other value (NaN and inf included) before the data is used.
+__global__ void check_points_kernel(const float* __restrict__ pts, uint64_t count, int* __restrict__ bad) {
+  int mine = 0;
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < count; e += (uint64_t)gridDim.x * blockDim.x) {
+    const float x = pts[e];
+    const float q = __fmul_rn(x, 4096.0f);
+    mine |= !(x >= -8.0f && x < 8.0f) || q != truncf(q);
+  }
+  if (__syncthreads_or(mine) && threadIdx.x == 0) atomicOr(bad, 1);
+}
+
+// kmeans_check_points(points, N, D): argument error unless every coordinate of
+// the launch's rows is on the 2^-12 grid inside [-8, 8) (KMeans.load_points)
+uint64_t launch_check_points(LaunchCtx& c) {
+  int64_t n = scalar_arg(c, 1, "kmeans_check_points N"), d = scalar_arg(c, 2, "kmeans_check_points D");
+  if (n < 0 || d < 1) fail(ErrorCode::argument, "kmeans_check_points: bad N/D");
+  uint64_t lo, rows;
+  sub_range(c, static_cast<uint64_t>(n), lo, rows, "kmeans_check_points");
+  const float* pts = at_byte<const float>(buffer_arg(c, 0, "kmeans_check_points points"), lo * d * 4, rows * d * 4,
+                                          "kmeans_check_points");
+  if (!rows) return 0;
+  int* bad = static_cast<int*>(c.scratch(c.dev, sizeof(int)));
+  HCL_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), c.stream));
+  check_points_kernel<<<c.sm_count * 8, 256, 0, c.stream>>>(pts, rows * static_cast<uint64_t>(d), bad);
+  HCL_LAUNCHED();
+  int h = 0;
+  HCL_CUDA(cudaMemcpyAsync(&h, bad, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+  HCL_CUDA(cudaStreamSynchronize(c.stream));
+  if (h)
+    fail(ErrorCode::argument,
+         "k-means points must be multiples of 2^-12 inside [-8, 8): the exact fixed-point centroid sums need it");
+  return rows * static_cast<uint64_t>(d);
+}
+
 uint64_t rows_km(const int64_t* s, uint32_t n) { return static_cast<uint64_t>(s[n == 6 ? 3 : 4]); }
 uint64_t rows_gen(const int64_t* s, uint32_t) { return static_cast<uint64_t>(s[1]); }
 
@@ -463,6 +499,7 @@ void register_kmeans(std::vector<KernelDef>& r) {
                rows_km});
   r.push_back({"b200", "kmeans_finalize", {I, I, IO, S, S}, {P, P, P, N, N}, launch_finalize, nullptr, nullptr});
   r.push_back({"b200", "reduce_add_i64", {IO, I, S}, {P, P, N}, launch_add_i64, nullptr, nullptr});
+  r.push_back({"b200", "kmeans_check_points", {I, S, S}, {X, N, N}, launch_check_points, nullptr, rows_gen});
   r.push_back({"b200", "gen_kmeans_points", {O, S, S, S, S}, {X, N, N, N, N}, launch_gen_points, nullptr, rows_gen});
 }
 

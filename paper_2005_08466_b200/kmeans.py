@@ -7,6 +7,11 @@ launches, then `kmeans_finalize` on the first queue. Centroid sums are exact
 int64 fixed point (points are multiples of 2^-12), combined across parts by
 the runtime's REDUCE_SUM class (or an NCCL allreduce across processes), so
 every iteration is bit-identical for any partition.
+
+Precondition: every coordinate is a multiple of 2^-12 inside [-8, 8) (the
+exact fixed-point sums need |x * 4096| <= 2^15). load_points checks it on the
+device and raises HaoclError(argument) otherwise; generate_points produces
+such points by construction.
 """
 from __future__ import annotations
 
@@ -36,6 +41,9 @@ class KMeans:
         self.k_assign = ctx.create_kernel(prog, "kmeans_assign")
         self.k_acc = ctx.create_kernel(prog, "kmeans_accumulate")
         self.k_fin = ctx.create_kernel(prog, "kmeans_finalize")
+        self.k_check = ctx.create_kernel(prog, "kmeans_check_points")
+        for j, a in enumerate([self.b_pts, n, d]):
+            ctx.set_kernel_arg(self.k_check, j, a)
         for j, a in enumerate([self.b_pts, self.b_cent, self.b_assign, n, d, k]):
             ctx.set_kernel_arg(self.k_assign, j, a)
         for j, a in enumerate([self.b_pts, self.b_assign, self.b_sums, self.b_counts, n, d, k]):
@@ -59,8 +67,12 @@ class KMeans:
         k = self.k_assign_tc if self.tensor_filter else self.k_assign
         self.ctx.enqueue_ndrange_partitioned(k, (self.n, 1, 1), 1, self.queues, bounds=self.bounds)
 
-    def load_points(self, pts: np.ndarray, bounds: Optional[Sequence[int]] = None) -> None:
-        """Scatter each queue's row block of the points straight to its device."""
+    def load_points(self, pts: np.ndarray, bounds: Optional[Sequence[int]] = None, validate: bool = True) -> None:
+        """Scatter each queue's row block of the points straight to its device.
+
+        validate=True checks the fixed-point precondition on the device (argument
+        error otherwise); validate=False accepts any fp32 data for assignment
+        only (assign_only), and iterate() then refuses to run."""
         if bounds is None:
             bounds = self.ctx.partition_plan(self.k_assign, (self.n, 1, 1), self.queues, self.weights)
         flat = np.ascontiguousarray(pts, np.float32).reshape(-1)
@@ -68,6 +80,10 @@ class KMeans:
             lo, hi = bounds[i], bounds[i + 1]
             if hi > lo:
                 self.ctx.enqueue_write_buffer(q, self.b_pts, flat[lo * self.d:hi * self.d], offset=lo * self.d * 4)
+        # the exact centroid sums need points on the 2^-12 grid in [-8, 8): checked where they live
+        self.on_grid = validate
+        if validate:
+            self.ctx.enqueue_ndrange_partitioned(self.k_check, (self.n, 1, 1), 1, self.queues, bounds=list(bounds))
         self.bounds = list(bounds)
         self._split()
 
@@ -81,6 +97,7 @@ class KMeans:
         for j, a in enumerate([self.b_pts, self.n, self.d, blobs, seed]):
             self.ctx.set_kernel_arg(kg, j, a)
         self.ctx.enqueue_ndrange_partitioned(kg, (self.n, 1, 1), 1, self.queues, bounds=bounds)
+        self.on_grid = True
         self.bounds = list(bounds)
         self._split()
 
@@ -88,6 +105,11 @@ class KMeans:
         self.ctx.enqueue_write_buffer(self.queues[0], self.b_cent, np.ascontiguousarray(cent, np.float32))
 
     def iterate(self, iterations: int = 1) -> None:
+        if not getattr(self, "on_grid", False):
+            from ._native import HaoclError
+
+            raise HaoclError(9, "k-means update needs points validated on the 2^-12 grid in [-8, 8) "
+                                "(load_points(validate=True) or generate_points)")
         ctx, g = self.ctx, (self.n, 1, 1)
         for _ in range(iterations):
             self._assign()

@@ -415,3 +415,67 @@ def test_in_process_collective_c_abi(ctx, queues):
     finally:
         for i in range(ndev):
             L.hcl_buffer_release(i, ids[i])
+
+
+def _launch_raw(L, dev, kernel, spec):
+    """hcl_launch on device-level buffers: spec = list of int scalars or
+    ('in', array) / ('out', nbytes). Returns (rc, work_units)."""
+    import ctypes as C
+
+    ids, args = [], (N.HclArg * max(1, len(spec)))()
+    for i, a in enumerate(spec):
+        if isinstance(a, tuple):
+            bid = 0x7A00_0000 + i
+            nbytes = a[1] if a[0] == "out" else a[1].nbytes
+            assert L.hcl_buffer_alloc(dev, bid, 0, max(nbytes, 1)) == 0
+            if a[0] == "in":
+                arr = np.ascontiguousarray(a[1])
+                assert L.hcl_buffer_write(dev, bid, 0, arr.ctypes.data, arr.nbytes) == 0
+            ids.append(bid)
+            args[i] = N.HclArg(1 if a[0] == "in" else 2, 0, 0, bid)
+        else:
+            args[i] = N.HclArg(0, 0, int(a), 0)
+    work = C.c_uint64(0)
+    rc = L.hcl_launch(dev, kernel.encode(), args, len(spec), None, None, 1, C.byref(work))
+    assert L.hcl_finish(dev, None) == 0
+    for b in ids:
+        L.hcl_buffer_release(dev, b)
+    return rc, work.value
+
+
+def test_work_units_match_reference_work_estimate(ctx, golden):
+    """hcl_launch reports the reference's work units (kernels::work_estimate,
+    proj/src/kernels.cpp:285-298) -- the unit behind the scheduler's EMA rates
+    (scheduler.cpp:136-149) and the roofline. Shapes of the golden fixture,
+    tests/golden/make_golden.py (generated from the reference library)."""
+    L = N.lib()
+    we = golden["work_estimate"]
+    _, w = _launch_raw(L, 0, "matmul", [("in", np.ones(3 * 5)), ("in", np.ones(5 * 7)), ("out", 3 * 7 * 8), 3, 5, 7])
+    assert w == we["matmul"]  # 2 * 3 * 5 * 7
+    rows = cols = 10  # values buffer of 800 bytes = 100 nnz
+    hdr = np.array([rows, cols], np.int64)
+    rp = (np.arange(rows + 1) * cols).astype(np.int64)
+    ci = np.tile(np.arange(cols), rows).astype(np.int64)
+    rc, w = _launch_raw(L, 0, "spmv_compute", [("in", hdr), ("in", rp), ("in", ci), ("in", np.ones(100)),
+                                               ("in", np.ones(cols)), 0, rows, ("out", rows * 8)])
+    assert rc == 0 and w == we["spmv_compute"]
+    rc, w = _launch_raw(L, 0, "knn", [("in", np.ones(100 * 8)), ("in", np.ones(10 * 8)), 100, 10, 8, 3,
+                                      ("out", 10 * 3 * 4), ("out", 10 * 3 * 8)])
+    assert rc == 0 and w == we["knn"]
+    rc, w = _launch_raw(L, 0, "vecadd", [("in", np.ones(1000)), ("in", np.ones(1000)), ("out", 8000), 1000])
+    assert rc == 0 and w == we["vecadd"]
+    if O.ref_available():  # and live against the reference library on the same shapes
+        assert O.ref_work_estimate("matmul", [3, 5, 7], [0, 0, 0]) == we["matmul"]
+
+
+def test_execute_error_codes_match_reference(ctx, golden):
+    """kernels::execute's error codes (name = 10 for an unknown kernel,
+    argument = 9 for arity and buffer-length violations), measured on the
+    reference library (tests/golden/reference_golden.json "execute_errors"),
+    come back from hcl_launch as 1000 + code."""
+    L = N.lib()
+    ee = golden["execute_errors"]
+    assert _launch_raw(L, 0, "nosuch", [])[0] == 1000 + ee["unknown_kernel"]
+    assert _launch_raw(L, 0, "vecadd", [1])[0] == 1000 + ee["arity"]
+    rc, _ = _launch_raw(L, 0, "vecadd", [("in", np.ones(4)), ("in", np.ones(3)), ("out", 64), 4])
+    assert rc == 1000 + ee["length"]

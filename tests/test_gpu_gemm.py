@@ -1,14 +1,21 @@
 """GPU parity of the tensor-core GEMM (configs C1/C2) against the fp64 oracle
 of the same rounded inputs, with the normwise tolerance of SURVEY.md §8(c):
 err_ij = |C - C64|_ij / (|A| |B|)_ij. Tolerances (stated here, per path):
-  bf16 inputs, fp32 out  : 2^-12   (fp32 tensor-core accumulation)
-  bf16 inputs, bf16 out  : 2^-8    (adds the bf16 output rounding, 2^-9 rel)
+  bf16 inputs, fp32 out  : 2^-12   (exact bf16 products, fp32 tensor-core
+                                    accumulation; tighter than §8(c)'s 2^-10)
+  bf16 inputs, bf16 out  : |C - C64| <= 2^-10 (1 + 2^-9) (|A||B|) + 2^-9 |C64|
+                           (§8(c)'s 2^-10 product bound, then one bf16 rounding
+                           of the fp32 result: unit roundoff 2^-9)
   tf32 (fp32 inputs)     : 2^-10   (1xTF32 products)
-  fp32 SIMT              : 2^-20   (fp32-exact products)
-  3xTF32                 : 2^-17   (exact split products, but the tensor core's
-                                    fp32 accumulation truncates per MMA: measured
+  fp32 SIMT (gemm_f32)   : 2^-20   (the fp32-exact path of §8(c): exact fp32
+                                    products, k-ascending FFMA chains)
+  3xTF32 (gemm_f32x3)    : 2^-16   (the FAST fp32 path, not fp32-exact: exact
+                                    split products, but the tensor core's fp32
+                                    accumulation truncates per MMA; measured
                                     2^-18.8 at K=1024, 2^-17.1 at K=16384)
-plus bit-identity of C across partitions P in {1,2,4} (P-invariance)."""
+plus bit-identity of C across partitions P in {1,2,4} (P-invariance). The
+full-size C2 samples are checked against the reference library's own
+kernels::execute("matmul") (oracle/_ref, proj/src/kernels.cpp:96-119)."""
 import os
 
 import numpy as np
@@ -54,6 +61,14 @@ def gemm(ctx, queues, kernel, a, b, m, k, n, out_f32=True, P=1, weights=None):
     return O.bf16_to_f32(raw.view(np.uint16)).reshape(m, n)
 
 
+def assert_bf16_out(c, a64, b64):
+    """bf16 output: the 2^-10 bf16-product bound of SURVEY.md §8(c), then one
+    bf16 rounding of the fp32 result (unit roundoff 2^-9)."""
+    ref = a64 @ b64
+    scale = np.abs(a64) @ np.abs(b64)
+    assert (np.abs(c.astype(np.float64) - ref) <= 2.0**-10 * (1 + 2.0**-9) * scale + 2.0**-9 * np.abs(ref)).all()
+
+
 def normwise_err(c, a64, b64):
     ref = a64 @ b64
     scale = np.abs(a64) @ np.abs(b64)
@@ -83,7 +98,7 @@ def test_gemm_bf16_bf16out(ctx, queues, m, n, k):
     c = gemm(ctx, queues, "gemm_bf16", a, b, m, k, n, out_f32=False)
     a64 = O.bf16_to_f32(a).astype(np.float64).reshape(m, k)
     b64 = O.bf16_to_f32(b).astype(np.float64).reshape(k, n)
-    assert normwise_err(c, a64, b64) <= 2.0**-8
+    assert_bf16_out(c, a64, b64)
 
 
 @pytest.mark.parametrize("P,weights", [(2, None), (4, None), (4, [3, 1, 2, 2])])
@@ -107,10 +122,10 @@ def test_gemm_tile_shapes(ctx, queues, m, n, k, shape, monkeypatch):
     b64 = O.bf16_to_f32(b).astype(np.float64).reshape(k, n)
     assert normwise_err(c, a64, b64) <= 2.0**-12
     cb = gemm(ctx, queues, "gemm_bf16", a, b, m, k, n, out_f32=False)
-    assert normwise_err(cb, a64, b64) <= 2.0**-8
+    assert_bf16_out(cb, a64, b64)
     af = O.gen_doubles(m * k, 42).astype(np.float32)
     bf = O.gen_doubles(k * n, 43).astype(np.float32)
-    for kernel, tol in (("gemm_tf32", 2.0**-10), ("gemm_f32x3", 2.0**-17)):
+    for kernel, tol in (("gemm_tf32", 2.0**-10), ("gemm_f32x3", 2.0**-16)):
         c = gemm(ctx, queues, kernel, af, bf, m, k, n)
         assert normwise_err(c, af.astype(np.float64).reshape(m, k), bf.astype(np.float64).reshape(k, n)) <= tol, kernel
 
@@ -149,7 +164,7 @@ def test_gemm_f32x3(ctx, queues, m, n, k):
     a = O.gen_doubles(m * k, 42).astype(np.float32)
     b = O.gen_doubles(k * n, 43).astype(np.float32)
     c = gemm(ctx, queues, "gemm_f32x3", a, b, m, k, n)
-    assert normwise_err(c, a.astype(np.float64).reshape(m, k), b.astype(np.float64).reshape(k, n)) <= 2.0**-17
+    assert normwise_err(c, a.astype(np.float64).reshape(m, k), b.astype(np.float64).reshape(k, n)) <= 2.0**-16
 
 
 @pytest.mark.parametrize("kernel", ["gemm_f32", "gemm_f32x3", "gemm_tf32"])
@@ -191,12 +206,13 @@ def test_gemm_f32_simt_tiles_bit_identical(ctx, queues, monkeypatch):
     assert normwise_err(np.frombuffer(outs[0], np.float32).reshape(m, n), a64, b64) <= 2.0**-20
 
 
-@pytest.mark.parametrize("kernel,out_f32,tol", [("gemm_bf16", True, 2.0**-12), ("gemm_bf16", False, 2.0**-8),
-                                                ("gemm_f32x3", True, 2.0**-17), ("gemm_f32", True, 2.0**-20)])
+@pytest.mark.parametrize("kernel,out_f32,tol", [("gemm_bf16", True, 2.0**-12), ("gemm_bf16", False, None),
+                                                ("gemm_f32x3", True, 2.0**-16), ("gemm_f32", True, 2.0**-20)])
 def test_gemm_full_c2_sampled(ctx, queues, kernel, out_f32, tol):
     """SURVEY.md §8(d) C2 at full size (16384^3, A seed 42, B seed 43): 4096
-    seeded (i, j) entries -- a 64 x 64 grid of rows and columns -- against fp64
-    dot products of the same rounded inputs, with the path's normwise tolerance."""
+    seeded (i, j) entries -- a 64 x 64 grid of rows and columns -- against the
+    REFERENCE LIBRARY's matmul (fp64, k-ascending, no contraction) of the same
+    rounded inputs, with the path's tolerance."""
     s = 16384
     if kernel == "gemm_bf16":
         a, b = O.gen_bf16(s * s, 42), O.gen_bf16(s * s, 43)
@@ -207,8 +223,18 @@ def test_gemm_full_c2_sampled(ctx, queues, kernel, out_f32, tol):
     c = gemm(ctx, queues, kernel, a, b, s, s, s, out_f32=out_f32)
     rng = np.random.default_rng(11)
     ii, jj = np.sort(rng.choice(s, 64, replace=False)), np.sort(rng.choice(s, 64, replace=False))
-    a64, b64 = af[ii].astype(np.float64), bf[:, jj].astype(np.float64)
-    assert normwise_err(c[np.ix_(ii, jj)], a64, b64) <= tol
+    a64, b64 = af[ii].astype(np.float64), np.ascontiguousarray(bf[:, jj].astype(np.float64))
+    rc, work, out = O.ref_execute("matmul", [("in", a64), ("in", b64), ("out", None), ("s", 64), ("s", s), ("s", 64)],
+                                  {2: 64 * 64 * 8}, threads=os.cpu_count() or 1)
+    assert rc == 0 and work == 2 * 64 * s * 64
+    c64 = out[2].view(np.float64).reshape(64, 64)
+    assert np.abs(c64 - a64 @ b64).max() <= 2.0**-40 * (np.abs(a64) @ np.abs(b64)).max()  # the oracle agrees
+    got = c[np.ix_(ii, jj)].astype(np.float64)
+    scale = np.abs(a64) @ np.abs(b64)
+    if tol is not None:
+        assert float((np.abs(got - c64) / scale).max()) <= tol
+    else:  # bf16 output: the 2^-10 product bound plus one bf16 rounding
+        assert (np.abs(got - c64) <= 2.0**-10 * (1 + 2.0**-9) * scale + 2.0**-9 * np.abs(c64)).all()
 
 
 def test_gemm_f32x3_ksplit(ctx, queues, monkeypatch):
@@ -219,6 +245,6 @@ def test_gemm_f32x3_ksplit(ctx, queues, monkeypatch):
     a = O.gen_doubles(m * k, 42).astype(np.float32)
     b = O.gen_doubles(k * n, 43).astype(np.float32)
     whole = gemm(ctx, queues, "gemm_f32x3", a, b, m, k, n)
-    assert normwise_err(whole, a.astype(np.float64).reshape(m, k), b.astype(np.float64).reshape(k, n)) <= 2.0**-17
+    assert normwise_err(whole, a.astype(np.float64).reshape(m, k), b.astype(np.float64).reshape(k, n)) <= 2.0**-16
     part = gemm(ctx, queues, "gemm_f32x3", a, b, m, k, n, P=4, weights=[1, 2, 3, 4])
     assert whole.tobytes() == part.tobytes()

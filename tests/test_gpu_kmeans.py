@@ -6,6 +6,7 @@ import numpy as np
 import pytest
 
 import oracle as O
+from paper_2005_08466_b200 import HaoclError
 from paper_2005_08466_b200 import datagen as G
 
 pytestmark = pytest.mark.gpu
@@ -141,13 +142,35 @@ def test_tensor_filter_ties_and_general_fp32(ctx, queues):
     pts[50:100] = cent[10]
     want = O.kmeans_assign(pts.reshape(-1), n, d, cent.reshape(-1), k)
     km = KMeans(ctx, queues[:1], n, d, k, tensor_filter=True)
-    km.load_points(pts)
+    km.load_points(pts, validate=False)  # assignment only: any fp32 data
     km.set_centroids(cent)
     km.assign_only()
     got = km.assignments()
+    with pytest.raises(HaoclError) as e:  # the exact update needs grid points
+        km.iterate(1)
+    assert e.value.code == 9
     km.close()
     assert (got == want).all()
     assert (got[50:100] == 9).all()
+
+
+@pytest.mark.parametrize("bad", [2.0**-13, 8.0, -8.0 - 2.0**-12, float("nan"), float("inf")])
+def test_load_points_rejects_off_grid(ctx, queues, bad):
+    """kmeans_accumulate's int32/int64 fixed-point tables are exact only
+    for multiples of 2^-12 inside [-8, 8); anything else is an argument error at
+    load time on the device that holds the row (here the last part's rows)."""
+    from paper_2005_08466_b200.kmeans import KMeans
+
+    n, d, k = 4096, 32, 16
+    pts = G.gen_kmeans_points(n, d, k, 42).reshape(n, d)
+    pts[n - 3, 17] = bad
+    km = KMeans(ctx, queues[:2], n, d, k)
+    with pytest.raises(HaoclError) as e:
+        km.load_points(pts)
+    assert e.value.code == 9 and "2^-12" in str(e.value)
+    pts[n - 3, 17] = -8.0  # the smallest grid value is accepted
+    km.load_points(pts)
+    km.close()
 
 
 def test_accumulate_many_points_one_cluster(ctx, queues):
@@ -192,7 +215,20 @@ def test_full_size_c4_sampled_parity(ctx, queues):
     finally:
         km.close()
     rng = np.random.default_rng(7)
+    sample, sample_got = [], []
     for off in rng.choice(n // 1024, 64, replace=False) * 1024:
         pts = G.gen_kmeans_points(1024, d, k, 42, first=int(off))
         want = O.kmeans_assign(pts, 1024, d, cent, k)
         assert (got[off:off + 1024] == want).all(), off
+        sample.append(pts)
+        sample_got.append(got[off:off + 1024])
+    # the same 2^16 assignments from the REFERENCE LIBRARY's knn with k = 1
+    # (fp64, diff = ref - query, ties to the smaller index; kernels.cpp:195-233)
+    import os
+
+    q = 1 << 16
+    rc, work, out = O.ref_execute("knn", [("in", cent.astype(np.float64)), ("in", np.concatenate(sample).astype(np.float64)),
+                                         ("s", k), ("s", q), ("s", d), ("s", 1), ("out", None), ("out", None)],
+                                  {6: q * 4, 7: q * 8}, threads=os.cpu_count() or 1)
+    assert rc == 0 and work == d * k * q
+    assert (out[6].view(np.int32) == np.concatenate(sample_got)).all()

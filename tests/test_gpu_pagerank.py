@@ -211,6 +211,26 @@ def test_step_rejects_short_col_buffer_and_revalidates(ctx, queues, graph):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("P", [1, 4])
+def test_pagerank_vs_reference_spmv_scale20(ctx, queues, P):
+    """20 GPU iterations (the default fused step, R-MAT scale 20, 2^24 edges)
+    against PageRank iterated on the REFERENCE LIBRARY's spmv_compute in
+    fp64/int64 (oracle/_ref, proj/src/kernels.cpp:132-152): normwise (L1)
+    relative error <= 1e-5, elementwise <= 1e-4."""
+    from paper_2005_08466_b200.pagerank import PageRank
+
+    rp, ci, val, deg = G.pagerank_csr(20, 1 << 24, 42)
+    pr = PageRank(ctx, queues[:P], rp, ci, val, deg, fused=True)
+    pr.reset()
+    pr.iterate(20)
+    got = pr.ranks().astype(np.float64)
+    pr.close()
+    want = O.ref_pagerank(rp, ci, deg, 20)
+    assert np.abs(got - want).sum() / np.abs(want).sum() <= 1e-5
+    assert (np.abs(got - want) / want).max() <= 1e-4
+
+
+@pytest.mark.gpu
 def test_pagerank_full_c3(ctx, queues):
     """SURVEY.md §8(d) C3 at full size: R-MAT scale 24, 2^28 edges, seed 42,
     20 iterations with the default kernels (implicit values, 64-nnz warp units):

@@ -182,3 +182,17 @@ def test_kmeans_restatement_properties():
     perm = np.random.default_rng(0).permutation(2000)
     s2, c2 = O.kmeans_accumulate(pts.reshape(-1, 8)[perm].ravel().copy(), 2000, 8, a[perm].copy(), 16)
     assert (s == s2).all() and (c == c2).all()
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built")
+def test_pagerank_restatement_vs_reference_spmv():
+    """The restated fp32 PageRank (both summation orders) stays within the
+    SURVEY.md §8(c) tolerance of PageRank iterated on the reference library's
+    own spmv_compute in fp64/int64: normwise (L1) <= 1e-5 after 20 iterations."""
+    sc = 14
+    rp, ci, val, deg = O.pagerank_csr(sc, 16 << sc, 42)
+    want = O.ref_pagerank(rp, ci, deg, 20)
+    for order in (False, True):
+        got = O.pagerank(rp, ci, val, deg, 20, b200_order=order).astype(np.float64)
+        assert np.abs(got - want).sum() / np.abs(want).sum() <= 1e-5
+        assert (np.abs(got - want) / want).max() <= 1e-4
