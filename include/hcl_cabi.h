@@ -70,6 +70,10 @@ enum hcl_part_class {
                               uint64 device addresses of the EXCHANGE output's copies
                               on the other parts' devices; the next argument is
                               their count (parts - 1) */
+  HCL_PART_LOCAL = 7,     /* per-device workspace (inout): allocated whole and
+                              zero-filled on every part's device, never copied
+                              between devices; its contents are private to the
+                              device (pagerank_step_binned's bin values) */
   HCL_PART_MERGE_TOPK = 4  /* each part produces full-size per-query sorted
                               top-k lists (an index and a distance output); the
                               runtime folds them pairwise with the kernel's

@@ -45,6 +45,27 @@ int hcl_pagerank_units(const int32_t* row_ptr, int64_t rows, int64_t warp_nnz, i
 int hcl_pagerank_relabel(const int32_t* row_ptr, const int32_t* col_idx, const float* val, const int32_t* outdeg,
                          int64_t v, int32_t* new_row_ptr, int32_t* new_col, float* new_val, int32_t* new_outdeg,
                          int32_t* perm, int threads);
+/* Propagation-blocking layout of one part's rows [lo, hi) for the binned
+ * PageRank step (pagerank_step_binned, csrc/host/pagerank_bins.cpp): chunks of
+ * the part's edges in source order regrouped by destination bin, and the
+ * bin-major destination stream. build returns an opaque handle (NULL on bad
+ * arguments) and fills the sizes; export copies the arrays (any may be NULL):
+ * chunks int32[8*n_chunks] {u0, span, src_off, n_edges, desc_off, n_seg, 0, 0},
+ * src_local uint16[n_src], gtab uint32[(n_chunks+1)*gstride], dst16
+ * uint16[n_entries], units int32[4*n_units] {bin, e0, e1, slot}, slot_units
+ * int32[n_slots], cdesc uint32[n_desc] (per chunk: {bitmap, k_base} per
+ * 32-entry window, then one delta per non-empty segment). */
+typedef struct hcl_pr_bins_info {
+  int64_t lo, hi, bin_rows, chunk_edges, span_max, unit_edges;
+  int64_t n_edges, n_chunks, n_bins, gstride, n_entries, n_src, n_units, n_slots, n_desc;
+} hcl_pr_bins_info;
+void* hcl_pagerank_bins_build(const int32_t* row_ptr, const int32_t* col_idx, int64_t v, int64_t lo, int64_t hi,
+                              int64_t bin_rows, int64_t chunk_edges, int64_t span_max, int64_t unit_edges,
+                              hcl_pr_bins_info* info);
+int hcl_pagerank_bins_export(void* h, int32_t* chunks, uint16_t* src_local, uint32_t* gtab, uint16_t* dst16,
+                             int32_t* units, int32_t* slot_units, uint32_t* cdesc);
+void hcl_pagerank_bins_free(void* h);
+
 /* CSR-adaptive row blocks (<= max_nnz per multi-row block); out may be NULL to
  * count. Returns the number of blocks; out[0..n] are block start rows. */
 int64_t hcl_csr_row_blocks(const int32_t* row_ptr, int64_t rows, int64_t max_nnz, int32_t* out);

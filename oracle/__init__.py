@@ -279,9 +279,11 @@ def spmv_f32_b200(row_ptr, col_idx, val, x, lo: int, hi: int) -> np.ndarray:
     return y
 
 
-def pagerank(row_ptr, col_idx, val, outdeg, iterations: int, b200_order: bool = False) -> np.ndarray:
+def pagerank(row_ptr, col_idx, val, outdeg, iterations: int, b200_order=False) -> np.ndarray:
     """PageRank; b200_order=False sums rows in the reference's ascending order,
-    True in the GPU kernel's restated order (bit-exact check)."""
+    True in the warp-unit kernel's restated order, "fixed" in the binned step's
+    order-free 2^-56 fixed-point sums (bit-exact checks)."""
+    b200_order = 2 if b200_order == "fixed" else int(bool(b200_order))
     v = len(row_ptr) - 1
     x = np.empty(v, np.float32)
     lib().ho_pagerank(v, _ptr(row_ptr, _i32p), _ptr(col_idx, _i32p), _ptr(val, _f32p),

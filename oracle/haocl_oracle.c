@@ -7,6 +7,7 @@
  */
 #include "haocl_oracle.h"
 
+#include <math.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -488,10 +489,31 @@ void ho_spmv_f32_b200(const int32_t* row_ptr, const int32_t* col_idx, const floa
     y[i - lo] = row_sum_b200(col_idx, val, x, row_ptr[i], (int64_t)row_ptr[i + 1] - row_ptr[i]);
 }
 
+/* Order-free row sums of the binned (propagation-blocking) step
+ * (csrc/k_graph.cu, pagerank_step_binned): every product val[p] * x[col[p]]
+ * (= fl32(fl32(1/outdeg) * x), the gather input c of the source) is rounded
+ * to the 2^-56 fixed-point grid (round to nearest even; the scaled product is
+ * exact in fp64, so llrint rounds once), the row sum is the exact integer sum
+ * in any order (mass <= 1 < 2^7), and y = fl32(fl64(sum) * 2^-56). 2^-56 is
+ * also the dangling sum's grid. */
+void ho_spmv_f32_fixed(const int32_t* row_ptr, const int32_t* col_idx, const float* val,
+                       const float* x, int64_t lo, int64_t hi, float* y) {
+  for (int64_t i = lo; i < hi; ++i) {
+    int64_t sum = 0;
+    for (int32_t p = row_ptr[i]; p < row_ptr[i + 1]; ++p) {
+      float c = val[p] * x[col_idx[p]];
+      sum += llrint((double)c * 0x1p56);
+    }
+    y[i - lo] = (float)((double)sum * 0x1p-56);
+  }
+}
+
 /* PageRank (restated; not in the reference). d = 0.85, x0 = 1/V, dangling mass
  * summed exactly in 2^-56 fixed point (order free), then
  *   x_new[i] = base + d * (y[i] + dangling * invV)
- * with every operation individually rounded in fp32. */
+ * with every operation individually rounded in fp32. Row sums y: order 0 =
+ * ascending (the reference's), 1 = the warp-unit kernel's restated order,
+ * 2 = the binned step's order-free fixed-point sums. */
 void ho_pagerank(int64_t v, const int32_t* row_ptr, const int32_t* col_idx, const float* val,
                  const int32_t* outdeg, int iterations, int b200_order, float* x) {
   const float d = 0.85f;
@@ -505,7 +527,9 @@ void ho_pagerank(int64_t v, const int32_t* row_ptr, const int32_t* col_idx, cons
       if (outdeg[j] == 0) dsum += (int64_t)(x[j] * 0x1p56f);
     float dangling = (float)((double)dsum * 0x1p-56);
     float t = dangling * inv_v;
-    if (b200_order)
+    if (b200_order == 2)
+      ho_spmv_f32_fixed(row_ptr, col_idx, val, x, 0, v, y);
+    else if (b200_order)
       ho_spmv_f32_b200(row_ptr, col_idx, val, x, 0, v, y);
     else
       ho_spmv_f32(row_ptr, col_idx, val, x, 0, v, y);

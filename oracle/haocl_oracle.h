@@ -70,6 +70,8 @@ void ho_spmv_f32(const int32_t* row_ptr, const int32_t* col_idx, const float* va
                  const float* x, int64_t lo, int64_t hi, float* y);
 void ho_spmv_f32_b200(const int32_t* row_ptr, const int32_t* col_idx, const float* val,
                       const float* x, int64_t lo, int64_t hi, float* y);
+void ho_spmv_f32_fixed(const int32_t* row_ptr, const int32_t* col_idx, const float* val,
+                       const float* x, int64_t lo, int64_t hi, float* y);
 void ho_pagerank(int64_t v, const int32_t* row_ptr, const int32_t* col_idx, const float* val,
                  const int32_t* outdeg, int iterations, int b200_order, float* x);
 void ho_kmeans_points(uint64_t seed, int64_t first, int64_t count, int64_t d, int64_t blobs,

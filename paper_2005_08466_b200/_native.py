@@ -159,7 +159,17 @@ DATAGEN = [
     ("hcl_pagerank_units", C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_void_p, C.c_void_p, i64p, i64p]),
     ("hcl_pagerank_relabel", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p,
                                        C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int]),
+    ("hcl_pagerank_bins_build", C.c_void_p, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_int64,
+                                             C.c_int64, C.c_int64, C.c_int64, C.c_void_p]),
+    ("hcl_pagerank_bins_export", C.c_int, [C.c_void_p] + [C.c_void_p] * 7),
+    ("hcl_pagerank_bins_free", None, [C.c_void_p]),
 ]
+
+
+class PrBinsInfo(C.Structure):
+    _fields_ = [(n, C.c_int64) for n in ("lo", "hi", "bin_rows", "chunk_edges", "span_max", "unit_edges", "n_edges",
+                                          "n_chunks", "n_bins", "gstride", "n_entries", "n_src", "n_units",
+                                          "n_slots", "n_desc")]
 
 EXTRA = []  # appended by workload modules
 

@@ -355,7 +355,7 @@ struct HostContext::Impl {
         BufferRec& b = buffer(args[i].buffer);
         uint64_t first, len;
         slice(i, part, first, len);
-        if (k.kinds[i] == HCL_ARG_OUT)
+        if (k.kinds[i] == HCL_ARG_OUT || k.classes[i] == HCL_PART_LOCAL)  // LOCAL: private workspace
           ensure_alloc(args[i].buffer, b, part.gid, first, len);
         else
           ensure_valid(args[i].buffer, b, part.gid, first, len, &q);
@@ -466,6 +466,7 @@ struct HostContext::Impl {
     for (uint32_t i = 0; i < n; ++i) {
       if (!args[i].is_buffer || k.kinds[i] == HCL_ARG_IN) continue;
       BufferRec& b = buffer(args[i].buffer);
+      if (k.classes[i] == HCL_PART_LOCAL) continue;  // device-private contents: no validity to track
       if (!whole && k.classes[i] == HCL_PART_REDUCE_SUM) {
         // sum the parts' int64 partials onto the first part's device
         std::vector<int> gids;

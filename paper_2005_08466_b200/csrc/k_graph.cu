@@ -29,6 +29,7 @@
 #include <string>
 
 #include "common.hpp"
+#include "ptx.cuh"
 #include "../../include/hcl_cabi.h"
 
 namespace hcl {
@@ -141,10 +142,11 @@ __device__ __forceinline__ void pr_store_x(float* __restrict__ y, int r, int lo,
 
 // end of an exchange kernel: the block's dangling partial into dsum', and the
 // peer stores made visible system-wide before the allreduce that follows
-__device__ __forceinline__ void pr_exchange_flush(unsigned long long dang, unsigned long long* dsum_next) {
+__device__ __forceinline__ void pr_exchange_flush(unsigned long long dang, unsigned long long* dsum_next,
+                                                  int n_peers = 1) {
   for (int o = 16; o > 0; o >>= 1) dang += __shfl_xor_sync(0xffffffffu, dang, o);
   if ((threadIdx.x & 31) == 0 && dang) atomicAdd(dsum_next, dang);
-  __threadfence_system();
+  if (n_peers) __threadfence_system();  // same-device readers are ordered by the kernel boundary
 }
 
 template <bool UPDATE>
@@ -481,8 +483,485 @@ uint64_t launch_pr_dangling(LaunchCtx& c) {
   return static_cast<uint64_t>(v);
 }
 
+// ---------------------------------------------------------------------------
+// Binned PageRank step (propagation blocking; layout: csrc/host/pagerank_bins.cpp).
+//
+// The pull formulation gathers x at 2^28 random column indices per iteration:
+// one 32-byte sector per 4-byte value, bounded by the L1TEX wavefront rate
+// (~0.95 ms at C3), a quarter of HBM speed. The binned step replaces the
+// random gathers by two streaming passes:
+//   scatter: per chunk of the edges in source order, stage the chunk's gather
+//            inputs c[u0 .. u0+span) in shared memory and write each edge's
+//            value c[src] into its destination bin's segment (bin-major
+//            stream; consecutive lanes write consecutive addresses);
+//   gather:  per bin (heavy bins split into units), stream the bin's values
+//            and uint16 destination offsets into a shared-memory accumulator
+//            of the bin's rows, then finish the rows (the PageRank update, the
+//            next gather input xs' = fl(1/outdeg) x' into every device's copy,
+//            the dangling partial) -- the same epilogue as
+//            pagerank_step_exchange.
+// Row sums are order free: each value is rounded to the 2^-56 fixed-point grid
+// (RN; values are < 1, sums <= 1 < 2^8) and summed exactly in uint64, so the
+// result does not depend on the layout, the unit split or the atomics' order;
+// the oracle restates it (ho_spmv_f32_fixed). Bytes per edge and iteration:
+// 2 (src_local) + 4 (value write) + 4 (value read) + 2 (dst16) = 12, against
+// 8 for the pull CSR's col_idx + gathered x sector-free ideal -- but streamed.
+
+constexpr int PB_T = 512;
+constexpr int PB_WARPS = PB_T / 32;
+
+// parts table row (int64): one per partition of the rows, built by
+// paper_2005_08466_b200/pagerank.py from hcl_pagerank_bins_build
+enum PbPart {
+  PB_LO = 0, PB_HI, PB_CHUNK0, PB_NCHUNKS, PB_NBINS, PB_GSTRIDE, PB_DESC0, PB_SRC0, PB_ENT0, PB_UNIT0,
+  PB_NUNITS, PB_SLOT0, PB_NSLOTS, PB_BINROWS, PB_SPAN, PB_NEDGES, PB_CHUNK_EDGES, PB_FIELDS = 20
+};
+
+__device__ __forceinline__ int ld_stream_u16(const uint16_t* p) {
+  unsigned short v;
+  asm volatile("ld.global.nc.L1::no_allocate.u16 %0, [%1];" : "=h"(v) : "l"(p));
+  return v;
+}
+
+// block-wide exclusive scan of n <= PB_T * 8 ints in shared memory (in place);
+// returns the total. tmp: PB_WARPS ints.
+__device__ int block_exclusive_scan(int* a, int n, int* tmp) {
+  constexpr int PER = 8;
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  int v[PER], sum = 0;
+#pragma unroll
+  for (int k = 0; k < PER; ++k) {
+    const int i = t * PER + k;
+    v[k] = i < n ? a[i] : 0;
+    sum += v[k];
+  }
+  int incl = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) tmp[w] = incl;
+  __syncthreads();
+  if (w == 0) {
+    int x = lane < PB_WARPS ? tmp[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane < PB_WARPS) tmp[lane] = x;
+  }
+  __syncthreads();
+  int run = incl - sum + (w ? tmp[w - 1] : 0);
+  const int total = tmp[PB_WARPS - 1];
+#pragma unroll
+  for (int k = 0; k < PER; ++k) {
+    const int i = t * PER + k;
+    if (i < n) a[i] = run;
+    run += v[k];
+  }
+  __syncthreads();
+  return total;
+}
+
+// Phase 1, persistent CTAs (2 per SM) walking the chunks; each CTA keeps two
+// stages, so chunk i+1's bulk copies (TMA) fly while chunk i is written out.
+// A stage holds the chunk's descriptor (per 32-entry window {bitmap of the
+// entries that start a non-empty segment, segments started before the
+// window}, then per segment delta = bin-major start - chunk-local start), its
+// src_local and the gather inputs c[u0 .. u0+span) (from the 16-byte aligned
+// address below u0). Entry f of window w belongs to segment k = k_base[w] +
+// popcount(bitmap[w] & lanes <= f) - 1 and goes to vals[delta[k] + f]: each
+// warp writes a contiguous run of windows, consecutive lanes to consecutive
+// addresses inside a segment. No search and no block-wide step per chunk.
+__global__ void __launch_bounds__(PB_T, 2) pr_bin_scatter_kernel(const int64_t* __restrict__ part,
+                                                                 const int4* __restrict__ chunks,
+                                                                 const uint16_t* __restrict__ src_local,
+                                                                 const uint32_t* __restrict__ cdesc,
+                                                                 const float* __restrict__ xs, int64_t v,
+                                                                 float* __restrict__ vals, int nst) {
+  extern __shared__ __align__(128) uint8_t pb_smem[];
+  const int64_t n_chunks = part[PB_NCHUNKS], nb = part[PB_NBINS];
+  const int64_t span_max = part[PB_SPAN], ce = part[PB_CHUNK_EDGES];
+  const int64_t nwin_max = (ce + 31) >> 5;
+  const int64_t wcap = (2 * nwin_max + 3) & ~int64_t(3), dcap = (nb + 3) & ~int64_t(3);  // words
+  const int64_t scap = ((ce + 7) & ~int64_t(7)) / 2, ccap = (span_max + 6) & ~int64_t(3);
+  const int64_t stage_words = wcap + dcap + scap + ccap;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(pb_smem + nst * stage_words * 4);  // nst stages + the records
+  int4* rec = reinterpret_cast<int4*>(bar + 4);  // this CTA's chunk records (2 int4 each)
+  chunks += 2 * part[PB_CHUNK0];
+  src_local += part[PB_SRC0];
+  cdesc += part[PB_DESC0];
+  vals += part[PB_ENT0];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned lanemask_le = 0xffffffffu >> (31 - lane);
+  auto stage = [&](int b) { return pb_smem + static_cast<int64_t>(b) * stage_words * 4; };
+  // one elected thread: the chunk's bulk copies into stage b
+  auto issue = [&](const int4& C, const int4& D, int b) {
+    uint8_t* st = stage(b);
+    const int nwin = (C.w + 31) >> 5;
+    const int64_t ua = C.x & ~3, cnt = ((C.x - ua) + C.y + 3) & ~3;
+    const int wwords = (2 * nwin + 3) & ~3, dwords = (D.y + 3) & ~3;
+    const uint32_t sbytes = C.y > 1 ? ((C.w + 7) & ~7) * 2 : 0;
+    const uint32_t cbytes = ua + cnt <= v ? static_cast<uint32_t>(cnt * 4) : 0;
+    ptx::mbar_arrive_expect_tx(&bar[b], static_cast<uint32_t>(wwords + dwords) * 4 + sbytes + cbytes);
+    ptx::bulk_load(st, cdesc + D.x, static_cast<uint32_t>(wwords) * 4, &bar[b]);
+    if (dwords) ptx::bulk_load(st + wcap * 4, cdesc + D.x + wwords, static_cast<uint32_t>(dwords) * 4, &bar[b]);
+    if (sbytes) ptx::bulk_load(st + (wcap + dcap) * 4, src_local + C.z, sbytes, &bar[b]);
+    if (cbytes) ptx::bulk_load(st + (wcap + dcap + scap) * 4, xs + ua, cbytes, &bar[b]);
+  };
+  if (threadIdx.x == 0) {
+    ptx::mbar_init(&bar[0], 1);
+    ptx::mbar_init(&bar[1], 1);
+    ptx::mbar_init(&bar[2], 1);
+    ptx::fence_mbar_init();
+  }
+  __syncthreads();
+  // this CTA's chunks: blockIdx.x, + gridDim.x, ... (neighbouring CTAs write
+  // neighbouring segments of each bin at about the same time); their records
+  // are copied into shared memory once (no global load on the per-chunk path)
+  const int nrec = static_cast<int>((n_chunks - blockIdx.x + gridDim.x - 1) / gridDim.x);
+  if (nrec <= 0) return;
+  for (int i = threadIdx.x; i < 2 * nrec; i += PB_T)
+    rec[i] = __ldg(chunks + 2 * (blockIdx.x + static_cast<int64_t>(i >> 1) * gridDim.x) + (i & 1));
+  __syncthreads();
+  if (threadIdx.x == 0) issue(rec[0], rec[1], 0);
+  for (int it = 0; it < nrec; ++it) {
+    const int b = nst == 2 ? (it & 1) : 0;
+    if (nst == 2 && it + 1 < nrec && threadIdx.x == 0) issue(rec[2 * it + 2], rec[2 * it + 3], b ^ 1);
+    const int4 C = rec[2 * it];  // u0, span, src_off, n
+    uint8_t* st = stage(b);
+    const uint2* win = reinterpret_cast<const uint2*>(st);
+    const int* delta = reinterpret_cast<const int*>(st + wcap * 4);
+    const uint16_t* sl = reinterpret_cast<const uint16_t*>(st + (wcap + dcap) * 4);
+    float* cs = reinterpret_cast<float*>(st + (wcap + dcap + scap) * 4);
+    const int64_t ua = C.x & ~3, cnt = ((C.x - ua) + C.y + 3) & ~3;
+    if (ua + cnt > v) {  // c's tail is not 16-byte complete: plain loads
+      for (int i = threadIdx.x; i < C.y; i += PB_T) cs[C.x - ua + i] = __ldg(xs + C.x + i);
+      __syncthreads();
+    }
+    ptx::mbar_wait(&bar[b], static_cast<uint32_t>((nst == 2 ? it >> 1 : it) & 1));
+    const float* csu = cs + (C.x - ua);
+    const int nwin = (C.w + 31) >> 5;
+    const int per = (nwin + PB_WARPS - 1) / PB_WARPS;
+    const int w0 = warp * per, w1 = min(nwin, w0 + per);
+    const int wfull = min(w1, C.w >> 5);  // windows without a ragged tail
+    auto dest = [&](int w, int f) -> unsigned {
+      const uint2 d = win[w];
+      return static_cast<unsigned>(delta[static_cast<int>(d.y + __popc(d.x & lanemask_le)) - 1] + f);
+    };
+    if (C.y == 1) {  // single-source piece: every entry is c[u0]
+      const float val = csu[0];
+      int w = w0;
+      for (; w < wfull; ++w) vals[dest(w, 32 * w + lane)] = val;
+      if (w < w1 && 32 * w + lane < C.w) vals[dest(w, 32 * w + lane)] = val;
+    } else {
+      int w = w0;
+#pragma unroll 4
+      for (; w < wfull; ++w) {
+        const int f = 32 * w + lane;
+        vals[dest(w, f)] = csu[sl[f]];
+      }
+      if (w < w1 && 32 * w + lane < C.w) vals[dest(w, 32 * w + lane)] = csu[sl[32 * w + lane]];
+    }
+    __syncthreads();  // every warp is done with stage b before it is refilled
+    if (nst == 1 && it + 1 < nrec && threadIdx.x == 0) issue(rec[2 * it + 2], rec[2 * it + 3], 0);
+  }
+}
+
+// shared-memory 32-bit add under a predicate, without a branch (atom returns
+// the old value; 0 when the predicate is off)
+__device__ __forceinline__ unsigned atoms_add_if(unsigned* p, unsigned v, bool pred) {
+  unsigned old;
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %3, 0;\n\tmov.u32 %0, 0;\n\t"
+      "@q atom.shared.add.u32 %0, [%1], %2;\n\t}"
+      : "=r"(old)
+      : "r"(ptx::smem_u32(p)), "r"(v), "r"(static_cast<unsigned>(pred))
+      : "memory");
+  return old;
+}
+__device__ __forceinline__ void reds_add_if(unsigned* p, unsigned v, bool pred) {
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q red.shared.add.u32 [%0], %1;\n\t}" ::"r"(
+          ptx::smem_u32(p)),
+      "r"(v), "r"(static_cast<unsigned>(pred))
+      : "memory");
+}
+
+// Phase 2, one unit per CTA. The unit's entries stream through shared memory
+// by bulk copies (TMA): one elected thread keeps PBG_STAGES stages of
+// PBG_STAGE entries (values + uint16 destinations) in flight, so the HBM
+// stream does not wait for the atomics; each thread takes 8 consecutive
+// entries of a stage. The bin's row sums live in shared memory as two uint32
+// words per row (64-bit shared atomics compile to CAS loops; the low word's
+// carry goes into the high word, so (hi, lo) is the exact 64-bit sum in any
+// order).
+constexpr int PBG_T = 1024, PBG_STAGE = 8 * PBG_T, PBG_STAGES = 2;
+constexpr int PBG_STAGE_BYTES = PBG_STAGE * 6;
+__global__ void __launch_bounds__(PBG_T) pr_bin_gather_kernel(const int64_t* __restrict__ part,
+                                                             const int4* __restrict__ units,
+                                                             const int* __restrict__ slot_units,
+                                                             const float* __restrict__ vals,
+                                                             const uint16_t* __restrict__ dst16,
+                                                             unsigned long long* __restrict__ slot_acc,
+                                                             unsigned int* __restrict__ slot_cnt,
+                                                             const unsigned long long* __restrict__ dsum,
+                                                             float* __restrict__ y, int lo, float base, float damp,
+                                                             float inv_v, const unsigned long long* __restrict__ peers,
+                                                             int n_peers, const float* __restrict__ inv_outdeg,
+                                                             float* __restrict__ xs_next,
+                                                             unsigned long long* __restrict__ dsum_next) {
+  extern __shared__ __align__(128) uint8_t pg_smem[];
+  __shared__ int last_flag;
+  const int64_t W = part[PB_BINROWS], hi = part[PB_HI];
+  uint8_t* stage0 = pg_smem;
+  uint64_t* full = reinterpret_cast<uint64_t*>(stage0 + PBG_STAGES * PBG_STAGE_BYTES);
+  uint64_t* empty = full + PBG_STAGES;
+  unsigned* acc_lo = reinterpret_cast<unsigned*>(empty + PBG_STAGES);
+  unsigned* acc_hi = acc_lo + W;
+  const int4 U = __ldg(units + part[PB_UNIT0] + blockIdx.x);  // bin, e0, e1, slot
+  const int64_t row0 = lo + static_cast<int64_t>(U.x) * W;
+  const int64_t rem = hi - row0;
+  const int nrows = static_cast<int>(W < rem ? W : rem);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  vals += part[PB_ENT0];
+  dst16 += part[PB_ENT0];
+  const int64_t n_ent = U.z - U.y, n_st = (n_ent + PBG_STAGE - 1) / PBG_STAGE;
+  auto issue = [&](int64_t st) {  // stage st of the unit into buffer st % PBG_STAGES
+    const int b = static_cast<int>(st % PBG_STAGES);
+    uint8_t* sp = stage0 + b * PBG_STAGE_BYTES;
+    const int64_t e = U.y + st * PBG_STAGE;
+    const uint32_t cnt = static_cast<uint32_t>(min(static_cast<int64_t>(PBG_STAGE), U.z - e));  // multiple of 8
+    ptx::mbar_arrive_expect_tx(&full[b], cnt * 6);
+    ptx::bulk_load(sp, vals + e, cnt * 4, &full[b]);
+    ptx::bulk_load(sp + PBG_STAGE * 4, dst16 + e, cnt * 2, &full[b]);
+  };
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < PBG_STAGES; ++b) {
+      ptx::mbar_init(&full[b], 1);
+      ptx::mbar_init(&empty[b], PBG_T / 32);
+    }
+    ptx::fence_mbar_init();
+    for (int64_t st = 0; st < min(n_st, static_cast<int64_t>(PBG_STAGES)); ++st) issue(st);
+  }
+  for (int r = threadIdx.x; r < nrows; r += PBG_T) acc_lo[r] = acc_hi[r] = 0u;
+  __syncthreads();
+  for (int64_t st = 0; st < n_st; ++st) {
+    const int b = static_cast<int>(st % PBG_STAGES);
+    ptx::mbar_wait(&full[b], static_cast<uint32_t>((st / PBG_STAGES) & 1));
+    const uint8_t* sp = stage0 + b * PBG_STAGE_BYTES;
+    const int cnt = static_cast<int>(min(static_cast<int64_t>(PBG_STAGE), n_ent - st * PBG_STAGE));
+    // this thread's group of 8 consecutive entries: the lanes of a warp take
+    // groups 32 apart (skewed by the warp so the stage reads spread over the
+    // banks), so the lanes of one atomic rarely share a hub row's run
+    const int grp = lane * (PBG_T / 32) + ((warp + lane) & (PBG_T / 32 - 1));
+    {
+      // segments are sorted by destination, so a hub row's entries come in
+      // runs -- each run is added up in registers and lands with one
+      // (predicated, branch-free) atomic at its last entry. Lanes past a
+      // ragged last stage carry value 0 (no atomics) but stay converged.
+      const bool valid = 8 * grp < cnt;
+      const float4 zf = make_float4(0.f, 0.f, 0.f, 0.f);
+      const float4 va = valid ? reinterpret_cast<const float4*>(sp)[2 * grp] : zf;
+      const float4 vb = valid ? reinterpret_cast<const float4*>(sp)[2 * grp + 1] : zf;
+      const uint4 d = valid ? reinterpret_cast<const uint4*>(sp + PBG_STAGE * 4)[grp] : make_uint4(0, 0, 0, 0);
+      const float vv[8] = {va.x, va.y, va.z, va.w, vb.x, vb.y, vb.z, vb.w};
+      const unsigned dd[8] = {d.x & 0xffffu, d.x >> 16, d.y & 0xffffu, d.y >> 16,
+                              d.z & 0xffffu, d.z >> 16, d.w & 0xffffu, d.w >> 16};
+      unsigned long long run = 0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const unsigned long long q = __float2ull_rn(__fmul_rn(vv[k], 0x1p56f));
+        run = (k > 0 && dd[k] == dd[k - 1]) ? run + q : q;
+        const bool last = k == 7 || dd[k] != dd[k + 1];
+        const unsigned ql = static_cast<unsigned>(run);
+        const unsigned old = atoms_add_if(acc_lo + dd[k], ql, last && ql != 0u);
+        const unsigned qh = static_cast<unsigned>(run >> 32) + (old + ql < ql);  // carry out of the low word
+        if (__any_sync(0xffffffffu, last && qh != 0u)) reds_add_if(acc_hi + dd[k], qh, last && qh != 0u);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) ptx::mbar_arrive(&empty[b]);
+    if (threadIdx.x == 0 && st + PBG_STAGES < n_st) {  // refill once every warp is done with the stage
+      ptx::mbar_wait(&empty[b], static_cast<uint32_t>((st / PBG_STAGES) & 1));
+      issue(st + PBG_STAGES);
+    }
+  }
+  __syncthreads();
+  auto acc = [&](int r) -> unsigned long long {
+    return (static_cast<unsigned long long>(acc_hi[r]) << 32) | acc_lo[r];
+  };
+  if (U.w >= 0) {  // a heavy bin split into units: combine in the slot, the last unit finishes the rows
+    const int slot = static_cast<int>(part[PB_SLOT0]) + U.w;
+    unsigned long long* sa = slot_acc + static_cast<int64_t>(slot) * W;
+    for (int r = threadIdx.x; r < nrows; r += PBG_T)
+      if (const unsigned long long a = acc(r)) atomicAdd(sa + r, a);
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0)
+      last_flag = atomicAdd(slot_cnt + slot, 1u) == static_cast<unsigned>(__ldg(slot_units + slot) - 1);
+    __syncthreads();
+    if (!last_flag) return;
+    __threadfence();
+    for (int r = threadIdx.x; r < nrows; r += PBG_T) {
+      const unsigned long long a = __ldcg(sa + r);
+      acc_lo[r] = static_cast<unsigned>(a);
+      acc_hi[r] = static_cast<unsigned>(a >> 32);
+      sa[r] = 0ull;  // the slot is zero again for the next step
+    }
+    if (threadIdx.x == 0) slot_cnt[slot] = 0u;
+    __syncthreads();
+  }
+  const Update upd = pr_update<true>(dsum, base, damp, inv_v);
+  const Fanout fo = load_fanout(peers, n_peers, xs_next, inv_outdeg);
+  unsigned long long dang = 0;
+  for (int r = threadIdx.x; r < nrows; r += PBG_T) {
+    const float s = static_cast<float>(__ll2double_rn(static_cast<long long>(acc(r))) * 0x1p-56);
+    pr_store_x<true, true>(y, static_cast<int>(row0 + r), lo, s, upd, fo, dang);
+  }
+  pr_exchange_flush(dang, dsum_next, n_peers);
+}
+
+struct PbPartRow {
+  int64_t f[PB_FIELDS];
+};
+struct PbKey {
+  int dev;
+  const void* ptr;
+  uint64_t version;
+  bool operator<(const PbKey& o) const { return std::tie(dev, ptr, version) < std::tie(o.dev, o.ptr, o.version); }
+};
+std::mutex g_pb_mu;
+std::map<PbKey, std::vector<PbPartRow>> g_pb_parts;
+
+// pagerank_step_binned(parts chunks src_local gtab dst16 units slot_units xs dsum x' | V n_parts |
+//                      peers n_peers inv_outdeg xs' dsum' | vals(LOCAL) slot_acc(LOCAL))
+uint64_t launch_pr_binned(LaunchCtx& c) {
+  const char* what = "pagerank_step_binned";
+  const int64_t v = scalar_arg(c, 10, what), n_parts = scalar_arg(c, 11, what);
+  const int n_peers = static_cast<int>(scalar_arg(c, 13, what));
+  if (v < 1 || v > INT32_MAX - 1 || n_parts < 1) fail(ErrorCode::argument, std::string(what) + ": bad V or parts");
+  const BufView& PT = buffer_arg(c, 0, what);
+  if (PT.first_byte != 0 || PT.bytes != static_cast<uint64_t>(n_parts) * PB_FIELDS * 8)
+    fail(ErrorCode::argument, std::string(what) + ": the parts table holds " + std::to_string(PB_FIELDS) +
+                                  " int64 per part");
+  const BufView& CH = buffer_arg(c, 1, what);
+  const BufView& SL = buffer_arg(c, 2, what);
+  const BufView& GT = buffer_arg(c, 3, what);
+  const BufView& DS = buffer_arg(c, 4, what);
+  const BufView& UN = buffer_arg(c, 5, what);
+  const BufView& SU = buffer_arg(c, 6, what);
+  const BufView& XS = buffer_arg(c, 7, what);
+  const BufView& D = buffer_arg(c, 8, what);
+  const BufView& PB = buffer_arg(c, 12, what);
+  const BufView& OD = buffer_arg(c, 14, what);
+  const BufView& XN = buffer_arg(c, 15, what);
+  const BufView& DN = buffer_arg(c, 16, what);
+  const BufView& VA = buffer_arg(c, 17, what);
+  const BufView& SA = buffer_arg(c, 18, what);
+  if (XS.bytes != static_cast<uint64_t>(v) * 4 || OD.bytes != static_cast<uint64_t>(v) * 4 ||
+      XN.bytes != static_cast<uint64_t>(v) * 4 || D.bytes != 8 || DN.bytes != 8)
+    fail(ErrorCode::argument, std::string(what) + ": xs, inv_outdeg, xs' must hold V floats, dsum/dsum' one uint64");
+  if (n_peers < 0 || n_peers > PR_MAX_PEERS || PB.bytes < static_cast<uint64_t>(n_peers) * 8)
+    fail(ErrorCode::argument, std::string(what) + ": peers must list 0..7 device addresses");
+  uint64_t lo, rows;
+  sub_range(c, static_cast<uint64_t>(v), lo, rows, what);
+  float* y = at_byte<float>(buffer_arg(c, 9, what), lo * 4, rows * 4, what);
+  HCL_CUDA(cudaMemsetAsync(DN.ptr, 0, 8, c.stream));
+  if (!rows) return 0;
+  // the host copy of the parts table (read once per table contents)
+  std::vector<PbPartRow> parts;
+  {
+    std::lock_guard<std::mutex> lock(g_pb_mu);
+    auto it = PT.version ? g_pb_parts.find({c.dev, PT.ptr, PT.version}) : g_pb_parts.end();
+    if (it != g_pb_parts.end()) parts = it->second;
+  }
+  if (parts.empty()) {
+    parts.resize(static_cast<size_t>(n_parts));
+    HCL_CUDA(cudaMemcpyAsync(parts.data(), PT.ptr, PT.bytes, cudaMemcpyDeviceToHost, c.stream));
+    HCL_CUDA(cudaStreamSynchronize(c.stream));
+    if (PT.version) {
+      std::lock_guard<std::mutex> lock(g_pb_mu);
+      if (g_pb_parts.size() > 256) g_pb_parts.clear();
+      g_pb_parts[{c.dev, PT.ptr, PT.version}] = parts;
+    }
+  }
+  int pi = -1;
+  for (int i = 0; i < static_cast<int>(parts.size()); ++i)
+    if (parts[i].f[PB_LO] == static_cast<int64_t>(lo) && parts[i].f[PB_HI] == static_cast<int64_t>(lo + rows)) pi = i;
+  if (pi < 0) fail(ErrorCode::argument, std::string(what) + ": no part of the layout covers rows [" +
+                                            std::to_string(lo) + ", " + std::to_string(lo + rows) + ")");
+  const int64_t* P = parts[pi].f;
+  const int64_t nb = P[PB_NBINS], gs = P[PB_GSTRIDE], W = P[PB_BINROWS], span = P[PB_SPAN];
+  if (nb > PB_T * 8 || nb < 1 || gs < nb + 1 || (gs & 3) || W < 8 || W > 65536 || span < 1 || (P[PB_ENT0] & 7) ||
+      (P[PB_SRC0] & 7) || (P[PB_DESC0] & 3) || P[PB_CHUNK_EDGES] < 8 || P[PB_CHUNK_EDGES] > 65536)
+    fail(ErrorCode::argument, std::string(what) + ": bad layout geometry");
+  // bounds of every array this part touches
+  auto need = [&](const BufView& b, uint64_t bytes, const char* name) {
+    if (b.first_byte != 0 || b.bytes < bytes) fail(ErrorCode::argument, std::string(what) + ": " + name + " too short");
+  };
+  need(CH, static_cast<uint64_t>(P[PB_CHUNK0] + P[PB_NCHUNKS]) * 32, "chunks");
+  need(GT, static_cast<uint64_t>(P[PB_DESC0]) * 4, "chunk descriptors");
+  need(UN, static_cast<uint64_t>(P[PB_UNIT0] + P[PB_NUNITS]) * 16, "units");
+  need(SU, static_cast<uint64_t>(P[PB_SLOT0] + P[PB_NSLOTS]) * 4, "slot_units");
+  need(SL, static_cast<uint64_t>(P[PB_SRC0]) * 2, "src_local");
+  need(SA, static_cast<uint64_t>(P[PB_SLOT0] + P[PB_NSLOTS]) * (W * 8 + 4), "slot accumulators");
+  if (VA.bytes / 4 < DS.bytes / 2 || VA.first_byte != 0 || DS.first_byte != 0 || (DS.bytes / 2) < 8)
+    fail(ErrorCode::argument, std::string(what) + ": vals must hold one float per dst16 entry");
+  const int64_t* dpart = reinterpret_cast<const int64_t*>(PT.ptr) + static_cast<int64_t>(pi) * PB_FIELDS;
+  // phase 1
+  const int64_t ce = P[PB_CHUNK_EDGES];
+  const int64_t nwin_max = (ce + 31) >> 5;
+  const int64_t stage_words = ((2 * nwin_max + 3) & ~int64_t(3)) + ((nb + 3) & ~int64_t(3)) +
+                              ((ce + 7) & ~int64_t(7)) / 2 + ((span + 6) & ~int64_t(3));
+  const int64_t recs_max = (P[PB_NCHUNKS] + c.sm_count - 1) / c.sm_count + 1;  // any grid >= sm_count
+  // two CTAs per SM; two stages per CTA when they fit (copies of chunk i+1 in
+  // flight while chunk i is written), else one (the other CTA overlaps)
+  auto smem_for = [&](int nst) {
+    return static_cast<size_t>(nst * stage_words) * 4 + 32 + static_cast<size_t>(recs_max) * 32 + 64;
+  };
+  int nst = 2 * (smem_for(2) + 1024) <= 228 * 1024 ? 2 : 1;
+  if (const char* e = std::getenv("HCL_PB_NST")) nst = std::atoi(e) == 2 && smem_for(2) <= 227 * 1024 ? 2 : 1;
+  const size_t smem1 = smem_for(nst);
+  HCL_CUDA(cudaFuncSetAttribute(pr_bin_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(smem1)));
+  int per_sm = 1;
+  HCL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pr_bin_scatter_kernel, PB_T, smem1));
+  const int grid1 = static_cast<int>(std::min<int64_t>(P[PB_NCHUNKS],
+                                                       static_cast<int64_t>(std::min(2, std::max(1, per_sm))) * c.sm_count));
+  if (grid1 > 0) {
+    pr_bin_scatter_kernel<<<grid1, PB_T, smem1, c.stream>>>(
+        dpart, reinterpret_cast<const int4*>(CH.ptr), reinterpret_cast<const uint16_t*>(SL.ptr),
+        reinterpret_cast<const uint32_t*>(GT.ptr), reinterpret_cast<const float*>(XS.ptr), v,
+        reinterpret_cast<float*>(VA.ptr), nst);
+    HCL_LAUNCHED();
+  }
+  // phase 2
+  const size_t smem2 = static_cast<size_t>(PBG_STAGES) * PBG_STAGE_BYTES + 2 * PBG_STAGES * 8 +
+                       static_cast<size_t>(W) * 8;
+  HCL_CUDA(cudaFuncSetAttribute(pr_bin_gather_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(smem2)));
+  const int64_t n_slots_total = static_cast<int64_t>(SA.bytes / (W * 8 + 4));
+  unsigned long long* slot_acc = reinterpret_cast<unsigned long long*>(SA.ptr);
+  unsigned int* slot_cnt = reinterpret_cast<unsigned int*>(slot_acc + n_slots_total * W);
+  const float base = static_cast<float>((1.0 - 0.85) / v), damp = 0.85f, inv_v = static_cast<float>(1.0 / v);
+  if (P[PB_NUNITS] > 0) {
+    pr_bin_gather_kernel<<<static_cast<unsigned>(P[PB_NUNITS]), PBG_T, smem2, c.stream>>>(
+        dpart, reinterpret_cast<const int4*>(UN.ptr), reinterpret_cast<const int*>(SU.ptr),
+        reinterpret_cast<const float*>(VA.ptr), reinterpret_cast<const uint16_t*>(DS.ptr), slot_acc, slot_cnt,
+        reinterpret_cast<const unsigned long long*>(D.ptr), y, static_cast<int>(lo), base, damp, inv_v,
+        reinterpret_cast<const unsigned long long*>(PB.ptr), n_peers, reinterpret_cast<const float*>(OD.ptr),
+        reinterpret_cast<float*>(XN.ptr), reinterpret_cast<unsigned long long*>(DN.ptr));
+    HCL_LAUNCHED();
+  }
+  return 2ull * static_cast<uint64_t>(P[PB_NEDGES]);  // the reference's spmv_compute units (kernels.cpp:292)
+}
+
 uint64_t rows_pr(const int64_t* s, uint32_t n) { return static_cast<uint64_t>(s[n == 13 ? 8 : 7]); }
 uint64_t rows_pr_imp(const int64_t* s, uint32_t) { return static_cast<uint64_t>(s[7]); }
+uint64_t rows_pr_binned(const int64_t* s, uint32_t) { return static_cast<uint64_t>(s[10]); }
 
 }  // namespace
 
@@ -506,6 +985,12 @@ void register_graph(std::vector<KernelDef>& r) {
   // row_ptr col units long_rows xs dsum x' | V nnz_off n_units n_long warp_nnz | peers n_peers inv_outdeg xs' dsum'
   // (inv_outdeg = fl(1/outdeg) as fp32, 0 for dangling vertices: datagen.pagerank_inv_outdeg)
   constexpr uint8_t XG = HCL_PART_EXCHANGE, PR = HCL_PART_PEERS, RS = HCL_PART_REDUCE_SUM;
+  // binned step (propagation blocking): the layout of hcl_pagerank_bins_build per part + the exchange epilogue
+  constexpr uint8_t IO = HCL_ARG_INOUT, LC = HCL_PART_LOCAL;
+  r.push_back({"b200", "pagerank_step_binned",
+               {I, I, I, I, I, I, I, I, I, O, S, S, I, S, I, O, O, IO, IO},
+               {P, P, P, P, P, P, P, P, P, X, N, N, PR, N, P, XG, RS, LC, LC}, launch_pr_binned, nullptr,
+               rows_pr_binned});
   r.push_back({"b200", "pagerank_step_exchange", {I, I, I, I, I, I, O, S, S, S, S, S, I, S, I, O, O},
                {P, P, P, P, P, P, X, N, N, N, N, N, PR, N, P, XG, RS}, launch_pr<true, true, true>, nullptr,
                rows_pr_imp});

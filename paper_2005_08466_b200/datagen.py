@@ -119,3 +119,49 @@ def pagerank_inv_outdeg(outdeg: np.ndarray) -> np.ndarray:
     nz = d > 0
     inv[nz] = np.float32(1.0) / d[nz].astype(np.float32)
     return inv
+
+
+# binned (propagation-blocking) PageRank layout defaults: 16384-row bins (the
+# gather's shared-memory accumulator is bin_rows x 8 bytes; dst16 offsets need
+# bin_rows <= 65536), chunks of <= 65536 edges spanning <= 8192 sources (the
+# scatter stages a chunk's descriptor, src_local and gather inputs in shared
+# memory; measured at C3 on B200: 65536-edge chunks 1.00 ms per iteration,
+# 32768 1.12-1.15, 16384 1.25-1.27 -- the per-chunk cost dominates)
+PR_BIN_ROWS, PR_CHUNK_EDGES, PR_SPAN_MAX = 16384, 65536, 8192
+
+
+def pagerank_bins(row_ptr: np.ndarray, col_idx: np.ndarray, lo: int = 0, hi: int | None = None,
+                  bin_rows: int = PR_BIN_ROWS, chunk_edges: int = PR_CHUNK_EDGES, span_max: int = PR_SPAN_MAX,
+                  unit_edges: int = 0) -> dict:
+    """Propagation-blocking layout of rows [lo, hi) (hcl_pagerank_bins_build):
+    a dict of numpy arrays (chunks, src_local, gtab, dst16, units, slot_units, cdesc)
+    plus the sizes. unit_edges = 0 sizes the gather units for ~4 per SM of a
+    148-SM B200 (heavy bins split, the rest one unit per bin)."""
+    import ctypes as C
+
+    rp = np.ascontiguousarray(row_ptr, np.int32)
+    ci = np.ascontiguousarray(col_idx, np.int32)
+    v = len(rp) - 1
+    hi = v if hi is None else hi
+    if unit_edges <= 0:
+        unit_edges = max(4096, int(rp[hi]) - int(rp[lo])) // (148 * 4) + 8
+    info = N.PrBinsInfo()
+    h = N.lib().hcl_pagerank_bins_build(rp.ctypes.data, ci.ctypes.data, v, lo, hi, bin_rows, chunk_edges, span_max,
+                                        unit_edges, C.byref(info))
+    if not h:
+        raise N.HaoclError(9, "pagerank_bins: bad arguments")
+    try:
+        out = {f: int(getattr(info, f)) for f, _ in N.PrBinsInfo._fields_}
+        out["chunks"] = np.empty(8 * info.n_chunks, np.int32)
+        out["src_local"] = np.empty(max(1, info.n_src), np.uint16)
+        out["gtab"] = np.empty((info.n_chunks + 1) * info.gstride, np.uint32)
+        out["dst16"] = np.empty(max(8, info.n_entries), np.uint16)
+        out["units"] = np.empty(max(4, 4 * info.n_units), np.int32)
+        out["slot_units"] = np.empty(max(1, info.n_slots), np.int32)
+        out["cdesc"] = np.empty(max(4, info.n_desc), np.uint32)
+        N.lib().hcl_pagerank_bins_export(h, *(out[k].ctypes.data for k in
+                                              ("chunks", "src_local", "gtab", "dst16", "units", "slot_units",
+                                               "cdesc")))
+    finally:
+        N.lib().hcl_pagerank_bins_free(h)
+    return out

@@ -15,7 +15,7 @@ from typing import Optional, Sequence
 
 import numpy as np
 
-from .datagen import pagerank_inv_outdeg, pagerank_relabel, pagerank_units
+from .datagen import pagerank_bins, pagerank_inv_outdeg, pagerank_relabel, pagerank_units
 from .runtime import Handle, HostContext, spmv_partition_ranges
 
 DEFAULT_WARP_NNZ = 64  # measured best at scale 24 (profiles/r01_pagerank_experiments.txt)
@@ -25,7 +25,8 @@ class PageRank:
     def __init__(self, ctx: HostContext, queues: Sequence[Handle], row_ptr: np.ndarray, col_idx: np.ndarray,
                  val: np.ndarray, outdeg: np.ndarray, max_nnz: int = DEFAULT_WARP_NNZ,
                  weights: Optional[Sequence[int]] = None, relabel: bool = False, implicit: bool = True,
-                 fused: bool = False):
+                 fused: bool = False, binned: bool = False, bounds: Optional[Sequence[int]] = None,
+                 bin_options: Optional[dict] = None):
         """relabel: store the graph degree-ordered (hcl_pagerank_relabel) so the
         hot ranks form a dense prefix of x; per-row sums are unchanged, and
         ranks()/spmv() map results back to the caller's vertex ids. implicit: the
@@ -37,6 +38,13 @@ class PageRank:
         # NVLink stores through the runtime-filled PEERS list) and its dangling partial
         # (REDUCE_SUM); no prep pass and no copies of the rank vector between iterations
         self.fused = fused and implicit
+        # binned: one partitioned pagerank_step_binned per iteration (propagation blocking:
+        # a scatter pass streams each edge's value into its destination bin, a gather pass
+        # accumulates each bin in shared memory -- no random gathers; order-free 2^-56
+        # fixed-point row sums) with the same exchange epilogue as the fused step
+        self.binned = binned
+        if binned:
+            self.fused = False
         self.ctx, self.queues = ctx, list(queues)
         self.perm = None
         if relabel:
@@ -47,7 +55,8 @@ class PageRank:
         units, long_rows, n_long = pagerank_units(row_ptr, max_nnz)
         self.n_units, self.n_long = len(units), n_long
         rp64 = np.ascontiguousarray(row_ptr, np.int64)
-        self.bounds = [int(b) for b in spmv_partition_ranges(rp64, len(self.queues), weights)]
+        self.bounds = [int(b) for b in (bounds if bounds is not None else
+                                        spmv_partition_ranges(rp64, len(self.queues), weights))]
         q0 = self.queues[0]
         mk = ctx.create_buffer
         self.b_rp, self.b_units, self.b_long = mk(row_ptr.nbytes), mk(units.nbytes), mk(long_rows.nbytes)
@@ -93,18 +102,86 @@ class PageRank:
                                        self.b_dsum2[i], self.b_x[0]] + self.tail +
                                       [self.b_peers, P - 1, self.b_inv, self.b_xs2[1 - i], self.b_dsum2[1 - i]]):
                     ctx.set_kernel_arg(kk, j, a)
+        if self.binned:
+            self._setup_binned(row_ptr, col_idx, outdeg, bin_options or {})
         self.cur = 0
+
+    def _setup_binned(self, row_ptr, col_idx, outdeg, opts) -> None:
+        """Per part with rows: the propagation-blocking layout of its rows
+        (hcl_pagerank_bins_build), concatenated into one buffer per array with
+        a parts table the kernel selects its part from by its row range."""
+        ctx, q0, mk = self.ctx, self.queues[0], self.ctx.create_buffer
+        P = len(self.queues)
+        parts, arrays = [], {k: [] for k in ("chunks", "src_local", "cdesc", "dst16", "units", "slot_units")}
+        base = dict(chunk=0, src=0, desc=0, ent=0, unit=0, slot=0)
+        self.layouts = []
+        for i in range(P):
+            lo, hi = self.bounds[i], self.bounds[i + 1]
+            if hi <= lo:
+                continue
+            L = pagerank_bins(row_ptr, col_idx, lo, hi, **opts)
+            self.layouts.append(L)
+            parts.append([lo, hi, base["chunk"], L["n_chunks"], L["n_bins"], L["gstride"], base["desc"], base["src"],
+                          base["ent"], base["unit"], L["n_units"], base["slot"], L["n_slots"], L["bin_rows"],
+                          L["span_max"], L["n_edges"], L["chunk_edges"], 0, 0, 0])
+            arrays["chunks"].append(L["chunks"][:8 * L["n_chunks"]])
+            arrays["src_local"].append(L["src_local"][:L["n_src"]])
+            arrays["cdesc"].append(L["cdesc"][:L["n_desc"]])
+            arrays["dst16"].append(L["dst16"][:L["n_entries"]])
+            arrays["units"].append(L["units"][:4 * L["n_units"]])
+            arrays["slot_units"].append(L["slot_units"][:L["n_slots"]])
+            base["chunk"] += L["n_chunks"]
+            base["src"] += L["n_src"]
+            base["desc"] += L["n_desc"]
+            base["ent"] += L["n_entries"]
+            base["unit"] += L["n_units"]
+            base["slot"] += L["n_slots"]
+        self.bin_rows = self.layouts[0]["bin_rows"]
+        table = np.array(parts, np.int64).reshape(-1)
+        cat = {k: np.concatenate(v) if sum(len(x) for x in v) else np.zeros(8, v[0].dtype if v else np.int32)
+               for k, v in arrays.items()}
+        cat["dst16"] = np.concatenate([cat["dst16"], np.zeros(8, np.uint16)])  # >= 8 entries
+        self.b_parts = mk(table.nbytes)
+        ctx.enqueue_write_buffer(q0, self.b_parts, table)
+        self.b_bins = {}
+        for k, a in cat.items():
+            self.b_bins[k] = mk(a.nbytes)
+            ctx.enqueue_write_buffer(q0, self.b_bins[k], np.ascontiguousarray(a))
+        n_slots = max(1, base["slot"])
+        self.b_vals = mk(4 * len(cat["dst16"]))  # LOCAL: zero-filled per device (padding entries stay 0)
+        self.b_slot_acc = mk(n_slots * (self.bin_rows * 8 + 4))
+        self.b_xs2, self.b_dsum2 = [mk(self.v * 4), mk(self.v * 4)], [mk(8), mk(8)]
+        self.b_inv = mk(self.v * 4)
+        ctx.enqueue_write_buffer(q0, self.b_inv, pagerank_inv_outdeg(outdeg))
+        self.b_peers = mk(8 * max(1, len(parts) - 1))
+        prog = ctx.create_program("b200")
+        self.k_prep0 = ctx.create_kernel(prog, "pagerank_prep")
+        for j, a in enumerate([self.b_x[0], self.b_deg, self.b_dsum2[0], self.b_xs2[0], self.v]):
+            ctx.set_kernel_arg(self.k_prep0, j, a)
+        self.k_bin = [ctx.create_kernel(prog, "pagerank_step_binned") for _ in range(2)]
+        B = self.b_bins
+        for i, kk in enumerate(self.k_bin):  # reads xs[i], dsum[i]; writes x rows, xs[1-i], dsum[1-i]
+            for j, a in enumerate([self.b_parts, B["chunks"], B["src_local"], B["cdesc"], B["dst16"], B["units"],
+                                   B["slot_units"], self.b_xs2[i], self.b_dsum2[i], self.b_x[0], self.v, len(parts),
+                                   self.b_peers, len(parts) - 1, self.b_inv, self.b_xs2[1 - i], self.b_dsum2[1 - i],
+                                   self.b_vals, self.b_slot_acc]):
+                ctx.set_kernel_arg(kk, j, a)
 
     def reset(self) -> None:
         x0 = np.full(self.v, np.float32(1.0 / self.v), np.float32)
         self.ctx.enqueue_write_buffer(self.queues[0], self.b_x[0], x0)
         self.cur = 0
-        if self.fused:  # iteration 0's gather input and dangling sum
+        if self.fused or self.binned:  # iteration 0's gather input and dangling sum
             self.ctx.enqueue_ndrange_kernel(self.queues[0], self.k_prep0)
 
     def iterate(self, iterations: int) -> None:
         ctx = self.ctx
         for _ in range(iterations):
+            if self.binned:
+                ctx.enqueue_ndrange_partitioned(self.k_bin[self.cur], (self.v, 1, 1), 1, self.queues,
+                                                bounds=self.bounds)
+                self.cur = 1 - self.cur
+                continue
             if self.fused:
                 ctx.enqueue_ndrange_partitioned(self.k_stepx[self.cur], (self.v, 1, 1), 1, self.queues,
                                                 bounds=self.bounds)
@@ -127,7 +204,7 @@ class PageRank:
 
     def ranks(self) -> np.ndarray:
         self.finish()
-        bx = self.b_x[0] if self.fused else self.b_x[self.cur]
+        bx = self.b_x[0] if (self.fused or self.binned) else self.b_x[self.cur]
         return self._to_caller(self.ctx.enqueue_read_buffer(self.queues[0], bx).view(np.float32))
 
     def _to_caller(self, r: np.ndarray) -> np.ndarray:
@@ -157,6 +234,9 @@ class PageRank:
             self.ctx.release(b)
         if self.implicit:
             self.ctx.release(self.b_xs)
-        if self.fused:
+        if self.fused or self.binned:
             for b in (*self.b_xs2, *self.b_dsum2, self.b_peers, self.b_inv):
+                self.ctx.release(b)
+        if self.binned:
+            for b in (self.b_parts, *self.b_bins.values(), self.b_vals, self.b_slot_acc):
                 self.ctx.release(b)
