@@ -491,6 +491,11 @@ class PageRankW(Workload):
         self.q = q = ctx.create_queue(0)
         t0 = time.perf_counter()
         rp, ci, val, deg = G.pagerank_csr(self.scale, self.e, 42)
+        # default step: the binned (propagation-blocking) kernel; BENCH_PR_KERNEL=pull
+        # selects the warp-unit pull SpMV (fused exchange step) of round 1
+        self.binned = os.environ.get("BENCH_PR_KERNEL", "binned") == "binned"
+        if self.binned:
+            return self.setup_binned(rp, ci, val, deg, t0)
         # degree-ordered vertex ids (per-row sums unchanged; tests/test_gpu_pagerank.py)
         self.relabel = os.environ.get("BENCH_PR_RELABEL", "0") == "1"
         if self.relabel:
@@ -617,6 +622,70 @@ class PageRankW(Workload):
                   f"{self.rank_kernel_ms():.4f} ms", file=sys.stderr, flush=True)
             self.reset()
 
+    def setup_binned(self, rp, ci, val, deg, t0):
+        """The rank's rows [lo, hi) (cost-balanced: nnz + row_cost * N per row)
+        as one propagation-blocking part; the gather epilogue stores the next
+        gather input xs' of its rows into every rank's xs' (IPC-mapped peer
+        buffers over NVLink) and an 8-byte allreduce of the dangling sums is the
+        only collective per step."""
+        import numpy as np
+        import torch
+
+        from paper_2005_08466_b200 import HostContext, spmv_partition_ranges
+        from paper_2005_08466_b200 import datagen as G
+        from paper_2005_08466_b200.pagerank import BinnedLayout
+
+        d, ctx, q, mk = self.dist, self.ctx, self.q, self.ctx.create_buffer
+        self.relabel, self.implicit, self.fused, self.wn = False, True, True, 0
+        self.row_cost = row_cost = float(os.environ.get("BENCH_PR_ROW_COST", "2.5")) * d.world
+        cum = rp.astype(np.int64) + np.round(row_cost * np.arange(len(rp))).astype(np.int64)
+        self.bounds = [int(x) for x in spmv_partition_ranges(cum, d.world)]
+        lo, hi = self.bounds[d.rank], self.bounds[d.rank + 1]
+        self.lo, self.rows = lo, hi - lo
+        self.nnz_local = int(rp[hi]) - int(rp[lo])
+        t1 = time.perf_counter()
+        self.bl = BinnedLayout(ctx, q, rp, ci, [lo, hi])
+        self.layout_s = time.perf_counter() - t1
+        ctx.add_data_creation_ms((time.perf_counter() - t0) * 1e3)
+        self.b_deg, self.b_inv, self.b_x = mk(deg.nbytes), mk(self.v * 4), [mk(self.v * 4)]
+        ctx.enqueue_write_buffer(q, self.b_deg, deg)
+        ctx.enqueue_write_buffer(q, self.b_inv, G.pagerank_inv_outdeg(deg))
+        if d.world > 1:
+            uid = d.bcast_bytes(HostContext.nccl_unique_id() if d.rank == 0 else None)
+            ctx.init_collectives(q, d.rank, d.world, uid)
+        self.b_xs2 = [mk(self.v * 4), mk(self.v * 4)]
+        handles = d.allgather_bytes(b"".join(ctx.share_buffer(q, b) for b in self.b_xs2)) if d.world > 1 else None
+        self.b_dsum2 = [mk(8), mk(8)]
+        self.b_peers = []
+        for i in range(2):  # b_peers[i]: the peers' copies of xs2[i]
+            addrs = [ctx.open_shared_buffer(q, handles[r][64 * i:64 * (i + 1)], self.v * 4)
+                     for r in range(d.world) if r != d.rank] if d.world > 1 else []
+            arr = np.array(addrs or [0], np.uint64)
+            bp = mk(arr.nbytes)
+            ctx.enqueue_write_buffer(q, bp, arr)
+            self.b_peers.append(bp)
+        # kernel i reads xs[i], dsum[i]; writes x rows, xs[1-i] (here + peers), dsum[1-i]
+        self.k_stepx = [self.bl.kernel(self.v, self.b_xs2[i], self.b_dsum2[i], self.b_x[0], self.b_peers[1 - i],
+                                       d.world - 1, self.b_inv, self.b_xs2[1 - i], self.b_dsum2[1 - i])
+                        for i in range(2)]
+        prog = ctx.create_program("b200")
+        self.k_prep0 = ctx.create_kernel(prog, "pagerank_prep")  # x0 -> xs[0], dsum[0]
+        for j, a in enumerate([self.b_x[0], self.b_deg, self.b_dsum2[0], self.b_xs2[0], self.v]):
+            ctx.set_kernel_arg(self.k_prep0, j, a)
+        self.traffic_key = f"pagerank_step_binned_scale{self.scale}"
+        self.x0 = torch.full((self.v,), 1.0 / self.v, dtype=torch.float32).pin_memory()
+        self.r_host = torch.empty(self.rows, dtype=torch.float32, pin_memory=True)
+        # parity guard (bit-exact 20-iteration checks are in tests/test_pagerank_bins.py):
+        # after one step the rows of all ranks carry the whole mass
+        self.reset()
+        self.step()
+        ctx.finish(q)
+        d.barrier()
+        x = ctx.enqueue_read_buffer(q, self.b_x[0], offset=lo * 4, length=self.rows * 4).view(np.float32)
+        self.check = float(abs(d.allsum(float(x.astype(np.float64).sum())) - 1.0))
+        assert self.check <= 1e-3, f"pagerank binned parity guard: mass {self.check}"
+        self.reset()
+
     def reset(self):
         ctx, q = self.ctx, self.q
         if self.fused:
@@ -672,8 +741,8 @@ class PageRankW(Workload):
         return self.step_kernel if self.fused else self.spmv
 
     def dominant_work(self):
-        # SURVEY.md §8(d) algorithmic bytes of the CSR formulation (nnz*8 + (V+1)*4 + 2*V*4), also
-        # with implicit values (which move nnz*4 fewer bytes for the same work)
+        # SURVEY.md §8(d) algorithmic bytes of the CSR formulation (nnz*8 + (V+1)*4 + 2*V*4), for
+        # every kernel variant (the binned step moves ~12 bytes per edge for the same work)
         return self.nnz_local * 8.0 + (self.rows + 1) * 4 + self.rows * 4 * 2
 
     def e2e_step(self):
@@ -698,6 +767,20 @@ class PageRankW(Workload):
         return "hbm", pk["hbm_gbs"], "GB/s", 1e9, "MEASURED_PEAKS.json hbm_gbs"
 
     def config(self):
+        if self.binned:
+            L = self.bl.layouts[0]
+            return {"workload": f"PageRank iteration (C3): R-MAT scale {self.scale}, {self.e} edges, rows split over "
+                                f"{self.dist.world} rank(s) (cost-balanced), binned step: propagation blocking "
+                                "(scatter edge values into destination bins, shared-memory fixed-point gather), "
+                                "next gather input stored to every rank over NVLink, dangling-sum allreduce",
+                    "kernel": "pagerank_step_binned (pr_bin_scatter + pr_bin_gather)",
+                    "row_sums": "order-free: values rounded to 2^-56, exact uint64 sums (oracle ho_spmv_f32_fixed)",
+                    "layout": {k: L[k] for k in ("bin_rows", "chunk_edges", "span_max", "n_chunks", "n_bins",
+                                                 "n_units", "n_slots")},
+                    "layout_build_s": round(self.layout_s, 2),
+                    "algorithmic_bytes_per_iteration": self.work_per_step(), "rank_sum_err": self.check,
+                    "row_cost_nnz_per_row": self.row_cost,
+                    "l2": "2.35 GB algorithmic (~3.6 GB moved) per iteration > L2"}
         return {"workload": f"PageRank iteration (C3): R-MAT scale {self.scale}, {self.e} edges, int32/fp32 pull CSR, "
                             f"nnz-balanced rows over {self.dist.world} rank(s), " + (
                                 "fused step: x' rows + next gather input xs' stored to every rank over NVLink, "
@@ -793,8 +876,8 @@ class KMeansW(Workload):
         return self._assign
 
     def dominant_work(self):
-        if self.tc:  # tensor work actually issued per (point, centroid): 3 split products x D + the K=16 |c|^2 MMA
-            return 2.0 * self.rows * self.K * (3 * self.D + 16)
+        if self.tc:  # the assignment as one bf16 GEMM, 2 N K D flop (10.4 ms at C4 at the
+            return 2.0 * self.rows * self.K * self.D  # bf16 peak) -- not the split-operand MMAs actually issued
         return 3.0 * self.rows * self.K * self.D
 
     def e2e_step(self):
@@ -812,7 +895,8 @@ class KMeansW(Workload):
     def roofline(self, pk):
         if self.tc:
             return ("tensor", pk["bf16_tflops"], "TFLOP/s", 1e12,
-                    "MEASURED_PEAKS.json bf16_tflops; achieved = bf16 MMA flops issued (2 N K (3D + 16))")
+                    "MEASURED_PEAKS.json bf16_tflops; achieved = 2 N K D / assign time: the assignment's "
+                    "algorithmic bf16-GEMM bound (SURVEY.md §8(d) C4), frac = that GEMM's time / assign time")
         sm = pk.get("sm_max_mhz", 1965.0)
         # exact (non-FMA) fp32: one add or multiply per lane per clock (FADD2 issues
         # two lanes' worth but occupies the FP32 pipe twice, measured)
@@ -989,21 +1073,18 @@ def run_reference(args):
     return 0
 
 
-def run_b200(args):
+def measure(wl, args, dist, sampler=None, cpu_seconds=10.0):
+    """W warm-up steps, then K timed steps (CUDA events on the runtime's
+    stream, max over ranks), the dominant kernel alone, and the e2e loop through
+    the public API with host buffers. Returns the JSON line (rank 0) or None."""
     from paper_2005_08466_b200 import _native as N
 
-    dist = Dist("nccl")
     torch = dist.torch
-    torch.cuda.set_device(dist.local)
-    if dist.world != args.gpus and dist.rank == 0:
-        print(f"warning: WORLD_SIZE {dist.world} != --gpus {args.gpus}", file=sys.stderr)
-    wl = WORKLOADS[args.workload](args, dist)
     wl.setup()
     for _ in range(args.warmup):
         wl.step()
     wl.ctx.finish(wl.q)
     stream = wl.stream()
-    sampler = ClockSampler(list(range(dist.world))) if dist.rank == 0 else None
 
     # value: K steps, inputs resident, device time (CUDA events on the runtime's stream)
     dist.barrier()
@@ -1035,7 +1116,7 @@ def run_b200(args):
     # clock hold: a timed region shorter than ~3 nvidia-smi samples is followed by
     # the same steps, untimed, until the sampler has seen them under load
     hold_ms, t_hold = 0.0, time.time()
-    need_hold = dist.allmax(1.0 if sampler and sampler.count() < 3 else 0.0) > 0
+    need_hold = sampler is not None and dist.allmax(1.0 if sampler and sampler.count() < 3 else 0.0) > 0
     while need_hold:
         for _ in range(max(1, args.steps)):
             wl.step()
@@ -1077,7 +1158,7 @@ def run_b200(args):
     clocks = sampler.stop() if sampler else None
     if clocks is not None:
         clocks["hold_ms"] = round(hold_ms, 1)  # untimed repeat of the steps while sampling (short regions)
-
+    line = None
     if dist.rank == 0:
         pk = peaks()
         bound, peak, runit, rscale, psrc = wl.roofline(pk)
@@ -1096,17 +1177,59 @@ def run_b200(args):
             "e2e": {"value": round(wl.work_per_step() * args.steps / (e2e_ms / 1e3) / scale, 1), "unit": wl.unit,
                     "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
             "gpu_launches": launches_total,
-            "clocks": clocks,
         }
-        if args.workload == "gemm_bf16":
+        if clocks is not None:
+            line["clocks"] = clocks
+        if wl.name == "gemm_bf16":
             line["roofline"]["frac_of_sustained_peak"] = round(achieved / pk["bf16_tflops_sustained"], 4)
         if dist.world == 1 and not args.no_cpu_baseline:
             try:
-                v, _, desc, threads, kind, _ = cpu_leg(WORKLOADS[args.workload])
+                v, _, desc, threads, kind, _ = cpu_leg(type(wl), seconds=cpu_seconds)
                 line["cpu_baseline"] = {"value": round(v, 3), "unit": wl.unit, "cores": threads, "kind": kind,
                                         "sample": desc}
             except Exception as e:  # reported baseline only, never the measured path
                 line["cpu_baseline"] = {"value": None, "error": str(e)[:200]}
+    return line
+
+
+# the other BASELINE configs, measured in the same default run
+SECONDARY = (("C1", "gemm_f32"), ("C3", "pagerank"), ("C4", "kmeans"), ("C5", "conv"))
+
+
+def run_b200(args):
+    dist = Dist("nccl")
+    torch = dist.torch
+    torch.cuda.set_device(dist.local)
+    if dist.world != args.gpus and dist.rank == 0:
+        print(f"warning: WORLD_SIZE {dist.world} != --gpus {args.gpus}", file=sys.stderr)
+    sampler = ClockSampler(list(range(dist.world))) if dist.rank == 0 else None
+    wl = WORKLOADS[args.workload](args, dist)
+    line = measure(wl, args, dist, sampler)
+    wl.ctx.close()
+    del wl
+    if args.workload == "gemm_bf16" and not args.no_secondary:
+        # every other config of BASELINE.json through the same contract, so the
+        # driver's run records them too: a shorter timed loop each, CPU leg 3 s
+        sub = argparse.Namespace(**vars(args))
+        sub.steps, sub.warmup = max(3, min(args.steps, 10)), max(3, min(args.warmup, 3))
+        secondary = {}
+        for tag, name in SECONDARY:
+            t0 = time.perf_counter()
+            try:
+                w = WORKLOADS[name](sub, dist)
+                r = measure(w, sub, dist, None, cpu_seconds=3.0)
+                w.ctx.close()
+                del w
+                torch.cuda.empty_cache()
+            except Exception as e:  # one failing config must not hide the others
+                r = {"error": f"{type(e).__name__}: {str(e)[:300]}"} if dist.rank == 0 else None
+            if dist.rank == 0:
+                r = {k: v for k, v in r.items() if k not in ("metric", "higher_is_better", "vs_baseline")}
+                r["wall_s"] = round(time.perf_counter() - t0, 1)
+                secondary[tag] = r
+        if dist.rank == 0:
+            line["workloads"] = secondary
+    if dist.rank == 0:
         print(json.dumps(line), flush=True)
     dist.close()
     return 0
@@ -1120,6 +1243,8 @@ def main():
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="gemm_bf16")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true",
+                    help="headline config only (default: also C1, C3, C4, C5 under 'workloads')")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":

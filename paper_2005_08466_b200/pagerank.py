@@ -107,65 +107,19 @@ class PageRank:
         self.cur = 0
 
     def _setup_binned(self, row_ptr, col_idx, outdeg, opts) -> None:
-        """Per part with rows: the propagation-blocking layout of its rows
-        (hcl_pagerank_bins_build), concatenated into one buffer per array with
-        a parts table the kernel selects its part from by its row range."""
         ctx, q0, mk = self.ctx, self.queues[0], self.ctx.create_buffer
-        P = len(self.queues)
-        parts, arrays = [], {k: [] for k in ("chunks", "src_local", "cdesc", "dst16", "units", "slot_units")}
-        base = dict(chunk=0, src=0, desc=0, ent=0, unit=0, slot=0)
-        self.layouts = []
-        for i in range(P):
-            lo, hi = self.bounds[i], self.bounds[i + 1]
-            if hi <= lo:
-                continue
-            L = pagerank_bins(row_ptr, col_idx, lo, hi, **opts)
-            self.layouts.append(L)
-            parts.append([lo, hi, base["chunk"], L["n_chunks"], L["n_bins"], L["gstride"], base["desc"], base["src"],
-                          base["ent"], base["unit"], L["n_units"], base["slot"], L["n_slots"], L["bin_rows"],
-                          L["span_max"], L["n_edges"], L["chunk_edges"], 0, 0, 0])
-            arrays["chunks"].append(L["chunks"][:8 * L["n_chunks"]])
-            arrays["src_local"].append(L["src_local"][:L["n_src"]])
-            arrays["cdesc"].append(L["cdesc"][:L["n_desc"]])
-            arrays["dst16"].append(L["dst16"][:L["n_entries"]])
-            arrays["units"].append(L["units"][:4 * L["n_units"]])
-            arrays["slot_units"].append(L["slot_units"][:L["n_slots"]])
-            base["chunk"] += L["n_chunks"]
-            base["src"] += L["n_src"]
-            base["desc"] += L["n_desc"]
-            base["ent"] += L["n_entries"]
-            base["unit"] += L["n_units"]
-            base["slot"] += L["n_slots"]
-        self.bin_rows = self.layouts[0]["bin_rows"]
-        table = np.array(parts, np.int64).reshape(-1)
-        cat = {k: np.concatenate(v) if sum(len(x) for x in v) else np.zeros(8, v[0].dtype if v else np.int32)
-               for k, v in arrays.items()}
-        cat["dst16"] = np.concatenate([cat["dst16"], np.zeros(8, np.uint16)])  # >= 8 entries
-        self.b_parts = mk(table.nbytes)
-        ctx.enqueue_write_buffer(q0, self.b_parts, table)
-        self.b_bins = {}
-        for k, a in cat.items():
-            self.b_bins[k] = mk(a.nbytes)
-            ctx.enqueue_write_buffer(q0, self.b_bins[k], np.ascontiguousarray(a))
-        n_slots = max(1, base["slot"])
-        self.b_vals = mk(4 * len(cat["dst16"]))  # LOCAL: zero-filled per device (padding entries stay 0)
-        self.b_slot_acc = mk(n_slots * (self.bin_rows * 8 + 4))
+        self.bl = BinnedLayout(ctx, q0, row_ptr, col_idx, self.bounds, opts)
+        n_parts = self.bl.n_parts
         self.b_xs2, self.b_dsum2 = [mk(self.v * 4), mk(self.v * 4)], [mk(8), mk(8)]
         self.b_inv = mk(self.v * 4)
         ctx.enqueue_write_buffer(q0, self.b_inv, pagerank_inv_outdeg(outdeg))
-        self.b_peers = mk(8 * max(1, len(parts) - 1))
+        self.b_peers = mk(8 * max(1, n_parts - 1))
         prog = ctx.create_program("b200")
         self.k_prep0 = ctx.create_kernel(prog, "pagerank_prep")
         for j, a in enumerate([self.b_x[0], self.b_deg, self.b_dsum2[0], self.b_xs2[0], self.v]):
             ctx.set_kernel_arg(self.k_prep0, j, a)
-        self.k_bin = [ctx.create_kernel(prog, "pagerank_step_binned") for _ in range(2)]
-        B = self.b_bins
-        for i, kk in enumerate(self.k_bin):  # reads xs[i], dsum[i]; writes x rows, xs[1-i], dsum[1-i]
-            for j, a in enumerate([self.b_parts, B["chunks"], B["src_local"], B["cdesc"], B["dst16"], B["units"],
-                                   B["slot_units"], self.b_xs2[i], self.b_dsum2[i], self.b_x[0], self.v, len(parts),
-                                   self.b_peers, len(parts) - 1, self.b_inv, self.b_xs2[1 - i], self.b_dsum2[1 - i],
-                                   self.b_vals, self.b_slot_acc]):
-                ctx.set_kernel_arg(kk, j, a)
+        self.k_bin = [self.bl.kernel(self.v, self.b_xs2[i], self.b_dsum2[i], self.b_x[0], self.b_peers, n_parts - 1,
+                                     self.b_inv, self.b_xs2[1 - i], self.b_dsum2[1 - i]) for i in range(2)]
 
     def reset(self) -> None:
         x0 = np.full(self.v, np.float32(1.0 / self.v), np.float32)
@@ -238,5 +192,73 @@ class PageRank:
             for b in (*self.b_xs2, *self.b_dsum2, self.b_peers, self.b_inv):
                 self.ctx.release(b)
         if self.binned:
-            for b in (self.b_parts, *self.b_bins.values(), self.b_vals, self.b_slot_acc):
-                self.ctx.release(b)
+            self.bl.close()
+
+
+class BinnedLayout:
+    """Device copy of the propagation-blocking layout (hcl_pagerank_bins_build)
+    of every part [bounds[i], bounds[i+1]) with rows, concatenated into one
+    buffer per array with a parts table; pagerank_step_binned finds its part by
+    the row range of the launch. One part per process under torchrun (bench.py),
+    several logical devices in one process (tests)."""
+
+    ARRAYS = ("chunks", "src_local", "cdesc", "dst16", "units", "slot_units")
+
+    def __init__(self, ctx: HostContext, q0: Handle, row_ptr, col_idx, bounds: Sequence[int], opts=None):
+        self.ctx = ctx
+        mk = ctx.create_buffer
+        parts, arrays = [], {k: [] for k in self.ARRAYS}
+        base = dict(chunk=0, src=0, desc=0, ent=0, unit=0, slot=0)
+        self.layouts = []
+        for i in range(len(bounds) - 1):
+            lo, hi = int(bounds[i]), int(bounds[i + 1])
+            if hi <= lo:
+                continue
+            L = pagerank_bins(row_ptr, col_idx, lo, hi, **(opts or {}))
+            self.layouts.append({k: v for k, v in L.items() if not isinstance(v, np.ndarray)})
+            parts.append([lo, hi, base["chunk"], L["n_chunks"], L["n_bins"], L["gstride"], base["desc"], base["src"],
+                          base["ent"], base["unit"], L["n_units"], base["slot"], L["n_slots"], L["bin_rows"],
+                          L["span_max"], L["n_edges"], L["chunk_edges"], 0, 0, 0])
+            arrays["chunks"].append(L["chunks"][:8 * L["n_chunks"]])
+            arrays["src_local"].append(L["src_local"][:L["n_src"]])
+            arrays["cdesc"].append(L["cdesc"][:L["n_desc"]])
+            arrays["dst16"].append(L["dst16"][:L["n_entries"]])
+            arrays["units"].append(L["units"][:4 * L["n_units"]])
+            arrays["slot_units"].append(L["slot_units"][:L["n_slots"]])
+            base["chunk"] += L["n_chunks"]
+            base["src"] += L["n_src"]
+            base["desc"] += L["n_desc"]
+            base["ent"] += L["n_entries"]
+            base["unit"] += L["n_units"]
+            base["slot"] += L["n_slots"]
+        self.n_parts = len(parts)
+        self.n_edges = sum(L["n_edges"] for L in self.layouts)
+        self.bin_rows = self.layouts[0]["bin_rows"]
+        table = np.array(parts, np.int64).reshape(-1)
+        cat = {k: np.concatenate(v) if sum(len(x) for x in v) else np.zeros(8, v[0].dtype)
+               for k, v in arrays.items()}
+        cat["dst16"] = np.concatenate([cat["dst16"], np.zeros(8, np.uint16)])  # >= 8 entries
+        self.b_parts = mk(table.nbytes)
+        ctx.enqueue_write_buffer(q0, self.b_parts, table)
+        self.b = {}
+        for k, a in cat.items():
+            self.b[k] = mk(a.nbytes)
+            ctx.enqueue_write_buffer(q0, self.b[k], np.ascontiguousarray(a))
+        self.b_vals = mk(4 * len(cat["dst16"]))  # LOCAL: zero-filled per device (padding entries stay 0)
+        self.b_slot_acc = mk(max(1, base["slot"]) * (self.bin_rows * 8 + 4))
+
+    def kernel(self, v, xs, dsum, x_out, peers, n_peers, inv, xs_next, dsum_next) -> Handle:
+        """A pagerank_step_binned kernel bound to this layout: reads xs, dsum;
+        writes the part's rows of x_out, xs_next (here and through peers) and
+        the dangling partial dsum_next."""
+        ctx, B = self.ctx, self.b
+        k = ctx.create_kernel(ctx.create_program("b200"), "pagerank_step_binned")
+        for j, a in enumerate([self.b_parts, B["chunks"], B["src_local"], B["cdesc"], B["dst16"], B["units"],
+                               B["slot_units"], xs, dsum, x_out, v, self.n_parts, peers, n_peers, inv, xs_next,
+                               dsum_next, self.b_vals, self.b_slot_acc]):
+            ctx.set_kernel_arg(k, j, a)
+        return k
+
+    def close(self) -> None:
+        for b in (self.b_parts, *self.b.values(), self.b_vals, self.b_slot_acc):
+            self.ctx.release(b)
