@@ -3,8 +3,10 @@
 The NDRange is the batch: `conv3x3` runs as a partitioned launch over images
 (SPLIT_ROWS input and output, REPLICATE weights), with weights from the
 scheduler's measured rates or explicit ones (the heterogeneity-aware uneven
-split sweep). Input is stored zero-padded NHWC (`conv_pad_nhwc` converts a
-plain NHWC batch on the device).
+split sweep). With C == 64 the layer runs straight from plain NHWC
+(`conv3x3_nhwc`: each tile's input halo is one TMA box whose out-of-image
+part TMA zero-fills -- the padding is never materialised); other channel
+counts (or padded=True) pad on the device first (`conv_pad_nhwc` + `conv3x3`).
 """
 from __future__ import annotations
 
@@ -17,28 +19,32 @@ from .runtime import Handle, HostContext
 
 class Conv3x3:
     def __init__(self, ctx: HostContext, queues: Sequence[Handle], n: int, h: int, w: int, c: int, k: int,
-                 out_f32: bool = False):
+                 out_f32: bool = False, padded: Optional[bool] = None):
         self.ctx, self.queues = ctx, list(queues)
         self.n, self.h, self.w, self.c, self.k, self.out_f32 = n, h, w, c, k, out_f32
+        self.padded = (c != 64) if padded is None else padded
         self.es_out = 4 if out_f32 else 2
         mk = ctx.create_buffer
         self.b_in = mk(n * h * w * c * 2)
-        self.b_pad = mk(n * (h + 2) * (w + 2) * c * 2)
+        self.b_pad = mk(n * (h + 2) * (w + 2) * c * 2) if self.padded else None
         self.b_w = mk(k * 9 * c * 2)
         self.b_out = mk(n * h * w * k * self.es_out)
         prog = ctx.create_program("b200")
-        self.k_pad = ctx.create_kernel(prog, "conv_pad_nhwc")
-        self.k_conv = ctx.create_kernel(prog, "conv3x3")
-        for j, a in enumerate([self.b_in, self.b_pad, n, h, w, c]):
-            ctx.set_kernel_arg(self.k_pad, j, a)
-        for j, a in enumerate([self.b_pad, self.b_w, self.b_out, n, h, w, c, k, int(out_f32)]):
+        self.k_conv = ctx.create_kernel(prog, "conv3x3" if self.padded else "conv3x3_nhwc")
+        if self.padded:
+            self.k_pad = ctx.create_kernel(prog, "conv_pad_nhwc")
+            for j, a in enumerate([self.b_in, self.b_pad, n, h, w, c]):
+                ctx.set_kernel_arg(self.k_pad, j, a)
+        for j, a in enumerate([self.b_pad if self.padded else self.b_in, self.b_w, self.b_out, n, h, w, c, k,
+                               int(out_f32)]):
             ctx.set_kernel_arg(self.k_conv, j, a)
 
     def plan(self, weights: Optional[Sequence[int]] = None):
         return self.ctx.partition_plan(self.k_conv, (self.n, 1, 1), self.queues, weights)
 
     def load(self, x_nhwc_bf16: np.ndarray, w_krsc_bf16: np.ndarray, weights: Optional[Sequence[int]] = None):
-        """Scatter each queue's images (plain NHWC bf16 bits) to its device, pad there."""
+        """Scatter each queue's images (plain NHWC bf16 bits) to its device (padded
+        there when the layer runs the padded kernel)."""
         flat = np.ascontiguousarray(x_nhwc_bf16).reshape(-1)
         img = self.h * self.w * self.c
         bounds = self.plan(weights)
@@ -47,7 +53,8 @@ class Conv3x3:
             if hi > lo:
                 self.ctx.enqueue_write_buffer(q, self.b_in, flat[lo * img:hi * img], offset=lo * img * 2)
         self.ctx.enqueue_write_buffer(self.queues[0], self.b_w, np.ascontiguousarray(w_krsc_bf16))
-        self.ctx.enqueue_ndrange_partitioned(self.k_pad, (self.n, 1, 1), 1, self.queues, bounds=bounds)
+        if self.padded:
+            self.ctx.enqueue_ndrange_partitioned(self.k_pad, (self.n, 1, 1), 1, self.queues, bounds=bounds)
         self.bounds = bounds
 
     def run(self, weights: Optional[Sequence[int]] = None) -> None:
@@ -67,4 +74,5 @@ class Conv3x3:
 
     def close(self) -> None:
         for b in (self.b_in, self.b_pad, self.b_w, self.b_out):
-            self.ctx.release(b)
+            if b is not None:
+                self.ctx.release(b)

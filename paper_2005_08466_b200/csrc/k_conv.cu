@@ -439,6 +439,236 @@ __global__ void __launch_bounds__((CV2_EPI + 2) * 32, 1)
   }
 }
 
+// ---------------------------------------------------------------------------
+// v3: straight from unpadded NHWC (conv3x3_nhwc, C == 64). A CTA's tile is a
+// 16 (h) x 8 (w) block of output pixels (a CTA pair: 16 x 16); TMEM lane
+// m = 8 g + j is pixel (h0 + g, w0 + j). The producer loads the tile's input
+// halo as ONE 4D TMA box {64 ch, 16 w, 18 h, 1 image} at signed coordinates
+// (w0 - 1, h0 - 1): TMA zero-fills everything outside the image, which IS the
+// padding -- no padded copy of the input exists. In shared memory halo pixel
+// (a, b) is row 16 a + b (128 B, SWIZZLE_128B), so for tap (r, s) the MMA's A
+// operand starts at row 16 r + s: 8-row groups (one h each) 16 rows = 2048 B
+// apart (the descriptor's stride), 1024-byte aligned plus the row shift s
+// (address-based swizzle, as in v2). One 36 KB load feeds all 9 taps; the
+// halo re-read is 288 / 128 = 2.25 rows per pixel (v2: 3 x 136 / 128 = 3.2).
+constexpr int CV3_TW = 8, CV3_TH = 16;               // CTA tile: 8 w x 16 h = 128 pixels
+constexpr int CV3_BW = 16, CV3_BH = CV3_TH + 2;      // halo box: 16 w (>= 8 + 2, 8-row groups) x 18 h
+constexpr int CV3_A = CV3_BW * CV3_BH * 128;         // 36 KB
+template <bool OUTF32>
+struct CV3Cfg {
+  static constexpr int kStages = OUTF32 ? 4 : 3;
+  static constexpr size_t kObytes = OUTF32 ? 0 : static_cast<size_t>(CV2_EPI) * CV2_OSTAGE;
+  static constexpr size_t kSmem = static_cast<size_t>(CV2_B) + static_cast<size_t>(kStages) * CV3_A + kObytes + 1024 + 256;
+};
+
+struct Conv3Geom {
+  int th, tw, tiles_img, tiles;
+  __device__ Conv3Geom(int n_img, int H, int W) {
+    th = (H + CV3_TH - 1) / CV3_TH;
+    tw = (W + 2 * CV3_TW - 1) / (2 * CV3_TW);
+    tiles_img = th * tw;
+    tiles = n_img * tiles_img;
+  }
+  // pair tile t -> image, this CTA's h0, w0
+  __device__ void at(int t, uint32_t rank, int& n, int& h0, int& w0) const {
+    n = t / tiles_img;
+    const int q = t - n * tiles_img;
+    h0 = (q / tw) * CV3_TH;
+    w0 = (q % tw) * 2 * CV3_TW + static_cast<int>(rank) * CV3_TW;
+  }
+};
+
+// epilogue, fp32 output: each lane stores its pixel's channel chunks directly
+__device__ __forceinline__ void conv3_epilogue_loop_f32(const Conv3Geom& g, int H, int W, uint32_t rank, int warp,
+                                                        int lane, uint32_t tmem_base, uint64_t* tfull,
+                                                        uint64_t* tempty, void* __restrict__ out, int epi_mode) {
+  const int cluster = blockIdx.x / 2, nclusters = gridDim.x / 2;
+  const int c0 = (warp / 4) * 2, c1 = c0 + 2;
+  const int m = (warp % 4) * 32 + lane;
+  int acc = 0;
+  uint32_t acc_phase = 0;
+  for (int t = cluster; t < g.tiles; t += nclusters) {
+    int n, h0, w0;
+    g.at(t, rank, n, h0, w0);
+    const int h = h0 + m / CV3_TW, w = w0 + m % CV3_TW;
+    const bool ok = h < H && w < W && epi_mode == 0;
+    const int64_t opix = (static_cast<int64_t>(n) * H + h) * W + w;
+    ptx::mbar_wait(&tfull[acc], acc_phase);
+    ptx::tc_fence_after();
+    if (epi_mode != 1) conv_epilogue<true>(tmem_base, acc, warp, c0, c1, ok, opix, out);
+    ptx::tc_fence_before();
+    __syncwarp();
+    if (lane == 0) ptx::mbar_arrive_cluster_relaxed(ptx::mapa(ptx::smem_u32(&tempty[acc]), 0));
+    if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+  }
+}
+
+// epilogue, bf16 output: a warp's 32 pixels are 4 h x 8 w of the tile; their
+// 64-channel half goes through a swizzled 4 KB buffer and one 4D TMA store
+// {64 ch, 8 w, 4 h, 1} (pixels outside the image are clipped by TMA)
+__device__ __forceinline__ void conv3_epilogue_loop_tma(const Conv3Geom& g, uint32_t rank, int warp, int lane,
+                                                        uint32_t tmem_base, uint64_t* tfull, uint64_t* tempty,
+                                                        const CUtensorMap* tmO, uint8_t* obuf, int epi_mode) {
+  const int cluster = blockIdx.x / 2, nclusters = gridDim.x / 2;
+  const int half = warp / 4, quad = warp % 4;
+  int acc = 0;
+  uint32_t acc_phase = 0;
+  for (int t = cluster; t < g.tiles; t += nclusters) {
+    int n, h0, w0;
+    g.at(t, rank, n, h0, w0);
+    ptx::mbar_wait(&tfull[acc], acc_phase);
+    ptx::tc_fence_after();
+    uint32_t r0[32], r1[32];
+    if (epi_mode != 1) {
+      const uint32_t ta = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + static_cast<uint32_t>(acc * CV_BN + half * 64);
+      ptx::tmem_ld_32x32b_x32(ta, r0);
+      ptx::tmem_ld_32x32b_x32(ta + 32, r1);
+      ptx::tmem_ld_wait();
+    }
+    ptx::tc_fence_before();
+    __syncwarp();
+    if (lane == 0) ptx::mbar_arrive_cluster_relaxed(ptx::mapa(ptx::smem_u32(&tempty[acc]), 0));
+    if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    if (epi_mode != 0) continue;
+    if (lane == 0) ptx::bulk_wait_read0();  // the previous store has read this buffer
+    __syncwarp();
+    uint32_t pk[32];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      __nv_bfloat162 a = __floats2bfloat162_rn(__uint_as_float(r0[2 * j]), __uint_as_float(r0[2 * j + 1]));
+      __nv_bfloat162 b = __floats2bfloat162_rn(__uint_as_float(r1[2 * j]), __uint_as_float(r1[2 * j + 1]));
+      pk[j] = *reinterpret_cast<uint32_t*>(&a);
+      pk[16 + j] = *reinterpret_cast<uint32_t*>(&b);
+    }
+    uint8_t* row = obuf + lane * 128;
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      *reinterpret_cast<uint4*>(row + ((j ^ (lane & 7)) << 4)) =
+          make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+    ptx::fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+      ptx::tma_store_4d(tmO, obuf, half * 64, w0, h0 + quad * 4, n);
+      ptx::bulk_commit();
+    }
+  }
+  if (lane == 0) ptx::bulk_wait0();
+}
+
+template <bool OUTF32>
+__global__ void __launch_bounds__((CV2_EPI + 2) * 32, 1)
+    conv3x3_v3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                      const __grid_constant__ CUtensorMap tmO, void* __restrict__ out, int n_img, int H, int W,
+                      int epi_mode) {
+  constexpr int STAGES = CV3Cfg<OUTF32>::kStages;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem_b = smem;
+  uint8_t* smem_a = smem + CV2_B;                  // 72 KB: 1024-aligned
+  uint8_t* smem_o = smem_a + STAGES * CV3_A;       // 36 KB stages: 1024-aligned
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_o + CV3Cfg<OUTF32>::kObytes);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint64_t* bfull = tempty + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bfull + 1);
+  constexpr int PROD = CV2_EPI, MMA = CV2_EPI + 1;
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const uint32_t rank = ptx::cluster_ctarank();
+  const Conv3Geom g(n_img, H, W);
+
+  if (warp == PROD && lane == 0) {
+    ptx::prefetch_tmap(&tmA);
+    ptx::prefetch_tmap(&tmB);
+    if constexpr (!OUTF32) ptx::prefetch_tmap(&tmO);
+    for (int s = 0; s < STAGES; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      ptx::mbar_init(&tfull[a], 1);
+      ptx::mbar_init(&tempty[a], 2 * CV2_EPI);
+    }
+    ptx::mbar_init(bfull, 1);
+    ptx::fence_mbar_init();
+  }
+  if (warp == MMA) ptx::tmem_alloc<2>(tmem_slot, CV_TMEM);
+  ptx::tc_fence_before();
+  ptx::cluster_sync();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int cluster = blockIdx.x / 2, nclusters = gridDim.x / 2;
+
+  if (warp == PROD) {
+    if (lane == 0) {
+      // resident weights: 9 taps x this CTA's 64 output channels
+      if (rank == 0) ptx::mbar_arrive_expect_tx(bfull, CV2_B * 2);
+      const uint32_t bb = ptx::mapa(ptx::smem_u32(bfull), 0);
+      for (int tap = 0; tap < 9; ++tap)
+        ptx::tma_load_2d_pair(smem_b + tap * CV2_BTAP, &tmB, bb, tap * 64, static_cast<int>(rank) * CV_BNL);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = cluster; t < g.tiles; t += nclusters) {
+        int n, h0, w0;
+        g.at(t, rank, n, h0, w0);
+        ptx::mbar_wait(&empty[stage], phase ^ 1);
+        if (rank == 0) ptx::mbar_arrive_expect_tx(&full[stage], CV3_A * 2);
+        const uint32_t bar = ptx::mapa(ptx::smem_u32(&full[stage]), 0);
+        ptx::tma_load_4d_pair(smem_a + stage * CV3_A, &tmA, bar, 0, w0 - 1, h0 - 1, n);
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      }
+    }
+    __syncwarp();
+  } else if (warp == MMA) {
+    if (rank == 0) {
+      constexpr uint32_t idesc = ptx::umma_idesc(1, 0, 0, 2 * CV_BM, CV_BN);
+      ptx::mbar_wait(bfull, 0);
+      const uint64_t bdesc0 = ptx::umma_desc_sw128(ptx::smem_u32(smem_b), 16, 1024);
+      const uint64_t adesc0 = ptx::umma_desc_sw128(ptx::smem_u32(smem_a), 16, CV3_BW * 128);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int t = cluster; t < g.tiles; t += nclusters) {
+        ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
+        ptx::tc_fence_after();
+        const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * CV_BN);
+        ptx::mbar_wait(&full[stage], phase);
+        ptx::tc_fence_after();
+        const uint64_t adesc = adesc0 + static_cast<uint64_t>((stage * CV3_A) >> 4);
+#pragma unroll
+        for (int tap = 0; tap < 9; ++tap) {
+          const int r = tap / 3, s = tap % 3;
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            ptx::mma_elect<2, false>(d_tmem, adesc + static_cast<uint64_t>(((r * CV3_BW + s) * 128 + k * 32) >> 4),
+                                     bdesc0 + static_cast<uint64_t>((tap * CV2_BTAP + k * 32) >> 4), idesc,
+                                     (tap | k) != 0);
+        }
+        ptx::mma_commit_elect<2>(&empty[stage]);
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        ptx::mma_commit_elect<2>(&tfull[acc]);
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+    }
+    __syncwarp();
+  } else {
+    if constexpr (OUTF32)
+      conv3_epilogue_loop_f32(g, H, W, rank, warp, lane, tmem_base, tfull, tempty, out, epi_mode);
+    else
+      conv3_epilogue_loop_tma(g, rank, warp, lane, tmem_base, tfull, tempty, &tmO, smem_o + warp * CV2_OSTAGE,
+                              epi_mode);
+  }
+
+  ptx::tc_fence_before();
+  ptx::cluster_sync();
+  if (warp == MMA) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc<2>(tmem_base, CV_TMEM);
+  }
+}
+
 // NHWC -> zero-padded NHWC (one 16-byte vector of 8 channels per thread)
 __global__ void pad_nhwc_kernel(const uint4* __restrict__ in, uint4* __restrict__ out, int64_t n, int H, int W,
                                 int c8) {
@@ -521,6 +751,69 @@ uint64_t launch_conv(LaunchCtx& c) {
   return 2ull * cnt * H * W * K * 9 * C;
 }
 
+// conv3x3_nhwc(input NHWC bf16 (unpadded), weights KRSC, output NHWK, N, H, W, C, K, out_f32):
+// the whole layer from plain NHWC (v3 kernel; C == 64, K == 128)
+uint64_t launch_conv_nhwc(LaunchCtx& c) {
+  const int64_t n = scalar_arg(c, 3, "conv3x3_nhwc N"), H = scalar_arg(c, 4, "conv3x3_nhwc H");
+  const int64_t W = scalar_arg(c, 5, "conv3x3_nhwc W");
+  const int64_t C = scalar_arg(c, 6, "conv3x3_nhwc C"), K = scalar_arg(c, 7, "conv3x3_nhwc K");
+  const bool out_f32 = scalar_arg(c, 8, "conv3x3_nhwc out_f32") != 0;
+  if (n < 1 || H < 1 || W < 1 || C != 64 || K != CV_BN)
+    fail(ErrorCode::argument, "conv3x3_nhwc: need N,H,W >= 1, C == 64, K == 128 (this kernel's tile)");
+  const int64_t img_in = H * W * C * 2, img_out = H * W * K * (out_f32 ? 4 : 2);
+  const BufView& I = buffer_arg(c, 0, "conv3x3_nhwc input");
+  const BufView& Wt = buffer_arg(c, 1, "conv3x3_nhwc weights");
+  const BufView& O = buffer_arg(c, 2, "conv3x3_nhwc output");
+  if (Wt.first_byte != 0 || Wt.bytes != static_cast<uint64_t>(K * 9 * C * 2))
+    fail(ErrorCode::argument, "conv3x3_nhwc: weights must be K x 3 x 3 x C bf16");
+  if (c.whole && (I.bytes != static_cast<uint64_t>(n * img_in) || O.bytes != static_cast<uint64_t>(n * img_out)))
+    fail(ErrorCode::argument, "conv3x3_nhwc: input must be N x H x W x C bf16, output N x H x W x K");
+  uint64_t lo, cnt;
+  sub_range(c, static_cast<uint64_t>(n), lo, cnt, "conv3x3_nhwc");
+  const uint8_t* in = at_byte<const uint8_t>(I, lo * img_in, cnt * img_in, "conv3x3_nhwc input");
+  uint8_t* outp = at_byte<uint8_t>(O, lo * img_out, cnt * img_out, "conv3x3_nhwc output");
+  if (!cnt) return 0;
+  const uint64_t id[4] = {static_cast<uint64_t>(C), static_cast<uint64_t>(W), static_cast<uint64_t>(H), cnt};
+  const uint64_t is[3] = {static_cast<uint64_t>(C) * 2, static_cast<uint64_t>(W) * C * 2,
+                          static_cast<uint64_t>(H) * W * C * 2};
+  const uint32_t ib[4] = {64, CV3_BW, CV3_BH, 1};
+  CUtensorMap ta = make_tmap_4d_bf16(in, id, is, ib);
+  CUtensorMap tb = make_tmap_2d_bf16(Wt.ptr, 9 * C, K, 9 * C * 2, 64, CV_BNL);
+  CUtensorMap to{};
+  if (!out_f32) {
+    const uint64_t od[4] = {static_cast<uint64_t>(K), static_cast<uint64_t>(W), static_cast<uint64_t>(H), cnt};
+    const uint64_t os[3] = {static_cast<uint64_t>(K) * 2, static_cast<uint64_t>(W) * K * 2,
+                            static_cast<uint64_t>(H) * W * K * 2};
+    const uint32_t ob[4] = {64, CV3_TW, 4, 1};
+    to = make_tmap_4d_bf16(outp, od, os, ob);
+  }
+  void* kern = out_f32 ? reinterpret_cast<void*>(conv3x3_v3_kernel<true>) : reinterpret_cast<void*>(conv3x3_v3_kernel<false>);
+  const size_t smem = out_f32 ? CV3Cfg<true>::kSmem : CV3Cfg<false>::kSmem;
+  HCL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  const int64_t tiles = static_cast<int64_t>(cnt) * ceil_div(H, CV3_TH) * ceil_div(W, 2 * CV3_TW);
+  const int64_t clusters = std::min<int64_t>(tiles, c.sm_count / 2);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(clusters * 2));
+  cfg.blockDim = dim3((CV2_EPI + 2) * 32);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = c.stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  void* outv = static_cast<void*>(outp);
+  int cn = static_cast<int>(cnt), hh = static_cast<int>(H), ww = static_cast<int>(W);
+  const char* epi_env = std::getenv("HCL_CONV_EPI");
+  int epi_mode = epi_env ? std::atoi(epi_env) : 0;
+  void* params[] = {&ta, &tb, &to, &outv, &cn, &hh, &ww, &epi_mode};
+  HCL_CUDA(cudaLaunchKernelExC(&cfg, kern, params));
+  HCL_LAUNCHED();
+  return 2ull * cnt * H * W * K * 9 * C;
+}
+
 // conv_pad_nhwc(input NHWC bf16, output padded, N, H, W, C)
 uint64_t launch_pad(LaunchCtx& c) {
   const int64_t n = scalar_arg(c, 2, "conv_pad_nhwc N"), H = scalar_arg(c, 3, "conv_pad_nhwc H");
@@ -550,6 +843,8 @@ void register_conv(std::vector<KernelDef>& r) {
   r.push_back({"b200", "conv3x3", {I, I, O, S, S, S, S, S, S}, {X, P, X, N, N, N, N, N, N}, launch_conv, nullptr,
                rows_conv});
   r.push_back({"b200", "conv_pad_nhwc", {I, O, S, S, S, S}, {X, X, N, N, N, N}, launch_pad, nullptr, rows_pad});
+  r.push_back({"b200", "conv3x3_nhwc", {I, I, O, S, S, S, S, S, S}, {X, P, X, N, N, N, N, N, N}, launch_conv_nhwc,
+               nullptr, rows_conv});
 }
 
 }  // namespace hcl

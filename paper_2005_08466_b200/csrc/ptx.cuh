@@ -114,6 +114,17 @@ __device__ __forceinline__ void tma_load_2d_pair(void* smem, const CUtensorMap* 
       : "memory");
 }
 
+// 4D tile load for a CTA pair (signed coordinates: out-of-bounds elements are
+// zero-filled, e.g. a convolution's padding halo).
+__device__ __forceinline__ void tma_load_4d_pair(void* smem, const CUtensorMap* m, uint32_t bar_cluster, int c0,
+                                                 int c1, int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, "
+      "%5, %6}], [%2];" ::"r"(smem_u32(smem)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(bar_cluster), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+
 // ---- TMA stores (smem -> global, bulk-group completion) --------------------
 
 // generic-proxy smem writes -> visible to the async proxy (before a TMA store)

@@ -34,12 +34,12 @@ def ref_conv(x, w):
     return out, scale
 
 
-def run(ctx, queues, n, h, wd, c, k, out_f32, P=1, weights=None):
+def run(ctx, queues, n, h, wd, c, k, out_f32, P=1, weights=None, padded=None):
     from paper_2005_08466_b200.conv import Conv3x3
 
     xb = O.gen_bf16(n * h * wd * c, 42).reshape(n, h, wd, c)
     wb = O.gen_bf16(k * 9 * c, 43).reshape(k, 3, 3, c)
-    cv = Conv3x3(ctx, queues[:P], n, h, wd, c, k, out_f32=out_f32)
+    cv = Conv3x3(ctx, queues[:P], n, h, wd, c, k, out_f32=out_f32, padded=padded)
     cv.load(xb, wb, weights)
     cv.run()
     got = cv.output().copy()
@@ -48,7 +48,8 @@ def run(ctx, queues, n, h, wd, c, k, out_f32, P=1, weights=None):
 
 
 @pytest.mark.parametrize("n,h,wd,c,out_f32", [(2, 16, 16, 64, True), (3, 7, 37, 128, True), (2, 12, 30, 64, False),
-                                             (3, 9, 50, 64, False), (2, 5, 224, 64, False)])
+                                             (3, 9, 50, 64, False), (2, 5, 224, 64, False), (1, 33, 17, 64, True),
+                                             (2, 17, 9, 64, False)])
 def test_conv_matches_fp64_reference(ctx, queues, n, h, wd, c, out_f32):
     k = 128
     xb, wb, got = run(ctx, queues, n, h, wd, c, k, out_f32)
@@ -63,6 +64,17 @@ def test_conv_matches_fp64_reference(ctx, queues, n, h, wd, c, out_f32):
         i, y, xx, ko = (int(rng.integers(0, v)) for v in (n, h, wd, k))
         o = O.conv3x3_point(xb.reshape(-1), wb.reshape(-1), h, wd, c, k, i, y, xx, ko)
         assert abs(got[i, y, xx, ko] - o) <= (2.0**-12 if out_f32 else 2.0**-8) * max(scale[i, y, xx, ko], 1e-30)
+
+
+@pytest.mark.parametrize("n,h,wd,out_f32", [(2, 16, 16, True), (2, 12, 30, False), (3, 33, 47, False),
+                                           (1, 224, 224, False)])
+def test_conv_nhwc_equals_padded_path(ctx, queues, n, h, wd, out_f32):
+    """conv3x3_nhwc (halo tiles straight from NHWC, TMA zero fill) and the
+    padded kernel (conv_pad_nhwc + conv3x3) issue the same per-output MMA chain
+    (taps r, s, then 16-channel steps): outputs bit-identical, ragged tiles too."""
+    _, _, a = run(ctx, queues, n, h, wd, 64, 128, out_f32, padded=False)
+    _, _, b = run(ctx, queues, n, h, wd, 64, 128, out_f32, padded=True)
+    assert a.tobytes() == b.tobytes()
 
 
 @pytest.mark.parametrize("P,weights", [(2, None), (4, None), (4, [1, 3, 2, 2])])
