@@ -118,6 +118,28 @@ __device__ __forceinline__ int entry_k0(uint32_t key, int g) {
   return (bi / (KT_GCOLS / 32)) * KT_CW + g * KT_GCOLS + (bi % (KT_GCOLS / 32)) * 32;
 }
 
+// scan -> verify hand-off through named barriers: a waiting warp is parked by
+// bar.sync and takes no issue slot (polled mbarriers cost the ALU-bound scan
+// warps up to a quarter of their issue slots). Per list buffer b: LF(b) "lists
+// of b complete" (scan warps arrive, the verify set of b syncs), LE(b) "b free
+// again" (the verify set arrives, the scan warps sync before reusing b).
+constexpr int KT_HANDOFF = (KT_SCAN + KT_VER / 2) * 32;
+__device__ __forceinline__ void named_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+__device__ __forceinline__ void named_arrive(int id, int count) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+__device__ __forceinline__ int bar_lf(int b) { return 2 + b; }
+__device__ __forceinline__ int bar_le(int b) { return 4 + b; }
+
+// three-input minimum (sm_100: one FMNMX3)
+__device__ __forceinline__ float min3f(float a, float b, float c) {
+  float r;
+  asm("min.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, %0;" ::"n"(KT_SCAN * 32) : "memory"); }
 
 // exact fp32 distance in the oracle's order (ho_kmeans_assign)
@@ -144,9 +166,12 @@ __global__ void __launch_bounds__(KT_THREADS, 1)
                             int32_t* __restrict__ assign, int rows, int K, int* __restrict__ n_overflow,
                             int dbg) {
   // dbg (HCL_KM_DBG, diagnostics only; wrong results): bit 0 skips the exact
-  // verification, bit 1 the candidate masks, bit 2 the whole verify stage
+  // verification, bit 2 the whole verify stage, bit 4 counts exact checks
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // aligned by pointer arithmetic on the shared array (not through an integer
+  // cast), so the compiler keeps the shared address space: LDS/STS for the
+  // candidate lists instead of generic loads and stores
+  uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
   const KtLayout L(K);
   uint8_t* sb = smem + L.b;
   uint8_t* sa = smem + L.a;
@@ -271,7 +296,7 @@ __global__ void __launch_bounds__(KT_THREADS, 1)
       const float two_eps = 0x1p-9f * (sqrtf(xx) * cmax + xx + qmax);
       float m = __int_as_float(0x7f800000);
       int cnt = 0, ovf = 0;
-      ptx::mbar_wait(&lempty[buf], ((it >> 1) & 1) ^ 1);  // the verify warps are done with this buffer
+      if (it >= 2) named_sync(bar_le(buf), KT_HANDOFF);  // the verify warps are done with this buffer
       float2* my = lists + buf * KT_LBUF + (g * KT_ROWS + pl) * KT_LIST;
       for (int c = 0; c < nch; ++c) {
         ptx::mbar_wait(&tfull[acc], (tph >> acc) & 1);
@@ -289,16 +314,16 @@ __global__ void __launch_bounds__(KT_THREADS, 1)
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive_cluster_relaxed(ptx::mapa(ptx::smem_u32(&tempty[acc]), 0));
           }
-          const int k0 = c * KT_CW + g * KT_GCOLS + b * 32;
-          float g4[8];  // independent group minima (a shallow dependency tree); the MMA already added |c|^2
+          // batch minimum with 3-input mins (FMNMX3: 16 ALU ops for 32 scores instead of 31;
+          // the scan is ALU-bound), independent partial minima for a shallow tree
+          float g3[11];
 #pragma unroll
-          for (int j = 0; j < 32; j += 4) {
-            const float t0 = __uint_as_float(cur[j]), t1 = __uint_as_float(cur[j + 1]);
-            const float t2 = __uint_as_float(cur[j + 2]), t3 = __uint_as_float(cur[j + 3]);
-            g4[j / 4] = fminf(fminf(t0, t1), fminf(t2, t3));
-          }
-          const float bmin = fminf(fminf(fminf(g4[0], g4[1]), fminf(g4[2], g4[3])),
-                                   fminf(fminf(g4[4], g4[5]), fminf(g4[6], g4[7])));
+          for (int j = 0; j < 10; ++j)
+            g3[j] = min3f(__uint_as_float(cur[3 * j]), __uint_as_float(cur[3 * j + 1]), __uint_as_float(cur[3 * j + 2]));
+          g3[10] = fminf(__uint_as_float(cur[30]), __uint_as_float(cur[31]));
+          const float h0 = min3f(g3[0], g3[1], g3[2]), h1 = min3f(g3[3], g3[4], g3[5]);
+          const float h2 = min3f(g3[6], g3[7], g3[8]), h3 = fminf(g3[9], g3[10]);
+          const float bmin = min3f(h0, h1, fminf(h2, h3));
           m = fminf(m, bmin);
           const float thr = m + two_eps;
           // candidate mask: set.le gives exact 1.0/0.0 flags (one ALU op per
@@ -308,7 +333,7 @@ __global__ void __launch_bounds__(KT_THREADS, 1)
           // batch minimum (so of every candidate's t) carrying the batch
           // index in its low 4 bits -- an entry whose key exceeds the final
           // threshold is certainly stale; the rest are verified exactly.
-          if (!(dbg & 2)) {
+          {
             float acc[4] = {0x1p23f, 0.f, 0x1p23f, 0.f};  // 2^23 + bits 0-15 / 2^23 + bits 16-31
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
@@ -317,11 +342,7 @@ __global__ void __launch_bounds__(KT_THREADS, 1)
               acc[(j >> 4) * 2 + (j & 1)] = fmaf(f, static_cast<float>(1u << (j & 15)), acc[(j >> 4) * 2 + (j & 1)]);
             }
             const uint32_t lo = __float_as_uint(acc[0] + acc[1]), hi = __float_as_uint(acc[2] + acc[3]);
-            uint32_t mask = __byte_perm(lo, hi, 0x5410);
-            if (dbg & 8) {  // diagnostics: build the mask but skip the appends
-              ovf |= mask == 0x5a5a5a5au;
-              mask = 0;
-            }
+            const uint32_t mask = __byte_perm(lo, hi, 0x5410);
             if (mask) {
               if (cnt == KT_LIST) {  // drop entries the running minimum has excluded
                 int w = 0;
@@ -347,7 +368,7 @@ __global__ void __launch_bounds__(KT_THREADS, 1)
       xch[(buf * KT_GROUPS + g) * KT_ROWS + pl] = make_float2(m, __int_as_float(cnt | (ovf << 16)));
       if (g == 0) xeps[buf * KT_ROWS + pl] = two_eps;
       __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&lfull[buf]);
+      named_arrive(bar_lf(buf), KT_HANDOFF);
     }
   } else if (warp < KT_SCAN + KT_VER) {
     // ---------------- verify: final filter, exact check of multi-candidate points, store ----------------
@@ -360,10 +381,10 @@ __global__ void __launch_bounds__(KT_THREADS, 1)
       const int buf = vset;
       const int row = t * 2 * KT_ROWS + static_cast<int>(rank) * KT_ROWS + pl;
       const bool valid = row < rows;
-      ptx::mbar_wait(&lfull[buf], (it >> 1) & 1);
+      named_sync(bar_lf(buf), KT_HANDOFF);  // parked until the scan warps hand this tile over
       if (dbg & 4) {
         __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(&lempty[buf]);
+        named_arrive(bar_le(buf), KT_HANDOFF);
         continue;
       }
       float mall = __int_as_float(0x7f800000);
@@ -434,7 +455,7 @@ __global__ void __launch_bounds__(KT_THREADS, 1)
           }
       }
       __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&lempty[buf]);  // lists consumed (the queue is private)
+      named_arrive(bar_le(buf), KT_HANDOFF);  // lists consumed (the queue is private)
       const int row0 = row - lane;
       for (int i = lane; i < total; i += 32) {
         const int2 e = wq[i];
