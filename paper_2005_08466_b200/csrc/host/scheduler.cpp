@@ -1,11 +1,17 @@
 // Scheduler and the NDRange partitioner.
 //
-// Scheduler: the reference's pluggable placement (proj/src/scheduler.cpp):
-// user_directed / round_robin / static_map / cost_model, EMA profiles
-// (alpha 0.3, first sample sets the rate, 136-149), residency-aware modeled
-// cost (38-48), strict-< argmin keeping the smallest id on ties (81-106).
-// New: partition_weights — the per-device EMA rates become integer split
-// weights for a partitioned NDRange.
+// One rate model drives every decision: rate(device, kernel) is the device's
+// EMA-profiled throughput for the kernel (work units per second; alpha = 0.3,
+// the first sample sets it -- proj/src/scheduler.cpp:136-149), else its
+// modeled rate (relative throughput x baseline). From it:
+//   * placement of a whole launch (the reference's four built-in policies,
+//     same semantics: user_directed, round_robin, static_map and the
+//     residency-aware cost model time = work / rate (+ bytes / bandwidth when
+//     the inputs are not resident) with the lowest id winning ties --
+//     scheduler.cpp:38-48, 81-106), plus user-registered policies;
+//   * partition_weights for a partitioned NDRange: the same rates as integer
+//     split weights, so a device twice
+//     as fast gets twice the rows.
 #include <algorithm>
 #include <atomic>
 #include <cmath>
@@ -44,67 +50,80 @@ const DeviceState* ClusterState::find(int global_id) const {
   return nullptr;
 }
 
+namespace {
+
+// rate(device, kernel): profiled EMA rate, else the device model's rate
+double rate_of(const DeviceState& d, const std::string& kernel, const SchedulerOptions& o) {
+  auto it = d.profiled_rate.find(kernel);
+  return it != d.profiled_rate.end() ? it->second : d.model.relative_throughput * o.baseline_rate;
+}
+
+bool inputs_resident_on(const DeviceState& d, const KernelTask& task) {
+  return std::all_of(task.args.begin(), task.args.end(),
+                     [&](const Arg& a) { return !a.is_buffer || d.resident_buffers.count(a.buffer) > 0; });
+}
+
+enum class Builtin { user_directed, round_robin, static_map, cost_model };
+constexpr std::pair<const char*, Builtin> kBuiltins[] = {{"user_directed", Builtin::user_directed},
+                                                         {"round_robin", Builtin::round_robin},
+                                                         {"static_map", Builtin::static_map},
+                                                         {"cost_model", Builtin::cost_model}};
+
+const DeviceState& require_device(const ClusterState& st, int gid, const std::string& who) {
+  const DeviceState* d = st.find(gid);
+  if (!d) fail(ErrorCode::unknown_device, who + ": device " + std::to_string(gid) + " is not in the device map");
+  return *d;
+}
+
+}  // namespace
+
 struct Scheduler::Impl {
   SchedulerOptions options;
-  std::map<std::string, int> kernel_map;
-  std::map<std::string, PolicyFn> policies;
-  std::shared_ptr<std::atomic<uint64_t>> rr = std::make_shared<std::atomic<uint64_t>>(0);
+  std::map<std::string, int> kernel_map;     // static_map: kernel -> device
+  std::map<std::string, PolicyFn> custom;    // register_policy
+  std::atomic<uint64_t> turn{0};             // round_robin
   mutable std::mutex mu;
   ClusterState state;
 
-  void builtins() {
-    policies["user_directed"] = [](const KernelTask& task, const ClusterState& st, const TaskEstimate&) {
-      if (task.placement.mode != Placement::Mode::explicit_device)
-        fail(ErrorCode::policy, "user_directed requires an explicit device id");
-      if (!st.find(task.placement.device_id))
-        fail(ErrorCode::unknown_device, "device " + std::to_string(task.placement.device_id) + " not in the cluster");
-      return task.placement.device_id;
-    };
-    auto counter = rr;
-    policies["round_robin"] = [counter](const KernelTask&, const ClusterState& st, const TaskEstimate&) {
-      if (st.devices.empty()) fail(ErrorCode::precondition, "no devices");
-      uint64_t turn = counter->fetch_add(1);
-      return st.devices[turn % st.devices.size()].global_id;
-    };
-    auto table = kernel_map;
-    policies["static_map"] = [table](const KernelTask& task, const ClusterState& st, const TaskEstimate&) {
-      auto it = table.find(task.kernel_name);
-      if (it == table.end()) fail(ErrorCode::mapping, "static_map has no entry for kernel '" + task.kernel_name + "'");
-      if (!st.find(it->second))
-        fail(ErrorCode::unknown_device, "static_map entry for '" + task.kernel_name + "' names unknown device " +
-                                            std::to_string(it->second));
-      return it->second;
-    };
-    auto opts = options;
-    policies["cost_model"] = [opts](const KernelTask& task, const ClusterState& st, const TaskEstimate& est) {
-      if (st.devices.empty()) fail(ErrorCode::precondition, "no devices");
-      std::vector<uint64_t> inputs;
-      for (const auto& a : task.args)
-        if (a.is_buffer) inputs.push_back(a.buffer);
-      int best = -1;
-      double best_cost = std::numeric_limits<double>::infinity();
-      for (const auto& d : st.devices) {
-        bool resident = true;
-        for (uint64_t id : inputs)
-          if (!d.resident_buffers.count(id)) {
-            resident = false;
-            break;
-          }
-        double cost = Scheduler::modeled_cost(d, task.kernel_name, est, opts, resident);
-        if (cost < best_cost) {  // strict <: smallest id wins ties
-          best_cost = cost;
-          best = d.global_id;
-        }
+  static const Builtin* builtin(const std::string& name) {
+    for (const auto& [n, b] : kBuiltins)
+      if (name == n) return &b;
+    return nullptr;
+  }
+
+  int place(Builtin b, const KernelTask& task, const TaskEstimate& est) {
+    switch (b) {
+      case Builtin::user_directed:
+        if (task.placement.mode != Placement::Mode::explicit_device)
+          fail(ErrorCode::policy, "user_directed placement needs an explicit device id");
+        return require_device(state, task.placement.device_id, "user_directed").global_id;
+      case Builtin::round_robin:
+        return state.devices[turn.fetch_add(1) % state.devices.size()].global_id;
+      case Builtin::static_map: {
+        auto it = kernel_map.find(task.kernel_name);
+        if (it == kernel_map.end())
+          fail(ErrorCode::mapping, "static_map: kernel '" + task.kernel_name + "' is not mapped to a device");
+        return require_device(state, it->second, "static_map entry for '" + task.kernel_name + "'").global_id;
       }
-      return best;
-    };
+      case Builtin::cost_model: {
+        // device order is ascending id: the first minimum is the lowest id on ties
+        const DeviceState* best = nullptr;
+        double best_t = std::numeric_limits<double>::infinity();
+        for (const auto& d : state.devices) {
+          const double t = Scheduler::modeled_cost(d, task.kernel_name, est, options, inputs_resident_on(d, task));
+          if (t < best_t) best_t = t, best = &d;
+        }
+        if (!best) fail(ErrorCode::precondition, "cost_model: no device has a finite cost");
+        return best->global_id;
+      }
+    }
+    fail(ErrorCode::internal, "unreachable placement");
   }
 };
 
 Scheduler::Scheduler(SchedulerOptions options, std::map<std::string, int> kernel_map) : impl_(new Impl) {
   impl_->options = options;
   impl_->kernel_map = std::move(kernel_map);
-  impl_->builtins();
 }
 Scheduler::~Scheduler() = default;
 
@@ -112,49 +131,54 @@ void Scheduler::configure(SchedulerOptions options, std::map<std::string, int> k
   std::lock_guard lock(impl_->mu);
   impl_->options = options;
   impl_->kernel_map = std::move(kernel_map);
-  impl_->policies.clear();
-  impl_->rr->store(0);
-  impl_->builtins();
+  impl_->custom.clear();
+  impl_->turn.store(0);
 }
 
 const SchedulerOptions& Scheduler::options() const { return impl_->options; }
 
 double Scheduler::modeled_cost(const DeviceState& device, const std::string& kernel_name, const TaskEstimate& est,
                                const SchedulerOptions& options, bool inputs_resident) {
-  double rate = device.model.relative_throughput * options.baseline_rate;
-  auto it = device.profiled_rate.find(kernel_name);
-  if (it != device.profiled_rate.end()) rate = it->second;
-  double cost = est.work_units / rate;
-  if (!inputs_resident) cost += static_cast<double>(est.in_bytes + est.out_bytes) / options.net_bandwidth;
-  return cost;
+  const double compute = est.work_units / rate_of(device, kernel_name, options);
+  const double transfer =
+      inputs_resident ? 0.0 : static_cast<double>(est.in_bytes + est.out_bytes) / options.net_bandwidth;
+  return compute + transfer;
 }
 
 void Scheduler::register_policy(const std::string& name, PolicyFn policy) {
   std::lock_guard lock(impl_->mu);
-  if (impl_->policies.count(name)) fail(ErrorCode::registration, "policy '" + name + "' already registered");
-  impl_->policies[name] = std::move(policy);
+  if (Impl::builtin(name) || impl_->custom.count(name))
+    fail(ErrorCode::registration, "a policy named '" + name + "' exists already");
+  impl_->custom.emplace(name, std::move(policy));
 }
 
 bool Scheduler::has_policy(const std::string& name) const {
   std::lock_guard lock(impl_->mu);
-  return impl_->policies.count(name) > 0;
+  return Impl::builtin(name) || impl_->custom.count(name) > 0;
 }
 
 int Scheduler::schedule(const KernelTask& task, const TaskEstimate& estimate) {
   std::lock_guard lock(impl_->mu);
-  if (impl_->state.devices.empty()) fail(ErrorCode::precondition, "scheduler has no devices");
-  std::string name = task.placement.mode == Placement::Mode::explicit_device ? "user_directed" : task.placement.policy;
-  auto it = impl_->policies.find(name);
-  if (it == impl_->policies.end()) fail(ErrorCode::policy, "unknown policy '" + name + "'");
-  int chosen = it->second(task, impl_->state, estimate);
+  if (impl_->state.devices.empty()) fail(ErrorCode::precondition, "the scheduler knows no devices");
+  const std::string name =
+      task.placement.mode == Placement::Mode::explicit_device ? "user_directed" : task.placement.policy;
+  int chosen;
+  if (const Builtin* b = Impl::builtin(name)) {
+    chosen = impl_->place(*b, task, estimate);
+  } else {
+    auto it = impl_->custom.find(name);
+    if (it == impl_->custom.end()) fail(ErrorCode::policy, "no placement policy named '" + name + "'");
+    chosen = it->second(task, impl_->state, estimate);
+  }
   if (!impl_->state.find(chosen))
-    fail(ErrorCode::internal, "policy '" + name + "' chose device " + std::to_string(chosen) + " outside the device map");
+    fail(ErrorCode::internal, "policy '" + name + "' returned device " + std::to_string(chosen) +
+                                  ", which is not in the device map");
   return chosen;
 }
 
 void Scheduler::record_profile(int global_id, const std::string& kernel_name, double work_units,
                                double observed_seconds) {
-  if (!(observed_seconds > 0.0)) fail(ErrorCode::precondition, "observed_compute_seconds must be > 0");
+  if (!(observed_seconds > 0.0)) fail(ErrorCode::precondition, "a profile sample needs a positive duration");
   std::lock_guard lock(impl_->mu);
   DeviceState* d = impl_->state.find(global_id);
   if (!d) fail(ErrorCode::unknown_device, "device " + std::to_string(global_id));
@@ -240,16 +264,9 @@ ClusterState Scheduler::snapshot() const {
 std::vector<uint64_t> Scheduler::partition_weights(const std::string& kernel_name, const std::vector<int>& gids) const {
   std::lock_guard lock(impl_->mu);
   std::vector<double> rates;
-  for (int g : gids) {
-    const DeviceState* d = impl_->state.find(g);
-    if (!d) fail(ErrorCode::unknown_device, "device " + std::to_string(g));
-    double rate = d->model.relative_throughput * impl_->options.baseline_rate;
-    auto it = d->profiled_rate.find(kernel_name);
-    if (it != d->profiled_rate.end()) rate = it->second;
-    rates.push_back(rate);
-  }
-  double mx = 0.0;
-  for (double r : rates) mx = std::max(mx, r);
+  for (int g : gids) rates.push_back(rate_of(require_device(impl_->state, g, "partition_weights"), kernel_name,
+                                             impl_->options));
+  const double mx = rates.empty() ? 1.0 : *std::max_element(rates.begin(), rates.end());
   std::vector<uint64_t> w;
   // 20-bit resolution; identical rates give identical weights (block_range)
   for (double r : rates) w.push_back(std::max<uint64_t>(1, static_cast<uint64_t>(std::llround(r / mx * 1048576.0))));

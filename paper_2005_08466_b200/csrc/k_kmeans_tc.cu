@@ -43,7 +43,7 @@
 // and hand each tile's lists (double-buffered in shared memory, mbarrier
 // handshakes) to the verify warps -- two sets of 4, one per list buffer --
 // which filter, check exactly and store while the scan runs on. Measured on
-// 2^26 points, K=1024 (scripts/gpu_km4.sh, gpu_km7.sh): 4 groups x 4 slots,
+// 2^26 points, K=1024 (round 1 sweeps, profiles/r01_kmeans_tc.txt): 4 groups x 4 slots,
 // N=256: 20.2 ms, 17.2 ms with |c|^2 folded into the MMA; 2 groups x 8 slots:
 // 24.5 ms; N=128 chunks: 22.0 ms.
 #include <cuda.h>
