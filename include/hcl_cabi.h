@@ -129,6 +129,9 @@ int hcl_buffer_read_async(int dev, uint64_t id, uint64_t offset, void* dst, uint
 int hcl_buffer_copy_peer(int dst_dev, uint64_t dst_id, uint64_t dst_offset, int src_dev,
                          uint64_t src_id, uint64_t src_offset, uint64_t len);
 int hcl_buffer_release(int dev, uint64_t id); /* idempotent */
+/* Exchange the device allocations of two buffer ids (bookkeeping only; their
+ * pending-work dependencies travel with the memory). Commits a staged output. */
+int hcl_buffer_swap(int dev, uint64_t id_a, uint64_t id_b);
 /* Device pointer of the resident slice (ptr addresses logical byte first_byte). */
 int hcl_buffer_device_ptr(int dev, uint64_t id, void** ptr, uint64_t* first_byte,
                           uint64_t* bytes);

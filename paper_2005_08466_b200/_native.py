@@ -57,6 +57,7 @@ CABI = [
     ("hcl_buffer_copy_peer", C.c_int, [C.c_int, C.c_uint64, C.c_uint64, C.c_int, C.c_uint64, C.c_uint64,
                                        C.c_uint64]),
     ("hcl_buffer_release", C.c_int, [C.c_int, C.c_uint64]),
+    ("hcl_buffer_swap", C.c_int, [C.c_int, C.c_uint64, C.c_uint64]),
     ("hcl_buffer_device_ptr", C.c_int, [C.c_int, C.c_uint64, C.POINTER(C.c_void_p), u64p, u64p]),
     ("hcl_buffer_bind_external", C.c_int, [C.c_int, C.c_uint64, C.c_void_p, C.c_uint64, C.c_uint64]),
     ("hcl_launch", C.c_int, [C.c_int, C.c_char_p, C.POINTER(HclArg), C.c_uint32, u64p, u64p, C.c_uint32, u64p]),

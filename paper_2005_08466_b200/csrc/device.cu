@@ -614,6 +614,22 @@ int hcl_buffer_copy_peer(int dst_dev, uint64_t dst_id, uint64_t dst_offset, int 
   });
 }
 
+int hcl_buffer_swap(int dev, uint64_t id_a, uint64_t id_b) {
+  return guarded([&] {
+    Device& d = device(dev);
+    std::lock_guard<std::mutex> lock(d.mu);
+    auto a = d.bufs.find(id_a);
+    auto b = d.bufs.find(id_b);
+    if (b == d.bufs.end()) fail(ErrorCode::handle, "buffer_swap: buffer " + std::to_string(id_b) + " not on device");
+    if (a == d.bufs.end()) {  // id_a had no allocation here: it takes id_b's
+      d.bufs.emplace(id_a, b->second);
+      d.bufs.erase(b);
+      return;
+    }
+    std::swap(a->second, b->second);
+  });
+}
+
 int hcl_buffer_release(int dev, uint64_t id) {
   return guarded([&] {
     Device& d = device(dev);

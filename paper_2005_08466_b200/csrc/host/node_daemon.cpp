@@ -84,7 +84,7 @@ constexpr uint8_t kVersion = 1;
 // ErrorCode values of the wire contract (proj/include/haocl/error.hpp:11-36)
 enum Code : uint16_t {
   kInternal = 0, kProtocol = 1, kVersionErr = 2, kMalformed = 3, kEncoding = 4, kUnknownCall = 5,
-  kPrecondition = 7, kReassembly = 8, kArgument = 9, kName = 10, kUnknownDevice = 20,
+  kPrecondition = 7, kReassembly = 8, kArgument = 9, kName = 10, kSizeErr = 18, kUnknownDevice = 20,
 };
 
 struct WireError {
@@ -308,6 +308,7 @@ class NodeDaemon {
       uint64_t hbm = 0;
       hcl_device_info(d, &type, &rel, &sms, &hbm, nullptr, 0);
       rel_.push_back(rel);
+      max_buffer_ = std::max(max_buffer_, hbm);
       dev_mu_.push_back(std::make_unique<std::mutex>());
     }
     listen_fd_[0] = listen_on(port_);
@@ -452,6 +453,7 @@ class NodeDaemon {
         const uint64_t id = in.u64(), off = in.u64(), total = in.u64();
         const size_t len = in.left();
         if (off > total || len > total - off) werr(kMalformed, "data package exceeds total_len");
+        check_size(total, "data transfer");
         const auto done = put_chunk(id, off, total, in.here(), len);
         if (!done) return std::nullopt;  // only the completing chunk is acknowledged
         Out o;
@@ -551,7 +553,19 @@ class NodeDaemon {
     e.host_valid = true;
   }
 
+  // sizes come from the network: a buffer never exceeds one device's HBM
+  // (HCL_NODE_MAX_BUFFER lowers the cap), else a size error instead of an
+  // attempt to allocate it on the host
+  void check_size(uint64_t bytes, const char* what) const {
+    uint64_t cap = max_buffer_ ? max_buffer_ : (1ull << 40);
+    if (const char* e = std::getenv("HCL_NODE_MAX_BUFFER")) cap = std::min<uint64_t>(cap, std::strtoull(e, nullptr, 10));
+    if (bytes > cap)
+      werr(kSizeErr, std::string(what) + ": " + std::to_string(bytes) + " bytes exceeds the node's buffer cap of " +
+                         std::to_string(cap));
+  }
+
   void alloc(uint64_t id, uint64_t size) {
+    check_size(size, "alloc_buffer");
     std::lock_guard<std::mutex> l(store_mu_);
     Entry& e = store_[id];
     if (e.size >= size) return;
@@ -661,6 +675,7 @@ class NodeDaemon {
     std::lock_guard<std::mutex> dl(*dev_mu_[dev]);
     std::vector<hcl_arg> args(static_cast<size_t>(nargs));
     std::vector<uint64_t> outs;
+    std::vector<std::pair<uint64_t, uint64_t>> fresh;  // (output id, staging device id)
     {
       std::lock_guard<std::mutex> l(store_mu_);
       for (int k = 0; k < nargs; ++k) {
@@ -680,11 +695,13 @@ class NodeDaemon {
         auto it = store_.find(id);
         if (kinds[k] == HCL_ARG_OUT) {
           if (it == store_.end()) werr(kPrecondition, "output buffer " + std::to_string(id) + " not allocated");
-          // fresh zero-filled HBM: the reference zero-fills outputs (kernels.cpp:43-48)
-          hcl_buffer_release(dev, h.buffer_id);
-          check(hcl_buffer_alloc(dev, h.buffer_id, 0, it->second.size));
-          it->second.on_dev.erase(dev);
-          outs.push_back(id);
+          // fresh zero-filled HBM (the reference zero-fills outputs, kernels.cpp:43-48),
+          // under a staging id: the buffer's current copy survives a failed launch
+          const uint64_t staged = cid(id) | (1ull << 62);
+          hcl_buffer_release(dev, staged);
+          check(hcl_buffer_alloc(dev, staged, 0, it->second.size));
+          h.buffer_id = staged;
+          fresh.push_back({id, staged});
           continue;
         }
         if (it == store_.end() || it->second.session)
@@ -695,9 +712,18 @@ class NodeDaemon {
     }
     uint64_t work = 0;
     double ms = 0.0;
-    check(hcl_launch(dev, kernel.c_str(), args.data(), static_cast<uint32_t>(nargs), nullptr, nullptr,
-                     dims ? dims : 1, &work));
-    check(hcl_finish(dev, &ms));
+    int rc = hcl_launch(dev, kernel.c_str(), args.data(), static_cast<uint32_t>(nargs), nullptr, nullptr,
+                        dims ? dims : 1, &work);
+    if (rc == HCL_OK) rc = hcl_finish(dev, &ms);
+    if (rc != HCL_OK) {  // the outputs keep their previous contents
+      for (const auto& [id, staged] : fresh) hcl_buffer_release(dev, staged);
+      check(rc);
+    }
+    for (const auto& [id, staged] : fresh) {  // commit: the staged allocations become the outputs
+      check(hcl_buffer_swap(dev, cid(id), staged));
+      hcl_buffer_release(dev, staged);
+      outs.push_back(id);
+    }
     {
       std::lock_guard<std::mutex> l(store_mu_);
       for (uint64_t id : outs) {
@@ -725,6 +751,7 @@ class NodeDaemon {
   int port_;
   int listen_fd_[2] = {-1, -1};
   std::vector<double> rel_;
+  uint64_t max_buffer_ = 0;  // largest device HBM: the cap on network-supplied sizes
   std::vector<std::unique_ptr<std::mutex>> dev_mu_;
   std::atomic<bool> stopping_{false};
   int waiters_ = 0;

@@ -131,3 +131,19 @@ def test_shutdown_message_stops_the_daemon():
     d.wait()  # returns once the Shutdown is handled
     c.close()
     d.stop()
+
+
+def test_network_sizes_are_capped(node, monkeypatch):
+    """sizes from the wire (alloc_buffer, DataTransfer total_len)
+    are checked against the node's buffer cap (one device's HBM, lowered by
+    HCL_NODE_MAX_BUFFER) and answered with a size error (18) instead of an
+    attempt to allocate them."""
+    monkeypatch.setenv("HCL_NODE_MAX_BUFFER", "4096")
+    c, d = W.Conn(node.port), W.Conn(node.port + 1)
+    with pytest.raises(W.RemoteError) as e:
+        c.call(1, "alloc_buffer", [(W.HANDLE, 7), (W.I64, 1 << 40)], [(7, 1)])
+    assert e.value.code == 18
+    c.call(2, "alloc_buffer", [(W.HANDLE, 8), (W.I64, 4096)], [(8, 1)])  # at the cap: accepted
+    d.send(W.frame(W.DATA, 3, W.data_chunk(9, 0, 1 << 20, bytes(16))))
+    kind, cid, body = d.recv_frame()
+    assert cid == 3 and W.error_of(body)[0] == 18
