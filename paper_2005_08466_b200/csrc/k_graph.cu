@@ -698,8 +698,10 @@ __device__ __forceinline__ void reds_add_if(unsigned* p, unsigned v, bool pred) 
 // words per row (64-bit shared atomics compile to CAS loops; the low word's
 // carry goes into the high word, so (hi, lo) is the exact 64-bit sum in any
 // order).
-constexpr int PBG_T = 1024, PBG_STAGE = 8 * PBG_T, PBG_STAGES = 2;
-constexpr int PBG_STAGE_BYTES = PBG_STAGE * 6;
+// T threads per CTA, a stage of 8 T entries: T = 1024 with 16384-row bins (one
+// CTA per SM), T = 512 with <= 8192-row bins (two CTAs per SM)
+constexpr int PBG_STAGES = 2;
+template <int PBG_T>
 __global__ void __launch_bounds__(PBG_T) pr_bin_gather_kernel(const int64_t* __restrict__ part,
                                                              const int4* __restrict__ units,
                                                              const int* __restrict__ slot_units,
@@ -713,6 +715,7 @@ __global__ void __launch_bounds__(PBG_T) pr_bin_gather_kernel(const int64_t* __r
                                                              int n_peers, const float* __restrict__ inv_outdeg,
                                                              float* __restrict__ xs_next,
                                                              unsigned long long* __restrict__ dsum_next) {
+  constexpr int PBG_STAGE = 8 * PBG_T, PBG_STAGE_BYTES = PBG_STAGE * 6;
   extern __shared__ __align__(128) uint8_t pg_smem[];
   __shared__ int last_flag;
   const int64_t W = part[PB_BINROWS], hi = part[PB_HI];
@@ -939,16 +942,17 @@ uint64_t launch_pr_binned(LaunchCtx& c) {
     HCL_LAUNCHED();
   }
   // phase 2
-  const size_t smem2 = static_cast<size_t>(PBG_STAGES) * PBG_STAGE_BYTES + 2 * PBG_STAGES * 8 +
-                       static_cast<size_t>(W) * 8;
-  HCL_CUDA(cudaFuncSetAttribute(pr_bin_gather_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                static_cast<int>(smem2)));
+  const bool small_bins = W <= 8192;
+  const int gt = small_bins ? 512 : 1024;
+  const size_t smem2 = static_cast<size_t>(PBG_STAGES) * 8 * gt * 6 + 2 * PBG_STAGES * 8 + static_cast<size_t>(W) * 8;
+  auto gkern = small_bins ? pr_bin_gather_kernel<512> : pr_bin_gather_kernel<1024>;
+  HCL_CUDA(cudaFuncSetAttribute(gkern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem2)));
   const int64_t n_slots_total = static_cast<int64_t>(SA.bytes / (W * 8 + 4));
   unsigned long long* slot_acc = reinterpret_cast<unsigned long long*>(SA.ptr);
   unsigned int* slot_cnt = reinterpret_cast<unsigned int*>(slot_acc + n_slots_total * W);
   const float base = static_cast<float>((1.0 - 0.85) / v), damp = 0.85f, inv_v = static_cast<float>(1.0 / v);
   if (P[PB_NUNITS] > 0) {
-    pr_bin_gather_kernel<<<static_cast<unsigned>(P[PB_NUNITS]), PBG_T, smem2, c.stream>>>(
+    gkern<<<static_cast<unsigned>(P[PB_NUNITS]), gt, smem2, c.stream>>>(
         dpart, reinterpret_cast<const int4*>(UN.ptr), reinterpret_cast<const int*>(SU.ptr),
         reinterpret_cast<const float*>(VA.ptr), reinterpret_cast<const uint16_t*>(DS.ptr), slot_acc, slot_cnt,
         reinterpret_cast<const unsigned long long*>(D.ptr), y, static_cast<int>(lo), base, damp, inv_v,
