@@ -292,6 +292,8 @@ struct Entry {
 // collides with that context's buffers
 constexpr uint64_t kIdSpace = 1ull << 62;
 uint64_t cid(uint64_t wire_id) { return wire_id ^ kIdSpace; }
+// launch outputs are written under cid(id) ^ kStagedSpace, then swapped in
+constexpr uint64_t kStagedSpace = 1ull << 60;
 
 void check(int rc) {
   if (rc != HCL_OK) werr(static_cast<uint16_t>(rc - HCL_ERR_BASE), hcl_last_error());
@@ -697,7 +699,7 @@ class NodeDaemon {
           if (it == store_.end()) werr(kPrecondition, "output buffer " + std::to_string(id) + " not allocated");
           // fresh zero-filled HBM (the reference zero-fills outputs, kernels.cpp:43-48),
           // under a staging id: the buffer's current copy survives a failed launch
-          const uint64_t staged = cid(id) | (1ull << 62);
+          const uint64_t staged = cid(id) ^ kStagedSpace;
           hcl_buffer_release(dev, staged);
           check(hcl_buffer_alloc(dev, staged, 0, it->second.size));
           h.buffer_id = staged;

@@ -166,21 +166,24 @@ def test_finish_does_not_block_other_queues(ctx, queues):
     thread creates, writes and reads back a buffer on another queue. Those
     calls need only copy engines, so they must complete while A still waits
     (with one table lock held across the device sync they would queue behind it)."""
-    n = 6144  # zero-filled inputs (never written): no host data needed
+    n = 8192  # zero-filled inputs (never written): no host data needed
     ba, bb, bc = (ctx.create_buffer(n * n * 8) for _ in range(3))
     mk = kernel(ctx, "core", "matmul", [ba, bb, bc, n, n, n])
     ctx.enqueue_ndrange_kernel(queues[0], mk, (n, n, 1), 2)
     ctx.finish(queues[0])  # warm-up: allocation, first launch
+    reps = 4
     t_kernel = time.perf_counter()
-    ctx.enqueue_ndrange_kernel(queues[0], mk, (n, n, 1), 2)
+    for _ in range(reps):
+        ctx.enqueue_ndrange_kernel(queues[0], mk, (n, n, 1), 2)
     ctx.finish(queues[0])
     t_kernel = time.perf_counter() - t_kernel
-    assert t_kernel > 0.05, f"the blocking kernel is too short to test overlap ({t_kernel:.3f} s)"
+    assert t_kernel > 0.1, f"the blocking kernels are too short to test overlap ({t_kernel:.3f} s)"
 
     done = {}
 
     def waiter():
-        ctx.enqueue_ndrange_kernel(queues[0], mk, (n, n, 1), 2)
+        for _ in range(reps):
+            ctx.enqueue_ndrange_kernel(queues[0], mk, (n, n, 1), 2)
         done["enqueued"] = time.perf_counter()
         ctx.finish(queues[0])
         done["finished"] = time.perf_counter()
