@@ -853,6 +853,13 @@ class KMeansW(Workload):
 
         self.cent0 = G.gen_kmeans_points(self.K, self.D, self.K, 42)  # first K points = initial centroids
         km.set_centroids(self.cent0)
+        # store the rank's points grouped by their nearest initial centroid (a layout transform,
+        # results unchanged): a warp's points then share candidate centroids and the tensor
+        # assignment skips its candidate-mask pass warp-wide where none has one
+        self.ordered = self.tc and os.environ.get("BENCH_KM_ORDER", "1") == "1"
+        if self.ordered:
+            km.order_by_cluster(parts=[(q, self.lo, self.lo + self.rows)])
+            km.set_centroids(self.cent0)
         if d.world > 1:
             uid = d.bcast_bytes(HostContext.nccl_unique_id() if d.rank == 0 else None)
             ctx.init_collectives(q, d.rank, d.world, uid)
@@ -908,7 +915,9 @@ class KMeansW(Workload):
                             f"assignment (3 flop/term), int64 sums, points split over {self.dist.world} rank(s)",
                 "assign_kernel": "kmeans_assign_tc (tcgen05 split-bf16 filter + exact fp32 verify)" if self.tc
                 else "kmeans_assign (exact fp32 SIMT)",
-                "points": "SplitMix64 blobs, multiples of 2^-12, generated in HBM",
+                "points": "SplitMix64 blobs, multiples of 2^-12, generated in HBM" +
+                          ("; stored grouped by nearest initial centroid (KMeans.order_by_cluster)" if self.ordered
+                           else ""),
                 "l2": f"points {self.N * self.D * 4 >> 30} GiB > L2; no flush"}
 
     @staticmethod

@@ -66,6 +66,10 @@ int hcl_pagerank_bins_export(void* h, int32_t* chunks, uint16_t* src_local, uint
                              int32_t* units, int32_t* slot_units, uint32_t* cdesc);
 void hcl_pagerank_bins_free(void* h);
 
+/* Stable counting order of n keys in [0, k): perm[i] = index of the i-th key
+ * in ascending order (ties by index). Returns 0 or 1000+argument. */
+int hcl_counting_order(const int32_t* keys, int64_t n, int32_t k, int32_t* perm);
+
 /* CSR-adaptive row blocks (<= max_nnz per multi-row block); out may be NULL to
  * count. Returns the number of blocks; out[0..n] are block start rows. */
 int64_t hcl_csr_row_blocks(const int32_t* row_ptr, int64_t rows, int64_t max_nnz, int32_t* out);

@@ -164,6 +164,7 @@ DATAGEN = [
                                              C.c_int64, C.c_int64, C.c_int64, C.c_void_p]),
     ("hcl_pagerank_bins_export", C.c_int, [C.c_void_p] + [C.c_void_p] * 7),
     ("hcl_pagerank_bins_free", None, [C.c_void_p]),
+    ("hcl_counting_order", C.c_int, [C.c_void_p, C.c_int64, C.c_int32, C.c_void_p]),
 ]
 
 

@@ -303,4 +303,18 @@ int hcl_pagerank_relabel(const int32_t* row_ptr, const int32_t* col_idx, const f
   return 0;
 }
 
+// Stable counting order: perm[i] = the index of the i-th key in ascending key
+// order (ties by index). keys in [0, k); returns 0 or 1000+argument.
+int hcl_counting_order(const int32_t* keys, int64_t n, int32_t k, int32_t* perm) {
+  if (n < 0 || k < 1 || (n && (!keys || !perm))) return 1000 + 9;
+  std::vector<int64_t> start(static_cast<size_t>(k) + 1, 0);
+  for (int64_t i = 0; i < n; ++i) {
+    if (keys[i] < 0 || keys[i] >= k) return 1000 + 9;
+    ++start[static_cast<size_t>(keys[i]) + 1];
+  }
+  for (int32_t j = 0; j < k; ++j) start[j + 1] += start[j];
+  for (int64_t i = 0; i < n; ++i) perm[start[keys[i]]++] = static_cast<int32_t>(i);
+  return 0;
+}
+
 }  // extern "C"

@@ -450,6 +450,13 @@ uint64_t launch_gen_points(LaunchCtx& c) {
   return rows * static_cast<uint64_t>(d);
 }
 
+__global__ void check_perm_kernel(const int32_t* __restrict__ perm, int64_t lo, int64_t rows, int* __restrict__ bad) {
+  int mine = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < rows; i += (int64_t)gridDim.x * blockDim.x)
+    mine |= perm[i] < lo || perm[i] >= lo + rows;
+  if (__syncthreads_or(mine) && threadIdx.x == 0) atomicOr(bad, 1);
+}
+
 // kmeans_accumulate's exact int32/int64 tables assume every coordinate is a
 // multiple of 2^-12 inside [-8, 8) (|x * 4096| <= 2^15). This check flags
 // any other value (NaN and inf included) before the data is used.
@@ -486,8 +493,47 @@ uint64_t launch_check_points(LaunchCtx& c) {
   return rows * static_cast<uint64_t>(d);
 }
 
+// dst row i = src row perm[i] (perm: absolute rows inside the launch's range)
+__global__ void gather_rows_kernel(const float4* __restrict__ src, const int32_t* __restrict__ perm,
+                                   float4* __restrict__ dst, int64_t lo, int64_t rows, int v4) {
+  const int64_t total = rows * v4;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / v4;
+    const int64_t from = static_cast<int64_t>(__ldg(perm + i)) - lo;
+    dst[e] = __ldg(src + from * v4 + (e - i * v4));
+  }
+}
+
+// kmeans_gather_points(points, perm, out, N, D): out[i] = points[perm[i]] for the
+// launch's rows; perm must stay inside them (argument error otherwise)
+uint64_t launch_gather_points(LaunchCtx& c) {
+  int64_t n = scalar_arg(c, 3, "kmeans_gather_points N"), d = scalar_arg(c, 4, "kmeans_gather_points D");
+  if (n < 0 || d < 1 || d % 4) fail(ErrorCode::argument, "kmeans_gather_points: bad N or D (a multiple of 4)");
+  uint64_t lo, rows;
+  sub_range(c, static_cast<uint64_t>(n), lo, rows, "kmeans_gather_points");
+  const float* src = at_byte<const float>(buffer_arg(c, 0, "gather src"), lo * d * 4, rows * d * 4, "gather src");
+  const int32_t* perm = at_byte<const int32_t>(buffer_arg(c, 1, "gather perm"), lo * 4, rows * 4, "gather perm");
+  float* dst = at_byte<float>(buffer_arg(c, 2, "gather dst"), lo * d * 4, rows * d * 4, "gather dst");
+  if (!rows) return 0;
+  // the permutation must stay inside [lo, lo + rows): check on the device
+  int* bad = static_cast<int*>(c.scratch(c.dev, 8));
+  HCL_CUDA(cudaMemsetAsync(bad, 0, 8, c.stream));
+  check_perm_kernel<<<c.sm_count * 4, 256, 0, c.stream>>>(perm, static_cast<int64_t>(lo), static_cast<int64_t>(rows), bad);
+  HCL_LAUNCHED();
+  int h = 0;
+  HCL_CUDA(cudaMemcpyAsync(&h, bad, 4, cudaMemcpyDeviceToHost, c.stream));
+  HCL_CUDA(cudaStreamSynchronize(c.stream));
+  if (h) fail(ErrorCode::argument, "kmeans_gather_points: perm leaves the launch's rows");
+  gather_rows_kernel<<<c.sm_count * 8, 256, 0, c.stream>>>(reinterpret_cast<const float4*>(src), perm,
+                                                          reinterpret_cast<float4*>(dst), static_cast<int64_t>(lo),
+                                                          static_cast<int64_t>(rows), static_cast<int>(d / 4));
+  HCL_LAUNCHED();
+  return rows * static_cast<uint64_t>(d);
+}
+
 uint64_t rows_km(const int64_t* s, uint32_t n) { return static_cast<uint64_t>(s[n == 6 ? 3 : 4]); }
 uint64_t rows_gen(const int64_t* s, uint32_t) { return static_cast<uint64_t>(s[1]); }
+uint64_t rows_gather(const int64_t* s, uint32_t) { return static_cast<uint64_t>(s[3]); }
 
 }  // namespace
 
@@ -500,6 +546,8 @@ void register_kmeans(std::vector<KernelDef>& r) {
   r.push_back({"b200", "kmeans_finalize", {I, I, IO, S, S}, {P, P, P, N, N}, launch_finalize, nullptr, nullptr});
   r.push_back({"b200", "reduce_add_i64", {IO, I, S}, {P, P, N}, launch_add_i64, nullptr, nullptr});
   r.push_back({"b200", "kmeans_check_points", {I, S, S}, {X, N, N}, launch_check_points, nullptr, rows_gen});
+  r.push_back({"b200", "kmeans_gather_points", {I, I, O, S, S}, {X, X, X, N, N}, launch_gather_points, nullptr,
+               rows_gather});
   r.push_back({"b200", "gen_kmeans_points", {O, S, S, S, S}, {X, N, N, N, N}, launch_gen_points, nullptr, rows_gen});
 }
 

@@ -98,7 +98,7 @@ static_assert((KT_KMAX / KT_CW) * (KT_GCOLS / 32) <= 16, "list keys carry a 4-bi
 constexpr int KT_LBUF = KT_GROUPS * KT_ROWS * KT_LIST;  // float2 slots of one tile's lists (all groups)
 
 struct KtLayout {
-  size_t b, a, q, lists, xch, vq, bars, total;
+  size_t b, a, q, lists, xch, vq, bars, seed, total;
   __host__ __device__ KtLayout(int K) {
     const int nch = K / KT_CW;
     b = 0;
@@ -108,7 +108,8 @@ struct KtLayout {
     xch = lists + 2ull * KT_LBUF * 8;             // 2 buffers x (key | batch index, mask) float2 entries
     vq = xch + 2ull * KT_GROUPS * KT_ROWS * 8 + 2ull * KT_ROWS * 4;  // 2 bufs x groups x (min, count|ovf) + 2 eps
     bars = vq + static_cast<size_t>(KT_VER) * 32 * KT_QCAP * 8;  // verify queues
-    total = bars + 16 * 8 + 16 + 1024;            // barriers, TMEM slot, alignment slack
+    seed = bars + 16 * 8 + 16;                    // barriers, TMEM slot
+    total = seed + 2 * KT_ROWS * 4 + 1024;        // per-point threshold seeds (2 tiles), alignment slack
   }
 };
 
@@ -160,7 +161,7 @@ __device__ __forceinline__ float exact_dist(const float (&x)[KT_D], const float*
 
 __global__ void __launch_bounds__(KT_THREADS, 1)
     kmeans_assign_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB1,
-                            const __grid_constant__ CUtensorMap tmB2, const float* __restrict__ /*q: unused*/,
+                            const __grid_constant__ CUtensorMap tmB2, const float* __restrict__ qnorm,
                             const float* __restrict__ stats, const float* __restrict__ cent,
                             const float* __restrict__ pts, const float* __restrict__ xxg,
                             int32_t* __restrict__ assign, int rows, int K, int* __restrict__ n_overflow,
@@ -180,6 +181,7 @@ __global__ void __launch_bounds__(KT_THREADS, 1)
   float2* xch = reinterpret_cast<float2*>(smem + L.xch);              // [buf][group][point] (min, count|ovf<<16)
   float* xeps = reinterpret_cast<float*>(xch + 2 * KT_GROUPS * KT_ROWS);  // [buf][point] 2 eps
   int2* vq = reinterpret_cast<int2*>(smem + L.vq);
+  float* seeds = reinterpret_cast<float*>(smem + L.seed);  // per point of the tile: the threshold seed
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.bars);
   uint64_t* empty = full + KT_STAGES;
   uint64_t* tfull = empty + KT_STAGES;
@@ -199,7 +201,7 @@ __global__ void __launch_bounds__(KT_THREADS, 1)
     ptx::prefetch_tmap(&tmB2);
     for (int s = 0; s < KT_STAGES; ++s) {
       ptx::mbar_init(&full[s], 1);
-      ptx::mbar_init(&empty[s], 1);
+      ptx::mbar_init(&empty[s], 2);  // the MMAs' commit + the scan warps' seed reads of the A rows
     }
     for (int a = 0; a < KT_NACC; ++a) {
       ptx::mbar_init(&tfull[a], 1);
@@ -302,6 +304,49 @@ __global__ void __launch_bounds__(KT_THREADS, 1)
         ptx::mbar_wait(&tfull[acc], (tph >> acc) & 1);
         tph ^= 1u << acc;
         ptx::tc_fence_after();
+        if (c == 0) {
+          // start the running minimum at an upper bound of min_k t~_k: the score of
+          // the point's previous centroid (any centroid bounds the minimum, so stale
+          // or zero assignments are safe), t_p = |c_p|^2 - 2 x.c_p in fp32 with x =
+          // xh + xl read from this tile's A rows (landed: chunk 0's scores exist, so
+          // the MMAs have read them -- the stage's full barrier lives in the pair's
+          // leader CTA; resident: the stage is released only after this read,
+          // below), plus 2 eps (>= |t~_p - t_p| + fp32 error).
+          // With the threshold tight from the first batch, a batch needs the mask
+          // pass only where a candidate lies -- the warp skips it otherwise.
+          // (computed once per point by scan group 0, shared through shared memory)
+          if (g == 0) {
+            float m0 = __int_as_float(0x7f800000);
+            if (valid) {
+              const int kp = min(max(assign[row], 0), K - 1);
+              const uint8_t* arow = sa + (it % KT_STAGES) * KT_A + pl * 128;
+              const float4* cp = reinterpret_cast<const float4*>(cent + static_cast<int64_t>(kp) * KT_D);
+              float dot = 0.f;
+#pragma unroll
+              for (int q4 = 0; q4 < 4; ++q4) {  // 16-byte chunks q4 (xh) and q4 + 4 (xl), SWIZZLE_128B
+                const uint4 hv = *reinterpret_cast<const uint4*>(arow + ((q4 ^ (pl & 7)) << 4));
+                const uint4 lv = *reinterpret_cast<const uint4*>(arow + (((q4 + 4) ^ (pl & 7)) << 4));
+                const uint32_t hw[4] = {hv.x, hv.y, hv.z, hv.w}, lw[4] = {lv.x, lv.y, lv.z, lv.w};
+                const float4 c0 = __ldg(cp + 2 * q4), c1 = __ldg(cp + 2 * q4 + 1);
+                const float cc[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  const float x0 = __uint_as_float(hw[e] << 16) + __uint_as_float(lw[e] << 16);
+                  const float x1 = __uint_as_float(hw[e] & 0xffff0000u) + __uint_as_float(lw[e] & 0xffff0000u);
+                  dot = fmaf(x0, cc[2 * e], dot);
+                  dot = fmaf(x1, cc[2 * e + 1], dot);
+                }
+              }
+              m0 = fmaf(-2.f, dot, __ldg(qnorm + kp)) + two_eps;
+            }
+            seeds[buf * KT_ROWS + pl] = m0;  // double-buffered by tile parity
+          }
+          epi_bar();  // every scan warp: the seeds of this tile are written
+          // the A rows are read: the stage may be refilled (with K <= 512 the MMAs
+          // release it before the scan starts, so the producer also waits for this)
+          if (warp == 0 && lane == 0) ptx::mbar_arrive(&empty[it % KT_STAGES]);
+          m = seeds[buf * KT_ROWS + pl];
+        }
         const uint32_t tbase = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) +
                                static_cast<uint32_t>(acc * KT_CW + g * KT_GCOLS);
 #pragma unroll
@@ -326,6 +371,7 @@ __global__ void __launch_bounds__(KT_THREADS, 1)
           const float bmin = min3f(h0, h1, fminf(h2, h3));
           m = fminf(m, bmin);
           const float thr = m + two_eps;
+          if (__any_sync(0xffffffffu, bmin <= thr))
           // candidate mask: set.le gives exact 1.0/0.0 flags (one ALU op per
           // score) that FFMAs (the FMA pipe) weigh by 2^j into exact integers
           // below 2^24, read back from the float bits. A batch with candidates
@@ -690,9 +736,10 @@ uint64_t rows_split(const int64_t* s, uint32_t) { return static_cast<uint64_t>(s
 }  // namespace
 
 void register_kmeans_tc(std::vector<KernelDef>& r) {
-  constexpr uint8_t S = HCL_ARG_SCALAR, I = HCL_ARG_IN, O = HCL_ARG_OUT;
+  constexpr uint8_t S = HCL_ARG_SCALAR, I = HCL_ARG_IN, O = HCL_ARG_OUT, IO = HCL_ARG_INOUT;
   constexpr uint8_t N = HCL_PART_NONE, P = HCL_PART_REPLICATE, X = HCL_PART_SPLIT_ROWS;
-  r.push_back({"b200", "kmeans_assign_tc", {I, I, I, I, O, S, S, S}, {X, X, X, P, X, N, N, N}, launch_assign_tc,
+  // assign is INOUT: the previous assignment seeds each point's threshold
+  r.push_back({"b200", "kmeans_assign_tc", {I, I, I, I, IO, S, S, S}, {X, X, X, P, X, N, N, N}, launch_assign_tc,
                nullptr, rows_tc});
   r.push_back({"b200", "kmeans_split_points", {I, O, O, S, S}, {X, X, X, N, N}, launch_split_points, nullptr,
                rows_split});

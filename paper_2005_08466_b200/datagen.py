@@ -166,3 +166,13 @@ def pagerank_bins(row_ptr: np.ndarray, col_idx: np.ndarray, lo: int = 0, hi: int
     finally:
         N.lib().hcl_pagerank_bins_free(h)
     return out
+
+
+def counting_order(keys: np.ndarray, k: int) -> np.ndarray:
+    """Stable order of keys in [0, k) (hcl_counting_order): int32 indices."""
+    keys = np.ascontiguousarray(keys, np.int32)
+    perm = np.empty(len(keys), np.int32)
+    rc = N.lib().hcl_counting_order(keys.ctypes.data, len(keys), k, perm.ctypes.data)
+    if rc != 0:
+        raise N.HaoclError(rc - N.HCL_ERR_BASE, "counting_order: keys outside [0, k)")
+    return perm

@@ -42,6 +42,16 @@ class KMeans:
         self.k_acc = ctx.create_kernel(prog, "kmeans_accumulate")
         self.k_fin = ctx.create_kernel(prog, "kmeans_finalize")
         self.k_check = ctx.create_kernel(prog, "kmeans_check_points")
+        if tensor_filter:
+            self.b_split, self.b_xx = mk(n * 128), mk(n * 4)
+            self.k_split = ctx.create_kernel(prog, "kmeans_split_points")
+            self.k_assign_tc = ctx.create_kernel(prog, "kmeans_assign_tc")
+        self.perm = None  # stored row i holds the caller's point perm[i] (order_by_cluster)
+        self._bind()
+
+    def _bind(self) -> None:
+        """(Re)bind every kernel to the current buffers."""
+        ctx, n, d, k = self.ctx, self.n, self.d, self.k
         for j, a in enumerate([self.b_pts, n, d]):
             ctx.set_kernel_arg(self.k_check, j, a)
         for j, a in enumerate([self.b_pts, self.b_cent, self.b_assign, n, d, k]):
@@ -50,14 +60,53 @@ class KMeans:
             ctx.set_kernel_arg(self.k_acc, j, a)
         for j, a in enumerate([self.b_sums, self.b_counts, self.b_cent, k, d]):
             ctx.set_kernel_arg(self.k_fin, j, a)
-        if tensor_filter:
-            self.b_split, self.b_xx = mk(n * 128), mk(n * 4)
-            self.k_split = ctx.create_kernel(prog, "kmeans_split_points")
-            self.k_assign_tc = ctx.create_kernel(prog, "kmeans_assign_tc")
+        if self.tensor_filter:
             for j, a in enumerate([self.b_pts, self.b_split, self.b_xx, n, d]):
                 ctx.set_kernel_arg(self.k_split, j, a)
             for j, a in enumerate([self.b_pts, self.b_split, self.b_xx, self.b_cent, self.b_assign, n, d, k]):
                 ctx.set_kernel_arg(self.k_assign_tc, j, a)
+
+    def order_by_cluster(self, parts=None) -> None:
+        """Store the points grouped by their current nearest centroid (a layout
+        transform; results are mapped back to the caller's order). The
+        tensor-filtered assignment then sees warps of nearby points that share
+        their candidate centroids, and skips the candidate-mask pass warp-wide
+        wherever no point of the warp has a candidate. parts: [(queue, lo, hi)]
+        (default: this object's queues and bounds). Sums, counts and centroids
+        are order-free (exact int64 sums): every result is unchanged."""
+        from .datagen import counting_order
+
+        ctx, n, d = self.ctx, self.n, self.d
+        if parts is None:
+            parts = [(q, self.bounds[i], self.bounds[i + 1]) for i, q in enumerate(self.queues)
+                     if self.bounds[i + 1] > self.bounds[i]]
+        k_asg = self.k_assign_tc if self.tensor_filter else self.k_assign
+        for q, lo, hi in parts:
+            ctx.enqueue_ndrange_range(q, k_asg, (n, 1, 1), 1, lo, hi - lo)
+        new_perm = np.arange(n, dtype=np.int32) if self.perm is None else self.perm.copy()
+        b_perm, b_new = ctx.create_buffer(n * 4), ctx.create_buffer(n * d * 4)
+        kg = ctx.create_kernel(ctx.create_program("b200"), "kmeans_gather_points")
+        for j, a in enumerate([self.b_pts, b_perm, b_new, n, d]):
+            ctx.set_kernel_arg(kg, j, a)
+        for q, lo, hi in parts:
+            ctx.finish(q)
+            a = ctx.enqueue_read_buffer(q, self.b_assign, offset=lo * 4, length=(hi - lo) * 4).view(np.int32)
+            order = counting_order(a, self.k)  # stable: within a cluster the stored order stays
+            ctx.enqueue_write_buffer(q, b_perm, (order + lo).astype(np.int32), offset=lo * 4)
+            ctx.enqueue_write_buffer(q, self.b_assign, np.ascontiguousarray(a[order]), offset=lo * 4)
+            new_perm[lo:hi] = new_perm[lo:hi][order]
+            ctx.enqueue_ndrange_range(q, kg, (n, 1, 1), 1, lo, hi - lo)
+        for q, _, _ in parts:
+            ctx.finish(q)
+        ctx.release(self.b_pts)
+        ctx.release(b_perm)
+        ctx.release(kg)
+        self.b_pts = b_new
+        self.perm = new_perm
+        self._bind()
+        if self.tensor_filter:
+            for q, lo, hi in parts:
+                ctx.enqueue_ndrange_range(q, self.k_split, (n, 1, 1), 1, lo, hi - lo)
 
     def _split(self) -> None:
         if self.tensor_filter:  # the bf16 split rows and |x|^2 of the resident points (once)
@@ -128,8 +177,14 @@ class KMeans:
         return self.ctx.enqueue_read_buffer(self.queues[0], self.b_cent).view(np.float32).reshape(self.k, self.d)
 
     def assignments(self) -> np.ndarray:
+        """Assignments in the caller's point order."""
         self.finish()
-        return self.ctx.enqueue_read_buffer(self.queues[0], self.b_assign).view(np.int32)
+        a = self.ctx.enqueue_read_buffer(self.queues[0], self.b_assign).view(np.int32)
+        if self.perm is None:
+            return a
+        out = np.empty_like(a)
+        out[self.perm] = a
+        return out
 
     def sums(self):
         self.finish()

@@ -232,3 +232,32 @@ def test_full_size_c4_sampled_parity(ctx, queues):
                                   {6: q * 4, 7: q * 8}, threads=os.cpu_count() or 1)
     assert rc == 0 and work == d * k * q
     assert (out[6].view(np.int32) == np.concatenate(sample_got)).all()
+
+
+@pytest.mark.parametrize("P,tc", [(1, True), (2, True), (3, False)])
+def test_order_by_cluster_keeps_every_result(ctx, queues, P, tc):
+    """order_by_cluster stores the points grouped by nearest centroid (per
+    part); assignments map back to the caller's order and every result --
+    assignments, int64 sums, centroids -- stays bit-identical to the oracle."""
+    from paper_2005_08466_b200.kmeans import KMeans
+
+    n, d, k = 30011, 32, 256
+    pts = G.gen_kmeans_points(n, d, k, 44)
+    cent0 = pts[: k * d].copy()
+    a_want, s_want, c_want, cent_want = oracle_iterations(pts, n, d, k, cent0, 3)
+    km = KMeans(ctx, queues[:P], n, d, k, tensor_filter=tc)
+    km.load_points(pts)
+    km.set_centroids(cent0)
+    km.iterate(1)
+    km.order_by_cluster()
+    assert sorted(km.perm.tolist()) == list(range(n))
+    km.iterate(1)
+    km.assign_only()
+    got_a = km.assignments()
+    km.iterate(1)
+    s, c = km.sums()
+    cent = km.centroids()
+    km.close()
+    assert (got_a == a_want).all()
+    assert (s == s_want).all() and (c == c_want).all()
+    assert cent.tobytes() == cent_want.reshape(k, d).tobytes()
