@@ -142,11 +142,15 @@ class Dist:
         if self.world > 1 and backend:
             import torch.distributed as d
 
+            import datetime
+
+            # a rank that diverges should fail the run in minutes, not hold every GPU for NCCL's default 10
+            timeout = datetime.timedelta(seconds=int(os.environ.get("BENCH_PG_TIMEOUT_S", "240")))
             if backend == "nccl":
                 torch.cuda.set_device(self.local)
-                d.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+                d.init_process_group("nccl", device_id=torch.device("cuda", self.local), timeout=timeout)
             else:
-                d.init_process_group("gloo")
+                d.init_process_group("gloo", timeout=timeout)
             self.d = d
         self.dev = "cuda" if backend == "nccl" else "cpu"
 
@@ -1076,7 +1080,7 @@ def run_reference(args):
     return 0
 
 
-def measure(wl, args, dist, sampler=None, cpu_seconds=10.0):
+def measure(wl, args, dist, sampler=None, cpu_seconds=10.0, hold=True):
     """W warm-up steps, then K timed steps (CUDA events on the runtime's
     stream, max over ranks), the dominant kernel alone, and the e2e loop through
     the public API with host buffers. Returns the JSON line (rank 0) or None."""
@@ -1119,7 +1123,8 @@ def measure(wl, args, dist, sampler=None, cpu_seconds=10.0):
     # clock hold: a timed region shorter than ~3 nvidia-smi samples is followed by
     # the same steps, untimed, until the sampler has seen them under load
     hold_ms, t_hold = 0.0, time.time()
-    need_hold = sampler is not None and dist.allmax(1.0 if sampler and sampler.count() < 3 else 0.0) > 0
+    # (every rank takes part in these reductions; only rank 0 samples)
+    need_hold = hold and dist.allmax(1.0 if sampler and sampler.count() < 3 else 0.0) > 0
     while need_hold:
         for _ in range(max(1, args.steps)):
             wl.step()
@@ -1220,7 +1225,7 @@ def run_b200(args):
             t0 = time.perf_counter()
             try:
                 w = WORKLOADS[name](sub, dist)
-                r = measure(w, sub, dist, None, cpu_seconds=3.0)
+                r = measure(w, sub, dist, None, cpu_seconds=3.0, hold=False)
                 w.ctx.close()
                 del w
                 torch.cuda.empty_cache()
