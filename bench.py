@@ -170,6 +170,9 @@ class Dist:
     def allmax(self, x):
         return self._red(x, self.d.ReduceOp.MAX if self.d else None)
 
+    def allmin(self, x):
+        return self._red(x, self.d.ReduceOp.MIN if self.d else None)
+
     def allsum(self, x):
         return self._red(x, self.d.ReduceOp.SUM if self.d else None)
 
@@ -658,19 +661,27 @@ class PageRankW(Workload):
             uid = d.bcast_bytes(HostContext.nccl_unique_id() if d.rank == 0 else None)
             ctx.init_collectives(q, d.rank, d.world, uid)
         self.b_xs2 = [mk(self.v * 4), mk(self.v * 4)]
-        handles = d.allgather_bytes(b"".join(ctx.share_buffer(q, b) for b in self.b_xs2)) if d.world > 1 else None
         self.b_dsum2 = [mk(8), mk(8)]
         self.b_peers = []
-        for i in range(2):  # b_peers[i]: the peers' copies of xs2[i]
-            addrs = [ctx.open_shared_buffer(q, handles[r][64 * i:64 * (i + 1)], self.v * 4)
-                     for r in range(d.world) if r != d.rank] if d.world > 1 else []
-            arr = np.array(addrs or [0], np.uint64)
-            bp = mk(arr.nbytes)
-            ctx.enqueue_write_buffer(q, bp, arr)
-            self.b_peers.append(bp)
+        # xs' reaches the other ranks either through one NVSwitch multicast store per row
+        # (BENCH_PR_MCAST=1, default: symmetric-memory xs' buffers, egress 4 B/row) or
+        # through a store per peer into its IPC-mapped xs' (egress 4 (N-1) B/row)
+        self.mcast = d.world > 1 and os.environ.get("BENCH_PR_MCAST", "1") == "1" and self.bind_multicast()
+        if self.mcast:
+            n_peers = -1
+        else:
+            n_peers = d.world - 1
+            handles = d.allgather_bytes(b"".join(ctx.share_buffer(q, b) for b in self.b_xs2)) if d.world > 1 else None
+            for i in range(2):  # b_peers[i]: the peers' copies of xs2[i]
+                addrs = [ctx.open_shared_buffer(q, handles[r][64 * i:64 * (i + 1)], self.v * 4)
+                         for r in range(d.world) if r != d.rank] if d.world > 1 else []
+                arr = np.array(addrs or [0], np.uint64)
+                bp = mk(arr.nbytes)
+                ctx.enqueue_write_buffer(q, bp, arr)
+                self.b_peers.append(bp)
         # kernel i reads xs[i], dsum[i]; writes x rows, xs[1-i] (here + peers), dsum[1-i]
         self.k_stepx = [self.bl.kernel(self.v, self.b_xs2[i], self.b_dsum2[i], self.b_x[0], self.b_peers[1 - i],
-                                       d.world - 1, self.b_inv, self.b_xs2[1 - i], self.b_dsum2[1 - i])
+                                       n_peers, self.b_inv, self.b_xs2[1 - i], self.b_dsum2[1 - i])
                         for i in range(2)]
         prog = ctx.create_program("b200")
         self.k_prep0 = ctx.create_kernel(prog, "pagerank_prep")  # x0 -> xs[0], dsum[0]
@@ -689,6 +700,37 @@ class PageRankW(Workload):
         self.check = float(abs(d.allsum(float(x.astype(np.float64).sum())) - 1.0))
         assert self.check <= 1e-3, f"pagerank binned parity guard: mass {self.check}"
         self.reset()
+        if os.environ.get("BENCH_PR_RANK_TIMES") == "1":  # diagnostics: per-rank kernel time
+            print(f"rank {d.rank}: rows {self.rows} nnz {self.nnz_local} binned step "
+                  f"{self.rank_kernel_ms():.4f} ms", file=sys.stderr, flush=True)
+            self.reset()
+
+    def bind_multicast(self):
+        """Back xs'[0], xs'[1] with torch symmetric memory (one allocation per rank,
+        mapped into an NVSwitch multicast object) and hand the kernels the multicast
+        addresses; False (IPC peer stores instead) when the fabric has no multicast."""
+        import numpy as np
+        import torch
+        import torch.distributed._symmetric_memory as symm_mem
+
+        d, ctx, q = self.dist, self.ctx, self.q
+        self.symm = []
+        for i in range(2):
+            t = symm_mem.empty(self.v, dtype=torch.float32, device=torch.device("cuda", d.local))
+            t.zero_()
+            h = symm_mem.rendezvous(t, d.d.group.WORLD.group_name)
+            self.symm.append((t, h))
+        ok = all(h.multicast_ptr for _, h in self.symm)
+        if not d.allmin(float(ok)):
+            self.symm = []
+            return False
+        torch.cuda.synchronize()
+        for i, (t, h) in enumerate(self.symm):
+            ctx.bind_external(q, self.b_xs2[i], t.data_ptr())
+            bp = ctx.create_buffer(8)
+            ctx.enqueue_write_buffer(q, bp, np.array([h.multicast_ptr], np.uint64))
+            self.b_peers.append(bp)
+        return True
 
     def reset(self):
         ctx, q = self.ctx, self.q
@@ -784,6 +826,8 @@ class PageRankW(Workload):
                     "layout_build_s": round(self.layout_s, 2),
                     "algorithmic_bytes_per_iteration": self.work_per_step(), "rank_sum_err": self.check,
                     "row_cost_nnz_per_row": self.row_cost,
+                    "xs_exchange": ("NVSwitch multicast store (symmetric memory)" if self.mcast else
+                                    "IPC peer stores" if self.dist.world > 1 else "none (one rank)"),
                     "l2": "2.35 GB algorithmic (~3.6 GB moved) per iteration > L2"}
         return {"workload": f"PageRank iteration (C3): R-MAT scale {self.scale}, {self.e} edges, int32/fp32 pull CSR, "
                             f"nnz-balanced rows over {self.dist.world} rank(s), " + (

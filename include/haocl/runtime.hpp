@@ -295,6 +295,12 @@ class HostContext {
   // after which `completed` buffers are whole on the queue's device (the
   // peers' stores filled the rows this rank did not write).
   std::vector<uint8_t> share_buffer(Handle queue, Handle buffer);
+  // Back `buffer` on the queue's device with caller-owned device memory of at
+  // least its size (no copy; the caller keeps ownership and must keep it alive
+  // until the buffer is released). Bound as the buffer's whole allocation with
+  // nothing valid yet -- e.g. a symmetric-memory tensor whose NVSwitch
+  // multicast address a kernel stores through (pagerank_step_binned).
+  void bind_external(Handle queue, Handle buffer, uint64_t device_ptr);
   uint64_t open_shared_buffer(Handle queue, const std::vector<uint8_t>& ipc_handle, uint64_t bytes);
   void enqueue_barrier(Handle queue, const std::vector<Handle>& completed = {});
 

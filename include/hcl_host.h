@@ -82,6 +82,9 @@ int hcl_ctx_share_buffer(hcl_context* ctx, uint64_t queue, uint64_t buffer, uint
 int hcl_ctx_open_shared_buffer(hcl_context* ctx, uint64_t queue, const uint8_t* ipc_handle, uint64_t bytes,
                                uint64_t* device_address);
 int hcl_ctx_enqueue_barrier(hcl_context* ctx, uint64_t queue, const uint64_t* completed, int n);
+/* Back a buffer on the queue's device with caller-owned device memory (>= its
+ * size; e.g. a symmetric-memory allocation with an NVSwitch multicast mapping). */
+int hcl_ctx_bind_external(hcl_context* ctx, uint64_t queue, uint64_t buffer, uint64_t device_ptr);
 /* The row boundaries (nqueues+1) the partitioned launch would use. */
 int hcl_ctx_partition_plan(hcl_context* ctx, uint64_t kernel, const uint64_t global[3], const uint64_t* queues,
                            int nqueues, const uint64_t* weights, uint64_t* bounds);

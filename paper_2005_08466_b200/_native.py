@@ -106,6 +106,7 @@ HOST = [
     ("hcl_ctx_enqueue_allreduce_sum_i64", C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64]),
     ("hcl_ctx_enqueue_broadcast", C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_int]),
     ("hcl_ctx_share_buffer", C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_void_p]),
+    ("hcl_ctx_bind_external", C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint64]),
     ("hcl_ctx_open_shared_buffer", C.c_int, [C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64, u64p]),
     ("hcl_ctx_enqueue_barrier", C.c_int, [C.c_void_p, C.c_uint64, u64p, C.c_int]),
     ("hcl_ctx_partition_plan", C.c_int, [C.c_void_p, C.c_uint64, u64p, u64p, C.c_int, u64p, u64p]),

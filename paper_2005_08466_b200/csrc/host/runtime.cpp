@@ -944,6 +944,20 @@ std::vector<uint8_t> HostContext::share_buffer(Handle queue, Handle buffer) {
   return h;
 }
 
+void HostContext::bind_external(Handle queue, Handle buffer, uint64_t device_ptr) {
+  std::lock_guard lock(impl_->mu);
+  Impl::QueueRec& q = impl_->queue(queue.id);
+  Impl::BufferRec& b = impl_->buffer(buffer.id);
+  if (!device_ptr) fail(ErrorCode::argument, "bind_external: null device pointer");
+  check(hcl_buffer_bind_external(impl_->dev_index(q.gid), buffer.id, reinterpret_cast<void*>(device_ptr), 0, b.size));
+  Impl::Piece& p = b.pieces[q.gid];
+  p.allocated = true;
+  p.alloc_first = 0;
+  p.alloc_bytes = b.size;
+  p.valid.clear();
+  impl_->trace.record({q.gid, "alloc_buffer", buffer.id});
+}
+
 uint64_t HostContext::open_shared_buffer(Handle queue, const std::vector<uint8_t>& ipc_handle, uint64_t bytes) {
   std::lock_guard lock(impl_->mu);
   Impl::QueueRec& q = impl_->queue(queue.id);
@@ -1329,6 +1343,11 @@ int hcl_ctx_open_shared_buffer(hcl_context* ctx, uint64_t queue, const uint8_t* 
   return ctx_guarded([&] {
     *device_address = ctx->ctx.open_shared_buffer(H(HandleKind::queue, queue),
                                                   std::vector<uint8_t>(ipc_handle, ipc_handle + 64), bytes);
+  });
+}
+int hcl_ctx_bind_external(hcl_context* ctx, uint64_t queue, uint64_t buffer, uint64_t device_ptr) {
+  return ctx_guarded([&] {
+    ctx->ctx.bind_external(H(HandleKind::queue, queue), H(HandleKind::buffer, buffer), device_ptr);
   });
 }
 int hcl_ctx_enqueue_barrier(hcl_context* ctx, uint64_t queue, const uint64_t* completed, int n) {

@@ -113,16 +113,27 @@ struct Fanout {
   int n;
   float* xs;            // this device's xs'
   const float* inv;     // fl(1/outdeg), 0 for dangling vertices
+  float* mc;            // NVSwitch multicast address of xs' on every rank (n_peers == PR_MULTICAST), else null
 };
+
+// n_peers == PR_MULTICAST: peers[0] is the multicast mapping of the ranks' xs'
+// buffers (one store reaches every GPU through the switch: the egress per row
+// is 4 bytes whatever the rank count, not 4 * (N - 1))
+constexpr int PR_MULTICAST = -1;
 
 __device__ __forceinline__ Fanout load_fanout(const unsigned long long* peers, int n, float* xs, const float* inv) {
   Fanout f;
-  f.n = n;
+  f.mc = n == PR_MULTICAST ? reinterpret_cast<float*>(__ldg(peers)) : nullptr;
+  f.n = n < 0 ? 0 : n;
   f.xs = xs;
   f.inv = inv;
 #pragma unroll
-  for (int k = 0; k < PR_MAX_PEERS; ++k) f.p[k] = k < n ? reinterpret_cast<float*>(__ldg(peers + k)) : nullptr;
+  for (int k = 0; k < PR_MAX_PEERS; ++k) f.p[k] = k < f.n ? reinterpret_cast<float*>(__ldg(peers + k)) : nullptr;
   return f;
+}
+
+__device__ __forceinline__ void multimem_st(float* mc, float v) {
+  asm volatile("multimem.st.relaxed.sys.global.f32 [%0], %1;" ::"l"(mc), "f"(v) : "memory");
 }
 
 template <bool UPDATE, bool XCH>
@@ -132,7 +143,8 @@ __device__ __forceinline__ void pr_store_x(float* __restrict__ y, int r, int lo,
   if constexpr (XCH) {
     const float inv = __ldg(f.inv + r);  // the division is done once per graph, not per step
     const float xs = __fmul_rn(inv, v);
-    f.xs[r] = xs;
+    f.xs[r] = xs;  // (the multicast store lands here too, the same value)
+    if (f.mc) multimem_st(f.mc + r, xs);
 #pragma unroll
     for (int k = 0; k < PR_MAX_PEERS; ++k)
       if (k < f.n) f.p[k][r] = xs;
@@ -867,8 +879,8 @@ uint64_t launch_pr_binned(LaunchCtx& c) {
   if (XS.bytes != static_cast<uint64_t>(v) * 4 || OD.bytes != static_cast<uint64_t>(v) * 4 ||
       XN.bytes != static_cast<uint64_t>(v) * 4 || D.bytes != 8 || DN.bytes != 8)
     fail(ErrorCode::argument, std::string(what) + ": xs, inv_outdeg, xs' must hold V floats, dsum/dsum' one uint64");
-  if (n_peers < 0 || n_peers > PR_MAX_PEERS || PB.bytes < static_cast<uint64_t>(n_peers) * 8)
-    fail(ErrorCode::argument, std::string(what) + ": peers must list 0..7 device addresses");
+  if (n_peers < PR_MULTICAST || n_peers > PR_MAX_PEERS || PB.bytes < static_cast<uint64_t>(n_peers < 0 ? 1 : n_peers) * 8)
+    fail(ErrorCode::argument, std::string(what) + ": peers must list 0..7 device addresses (or -1: one multicast address)");
   uint64_t lo, rows;
   sub_range(c, static_cast<uint64_t>(v), lo, rows, what);
   float* y = at_byte<float>(buffer_arg(c, 9, what), lo * 4, rows * 4, what);

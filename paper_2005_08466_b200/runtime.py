@@ -240,6 +240,12 @@ class HostContext:
         check(self._L.hcl_ctx_share_buffer(self._ctx, queue.id, buffer.id, h))
         return bytes(h)
 
+    def bind_external(self, queue: Handle, buffer: Handle, device_ptr: int) -> None:
+        """Back `buffer` on the queue's device with caller-owned device memory
+        (>= the buffer's size, kept alive by the caller until release), e.g. a
+        torch symmetric-memory tensor whose multicast address a kernel stores to."""
+        check(self._L.hcl_ctx_bind_external(self._ctx, queue.id, buffer.id, device_ptr))
+
     def open_shared_buffer(self, queue: Handle, ipc_handle: bytes, nbytes: int) -> int:
         """Map a peer rank's shared buffer on the queue's device; returns its device
         address (what pagerank_step_exchange's peers list holds)."""

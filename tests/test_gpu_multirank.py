@@ -4,8 +4,9 @@ oracle. Skipped on a single-GPU box; run by `gpurun --gpus 2|4`.
 
 * PageRank, binned step (default) and the pull fused step: rows split over the
   ranks, each rank's gather epilogue stores the next gather input into every
-  rank's IPC-mapped xs' over NVLink, an 8-byte NCCL allreduce of the dangling
-  sums per step. 20 iterations, the ranks' rows gathered: bit-identical to the
+  rank's xs' -- one NVSwitch multicast store per row into symmetric memory
+  (binned, default) or a store per peer into its IPC-mapped xs' (binned_ipc,
+  pull) -- and an 8-byte NCCL allreduce of the dangling sums per step. 20 iterations, the ranks' rows gathered: bit-identical to the
   oracle's restatement (fixed-point order for binned, warp-unit order for pull).
 * k-means: points split over the ranks, int64 NCCL allreduce of sums and
   counts; centroids after 2 iterations bit-identical to the oracle.
@@ -55,9 +56,10 @@ def _worker(rank, world, port, case, q):
         q.put(("error", f"rank {rank}: {type(e).__name__}: {e}\n{traceback.format_exc()}"))
 
 
-def _pagerank(bench, dist, args, kernel):
+def _pagerank(bench, dist, args, kernel, mcast="1"):
     os.environ["BENCH_PR_SCALE"] = "14"
     os.environ["BENCH_PR_KERNEL"] = kernel
+    os.environ["BENCH_PR_MCAST"] = mcast
     wl = bench.PageRankW(args, dist)
     wl.setup()
     wl.reset()
@@ -97,6 +99,7 @@ def _gemm(bench, dist, args):
 
 _CASES = {
     "pagerank_binned": lambda b, d, a: _pagerank(b, d, a, "binned"),
+    "pagerank_binned_ipc": lambda b, d, a: _pagerank(b, d, a, "binned", mcast="0"),
     "pagerank_pull": lambda b, d, a: _pagerank(b, d, a, "pull"),
     "kmeans": _kmeans,
     "gemm": _gemm,
@@ -127,7 +130,7 @@ def _run(case):
     return world, payload
 
 
-@pytest.mark.parametrize("kernel", ["binned", "pull"])
+@pytest.mark.parametrize("kernel", ["binned", "binned_ipc", "pull"])
 def test_pagerank_exchange_multirank(kernel):
     import oracle as O
     from paper_2005_08466_b200 import datagen as G
@@ -139,7 +142,7 @@ def test_pagerank_exchange_multirank(kernel):
         lo = int(np.frombuffer(p[:8], np.int64)[0])
         rows = np.frombuffer(p[8:], np.float32)
         x[lo:lo + len(rows)] = rows
-    want = O.pagerank(rp, ci, val, deg, 20, b200_order="fixed" if kernel == "binned" else True)
+    want = O.pagerank(rp, ci, val, deg, 20, b200_order="fixed" if kernel.startswith("binned") else True)
     assert x.tobytes() == want.tobytes(), f"{world} ranks"
 
 
