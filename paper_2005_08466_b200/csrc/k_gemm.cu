@@ -632,12 +632,17 @@ uint64_t launch_gemm_f32x3(LaunchCtx& c) {
   float* cp = at_byte<float>(Cb, lo * n * 4, rows * n * 4, "gemm_f32x3 C");
   if (rows == 0) return 0;
   const int64_t r = static_cast<int64_t>(rows);
-  // optional K split (HCL_GEMM_KSPLIT = slices; a function of N and K only, so every row
-  // partition of one GEMM sums in the same order; slices reduced in order). Measured at
-  // C1 (1024^3): 51 us per launch unsplit, 52 us with 2 slices, 58 us with 4 -- the split
-  // kernels and launch gaps dominate at this size, so the default is unsplit.
+  // K split (slices of K' = 3K reduced in slice order, fp32 round-to-nearest). The
+  // tensor core's fp32 accumulation truncates per MMA, so its error grows with the
+  // accumulation length: each halving of K' per slice halves it (C1, 1024^3, measured
+  // normwise: 2^-18.8 unsplit, 2^-19.9 with 2 slices, 2^-20.8 with 4, 2^-22.0 with 8).
+  // Default: slices of ~768 K' (at most 4) when the fp32 slice workspace stays small
+  // (M N <= 2^24); HCL_GEMM_KSPLIT overrides. A function of M, N and K only, so every
+  // row partition of one GEMM sums in the same order (P-invariance).
   const int64_t nkb = ceil_div(3 * k, 32);
-  const int ksplit = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(env_int("HCL_GEMM_KSPLIT", 1), nkb)));
+  const int64_t ks_default = m * n <= (int64_t(1) << 24) ? std::max<int64_t>(1, std::min<int64_t>(4, 3 * k / 768)) : 1;
+  const int ksplit = static_cast<int>(
+      std::max<int64_t>(1, std::min<int64_t>(env_int("HCL_GEMM_KSPLIT", static_cast<int>(ks_default)), nkb)));
   const size_t a3_bytes = static_cast<size_t>(r * 3 * k * 4);
   const size_t b3_bytes = static_cast<size_t>(n * 3 * k * 4);
   const size_t ws_bytes = ksplit > 1 ? static_cast<size_t>(ksplit) * r * n * 4 : 0;

@@ -12,7 +12,10 @@ err_ij = |C - C64|_ij / (|A| |B|)_ij. Tolerances (stated here, per path):
   3xTF32 (gemm_f32x3)    : 2^-16   (the FAST fp32 path, not fp32-exact: exact
                                     split products, but the tensor core's fp32
                                     accumulation truncates per MMA; measured
-                                    2^-18.8 at K=1024, 2^-17.1 at K=16384)
+                                    2^-18.8 at K=1024 unsplit, 2^-17.1 at
+                                    K=16384) -- and 2^-20 at C1 (1024^3), where
+                                    the default K split into 4 slices summed
+                                    in order (2^-20.8 measured) applies
 plus bit-identity of C across partitions P in {1,2,4} (P-invariance). The
 full-size C2 samples are checked against the reference library's own
 kernels::execute("matmul") (oracle/_ref, proj/src/kernels.cpp:96-119)."""
@@ -164,7 +167,10 @@ def test_gemm_f32x3(ctx, queues, m, n, k):
     a = O.gen_doubles(m * k, 42).astype(np.float32)
     b = O.gen_doubles(k * n, 43).astype(np.float32)
     c = gemm(ctx, queues, "gemm_f32x3", a, b, m, k, n)
-    assert normwise_err(c, a.astype(np.float64).reshape(m, k), b.astype(np.float64).reshape(k, n)) <= 2.0**-16
+    err = normwise_err(c, a.astype(np.float64).reshape(m, k), b.astype(np.float64).reshape(k, n))
+    assert err <= 2.0**-16
+    if (m, n, k) == (1024, 1024, 1024):  # C1: the default 4-slice K split meets §8(c)'s fp32 bound
+        assert err <= 2.0**-20
 
 
 @pytest.mark.parametrize("kernel", ["gemm_f32", "gemm_f32x3", "gemm_tf32"])
