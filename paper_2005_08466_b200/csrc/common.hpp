@@ -63,6 +63,10 @@ void cuda_check(cudaError_t e, const char* what, const char* file, int line);
 // gpu_launches). Kernel launch sites use HCL_LAUNCHED() right after <<<>>>.
 extern std::atomic<uint64_t> g_kernel_launches;
 extern thread_local uint64_t t_kernel_launches;  // this thread's share (graph capture counts)
+// Set by a caller that times its launches itself (the HostContext runtime records one
+// CUDA-event pair per part for the scheduler's rates): hcl_launch then skips its own
+// pair (each timing event record serializes the stream's front end, ~2.5 us a record).
+extern thread_local bool t_launch_untimed;
 #define HCL_LAUNCHED()                                            \
   do {                                                            \
     ::hcl::g_kernel_launches.fetch_add(1, std::memory_order_relaxed); \

@@ -24,6 +24,7 @@ namespace hcl {
 
 std::atomic<uint64_t> g_kernel_launches{0};
 thread_local uint64_t t_kernel_launches = 0;
+thread_local bool t_launch_untimed = false;
 
 const char* error_code_name(ErrorCode code) {
   switch (code) {
@@ -70,6 +71,7 @@ namespace {
 struct Dep {
   cudaEvent_t ev = nullptr;
   cudaStream_t st = nullptr;
+  cudaStream_t waited = nullptr;  // a stream already ordered after ev (its wait need not repeat)
 };
 
 struct GraphEntry {
@@ -137,10 +139,14 @@ struct Device {
   }
   // make `s` wait for the writer (and, for a write, the readers) of `a`
   void wait_for(DevAlloc& a, cudaStream_t s, bool write) {
-    if (a.last_write.ev && a.last_write.st != s) HCL_CUDA(cudaStreamWaitEvent(s, a.last_write.ev, 0));
+    auto wait = [&](Dep& d) {
+      if (!d.ev || d.st == s || d.waited == s) return;
+      HCL_CUDA(cudaStreamWaitEvent(s, d.ev, 0));
+      d.waited = s;  // later work on s is stream-ordered after this wait
+    };
+    wait(a.last_write);
     if (write)
-      for (Dep& r : a.reads)
-        if (r.st != s) HCL_CUDA(cudaStreamWaitEvent(s, r.ev, 0));
+      for (Dep& r : a.reads) wait(r);
   }
   // record that an operation on `s` just read / wrote `a`
   cudaEvent_t note(DevAlloc& a, cudaStream_t s, bool write) {
@@ -739,8 +745,13 @@ int hcl_launch(int dev, const char* kernel, const hcl_arg* args, uint32_t nargs,
     for (uint32_t i = 0; i < nargs; ++i)
       if (args[i].kind != HCL_ARG_SCALAR)
         d.wait_for(alloc_of(d, args[i].buffer_id, kernel), d.stream, args[i].kind != HCL_ARG_IN);
-    cudaEvent_t e0 = d.event(), e1 = d.event();
-    HCL_CUDA(cudaEventRecord(e0, d.stream));
+    const bool timed = !t_launch_untimed;  // hcl_finish's device_ms counts the timed launches
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (timed) {
+      e0 = d.event();
+      e1 = d.event();
+      HCL_CUDA(cudaEventRecord(e0, d.stream));
+    }
     uint64_t w = 0;
     if (k->graphable && graphs_enabled()) {
       // the second identical launch is captured into a CUDA graph, later ones replay it
@@ -775,8 +786,10 @@ int hcl_launch(int dev, const char* kernel, const hcl_arg* args, uint32_t nargs,
     } else {
       w = k->launch(c);
     }
-    HCL_CUDA(cudaEventRecord(e1, d.stream));
-    d.timed.emplace_back(e0, e1);
+    if (timed) {
+      HCL_CUDA(cudaEventRecord(e1, d.stream));
+      d.timed.emplace_back(e0, e1);
+    }
     for (uint32_t i = 0; i < nargs; ++i)
       if (args[i].kind == HCL_ARG_IN) d.note(alloc_of(d, args[i].buffer_id, kernel), d.stream, false);
     for (uint32_t i = 0; i < nargs; ++i)

@@ -30,6 +30,7 @@
 
 namespace hcl {
 void set_last_error(const std::string& m);
+extern thread_local bool t_launch_untimed;  // csrc/common.hpp
 }
 
 namespace haocl {
@@ -442,7 +443,9 @@ struct HostContext::Impl {
       uint64_t goff[3] = {part.lo, 0, 0};
       uint64_t gsz[3] = {part.hi - part.lo, global[1], global[2]};
       trace.record({part.gid, "launch_kernel", 0});
+      hcl::t_launch_untimed = true;  // l.start / l.stop time this part (one event pair, not two)
       int rc = hcl_launch(dev, k.name.c_str(), cargs.data(), n, goff, whole ? nullptr : gsz, dims, &l.work);
+      hcl::t_launch_untimed = false;
       cudaEventRecord(l.stop, static_cast<cudaStream_t>(stream));
       part_done.emplace_back(static_cast<cudaStream_t>(stream), l.stop);
       scheduler.note_complete(part.gid);
