@@ -713,6 +713,14 @@ __device__ __forceinline__ void reds_add_if(unsigned* p, unsigned v, bool pred) 
 // T threads per CTA, a stage of 8 T entries: T = 1024 with 16384-row bins (one
 // CTA per SM), T = 512 with <= 8192-row bins (two CTAs per SM)
 constexpr int PBG_STAGES = 2;
+// Row r of a bin accumulates at shared word pb_swz(r): the low 5 bits (the bank)
+// XOR-folded with bits 5-9 and 10-14, a bijection inside each 32-row block. R-MAT
+// ids are skewed toward 0 in every bit, so dst mod 32 alone puts ~25% of the
+// entries on bank 0: the busiest bank of an atomic instruction averages 4.1
+// lanes, folded 2.7 (scratch evaluation of the C3 layout). ncu at C3: 66.5M ->
+// 39.4M atomic wavefronts, gather 545 -> 481 us alone (issue-bound after); inside
+// the step the gather is memory-bound and gains ~2%.
+__device__ __forceinline__ int pb_swz(int r) { return r ^ ((r >> 5) & 31) ^ ((r >> 10) & 31); }
 template <int PBG_T>
 __global__ void __launch_bounds__(PBG_T) pr_bin_gather_kernel(const int64_t* __restrict__ part,
                                                              const int4* __restrict__ units,
@@ -735,7 +743,7 @@ __global__ void __launch_bounds__(PBG_T) pr_bin_gather_kernel(const int64_t* __r
   uint64_t* full = reinterpret_cast<uint64_t*>(stage0 + PBG_STAGES * PBG_STAGE_BYTES);
   uint64_t* empty = full + PBG_STAGES;
   unsigned* acc_lo = reinterpret_cast<unsigned*>(empty + PBG_STAGES);
-  unsigned* acc_hi = acc_lo + W;
+  unsigned* acc_hi = acc_lo + ((W + 31) & ~int64_t(31));  // whole 32-row blocks (pb_swz)
   const int4 U = __ldg(units + part[PB_UNIT0] + blockIdx.x);  // bin, e0, e1, slot
   const int64_t row0 = lo + static_cast<int64_t>(U.x) * W;
   const int64_t rem = hi - row0;
@@ -761,7 +769,7 @@ __global__ void __launch_bounds__(PBG_T) pr_bin_gather_kernel(const int64_t* __r
     ptx::fence_mbar_init();
     for (int64_t st = 0; st < min(n_st, static_cast<int64_t>(PBG_STAGES)); ++st) issue(st);
   }
-  for (int r = threadIdx.x; r < nrows; r += PBG_T) acc_lo[r] = acc_hi[r] = 0u;
+  for (int r = threadIdx.x; r < nrows; r += PBG_T) acc_lo[pb_swz(r)] = acc_hi[pb_swz(r)] = 0u;
   __syncthreads();
   for (int64_t st = 0; st < n_st; ++st) {
     const int b = static_cast<int>(st % PBG_STAGES);
@@ -792,9 +800,10 @@ __global__ void __launch_bounds__(PBG_T) pr_bin_gather_kernel(const int64_t* __r
         run = (k > 0 && dd[k] == dd[k - 1]) ? run + q : q;
         const bool last = k == 7 || dd[k] != dd[k + 1];
         const unsigned ql = static_cast<unsigned>(run);
-        const unsigned old = atoms_add_if(acc_lo + dd[k], ql, last && ql != 0u);
+        const int sw = pb_swz(static_cast<int>(dd[k]));
+        const unsigned old = atoms_add_if(acc_lo + sw, ql, last && ql != 0u);
         const unsigned qh = static_cast<unsigned>(run >> 32) + (old + ql < ql);  // carry out of the low word
-        if (__any_sync(0xffffffffu, last && qh != 0u)) reds_add_if(acc_hi + dd[k], qh, last && qh != 0u);
+        if (__any_sync(0xffffffffu, last && qh != 0u)) reds_add_if(acc_hi + sw, qh, last && qh != 0u);
       }
     }
     __syncwarp();
@@ -805,8 +814,9 @@ __global__ void __launch_bounds__(PBG_T) pr_bin_gather_kernel(const int64_t* __r
     }
   }
   __syncthreads();
-  auto acc = [&](int r) -> unsigned long long {
-    return (static_cast<unsigned long long>(acc_hi[r]) << 32) | acc_lo[r];
+  auto acc = [&](int r) -> unsigned long long {  // row r's sum
+    const int sw = pb_swz(r);
+    return (static_cast<unsigned long long>(acc_hi[sw]) << 32) | acc_lo[sw];
   };
   if (U.w >= 0) {  // a heavy bin split into units: combine in the slot, the last unit finishes the rows
     const int slot = static_cast<int>(part[PB_SLOT0]) + U.w;
@@ -822,8 +832,8 @@ __global__ void __launch_bounds__(PBG_T) pr_bin_gather_kernel(const int64_t* __r
     __threadfence();
     for (int r = threadIdx.x; r < nrows; r += PBG_T) {
       const unsigned long long a = __ldcg(sa + r);
-      acc_lo[r] = static_cast<unsigned>(a);
-      acc_hi[r] = static_cast<unsigned>(a >> 32);
+      acc_lo[pb_swz(r)] = static_cast<unsigned>(a);
+      acc_hi[pb_swz(r)] = static_cast<unsigned>(a >> 32);
       sa[r] = 0ull;  // the slot is zero again for the next step
     }
     if (threadIdx.x == 0) slot_cnt[slot] = 0u;
@@ -956,7 +966,8 @@ uint64_t launch_pr_binned(LaunchCtx& c) {
   // phase 2
   const bool small_bins = W <= 8192;
   const int gt = small_bins ? 512 : 1024;
-  const size_t smem2 = static_cast<size_t>(PBG_STAGES) * 8 * gt * 6 + 2 * PBG_STAGES * 8 + static_cast<size_t>(W) * 8;
+  const size_t smem2 = static_cast<size_t>(PBG_STAGES) * 8 * gt * 6 + 2 * PBG_STAGES * 8 +
+                       static_cast<size_t>((W + 31) & ~int64_t(31)) * 8;
   auto gkern = small_bins ? pr_bin_gather_kernel<512> : pr_bin_gather_kernel<1024>;
   HCL_CUDA(cudaFuncSetAttribute(gkern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem2)));
   const int64_t n_slots_total = static_cast<int64_t>(SA.bytes / (W * 8 + 4));
