@@ -334,6 +334,31 @@ class GemmBf16(Workload):
     def work_per_step(self):
         return 2.0 * self.S**3
 
+    def e2e_phases(self):
+        """One e2e step with a device sync after each phase (wall ms on this rank):
+        A rows + this rank's B slice H2D, the B allgather, the GEMM, C rows D2H."""
+        ctx, q, S, d = self.ctx, self.q, self.S, self.dist
+        k, bA, bB, bC = self.sets[0]
+        out = {}
+
+        def phase(name, fn):
+            d.barrier()
+            t = time.perf_counter()
+            fn()
+            ctx.finish(q)
+            out[name] = (time.perf_counter() - t) * 1e3
+
+        r, kb = d.rank, getattr(self, "kb", [0, S])
+        phase("h2d", lambda: (ctx.enqueue_write_buffer(q, bA, self.a_host, offset=self.lo * S * 2),
+                              ctx.enqueue_write_buffer(q, bB, self.b_host[kb[r] * S:kb[r + 1] * S] if d.world > 1
+                                                       else self.b_host, offset=kb[r] * S * 2 if d.world > 1 else 0)))
+        if d.world > 1:
+            phase("allgather", lambda: ctx.enqueue_allgather(q, bB, [x * S * 2 for x in kb]))
+        phase("gemm", lambda: ctx.enqueue_ndrange_range(q, k, (S, S, 1), 2, self.lo, self.rows))
+        phase("d2h", lambda: ctx.enqueue_read_buffer(q, bC, offset=self.lo * S * 2, length=self.rows * S * 2,
+                                                     out=self.c_hosts[0]))
+        return out
+
     def e2e_bytes(self):
         S = self.S  # all ranks together: A once, B once (sliced + NVLink allgather), C once
         return 2 * S * S * 2, S * S * 2
@@ -1222,6 +1247,9 @@ def measure(wl, args, dist, sampler=None, cpu_seconds=10.0, hold=True):
     wl.ctx.finish(wl.q)
     e2e_ms = dist.allmax((time.perf_counter() - t0) * 1e3)
     dist.barrier()
+    # the e2e step's phases one after the other (the reference's per-phase report,
+    # bench.cpp:179-200), max over ranks; untimed for the line
+    phases = {k: round(dist.allmax(v), 3) for k, v in wl.e2e_phases().items()} if hasattr(wl, "e2e_phases") else None
     clocks = sampler.stop() if sampler else None
     if clocks is not None:
         clocks["hold_ms"] = round(hold_ms, 1)  # untimed repeat of the steps while sampling (short regions)
@@ -1244,6 +1272,7 @@ def measure(wl, args, dist, sampler=None, cpu_seconds=10.0, hold=True):
             "e2e": {"value": round(wl.work_per_step() * args.steps / (e2e_ms / 1e3) / scale, 1), "unit": wl.unit,
                     "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
             "gpu_launches": launches_total,
+            **({"e2e_phases_ms": phases} if phases else {}),
         }
         if clocks is not None:
             line["clocks"] = clocks
