@@ -929,6 +929,9 @@ class KMeansW(Workload):
         ctx.enqueue_ndrange_range(q, kg, (self.N, 1, 1), 1, self.lo, self.rows)
         if self.tc:  # bf16 split rows + |x|^2 of the resident points, once
             ctx.enqueue_ndrange_range(q, km.k_split, (self.N, 1, 1), 1, self.lo, self.rows)
+        km.on_grid = True  # generated on the 2^-12 grid by construction
+        if km.q16:  # the update's int16 fixed-point copy, once
+            ctx.enqueue_ndrange_range(q, km.k_quant, (self.N, 1, 1), 1, self.lo, self.rows)
         ctx.finish(q)
         from paper_2005_08466_b200 import datagen as G
 
@@ -954,7 +957,7 @@ class KMeansW(Workload):
     def step(self):
         c, q, km = self.ctx, self.q, self.km
         self._assign()
-        c.enqueue_ndrange_range(q, km.k_acc, (self.N, 1, 1), 1, self.lo, self.rows)
+        c.enqueue_ndrange_range(q, km.acc_kernel, (self.N, 1, 1), 1, self.lo, self.rows)
         if self.dist.world > 1:
             c.enqueue_allreduce_sum_i64(q, km.b_sums)
             c.enqueue_allreduce_sum_i64(q, km.b_counts)

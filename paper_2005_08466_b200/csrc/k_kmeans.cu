@@ -188,15 +188,29 @@ __global__ void __launch_bounds__(1024) kmeans_accumulate_kernel(const float* __
 // many loads the warps keep outstanding; the warps add each staged point into
 // the block's int32 table (lane = dimension, conflict-free, one shared atomic
 // per point) and count the chunk's assignments 32 at a time.
-constexpr int AC_CHUNK = 192, AC_STAGES = 3, AC_FLUSH = 64;
-static_assert(AC_FLUSH * AC_CHUNK < (1 << 15), "rows must stay below 2^16 points between flushes");
-constexpr int AC_STAGE_BYTES = AC_CHUNK * 128 + AC_CHUNK * 4;
+// PT = float: the caller's fp32 points (scaled by 2^12 here); PT = int16_t: the
+// points' 2^-12 fixed-point copy (kmeans_quantize_points), half the bytes per
+// point and twice the points per chunk -- the accumulation streams HBM, so the
+// half-size copy halves its time.
+constexpr int AC_STAGES = 3, AC_FLUSH = 64;
+template <typename PT>
+struct AcCfg {
+  static constexpr int kChunk = sizeof(PT) == 4 ? 192 : 384;
+  static constexpr int kStageBytes = kChunk * 32 * static_cast<int>(sizeof(PT)) + kChunk * 4;
+  static_assert(AC_FLUSH * kChunk < (1 << 15), "rows must stay below 2^16 points between flushes");
+};
+constexpr int AC_CHUNK = AcCfg<float>::kChunk;  // the fp32 path's chunk (host tail split)
+__device__ __forceinline__ int ac_fixed(float x) { return __float2int_rz(__fmul_rn(x, 4096.0f)); }
+__device__ __forceinline__ int ac_fixed(int16_t x) { return x; }
 
-__global__ void __launch_bounds__(1024) kmeans_accumulate32_bulk_kernel(const float* __restrict__ pts,
+template <typename PT>
+__global__ void __launch_bounds__(1024) kmeans_accumulate32_bulk_kernel(const PT* __restrict__ pts,
                                                                        const int32_t* __restrict__ assign,
                                                                        int64_t n, int k,
                                                                        unsigned long long* __restrict__ sums,
                                                                        unsigned long long* __restrict__ counts) {
+  constexpr int AC_CHUNK = AcCfg<PT>::kChunk, AC_STAGE_BYTES = AcCfg<PT>::kStageBytes;
+  constexpr int PB = 32 * static_cast<int>(sizeof(PT));  // bytes per point
   extern __shared__ __align__(128) uint8_t ac_smem[];
   int* tbl = reinterpret_cast<int*>(ac_smem);  // [k*32] sums + [k] counts
   const size_t tbl_bytes = (static_cast<size_t>(k) * 33 * 4 + 127) & ~size_t(127);
@@ -222,8 +236,8 @@ __global__ void __launch_bounds__(1024) kmeans_accumulate32_bulk_kernel(const fl
       const int s = static_cast<int>((ch - c0) % AC_STAGES);
       uint8_t* st = stage0 + s * AC_STAGE_BYTES;
       ptx::mbar_arrive_expect_tx(&full[s], AC_STAGE_BYTES);
-      ptx::bulk_load(st, pts + ch * AC_CHUNK * 32, AC_CHUNK * 128, &full[s]);
-      ptx::bulk_load(st + AC_CHUNK * 128, assign + ch * AC_CHUNK, AC_CHUNK * 4, &full[s]);
+      ptx::bulk_load(st, pts + ch * AC_CHUNK * 32, AC_CHUNK * PB, &full[s]);
+      ptx::bulk_load(st + AC_CHUNK * PB, assign + ch * AC_CHUNK, AC_CHUNK * 4, &full[s]);
     }
   }
   for (int64_t ch = c0; ch < c1; ++ch) {
@@ -231,11 +245,11 @@ __global__ void __launch_bounds__(1024) kmeans_accumulate32_bulk_kernel(const fl
     const int s = static_cast<int>(it % AC_STAGES);
     const uint32_t ph = static_cast<uint32_t>((it / AC_STAGES) & 1);
     ptx::mbar_wait(&full[s], ph);
-    const float* sp = reinterpret_cast<const float*>(stage0 + s * AC_STAGE_BYTES);
-    const int* sa = reinterpret_cast<const int*>(stage0 + s * AC_STAGE_BYTES + AC_CHUNK * 128);
-    if (warp < AC_CHUNK / 32) atomicAdd(&tbl[k * 32 + sa[warp * 32 + lane]], 1);  // counts: 32 points per atomic
-    for (int p = warp; p < AC_CHUNK; p += nwarps)
-      atomicAdd(&tbl[sa[p] * 32 + lane], __float2int_rz(__fmul_rn(sp[p * 32 + lane], 4096.0f)));
+    const PT* sp = reinterpret_cast<const PT*>(stage0 + s * AC_STAGE_BYTES);
+    const int* sa = reinterpret_cast<const int*>(stage0 + s * AC_STAGE_BYTES + AC_CHUNK * PB);
+    for (int w = warp; w < AC_CHUNK / 32; w += nwarps)  // counts: 32 points per atomic
+      atomicAdd(&tbl[k * 32 + sa[w * 32 + lane]], 1);
+    for (int p = warp; p < AC_CHUNK; p += nwarps) atomicAdd(&tbl[sa[p] * 32 + lane], ac_fixed(sp[p * 32 + lane]));
     __syncwarp();
     if (lane == 0) ptx::mbar_arrive(&empty[s]);
     if (threadIdx.x == 0 && ch + AC_STAGES < c1) {  // refill this stage once every warp is done with it
@@ -243,8 +257,8 @@ __global__ void __launch_bounds__(1024) kmeans_accumulate32_bulk_kernel(const fl
       uint8_t* st = stage0 + s * AC_STAGE_BYTES;
       const int64_t nx = ch + AC_STAGES;
       ptx::mbar_arrive_expect_tx(&full[s], AC_STAGE_BYTES);
-      ptx::bulk_load(st, pts + nx * AC_CHUNK * 32, AC_CHUNK * 128, &full[s]);
-      ptx::bulk_load(st + AC_CHUNK * 128, assign + nx * AC_CHUNK, AC_CHUNK * 4, &full[s]);
+      ptx::bulk_load(st, pts + nx * AC_CHUNK * 32, AC_CHUNK * PB, &full[s]);
+      ptx::bulk_load(st + AC_CHUNK * PB, assign + nx * AC_CHUNK, AC_CHUNK * 4, &full[s]);
     }
     // int32 overflow guard: |q| <= 2^15, so a row is exact while its block-local
     // count stays below 2^16. Rows past 2^15 are flushed every AC_FLUSH chunks
@@ -343,16 +357,16 @@ uint64_t launch_accumulate(LaunchCtx& c) {
   if (!rows) return 0;
   const uint64_t work = rows * static_cast<uint64_t>(d);
   const size_t bulk_smem = ((static_cast<size_t>(k) * 33 * 4 + 127) & ~size_t(127)) +
-                           AC_STAGES * AC_STAGE_BYTES + 2 * AC_STAGES * 8;
+                           AC_STAGES * AcCfg<float>::kStageBytes + 2 * AC_STAGES * 8;
   const char* bulk_env = std::getenv("HCL_KM_ACC_BULK");  // 0: the register-pipelined kernel only
   const bool bulk = (bulk_env ? std::atoi(bulk_env) != 0 : true) && d == 32 && bulk_smem <= 227 * 1024 &&
                     rows >= static_cast<uint64_t>(AC_CHUNK) && (reinterpret_cast<uintptr_t>(pts) & 15) == 0 &&
                     (reinterpret_cast<uintptr_t>(as) & 15) == 0;
   if (bulk) {  // whole chunks streamed by TMA; the < AC_CHUNK-point tail by the kernel below
-    HCL_CUDA(cudaFuncSetAttribute(kmeans_accumulate32_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(bulk_smem)));
+    HCL_CUDA(cudaFuncSetAttribute(kmeans_accumulate32_bulk_kernel<float>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bulk_smem)));
     const int bgrid = static_cast<int>(std::min<uint64_t>(c.sm_count, rows / AC_CHUNK));
-    kmeans_accumulate32_bulk_kernel<<<bgrid, 1024, bulk_smem, c.stream>>>(
+    kmeans_accumulate32_bulk_kernel<float><<<bgrid, 1024, bulk_smem, c.stream>>>(
         pts, as, static_cast<int64_t>(rows), static_cast<int>(k), reinterpret_cast<unsigned long long*>(S.ptr),
         reinterpret_cast<unsigned long long*>(Cn.ptr));
     HCL_LAUNCHED();
@@ -374,6 +388,98 @@ uint64_t launch_accumulate(LaunchCtx& c) {
       pts, as, static_cast<int64_t>(rows), static_cast<int>(d), static_cast<int>(k),
       reinterpret_cast<unsigned long long*>(S.ptr), reinterpret_cast<unsigned long long*>(Cn.ptr), use_smem);
   HCL_LAUNCHED();
+  return work;
+}
+
+// the < 384-point tail of the fixed-point accumulation: a warp per point, lane = dimension
+__global__ void kmeans_accumulate_q16_tail_kernel(const int16_t* __restrict__ pts, const int32_t* __restrict__ assign,
+                                                  int64_t n, unsigned long long* __restrict__ sums,
+                                                  unsigned long long* __restrict__ counts) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t p = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; p < n; p += gridDim.x * (blockDim.x / 32)) {
+    const int a = assign[p];
+    atomicAdd(&sums[static_cast<int64_t>(a) * 32 + lane],
+              static_cast<unsigned long long>(static_cast<long long>(pts[p * 32 + lane])));
+    if (lane == 0) atomicAdd(&counts[a], 1ull);
+  }
+}
+
+// kmeans_quantize_points(points f32, q16 out, N, D): q = x * 2^12 as int16 -- exact for
+// points on kmeans_check_points' grid (multiples of 2^-12 in [-8, 8))
+__global__ void quantize_points_kernel(const float4* __restrict__ pts, uint2* __restrict__ q, int64_t n4) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n4;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const float4 v = pts[i];
+    const int a = __float2int_rz(__fmul_rn(v.x, 4096.0f)), b = __float2int_rz(__fmul_rn(v.y, 4096.0f));
+    const int c = __float2int_rz(__fmul_rn(v.z, 4096.0f)), d = __float2int_rz(__fmul_rn(v.w, 4096.0f));
+    q[i] = make_uint2((static_cast<uint32_t>(a) & 0xffffu) | (static_cast<uint32_t>(b) << 16),
+                      (static_cast<uint32_t>(c) & 0xffffu) | (static_cast<uint32_t>(d) << 16));
+  }
+}
+
+uint64_t launch_quantize_points(LaunchCtx& c) {
+  const int64_t n = scalar_arg(c, 2, "kmeans_quantize_points N"), d = scalar_arg(c, 3, "kmeans_quantize_points D");
+  if (n < 0 || d < 1 || d % 4) fail(ErrorCode::argument, "kmeans_quantize_points: need D a multiple of 4");
+  uint64_t lo, rows;
+  sub_range(c, static_cast<uint64_t>(n), lo, rows, "kmeans_quantize_points");
+  const float* p = at_byte<const float>(buffer_arg(c, 0, "kmeans_quantize_points points"), lo * d * 4, rows * d * 4,
+                                        "kmeans_quantize_points points");
+  int16_t* q = at_byte<int16_t>(buffer_arg(c, 1, "kmeans_quantize_points q16"), lo * d * 2, rows * d * 2,
+                                "kmeans_quantize_points q16");
+  if (!rows) return 0;
+  const int64_t n4 = static_cast<int64_t>(rows) * d / 4;
+  const int grid = static_cast<int>(std::min<int64_t>(ceil_div(n4, 256), 8LL * c.sm_count));
+  quantize_points_kernel<<<grid, 256, 0, c.stream>>>(reinterpret_cast<const float4*>(p), reinterpret_cast<uint2*>(q),
+                                                     n4);
+  HCL_LAUNCHED();
+  return rows * static_cast<uint64_t>(d);
+}
+
+// kmeans_accumulate_q16(q16 points, assign, sums, counts, N, D, K): kmeans_accumulate over the
+// 2^-12 fixed-point copy (D = 32), the same integer sums
+uint64_t launch_accumulate_q16(LaunchCtx& c) {
+  const char* what = "kmeans_accumulate_q16";
+  int64_t n = scalar_arg(c, 4, what), d = scalar_arg(c, 5, what), k = scalar_arg(c, 6, what);
+  if (n < 0 || d != 32 || k < 1) fail(ErrorCode::argument, std::string(what) + ": needs D = 32, N >= 0, K >= 1");
+  const BufView& P = buffer_arg(c, 0, what);
+  const BufView& A = buffer_arg(c, 1, what);
+  const BufView& S = buffer_arg(c, 2, what);
+  const BufView& Cn = buffer_arg(c, 3, what);
+  if (S.first_byte != 0 || S.bytes != static_cast<uint64_t>(k * d) * 8 || Cn.first_byte != 0 ||
+      Cn.bytes != static_cast<uint64_t>(k) * 8)
+    fail(ErrorCode::argument, std::string(what) + ": sums must be K*D int64 and counts K int64");
+  uint64_t lo, rows;
+  sub_range(c, static_cast<uint64_t>(n), lo, rows, what);
+  const int16_t* pts = at_byte<const int16_t>(P, lo * d * 2, rows * d * 2, what);
+  const int32_t* as = at_byte<const int32_t>(A, lo * 4, rows * 4, what);
+  HCL_CUDA(cudaMemsetAsync(S.ptr, 0, S.bytes, c.stream));
+  HCL_CUDA(cudaMemsetAsync(Cn.ptr, 0, Cn.bytes, c.stream));
+  if (!rows) return 0;
+  const uint64_t work = rows * static_cast<uint64_t>(d);
+  using Q = AcCfg<int16_t>;
+  const size_t smem = ((static_cast<size_t>(k) * 33 * 4 + 127) & ~size_t(127)) + AC_STAGES * Q::kStageBytes +
+                      2 * AC_STAGES * 8;
+  if (smem > 227 * 1024) fail(ErrorCode::argument, std::string(what) + ": K too large for the shared-memory table");
+  if (rows >= static_cast<uint64_t>(Q::kChunk) && (reinterpret_cast<uintptr_t>(pts) & 15) == 0 &&
+      (reinterpret_cast<uintptr_t>(as) & 15) == 0) {
+    HCL_CUDA(cudaFuncSetAttribute(kmeans_accumulate32_bulk_kernel<int16_t>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    const int bgrid = static_cast<int>(std::min<uint64_t>(c.sm_count, rows / Q::kChunk));
+    kmeans_accumulate32_bulk_kernel<int16_t><<<bgrid, 1024, smem, c.stream>>>(
+        pts, as, static_cast<int64_t>(rows), static_cast<int>(k), reinterpret_cast<unsigned long long*>(S.ptr),
+        reinterpret_cast<unsigned long long*>(Cn.ptr));
+    HCL_LAUNCHED();
+    const uint64_t done = rows / Q::kChunk * Q::kChunk;
+    pts += done * 32;
+    as += done;
+    rows -= done;
+  }
+  if (rows) {
+    kmeans_accumulate_q16_tail_kernel<<<static_cast<unsigned>(ceil_div(rows, 8)), 256, 0, c.stream>>>(
+        pts, as, static_cast<int64_t>(rows), reinterpret_cast<unsigned long long*>(S.ptr),
+        reinterpret_cast<unsigned long long*>(Cn.ptr));
+    HCL_LAUNCHED();
+  }
   return work;
 }
 
@@ -534,6 +640,7 @@ uint64_t launch_gather_points(LaunchCtx& c) {
 uint64_t rows_km(const int64_t* s, uint32_t n) { return static_cast<uint64_t>(s[n == 6 ? 3 : 4]); }
 uint64_t rows_gen(const int64_t* s, uint32_t) { return static_cast<uint64_t>(s[1]); }
 uint64_t rows_gather(const int64_t* s, uint32_t) { return static_cast<uint64_t>(s[3]); }
+uint64_t rows_quant(const int64_t* s, uint32_t) { return static_cast<uint64_t>(s[2]); }
 
 }  // namespace
 
@@ -543,6 +650,10 @@ void register_kmeans(std::vector<KernelDef>& r) {
   r.push_back({"b200", "kmeans_assign", {I, I, O, S, S, S}, {X, P, X, N, N, N}, launch_assign, nullptr, rows_km});
   r.push_back({"b200", "kmeans_accumulate", {I, I, O, O, S, S, S}, {X, X, R, R, N, N, N}, launch_accumulate, nullptr,
                rows_km});
+  r.push_back({"b200", "kmeans_accumulate_q16", {I, I, O, O, S, S, S}, {X, X, R, R, N, N, N}, launch_accumulate_q16,
+               nullptr, rows_km});
+  r.push_back({"b200", "kmeans_quantize_points", {I, O, S, S}, {X, X, N, N}, launch_quantize_points, nullptr,
+               rows_quant});
   r.push_back({"b200", "kmeans_finalize", {I, I, IO, S, S}, {P, P, P, N, N}, launch_finalize, nullptr, nullptr});
   r.push_back({"b200", "reduce_add_i64", {IO, I, S}, {P, P, N}, launch_add_i64, nullptr, nullptr});
   r.push_back({"b200", "kmeans_check_points", {I, S, S}, {X, N, N}, launch_check_points, nullptr, rows_gen});

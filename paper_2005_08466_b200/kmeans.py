@@ -42,6 +42,13 @@ class KMeans:
         self.k_acc = ctx.create_kernel(prog, "kmeans_accumulate")
         self.k_fin = ctx.create_kernel(prog, "kmeans_finalize")
         self.k_check = ctx.create_kernel(prog, "kmeans_check_points")
+        # D = 32: the update streams a 2^-12 fixed-point int16 copy of the points (exact on
+        # the checked grid; half the bytes of fp32), made once per load / reorder
+        self.q16 = d == 32 and k <= 1024  # (the int32 table of K x 33 + three stages in shared memory)
+        if self.q16:
+            self.b_q16 = mk(n * d * 2)
+            self.k_quant = ctx.create_kernel(prog, "kmeans_quantize_points")
+            self.k_acc_q = ctx.create_kernel(prog, "kmeans_accumulate_q16")
         if tensor_filter:
             self.b_split, self.b_xx = mk(n * 128), mk(n * 4)
             self.k_split = ctx.create_kernel(prog, "kmeans_split_points")
@@ -60,6 +67,11 @@ class KMeans:
             ctx.set_kernel_arg(self.k_acc, j, a)
         for j, a in enumerate([self.b_sums, self.b_counts, self.b_cent, k, d]):
             ctx.set_kernel_arg(self.k_fin, j, a)
+        if self.q16:
+            for j, a in enumerate([self.b_pts, self.b_q16, n, d]):
+                ctx.set_kernel_arg(self.k_quant, j, a)
+            for j, a in enumerate([self.b_q16, self.b_assign, self.b_sums, self.b_counts, n, d, k]):
+                ctx.set_kernel_arg(self.k_acc_q, j, a)
         if self.tensor_filter:
             for j, a in enumerate([self.b_pts, self.b_split, self.b_xx, n, d]):
                 ctx.set_kernel_arg(self.k_split, j, a)
@@ -104,13 +116,23 @@ class KMeans:
         self.b_pts = b_new
         self.perm = new_perm
         self._bind()
-        if self.tensor_filter:
-            for q, lo, hi in parts:
+        for q, lo, hi in parts:
+            if self.tensor_filter:
                 ctx.enqueue_ndrange_range(q, self.k_split, (n, 1, 1), 1, lo, hi - lo)
+            if self.q16 and getattr(self, "on_grid", False):
+                ctx.enqueue_ndrange_range(q, self.k_quant, (n, 1, 1), 1, lo, hi - lo)
+
+    @property
+    def acc_kernel(self) -> Handle:
+        """The update's accumulation kernel: over the int16 fixed-point copy when the
+        points are on the grid and D = 32, else over the fp32 points (same sums)."""
+        return self.k_acc_q if self.q16 and getattr(self, "on_grid", False) else self.k_acc
 
     def _split(self) -> None:
         if self.tensor_filter:  # the bf16 split rows and |x|^2 of the resident points (once)
             self.ctx.enqueue_ndrange_partitioned(self.k_split, (self.n, 1, 1), 1, self.queues, bounds=self.bounds)
+        if self.q16 and getattr(self, "on_grid", False):  # after the grid check, in stream order
+            self.ctx.enqueue_ndrange_partitioned(self.k_quant, (self.n, 1, 1), 1, self.queues, bounds=self.bounds)
 
     def _assign(self) -> None:
         k = self.k_assign_tc if self.tensor_filter else self.k_assign
@@ -162,7 +184,7 @@ class KMeans:
         ctx, g = self.ctx, (self.n, 1, 1)
         for _ in range(iterations):
             self._assign()
-            ctx.enqueue_ndrange_partitioned(self.k_acc, g, 1, self.queues, bounds=self.bounds)
+            ctx.enqueue_ndrange_partitioned(self.acc_kernel, g, 1, self.queues, bounds=self.bounds)
             ctx.enqueue_ndrange_kernel(self.queues[0], self.k_fin)
 
     def assign_only(self) -> None:
@@ -198,3 +220,5 @@ class KMeans:
         if self.tensor_filter:
             self.ctx.release(self.b_split)
             self.ctx.release(self.b_xx)
+        if self.q16:
+            self.ctx.release(self.b_q16)

@@ -261,3 +261,39 @@ def test_order_by_cluster_keeps_every_result(ctx, queues, P, tc):
     assert (got_a == a_want).all()
     assert (s == s_want).all() and (c == c_want).all()
     assert cent.tobytes() == cent_want.reshape(k, d).tobytes()
+
+
+@pytest.mark.parametrize("n,k,P", [(384 * 7 + 5, 1024, 1), (100003, 64, 3), (383, 5, 1)])
+def test_accumulate_q16_equals_fp32_path(ctx, queues, n, k, P):
+    """kmeans_quantize_points + kmeans_accumulate_q16 (the update's int16 fixed-point
+    stream) give the same int64 sums and counts as kmeans_accumulate over the fp32
+    points and as the oracle -- bulk chunks, ragged tails and partitioned launches."""
+    pts = G.gen_kmeans_points(n, 32, max(k, 2), 7)
+    cent = pts[: k * 32].copy()
+    a = O.kmeans_assign(pts, n, 32, cent, k)
+    s_want, c_want = O.kmeans_accumulate(pts, n, 32, a, k)
+    qs = queues[:P]
+    mk = ctx.create_buffer
+    b_p, b_q, b_a, b_s, b_c = mk(n * 128), mk(n * 64), mk(n * 4), mk(k * 256), mk(k * 8)
+    ctx.enqueue_write_buffer(qs[0], b_p, pts)
+    ctx.enqueue_write_buffer(qs[0], b_a, a.astype(np.int32))
+    prog = ctx.create_program("b200")
+    kq = ctx.create_kernel(prog, "kmeans_quantize_points")
+    for j, v in enumerate([b_p, b_q, n, 32]):
+        ctx.set_kernel_arg(kq, j, v)
+    ctx.enqueue_ndrange_partitioned(kq, (n, 1, 1), 1, qs)
+    q16 = ctx.enqueue_read_buffer(qs[0], b_q).view(np.int16)
+    assert (q16 == np.round(pts * 4096).astype(np.int16)).all()
+    for name, src in (("kmeans_accumulate_q16", b_q), ("kmeans_accumulate", b_p)):
+        kk = ctx.create_kernel(prog, name)
+        for j, v in enumerate([src, b_a, b_s, b_c, n, 32, k]):
+            ctx.set_kernel_arg(kk, j, v)
+        ctx.enqueue_ndrange_partitioned(kk, (n, 1, 1), 1, qs)
+        for q in qs:
+            ctx.finish(q)
+        s = ctx.enqueue_read_buffer(qs[0], b_s).view(np.int64)
+        c = ctx.enqueue_read_buffer(qs[0], b_c).view(np.int64)
+        assert (s == s_want).all() and (c == c_want).all(), name
+        ctx.release(kk)
+    for b in (b_p, b_q, b_a, b_s, b_c):
+        ctx.release(b)
