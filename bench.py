@@ -748,12 +748,17 @@ class PageRankW(Workload):
 
         d, ctx, q = self.dist, self.ctx, self.q
         self.symm = []
-        for i in range(2):
-            t = symm_mem.empty(self.v, dtype=torch.float32, device=torch.device("cuda", d.local))
-            t.zero_()
-            h = symm_mem.rendezvous(t, d.d.group.WORLD.group_name)
-            self.symm.append((t, h))
-        ok = all(h.multicast_ptr for _, h in self.symm)
+        try:
+            for i in range(2):
+                t = symm_mem.empty(self.v, dtype=torch.float32, device=torch.device("cuda", d.local))
+                t.zero_()
+                h = symm_mem.rendezvous(t, d.d.group.WORLD.group_name)
+                self.symm.append((t, h))
+            ok = all(h.multicast_ptr for _, h in self.symm)
+        except Exception as e:  # no symmetric-memory support here: every rank falls back together
+            print(f"rank {d.rank}: no NVSwitch multicast ({type(e).__name__}: {e}); IPC peer stores",
+                  file=sys.stderr, flush=True)
+            ok = False
         if not d.allmin(float(ok)):
             self.symm = []
             return False
