@@ -195,6 +195,22 @@ class PageRank:
             self.bl.close()
 
 
+def part_bin_options(n_edges: int, sm_count: int = 148) -> dict:
+    """Chunking of one part's layout: ~16 chunks per scatter CTA (two per SM), so the
+    static chunk-to-CTA assignment stays balanced when a part holds a fraction of
+    the edges (one rank of N). chunk_edges = the power of two nearest to
+    n_edges / (32 * SMs), in [16384, 65536]; spans of 16384 sources below 65536-edge
+    chunks (the chunks then end on the edge count, not the span). Measured per part
+    at C3 (rank row ranges emulated on one GPU, scratch/pr_rank_split.py): N=1
+    65536/8192 (default) 0.97 ms; N=2 32768/16384 0.51 vs 0.56 ms; N=4 16384/16384
+    0.32 vs 0.38 ms; N=8 16384/16384 0.23 vs 0.28 ms (slowest part)."""
+    import math
+
+    raw = max(1.0, n_edges / (32.0 * sm_count))
+    ce = int(min(65536, max(16384, 2 ** round(math.log2(raw)))))
+    return dict(chunk_edges=ce, span_max=8192 if ce == 65536 else 16384)
+
+
 class BinnedLayout:
     """Device copy of the propagation-blocking layout (hcl_pagerank_bins_build)
     of every part [bounds[i], bounds[i+1]) with rows, concatenated into one
@@ -214,7 +230,8 @@ class BinnedLayout:
             lo, hi = int(bounds[i]), int(bounds[i + 1])
             if hi <= lo:
                 continue
-            L = pagerank_bins(row_ptr, col_idx, lo, hi, **(opts or {}))
+            L = pagerank_bins(row_ptr, col_idx, lo, hi,
+                              **(opts if opts is not None else part_bin_options(int(row_ptr[hi]) - int(row_ptr[lo]))))
             self.layouts.append({k: v for k, v in L.items() if not isinstance(v, np.ndarray)})
             parts.append([lo, hi, base["chunk"], L["n_chunks"], L["n_bins"], L["gstride"], base["desc"], base["src"],
                           base["ent"], base["unit"], L["n_units"], base["slot"], L["n_slots"], L["bin_rows"],
