@@ -206,3 +206,35 @@ def test_finish_does_not_block_other_queues(ctx, queues):
     assert t1 - t0 < 0.5 * t_kernel
     for h in (ba, bb, bc, b):
         ctx.release(h)
+
+
+def test_bind_external_memory(ctx, queues):
+    """bind_external (hcl_ctx_bind_external): a buffer backed by caller-owned
+    device memory (here a torch tensor, as bench.py binds symmetric-memory xs'
+    buffers) -- a kernel's output lands in that memory, reads go through the
+    runtime, the memory is not freed by release, and a second device gets a
+    copy through the usual residency rules."""
+    import torch
+
+    n = 1000
+    dev = ctx.get_device_ids()[0]
+    t = torch.full((n,), -1.0, dtype=torch.float64, device="cuda:0")
+    torch.cuda.synchronize()
+    out = ctx.create_buffer(n * 8)
+    ctx.bind_external(queues[0], out, t.data_ptr())
+    a = np.arange(n, dtype=np.float64)
+    b_a = ctx.create_buffer(n * 8)
+    ctx.enqueue_write_buffer(queues[0], b_a, a)
+    vk = kernel(ctx, "core", "vecadd", [b_a, b_a, out, n])
+    ctx.enqueue_ndrange_kernel(queues[0], vk, (n, 1, 1), 1)
+    ctx.finish(queues[0])
+    assert (t.cpu().numpy() == 2 * a).all()  # the kernel wrote the caller's memory
+    for q in queues:
+        assert (ctx.enqueue_read_buffer(q, out).view(np.float64) == 2 * a).all()
+    ctx.release(out)
+    ctx.release(b_a)
+    ctx.release(vk)
+    assert (t.cpu().numpy() == 2 * a).all()  # still the caller's (not freed)
+    with pytest.raises(Exception):
+        ctx.bind_external(queues[0], ctx.create_buffer(8), 0)  # null pointer: argument error
+    assert dev == ctx.get_device_ids()[0]
