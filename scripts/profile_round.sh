@@ -17,9 +17,12 @@ full() {  # name, kernel regex, skip, command...
   $NCU --set full --import-source on -k "regex:$re" -s "$skip" -c 1 -o "gpurun_out/$name" "$@" > "gpurun_out/$name.log" 2>&1
   echo "$name rc=$?"
 }
-full r02_gemm_bf16 gemm_tc 4 python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-secondary
-full r02_conv_nhwc conv3x3_v3 4 python bench.py --workload conv --steps 1 --warmup 3 --no-cpu-baseline
+case "${1:-all}" in
+  all)
+    full r02_gemm_bf16 gemm_tc 4 python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-secondary
+    full r02_conv_nhwc conv3x3_v3 4 python bench.py --workload conv --steps 1 --warmup 3 --no-cpu-baseline ;;
+esac
 full r02_pagerank_scatter pr_bin_scatter 4 python bench.py --workload pagerank --steps 1 --warmup 3 --no-cpu-baseline
 full r02_pagerank_gather pr_bin_gather 4 python bench.py --workload pagerank --steps 1 --warmup 3 --no-cpu-baseline
-full r02_kmeans_assign_tc assign_tc 1 python scripts/kmeans_assign_once.py 16777216
-full r02_kmeans_accumulate accumulate32 1 python scripts/kmeans_assign_once.py 16777216
+full r02_kmeans_assign_tc_ordered assign_tc 2 python scripts/kmeans_assign_once.py 16777216 1
+full r02_kmeans_accumulate_q16 accumulate32 0 python scripts/kmeans_assign_once.py 16777216 1
