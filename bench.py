@@ -772,7 +772,7 @@ class PageRankW(Workload):
 
     def reset(self):
         ctx, q = self.ctx, self.q
-        if self.fused:
+        if self.fused and self.dist.world > 1:
             ctx.finish(q)  # the previous step's collective: no peer store is still landing
             self.dist.barrier()
         ctx.enqueue_write_buffer(q, self.b_x[0], self.x0)
