@@ -192,12 +192,24 @@ __global__ void __launch_bounds__(1024) kmeans_accumulate_kernel(const float* __
 // points' 2^-12 fixed-point copy (kmeans_quantize_points), half the bytes per
 // point and twice the points per chunk -- the accumulation streams HBM, so the
 // half-size copy halves its time.
-constexpr int AC_STAGES = 3, AC_FLUSH = 64;
+constexpr int AC_FLUSH = 64;
+// int16 stream: two stages of 672 points (fewer, larger chunks: each refill waits
+// for every warp, so the per-chunk hand-off dominates small chunks). 2^27 points,
+// K=1024: 384 x 3 2.94 ms, 512 x 2 2.49, 640 x 2 2.33, 672 x 2 2.30 (the largest
+// pair that fits beside the K=1024 table)
+#ifndef HCL_AC_Q_CHUNK
+#define HCL_AC_Q_CHUNK 672
+#endif
+#ifndef HCL_AC_Q_STAGES
+#define HCL_AC_Q_STAGES 2
+#endif
 template <typename PT>
 struct AcCfg {
-  static constexpr int kChunk = sizeof(PT) == 4 ? 192 : 384;
+  static constexpr int kChunk = sizeof(PT) == 4 ? 192 : HCL_AC_Q_CHUNK;
+  static constexpr int kStages = sizeof(PT) == 4 ? 3 : HCL_AC_Q_STAGES;
   static constexpr int kStageBytes = kChunk * 32 * static_cast<int>(sizeof(PT)) + kChunk * 4;
-  static_assert(AC_FLUSH * kChunk < (1 << 15), "rows must stay below 2^16 points between flushes");
+  static constexpr int kFlush = ((1 << 15) - 1) / kChunk < AC_FLUSH ? ((1 << 15) - 1) / kChunk : AC_FLUSH;
+  static_assert(kFlush * kChunk < (1 << 15), "rows must stay below 2^16 points between flushes");
 };
 constexpr int AC_CHUNK = AcCfg<float>::kChunk;  // the fp32 path's chunk (host tail split)
 __device__ __forceinline__ int ac_fixed(float x) { return __float2int_rz(__fmul_rn(x, 4096.0f)); }
@@ -209,7 +221,7 @@ __global__ void __launch_bounds__(1024) kmeans_accumulate32_bulk_kernel(const PT
                                                                        int64_t n, int k,
                                                                        unsigned long long* __restrict__ sums,
                                                                        unsigned long long* __restrict__ counts) {
-  constexpr int AC_CHUNK = AcCfg<PT>::kChunk, AC_STAGE_BYTES = AcCfg<PT>::kStageBytes;
+  constexpr int AC_CHUNK = AcCfg<PT>::kChunk, AC_STAGE_BYTES = AcCfg<PT>::kStageBytes, AC_STAGES = AcCfg<PT>::kStages;
   constexpr int PB = 32 * static_cast<int>(sizeof(PT));  // bytes per point
   extern __shared__ __align__(128) uint8_t ac_smem[];
   int* tbl = reinterpret_cast<int*>(ac_smem);  // [k*32] sums + [k] counts
@@ -261,9 +273,9 @@ __global__ void __launch_bounds__(1024) kmeans_accumulate32_bulk_kernel(const PT
       ptx::bulk_load(st + AC_CHUNK * PB, assign + nx * AC_CHUNK, AC_CHUNK * 4, &full[s]);
     }
     // int32 overflow guard: |q| <= 2^15, so a row is exact while its block-local
-    // count stays below 2^16. Rows past 2^15 are flushed every AC_FLUSH chunks
-    // (at most AC_FLUSH * AC_CHUNK < 2^15 more points in between).
-    if ((it + 1) % AC_FLUSH == 0) {
+    // count stays below 2^16. Rows past 2^15 are flushed every kFlush chunks
+    // (at most kFlush * AC_CHUNK < 2^15 more points in between).
+    if ((it + 1) % AcCfg<PT>::kFlush == 0) {
       __syncthreads();
       for (int r = threadIdx.x; r < k; r += blockDim.x)
         if (tbl[k * 32 + r] >= (1 << 15)) {
@@ -357,7 +369,7 @@ uint64_t launch_accumulate(LaunchCtx& c) {
   if (!rows) return 0;
   const uint64_t work = rows * static_cast<uint64_t>(d);
   const size_t bulk_smem = ((static_cast<size_t>(k) * 33 * 4 + 127) & ~size_t(127)) +
-                           AC_STAGES * AcCfg<float>::kStageBytes + 2 * AC_STAGES * 8;
+                           AcCfg<float>::kStages * AcCfg<float>::kStageBytes + 2 * AcCfg<float>::kStages * 8;
   const char* bulk_env = std::getenv("HCL_KM_ACC_BULK");  // 0: the register-pipelined kernel only
   const bool bulk = (bulk_env ? std::atoi(bulk_env) != 0 : true) && d == 32 && bulk_smem <= 227 * 1024 &&
                     rows >= static_cast<uint64_t>(AC_CHUNK) && (reinterpret_cast<uintptr_t>(pts) & 15) == 0 &&
@@ -391,7 +403,7 @@ uint64_t launch_accumulate(LaunchCtx& c) {
   return work;
 }
 
-// the < 384-point tail of the fixed-point accumulation: a warp per point, lane = dimension
+// the < one-chunk tail of the fixed-point accumulation: a warp per point, lane = dimension
 __global__ void kmeans_accumulate_q16_tail_kernel(const int16_t* __restrict__ pts, const int32_t* __restrict__ assign,
                                                   int64_t n, unsigned long long* __restrict__ sums,
                                                   unsigned long long* __restrict__ counts) {
@@ -457,8 +469,8 @@ uint64_t launch_accumulate_q16(LaunchCtx& c) {
   if (!rows) return 0;
   const uint64_t work = rows * static_cast<uint64_t>(d);
   using Q = AcCfg<int16_t>;
-  const size_t smem = ((static_cast<size_t>(k) * 33 * 4 + 127) & ~size_t(127)) + AC_STAGES * Q::kStageBytes +
-                      2 * AC_STAGES * 8;
+  const size_t smem = ((static_cast<size_t>(k) * 33 * 4 + 127) & ~size_t(127)) + Q::kStages * Q::kStageBytes +
+                      2 * Q::kStages * 8;
   if (smem > 227 * 1024) fail(ErrorCode::argument, std::string(what) + ": K too large for the shared-memory table");
   if (rows >= static_cast<uint64_t>(Q::kChunk) && (reinterpret_cast<uintptr_t>(pts) & 15) == 0 &&
       (reinterpret_cast<uintptr_t>(as) & 15) == 0) {

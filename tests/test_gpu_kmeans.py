@@ -263,7 +263,7 @@ def test_order_by_cluster_keeps_every_result(ctx, queues, P, tc):
     assert cent.tobytes() == cent_want.reshape(k, d).tobytes()
 
 
-@pytest.mark.parametrize("n,k,P", [(384 * 7 + 5, 1024, 1), (100003, 64, 3), (383, 5, 1)])
+@pytest.mark.parametrize("n,k,P", [(672 * 7 + 5, 1024, 1), (100003, 64, 3), (671, 5, 1), (1 << 20, 1024, 2)])
 def test_accumulate_q16_equals_fp32_path(ctx, queues, n, k, P):
     """kmeans_quantize_points + kmeans_accumulate_q16 (the update's int16 fixed-point
     stream) give the same int64 sums and counts as kmeans_accumulate over the fp32
