@@ -124,11 +124,12 @@ def pagerank_inv_outdeg(outdeg: np.ndarray) -> np.ndarray:
 # binned (propagation-blocking) PageRank layout defaults: 8192-row bins (the
 # gather's shared-memory accumulator is bin_rows x 8 bytes: two gather CTAs per
 # SM; dst16 offsets need bin_rows <= 65536), chunks of <= 65536 edges spanning
-# <= 8192 sources (the scatter stages a chunk's descriptor, src_local and gather
-# inputs in shared memory). Measured at C3 on B200 (ms per iteration): 8192-row
-# bins 0.977, 16384-row 1.002; 65536-edge chunks 1.00, 32768 1.12-1.15, 16384
-# 1.25-1.27 -- the per-chunk cost dominates
-PR_BIN_ROWS, PR_CHUNK_EDGES, PR_SPAN_MAX = 8192, 65536, 8192
+# <= 16384 sources (the scatter stages a chunk's descriptor, src_local and gather
+# inputs in shared memory: 216 KB at these limits). Measured at C3 on B200 (ms
+# per iteration): 8192-row bins 0.977, 16384-row 1.002; 65536-edge chunks 1.00,
+# 32768 1.12-1.15, 16384 1.25-1.27 -- the per-chunk cost dominates; spans of
+# 16384 sources 0.967 vs 8192 0.993 (fewer, fuller chunks)
+PR_BIN_ROWS, PR_CHUNK_EDGES, PR_SPAN_MAX = 8192, 65536, 16384
 
 
 def pagerank_bins(row_ptr: np.ndarray, col_idx: np.ndarray, lo: int = 0, hi: int | None = None,

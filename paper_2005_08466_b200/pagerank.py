@@ -199,16 +199,17 @@ def part_bin_options(n_edges: int, sm_count: int = 148) -> dict:
     """Chunking of one part's layout: ~16 chunks per scatter CTA (two per SM), so the
     static chunk-to-CTA assignment stays balanced when a part holds a fraction of
     the edges (one rank of N). chunk_edges = the power of two nearest to
-    n_edges / (32 * SMs), in [16384, 65536]; spans of 16384 sources below 65536-edge
-    chunks (the chunks then end on the edge count, not the span). Measured per part
-    at C3 (rank row ranges emulated on one GPU, scratch/pr_rank_split.py): N=1
-    65536/8192 (default) 0.97 ms; N=2 32768/16384 0.51 vs 0.56 ms; N=4 16384/16384
-    0.32 vs 0.38 ms; N=8 16384/16384 0.23 vs 0.28 ms (slowest part)."""
+    n_edges / (32 * SMs), in [16384, 65536]; spans of up to 16384 sources (the
+    largest with 65536-edge chunks in one shared-memory stage; longer spans mean
+    fewer, fuller chunks). Measured at C3 (rank row ranges emulated on one GPU,
+    scratch/pr_rank_split.py; slowest part): N=1 65536/16384 0.967 ms vs 65536/8192
+    0.993 (12288: 0.980); N=2 32768/16384 0.51 vs 0.56 ms; N=4 16384/16384 0.32 vs
+    0.38 ms; N=8 16384/16384 0.23 vs 0.28 ms."""
     import math
 
     raw = max(1.0, n_edges / (32.0 * sm_count))
     ce = int(min(65536, max(16384, 2 ** round(math.log2(raw)))))
-    return dict(chunk_edges=ce, span_max=8192 if ce == 65536 else 16384)
+    return dict(chunk_edges=ce, span_max=16384)
 
 
 class BinnedLayout:
