@@ -24,6 +24,8 @@
 #include <mutex>
 #include <set>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "haocl/runtime.hpp"
 #include "hcl_cabi.h"
 #include "hcl_host.h"
@@ -36,6 +38,16 @@ extern thread_local bool t_launch_untimed;  // csrc/common.hpp
 namespace haocl {
 
 namespace {
+
+// NVTX ranges around the host API's phases (launch, transfers, collectives,
+// finish): visible in Nsight Systems / ncu range filters, no cost without a tool
+struct Range {
+  explicit Range(const char* name) { nvtxRangePushA(name); }
+  Range(const char* prefix, const std::string& what) { nvtxRangePushA((std::string(prefix) + what).c_str()); }
+  ~Range() { nvtxRangePop(); }
+  Range(const Range&) = delete;
+  Range& operator=(const Range&) = delete;
+};
 
 using Clock = std::chrono::steady_clock;
 double ms_since(Clock::time_point t) { return std::chrono::duration<double, std::milli>(Clock::now() - t).count(); }
@@ -317,6 +329,7 @@ struct HostContext::Impl {
 
   Handle launch_parts(KernelRec& k, const std::vector<Arg>& args, std::array<uint64_t, 3> global, uint32_t dims,
                       const std::vector<Part>& parts, bool whole) {
+    Range range("hcl:launch ", k.name);
     const uint32_t n = k.arity;
     const uint64_t rows = global[0];
     // per-argument byte geometry
@@ -729,6 +742,7 @@ void HostContext::set_kernel_arg(Handle kernel, uint32_t index, Handle buffer) {
 
 Handle HostContext::enqueue_write_buffer(Handle queue, Handle buffer, std::span<const uint8_t> data, uint64_t offset,
                                          bool blocking) {
+  Range range("hcl:write_buffer");
   int dev = -1;
   Handle ev;
   auto started = Clock::now();
@@ -764,6 +778,7 @@ Handle HostContext::enqueue_write_buffer(Handle queue, Handle buffer, std::span<
 
 void HostContext::enqueue_read_buffer_into(Handle queue, Handle buffer, void* dst, uint64_t offset, uint64_t len,
                                            bool blocking) {
+  Range range("hcl:read_buffer");
   struct Copy {
     int dev;
     uint64_t pos, n;
@@ -920,6 +935,7 @@ void HostContext::init_collectives(Handle queue, int rank, int nranks, const std
 }
 
 void HostContext::enqueue_allgather(Handle queue, Handle buffer, const std::vector<uint64_t>& bounds) {
+  Range range("hcl:allgather");
   std::lock_guard lock(impl_->mu);
   Impl::QueueRec& q = impl_->queue(queue.id);
   Impl::BufferRec& b = impl_->buffer(buffer.id);
@@ -988,6 +1004,7 @@ void HostContext::enqueue_barrier(Handle queue, const std::vector<Handle>& compl
 }
 
 void HostContext::enqueue_allreduce_sum_i64(Handle queue, Handle buffer) {
+  Range range("hcl:allreduce");
   std::lock_guard lock(impl_->mu);
   Impl::QueueRec& q = impl_->queue(queue.id);
   Impl::BufferRec& b = impl_->buffer(buffer.id);
@@ -1055,6 +1072,7 @@ Handle HostContext::launch_task(Handle queue, const KernelTask& task) {
 }
 
 TimingFragment HostContext::finish(Handle queue) {
+  Range range("hcl:finish");
   std::shared_ptr<std::mutex> op;
   {
     std::lock_guard lock(impl_->mu);
