@@ -63,9 +63,10 @@ for label, wts in [("even (block_range)", [1] * len(SMS)), ("even", [1] * len(SM
     ms = timed(wts)
     rows.append((label, wts, ctx.partition_plan(conv.k_conv, (N, 1, 1), queues, wts), ms))
 out_even = sample()
-ema_w = ctx.partition_weights("conv3x3", gids)  # rates profiled by the runs above
+KNAME = "conv3x3" if conv.padded else "conv3x3_nhwc"  # the profiled kernel's registry name
+ema_w = ctx.partition_weights(KNAME, gids)  # rates profiled by the runs above
 for label, wts in [("model (SM budgets)", SMS), ("EMA-profiled rates", None)]:
-    plan_w = wts if wts is not None else ctx.partition_weights("conv3x3", gids)
+    plan_w = wts if wts is not None else ctx.partition_weights(KNAME, gids)
     ms = timed(wts)
     rows.append((label, plan_w, ctx.partition_plan(conv.k_conv, (N, 1, 1), queues, plan_w), ms))
 same = sample() == out_even
@@ -74,7 +75,7 @@ if len(SMS) == 2:
         wts = [int(share * 1000), 1000 - int(share * 1000)]
         ms = timed(wts)
         rows.append((f"sweep {share:.2f}", wts, ctx.partition_plan(conv.k_conv, (N, 1, 1), queues, wts), ms))
-print(f"conv 3x3 {N}x{H}x{W}x{C}->{K} bf16 over {len(SMS)} logical devices on one B200, SM budgets {SMS}")
+print(f"conv 3x3 ({KNAME}) {N}x{H}x{W}x{C}->{K} bf16 over {len(SMS)} logical devices on one B200, SM budgets {SMS}")
 for label, wts, bounds, ms in rows[1:]:
     counts = [bounds[i + 1] - bounds[i] for i in range(len(bounds) - 1)]
     print(f"  {label:22s} images {counts}: {ms:7.3f} ms/launch = {flop / ms / 1e9:7.1f} TFLOP/s")
