@@ -293,43 +293,66 @@ class GemmBf16(Workload):
     def dominant_work(self):
         return 2.0 * self.rows * self.S * self.S
 
+    E2E_CHUNKS = 4
+
     def e2e_setup(self):
-        """Second buffer set + kernel: step i uses set i % 2, so step i's H2D
-        copies overlap step i-1's GEMM and D2H (non-blocking enqueue_write /
-        enqueue_read on the runtime's copy streams, RAW/WAR-ordered per buffer)."""
+        """The e2e step's buffers: two sets (step i uses set i % 2, so step i's
+        copies overlap step i-1's work), each holding B and the rank's rows in
+        E2E_CHUNKS row chunks with their own A and C buffers and GEMM kernel. A
+        chunk's D2H then depends only on its own GEMM, and the next chunk's GEMM
+        only on its own A -- the C rows stream back while later chunks compute,
+        and the next step's H2D streams in meanwhile (copies in both directions
+        on two copy streams each)."""
         import torch
 
         ctx, S = self.ctx, self.S
-        self.sets = [(self.k, self.bA, self.bB, self.bC)]
-        k2 = ctx.create_kernel(ctx.create_program("b200"), "gemm_bf16")
-        b2 = tuple(ctx.create_buffer(S * S * 2) for _ in range(3))
-        for i, v in enumerate([*b2, S, S, S, 0]):
-            ctx.set_kernel_arg(k2, i, v)
-        self.sets.append((k2, *b2))
+        prog = ctx.create_program("b200")
+        nc = max(1, min(self.E2E_CHUNKS, self.rows // 256))
+        cb = [self.rows * i // nc for i in range(nc + 1)]
+        self.chunk_bounds = cb
+        self.sets = []
+        for _ in range(2):
+            bB = ctx.create_buffer(S * S * 2)
+            chunks = []
+            for c in range(nc):
+                rc = cb[c + 1] - cb[c]
+                bA, bC = ctx.create_buffer(rc * S * 2), ctx.create_buffer(rc * S * 2)
+                k = ctx.create_kernel(prog, "gemm_bf16")
+                for i, v in enumerate([bA, bB, bC, rc, S, S, 0]):
+                    ctx.set_kernel_arg(k, i, v)
+                chunks.append((k, bA, bC, rc))
+            self.sets.append((bB, chunks))
         self.c_hosts = [self.c_host, torch.empty(self.rows * S, dtype=torch.int16, pin_memory=True)]
-        # allocate the second set on the device now (outside any timed region)
-        ctx.enqueue_write_buffer(self.q, b2[0], self.a_host, offset=self.lo * S * 2)
-        ctx.enqueue_write_buffer(self.q, b2[1], self.b_host)
-        ctx.enqueue_ndrange_range(self.q, k2, (S, S, 1), 2, self.lo, self.rows)
+        # allocate and touch both sets on the device now (outside any timed region)
+        for bB, chunks in self.sets:
+            ctx.enqueue_write_buffer(self.q, bB, self.b_host)
+            for c, (k, bA, bC, rc) in enumerate(chunks):
+                ctx.enqueue_write_buffer(self.q, bA, self.a_host[cb[c] * S:cb[c + 1] * S])
+                ctx.enqueue_ndrange_kernel(self.q, k, (rc, S, 1), 2)
         ctx.finish(self.q)
         self.e2e_i = 0
 
-    def e2e_step(self):
+    def _e2e_b(self, bB, blocking=False):
         ctx, q, S = self.ctx, self.q, self.S
-        s = self.e2e_i % 2
-        self.e2e_i += 1
-        k, bA, bB, bC = self.sets[s]
-        ctx.enqueue_write_buffer(q, bA, self.a_host, offset=self.lo * S * 2, blocking=False)
         if self.dist.world == 1:
-            ctx.enqueue_write_buffer(q, bB, self.b_host, blocking=False)
+            ctx.enqueue_write_buffer(q, bB, self.b_host, blocking=blocking)
         else:  # this rank's K-rows of B from host, the rest from the peers over NVLink
             r, kb = self.dist.rank, self.kb
             ctx.enqueue_write_buffer(q, bB, self.b_host[kb[r] * S:kb[r + 1] * S], offset=kb[r] * S * 2,
-                                     blocking=False)
-            ctx.enqueue_allgather(q, bB, [x * S * 2 for x in kb])
-        ctx.enqueue_ndrange_range(q, k, (S, S, 1), 2, self.lo, self.rows)
-        ctx.enqueue_read_buffer(q, bC, offset=self.lo * S * 2, length=self.rows * S * 2, out=self.c_hosts[s],
-                                blocking=False)
+                                     blocking=blocking)
+
+    def e2e_step(self):
+        ctx, q, S, cb = self.ctx, self.q, self.S, self.chunk_bounds
+        s = self.e2e_i % 2
+        self.e2e_i += 1
+        bB, chunks = self.sets[s]
+        self._e2e_b(bB)  # B first: the allgather (N > 1) needs every rank's slice
+        if self.dist.world > 1:
+            ctx.enqueue_allgather(q, bB, [x * S * 2 for x in self.kb])
+        for c, (k, bA, bC, rc) in enumerate(chunks):
+            ctx.enqueue_write_buffer(q, bA, self.a_host[cb[c] * S:cb[c + 1] * S], blocking=False)
+            ctx.enqueue_ndrange_kernel(q, k, (rc, S, 1), 2)
+            ctx.enqueue_read_buffer(q, bC, out=self.c_hosts[s][cb[c] * S:cb[c + 1] * S], blocking=False)
 
     def work_per_step(self):
         return 2.0 * self.S**3
@@ -337,8 +360,8 @@ class GemmBf16(Workload):
     def e2e_phases(self):
         """One e2e step with a device sync after each phase (wall ms on this rank):
         A rows + this rank's B slice H2D, the B allgather, the GEMM, C rows D2H."""
-        ctx, q, S, d = self.ctx, self.q, self.S, self.dist
-        k, bA, bB, bC = self.sets[0]
+        ctx, q, S, d, cb = self.ctx, self.q, self.S, self.dist, self.chunk_bounds
+        bB, chunks = self.sets[0]
         out = {}
 
         def phase(name, fn):
@@ -348,15 +371,17 @@ class GemmBf16(Workload):
             ctx.finish(q)
             out[name] = (time.perf_counter() - t) * 1e3
 
-        r, kb = d.rank, getattr(self, "kb", [0, S])
-        phase("h2d", lambda: (ctx.enqueue_write_buffer(q, bA, self.a_host, offset=self.lo * S * 2),
-                              ctx.enqueue_write_buffer(q, bB, self.b_host[kb[r] * S:kb[r + 1] * S] if d.world > 1
-                                                       else self.b_host, offset=kb[r] * S * 2 if d.world > 1 else 0)))
+        def h2d():
+            self._e2e_b(bB)
+            for c, (k, bA, bC, rc) in enumerate(chunks):
+                ctx.enqueue_write_buffer(q, bA, self.a_host[cb[c] * S:cb[c + 1] * S], blocking=False)
+
+        phase("h2d", h2d)
         if d.world > 1:
-            phase("allgather", lambda: ctx.enqueue_allgather(q, bB, [x * S * 2 for x in kb]))
-        phase("gemm", lambda: ctx.enqueue_ndrange_range(q, k, (S, S, 1), 2, self.lo, self.rows))
-        phase("d2h", lambda: ctx.enqueue_read_buffer(q, bC, offset=self.lo * S * 2, length=self.rows * S * 2,
-                                                     out=self.c_hosts[0]))
+            phase("allgather", lambda: ctx.enqueue_allgather(q, bB, [x * S * 2 for x in self.kb]))
+        phase("gemm", lambda: [ctx.enqueue_ndrange_kernel(q, k, (rc, S, 1), 2) for k, _, _, rc in chunks])
+        phase("d2h", lambda: [ctx.enqueue_read_buffer(q, bC, out=self.c_hosts[0][cb[c] * S:cb[c + 1] * S],
+                                                      blocking=False) for c, (_, _, bC, _) in enumerate(chunks)])
         return out
 
     def e2e_bytes(self):

@@ -11,7 +11,9 @@ oracle. Skipped on a single-GPU box; run by `gpurun --gpus 2|4`.
 * k-means: points split over the ranks, int64 NCCL allreduce of sums and
   counts; centroids after 2 iterations bit-identical to the oracle.
 * GEMM: B enters as 1/N K-row slices per rank + the NCCL allgather (the e2e
-  path); B complete and bit-identical on every rank, C rows within tolerance."""
+  path, the rank's rows in chunks whose C streams back while later chunks
+  compute); B complete and bit-identical on every rank, C rows within
+  tolerance and identical on the host."""
 import os
 import socket
 
@@ -89,11 +91,13 @@ def _gemm(bench, dist, args):
     wl.setup()
     wl.e2e_step()  # set 0: A rows + this rank's B slice from host, NCCL allgather of B, the GEMM
     wl.ctx.finish(wl.q)
-    k, bA, bB, bC = wl.sets[0]
+    bB, chunks = wl.sets[0]  # B, then the rank's row chunks (kernel, A, C, rows)
     S = wl.S
     b = wl.ctx.enqueue_read_buffer(wl.q, bB).view(np.uint16)
     ok_b = b.tobytes() == wl.b_host.numpy().view(np.uint16).tobytes()
-    c = wl.ctx.enqueue_read_buffer(wl.q, bC, offset=wl.lo * S * 2, length=wl.rows * S * 2).view(np.uint16)
+    c = np.concatenate([wl.ctx.enqueue_read_buffer(wl.q, bC).view(np.uint16) for _, _, bC, _ in chunks])
+    ok_host = c.tobytes() == wl.c_hosts[0].numpy().view(np.uint16).tobytes()  # the e2e D2H landed
+    assert ok_host, "e2e C rows on the host differ from the device's"
     return np.int64(wl.lo).tobytes() + np.int64(int(ok_b)).tobytes() + c.tobytes()
 
 
