@@ -202,7 +202,7 @@ def part_bin_options(n_edges: int, sm_count: int = 148) -> dict:
     n_edges / (32 * SMs), in [16384, 65536]; spans of up to 16384 sources (the
     largest with 65536-edge chunks in one shared-memory stage; longer spans mean
     fewer, fuller chunks). Measured at C3 (rank row ranges emulated on one GPU,
-    scratch/pr_rank_split.py; slowest part): N=1 65536/16384 0.967 ms vs 65536/8192
+    scripts/pr_rank_split.py; slowest part): N=1 65536/16384 0.967 ms vs 65536/8192
     0.993 (12288: 0.980); N=2 32768/16384 0.51 vs 0.56 ms; N=4 16384/16384 0.32 vs
     0.38 ms; N=8 16384/16384 0.23 vs 0.28 ms."""
     import math
