@@ -65,6 +65,11 @@ struct Cfg {
   static constexpr size_t kSmem = static_cast<size_t>(kStages) * kStage + kCBytes + 1024 + 256;
 };
 
+template <int CG, bool TF32, int BN, bool ONE>
+struct C_MC_OK {  // MC needs two 64-column B atoms per CTA (one per pair)
+  static constexpr bool value = Cfg<CG, TF32, BN, ONE>::kBNLocal / Cfg<CG, TF32, BN, ONE>::kMNAtom == 2;
+};
+
 struct TileMap {
   int num_m, num_n, group_m;
   __device__ __forceinline__ void get(int t, int& mt, int& nt) const {
@@ -78,7 +83,12 @@ struct TileMap {
   }
 };
 
-template <int CG, bool TF32, bool BMN, bool OUTF32, int BN, bool ONE>
+// MC: clusters of two CTA pairs computing vertically adjacent tiles (same B
+// columns); each CTA loads half of its B half and multicasts it to the
+// same-rank CTA of the other pair, so every B byte leaves L2 once per cluster
+// instead of twice. The stage's empty barrier then counts both pairs' MMA
+// commits (the other pair writes into this CTA's stage).
+template <int CG, bool TF32, bool BMN, bool OUTF32, int BN, bool ONE, bool MC = false>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmC, void* __restrict__ Cout, int M, int N, int K,
@@ -99,14 +109,18 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const uint32_t rank = CG == 2 ? ptx::cluster_ctarank() : 0;
+  const uint32_t crank = CG == 2 ? ptx::cluster_ctarank() : 0;
+  const uint32_t rank = MC ? (crank & 1u) : crank;  // CTA within its pair
+  const uint32_t lead = MC ? (crank & ~1u) : 0u;    // the pair's leader (cluster rank)
+  const uint32_t pr = MC ? (crank >> 1) : 0u;       // pair within the cluster
+  static_assert(!MC || (CG == 2 && BMN && C_MC_OK<CG, TF32, BN, ONE>::value), "MC: 2-CTA pairs, MN-major B");
 
   if (warp == 4 && lane == 0) {
     ptx::prefetch_tmap(&tmA);
     ptx::prefetch_tmap(&tmB);
     for (int s = 0; s < C::kStages; ++s) {
       ptx::mbar_init(&full[s], 1);
-      ptx::mbar_init(&empty[s], 1);
+      ptx::mbar_init(&empty[s], MC ? 2 : 1);
     }
     for (int a = 0; a < 2; ++a) {
       ptx::mbar_init(&tfull[a], 1);
@@ -155,9 +169,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           } else {
             if (rank == 0) ptx::mbar_arrive_expect_tx(&full[stage], C::kStage * 2);
-            const uint32_t bar = ptx::mapa(ptx::smem_u32(&full[stage]), 0);
+            const uint32_t bar = ptx::mapa(ptx::smem_u32(&full[stage]), lead);
             ptx::tma_load_2d_pair(sa, &tmA, bar, kb * C::kBK, m0);
-            if constexpr (BMN) {
+            if constexpr (BMN && MC) {  // atom pr of this CTA's B half, to the same-rank CTA of both pairs
+              ptx::tma_load_2d_pair_mc(sb + pr * C::kBK * 128, &tmB, ptx::smem_u32(&full[stage]) & 0xFEFFFFFFu,
+                                       static_cast<uint16_t>(0x5u << rank), n0 + static_cast<int>(pr) * C::kMNAtom,
+                                       kb * C::kBK);
+            } else if constexpr (BMN) {
 #pragma unroll
               for (int j = 0; j < C::kBNLocal / C::kMNAtom; ++j)
                 ptx::tma_load_2d_pair(sb + j * C::kBK * 128, &tmB, bar, n0 + j * C::kMNAtom, kb * C::kBK);
@@ -201,10 +219,16 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint64_t bdesc = bdesc0 + so + static_cast<uint64_t>((BMN ? k * (C::kUK / 8) * 1024 : k * 32) >> 4);
             ptx::mma_elect<CG, TF32>(d_tmem, adesc, bdesc, idesc, (kb != kb0) | (k != 0));
           }
-          ptx::mma_commit_elect<CG>(&empty[stage]);  // frees the smem slot when these MMAs finish
+          if constexpr (MC)  // both pairs write into every CTA's stage: release it in all four
+            ptx::mma_commit_elect_mask(&empty[stage], 0xF);
+          else
+            ptx::mma_commit_elect<CG>(&empty[stage]);  // frees the smem slot when these MMAs finish
           if (++stage == C::kStages) { stage = 0; phase ^= 1; }
         }
-        ptx::mma_commit_elect<CG>(&tfull[acc]);  // accumulator ready for the epilogue
+        if constexpr (MC)
+          ptx::mma_commit_elect_mask(&tfull[acc], static_cast<uint16_t>(0x3u << (2 * pr)));
+        else
+          ptx::mma_commit_elect<CG>(&tfull[acc]);  // accumulator ready for the epilogue
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
     }
@@ -290,7 +314,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
       if (lane == 0) {
         // relaxed: this barrier only returns the TMEM accumulator (no global-store ordering needed)
-        ptx::mbar_arrive_cluster_relaxed(ptx::mapa(ptx::smem_u32(&tempty[acc]), 0));
+        ptx::mbar_arrive_cluster_relaxed(ptx::mapa(ptx::smem_u32(&tempty[acc]), lead));
       }
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
@@ -376,7 +400,7 @@ CUtensorMap make_tmap(const void* base, bool f32, uint64_t inner, uint64_t outer
   return m;
 }
 
-template <int CG, bool TF32, bool BMN, bool OUTF32, int BN = 256, bool ONE = false>
+template <int CG, bool TF32, bool BMN, bool OUTF32, int BN = 256, bool ONE = false, bool MC = false>
 void run_gemm(const void* A, const void* B, void* Cp, int64_t M, int64_t N, int64_t K, int64_t ldc,
               int sm_count, cudaStream_t stream, int group_m, bool persistent, int ksplit = 1) {
   using C = Cfg<CG, TF32, BN, ONE>;
@@ -397,7 +421,7 @@ void run_gemm(const void* A, const void* B, void* Cp, int64_t M, int64_t N, int6
                              CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) fail(ErrorCode::argument, "cuTensorMapEncodeTiled (C) failed");
   }
-  auto kern = gemm_tc_kernel<CG, TF32, BMN, OUTF32, BN, ONE>;
+  auto kern = gemm_tc_kernel<CG, TF32, BMN, OUTF32, BN, ONE, MC>;
   // per launch: the attribute is per device context and launches may target several GPUs
   HCL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(C::kSmem)));
   const int64_t tiles = ceil_div(M, kBM * CG) * ceil_div(N, BN) * ksplit;
@@ -417,7 +441,7 @@ void run_gemm(const void* A, const void* B, void* Cp, int64_t M, int64_t N, int6
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.x = MC ? 2 * CG : CG;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
@@ -456,6 +480,15 @@ int pick_shape(int64_t M, int64_t N, int sm_count, int ksplit = 1) {
   return best;
 }
 
+// B multicast across two CTA pairs (HCL_GEMM_MC=1): the clusters' two tiles must be
+// vertically adjacent with the same B columns -- whole raster groups of an even
+// number of M tiles, an even tile count, no K split
+bool mc_ok(int64_t M, int64_t N, int group_m, int ksplit) {
+  if (env_int("HCL_GEMM_MC", 0) == 0 || ksplit != 1 || group_m % 2) return false;
+  const int64_t num_m = ceil_div(M, kBM * 2), num_n = ceil_div(N, 256);
+  return num_m % group_m == 0 && (num_m * num_n) % 2 == 0;
+}
+
 template <bool TF32, bool BMN, bool OUTF32>
 void dispatch_shape(int shape, const void* a, const void* b, void* cp, int64_t M, int64_t n, int64_t k,
                     const LaunchCtx& c, int group_m, int ksplit = 1) {
@@ -471,8 +504,14 @@ void dispatch_shape(int shape, const void* a, const void* b, void* cp, int64_t M
       run_gemm<1, TF32, BMN, OUTF32, 64>(a, b, cp, M, n, k, n, c.sm_count, c.stream, group_m, persist, ksplit);
       break;
     default:
-      if (persist || env_int("HCL_GEMM_ONE", 1) == 0)
+      if (!persist && env_int("HCL_GEMM_ONE", 1) == 0 && mc_ok(M, n, group_m, ksplit) && BMN && !TF32)
+        run_gemm<2, TF32, BMN, OUTF32, 256, false, BMN && !TF32>(a, b, cp, M, n, k, n, c.sm_count, c.stream, group_m,
+                                                                false, ksplit);
+      else if (persist || env_int("HCL_GEMM_ONE", 1) == 0)
         run_gemm<2, TF32, BMN, OUTF32, 256>(a, b, cp, M, n, k, n, c.sm_count, c.stream, group_m, persist, ksplit);
+      else if (mc_ok(M, n, group_m, ksplit) && BMN && !TF32)
+        run_gemm<2, TF32, BMN, OUTF32, 256, true, BMN && !TF32>(a, b, cp, M, n, k, n, c.sm_count, c.stream, group_m,
+                                                               false, ksplit);
       else
         run_gemm<2, TF32, BMN, OUTF32, 256, true>(a, b, cp, M, n, k, n, c.sm_count, c.stream, group_m, false,
                                                   ksplit);

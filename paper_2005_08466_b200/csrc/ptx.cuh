@@ -258,6 +258,30 @@ __device__ __forceinline__ void mma_commit_elect(uint64_t* bar) {
         : "memory");
 }
 
+// tcgen05.commit to the barrier at `bar`'s offset in every CTA of `mask` (cluster
+// ranks), one elected lane of the calling warp
+__device__ __forceinline__ void mma_commit_elect_mask(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}" ::"r"(
+          smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
+
+// 2D tile load for a CTA pair, multicast to the CTAs of `mask` (same smem offset in
+// each); the bytes complete on the barrier at `bar_cta`'s offset in each
+// destination's pair leader (bar_cta: this CTA's barrier address with the peer bit
+// cleared, the CUTLASS SM100_TMA_2SM_LOAD_MULTICAST convention)
+__device__ __forceinline__ void tma_load_2d_pair_mc(void* smem, const CUtensorMap* m, uint32_t bar_cta, uint16_t mask,
+                                                    int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%4, %5}], [%2], %3;" ::"r"(smem_u32(smem)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(bar_cta), "h"(mask), "r"(c0), "r"(c1)
+      : "memory");
+}
+
 // Arrive on `bar` (same smem offset in every CTA of `mask`) when all prior
 // tcgen05.mma of this thread complete. Implies fence::before_thread_sync.
 template <int CG>

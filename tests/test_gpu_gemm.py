@@ -254,3 +254,20 @@ def test_gemm_f32x3_ksplit(ctx, queues, monkeypatch):
     assert normwise_err(whole, a.astype(np.float64).reshape(m, k), b.astype(np.float64).reshape(k, n)) <= 2.0**-16
     part = gemm(ctx, queues, "gemm_f32x3", a, b, m, k, n, P=4, weights=[1, 2, 3, 4])
     assert whole.tobytes() == part.tobytes()
+
+
+@pytest.mark.parametrize("one", ["1", "0"])
+def test_gemm_bf16_b_multicast_bit_identical(ctx, queues, monkeypatch, one):
+    """HCL_GEMM_MC=1: clusters of two CTA pairs on vertically adjacent tiles, each
+    B atom loaded once and multicast to both pairs (TMA .multicast::cluster) --
+    the same MMAs in the same order, so C is bit-identical to the default path."""
+    m = n = 4096
+    k = 1024
+    a = O.gen_bf16(m * k, 42)
+    b = O.gen_bf16(k * n, 43)
+    monkeypatch.setenv("HCL_GEMM_ONE", one)
+    monkeypatch.setenv("HCL_GEMM_MC", "0")
+    want = gemm(ctx, queues, "gemm_bf16", a, b, m, k, n, out_f32=False)  # C2's bf16-out (TMA-store) path
+    monkeypatch.setenv("HCL_GEMM_MC", "1")
+    got = gemm(ctx, queues, "gemm_bf16", a, b, m, k, n, out_f32=False)
+    assert got.tobytes() == want.tobytes()
