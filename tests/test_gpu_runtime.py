@@ -238,3 +238,35 @@ def test_bind_external_memory(ctx, queues):
     with pytest.raises(Exception):
         ctx.bind_external(queues[0], ctx.create_buffer(8), 0)  # null pointer: argument error
     assert dev == ctx.get_device_ids()[0]
+
+
+def test_zero_row_parts(ctx, queues):
+    """Empty parts: a partitioned launch whose weights give one queue no rows, and
+    a rank-style sub-range launch of zero rows, leave the result exactly as the
+    whole launch computes it (the empty part launches nothing and moves nothing)."""
+    if len(queues) < 2:
+        pytest.skip("needs two logical devices")
+    m, n, k = 300, 256, 128
+    a = O.gen_bf16(m * k, 42)
+    b = O.gen_bf16(k * n, 43)
+    outs = []
+    for mode in ("whole", "zero-weight", "zero-range"):
+        kh = kernel(ctx, "b200", "gemm_bf16", [])
+        ba, bb, bc = ctx.create_buffer(a.nbytes), ctx.create_buffer(b.nbytes), ctx.create_buffer(m * n * 4)
+        ctx.enqueue_write_buffer(queues[0], ba, a)
+        ctx.enqueue_write_buffer(queues[0], bb, b)
+        for i, v in enumerate([ba, bb, bc, m, k, n, 1]):
+            ctx.set_kernel_arg(kh, i, v)
+        if mode == "whole":
+            ctx.enqueue_ndrange_kernel(queues[0], kh, (m, n, 1), 2)
+        elif mode == "zero-weight":
+            ctx.enqueue_ndrange_partitioned(kh, (m, n, 1), 2, queues[:2], [0, 1])
+        else:
+            ctx.enqueue_ndrange_range(queues[1], kh, (m, n, 1), 2, 0, 0)  # nothing
+            ctx.enqueue_ndrange_range(queues[0], kh, (m, n, 1), 2, 0, m)
+        for q in queues[:2]:
+            ctx.finish(q)
+        outs.append(ctx.enqueue_read_buffer(queues[0], bc).tobytes())
+        for x in (ba, bb, bc, kh):
+            ctx.release(x)
+    assert outs[1] == outs[0] and outs[2] == outs[0]
