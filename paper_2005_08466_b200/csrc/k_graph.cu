@@ -803,7 +803,9 @@ __global__ void __launch_bounds__(PBG_T) pr_bin_gather_kernel(const int64_t* __r
         const int sw = pb_swz(static_cast<int>(dd[k]));
         const unsigned old = atoms_add_if(acc_lo + sw, ql, last && ql != 0u);
         const unsigned qh = static_cast<unsigned>(run >> 32) + (old + ql < ql);  // carry out of the low word
-        if (__any_sync(0xffffffffu, last && qh != 0u)) reds_add_if(acc_hi + sw, qh, last && qh != 0u);
+        // predicated, not branched on a vote: the vote's convergence barriers cost more
+        // issue slots than the mostly-off red (gather 469 -> 449 us at C3)
+        reds_add_if(acc_hi + sw, qh, last && qh != 0u);
       }
     }
     __syncwarp();
