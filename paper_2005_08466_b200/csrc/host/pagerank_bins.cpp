@@ -14,7 +14,8 @@
 //     a hub row's entries form runs the gather adds up before its atomics);
 //     gtab[s][j] is where segment (s, j)
 //     starts, gtab[S][j] where bin j's entries end. dst16[] holds each entry's
-//     destination as an offset inside its bin. Bins start at multiples of 8
+//     destination as an offset inside its bin, bank-folded (o ^ ((o >> 5) & 31) ^
+//     ((o >> 10) & 31): the gather's accumulator word, an involution). Bins start at multiples of 8
 //     entries (padding entries: destination 0, value 0, which adds nothing).
 //   * per chunk, a descriptor for the scatter: for every 32-entry window of
 //     the chunk's bin-grouped entries {bitmap of the entries that start a
@@ -204,7 +205,10 @@ void* hcl_pagerank_bins_build(const int32_t* row_ptr, const int32_t* col_idx, in
         if (loc[j + 1] - loc[j] > 1) std::sort(key.begin() + loc[j], key.begin() + loc[j + 1]);
         for (int64_t q = loc[j]; q < loc[j + 1]; ++q) {
           b->src_local[src_off[s] + q] = static_cast<uint16_t>(key[q] & 0xffffu);
-          b->dst16[G[s * gs + j] + (q - loc[j])] = static_cast<uint16_t>(key[q] >> 16);
+          // stored bank-folded (pb_swz in csrc/k_graph.cu, an involution inside each
+          // 32-row block): the gather indexes its accumulator with it directly
+          const uint32_t d = key[q] >> 16;
+          b->dst16[G[s * gs + j] + (q - loc[j])] = static_cast<uint16_t>(d ^ ((d >> 5) & 31u) ^ ((d >> 10) & 31u));
         }
         win[2 * (loc[j] / 32)] |= 1u << (loc[j] % 32);
         dl[k++] = static_cast<int32_t>(static_cast<int64_t>(G[s * gs + j]) - loc[j]);

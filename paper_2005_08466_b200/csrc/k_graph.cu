@@ -800,7 +800,7 @@ __global__ void __launch_bounds__(PBG_T) pr_bin_gather_kernel(const int64_t* __r
         run = (k > 0 && dd[k] == dd[k - 1]) ? run + q : q;
         const bool last = k == 7 || dd[k] != dd[k + 1];
         const unsigned ql = static_cast<unsigned>(run);
-        const int sw = pb_swz(static_cast<int>(dd[k]));
+        const int sw = static_cast<int>(dd[k]);  // dst16 is stored bank-folded (pb_swz)
         const unsigned old = atoms_add_if(acc_lo + sw, ql, last && ql != 0u);
         const unsigned qh = static_cast<unsigned>(run >> 32) + (old + ql < ql);  // carry out of the low word
         // predicated, not branched on a vote: the vote's convergence barriers cost more

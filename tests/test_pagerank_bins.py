@@ -57,7 +57,9 @@ def decode(L, v):
     dst = np.full(L["n_entries"], -1, np.int64)
     for j in range(B):
         assert g[0, j] % 8 == 0
-        dst[g[0, j]:g[S, j]] = L["lo"] + j * W + L["dst16"][g[0, j]:g[S, j]].astype(np.int64)
+        o = L["dst16"][g[0, j]:g[S, j]].astype(np.int64)
+        o = o ^ ((o >> 5) & 31) ^ ((o >> 10) & 31)  # stored bank-folded (an involution)
+        dst[g[0, j]:g[S, j]] = L["lo"] + j * W + o
     m = src >= 0
     assert ((dst >= 0) == m).all() and (dst[m] < L["hi"]).all()
     # units tile each bin's padded range; split bins carry a slot with their unit count
