@@ -743,7 +743,9 @@ __global__ void __launch_bounds__(PBG_T) pr_bin_gather_kernel(const int64_t* __r
   uint64_t* full = reinterpret_cast<uint64_t*>(stage0 + PBG_STAGES * PBG_STAGE_BYTES);
   uint64_t* empty = full + PBG_STAGES;
   unsigned* acc_lo = reinterpret_cast<unsigned*>(empty + PBG_STAGES);
-  unsigned* acc_hi = acc_lo + ((W + 31) & ~int64_t(31));  // whole 32-row blocks (pb_swz)
+  // whole 32-row blocks (pb_swz); with <= 8192-row bins the high words sit at a
+  // constant offset, so each atomic pair shares one address register
+  unsigned* acc_hi = acc_lo + (PBG_T == 512 ? 8192 : ((W + 31) & ~int64_t(31)));
   const int4 U = __ldg(units + part[PB_UNIT0] + blockIdx.x);  // bin, e0, e1, slot
   const int64_t row0 = lo + static_cast<int64_t>(U.x) * W;
   const int64_t rem = hi - row0;
@@ -969,7 +971,7 @@ uint64_t launch_pr_binned(LaunchCtx& c) {
   const bool small_bins = W <= 8192;
   const int gt = small_bins ? 512 : 1024;
   const size_t smem2 = static_cast<size_t>(PBG_STAGES) * 8 * gt * 6 + 2 * PBG_STAGES * 8 +
-                       static_cast<size_t>((W + 31) & ~int64_t(31)) * 8;
+                       (small_bins ? 8192 * 8 : static_cast<size_t>((W + 31) & ~int64_t(31)) * 8);
   auto gkern = small_bins ? pr_bin_gather_kernel<512> : pr_bin_gather_kernel<1024>;
   HCL_CUDA(cudaFuncSetAttribute(gkern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem2)));
   const int64_t n_slots_total = static_cast<int64_t>(SA.bytes / (W * 8 + 4));
