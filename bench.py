@@ -742,7 +742,8 @@ class PageRankW(Workload):
                                        n_peers, self.b_inv, self.b_xs2[1 - i], self.b_dsum2[1 - i])
                         for i in range(2)]
         prog = ctx.create_program("b200")
-        self.k_prep0 = ctx.create_kernel(prog, "pagerank_prep")  # x0 -> xs[0], dsum[0]
+        # x0 -> xs[0] (scaled by 2^56: the binned step's fixed-point gather input), dsum[0]
+        self.k_prep0 = ctx.create_kernel(prog, "pagerank_prep_fixed")
         for j, a in enumerate([self.b_x[0], self.b_deg, self.b_dsum2[0], self.b_xs2[0], self.v]):
             ctx.set_kernel_arg(self.k_prep0, j, a)
         self.traffic_key = f"pagerank_step_binned_scale{self.scale}"

@@ -114,6 +114,7 @@ struct Fanout {
   float* xs;            // this device's xs'
   const float* inv;     // fl(1/outdeg), 0 for dangling vertices
   float* mc;            // NVSwitch multicast address of xs' on every rank (n_peers == PR_MULTICAST), else null
+  float scale;          // xs' = fl(inv * x') * scale: 1, or 2^56 for the binned step (exact: a power of two)
 };
 
 // n_peers == PR_MULTICAST: peers[0] is the multicast mapping of the ranks' xs'
@@ -121,8 +122,10 @@ struct Fanout {
 // is 4 bytes whatever the rank count, not 4 * (N - 1))
 constexpr int PR_MULTICAST = -1;
 
-__device__ __forceinline__ Fanout load_fanout(const unsigned long long* peers, int n, float* xs, const float* inv) {
+__device__ __forceinline__ Fanout load_fanout(const unsigned long long* peers, int n, float* xs, const float* inv,
+                                              float scale = 1.f) {
   Fanout f;
+  f.scale = scale;
   f.mc = n == PR_MULTICAST ? reinterpret_cast<float*>(__ldg(peers)) : nullptr;
   f.n = n < 0 ? 0 : n;
   f.xs = xs;
@@ -142,7 +145,7 @@ __device__ __forceinline__ void pr_store_x(float* __restrict__ y, int r, int lo,
   const float v = pr_store<UPDATE>(y, r, lo, s, u);
   if constexpr (XCH) {
     const float inv = __ldg(f.inv + r);  // the division is done once per graph, not per step
-    const float xs = __fmul_rn(inv, v);
+    const float xs = __fmul_rn(__fmul_rn(inv, v), f.scale);
     f.xs[r] = xs;  // (the multicast store lands here too, the same value)
     if (f.mc) multimem_st(f.mc + r, xs);
 #pragma unroll
@@ -442,7 +445,7 @@ uint64_t launch_pr(LaunchCtx& c) {
 // to val[p] * x[col[p]], and the 4-byte-per-edge value stream disappears.
 __global__ void __launch_bounds__(256) pr_prep_kernel(const float* __restrict__ x, const int* __restrict__ outdeg,
                                                       int64_t v, float* __restrict__ xs,
-                                                      unsigned long long* __restrict__ out) {
+                                                      unsigned long long* __restrict__ out, float scale) {
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   unsigned long long s = 0;
@@ -450,13 +453,15 @@ __global__ void __launch_bounds__(256) pr_prep_kernel(const float* __restrict__ 
     const int d = __ldcs(outdeg + i);
     const float xi = __ldcs(x + i);
     if (d == 0) s += static_cast<unsigned long long>(__float2ll_rz(__fmul_rn(xi, 0x1p56f)));
-    xs[i] = d ? __fmul_rn(__fdiv_rn(1.0f, static_cast<float>(d)), xi) : 0.f;
+    xs[i] = d ? __fmul_rn(__fmul_rn(__fdiv_rn(1.0f, static_cast<float>(d)), xi), scale) : 0.f;
   }
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
   if ((threadIdx.x & 31) == 0 && s) atomicAdd(out, s);
 }
 
-// pagerank_prep(x, outdeg, dsum, xs, V)
+// pagerank_prep(x, outdeg, dsum, xs, V); pagerank_prep_fixed: the same with xs scaled by
+// 2^56 (the binned step's gather input: its fixed-point terms are then one conversion)
+template <bool FIXED>
 uint64_t launch_pr_prep(LaunchCtx& c) {
   int64_t v = scalar_arg(c, 4, "pagerank_prep V");
   const BufView& X = buffer_arg(c, 0, "pagerank_prep x");
@@ -472,7 +477,7 @@ uint64_t launch_pr_prep(LaunchCtx& c) {
   pr_prep_kernel<<<grid, 256, 0, c.stream>>>(reinterpret_cast<const float*>(X.ptr),
                                              reinterpret_cast<const int*>(O.ptr), v,
                                              reinterpret_cast<float*>(XS.ptr),
-                                             reinterpret_cast<unsigned long long*>(D.ptr));
+                                             reinterpret_cast<unsigned long long*>(D.ptr), FIXED ? 0x1p56f : 1.f);
   HCL_LAUNCHED();
   return static_cast<uint64_t>(v);
 }
@@ -798,7 +803,9 @@ __global__ void __launch_bounds__(PBG_T) pr_bin_gather_kernel(const int64_t* __r
       unsigned long long run = 0;
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
-        const unsigned long long q = __float2ull_rn(__fmul_rn(vv[k], 0x1p56f));
+        // the gather input is scaled by 2^56 (pagerank_prep_fixed / the epilogue below):
+        // the fixed-point term is one conversion, the same value as fl(v * 2^56)
+        const unsigned long long q = __float2ull_rn(vv[k]);
         run = (k > 0 && dd[k] == dd[k - 1]) ? run + q : q;
         const bool last = k == 7 || dd[k] != dd[k + 1];
         const unsigned ql = static_cast<unsigned>(run);
@@ -844,7 +851,7 @@ __global__ void __launch_bounds__(PBG_T) pr_bin_gather_kernel(const int64_t* __r
     __syncthreads();
   }
   const Update upd = pr_update<true>(dsum, base, damp, inv_v);
-  const Fanout fo = load_fanout(peers, n_peers, xs_next, inv_outdeg);
+  const Fanout fo = load_fanout(peers, n_peers, xs_next, inv_outdeg, 0x1p56f);
   unsigned long long dang = 0;
   for (int r = threadIdx.x; r < nrows; r += PBG_T) {
     const float s = static_cast<float>(__ll2double_rn(static_cast<long long>(acc(r))) * 0x1p-56);
@@ -866,6 +873,7 @@ std::mutex g_pb_mu;
 std::map<PbKey, std::vector<PbPartRow>> g_pb_parts;
 
 // pagerank_step_binned(parts chunks src_local gtab dst16 units slot_units xs dsum x' | V n_parts |
+// (xs and xs' are the gather inputs scaled by 2^56: pagerank_prep_fixed, this epilogue)
 //                      peers n_peers inv_outdeg xs' dsum' | vals(LOCAL) slot_acc(LOCAL))
 uint64_t launch_pr_binned(LaunchCtx& c) {
   const char* what = "pagerank_step_binned";
@@ -1008,7 +1016,9 @@ void register_graph(std::vector<KernelDef>& r) {
   r.push_back({"b200", "pagerank_dangling", {I, I, O, S}, {P, P, P, N}, launch_pr_dangling, nullptr, nullptr});
   // implicit values (val = 1/outdeg(src)): pagerank_prep(x, outdeg, dsum, xs, V), then
   // pagerank_step_implicit(row_ptr col units long_rows xs dsum x' | V nnz_off n_units n_long warp_nnz)
-  r.push_back({"b200", "pagerank_prep", {I, I, O, O, S}, {P, P, P, P, N}, launch_pr_prep, nullptr, nullptr});
+  r.push_back({"b200", "pagerank_prep", {I, I, O, O, S}, {P, P, P, P, N}, launch_pr_prep<false>, nullptr, nullptr});
+  r.push_back({"b200", "pagerank_prep_fixed", {I, I, O, O, S}, {P, P, P, P, N}, launch_pr_prep<true>, nullptr,
+               nullptr});
   r.push_back({"b200", "pagerank_step_implicit", {I, I, I, I, I, I, O, S, S, S, S, S},
                {P, P, P, P, P, P, X, N, N, N, N, N}, launch_pr<true, true>, nullptr, rows_pr_imp});
   // the implicit step fused with the next prep and the exchange: x' rows, xs' rows here and on

@@ -115,7 +115,8 @@ class PageRank:
         ctx.enqueue_write_buffer(q0, self.b_inv, pagerank_inv_outdeg(outdeg))
         self.b_peers = mk(8 * max(1, n_parts - 1))
         prog = ctx.create_program("b200")
-        self.k_prep0 = ctx.create_kernel(prog, "pagerank_prep")
+        # the binned step's gather input is xs scaled by 2^56 (its fixed-point grid)
+        self.k_prep0 = ctx.create_kernel(prog, "pagerank_prep_fixed")
         for j, a in enumerate([self.b_x[0], self.b_deg, self.b_dsum2[0], self.b_xs2[0], self.v]):
             ctx.set_kernel_arg(self.k_prep0, j, a)
         self.k_bin = [self.bl.kernel(self.v, self.b_xs2[i], self.b_dsum2[i], self.b_x[0], self.b_peers, n_parts - 1,
