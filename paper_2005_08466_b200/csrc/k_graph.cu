@@ -810,8 +810,12 @@ __global__ void __launch_bounds__(PBG_T) pr_bin_gather_kernel(const int64_t* __r
         const bool last = k == 7 || dd[k] != dd[k + 1];
         const unsigned ql = static_cast<unsigned>(run);
         const int sw = static_cast<int>(dd[k]);  // dst16 is stored bank-folded (pb_swz)
-        const unsigned old = atoms_add_if(acc_lo + sw, ql, last && ql != 0u);
-        const unsigned qh = static_cast<unsigned>(run >> 32) + (old + ql < ql);  // carry out of the low word
+        const unsigned old = atoms_add_if(acc_lo + sw, ql, last);  // (a zero ql adds nothing)
+        // carry out of the low word: add with carry-out, then the high half plus the carry
+        unsigned qh;
+        asm("{\n\t.reg .u32 t;\n\tadd.cc.u32 t, %1, %2;\n\taddc.u32 %0, %3, 0;\n\t}"
+            : "=r"(qh)
+            : "r"(old), "r"(ql), "r"(static_cast<unsigned>(run >> 32)));
         // predicated, not branched on a vote: the vote's convergence barriers cost more
         // issue slots than the mostly-off red (gather 469 -> 449 us at C3)
         reds_add_if(acc_hi + sw, qh, last && qh != 0u);
