@@ -133,6 +133,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   if constexpr (CG == 2) ptx::cluster_sync(); else __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  ptx::grid_dep_wait();  // the prologue above overlaps the producing launch's tail (PDL)
+  ptx::grid_dep_launch();
 
   const TileMap map{static_cast<int>((M + kBM * CG - 1) / (kBM * CG)), (N + kBN - 1) / kBN, group_m};
   const int tiles = map.num_m * map.num_n;
@@ -402,7 +404,7 @@ CUtensorMap make_tmap(const void* base, bool f32, uint64_t inner, uint64_t outer
 
 template <int CG, bool TF32, bool BMN, bool OUTF32, int BN = 256, bool ONE = false, bool MC = false>
 void run_gemm(const void* A, const void* B, void* Cp, int64_t M, int64_t N, int64_t K, int64_t ldc,
-              int sm_count, cudaStream_t stream, int group_m, bool persistent, int ksplit = 1) {
+              int sm_count, cudaStream_t stream, int group_m, bool persistent, int ksplit = 1, bool pdl = false) {
   using C = Cfg<CG, TF32, BN, ONE>;
   const uint64_t es = C::kElem;
   const CUtensorMapL2promotion promo = l2_promotion();
@@ -439,13 +441,15 @@ void run_gemm(const void* A, const void* B, void* Cp, int64_t M, int64_t N, int6
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = C::kSmem;
   cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = MC ? 2 * CG : CG;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl ? 2 : 1;
   HCL_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, tc, Cp, static_cast<int>(M), static_cast<int>(N),
                               static_cast<int>(K), ldc, group_m, tma_c, ksplit));
   HCL_LAUNCHED();
@@ -491,30 +495,30 @@ bool mc_ok(int64_t M, int64_t N, int group_m, int ksplit) {
 
 template <bool TF32, bool BMN, bool OUTF32>
 void dispatch_shape(int shape, const void* a, const void* b, void* cp, int64_t M, int64_t n, int64_t k,
-                    const LaunchCtx& c, int group_m, int ksplit = 1) {
+                    const LaunchCtx& c, int group_m, int ksplit = 1, bool pdl = false) {
   const bool persist = c.sm_budgeted || env_int("HCL_GEMM_PERSIST", 0) != 0;
   switch (shape) {
     case 1:
-      run_gemm<1, TF32, BMN, OUTF32, 256>(a, b, cp, M, n, k, n, c.sm_count, c.stream, group_m, persist, ksplit);
+      run_gemm<1, TF32, BMN, OUTF32, 256>(a, b, cp, M, n, k, n, c.sm_count, c.stream, group_m, persist, ksplit, pdl);
       break;
     case 2:
-      run_gemm<2, TF32, BMN, OUTF32, 128>(a, b, cp, M, n, k, n, c.sm_count, c.stream, group_m, persist, ksplit);
+      run_gemm<2, TF32, BMN, OUTF32, 128>(a, b, cp, M, n, k, n, c.sm_count, c.stream, group_m, persist, ksplit, pdl);
       break;
     case 3:
-      run_gemm<1, TF32, BMN, OUTF32, 64>(a, b, cp, M, n, k, n, c.sm_count, c.stream, group_m, persist, ksplit);
+      run_gemm<1, TF32, BMN, OUTF32, 64>(a, b, cp, M, n, k, n, c.sm_count, c.stream, group_m, persist, ksplit, pdl);
       break;
     default:
       if (!persist && env_int("HCL_GEMM_ONE", 1) == 0 && mc_ok(M, n, group_m, ksplit) && BMN && !TF32)
         run_gemm<2, TF32, BMN, OUTF32, 256, false, BMN && !TF32>(a, b, cp, M, n, k, n, c.sm_count, c.stream, group_m,
-                                                                false, ksplit);
+                                                                false, ksplit, pdl);
       else if (persist || env_int("HCL_GEMM_ONE", 1) == 0)
-        run_gemm<2, TF32, BMN, OUTF32, 256>(a, b, cp, M, n, k, n, c.sm_count, c.stream, group_m, persist, ksplit);
+        run_gemm<2, TF32, BMN, OUTF32, 256>(a, b, cp, M, n, k, n, c.sm_count, c.stream, group_m, persist, ksplit, pdl);
       else if (mc_ok(M, n, group_m, ksplit) && BMN && !TF32)
         run_gemm<2, TF32, BMN, OUTF32, 256, true, BMN && !TF32>(a, b, cp, M, n, k, n, c.sm_count, c.stream, group_m,
-                                                               false, ksplit);
+                                                               false, ksplit, pdl);
       else
         run_gemm<2, TF32, BMN, OUTF32, 256, true>(a, b, cp, M, n, k, n, c.sm_count, c.stream, group_m, false,
-                                                  ksplit);
+                                                  ksplit, pdl);
       break;
   }
 }
@@ -522,6 +526,7 @@ void dispatch_shape(int shape, const void* a, const void* b, void* cp, int64_t M
 // C = sum over the ksplit workspace slices, in slice order (deterministic)
 __global__ void __launch_bounds__(256) ksplit_reduce_kernel(const float4* __restrict__ ws, float4* __restrict__ out,
                                                             int64_t n4, int ksplit) {
+  ptx::grid_dep_wait();
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += stride) {
     float4 a = ws[i];
@@ -599,7 +604,7 @@ uint64_t launch_gemm_tc(LaunchCtx& c) {
 // The three products become ONE K-major TF32 GEMM over K' = 3K:
 //   A'[r] = [hi(a_r) | hi(a_r) | lo(a_r)],  B'^T[n] = [hi(b_n) | lo(b_n) | hi(b_n)]
 // built by one memory-bound split launch (A rows and B columns), then the same tcgen05 kernel as
-// gemm_tf32. The split products are exact, but the tensor core's fp32
+// gemm_tf32 (and the K-slice reduction), chained as programmatic dependent launches. The split products are exact, but the tensor core's fp32
 // accumulation truncates per MMA, so the measured normwise error is ~2^-19 at
 // K=1024 and ~2^-17 at K=16384 (SIMT gemm_f32: ~2^-22) -- at 1/3 of the TF32
 // tensor rate instead of the FFMA rate (16384^3: 192 vs 37 TFLOP/s).
@@ -702,12 +707,24 @@ uint64_t launch_gemm_f32x3(LaunchCtx& c) {
   const int group_m = std::max(1, env_int("HCL_GEMM_GROUP", kGroupM));
   int shape = env_int("HCL_GEMM_SHAPE", -1);
   if (shape < 0 || shape > 3) shape = pick_shape(r, n, c.sm_count, ksplit);
-  dispatch_shape<true, false, true>(shape, a3, b3, ksplit > 1 ? ws : cp, r, n, 3 * k, c, group_m, ksplit);
+  // programmatic dependent launches: split -> GEMM -> reduce overlap each launch's
+  // prologue with the previous one's tail (HCL_GEMM_PDL=0: plain stream order)
+  const bool pdl = env_int("HCL_GEMM_PDL", 1) != 0;
+  dispatch_shape<true, false, true>(shape, a3, b3, ksplit > 1 ? ws : cp, r, n, 3 * k, c, group_m, ksplit, pdl);
   if (ksplit > 1) {
     const int64_t n4 = r * n / 4;  // N % 4 == 0
     const unsigned blocks = static_cast<unsigned>(std::min<int64_t>(ceil_div(n4, 256), 8LL * c.sm_count));
-    ksplit_reduce_kernel<<<blocks, 256, 0, c.stream>>>(reinterpret_cast<const float4*>(ws),
-                                                       reinterpret_cast<float4*>(cp), n4, ksplit);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(blocks);
+    cfg.blockDim = dim3(256);
+    cfg.stream = c.stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    HCL_CUDA(cudaLaunchKernelEx(&cfg, ksplit_reduce_kernel, reinterpret_cast<const float4*>(ws),
+                                reinterpret_cast<float4*>(cp), n4, ksplit));
     HCL_LAUNCHED();
   }
   return 2ull * rows * static_cast<uint64_t>(n) * static_cast<uint64_t>(k);

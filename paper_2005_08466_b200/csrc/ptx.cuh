@@ -357,4 +357,11 @@ __host__ __device__ constexpr uint32_t umma_idesc(uint32_t fmt, uint32_t a_major
          | (a_major << 15) | (b_major << 16) | ((n >> 3) << 17) | ((m >> 4) << 24);
 }
 
+// Programmatic dependent launch: wait until the preceding kernel of the stream
+// has completed and its writes are visible (a no-op when this launch was not
+// made with cudaLaunchAttributeProgrammaticStreamSerialization)
+__device__ __forceinline__ void grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// ... and let the next launch of the stream start its prologue now
+__device__ __forceinline__ void grid_dep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 }  // namespace hcl::ptx
