@@ -92,10 +92,12 @@ template <int CG, bool TF32, bool BMN, bool OUTF32, int BN, bool ONE, bool MC = 
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmC, void* __restrict__ Cout, int M, int N, int K,
-                   int64_t ldc, int group_m, int tma_c, int ksplit) {
+                   int64_t ldc, int group_m, int tma_c, int ksplit, int kseg) {
   // ksplit > 1 (fp32 output only): work unit t = (tile, K slice t / tiles); slice s
   // accumulates k-blocks [nk*s/ksplit, nk*(s+1)/ksplit) into C + s*M*ldc (a workspace
   // the launcher reduces in slice order)
+  // kseg > 0 (K-major A and B, kseg % kBK == 0): the K' = 3 kseg operands are stored
+  // as [hi | lo] (2 kseg per row) and read as A' = [hi | hi | lo], B' = [hi | lo | hi]
   using C = Cfg<CG, TF32, BN, ONE>;
   constexpr int kBN = C::kBN;
   static_assert(!BMN || C::kBNLocal % C::kMNAtom == 0, "MN-major B needs whole 128-byte atoms per CTA");
@@ -157,22 +159,28 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int n0 = nt * kBN + static_cast<int>(rank) * C::kBNLocal;
         for (int kb = kb0; kb < kb1; ++kb) {
           ptx::mbar_wait(&empty[stage], phase ^ 1);
+          int ca = kb * C::kBK, cb = ca;  // A / B column of this k-block
+          if (kseg) {
+            const int sg = ca / kseg, off = ca - sg * kseg;
+            ca = (sg == 2 ? kseg : 0) + off;
+            cb = (sg == 1 ? kseg : 0) + off;
+          }
           uint8_t* sa = smem + stage * C::kStage;
           uint8_t* sb = sa + C::kABytes;
           if constexpr (CG == 1) {
             ptx::mbar_arrive_expect_tx(&full[stage], C::kStage);
-            ptx::tma_load_2d(sa, &tmA, &full[stage], kb * C::kBK, m0);
+            ptx::tma_load_2d(sa, &tmA, &full[stage], ca, m0);
             if constexpr (BMN) {
 #pragma unroll
               for (int j = 0; j < C::kBNLocal / C::kMNAtom; ++j)
                 ptx::tma_load_2d(sb + j * C::kBK * 128, &tmB, &full[stage], n0 + j * C::kMNAtom, kb * C::kBK);
             } else {
-              ptx::tma_load_2d(sb, &tmB, &full[stage], kb * C::kBK, n0);
+              ptx::tma_load_2d(sb, &tmB, &full[stage], cb, n0);
             }
           } else {
             if (rank == 0) ptx::mbar_arrive_expect_tx(&full[stage], C::kStage * 2);
             const uint32_t bar = ptx::mapa(ptx::smem_u32(&full[stage]), lead);
-            ptx::tma_load_2d_pair(sa, &tmA, bar, kb * C::kBK, m0);
+            ptx::tma_load_2d_pair(sa, &tmA, bar, ca, m0);
             if constexpr (BMN && MC) {  // atom pr of this CTA's B half, to the same-rank CTA of both pairs
               ptx::tma_load_2d_pair_mc(sb + pr * C::kBK * 128, &tmB, ptx::smem_u32(&full[stage]) & 0xFEFFFFFFu,
                                        static_cast<uint16_t>(0x5u << rank), n0 + static_cast<int>(pr) * C::kMNAtom,
@@ -182,7 +190,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               for (int j = 0; j < C::kBNLocal / C::kMNAtom; ++j)
                 ptx::tma_load_2d_pair(sb + j * C::kBK * 128, &tmB, bar, n0 + j * C::kMNAtom, kb * C::kBK);
             } else {
-              ptx::tma_load_2d_pair(sb, &tmB, bar, kb * C::kBK, n0);
+              ptx::tma_load_2d_pair(sb, &tmB, bar, cb, n0);
             }
           }
           if (++stage == C::kStages) { stage = 0; phase ^= 1; }
@@ -404,13 +412,15 @@ CUtensorMap make_tmap(const void* base, bool f32, uint64_t inner, uint64_t outer
 
 template <int CG, bool TF32, bool BMN, bool OUTF32, int BN = 256, bool ONE = false, bool MC = false>
 void run_gemm(const void* A, const void* B, void* Cp, int64_t M, int64_t N, int64_t K, int64_t ldc,
-              int sm_count, cudaStream_t stream, int group_m, bool persistent, int ksplit = 1, bool pdl = false) {
+              int sm_count, cudaStream_t stream, int group_m, bool persistent, int ksplit = 1, bool pdl = false,
+              int kseg = 0) {
   using C = Cfg<CG, TF32, BN, ONE>;
   const uint64_t es = C::kElem;
   const CUtensorMapL2promotion promo = l2_promotion();
-  CUtensorMap ta = make_tmap(A, TF32, K, M, K * es, C::kBK, kBM, promo);
+  const int64_t kst = kseg ? 2 * kseg : K;  // stored K extent of A and K-major B
+  CUtensorMap ta = make_tmap(A, TF32, kst, M, kst * es, C::kBK, kBM, promo);
   CUtensorMap tb = BMN ? make_tmap(B, TF32, N, K, N * es, C::kMNAtom, C::kBK, promo)
-                       : make_tmap(B, TF32, K, N, K * es, C::kBK, C::kBNLocal, promo);
+                       : make_tmap(B, TF32, kst, N, kst * es, C::kBK, C::kBNLocal, promo);
   CUtensorMap tc{};
   const int tma_c = C::kTmaC && !OUTF32 && env_int("HCL_GEMM_TMAC", 1) ? 1 : 0;
   if (tma_c) {  // C (M x N bf16), box 32 x 32, SWIZZLE_64B
@@ -451,7 +461,7 @@ void run_gemm(const void* A, const void* B, void* Cp, int64_t M, int64_t N, int6
   cfg.attrs = attr;
   cfg.numAttrs = pdl ? 2 : 1;
   HCL_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, tc, Cp, static_cast<int>(M), static_cast<int>(N),
-                              static_cast<int>(K), ldc, group_m, tma_c, ksplit));
+                              static_cast<int>(K), ldc, group_m, tma_c, ksplit, kseg));
   HCL_LAUNCHED();
 }
 
@@ -495,30 +505,30 @@ bool mc_ok(int64_t M, int64_t N, int group_m, int ksplit) {
 
 template <bool TF32, bool BMN, bool OUTF32>
 void dispatch_shape(int shape, const void* a, const void* b, void* cp, int64_t M, int64_t n, int64_t k,
-                    const LaunchCtx& c, int group_m, int ksplit = 1, bool pdl = false) {
+                    const LaunchCtx& c, int group_m, int ksplit = 1, bool pdl = false, int kseg = 0) {
   const bool persist = c.sm_budgeted || env_int("HCL_GEMM_PERSIST", 0) != 0;
   switch (shape) {
     case 1:
-      run_gemm<1, TF32, BMN, OUTF32, 256>(a, b, cp, M, n, k, n, c.sm_count, c.stream, group_m, persist, ksplit, pdl);
+      run_gemm<1, TF32, BMN, OUTF32, 256>(a, b, cp, M, n, k, n, c.sm_count, c.stream, group_m, persist, ksplit, pdl, kseg);
       break;
     case 2:
-      run_gemm<2, TF32, BMN, OUTF32, 128>(a, b, cp, M, n, k, n, c.sm_count, c.stream, group_m, persist, ksplit, pdl);
+      run_gemm<2, TF32, BMN, OUTF32, 128>(a, b, cp, M, n, k, n, c.sm_count, c.stream, group_m, persist, ksplit, pdl, kseg);
       break;
     case 3:
-      run_gemm<1, TF32, BMN, OUTF32, 64>(a, b, cp, M, n, k, n, c.sm_count, c.stream, group_m, persist, ksplit, pdl);
+      run_gemm<1, TF32, BMN, OUTF32, 64>(a, b, cp, M, n, k, n, c.sm_count, c.stream, group_m, persist, ksplit, pdl, kseg);
       break;
     default:
       if (!persist && env_int("HCL_GEMM_ONE", 1) == 0 && mc_ok(M, n, group_m, ksplit) && BMN && !TF32)
         run_gemm<2, TF32, BMN, OUTF32, 256, false, BMN && !TF32>(a, b, cp, M, n, k, n, c.sm_count, c.stream, group_m,
-                                                                false, ksplit, pdl);
+                                                                false, ksplit, pdl, kseg);
       else if (persist || env_int("HCL_GEMM_ONE", 1) == 0)
-        run_gemm<2, TF32, BMN, OUTF32, 256>(a, b, cp, M, n, k, n, c.sm_count, c.stream, group_m, persist, ksplit, pdl);
+        run_gemm<2, TF32, BMN, OUTF32, 256>(a, b, cp, M, n, k, n, c.sm_count, c.stream, group_m, persist, ksplit, pdl, kseg);
       else if (mc_ok(M, n, group_m, ksplit) && BMN && !TF32)
         run_gemm<2, TF32, BMN, OUTF32, 256, true, BMN && !TF32>(a, b, cp, M, n, k, n, c.sm_count, c.stream, group_m,
-                                                               false, ksplit, pdl);
+                                                               false, ksplit, pdl, kseg);
       else
         run_gemm<2, TF32, BMN, OUTF32, 256, true>(a, b, cp, M, n, k, n, c.sm_count, c.stream, group_m, false,
-                                                  ksplit, pdl);
+                                                  ksplit, pdl, kseg);
       break;
   }
 }
@@ -620,7 +630,7 @@ __device__ __forceinline__ float tf32_hi(float x) {
 __global__ void __launch_bounds__(256) split3_both_kernel(const float4* __restrict__ a, float4* __restrict__ a3,
                                                           int64_t rows, int64_t k4, int a_blocks,
                                                           const float* __restrict__ b, float* __restrict__ b3,
-                                                          int64_t K, int64_t N, int gx) {
+                                                          int64_t K, int64_t N, int gx, bool seg) {
   if (static_cast<int>(blockIdx.x) < a_blocks) {
     const int64_t total = rows * k4;
     for (int64_t i = blockIdx.x * 256ll + threadIdx.x; i < total; i += static_cast<int64_t>(a_blocks) * 256) {
@@ -628,10 +638,16 @@ __global__ void __launch_bounds__(256) split3_both_kernel(const float4* __restri
       float4 v = a[i], h, l;
       h.x = tf32_hi(v.x); h.y = tf32_hi(v.y); h.z = tf32_hi(v.z); h.w = tf32_hi(v.w);
       l.x = v.x - h.x; l.y = v.y - h.y; l.z = v.z - h.z; l.w = v.w - h.w;
-      float4* o = a3 + r * 3 * k4 + c;
-      o[0] = h;
-      o[k4] = h;
-      o[2 * k4] = l;
+      if (seg) {  // [hi | lo]
+        float4* o = a3 + r * 2 * k4 + c;
+        o[0] = h;
+        o[k4] = l;
+      } else {
+        float4* o = a3 + r * 3 * k4 + c;
+        o[0] = h;
+        o[k4] = h;
+        o[2 * k4] = l;
+      }
     }
     return;
   }
@@ -648,10 +664,10 @@ __global__ void __launch_bounds__(256) split3_both_kernel(const float4* __restri
     const int64_t n = n0 + i, k = k0 + tx;
     if (n < N && k < K) {
       const float v = tile[tx][i], h = tf32_hi(v);
-      float* o = b3 + n * 3 * K + k;
+      float* o = b3 + n * (seg ? 2 : 3) * K + k;
       o[0] = h;
       o[K] = v - h;
-      o[2 * K] = h;
+      if (!seg) o[2 * K] = h;
     }
   }
 }
@@ -687,8 +703,11 @@ uint64_t launch_gemm_f32x3(LaunchCtx& c) {
   const int64_t ks_default = m * n <= (int64_t(1) << 24) ? std::max<int64_t>(1, std::min<int64_t>(4, 3 * k / 768)) : 1;
   const int ksplit = static_cast<int>(
       std::max<int64_t>(1, std::min<int64_t>(env_int("HCL_GEMM_KSPLIT", static_cast<int>(ks_default)), nkb)));
-  const size_t a3_bytes = static_cast<size_t>(r * 3 * k * 4);
-  const size_t b3_bytes = static_cast<size_t>(n * 3 * k * 4);
+  // K-block aligned K: the operands are stored once as [hi | lo] and the GEMM's
+  // producer reads the three segments from them (HCL_GEMM_SEG=0: materialised 3K rows)
+  const bool seg = k % 32 == 0 && env_int("HCL_GEMM_SEG", 1) != 0;
+  const size_t a3_bytes = static_cast<size_t>(r * (seg ? 2 : 3) * k * 4);
+  const size_t b3_bytes = static_cast<size_t>(n * (seg ? 2 : 3) * k * 4);
   const size_t ws_bytes = ksplit > 1 ? static_cast<size_t>(ksplit) * r * n * 4 : 0;
   uint8_t* s = static_cast<uint8_t*>(c.scratch(c.dev, a3_bytes + b3_bytes + ws_bytes));
   float* a3 = reinterpret_cast<float*>(s);
@@ -701,7 +720,7 @@ uint64_t launch_gemm_f32x3(LaunchCtx& c) {
     const int64_t b_blocks = static_cast<int64_t>(gx) * ceil_div(k, 32);
     split3_both_kernel<<<static_cast<unsigned>(a_blocks + b_blocks), 256, 0, c.stream>>>(
         reinterpret_cast<const float4*>(a), reinterpret_cast<float4*>(a3), r, k / 4, a_blocks,
-        reinterpret_cast<const float*>(B.ptr), b3, k, n, gx);
+        reinterpret_cast<const float*>(B.ptr), b3, k, n, gx, seg);
     HCL_LAUNCHED();
   }
   const int group_m = std::max(1, env_int("HCL_GEMM_GROUP", kGroupM));
@@ -710,7 +729,8 @@ uint64_t launch_gemm_f32x3(LaunchCtx& c) {
   // programmatic dependent launches: split -> GEMM -> reduce overlap each launch's
   // prologue with the previous one's tail (HCL_GEMM_PDL=0: plain stream order)
   const bool pdl = env_int("HCL_GEMM_PDL", 1) != 0;
-  dispatch_shape<true, false, true>(shape, a3, b3, ksplit > 1 ? ws : cp, r, n, 3 * k, c, group_m, ksplit, pdl);
+  dispatch_shape<true, false, true>(shape, a3, b3, ksplit > 1 ? ws : cp, r, n, 3 * k, c, group_m, ksplit, pdl,
+                                    seg ? static_cast<int>(k) : 0);
   if (ksplit > 1) {
     const int64_t n4 = r * n / 4;  // N % 4 == 0
     const unsigned blocks = static_cast<unsigned>(std::min<int64_t>(ceil_div(n4, 256), 8LL * c.sm_count));

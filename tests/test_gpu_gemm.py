@@ -256,6 +256,25 @@ def test_gemm_f32x3_ksplit(ctx, queues, monkeypatch):
     assert whole.tobytes() == part.tobytes()
 
 
+@pytest.mark.parametrize("m,k,n,ks", [(1024, 1024, 1024, ""), (300, 96, 260, "3"), (257, 2048, 132, "1"),
+                                       (130, 100, 68, "")])
+def test_gemm_f32x3_segments_bit_identical(ctx, queues, monkeypatch, m, k, n, ks):
+    """K a multiple of 32: the split stores [hi | lo] once per operand and the
+    GEMM's producer reads A' = [hi|hi|lo], B' = [hi|lo|hi] segment by segment
+    (HCL_GEMM_SEG, default) -- the same MMAs in the same order as the
+    materialised 3K layout, so C is bit-identical (K = 100: no segments)."""
+    if ks:
+        monkeypatch.setenv("HCL_GEMM_KSPLIT", ks)
+    a = O.gen_doubles(m * k, 44).astype(np.float32)
+    b = O.gen_doubles(k * n, 45).astype(np.float32)
+    monkeypatch.setenv("HCL_GEMM_SEG", "0")
+    want = gemm(ctx, queues, "gemm_f32x3", a, b, m, k, n)
+    monkeypatch.setenv("HCL_GEMM_SEG", "1")
+    got = gemm(ctx, queues, "gemm_f32x3", a, b, m, k, n)
+    assert got.tobytes() == want.tobytes()
+    assert normwise_err(got, a.astype(np.float64).reshape(m, k), b.astype(np.float64).reshape(k, n)) <= 2.0**-16
+
+
 @pytest.mark.parametrize("one", ["1", "0"])
 def test_gemm_bf16_b_multicast_bit_identical(ctx, queues, monkeypatch, one):
     """HCL_GEMM_MC=1: clusters of two CTA pairs on vertically adjacent tiles, each
