@@ -270,7 +270,7 @@ std::string graph_key(const KernelDef* k, const std::vector<LaunchArg>& la, cons
   put(&d.scratch, sizeof(d.scratch));
   put(&d.scratch_bytes, sizeof(d.scratch_bytes));
   for (const char* v : {"HCL_GEMM_SHAPE", "HCL_GEMM_CG", "HCL_GEMM_B_KMAJOR", "HCL_GEMM_GROUP", "HCL_GEMM_PROMO",
-                        "HCL_GEMM_TMAC", "HCL_GEMM_ONE", "HCL_GEMM_PERSIST", "HCL_GEMM_KSPLIT", "HCL_GEMM_PDL", "HCL_GEMM_SEG", "HCL_SIMT_MS",
+                        "HCL_GEMM_TMAC", "HCL_GEMM_ONE", "HCL_GEMM_PERSIST", "HCL_GEMM_KSPLIT", "HCL_GEMM_PDL", "HCL_GEMM_SEG", "HCL_SIMT_MS", "HCL_SIMT_KSPLIT",
                         "HCL_SIMT_TILE"}) {
     const char* e = std::getenv(v);
     key += '|';

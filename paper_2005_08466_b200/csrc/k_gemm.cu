@@ -868,6 +868,7 @@ template <int BM, int BN, int TM, int TN>
 __global__ void __launch_bounds__(256) gemm_f32_ms_kernel(const float* __restrict__ At, int64_t lda,
                                                           const float* __restrict__ B, float* __restrict__ Cc,
                                                           int64_t M, int64_t N, int64_t K) {
+  // gridDim.z > 1: K slice blockIdx.z (k-tiles [nkt z / Z, nkt (z+1) / Z)) into C + z M N
   static_assert((BM / TM) * (BN / TN) == 256, "256 threads");
   constexpr int RSTEP = BM * 4 / TM, CSTEP = BN * 4 / TN;
   constexpr int A_CH = MS_K * BM / 4, B_CH = MS_K * BN / 4;  // 16-byte chunks per stage
@@ -877,8 +878,12 @@ __global__ void __launch_bounds__(256) gemm_f32_ms_kernel(const float* __restric
   const int tid = threadIdx.x;
   const int tx = tid % (BN / TN), ty = tid / (BN / TN);
   const int64_t row0 = blockIdx.y * (int64_t)BM, col0 = blockIdx.x * (int64_t)BN;
-  const int nk = static_cast<int>((K + MS_K - 1) / MS_K);
+  const int nkt = static_cast<int>((K + MS_K - 1) / MS_K);
+  const int kt0 = static_cast<int>(static_cast<int64_t>(nkt) * blockIdx.z / gridDim.z);
+  const int nk = static_cast<int>(static_cast<int64_t>(nkt) * (blockIdx.z + 1) / gridDim.z) - kt0;
+  Cc += static_cast<int64_t>(blockIdx.z) * M * N;
   auto issue = [&](int stage, int kt) {
+    kt += kt0;
     const int64_t k0 = static_cast<int64_t>(kt) * MS_K;
     for (int ch = tid; ch < A_CH; ch += 256) {
       const int kk = ch / (BM / 4), m4 = (ch % (BM / 4)) * 4;
@@ -954,11 +959,12 @@ __global__ void __launch_bounds__(256) gemm_f32_ms_kernel(const float* __restric
 
 template <int BM, int BN, int TM, int TN>
 void run_gemm_f32_ms(const float* At, int64_t lda, const float* b, float* cp, int64_t r, int64_t n, int64_t k,
-                     cudaStream_t stream) {
+                     cudaStream_t stream, int ksplit = 1) {
   const size_t smem = static_cast<size_t>(MS_STAGES) * MS_K * (BM + BN) * 4;
   auto kern = gemm_f32_ms_kernel<BM, BN, TM, TN>;
   HCL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-  dim3 grid(static_cast<unsigned>(ceil_div(n, BN)), static_cast<unsigned>(ceil_div(r, BM)));
+  dim3 grid(static_cast<unsigned>(ceil_div(n, BN)), static_cast<unsigned>(ceil_div(r, BM)),
+            static_cast<unsigned>(ksplit));
   kern<<<grid, 256, smem, stream>>>(At, lda, b, cp, r, n, k);
   HCL_LAUNCHED();
 }
@@ -984,22 +990,41 @@ uint64_t launch_gemm_f32(LaunchCtx& c) {
   const int64_t r = static_cast<int64_t>(rows);
   // tile: 128x128 (8x8 per thread) when the grid fills the GPU twice, else
   // 64x64 (4x4); 128x64 (8x4) is available; HCL_SIMT_TILE=0|1|2 forces one
-  // (every shape computes each output with the same FMA chain, so results
-  // are identical)
+  // (every shape computes each output with the same FMA chains, so results
+  // are identical for a given K split)
   const int64_t sms = c.sm_count;
   int tile = env_int("HCL_SIMT_TILE", -1);
   if (tile < 0 || tile > 2)
-    tile = ceil_div(r, 128) * ceil_div(n, 128) >= 2 * sms ? 0 : 2;  // 1024^3: 64x64 measured best (24.5 TF)
+    tile = ceil_div(r, 128) * ceil_div(n, 128) >= 2 * sms ? 0 : 2;  // without a K split: 64x64 at 1024^3 (24.5 TF)
   if (n % 4 == 0 && env_int("HCL_SIMT_MS", 1)) {
-    // multistage path: At = A^T (K x rows, pitch rounded up to 4 floats)
+    // multistage path: At = A^T (K x rows, pitch rounded up to 4 floats).
+    // K split when the 128x128 grid is small: slices of the k-tiles, each one FMA
+    // chain in ascending k, summed in slice order by ksplit_reduce_kernel; a
+    // function of M, N and K only, so row partitions agree. 128x128 tiles then
+    // fill the GPU. HCL_SIMT_KSPLIT overrides (1 = one chain per output).
+    const int64_t t128 = ceil_div(m, 128) * ceil_div(n, 128), nkt = ceil_div(k, MS_K);
+    const int64_t ks_default = std::max<int64_t>(1, std::min<int64_t>({8, 2 * sms / t128, nkt / 4}));
+    const int ksplit = static_cast<int>(
+        std::max<int64_t>(1, std::min<int64_t>(env_int("HCL_SIMT_KSPLIT", static_cast<int>(ks_default)), nkt)));
+    if (ksplit > 1 && env_int("HCL_SIMT_TILE", -1) < 0) tile = 0;
     const int64_t lda = (r + 3) / 4 * 4;
-    float* at = static_cast<float*>(c.scratch(c.dev, static_cast<size_t>(k * lda) * 4));
+    const size_t at_floats = static_cast<size_t>(k * lda + 3) & ~size_t(3);  // the workspace stays 16-byte aligned
+    float* at = static_cast<float*>(
+        c.scratch(c.dev, (at_floats + (ksplit > 1 ? static_cast<size_t>(ksplit) * r * n : 0)) * 4));
+    float* out = ksplit > 1 ? at + at_floats : cp;
     dim3 tg(static_cast<unsigned>(ceil_div(k, 32)), static_cast<unsigned>(ceil_div(r, 32)));
     transpose_pitched_kernel<<<tg, dim3(32, 8), 0, c.stream>>>(a, at, r, k, lda);
     HCL_LAUNCHED();
-    if (tile == 0) run_gemm_f32_ms<128, 128, 8, 8>(at, lda, bp, cp, r, n, k, c.stream);
-    else if (tile == 1) run_gemm_f32_ms<128, 64, 8, 4>(at, lda, bp, cp, r, n, k, c.stream);
-    else run_gemm_f32_ms<64, 64, 4, 4>(at, lda, bp, cp, r, n, k, c.stream);
+    if (tile == 0) run_gemm_f32_ms<128, 128, 8, 8>(at, lda, bp, out, r, n, k, c.stream, ksplit);
+    else if (tile == 1) run_gemm_f32_ms<128, 64, 8, 4>(at, lda, bp, out, r, n, k, c.stream, ksplit);
+    else run_gemm_f32_ms<64, 64, 4, 4>(at, lda, bp, out, r, n, k, c.stream, ksplit);
+    if (ksplit > 1) {
+      const int64_t n4 = r * n / 4;
+      const unsigned blocks = static_cast<unsigned>(std::min<int64_t>(ceil_div(n4, 256), 8LL * c.sm_count));
+      ksplit_reduce_kernel<<<blocks, 256, 0, c.stream>>>(reinterpret_cast<const float4*>(out),
+                                                         reinterpret_cast<float4*>(cp), n4, ksplit);
+      HCL_LAUNCHED();
+    }
     return 2ull * rows * static_cast<uint64_t>(n) * static_cast<uint64_t>(k);
   }
   if (tile == 0) {

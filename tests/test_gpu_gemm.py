@@ -202,6 +202,7 @@ def test_gemm_f32_simt_tiles_bit_identical(ctx, queues, monkeypatch):
     a = O.gen_doubles(m * k, 42).astype(np.float32)
     b = O.gen_doubles(k * n, 43).astype(np.float32)
     outs = []
+    monkeypatch.setenv("HCL_SIMT_KSPLIT", "1")  # one FMA chain per output (the register-prefetch kernel's)
     for ms in "01":  # register-prefetch kernel and the cp.async multistage kernel
         monkeypatch.setenv("HCL_SIMT_MS", ms)
         for t in "012":
@@ -210,6 +211,27 @@ def test_gemm_f32_simt_tiles_bit_identical(ctx, queues, monkeypatch):
     assert all(o == outs[0] for o in outs)
     a64, b64 = a.astype(np.float64).reshape(m, k), b.astype(np.float64).reshape(k, n)
     assert normwise_err(np.frombuffer(outs[0], np.float32).reshape(m, n), a64, b64) <= 2.0**-20
+
+
+@pytest.mark.parametrize("m,n,k", [(1024, 1024, 1024), (701, 520, 301)])
+def test_gemm_f32_simt_ksplit(ctx, queues, monkeypatch, m, n, k):
+    """Small grids split K (slices of k-tiles, each an ascending FMA chain, summed
+    in slice order): within the fp32 bound, and identical across tile shapes."""
+    a = O.gen_doubles(m * k, 46).astype(np.float32)
+    b = O.gen_doubles(k * n, 47).astype(np.float32)
+    a64, b64 = a.astype(np.float64).reshape(m, k), b.astype(np.float64).reshape(k, n)
+    default = gemm(ctx, queues, "gemm_f32", a, b, m, k, n)
+    assert normwise_err(default, a64, b64) <= 2.0**-20
+    monkeypatch.setenv("HCL_SIMT_KSPLIT", "4")
+    outs = []
+    for t in "012":
+        monkeypatch.setenv("HCL_SIMT_TILE", t)
+        outs.append(gemm(ctx, queues, "gemm_f32", a, b, m, k, n).tobytes())
+    assert all(o == outs[0] for o in outs)
+    assert outs[0] == default.tobytes()  # both sizes take 4 slices by default
+    monkeypatch.setenv("HCL_SIMT_KSPLIT", "1")
+    one = gemm(ctx, queues, "gemm_f32", a, b, m, k, n)
+    assert normwise_err(one, a64, b64) <= 2.0**-20
 
 
 @pytest.mark.parametrize("kernel,out_f32,tol", [("gemm_bf16", True, 2.0**-12), ("gemm_bf16", False, None),
