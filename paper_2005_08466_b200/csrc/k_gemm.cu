@@ -751,7 +751,8 @@ uint64_t launch_gemm_f32x3(LaunchCtx& c) {
 }
 
 // ---------------------------------------------------------------------------
-// fp32 SIMT GEMM (exact fp32 products, FFMA accumulate in ascending k): BMxBN
+// fp32 SIMT GEMM (exact fp32 products, FFMA accumulate in ascending k; the
+// multistage kernel below may run K slices, each such a chain, summed in order): BMxBN
 // tile per 256-thread block, TMxTN outputs per thread, K panels of 16
 // double-buffered in shared memory with register-staged prefetch (the next
 // panel's global loads are in flight while the current one is multiplied).
@@ -850,7 +851,7 @@ __global__ void __launch_bounds__(256) gemm_f32_simt_kernel(const float* __restr
 // pitch padded to 4 floats) so both operand tiles are contiguous k-rows, copied
 // with 16-byte cp.async (zero-filled past the edges) into a 3-stage ring; the
 // register tile and the FFMA chain per output are those of gemm_f32_simt_kernel
-// (k ascending), so results are bit-identical to it.
+// (k ascending), so results are bit-identical to it with one K slice.
 constexpr int MS_K = 16, MS_STAGES = 3;
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
