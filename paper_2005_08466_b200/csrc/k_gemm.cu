@@ -906,6 +906,8 @@ __global__ void __launch_bounds__(256) gemm_f32_ms_kernel(const float* __restric
   for (int i = 0; i < TM; ++i)
 #pragma unroll
     for (int j = 0; j < TN; ++j) acc[i][j] = 0.f;
+  ptx::grid_dep_wait();  // At is the previous launch's output (PDL)
+  ptx::grid_dep_launch();
 #pragma unroll
   for (int st = 0; st < MS_STAGES - 1; ++st) {
     if (st < nk) issue(st, st);
@@ -960,13 +962,23 @@ __global__ void __launch_bounds__(256) gemm_f32_ms_kernel(const float* __restric
 
 template <int BM, int BN, int TM, int TN>
 void run_gemm_f32_ms(const float* At, int64_t lda, const float* b, float* cp, int64_t r, int64_t n, int64_t k,
-                     cudaStream_t stream, int ksplit = 1) {
+                     cudaStream_t stream, int ksplit = 1, bool pdl = false) {
   const size_t smem = static_cast<size_t>(MS_STAGES) * MS_K * (BM + BN) * 4;
   auto kern = gemm_f32_ms_kernel<BM, BN, TM, TN>;
   HCL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   dim3 grid(static_cast<unsigned>(ceil_div(n, BN)), static_cast<unsigned>(ceil_div(r, BM)),
             static_cast<unsigned>(ksplit));
-  kern<<<grid, 256, smem, stream>>>(At, lda, b, cp, r, n, k);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  HCL_CUDA(cudaLaunchKernelEx(&cfg, kern, At, lda, b, cp, r, n, k));
   HCL_LAUNCHED();
 }
 
@@ -1016,14 +1028,25 @@ uint64_t launch_gemm_f32(LaunchCtx& c) {
     dim3 tg(static_cast<unsigned>(ceil_div(k, 32)), static_cast<unsigned>(ceil_div(r, 32)));
     transpose_pitched_kernel<<<tg, dim3(32, 8), 0, c.stream>>>(a, at, r, k, lda);
     HCL_LAUNCHED();
-    if (tile == 0) run_gemm_f32_ms<128, 128, 8, 8>(at, lda, bp, out, r, n, k, c.stream, ksplit);
-    else if (tile == 1) run_gemm_f32_ms<128, 64, 8, 4>(at, lda, bp, out, r, n, k, c.stream, ksplit);
-    else run_gemm_f32_ms<64, 64, 4, 4>(at, lda, bp, out, r, n, k, c.stream, ksplit);
+    // transpose -> GEMM -> reduction as programmatic dependent launches (HCL_GEMM_PDL)
+    const bool pdl = env_int("HCL_GEMM_PDL", 1) != 0;
+    if (tile == 0) run_gemm_f32_ms<128, 128, 8, 8>(at, lda, bp, out, r, n, k, c.stream, ksplit, pdl);
+    else if (tile == 1) run_gemm_f32_ms<128, 64, 8, 4>(at, lda, bp, out, r, n, k, c.stream, ksplit, pdl);
+    else run_gemm_f32_ms<64, 64, 4, 4>(at, lda, bp, out, r, n, k, c.stream, ksplit, pdl);
     if (ksplit > 1) {
       const int64_t n4 = r * n / 4;
       const unsigned blocks = static_cast<unsigned>(std::min<int64_t>(ceil_div(n4, 256), 8LL * c.sm_count));
-      ksplit_reduce_kernel<<<blocks, 256, 0, c.stream>>>(reinterpret_cast<const float4*>(out),
-                                                         reinterpret_cast<float4*>(cp), n4, ksplit);
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3(blocks);
+      cfg.blockDim = dim3(256);
+      cfg.stream = c.stream;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[0].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = pdl ? 1 : 0;
+      HCL_CUDA(cudaLaunchKernelEx(&cfg, ksplit_reduce_kernel, reinterpret_cast<const float4*>(out),
+                                  reinterpret_cast<float4*>(cp), n4, ksplit));
       HCL_LAUNCHED();
     }
     return 2ull * rows * static_cast<uint64_t>(n) * static_cast<uint64_t>(k);
